@@ -1,0 +1,176 @@
+/* nmt.h - C ABI of libnmt.so: batched GPU querying of an attention-based encoder-decoder
+ * (the DL4MT/Nematus conditional-GRU model) as used by arXiv 1605.04809 as a phrase-based
+ * decoder feature function.  sm_100a (B200) only; there is no CPU fallback.
+ *
+ * Problem statement (§5.1): "We assume ... that the neural model has already
+ * been initialized with the source sentence and that the source sentence context is available at
+ * all time" (nmt_encode -> context handle); given a set of (hypothesis state, next words), one
+ * forward step "(H_i, P_i) <- NMT(H_{i-1}, E_i)" (Alg. 1) yields the word
+ * probabilities and the successor states, which are cached at the target nodes and "reused ... as
+ * initial states when scoring another batch of hypotheses at later time"
+ * (nmt_score_batch -> log-probs + child state handles).  Several models are combined as separately
+ * weighted features through the ensemble hook.
+ *
+ * Conventions (all calls):
+ *  - Every call returns nmt_status; NMT_OK = 0.  On error no output array is written and
+ *    nmt_last_error() returns a thread-local message naming the offending argument/param/file.
+ *  - Pointers marked [host] are host memory, [dev] device memory of the model's device.
+ *    The caller owns every input and output array; the library owns models, contexts and
+ *    the per-context state arena.  Handles die with nmt_ctx_free.
+ *  - Ids are int32 in [0, V); y_prev = -1 denotes BOS (zero embedding).  nmt_state is an opaque
+ *    per-context node id (int64).
+ *  - A model is immutable after load and may be shared by contexts; calls on one model are
+ *    serialised on the model's stream (one writer per context).
+ *  - Determinism: identical call sequences give bit-identical outputs on one GPU type.  Child ids
+ *    are assigned in first-appearance order of the (parent-major, candidate-order) request stream.
+ */
+#ifndef NMT_H
+#define NMT_H
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define NMT_API __attribute__((visibility("default")))
+#else
+#define NMT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NMT_OK = 0,
+  NMT_ERR_INVALID_ARG = 1,   /* null pointer, negative count, bad CSR offsets */
+  NMT_ERR_IO = 2,            /* params file cannot be opened/read/written */
+  NMT_ERR_FORMAT = 3,        /* malformed params header or payload length */
+  NMT_ERR_MISSING_PARAM = 4, /* "missing parameter <name>" */
+  NMT_ERR_SHAPE = 5,         /* "<name>: expected RxC, got RxC" */
+  NMT_ERR_EMPTY_SOURCE = 6,  /* len == 0 */
+  NMT_ERR_TOKEN_RANGE = 7,   /* a word id outside [0, V) */
+  NMT_ERR_BAD_STATE = 8,     /* unknown / foreign state handle (cf. "unscored expansion") */
+  NMT_ERR_CAPACITY = 9,      /* source longer than max_src_len, arena or batch beyond limits */
+  NMT_ERR_CUDA = 10,         /* CUDA runtime/driver error, or no sm_100 device */
+  NMT_ERR_NCCL = 11,
+  NMT_ERR_OOM = 12
+} nmt_status;
+
+NMT_API const char* nmt_last_error(void);
+
+typedef enum {
+  NMT_PREC_FP32CLASS = 0, /* every GEMM in split bf16x3 (hi*hi + hi*lo + lo*hi), fp32 accumulate;
+                             parity bound max|dlogp| <= 1e-3 (BASELINE north_star) */
+  NMT_PREC_BF16 = 1       /* single-pass bf16 GEMMs, fp32 accumulate; bound <= 2e-2 */
+} nmt_precision;
+
+typedef enum {
+  NMT_READOUT_TANH = 0,  /* DL4MT/Nematus deep output: t = tanh(s2 W_l + e W_p + c W_ctx + b) */
+  NMT_READOUT_MAXOUT = 1 /* Bahdanau 2014 maxout: t_k = max(pre_2k, pre_2k+1) */
+} nmt_readout;
+
+typedef struct {
+  int32_t dim_emb;     /* E   (500) */
+  int32_t dim_hid;     /* H   (1024); any H <= 1024 (padded to a multiple of 128 on the device) */
+  int32_t vocab_src;   /* V_s (50k En / 100k Ru BPE) */
+  int32_t vocab_tgt;   /* V_t */
+  int32_t max_src_len; /* Tx limit incl. EOS (50 words) */
+  nmt_readout readout;
+} nmt_dims;
+
+typedef struct {
+  int32_t device;          /* CUDA device ordinal */
+  nmt_precision precision; /* GEMM recipe, see above */
+  int32_t max_src_len;     /* 0 -> 64 */
+  void* stream;            /* cudaStream_t the model's work is issued on; NULL -> a private stream */
+} nmt_opts;
+
+typedef struct nmt_model nmt_model;
+typedef struct nmt_ctx nmt_ctx;
+typedef struct nmt_ensemble nmt_ensemble;
+typedef int64_t nmt_state;
+
+/* ---- models -------------------------------------------------------------------------------
+ * Params container ("text header + little-endian float32 payload"):
+ *   "NMTPARAMS 1\n" "dims E H Vs Vt readout=<tanh|maxout> eos=<id> unk=<id>\n" "arrays n\n"
+ *   n lines "<name> <rows> <cols>\n" (Nematus names), zero padding to 64 bytes,
+ *   then the arrays row-major float32 LE in header order.  Every required name must be present
+ *   (NMT_ERR_MISSING_PARAM), shapes must agree with dims (NMT_ERR_SHAPE), the payload length must
+ *   be exact (NMT_ERR_FORMAT).  Weights are re-laid out on the device at load (bf16 K-major
+ *   tiles, hi/lo splits, precomputed embedding projections); the host copy is not kept.        */
+NMT_API nmt_status nmt_load(const char* params_path, const nmt_opts* opts, nmt_model** out);
+NMT_API nmt_status nmt_load_buffer(const void* buf /*[host]*/, size_t len, const nmt_opts* opts, nmt_model** out);
+NMT_API nmt_status nmt_model_dims(const nmt_model* m, nmt_dims* out);
+/* Releases the caller's handle; the device memory goes when the last context of the model is freed
+ * too (models and contexts may be freed in any order). */
+NMT_API void nmt_model_free(nmt_model* m);
+
+/* ---- source context --------------------------------------------------------
+ * Bidirectional-GRU encoder over src_ids[0..len) [host] (the caller appends EOS, Nematus
+ * convention); computes ctx = [fwd_j ; bwd_j], s_0 = tanh(mean_j ctx_j W_init + b_init) and the
+ * attention keys pctx = ctx Wc_att + b_att.  len == 0 -> NMT_ERR_EMPTY_SOURCE; len > max_src_len
+ * -> NMT_ERR_CAPACITY.  The returned context owns a state arena whose root node is (s_0, BOS).  */
+NMT_API nmt_status nmt_encode(nmt_model* m, const int32_t* src_ids, int32_t len, nmt_ctx** out);
+NMT_API nmt_state nmt_root(const nmt_ctx* c);
+NMT_API void nmt_ctx_free(nmt_ctx* c);
+
+/* ---- batched scoring (Alg. 1; parent-indexed rows, DESIGN.md §2 A13) -----
+ * parents[n_parents], cand_offsets[n_parents+1] (CSR, offsets[0] = 0, non-decreasing) and
+ * cand_words[N_cand] are [host].  For every candidate i of parent k:
+ *   out_logprob[i] = log p(cand_words[i] | parent k)  (log-softmax over the WHOLE target vocab,
+ *                    PAPER.md:107; the logits are never materialised)
+ *   out_child[i]   = state handle of the node (parent k, word) - interned: the same (parent,
+ *                    word) pair always yields the same handle and a bit-identical log-prob.
+ * out_argmax[n_parents] (may be NULL) = most probable next word of each parent (lowest id on
+ * ties), -1 for a parent with no candidates.  Each distinct parent with >= 1 candidate that was
+ * never stepped is stepped once (GRU1 -> attention -> GRU2 -> readout -> vocab log-softmax) and
+ * its (s2, t, logZ, argmax) cached; later calls reuse it.  N_cand == 0 is a no-op.           */
+NMT_API nmt_status nmt_score_batch(nmt_ctx* c, int32_t n_parents, const nmt_state* parents,
+                           const int32_t* cand_offsets, const int32_t* cand_words,
+                           float* out_logprob, nmt_state* out_child, int32_t* out_argmax);
+
+/* Same, device-resident: all pointers [dev]; int32 parents/children (node ids < 2^31);
+ * n_cand must equal cand_offsets[n_parents].  Issued asynchronously on the model stream, no host
+ * synchronisation; invalid ids are reported by the next nmt_ctx_check().                     */
+NMT_API nmt_status nmt_score_batch_dev(nmt_ctx* c, int32_t n_parents, const int32_t* parents,
+                               const int32_t* cand_offsets, int32_t n_cand, const int32_t* cand_words,
+                               float* out_logprob, int32_t* out_child, int32_t* out_argmax);
+/* Waits for the model stream and reports a device-side validation error of earlier _dev calls. */
+NMT_API nmt_status nmt_ctx_check(nmt_ctx* c);
+/* Number of nodes and stepped nodes in the context's arena (synchronises the stream). */
+NMT_API nmt_status nmt_ctx_stats(nmt_ctx* c, int64_t* n_nodes, int64_t* n_stepped);
+
+/* ---- synthetic parents (bench / tests): n nodes with given input state s[n x H] [host] and
+ * previous word y_prev[n] [host] (-1 = BOS), not children of any node.                         */
+NMT_API nmt_status nmt_inject_states(nmt_ctx* c, int32_t n, const float* s, const int32_t* y_prev, nmt_state* out);
+
+/* ---- test-only exports ----------------------------------------------------------------------- */
+/* full log-prob row of one node over the whole vocab (normalisation tests); steps the node if
+ * needed.  out [host, vocab_tgt floats]                                                          */
+NMT_API nmt_status nmt_logprobs_full(nmt_ctx* c, nmt_state node, float* out);
+/* encoder outputs: ctx [Tx x 2H], pctx [Tx x 2H], s0 [H]; any pointer may be NULL [host]         */
+NMT_API nmt_status nmt_debug_encoder(nmt_ctx* c, float* ctx, float* pctx, float* s0);
+/* per-stage intermediates of one node's step (without caching): s1[H], alpha[Tx], c[2H], s2[H],
+ * t[E], logZ[1], argmax[1]; any pointer may be NULL [host]                                       */
+NMT_API nmt_status nmt_debug_intermediates(nmt_ctx* c, nmt_state node, float* s1, float* alpha, float* ctxv,
+                                   float* s2, float* t, float* logZ, int32_t* argmax);
+/* GEMM engine unit test: C[M x N] = A[M x K] . B[K x N] (+ bias[N]) with the tcgen05 kernel;
+ * split = 1 -> bf16x3.  A, B, bias, C are [host] fp32 row-major; N % 128 == 0, K % 64 == 0.     */
+NMT_API nmt_status nmt_test_gemm(int32_t M, int32_t N, int32_t K, int32_t split, const float* A, const float* B,
+                         const float* bias, float* C);
+
+/* ---- ensemble hook (models as separately weighted features; north_star NCCL reduce)
+ * One member per GPU/process.  nccl_unique_id points to the 128-byte ncclUniqueId broadcast by the
+ * harness (torch process group).  combine: out = sum over members of (mode 0) weight*logp or
+ * (mode 1) weight*exp(logp), then log in mode 1, reduced to `root` over NVLink; in and out are
+ * [dev] float[n] on the member's model stream; out is written on the root only.                 */
+NMT_API nmt_status nmt_ensemble_init(int32_t n_members, int32_t rank, const void* nccl_unique_id, int32_t device,
+                             nmt_ensemble** out);
+NMT_API nmt_status nmt_ensemble_get_unique_id(void* out128);
+NMT_API nmt_status nmt_ensemble_combine(nmt_ensemble* e, const float* member_logprob, int32_t n, float weight,
+                                int32_t mode, int32_t root, float* out, void* stream);
+NMT_API void nmt_ensemble_free(nmt_ensemble* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NMT_H */

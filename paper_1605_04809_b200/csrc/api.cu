@@ -1,0 +1,1204 @@
+// api.cu - host runtime behind the C ABI of include/nmt.h: params loading + device re-layout,
+// per-context arenas, the orchestration of the encoder and of one batched decoder step.
+//
+// Hot path of one nmt_score_batch call:
+//   planner (D0, device hash: intern (parent,w), unique unstepped parents -> rows)
+//   -> D1 gather s -> GEMM s.[U|Ux] -> GRU1 gates -> GEMM s1.W_comb_att -> attention (MUFU)
+//   -> GEMM [s1|c].[U_nl;Wc | Ux_nl | Wcx] -> GRU2 gates -> GEMM [c|s2].[W_ctx;W_l] -> readout
+//   -> GEMM t.W_o with fused online log-sum-exp (logits never written) -> finalize logZ
+//   -> gather-dot log p for every candidate (fresh rows and cache hits alike).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.h"
+
+using namespace nmt;
+
+static thread_local std::string g_err;
+
+namespace nmt {
+nmt_status set_error(nmt_status c, const std::string& m) {
+  g_err = m;
+  return c;
+}
+}  // namespace nmt
+
+namespace {
+
+nmt_status fail(nmt_status c, const std::string& m) { return nmt::set_error(c, m); }
+
+template <typename F>
+nmt_status guard(F&& f) {
+  try {
+    f();
+    return NMT_OK;
+  } catch (const NmtError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host out of memory";
+    return NMT_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NMT_ERR_INVALID_ARG;
+  }
+}
+
+template <typename T>
+T* dalloc(size_t n) {
+  if (n == 0) n = 1;
+  void* p = nullptr;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  // legacy-stream memset + device sync: the model stream is non-blocking and must see zeros
+  CK(cudaMemset(p, 0, n * sizeof(T)));
+  CK(cudaDeviceSynchronize());
+  return static_cast<T*>(p);
+}
+template <typename T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+struct Arr {
+  const float* h;  // host pointer into the params buffer
+  int rows, cols;
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------ model
+struct nmt_model {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  bool split = false;
+  int E, H, Vs, V, RO, maxout, maxTx;
+  int Ep, Hp, Cp, Vp, ROp, sf;
+  // encoder
+  float* Wemb_src = nullptr;   // [Vs][E]
+  __nv_bfloat16* Wenc = nullptr;  // [6Hp][2Ep]
+  float* benc = nullptr;       // [6Hp]
+  int NB = 0, UPC = 0;
+  float* Uarr = nullptr;       // [2][NB][3UPC][H]
+  float* W_init = nullptr;     // [2H][H]
+  float* b_init = nullptr;     // [H]
+  __nv_bfloat16* Watt = nullptr;  // [Cp][2Cp]
+  float* b_att = nullptr;      // [Cp]
+  // decoder
+  float* U_att = nullptr;      // [Cp]
+  float c_tt = 0.f;
+  __nv_bfloat16* W_h1 = nullptr;  // [3Hp][sf Hp]
+  float* Ex = nullptr;            // [V+1][3Hp]
+  __nv_bfloat16* W_q = nullptr;   // [Cp][sf Hp]
+  __nv_bfloat16* W_g2 = nullptr;  // [4Hp][sf (Hp+Cp)]
+  float* b_nl = nullptr;          // [2Hp]
+  float* bx_nl = nullptr;         // [Hp]
+  __nv_bfloat16* W_ro = nullptr;  // [ROp][sf (Cp+Hp)]
+  float* Eproj = nullptr;         // [V+1][ROp]
+  __nv_bfloat16* W_o = nullptr;   // [Vp][sf Ep]
+  float* W_o32 = nullptr;         // [V][Ep]
+  float* b_o = nullptr;           // [V]
+  CUtensorMap tm_Wenc, tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo;
+  // encoder workspace
+  int Tpad = 0;
+  __nv_bfloat16* Xsrc = nullptr;  // [Tpad][2Ep]
+  float* Pin = nullptr;           // [Tpad][6Hp]
+  __nv_bfloat16* ctxbf = nullptr; // [Tpad][4Hp]
+  float* hbuf = nullptr;
+  int* bar = nullptr;
+  int* d_src = nullptr;
+  CUtensorMap tm_Xsrc, tm_ctxbf;
+  // step workspace
+  int R_cap = 0, NC_cap = 0;
+  __nv_bfloat16 *A_s = nullptr, *X = nullptr, *A_t = nullptr;
+  float *G1 = nullptr, *S1 = nullptr, *Q = nullptr, *Cf = nullptr, *G2 = nullptr, *RO_buf = nullptr, *alpha = nullptr;
+  float4* part = nullptr;
+  int *row_src = nullptr, *row_y = nullptr, *row_dst = nullptr, *row_node = nullptr;
+  int *cand_k = nullptr, *cand_hslot = nullptr;
+  int *in_par = nullptr, *in_off = nullptr, *in_words = nullptr;
+  float* out_logp = nullptr;
+  int *out_child = nullptr, *out_amax = nullptr;
+  float* in_s = nullptr;
+  CUtensorMap tm_As, tm_X, tm_At;
+  // pinned host staging
+  void* pin = nullptr;
+  size_t pin_bytes = 0;
+  std::mutex mu;
+  // lifetime: one reference held by the user handle plus one per live context, so that
+  // nmt_model_free and nmt_ctx_free may be called in any order
+  std::atomic<int> refs{1};
+
+  ~nmt_model();
+  void free_ws();
+  void ensure_ws(int R, int NC);
+  void* pinned(size_t bytes);
+};
+
+static void free_all_model(nmt_model* m) {
+  for (float** p : {&m->Wemb_src, &m->benc, &m->Uarr, &m->W_init, &m->b_init, &m->b_att, &m->U_att, &m->Ex, &m->b_nl,
+                    &m->bx_nl, &m->Eproj, &m->W_o32, &m->b_o, &m->Pin, &m->hbuf})
+    dfree(*p);
+  for (__nv_bfloat16** p : {&m->Wenc, &m->Watt, &m->W_h1, &m->W_q, &m->W_g2, &m->W_ro, &m->W_o, &m->Xsrc, &m->ctxbf})
+    dfree(*p);
+  dfree(m->bar);
+  dfree(m->d_src);
+  m->free_ws();
+  if (m->pin) cudaFreeHost(m->pin);
+  m->pin = nullptr;
+}
+
+nmt_model::~nmt_model() {
+  cudaSetDevice(device);
+  if (st) cudaStreamSynchronize(st);
+  free_all_model(this);
+  if (own_stream && st) cudaStreamDestroy(st);
+}
+
+void nmt_model::free_ws() {
+  for (__nv_bfloat16** p : {&A_s, &X, &A_t}) dfree(*p);
+  for (float** p : {&G1, &S1, &Q, &Cf, &G2, &RO_buf, &alpha, &out_logp, &in_s}) dfree(*p);
+  dfree(part);
+  for (int** p : {&row_src, &row_y, &row_dst, &row_node, &cand_k, &cand_hslot, &in_par, &in_off, &in_words,
+                  &out_child, &out_amax})
+    dfree(*p);
+  R_cap = NC_cap = 0;
+}
+
+void* nmt_model::pinned(size_t bytes) {
+  if (bytes > pin_bytes) {
+    if (pin) {
+      CK(cudaStreamSynchronize(st));
+      cudaFreeHost(pin);
+      pin = nullptr;
+    }
+    size_t nb = std::max(bytes, pin_bytes * 2);
+    CK(cudaMallocHost(&pin, nb));
+    pin_bytes = nb;
+  }
+  return pin;
+}
+
+void nmt_model::ensure_ws(int R, int NC) {
+  if (R <= R_cap && NC <= NC_cap) return;
+  CK(cudaStreamSynchronize(st));
+  int nR = std::max(R_cap, round_up(std::max(R, 128), 128));
+  if (R > R_cap) nR = round_up(std::max(R, R_cap * 3 / 2), 128);
+  int nNC = std::max(NC_cap, std::max(NC, 1024));
+  if (NC > NC_cap) nNC = std::max(NC, NC_cap * 3 / 2);
+  free_ws();
+  R_cap = nR;
+  NC_cap = nNC;
+  A_s = dalloc<__nv_bfloat16>((size_t)R_cap * sf * Hp);
+  G1 = dalloc<float>((size_t)R_cap * 3 * Hp);
+  S1 = dalloc<float>((size_t)R_cap * Hp);
+  X = dalloc<__nv_bfloat16>((size_t)R_cap * sf * 4 * Hp);
+  Q = dalloc<float>((size_t)R_cap * Cp);
+  Cf = dalloc<float>((size_t)R_cap * Cp);
+  alpha = dalloc<float>((size_t)R_cap * maxTx);
+  G2 = dalloc<float>((size_t)R_cap * 4 * Hp);
+  RO_buf = dalloc<float>((size_t)R_cap * ROp);
+  A_t = dalloc<__nv_bfloat16>((size_t)R_cap * sf * Ep);
+  part = dalloc<float4>((size_t)R_cap * (Vp / 256));
+  row_src = dalloc<int>(R_cap);
+  row_y = dalloc<int>(R_cap);
+  row_dst = dalloc<int>(R_cap);
+  row_node = dalloc<int>(R_cap);
+  in_par = dalloc<int>(R_cap);
+  in_off = dalloc<int>(R_cap + 1);
+  out_amax = dalloc<int>(R_cap);
+  in_s = dalloc<float>((size_t)R_cap * H);
+  cand_k = dalloc<int>(NC_cap);
+  cand_hslot = dalloc<int>(NC_cap);
+  in_words = dalloc<int>(NC_cap);
+  out_logp = dalloc<float>(NC_cap);
+  out_child = dalloc<int>(NC_cap);
+  tm_As = make_tmap_bf16(A_s, R_cap, (uint64_t)sf * Hp, 128);
+  tm_X = make_tmap_bf16(X, R_cap, (uint64_t)sf * 4 * Hp, 128);
+  tm_At = make_tmap_bf16(A_t, R_cap, (uint64_t)sf * Ep, 128);
+}
+
+// ------------------------------------------------------------------------------------ context
+struct nmt_ctx {
+  nmt_model* m = nullptr;
+  int Tx = 0;
+  float* ctx = nullptr;   // [Tx][Cp]
+  float* pctx = nullptr;  // [Tx][Cp]
+  int node_cap = 0, slot_cap = 0;
+  int64_t hcap = 0;
+  int* counters = nullptr;
+  int *node_word = nullptr, *node_parent = nullptr, *node_src = nullptr, *node_slot = nullptr, *node_claim = nullptr;
+  unsigned long long* hkeys = nullptr;
+  int* hvals = nullptr;
+  float *S = nullptr, *T = nullptr, *logZ = nullptr;
+  int* amax = nullptr;
+  // host mirror of the device counters (exact when !stale; otherwise upper bounds)
+  int64_t n_nodes = 0, n_slots = 0;
+  bool stale = false;
+
+  CtxDev dev() const {
+    CtxDev c{};
+    c.counters = counters;
+    c.node_word = node_word;
+    c.node_parent = node_parent;
+    c.node_src = node_src;
+    c.node_slot = node_slot;
+    c.node_claim = node_claim;
+    c.hkeys = hkeys;
+    c.hvals = hvals;
+    c.hmask = (uint64_t)hcap - 1;
+    c.S = S;
+    c.T = T;
+    c.logZ = logZ;
+    c.amax = amax;
+    c.V = m->V;
+    c.H = m->H;
+    c.Hp = m->Hp;
+    c.Ep = m->Ep;
+    return c;
+  }
+  void sync_counters();
+  void grow_nodes(int64_t need);
+  void grow_slots(int64_t need);
+  void ensure(int64_t add_nodes, int64_t add_slots);
+  ~nmt_ctx();
+};
+
+template <typename T>
+static T* grow_copy(T* old, size_t old_n, size_t new_n, cudaStream_t st) {
+  T* p = dalloc<T>(new_n);
+  if (old && old_n) CK(cudaMemcpyAsync(p, old, old_n * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  return p;
+}
+
+void nmt_ctx::sync_counters() {
+  int h[CNT_N];
+  CK(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, m->st));
+  CK(cudaStreamSynchronize(m->st));
+  n_nodes = h[CNT_NODES];
+  n_slots = h[CNT_SLOTS];
+  stale = false;
+}
+
+void nmt_ctx::grow_nodes(int64_t need) {
+  int64_t nc = std::max<int64_t>(need, (int64_t)node_cap * 2);
+  if (nc > INT32_MAX / 2) throw NmtError(NMT_ERR_CAPACITY, "state arena: too many nodes");
+  cudaStream_t st = m->st;
+  CK(cudaStreamSynchronize(st));
+  auto g = [&](int*& p, int fill) {
+    int* q = grow_copy(p, node_cap, nc, st);
+    fill_i32(q + node_cap, nc - node_cap, fill, st);
+    dfree(p);
+    p = q;
+  };
+  g(node_word, 0);
+  g(node_parent, -1);
+  g(node_src, 0);
+  g(node_slot, -1);
+  g(node_claim, INT32_MAX);
+  int64_t nh = 1;
+  while (nh < 2 * nc) nh <<= 1;
+  if (nh != hcap) {
+    unsigned long long* nk = dalloc<unsigned long long>(nh);
+    int* nv = dalloc<int>(nh);
+    CK(cudaMemsetAsync(nk, 0xff, nh * sizeof(unsigned long long), st));
+    fill_i32(nv, nh, INT32_MIN, st);
+    if (hkeys) rehash(hkeys, hvals, hcap, nk, nv, (uint64_t)nh - 1, st);
+    CK(cudaStreamSynchronize(st));
+    dfree(hkeys);
+    dfree(hvals);
+    hkeys = nk;
+    hvals = nv;
+    hcap = nh;
+  }
+  CK(cudaStreamSynchronize(st));
+  node_cap = (int)nc;
+}
+
+void nmt_ctx::grow_slots(int64_t need) {
+  int64_t nc = std::max<int64_t>(need, (int64_t)slot_cap * 2);
+  if (nc > INT32_MAX / 2) throw NmtError(NMT_ERR_CAPACITY, "state arena: too many stepped nodes");
+  cudaStream_t st = m->st;
+  CK(cudaStreamSynchronize(st));
+  float* nS = grow_copy(S, (size_t)slot_cap * m->Hp, (size_t)nc * m->Hp, st);
+  float* nT = grow_copy(T, (size_t)slot_cap * m->Ep, (size_t)nc * m->Ep, st);
+  float* nZ = grow_copy(logZ, slot_cap, nc, st);
+  int* nA = grow_copy(amax, slot_cap, nc, st);
+  CK(cudaStreamSynchronize(st));
+  dfree(S);
+  dfree(T);
+  dfree(logZ);
+  dfree(amax);
+  S = nS;
+  T = nT;
+  logZ = nZ;
+  amax = nA;
+  slot_cap = (int)nc;
+}
+
+void nmt_ctx::ensure(int64_t add_nodes, int64_t add_slots) {
+  if (n_nodes + add_nodes > node_cap || n_slots + add_slots > slot_cap) {
+    if (stale) sync_counters();
+    if (n_nodes + add_nodes > node_cap) grow_nodes(n_nodes + add_nodes);
+    if (n_slots + add_slots > slot_cap) grow_slots(n_slots + add_slots);
+  }
+}
+
+static void model_release(nmt_model* m) {
+  if (m && m->refs.fetch_sub(1) == 1) delete m;
+}
+
+nmt_ctx::~nmt_ctx() {
+  if (m) {
+    cudaSetDevice(m->device);
+    cudaStreamSynchronize(m->st);
+  }
+  for (int** p : {&counters, &node_word, &node_parent, &node_src, &node_slot, &node_claim, &hvals, &amax}) dfree(*p);
+  dfree(hkeys);
+  for (float** p : {&ctx, &pctx, &S, &T, &logZ}) dfree(*p);
+  model_release(m);
+}
+
+// ------------------------------------------------------------------------------------ loading
+static const char* kNames[] = {
+    "Wemb", "Wemb_dec", "encoder_W", "encoder_b", "encoder_U", "encoder_Wx", "encoder_bx", "encoder_Ux",
+    "encoder_r_W", "encoder_r_b", "encoder_r_U", "encoder_r_Wx", "encoder_r_bx", "encoder_r_Ux", "ff_state_W",
+    "ff_state_b", "decoder_W", "decoder_b", "decoder_U", "decoder_Wx", "decoder_bx", "decoder_Ux", "decoder_U_nl",
+    "decoder_b_nl", "decoder_Ux_nl", "decoder_bx_nl", "decoder_Wc", "decoder_Wcx", "decoder_W_comb_att",
+    "decoder_Wc_att", "decoder_b_att", "decoder_U_att", "decoder_c_tt", "ff_logit_lstm_W", "ff_logit_lstm_b",
+    "ff_logit_prev_W", "ff_logit_prev_b", "ff_logit_ctx_W", "ff_logit_ctx_b", "ff_logit_W", "ff_logit_b"};
+
+static std::map<std::string, std::pair<int, int>> expected_shapes(int E, int H, int Vs, int V, int RO) {
+  const int C = 2 * H;
+  std::map<std::string, std::pair<int, int>> s;
+  s["Wemb"] = {Vs, E};
+  s["Wemb_dec"] = {V, E};
+  for (std::string p : {"encoder", "encoder_r", "decoder"}) {
+    s[p + "_W"] = {E, 2 * H};
+    s[p + "_b"] = {1, 2 * H};
+    s[p + "_U"] = {H, 2 * H};
+    s[p + "_Wx"] = {E, H};
+    s[p + "_bx"] = {1, H};
+    s[p + "_Ux"] = {H, H};
+  }
+  s["ff_state_W"] = {C, H};
+  s["ff_state_b"] = {1, H};
+  s["decoder_U_nl"] = {H, 2 * H};
+  s["decoder_b_nl"] = {1, 2 * H};
+  s["decoder_Ux_nl"] = {H, H};
+  s["decoder_bx_nl"] = {1, H};
+  s["decoder_Wc"] = {C, 2 * H};
+  s["decoder_Wcx"] = {C, H};
+  s["decoder_W_comb_att"] = {H, C};
+  s["decoder_Wc_att"] = {C, C};
+  s["decoder_b_att"] = {1, C};
+  s["decoder_U_att"] = {C, 1};
+  s["decoder_c_tt"] = {1, 1};
+  s["ff_logit_lstm_W"] = {H, RO};
+  s["ff_logit_lstm_b"] = {1, RO};
+  s["ff_logit_prev_W"] = {E, RO};
+  s["ff_logit_prev_b"] = {1, RO};
+  s["ff_logit_ctx_W"] = {C, RO};
+  s["ff_logit_ctx_b"] = {1, RO};
+  s["ff_logit_W"] = {E, V};
+  s["ff_logit_b"] = {1, V};
+  return s;
+}
+
+struct Upload {  // temporary device copy of one raw fp32 array
+  float* d = nullptr;
+  Upload(const Arr& a, cudaStream_t st) {
+    d = dalloc<float>((size_t)a.rows * a.cols);
+    CK(cudaMemcpyAsync(d, a.h, (size_t)a.rows * a.cols * 4, cudaMemcpyHostToDevice, st));
+  }
+  ~Upload() {
+    if (d) {
+      cudaDeviceSynchronize();
+      cudaFree(d);
+    }
+  }
+};
+
+static float* upload_vec(const std::vector<float>& v, cudaStream_t st) {
+  float* d = dalloc<float>(v.size());
+  CK(cudaMemcpyAsync(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  return d;
+}
+
+static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
+  cudaStream_t st = m->st;
+  const int E = m->E, H = m->H, V = m->V, Vs = m->Vs, RO = m->RO;
+  const int Ep = m->Ep, Hp = m->Hp, Cp = m->Cp, Vp = m->Vp, ROp = m->ROp, sf = m->sf;
+  const int C = 2 * H;
+  const int lo_h = m->split ? Hp : 0;
+  auto cmap = [&](int i) { return i < H ? i : Hp + i - H; };
+  auto hv = [&](const char* n) { return A.at(n).h; };
+
+  // ---- encoder
+  {
+    Upload w(A.at("Wemb"), st);
+    m->Wemb_src = w.d;
+    w.d = nullptr;
+  }
+  m->Wenc = dalloc<__nv_bfloat16>((size_t)6 * Hp * 2 * Ep);
+  std::vector<float> benc(6 * Hp, 0.f);
+  m->UPC = std::max(1, (H + 63) / 64);
+  m->NB = (H + m->UPC - 1) / m->UPC;
+  std::vector<float> uarr((size_t)2 * m->NB * 3 * m->UPC * H, 0.f);
+  for (int d = 0; d < 2; ++d) {
+    const std::string p = d ? "encoder_r" : "encoder";
+    Upload W(A.at(p + "_W"), st), Wx(A.at(p + "_Wx"), st);
+    for (int g = 0; g < 2; ++g)
+      pack_T(W.d + g * H, 2 * H, E, H, m->Wenc, 2 * Ep, d * 3 * Hp + g * Hp, 0, 0, 0, H, Hp, Ep, st);
+    pack_T(Wx.d, H, E, H, m->Wenc, 2 * Ep, d * 3 * Hp + 2 * Hp, 0, 0, 0, H, Hp, Ep, st);
+    const float* b = hv((p + "_b").c_str());
+    const float* bx = hv((p + "_bx").c_str());
+    for (int j = 0; j < H; ++j) {
+      benc[d * 3 * Hp + j] = b[j];
+      benc[d * 3 * Hp + Hp + j] = b[H + j];
+      benc[d * 3 * Hp + 2 * Hp + j] = bx[j];
+    }
+    const float* U = hv((p + "_U").c_str());
+    const float* Ux = hv((p + "_Ux").c_str());
+    for (int cb = 0; cb < m->NB; ++cb)
+      for (int g = 0; g < 3; ++g)
+        for (int u = 0; u < m->UPC; ++u) {
+          const int jj = cb * m->UPC + u;
+          if (jj >= H) continue;
+          float* dst = &uarr[(((size_t)(d * m->NB + cb) * 3 * m->UPC) + g * m->UPC + u) * H];
+          for (int k = 0; k < H; ++k) dst[k] = g < 2 ? U[(size_t)k * 2 * H + g * H + jj] : Ux[(size_t)k * H + jj];
+        }
+  }
+  m->benc = upload_vec(benc, st);
+  m->Uarr = upload_vec(uarr, st);
+  m->W_init = upload_vec(std::vector<float>(hv("ff_state_W"), hv("ff_state_W") + (size_t)C * H), st);
+  m->b_init = upload_vec(std::vector<float>(hv("ff_state_b"), hv("ff_state_b") + H), st);
+  m->Watt = dalloc<__nv_bfloat16>((size_t)Cp * 2 * Cp);
+  {
+    Upload w(A.at("decoder_Wc_att"), st);
+    pack_T(w.d, C, C, C, m->Watt, 2 * Cp, 0, 0, 1, 1, H, Hp, Cp, st);
+  }
+  std::vector<float> batt(Cp, 0.f), uatt(Cp, 0.f);
+  for (int i = 0; i < C; ++i) {
+    batt[cmap(i)] = hv("decoder_b_att")[i];
+    uatt[cmap(i)] = hv("decoder_U_att")[i];
+  }
+  m->b_att = upload_vec(batt, st);
+  m->U_att = upload_vec(uatt, st);
+  m->c_tt = hv("decoder_c_tt")[0];
+
+  // ---- decoder GEMM operands (K-major bf16, hi | lo in FP32CLASS)
+  m->W_h1 = dalloc<__nv_bfloat16>((size_t)3 * Hp * sf * Hp);
+  {
+    Upload U(A.at("decoder_U"), st), Ux(A.at("decoder_Ux"), st);
+    for (int g = 0; g < 2; ++g) pack_T(U.d + g * H, 2 * H, H, H, m->W_h1, sf * Hp, g * Hp, 0, 0, 0, H, Hp, lo_h, st);
+    pack_T(Ux.d, H, H, H, m->W_h1, sf * Hp, 2 * Hp, 0, 0, 0, H, Hp, lo_h, st);
+  }
+  m->W_q = dalloc<__nv_bfloat16>((size_t)Cp * sf * Hp);
+  {
+    Upload w(A.at("decoder_W_comb_att"), st);
+    pack_T(w.d, C, H, C, m->W_q, sf * Hp, 0, 0, 1, 0, H, Hp, lo_h, st);
+  }
+  const int ldg2 = Hp + Cp;
+  m->W_g2 = dalloc<__nv_bfloat16>((size_t)4 * Hp * sf * ldg2);
+  {
+    const int lo = m->split ? ldg2 : 0;
+    Upload Unl(A.at("decoder_U_nl"), st), Wc(A.at("decoder_Wc"), st), Uxnl(A.at("decoder_Ux_nl"), st),
+        Wcx(A.at("decoder_Wcx"), st);
+    for (int g = 0; g < 2; ++g) {
+      pack_T(Unl.d + g * H, 2 * H, H, H, m->W_g2, sf * ldg2, g * Hp, 0, 0, 0, H, Hp, lo, st);
+      pack_T(Wc.d + g * H, 2 * H, C, H, m->W_g2, sf * ldg2, g * Hp, Hp, 0, 1, H, Hp, lo, st);
+    }
+    pack_T(Uxnl.d, H, H, H, m->W_g2, sf * ldg2, 2 * Hp, 0, 0, 0, H, Hp, lo, st);
+    pack_T(Wcx.d, H, C, H, m->W_g2, sf * ldg2, 3 * Hp, Hp, 0, 1, H, Hp, lo, st);
+  }
+  std::vector<float> bnl(2 * Hp, 0.f), bxnl(Hp, 0.f);
+  for (int j = 0; j < H; ++j) {
+    bnl[j] = hv("decoder_b_nl")[j];
+    bnl[Hp + j] = hv("decoder_b_nl")[H + j];
+    bxnl[j] = hv("decoder_bx_nl")[j];
+  }
+  m->b_nl = upload_vec(bnl, st);
+  m->bx_nl = upload_vec(bxnl, st);
+  const int ldro = Cp + Hp;
+  m->W_ro = dalloc<__nv_bfloat16>((size_t)ROp * sf * ldro);
+  {
+    const int lo = m->split ? ldro : 0;
+    Upload Wctx(A.at("ff_logit_ctx_W"), st), Wl(A.at("ff_logit_lstm_W"), st);
+    pack_T(Wctx.d, RO, C, RO, m->W_ro, sf * ldro, 0, 0, 0, 1, H, Hp, lo, st);
+    pack_T(Wl.d, RO, H, RO, m->W_ro, sf * ldro, 0, Cp, 0, 0, H, Hp, lo, st);
+  }
+  m->W_o = dalloc<__nv_bfloat16>((size_t)Vp * sf * Ep);
+  m->W_o32 = dalloc<float>((size_t)V * Ep);
+  {
+    Upload Wo(A.at("ff_logit_W"), st);
+    pack_T(Wo.d, V, E, V, m->W_o, sf * Ep, 0, 0, 0, 0, H, Hp, m->split ? Ep : 0, st);
+    transpose_f32(Wo.d, E, V, m->W_o32, Ep, st);
+  }
+  m->b_o = upload_vec(std::vector<float>(hv("ff_logit_b"), hv("ff_logit_b") + V), st);
+  {  // b_o folded into the vocabulary GEMM as bf16 hi + lo columns
+    std::vector<__nv_bfloat16> bh(V), bl(V);
+    for (int w = 0; w < V; ++w) {
+      const float b = hv("ff_logit_b")[w];
+      bh[w] = __float2bfloat16_rn(b);
+      bl[w] = __float2bfloat16_rn(b - __bfloat162float(bh[w]));
+    }
+    const size_t pitch = (size_t)sf * Ep * 2;
+    CK(cudaMemcpy2DAsync(m->W_o + E, pitch, bh.data(), 2, 2, V, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpy2DAsync(m->W_o + (m->split ? Ep + E : E + 1), pitch, bl.data(), 2, 2, V, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  // ---- precomputed target-embedding projections (always bf16x3): Ex = e.[W|Wx] + [b|bx],
+  //      Eproj = e.W_p + b_p + b_l + b_ctx; row V is the BOS row (zero embedding -> biases only)
+  {
+    const int Vr = round_up(V, 128);
+    __nv_bfloat16* Aemb = dalloc<__nv_bfloat16>((size_t)Vr * 2 * Ep);
+    {
+      Upload e(A.at("Wemb_dec"), st);
+      pack_rows(e.d, E, V, E, Aemb, 2 * Ep, 0, Ep, st);
+    }
+    CUtensorMap tmE = make_tmap_bf16(Aemb, Vr, 2 * Ep, 128);
+    __nv_bfloat16* B1 = dalloc<__nv_bfloat16>((size_t)3 * Hp * 2 * Ep);
+    {
+      Upload W(A.at("decoder_W"), st), Wx(A.at("decoder_Wx"), st);
+      for (int g = 0; g < 2; ++g) pack_T(W.d + g * H, 2 * H, E, H, B1, 2 * Ep, g * Hp, 0, 0, 0, H, Hp, Ep, st);
+      pack_T(Wx.d, H, E, H, B1, 2 * Ep, 2 * Hp, 0, 0, 0, H, Hp, Ep, st);
+    }
+    std::vector<float> b1(3 * Hp, 0.f);
+    for (int j = 0; j < H; ++j) {
+      b1[j] = hv("decoder_b")[j];
+      b1[Hp + j] = hv("decoder_b")[H + j];
+      b1[2 * Hp + j] = hv("decoder_bx")[j];
+    }
+    float* db1 = upload_vec(b1, st);
+    m->Ex = dalloc<float>((size_t)(V + 1) * 3 * Hp);
+    CUtensorMap tmB1 = make_tmap_bf16(B1, 3 * Hp, 2 * Ep, 128);
+    gemm_store(tmE, tmB1, gemm_shape(V, nullptr, 3 * Hp, Ep, 0, true, Ep, Ep), m->Ex, 3 * Hp, db1, V, st);
+    CK(cudaMemcpyAsync(m->Ex + (size_t)V * 3 * Hp, db1, 3 * Hp * 4, cudaMemcpyDeviceToDevice, st));
+
+    __nv_bfloat16* Bp = dalloc<__nv_bfloat16>((size_t)ROp * 2 * Ep);
+    {
+      Upload Wp(A.at("ff_logit_prev_W"), st);
+      pack_T(Wp.d, RO, E, RO, Bp, 2 * Ep, 0, 0, 0, 0, H, Hp, Ep, st);
+    }
+    std::vector<float> bsum(ROp, 0.f);
+    for (int k = 0; k < RO; ++k)
+      bsum[k] = hv("ff_logit_prev_b")[k] + hv("ff_logit_lstm_b")[k] + hv("ff_logit_ctx_b")[k];
+    float* dbs = upload_vec(bsum, st);
+    m->Eproj = dalloc<float>((size_t)(V + 1) * ROp);
+    CUtensorMap tmBp = make_tmap_bf16(Bp, ROp, 2 * Ep, 128);
+    gemm_store(tmE, tmBp, gemm_shape(V, nullptr, ROp, Ep, 0, true, Ep, Ep), m->Eproj, ROp, dbs, V, st);
+    CK(cudaMemcpyAsync(m->Eproj + (size_t)V * ROp, dbs, ROp * 4, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    dfree(Aemb);
+    dfree(B1);
+    dfree(Bp);
+    dfree(db1);
+    dfree(dbs);
+  }
+
+  // ---- tensor maps of the weight operands
+  m->tm_Wenc = make_tmap_bf16(m->Wenc, 6 * Hp, 2 * Ep, 128);
+  m->tm_Watt = make_tmap_bf16(m->Watt, Cp, 2 * Cp, 128);
+  m->tm_Wh1 = make_tmap_bf16(m->W_h1, 3 * Hp, sf * Hp, 128);
+  m->tm_Wq = make_tmap_bf16(m->W_q, Cp, sf * Hp, 128);
+  m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, 128);
+  m->tm_Wro = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 128);
+  m->tm_Wo = make_tmap_bf16(m->W_o, Vp, sf * Ep, 256);
+
+  // ---- encoder workspace
+  m->Tpad = round_up(m->maxTx, 128);
+  m->Xsrc = dalloc<__nv_bfloat16>((size_t)m->Tpad * 2 * Ep);
+  m->Pin = dalloc<float>((size_t)m->Tpad * 6 * Hp);
+  m->ctxbf = dalloc<__nv_bfloat16>((size_t)m->Tpad * 4 * Hp);
+  m->hbuf = dalloc<float>(4 * Hp);
+  m->bar = dalloc<int>(2);
+  m->d_src = dalloc<int>(m->maxTx);
+  m->tm_Xsrc = make_tmap_bf16(m->Xsrc, m->Tpad, 2 * Ep, 128);
+  m->tm_ctxbf = make_tmap_bf16(m->ctxbf, m->Tpad, 4 * Hp, 128);
+  CK(cudaStreamSynchronize(st));
+}
+
+static void parse_and_build(const char* buf, size_t len, const nmt_opts* opts, nmt_model** out) {
+  if (!out) throw NmtError(NMT_ERR_INVALID_ARG, "out is NULL");
+  // header lines
+  size_t pos = 0;
+  auto line = [&]() -> std::string {
+    size_t e = pos;
+    while (e < len && buf[e] != '\n') ++e;
+    if (e >= len) throw NmtError(NMT_ERR_FORMAT, "params: truncated header");
+    std::string s(buf + pos, e - pos);
+    pos = e + 1;
+    return s;
+  };
+  if (line() != "NMTPARAMS 1") throw NmtError(NMT_ERR_FORMAT, "params: bad magic (expected 'NMTPARAMS 1')");
+  std::istringstream dl(line());
+  std::string tag, ro_kv;
+  int E = 0, H = 0, Vs = 0, V = 0;
+  dl >> tag >> E >> H >> Vs >> V >> ro_kv;
+  if (tag != "dims" || E <= 0 || H <= 0 || Vs <= 0 || V <= 0) throw NmtError(NMT_ERR_FORMAT, "params: bad dims line");
+  int maxout;
+  if (ro_kv == "readout=tanh") maxout = 0;
+  else if (ro_kv == "readout=maxout") maxout = 1;
+  else throw NmtError(NMT_ERR_FORMAT, "params: bad readout '" + ro_kv + "'");
+  if (H > 1024) throw NmtError(NMT_ERR_SHAPE, "dim_hid > 1024 not supported");
+  std::istringstream al(line());
+  int n = 0;
+  al >> tag >> n;
+  if (tag != "arrays" || n <= 0) throw NmtError(NMT_ERR_FORMAT, "params: bad arrays line");
+  std::vector<std::tuple<std::string, int, int>> hdr;
+  for (int i = 0; i < n; ++i) {
+    std::istringstream ls(line());
+    std::string name;
+    int r = 0, c = 0;
+    ls >> name >> r >> c;
+    if (name.empty() || r <= 0 || c <= 0) throw NmtError(NMT_ERR_FORMAT, "params: bad array line " + std::to_string(i));
+    hdr.emplace_back(name, r, c);
+  }
+  pos = (pos + 63) / 64 * 64;
+  size_t need = 0;
+  for (auto& h : hdr) need += (size_t)std::get<1>(h) * std::get<2>(h) * 4;
+  if (pos + need != len)
+    throw NmtError(NMT_ERR_FORMAT, "params: payload is " + std::to_string(len > pos ? len - pos : 0) +
+                                       " bytes, header declares " + std::to_string(need));
+  const int RO = maxout ? 2 * E : E;
+  auto exp = expected_shapes(E, H, Vs, V, RO);
+  std::map<std::string, Arr> A;
+  size_t off = pos;
+  for (auto& h : hdr) {
+    const std::string& nm = std::get<0>(h);
+    A[nm] = Arr{reinterpret_cast<const float*>(buf + off), std::get<1>(h), std::get<2>(h)};
+    off += (size_t)std::get<1>(h) * std::get<2>(h) * 4;
+  }
+  for (const char* nm : kNames) {
+    auto it = A.find(nm);
+    if (it == A.end()) throw NmtError(NMT_ERR_MISSING_PARAM, std::string("missing parameter ") + nm);
+    auto e = exp.at(nm);
+    if (it->second.rows != e.first || it->second.cols != e.second)
+      throw NmtError(NMT_ERR_SHAPE, std::string(nm) + ": expected " + std::to_string(e.first) + "x" +
+                                        std::to_string(e.second) + ", got " + std::to_string(it->second.rows) + "x" +
+                                        std::to_string(it->second.cols));
+  }
+  nmt_opts o{};
+  if (opts) o = *opts;
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (o.device < 0 || o.device >= ndev) throw NmtError(NMT_ERR_CUDA, "no such CUDA device");
+  CK(cudaSetDevice(o.device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, o.device));
+  if (prop.major != 10) throw NmtError(NMT_ERR_CUDA, std::string("libnmt needs an sm_100 GPU, found ") + prop.name);
+  std::unique_ptr<nmt_model> m(new nmt_model());
+  m->device = o.device;
+  if (o.stream) {
+    m->st = static_cast<cudaStream_t>(o.stream);
+  } else {
+    CK(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
+    m->own_stream = true;
+  }
+  m->split = o.precision == NMT_PREC_FP32CLASS;
+  m->sf = m->split ? 2 : 1;
+  m->E = E;
+  m->H = H;
+  m->Vs = Vs;
+  m->V = V;
+  m->RO = RO;
+  m->maxout = maxout;
+  m->maxTx = o.max_src_len > 0 ? o.max_src_len : 64;
+  m->Ep = round_up(E + 2, 64);
+  m->Hp = round_up(H, 128);
+  m->Cp = 2 * m->Hp;
+  m->Vp = round_up(V, 256);
+  m->ROp = round_up(RO, 128);
+  build_model(m.get(), A);
+  *out = m.release();
+}
+
+// ------------------------------------------------------------------------------------ step
+static StepDev step_view(nmt_model* m, nmt_ctx* c) {
+  StepDev d{};
+  d.R = c->counters + CNT_R;
+  d.row_src = m->row_src;
+  d.row_y = m->row_y;
+  d.row_dst = m->row_dst;
+  d.V = m->V;
+  d.H = m->H;
+  d.Hp = m->Hp;
+  d.Cp = m->Cp;
+  d.E = m->E;
+  d.Ep = m->Ep;
+  d.ROp = m->ROp;
+  d.maxout = m->maxout;
+  d.A_s = m->A_s;
+  d.lda_s = m->sf * m->Hp;
+  d.lo_s = m->split ? m->Hp : 0;
+  d.G1 = m->G1;
+  d.Ex = m->Ex;
+  d.S1 = m->S1;
+  d.X = m->X;
+  d.ldx = m->sf * 4 * m->Hp;
+  d.lo_x = m->split ? 4 * m->Hp : 0;
+  d.Q = m->Q;
+  d.Cf = m->Cf;
+  d.alpha_out = m->alpha;
+  d.alpha_ld = m->maxTx;
+  d.G2 = m->G2;
+  d.b_nl = m->b_nl;
+  d.bx_nl = m->bx_nl;
+  d.RO = m->RO_buf;
+  d.Eproj = m->Eproj;
+  d.A_t = m->A_t;
+  d.lda_t = m->sf * m->Ep;
+  d.lo_t = m->split ? m->Ep : 0;
+  d.part = m->part;
+  d.n_tiles = m->Vp / 256;
+  return d;
+}
+
+// one decoder forward step over the rows planned in m->row_* (count at c->counters[CNT_R])
+static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
+  cudaStream_t st = m->st;
+  const StepDev d = step_view(m, c);
+  AttnCtx a{c->pctx, c->ctx, m->U_att, m->c_tt, c->Tx};
+  const int* Rd = d.R;
+  const int Hp = m->Hp, Cp = m->Cp, Ep = m->Ep;
+  const bool sp = m->split;
+  step_elementwise(EW_GATHER, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
+  gemm_store(m->tm_As, m->tm_Wh1, gemm_shape(0, Rd, 3 * Hp, Hp, 0, sp, Hp, Hp), m->G1, 3 * Hp, nullptr, R_max, st);
+  step_elementwise(EW_GRU1, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
+  gemm_store(m->tm_X, m->tm_Wq, gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp), m->Q, Cp, nullptr, R_max, st);
+  step_elementwise(EW_ATTN, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
+  {
+    GemmShape g = gemm_shape(0, Rd, 4 * Hp, Hp + Cp, 0, sp, 4 * Hp, Hp + Cp);
+    g.nreg = 3;
+    g.reg_n_end[0] = 2 * Hp, g.reg_k0[0] = 0, g.reg_k1[0] = Hp + Cp;  // gates: s1 U_nl + c Wc
+    g.reg_n_end[1] = 3 * Hp, g.reg_k0[1] = 0, g.reg_k1[1] = Hp;       // s1 Ux_nl
+    g.reg_n_end[2] = 4 * Hp, g.reg_k0[2] = Hp, g.reg_k1[2] = Hp + Cp; // c Wcx
+    gemm_store(m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, nullptr, R_max, st);
+  }
+  step_elementwise(EW_GRU2, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
+  gemm_store(m->tm_X, m->tm_Wro, gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp), m->RO_buf, m->ROp,
+             nullptr, R_max, st);
+  step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
+  gemm_lse(m->tm_At, m->tm_Wo, gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep), m->part, m->V, R_max, st);
+  step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
+}
+
+static PlanIO plan_io(nmt_model* m, int np, int nc, const int* par, const int* off, const int* words) {
+  PlanIO io{};
+  io.n_par = np;
+  io.n_cand = nc;
+  io.parents = par;
+  io.offsets = off;
+  io.words = words;
+  io.cand_k = m->cand_k;
+  io.cand_hslot = m->cand_hslot;
+  io.row_src = m->row_src;
+  io.row_y = m->row_y;
+  io.row_dst = m->row_dst;
+  io.row_node = m->row_node;
+  return io;
+}
+
+static void run_call(nmt_model* m, nmt_ctx* c, const PlanIO& io, float* out_logp, int* out_child,
+                     long long* out_child64, int* out_amax) {
+  const CtxDev cd = c->dev();
+  plan(cd, io, c->counters + CNT_R, m->st);
+  run_step(m, c, io.n_par);
+  gather_dot(cd, io, m->W_o32, m->b_o, m->Ep, out_logp, out_child, out_child64, out_amax, m->st);
+}
+
+// step one node (if not yet stepped) outside a score_batch; dst = scratch slot 1 when `scratch`
+static int step_single(nmt_model* m, nmt_ctx* c, int node, bool scratch) {
+  cudaStream_t st = m->st;
+  if (c->stale) c->sync_counters();
+  if (node < 0 || node >= c->n_nodes) throw NmtError(NMT_ERR_BAD_STATE, "unknown state " + std::to_string(node));
+  int info[4];  // word, parent, src, slot
+  CK(cudaMemcpyAsync(&info[0], c->node_word + node, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&info[1], c->node_parent + node, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&info[2], c->node_src + node, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&info[3], c->node_slot + node, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (!scratch && info[3] >= 0) return info[3];
+  int src = info[2];
+  if (info[1] >= 0) {
+    CK(cudaMemcpyAsync(&src, c->node_slot + info[1], 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  m->ensure_ws(1, 1);
+  c->ensure(0, 1);
+  const int dst = scratch ? 1 : (int)c->n_slots;
+  const int one = 1;
+  CK(cudaMemcpyAsync(m->row_src, &src, 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(m->row_y, &info[0], 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(m->row_dst, &dst, 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->counters + CNT_R, &one, 4, cudaMemcpyHostToDevice, st));
+  run_step(m, c, 1);
+  if (!scratch) {
+    CK(cudaMemcpyAsync(c->node_slot + node, &dst, 4, cudaMemcpyHostToDevice, st));
+    const int ns = dst + 1;
+    CK(cudaMemcpyAsync(c->counters + CNT_SLOTS, &ns, 4, cudaMemcpyHostToDevice, st));
+    c->n_slots = ns;
+  }
+  CK(cudaStreamSynchronize(st));
+  return dst;
+}
+
+// ------------------------------------------------------------------------------------ C ABI
+extern "C" {
+
+const char* nmt_last_error(void) { return g_err.c_str(); }
+
+nmt_status nmt_load_buffer(const void* buf, size_t len, const nmt_opts* opts, nmt_model** out) {
+  if (!buf) return fail(NMT_ERR_INVALID_ARG, "buf is NULL");
+  return guard([&] { parse_and_build(static_cast<const char*>(buf), len, opts, out); });
+}
+
+nmt_status nmt_load(const char* path, const nmt_opts* opts, nmt_model** out) {
+  if (!path) return fail(NMT_ERR_INVALID_ARG, "params_path is NULL");
+  std::ifstream f(path, std::ios::binary | std::ios::ate);
+  if (!f) return fail(NMT_ERR_IO, std::string("cannot open params file ") + path);
+  const std::streamsize n = f.tellg();
+  f.seekg(0);
+  std::vector<char> buf((size_t)n);
+  if (!f.read(buf.data(), n)) return fail(NMT_ERR_IO, std::string("cannot read params file ") + path);
+  return nmt_load_buffer(buf.data(), buf.size(), opts, out);
+}
+
+nmt_status nmt_model_dims(const nmt_model* m, nmt_dims* out) {
+  if (!m || !out) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
+  out->dim_emb = m->E;
+  out->dim_hid = m->H;
+  out->vocab_src = m->Vs;
+  out->vocab_tgt = m->V;
+  out->max_src_len = m->maxTx;
+  out->readout = m->maxout ? NMT_READOUT_MAXOUT : NMT_READOUT_TANH;
+  return NMT_OK;
+}
+
+void nmt_model_free(nmt_model* m) { model_release(m); }
+
+nmt_status nmt_encode(nmt_model* m, const int32_t* src, int32_t len, nmt_ctx** out) {
+  if (!m || !out) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
+  if (len == 0) return fail(NMT_ERR_EMPTY_SOURCE, "empty source");
+  if (len < 0 || !src) return fail(NMT_ERR_INVALID_ARG, "bad source");
+  if (len > m->maxTx)
+    return fail(NMT_ERR_CAPACITY, "source length " + std::to_string(len) + " > max_src_len " + std::to_string(m->maxTx));
+  for (int i = 0; i < len; ++i)
+    if (src[i] < 0 || src[i] >= m->Vs)
+      return fail(NMT_ERR_TOKEN_RANGE, "source token " + std::to_string(src[i]) + " at " + std::to_string(i) +
+                                           " outside [0, " + std::to_string(m->Vs) + ")");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    cudaStream_t st = m->st;
+    std::unique_ptr<nmt_ctx> c(new nmt_ctx());
+    m->refs.fetch_add(1);
+    c->m = m;
+    c->Tx = len;
+    c->ctx = dalloc<float>((size_t)len * m->Cp);
+    c->pctx = dalloc<float>((size_t)len * m->Cp);
+    c->counters = dalloc<int>(CNT_N);
+    c->grow_nodes(4096);
+    c->grow_slots(1024);
+    // E1/E2: embeddings -> input projections of both directions (split bf16x3 GEMM)
+    CK(cudaMemcpyAsync(m->d_src, src, len * 4, cudaMemcpyHostToDevice, st));
+    enc_gather(m->Wemb_src, m->d_src, len, m->E, m->Ep, m->Xsrc, st);
+    gemm_store(m->tm_Xsrc, m->tm_Wenc, gemm_shape(len, nullptr, 6 * m->Hp, m->Ep, 0, true, m->Ep, m->Ep), m->Pin,
+               6 * m->Hp, m->benc, len, st);
+    // E3/E4: recurrence
+    EncDev e{};
+    e.H = m->H;
+    e.Hp = m->Hp;
+    e.NB = m->NB;
+    e.UPC = m->UPC;
+    e.Uarr = m->Uarr;
+    e.Pin = m->Pin;
+    e.ctx = c->ctx;
+    e.hbuf = m->hbuf;
+    e.bar = m->bar;
+    e.W_init = m->W_init;
+    e.b_init = m->b_init;
+    e.ctxbf = m->ctxbf;
+    enc_recur(e, len, st);
+    // E5: s0 into slot 0; E7: pctx = ctx.Wc_att + b_att
+    enc_init(e, len, c->S, st);
+    gemm_store(m->tm_ctxbf, m->tm_Watt, gemm_shape(len, nullptr, m->Cp, m->Cp, 0, true, m->Cp, m->Cp), c->pctx, m->Cp,
+               m->b_att, len, st);
+    // root node 0 = (s0, BOS)
+    const int cnt[CNT_N] = {1, 2, 0, 0};
+    const int w = -1, par = -1, srcslot = 0;
+    CK(cudaMemcpyAsync(c->counters, cnt, sizeof(cnt), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->node_word, &w, 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->node_parent, &par, 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->node_src, &srcslot, 4, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    c->n_nodes = 1;
+    c->n_slots = 2;
+    *out = c.release();
+  });
+}
+
+nmt_state nmt_root(const nmt_ctx* c) { return c ? 0 : -1; }
+
+void nmt_ctx_free(nmt_ctx* c) { delete c; }
+
+nmt_status nmt_score_batch(nmt_ctx* c, int32_t np, const nmt_state* parents, const int32_t* off, const int32_t* words,
+                           float* out_logp, nmt_state* out_child, int32_t* out_argmax) {
+  if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");
+  if (np < 0) return fail(NMT_ERR_INVALID_ARG, "n_parents < 0");
+  if (np > 0 && (!parents || !off)) return fail(NMT_ERR_INVALID_ARG, "parents/cand_offsets is NULL");
+  nmt_model* m = c->m;
+  const int nc = np > 0 ? off[np] : 0;
+  if (np > 0 && off[0] != 0) return fail(NMT_ERR_INVALID_ARG, "cand_offsets[0] != 0");
+  for (int k = 0; k < np; ++k)
+    if (off[k + 1] < off[k]) return fail(NMT_ERR_INVALID_ARG, "cand_offsets decrease at " + std::to_string(k));
+  if (nc > 0 && (!words || !out_logp || !out_child)) return fail(NMT_ERR_INVALID_ARG, "NULL candidate/output array");
+  for (int i = 0; i < nc; ++i)
+    if (words[i] < 0 || words[i] >= m->V)
+      return fail(NMT_ERR_TOKEN_RANGE, "cand_words[" + std::to_string(i) + "] = " + std::to_string(words[i]) +
+                                           " outside [0, " + std::to_string(m->V) + ")");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    cudaStream_t st = m->st;
+    if (c->stale) c->sync_counters();
+    for (int k = 0; k < np; ++k)
+      if (parents[k] < 0 || parents[k] >= c->n_nodes)
+        throw NmtError(NMT_ERR_BAD_STATE, "unknown state " + std::to_string(parents[k]) + " (parents[" +
+                                              std::to_string(k) + "])");
+    if (np == 0) return;
+    m->ensure_ws(np, nc);
+    c->ensure(nc, np);
+    // stage the request in pinned memory: parents | offsets | words
+    int* h = static_cast<int*>(m->pinned((size_t)(2 * np + 1 + nc) * 4 + (size_t)(nc + np + CNT_N) * 8 + 64));
+    int* hp = h;
+    int* ho = hp + np;
+    int* hw = ho + np + 1;
+    for (int k = 0; k < np; ++k) hp[k] = (int)parents[k];
+    std::memcpy(ho, off, (size_t)(np + 1) * 4);
+    if (nc) std::memcpy(hw, words, (size_t)nc * 4);
+    CK(cudaMemcpyAsync(m->in_par, hp, (size_t)np * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m->in_off, ho, (size_t)(np + 1) * 4, cudaMemcpyHostToDevice, st));
+    if (nc) CK(cudaMemcpyAsync(m->in_words, hw, (size_t)nc * 4, cudaMemcpyHostToDevice, st));
+    const PlanIO io = plan_io(m, np, nc, m->in_par, m->in_off, m->in_words);
+    run_call(m, c, io, m->out_logp, m->out_child, nullptr, m->out_amax);
+    float* rl = reinterpret_cast<float*>(hw + nc);
+    int* rc = reinterpret_cast<int*>(rl + nc);
+    int* ra = rc + nc;
+    int* rcnt = ra + np;
+    if (nc) {
+      CK(cudaMemcpyAsync(rl, m->out_logp, (size_t)nc * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(rc, m->out_child, (size_t)nc * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaMemcpyAsync(ra, m->out_amax, (size_t)np * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rcnt, c->counters, CNT_N * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (rcnt[CNT_ERR]) {
+      const int z = 0;
+      CK(cudaMemcpy(c->counters + CNT_ERR, &z, 4, cudaMemcpyHostToDevice));
+      throw NmtError(NMT_ERR_BAD_STATE, "device-side validation failed (flags " + std::to_string(rcnt[CNT_ERR]) + ")");
+    }
+    c->n_nodes = rcnt[CNT_NODES];
+    c->n_slots = rcnt[CNT_SLOTS];
+    if (nc) std::memcpy(out_logp, rl, (size_t)nc * 4);
+    for (int i = 0; i < nc; ++i) out_child[i] = rc[i];
+    if (out_argmax) std::memcpy(out_argmax, ra, (size_t)np * 4);
+  });
+}
+
+nmt_status nmt_score_batch_dev(nmt_ctx* c, int32_t np, const int32_t* parents, const int32_t* off, int32_t nc,
+                               const int32_t* words, float* out_logp, int32_t* out_child, int32_t* out_argmax) {
+  if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");
+  if (np < 0 || nc < 0) return fail(NMT_ERR_INVALID_ARG, "negative count");
+  if (np == 0) return NMT_OK;
+  if (!parents || !off || (nc > 0 && (!words || !out_logp))) return fail(NMT_ERR_INVALID_ARG, "NULL device array");
+  nmt_model* m = c->m;
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    m->ensure_ws(np, nc);
+    c->ensure(nc, np);
+    const PlanIO io = plan_io(m, np, nc, parents, off, words);
+    run_call(m, c, io, out_logp, out_child, nullptr, out_argmax);
+    c->n_nodes += nc;  // upper bounds until the next sync
+    c->n_slots += np;
+    c->stale = true;
+  });
+}
+
+nmt_status nmt_ctx_check(nmt_ctx* c) {
+  if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->m->mu);
+    CK(cudaSetDevice(c->m->device));
+    int h[CNT_N];
+    CK(cudaMemcpyAsync(h, c->counters, sizeof(h), cudaMemcpyDeviceToHost, c->m->st));
+    CK(cudaStreamSynchronize(c->m->st));
+    c->n_nodes = h[CNT_NODES];
+    c->n_slots = h[CNT_SLOTS];
+    c->stale = false;
+    if (h[CNT_ERR]) {
+      const int z = 0;
+      CK(cudaMemcpy(c->counters + CNT_ERR, &z, 4, cudaMemcpyHostToDevice));
+      throw NmtError((h[CNT_ERR] & ERR_TOKEN) ? NMT_ERR_TOKEN_RANGE
+                                              : ((h[CNT_ERR] & ERR_OFFSETS) ? NMT_ERR_INVALID_ARG : NMT_ERR_BAD_STATE),
+                     "device-side validation failed (flags " + std::to_string(h[CNT_ERR]) + ")");
+    }
+  });
+}
+
+nmt_status nmt_ctx_stats(nmt_ctx* c, int64_t* n_nodes, int64_t* n_stepped) {
+  if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->m->mu);
+    CK(cudaSetDevice(c->m->device));
+    c->sync_counters();
+    if (n_nodes) *n_nodes = c->n_nodes;
+    if (n_stepped) *n_stepped = c->n_slots - 2;  // slots 0 (s0) and 1 (scratch) are not steps
+  });
+}
+
+nmt_status nmt_inject_states(nmt_ctx* c, int32_t n, const float* s, const int32_t* y, nmt_state* out) {
+  if (!c || n < 0 || (n > 0 && (!s || !y || !out))) return fail(NMT_ERR_INVALID_ARG, "bad argument");
+  nmt_model* m = c->m;
+  for (int i = 0; i < n; ++i)
+    if (y[i] < -1 || y[i] >= m->V) return fail(NMT_ERR_TOKEN_RANGE, "y_prev out of range");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    if (n == 0) return;
+    cudaStream_t st = m->st;
+    if (c->stale) c->sync_counters();
+    m->ensure_ws(n, n);
+    c->ensure(n, n);
+    // (in_s holds R_cap x H floats; the y and ids use the candidate scratch)
+    CK(cudaMemcpyAsync(m->in_s, s, (size_t)n * m->H * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m->in_words, y, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    inject(c->dev(), n, m->in_s, m->in_words, m->out_child, st);
+    std::vector<int> ids(n);
+    CK(cudaMemcpyAsync(ids.data(), m->out_child, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int i = 0; i < n; ++i) out[i] = ids[i];
+    c->n_nodes += n;
+    c->n_slots += n;
+  });
+}
+
+nmt_status nmt_logprobs_full(nmt_ctx* c, nmt_state node, float* out) {
+  if (!c || !out) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
+  nmt_model* m = c->m;
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    const int slot = step_single(m, c, (int)node, false);
+    float* d = dalloc<float>(m->V);
+    full_row(c->T, m->W_o32, m->b_o, c->logZ, slot, m->Ep, m->V, d, m->st);
+    CK(cudaMemcpyAsync(out, d, (size_t)m->V * 4, cudaMemcpyDeviceToHost, m->st));
+    CK(cudaStreamSynchronize(m->st));
+    dfree(d);
+  });
+}
+
+nmt_status nmt_debug_encoder(nmt_ctx* c, float* ctx, float* pctx, float* s0) {
+  if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");
+  nmt_model* m = c->m;
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    const int H = m->H, Hp = m->Hp, Cp = m->Cp, Tx = c->Tx;
+    std::vector<float> a((size_t)Tx * Cp), b((size_t)Tx * Cp), s(Hp);
+    CK(cudaMemcpyAsync(a.data(), c->ctx, a.size() * 4, cudaMemcpyDeviceToHost, m->st));
+    CK(cudaMemcpyAsync(b.data(), c->pctx, b.size() * 4, cudaMemcpyDeviceToHost, m->st));
+    CK(cudaMemcpyAsync(s.data(), c->S, (size_t)Hp * 4, cudaMemcpyDeviceToHost, m->st));
+    CK(cudaStreamSynchronize(m->st));
+    for (int j = 0; j < Tx; ++j)
+      for (int i = 0; i < 2 * H; ++i) {
+        const int ci = i < H ? i : Hp + i - H;
+        if (ctx) ctx[(size_t)j * 2 * H + i] = a[(size_t)j * Cp + ci];
+        if (pctx) pctx[(size_t)j * 2 * H + i] = b[(size_t)j * Cp + ci];
+      }
+    if (s0) std::memcpy(s0, s.data(), (size_t)H * 4);
+  });
+}
+
+nmt_status nmt_debug_intermediates(nmt_ctx* c, nmt_state node, float* s1, float* alpha, float* ctxv, float* s2,
+                                   float* t, float* logZ, int32_t* argmax) {
+  if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");
+  nmt_model* m = c->m;
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    step_single(m, c, (int)node, true);
+    cudaStream_t st = m->st;
+    const int H = m->H, Hp = m->Hp, Cp = m->Cp;
+    std::vector<float> hs1(Hp), hal(m->maxTx), hc(Cp), hs2(Hp), ht(m->Ep);
+    float z;
+    int am;
+    CK(cudaMemcpyAsync(hs1.data(), m->S1, Hp * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hal.data(), m->alpha, m->maxTx * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc.data(), m->Cf, Cp * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs2.data(), c->S + (size_t)1 * Hp, Hp * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ht.data(), c->T + (size_t)1 * m->Ep, m->Ep * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&z, c->logZ + 1, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&am, c->amax + 1, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (s1) std::memcpy(s1, hs1.data(), H * 4);
+    if (alpha) std::memcpy(alpha, hal.data(), c->Tx * 4);
+    if (ctxv)
+      for (int i = 0; i < 2 * H; ++i) ctxv[i] = hc[i < H ? i : Hp + i - H];
+    if (s2) std::memcpy(s2, hs2.data(), H * 4);
+    if (t) std::memcpy(t, ht.data(), m->E * 4);
+    if (logZ) *logZ = z;
+    if (argmax) *argmax = am;
+  });
+}
+
+nmt_status nmt_test_gemm(int32_t M, int32_t N, int32_t K, int32_t split, const float* A, const float* B,
+                         const float* bias, float* C) {
+  if (M <= 0 || N <= 0 || K <= 0 || N % 128 || K % 64 || !A || !B || !C)
+    return fail(NMT_ERR_INVALID_ARG, "nmt_test_gemm: bad shape or NULL");
+  return guard([&] {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const int sf = split ? 2 : 1;
+    const int Mp = round_up(M, 128);
+    float *dA = dalloc<float>((size_t)M * K), *dB = dalloc<float>((size_t)K * N), *dC = dalloc<float>((size_t)M * N);
+    float* db = bias ? dalloc<float>(N) : nullptr;
+    CK(cudaMemcpy(dA, A, (size_t)M * K * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, B, (size_t)K * N * 4, cudaMemcpyHostToDevice));
+    if (bias) CK(cudaMemcpy(db, bias, (size_t)N * 4, cudaMemcpyHostToDevice));
+    __nv_bfloat16* a = dalloc<__nv_bfloat16>((size_t)Mp * sf * K);
+    __nv_bfloat16* b = dalloc<__nv_bfloat16>((size_t)N * sf * K);
+    pack_rows(dA, K, M, K, a, sf * K, 0, split ? K : 0, st);
+    pack_T(dB, N, K, N, b, sf * K, 0, 0, 0, 0, 1, 1, split ? K : 0, st);
+    CUtensorMap ta = make_tmap_bf16(a, Mp, sf * K, 128), tb = make_tmap_bf16(b, N, sf * K, 128);
+    gemm_store(ta, tb, gemm_shape(M, nullptr, N, K, 0, split != 0, K, K), dC, N, db, M, st);
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(C, dC, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+    dfree(dA);
+    dfree(dB);
+    dfree(dC);
+    dfree(db);
+    dfree(a);
+    dfree(b);
+    cudaStreamDestroy(st);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,304 @@
+// gemm.cu - persistent warp-specialised tcgen05 GEMM engine for sm_100a.
+//
+//   C[M x N] = A[M x K] . B[N x K]^T        A, B bf16 K-major in HBM, fp32 accumulate in TMEM.
+//
+// Roles (192 threads, 1 CTA / SM): warp 0 = TMA producer (one elected lane), warp 1 = TMEM
+// allocator + MMA issuer (one elected lane), warps 2..5 = epilogue (thread = accumulator row =
+// TMEM lane).  Operand tiles 128 x 64 (A) and BN x 64 (B) are staged by TMA into a STAGES-deep
+// 128B-swizzled ring guarded by full/empty mbarriers; accumulators are double buffered in TMEM
+// (2 x BN fp32 columns) so the epilogue of tile i overlaps the MMAs of tile i+1.
+//
+// Split precision (NMT_PREC_FP32CLASS): x = hi + lo (both bf16); A.B ~ Ahi.Bhi + Ahi.Blo + Alo.Bhi,
+// realised as three K passes over the same accumulator; the lo halves live at a column offset
+// of the same tensors (a_lo_off / b_lo_off).
+// K ranges per N range ("regions") let one GEMM compute [gates | hUx | cWcx] of a GRU over a
+// concatenated activation buffer without multiplying zero blocks.
+//
+// Epilogues: EPI_STORE writes fp32 (+bias[col]); EPI_LSE is the fused vocabulary epilogue of
+// step D8: per (row, N-tile) running max, sum of exp and argmax of the logits -
+// the logits never leave the chip (PAPER.md:120 computes P_i explicitly; we never do).
+#include <cuda.h>
+
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace nmt {
+
+constexpr int BM = 128, BK = 64;
+constexpr int EPI_STORE = 0, EPI_LSE = 1;
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int BYTES = 1024 + STAGES * (A_BYTES + B_BYTES) + (2 * STAGES + 4) * 8 + 16;
+};
+
+struct RegionK {
+  int k0, k1;  // in units of BK blocks
+};
+
+NMT_DEV RegionK region_of(const GemmShape& g, int n0) {
+  int r = 0;
+#pragma unroll 1
+  while (r < g.nreg - 1 && n0 >= g.reg_n_end[r]) ++r;
+  return RegionK{g.reg_k0[r] / BK, g.reg_k1[r] / BK};
+}
+
+template <int BN, int STAGES, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmShape g,
+           EpiParams ep) {
+  using S = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * S::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * S::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int M = g.M_dev ? *g.M_dev : g.M;
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = g.N / BN;
+  const int total = num_m * num_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int m = t % num_m, n = t / num_m;
+        const RegionK rk = region_of(g, n * BN);
+        for (int pass = 0; pass < g.passes; ++pass) {
+          const int aoff = g.a_col0 + (pass == 2 ? g.a_lo_off : 0);
+          const int boff = (pass == 1 ? g.b_lo_off : 0);
+          for (int kb = rk.k0; kb < rk.k1; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES);
+            tma_load_2d(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, m * BM);
+            tma_load_2d(&tmB, &full[stage], sB + stage * S::B_BYTES, boff + kb * BK, n * BN);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        const int n = t / num_m;
+        const RegionK rk = region_of(g, n * BN);
+        const int acc = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        const int nkb = g.passes * (rk.k1 - rk.k0);
+        for (int i = 0; i < nkb; ++i) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * S::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * S::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else {  // ---------------- epilogue warps 2..5
+    const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
+    const int row_in_tile = q * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      const int m = t % num_m, n = t / num_m;
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int grow = m * BM + row_in_tile;
+      const bool valid = grow < M;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if constexpr (EPI == EPI_STORE) {
+        float* orow = ep.out + (size_t)grow * ep.ldc + n * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(tbase + c * 32, v);
+          if (valid) {
+            if (ep.bias) {
+              const float* b = ep.bias + n * BN + c * 32;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += __ldg(b + j);
+            }
+            float4* o = reinterpret_cast<float4*>(orow + c * 32);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+        }
+      } else {  // EPI_LSE: online (max, sum exp, argmax) over this tile's BN logits of the row
+        constexpr float LOG2E = 1.4426950408889634f;
+        float mx = -INFINITY, sm = 0.f;
+        int am = 0;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(tbase + c * 32, v);
+          const int col0 = n * BN + c * 32;
+          float cm = -INFINITY;
+          int ci = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (col0 + j >= ep.n_valid) v[j] = -INFINITY;
+            if (v[j] > cm) {
+              cm = v[j];
+              ci = j;
+            }
+          }
+          if (cm > mx) {  // strict: earlier (lower id) wins ties
+            sm = sm * ex2_approx((mx - cm) * LOG2E);
+            mx = cm;
+            am = col0 + ci;
+          }
+          if (cm > -INFINITY) {
+            const float mb = mx * LOG2E;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sm += ex2_approx(fmaf(v[j], LOG2E, -mb));
+          }
+        }
+        if (valid) ep.part[(size_t)grow * ep.n_tiles + n] = make_float4(mx, sm, __int_as_float(am), 0.f);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 2 * BN);
+  }
+}
+
+// ------------------------------------------------------------------------------------- host side
+typedef CUresult (*PFN_tmapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                         const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                         CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                         CUtensorMapFloatOOBfill);
+
+static PFN_tmapEncodeTiled get_encode_fn() {
+  static PFN_tmapEncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_tmapEncodeTiled>(p);
+  });
+  if (!fn) throw NmtError(NMT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw NmtError(NMT_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") rows=" +
+                                     std::to_string(rows) + " cols=" + std::to_string(cols));
+  return m;
+}
+
+template <int BN, int STAGES, int EPI>
+static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, const EpiParams& ep, int M_max,
+                   cudaStream_t st) {
+  using S = GemmSmem<BN, STAGES>;
+  static bool attr_set = false;  // per template instance; set once per process (single device use)
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_gemm<BN, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
+    attr_set = true;
+  }
+  const int tiles = ((M_max + BM - 1) / BM) * (g.N / BN);
+  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  if (grid <= 0) return;
+  k_gemm<BN, STAGES, EPI><<<grid, 192, S::BYTES, st>>>(a, b, g, ep);
+  CK(cudaGetLastError());
+}
+
+void gemm_validate(const GemmShape& g, int BN) {
+  if (g.N % BN) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: N not a multiple of the N tile");
+  for (int r = 0; r < g.nreg; ++r) {
+    if (g.reg_k0[r] % BK || g.reg_k1[r] % BK || g.reg_k1[r] <= g.reg_k0[r])
+      throw NmtError(NMT_ERR_INVALID_ARG, "gemm: bad K region");
+    if (r < g.nreg - 1 && g.reg_n_end[r] % BN) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: region not tile aligned");
+  }
+}
+
+// fp32 output GEMM; BN = 128 (more CTAs for the mid-size decoder GEMMs).
+void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc,
+                const float* bias, int M_max, cudaStream_t st) {
+  gemm_validate(g, 128);
+  EpiParams ep{};
+  ep.out = out;
+  ep.ldc = ldc;
+  ep.bias = bias;
+  launch<128, 6, EPI_STORE>(a, b, g, ep, M_max, st);
+}
+
+// fused vocabulary GEMM + online log-sum-exp partials; BN = 256.
+void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
+              cudaStream_t st) {
+  gemm_validate(g, 256);
+  EpiParams ep{};
+  ep.part = part;
+  ep.n_valid = n_valid;
+  ep.n_tiles = g.N / 256;
+  launch<256, 4, EPI_LSE>(a, b, g, ep, M_max, st);
+}
+
+}  // namespace nmt

@@ -1,0 +1,77 @@
+// internal.h - shared declarations of the libnmt host runtime and kernel launchers.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/nmt.h"
+
+namespace nmt {
+
+struct NmtError {
+  nmt_status code;
+  std::string msg;
+  NmtError(nmt_status c, std::string m) : code(c), msg(std::move(m)) {}
+};
+
+#define CK(expr)                                                                                           \
+  do {                                                                                                     \
+    cudaError_t _e = (expr);                                                                               \
+    if (_e != cudaSuccess)                                                                                 \
+      throw ::nmt::NmtError(_e == cudaErrorMemoryAllocation ? NMT_ERR_OOM : NMT_ERR_CUDA,                   \
+                            std::string(#expr) + ": " + cudaGetErrorString(_e));                          \
+  } while (0)
+
+// --------------------------------------------------------------------------- GEMM engine
+struct GemmShape {
+  int M;             // rows (if M_dev == nullptr)
+  const int* M_dev;  // device-resident row count (dynamic batch size), or nullptr
+  int N;             // output columns, multiple of the N tile
+  int a_col0;        // first column of A used
+  int a_lo_off;      // split: column offset of A's lo half relative to the hi column
+  int b_lo_off;      // split: column offset of B's lo half
+  int passes;        // 1 (bf16) or 3 (bf16x3: hi.hi + hi.lo + lo.hi)
+  int nreg;          // number of N regions (>= 1)
+  int reg_n_end[4];  // region r covers output columns [reg_n_end[r-1], reg_n_end[r])
+  int reg_k0[4];     // K range [k0, k1) of region r (multiples of 64, relative to a_col0 / 0)
+  int reg_k1[4];
+};
+
+struct EpiParams {
+  float* out;
+  int ldc;
+  const float* bias;
+  float4* part;
+  int n_valid;
+  int n_tiles;
+};
+
+CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc,
+                const float* bias, int M_max, cudaStream_t st);
+void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
+              cudaStream_t st);
+
+inline GemmShape gemm_shape(int M, const int* M_dev, int N, int K, int a_col0, bool split, int a_lo_off,
+                            int b_lo_off) {
+  GemmShape g{};
+  g.M = M;
+  g.M_dev = M_dev;
+  g.N = N;
+  g.a_col0 = a_col0;
+  g.a_lo_off = a_lo_off;
+  g.b_lo_off = b_lo_off;
+  g.passes = split ? 3 : 1;
+  g.nreg = 1;
+  g.reg_n_end[0] = N;
+  g.reg_k0[0] = 0;
+  g.reg_k1[0] = K;
+  return g;
+}
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+}  // namespace nmt

@@ -1,0 +1,744 @@
+// kernels.cu - non-GEMM kernels of the decoder step, the device-side state cache (planner),
+// the bidirectional-GRU encoder and load-time weight packing.
+//
+// Model equations (DL4MT/Nematus cGRU; PAPER.md:13, :30 name the model, SURVEY §8(c) writes them
+// out; DESIGN.md §2 lists the readings A1-A24):
+//   GRU(x,h):  [r|u] = sigm(xW + b + hU);  h~ = tanh(r*(hUx) + xWx + bx);  h' = u*h + (1-u)*h~
+//   step:      s1 = GRU1(e, s);  a_j = tanh(pctx_j + s1 W_comb_att).U_att + c_tt;  alpha = softmax_j(a)
+//              c = sum_j alpha_j ctx_j;  [r2|u2] = sigm(s1 U_nl + b_nl + c Wc)
+//              s2 = u2*s1 + (1-u2)*tanh(r2*(s1 Ux_nl + bx_nl) + c Wcx)
+//              t  = tanh(s2 W_l + e W_p + c W_ctx + b)   |  maxout pairs (2k, 2k+1)
+//              log p(w) = t.W_o[:,w] + b_o[w] - logsumexp_v(t W_o + b_o)
+// Device layouts: hidden dims padded to Hp = roundup(H,128), context dims to
+// Cp = 2 Hp with cmap(i) = i < H ? i : Hp + i - H, embedding/readout width to Ep = roundup(E+2,64).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nmt {
+
+NMT_DEV int cmap_(int i, int H, int Hp) { return i < H ? i : Hp + (i - H); }
+
+NMT_DEV void store_split(__nv_bfloat16* hi_ptr, int lo_off, float x) {
+  __nv_bfloat16 h, l;
+  split_bf16(x, h, l);
+  hi_ptr[0] = h;
+  if (lo_off > 0) hi_ptr[lo_off] = l;
+}
+
+// ===================================================================================== packing
+// dst[rowmap(n)][col0 + kmap(k)] = split(src[k * ld_src + n])  (transpose-pack a [K x N] matrix
+// into an N x K K-major bf16 operand; lo half at +lo_off columns if lo_off > 0)
+__global__ void k_pack_T(const float* __restrict__ src, int ld_src, int K, int N, __nv_bfloat16* dst, int ld_dst,
+                         int row0, int col0, int rmap, int kmap, int H, int Hp, int lo_off) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)K * N) return;
+  const int k = (int)(idx / N), n = (int)(idx % N);
+  const int r = row0 + (rmap ? cmap_(n, H, Hp) : n);
+  const int c = col0 + (kmap ? cmap_(k, H, Hp) : k);
+  store_split(dst + (int64_t)r * ld_dst + c, lo_off, src[(int64_t)k * ld_src + n]);
+}
+void pack_T(const float* src, int ld_src, int K, int N, __nv_bfloat16* dst, int ld_dst, int row0, int col0, int rmap,
+            int kmap, int H, int Hp, int lo_off, cudaStream_t st) {
+  const int64_t n = (int64_t)K * N;
+  if (!n) return;
+  k_pack_T<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, ld_src, K, N, dst, ld_dst, row0, col0, rmap, kmap, H, Hp,
+                                                        lo_off);
+  CK(cudaGetLastError());
+}
+
+// dst[r][col0 + k] = split(src[r * ld_src + k]) for r < rows, k < K (row-major copy)
+__global__ void k_pack_rows(const float* __restrict__ src, int ld_src, int rows, int K, __nv_bfloat16* dst,
+                            int ld_dst, int col0, int lo_off) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)rows * K) return;
+  const int r = (int)(idx / K), k = (int)(idx % K);
+  store_split(dst + (int64_t)r * ld_dst + col0 + k, lo_off, src[(int64_t)r * ld_src + k]);
+}
+void pack_rows(const float* src, int ld_src, int rows, int K, __nv_bfloat16* dst, int ld_dst, int col0, int lo_off,
+               cudaStream_t st) {
+  const int64_t n = (int64_t)rows * K;
+  if (!n) return;
+  k_pack_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, ld_src, rows, K, dst, ld_dst, col0, lo_off);
+  CK(cudaGetLastError());
+}
+
+// fp32 [K x N] -> fp32 [N x ld_dst] transposed (W_o columns as contiguous per-word rows)
+__global__ void k_transpose_f32(const float* __restrict__ src, int K, int N, float* dst, int ld_dst) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)K * N) return;
+  const int k = (int)(idx / N), n = (int)(idx % N);
+  dst[(int64_t)n * ld_dst + k] = src[idx];
+}
+void transpose_f32(const float* src, int K, int N, float* dst, int ld_dst, cudaStream_t st) {
+  const int64_t n = (int64_t)K * N;
+  k_transpose_f32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, K, N, dst, ld_dst);
+  CK(cudaGetLastError());
+}
+
+// ===================================================================================== planner
+// Device-side state cache (SURVEY §8(a) D0; PAPER.md:109 "collapsed edges", :121 "Cache state
+// pointers and probabilities at target nodes").  Keys (parent, word) -> child id in an open-
+// addressing table; child ids are assigned in first-appearance order of the request stream.
+constexpr int64_t KEY_EMPTY = -1;
+constexpr int VAL_INIT = INT32_MIN;
+
+NMT_DEV uint64_t mix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return x;
+}
+
+NMT_DEV int hash_insert(unsigned long long* keys, uint64_t mask, int64_t key) {
+  uint64_t h = mix64((uint64_t)key) & mask;
+  while (true) {
+    const unsigned long long prev = atomicCAS(&keys[h], (unsigned long long)KEY_EMPTY, (unsigned long long)key);
+    if (prev == (unsigned long long)KEY_EMPTY || prev == (unsigned long long)key) return (int)h;
+    h = (h + 1) & mask;
+  }
+}
+
+__global__ void k_plan_intern(CtxDev c, PlanIO io) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_nodes = c.counters[CNT_NODES];
+  if (i < io.n_cand) {
+    int lo = 0, hi = io.n_par;  // find k with offsets[k] <= i < offsets[k+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (io.offsets[mid] <= i) lo = mid; else hi = mid;
+    }
+    const int k = lo;
+    io.cand_k[i] = k;
+    const int p = io.parents[k], w = io.words[i];
+    int slot = -1;
+    if (p < 0 || p >= n_nodes) {
+      atomicOr(&c.counters[CNT_ERR], ERR_BAD_STATE);
+    } else if (w < 0 || w >= c.V) {
+      atomicOr(&c.counters[CNT_ERR], ERR_TOKEN);
+    } else {
+      slot = hash_insert(c.hkeys, c.hmask, ((int64_t)p << 32) | (uint32_t)w);
+      atomicMax(&c.hvals[slot], -2 - i);
+    }
+    io.cand_hslot[i] = slot;
+  }
+  if (i < io.n_par) {
+    const int p = io.parents[i];
+    const int o0 = io.offsets[i], o1 = io.offsets[i + 1];
+    if (o1 < o0) atomicOr(&c.counters[CNT_ERR], ERR_OFFSETS);
+    if (p < 0 || p >= n_nodes) atomicOr(&c.counters[CNT_ERR], ERR_BAD_STATE);
+    else if (o1 > o0) atomicMin(&c.node_claim[p], i);
+  }
+}
+
+// block-wide exclusive scan of one int per thread (1024 threads); returns the total
+NMT_DEV int block_scan_excl(int v, int* smem32, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem32[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int s = lane < (int)(blockDim.x >> 5) ? smem32[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    smem32[lane] = s;  // inclusive warp totals
+  }
+  __syncthreads();
+  const int warp_prefix = warp ? smem32[warp - 1] : 0;
+  total = smem32[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return warp_prefix + x - v;
+}
+
+// single-CTA pass: new node ids (first appearances), row list of parents to step.
+__global__ void __launch_bounds__(1024) k_plan_assign(CtxDev c, PlanIO io, int* R_out) {
+  __shared__ int sm[32];
+  const int n_nodes0 = c.counters[CNT_NODES];
+  const int n_slots0 = c.counters[CNT_SLOTS];
+  int base = 0;
+  for (int i0 = 0; i0 < io.n_cand; i0 += blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    int hs = -1, flag = 0;
+    if (i < io.n_cand) {
+      hs = io.cand_hslot[i];
+      flag = hs >= 0 && c.hvals[hs] == -2 - i;
+    }
+    int tot;
+    const int ex = block_scan_excl(flag, sm, tot);
+    if (flag) {
+      const int id = n_nodes0 + base + ex;
+      const int k = io.cand_k[i];
+      c.node_word[id] = io.words[i];
+      c.node_parent[id] = io.parents[k];
+      c.node_slot[id] = -1;
+      c.node_claim[id] = INT32_MAX;
+      c.hvals[hs] = id;
+    }
+    base += tot;
+  }
+  const int n_new = base;
+  base = 0;
+  for (int k0 = 0; k0 < io.n_par; k0 += blockDim.x) {
+    const int k = k0 + threadIdx.x;
+    int need = 0, p = -1;
+    if (k < io.n_par) {
+      p = io.parents[k];
+      need = p >= 0 && p < n_nodes0 && io.offsets[k + 1] > io.offsets[k] && c.node_slot[p] < 0 &&
+             c.node_claim[p] == k;
+    }
+    int tot;
+    const int ex = block_scan_excl(need, sm, tot);
+    if (need) {
+      const int r = base + ex;
+      const int par = c.node_parent[p];
+      io.row_src[r] = par >= 0 ? c.node_slot[par] : c.node_src[p];
+      io.row_y[r] = c.node_word[p];
+      io.row_dst[r] = n_slots0 + r;
+      io.row_node[r] = p;
+    }
+    __syncthreads();
+    if (need) c.node_slot[p] = n_slots0 + base + ex;
+    base += tot;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < io.n_par; k += blockDim.x) {  // release claims
+    const int p = io.parents[k];
+    if (p >= 0 && p < n_nodes0) c.node_claim[p] = INT32_MAX;
+  }
+  if (threadIdx.x == 0) {
+    c.counters[CNT_NODES] = n_nodes0 + n_new;
+    c.counters[CNT_SLOTS] = n_slots0 + base;
+    *R_out = base;
+  }
+}
+
+void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st) {
+  const int n = io.n_cand > io.n_par ? io.n_cand : io.n_par;
+  if (n > 0) {
+    k_plan_intern<<<(n + 255) / 256, 256, 0, st>>>(c, io);
+    CK(cudaGetLastError());
+  }
+  k_plan_assign<<<1, 1024, 0, st>>>(c, io, R_dev);
+  CK(cudaGetLastError());
+}
+
+// rehash all entries of an old table into a new (larger) one
+__global__ void k_rehash(const unsigned long long* okeys, const int* ovals, int64_t ocap, unsigned long long* nkeys,
+                         int* nvals, uint64_t nmask) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ocap) return;
+  const int64_t key = (int64_t)okeys[i];
+  if (key == KEY_EMPTY) return;
+  const int s = hash_insert(nkeys, nmask, key);
+  nvals[s] = ovals[i];
+}
+void rehash(const unsigned long long* okeys, const int* ovals, int64_t ocap, unsigned long long* nkeys, int* nvals,
+            uint64_t nmask, cudaStream_t st) {
+  k_rehash<<<(unsigned)((ocap + 255) / 256), 256, 0, st>>>(okeys, ovals, ocap, nkeys, nvals, nmask);
+  CK(cudaGetLastError());
+}
+
+__global__ void k_fill_i32(int* p, int64_t n, int v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+void fill_i32(int* p, int64_t n, int v, cudaStream_t st) {
+  if (n <= 0) return;
+  k_fill_i32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, n, v);
+  CK(cudaGetLastError());
+}
+
+// inject parentless nodes with their own input slots (synthetic parents for bench/tests)
+__global__ void k_inject(CtxDev c, int n, const float* s, const int* y, int* out_ids) {
+  const int n_nodes0 = c.counters[CNT_NODES], n_slots0 = c.counters[CNT_SLOTS];
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int slot = n_slots0 + i;
+    for (int j = threadIdx.x; j < c.H; j += blockDim.x) c.S[(int64_t)slot * c.Hp + j] = s[(int64_t)i * c.H + j];
+    if (threadIdx.x == 0) {
+      const int id = n_nodes0 + i;
+      c.node_word[id] = y[i];
+      c.node_parent[id] = -1;
+      c.node_src[id] = slot;
+      c.node_slot[id] = -1;
+      c.node_claim[id] = INT32_MAX;
+      out_ids[i] = id;
+    }
+  }
+}
+__global__ void k_inject_commit(CtxDev c, int n) {
+  c.counters[CNT_NODES] += n;
+  c.counters[CNT_SLOTS] += n;
+}
+void inject(const CtxDev& c, int n, const float* s, const int* y, int* out_ids, cudaStream_t st) {
+  k_inject<<<n < 1024 ? n : 1024, 256, 0, st>>>(c, n, s, y, out_ids);
+  CK(cudaGetLastError());
+  k_inject_commit<<<1, 1, 0, st>>>(c, n);
+  CK(cudaGetLastError());
+}
+
+// ===================================================================================== step D1-D7
+// D1: gather the parents' input states into the bf16 A operand of GRU1's recurrent GEMM
+__global__ void k_gather_state(StepDev d, const float* __restrict__ S) {
+  const int R = *d.R;
+  for (int r = blockIdx.x; r < R; r += gridDim.x) {
+    const float* src = S + (int64_t)d.row_src[r] * d.Hp;
+    __nv_bfloat16* dst = d.A_s + (int64_t)r * d.lda_s;
+    for (int k = threadIdx.x; k < d.H; k += blockDim.x) store_split(dst + k, d.lo_s, src[k]);
+  }
+}
+
+// D2: GRU1 gates.  G1 = s.[U|Ux] (GEMM), Ex[y] = e.[W|Wx] + [b|bx] (precomputed per word).
+__global__ void k_gru1(StepDev d, const float* __restrict__ S) {
+  const int R = *d.R;
+  const int H = d.H, Hp = d.Hp;
+  for (int r = blockIdx.x; r < R; r += gridDim.x) {
+    const int y = d.row_y[r];
+    const float* g = d.G1 + (int64_t)r * 3 * Hp;
+    const float* ex = d.Ex + (int64_t)(y < 0 ? d.V : y) * 3 * Hp;
+    const float* s = S + (int64_t)d.row_src[r] * Hp;
+    for (int j = threadIdx.x; j < H; j += blockDim.x) {
+      const float rg = 1.f / (1.f + expf(-(ex[j] + g[j])));
+      const float ug = 1.f / (1.f + expf(-(ex[Hp + j] + g[Hp + j])));
+      const float ht = tanhf(rg * g[2 * Hp + j] + ex[2 * Hp + j]);
+      const float s1 = ug * s[j] + (1.f - ug) * ht;
+      d.S1[(int64_t)r * Hp + j] = s1;
+      store_split(d.X + (int64_t)r * d.ldx + j, d.lo_x, s1);
+    }
+  }
+}
+
+// D4+D5: MLP attention energies (MUFU tanh), softmax over source positions, context vector.
+// One CTA = RPB rows of the same sentence; thread owns 8 consecutive context columns.
+template <int RPB>
+__global__ void k_attention(StepDev d, AttnCtx a) {
+  const int R = *d.R;
+  const int r0 = blockIdx.x * RPB;
+  if (r0 >= R) return;
+  const int Cp = d.Cp, Tx = a.Tx;
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = threadIdx.x * 8;
+  extern __shared__ float sm[];
+  float* red = sm;                     // [nw][RPB][Tx]
+  float* alpha = sm + nw * RPB * Tx;   // [RPB][Tx]
+  float q[RPB][8], u[8];
+#pragma unroll
+  for (int rr = 0; rr < RPB; ++rr) {
+    const bool ok = r0 + rr < R;
+    const float4* qp = reinterpret_cast<const float4*>(d.Q + (int64_t)(r0 + rr) * Cp + c0);
+    float4 x0 = ok ? qp[0] : make_float4(0, 0, 0, 0), x1 = ok ? qp[1] : make_float4(0, 0, 0, 0);
+    q[rr][0] = x0.x; q[rr][1] = x0.y; q[rr][2] = x0.z; q[rr][3] = x0.w;
+    q[rr][4] = x1.x; q[rr][5] = x1.y; q[rr][6] = x1.z; q[rr][7] = x1.w;
+  }
+  {
+    const float4* up = reinterpret_cast<const float4*>(a.U_att + c0);
+    float4 x0 = up[0], x1 = up[1];
+    u[0] = x0.x; u[1] = x0.y; u[2] = x0.z; u[3] = x0.w; u[4] = x1.x; u[5] = x1.y; u[6] = x1.z; u[7] = x1.w;
+  }
+  for (int j = 0; j < Tx; ++j) {
+    const float4* pp = reinterpret_cast<const float4*>(a.pctx + (int64_t)j * Cp + c0);
+    const float4 p0 = pp[0], p1 = pp[1];
+    const float p[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    float acc[RPB];
+#pragma unroll
+    for (int rr = 0; rr < RPB; ++rr) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s = fmaf(tanh_approx(p[k] + q[rr][k]), u[k], s);
+      acc[rr] = s;
+    }
+#pragma unroll
+    for (int rr = 0; rr < RPB; ++rr) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int rr = 0; rr < RPB; ++rr) red[(warp * RPB + rr) * Tx + j] = acc[rr];
+    }
+  }
+  __syncthreads();
+  for (int rr = warp; rr < RPB; rr += nw) {  // softmax over j for row rr
+    float mx = -INFINITY;
+    for (int j = lane; j < Tx; j += 32) {
+      float e = a.c_tt;
+      for (int w = 0; w < nw; ++w) e += red[(w * RPB + rr) * Tx + j];
+      alpha[rr * Tx + j] = e;
+      mx = fmaxf(mx, e);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+    for (int j = lane; j < Tx; j += 32) {
+      const float e = expf(alpha[rr * Tx + j] - mx);
+      alpha[rr * Tx + j] = e;
+      sum += e;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float inv = 1.f / sum;
+    for (int j = lane; j < Tx; j += 32) {
+      alpha[rr * Tx + j] *= inv;
+      if (r0 + rr < R && d.alpha_out) d.alpha_out[(int64_t)(r0 + rr) * d.alpha_ld + j] = alpha[rr * Tx + j];
+    }
+  }
+  __syncthreads();
+  float cacc[RPB][8];
+#pragma unroll
+  for (int rr = 0; rr < RPB; ++rr)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cacc[rr][k] = 0.f;
+  for (int j = 0; j < Tx; ++j) {
+    const float4* cp = reinterpret_cast<const float4*>(a.ctx + (int64_t)j * Cp + c0);
+    const float4 x0 = cp[0], x1 = cp[1];
+    const float cv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+    for (int rr = 0; rr < RPB; ++rr) {
+      const float al = alpha[rr * Tx + j];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cacc[rr][k] = fmaf(al, cv[k], cacc[rr][k]);
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < RPB; ++rr) {
+    const int r = r0 + rr;
+    if (r >= R) break;
+    float4* o = reinterpret_cast<float4*>(d.Cf + (int64_t)r * Cp + c0);
+    o[0] = make_float4(cacc[rr][0], cacc[rr][1], cacc[rr][2], cacc[rr][3]);
+    o[1] = make_float4(cacc[rr][4], cacc[rr][5], cacc[rr][6], cacc[rr][7]);
+    __nv_bfloat16* xp = d.X + (int64_t)r * d.ldx + d.Hp + c0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) store_split(xp + k, d.lo_x, cacc[rr][k]);
+  }
+}
+
+// D6: GRU2 gates.  G2 = [s1 U_nl + c Wc | s1 Ux_nl | c Wcx] (one region GEMM).
+__global__ void k_gru2(StepDev d, float* __restrict__ S) {
+  const int R = *d.R;
+  const int H = d.H, Hp = d.Hp;
+  for (int r = blockIdx.x; r < R; r += gridDim.x) {
+    const float* g = d.G2 + (int64_t)r * 4 * Hp;
+    const float* s1 = d.S1 + (int64_t)r * Hp;
+    float* s2o = S + (int64_t)d.row_dst[r] * Hp;
+    for (int j = threadIdx.x; j < H; j += blockDim.x) {
+      const float rg = 1.f / (1.f + expf(-(g[j] + d.b_nl[j])));
+      const float ug = 1.f / (1.f + expf(-(g[Hp + j] + d.b_nl[Hp + j])));
+      const float ht = tanhf(rg * (g[2 * Hp + j] + d.bx_nl[j]) + g[3 * Hp + j]);
+      const float s2 = ug * s1[j] + (1.f - ug) * ht;
+      s2o[j] = s2;
+      store_split(d.X + (int64_t)r * d.ldx + d.Hp + d.Cp + j, d.lo_x, s2);
+    }
+  }
+}
+
+// D7: readout activation.  RO = c W_ctx + s2 W_l (GEMM), Ep[y] = e W_p + b_p + b_l + b_ctx.
+// Writes t (fp32) to the arena and the bf16 A operand of the vocabulary GEMM with the two
+// bias columns (b_o folded into the GEMM as hi + lo).
+__global__ void k_readout(StepDev d, float* __restrict__ T) {
+  const int R = *d.R;
+  const int E = d.E, Ep = d.Ep;
+  for (int r = blockIdx.x; r < R; r += gridDim.x) {
+    const int y = d.row_y[r];
+    const float* pre = d.RO + (int64_t)r * d.ROp;
+    const float* epr = d.Eproj + (int64_t)(y < 0 ? d.V : y) * d.ROp;
+    float* to = T + (int64_t)d.row_dst[r] * Ep;
+    __nv_bfloat16* at = d.A_t + (int64_t)r * d.lda_t;
+    for (int k = threadIdx.x; k < Ep; k += blockDim.x) {
+      float t;
+      if (k < E) {
+        if (d.maxout) t = fmaxf(pre[2 * k] + epr[2 * k], pre[2 * k + 1] + epr[2 * k + 1]);
+        else t = tanhf(pre[k] + epr[k]);
+        to[k] = t;
+        store_split(at + k, d.lo_t, t);
+      } else {
+        // bias columns: bf16 path A[E] = A[E+1] = 1 (b_hi, b_lo in B); split path hi[E] = 1, lo[E] = 0
+        const float one = (k == E || (k == E + 1 && d.lo_t == 0)) ? 1.f : 0.f;
+        at[k] = __float2bfloat16_rn(one);
+        if (d.lo_t > 0) at[k + d.lo_t] = __float2bfloat16_rn(0.f);
+      }
+    }
+  }
+}
+
+// D9a: combine the per-tile (max, sum, argmax) partials of each row in fixed tile order.
+__global__ void k_finalize(StepDev d, float* __restrict__ logZ, int* __restrict__ amax) {
+  const int R = *d.R;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= R) return;
+  const float4* p = d.part + (int64_t)warp * d.n_tiles;
+  float m = -INFINITY, s = 0.f;
+  int am = 0x7fffffff;
+  for (int i = lane; i < d.n_tiles; i += 32) {
+    const float4 v = p[i];
+    if (v.x > m) {
+      s = s * expf(m - v.x) + v.y;
+      m = v.x;
+      am = __float_as_int(v.z);
+    } else if (v.x > -INFINITY) {
+      s += v.y * expf(v.x - m);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const int a2 = __shfl_xor_sync(0xffffffffu, am, o);
+    const float mm = fmaxf(m, m2);
+    const float ns = (m > -INFINITY ? s * expf(m - mm) : 0.f) + (m2 > -INFINITY ? s2 * expf(m2 - mm) : 0.f);
+    int na;
+    if (m2 > m) na = a2;
+    else if (m > m2) na = am;
+    else na = min(am, a2);
+    m = mm;
+    s = ns;
+    am = na;
+  }
+  if (lane == 0) {
+    const int slot = d.row_dst[warp];
+    logZ[slot] = m + logf(s);
+    amax[slot] = am;
+  }
+}
+
+// D9b: per candidate log p = t . W_o[:,w] + b_o[w] - logZ (fp32 gather-dot; also serves cache hits)
+__global__ void k_gather_dot(CtxDev c, PlanIO io, const float* __restrict__ Wo32, const float* __restrict__ bo,
+                             int Ep, float* out_logp, int* out_child32, long long* out_child64) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= io.n_cand) return;
+  const int hs = io.cand_hslot[warp];
+  if (hs < 0) {
+    if (lane == 0) {
+      out_logp[warp] = __int_as_float(0x7fc00000);
+      if (out_child32) out_child32[warp] = -1;
+      if (out_child64) out_child64[warp] = -1;
+    }
+    return;
+  }
+  const int p = io.parents[io.cand_k[warp]];
+  const int slot = c.node_slot[p];
+  const int w = io.words[warp];
+  const float4* t = reinterpret_cast<const float4*>(c.T + (int64_t)slot * Ep);
+  const float4* wo = reinterpret_cast<const float4*>(Wo32 + (int64_t)w * Ep);
+  float s = 0.f;
+  for (int k = lane; k < Ep / 4; k += 32) {
+    const float4 a = t[k], b = wo[k];
+    s = fmaf(a.x, b.x, s);
+    s = fmaf(a.y, b.y, s);
+    s = fmaf(a.z, b.z, s);
+    s = fmaf(a.w, b.w, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    out_logp[warp] = s + bo[w] - c.logZ[slot];
+    const int ch = c.hvals[hs];
+    if (out_child32) out_child32[warp] = ch;
+    if (out_child64) out_child64[warp] = ch;
+  }
+}
+
+__global__ void k_argmax_out(CtxDev c, PlanIO io, int* out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= io.n_par) return;
+  const int p = io.parents[k];
+  int v = -1;
+  if (p >= 0 && p < c.counters[CNT_NODES]) {
+    const int slot = c.node_slot[p];
+    if (slot >= 0) v = c.amax[slot];
+  }
+  out[k] = v;
+}
+
+// full log-prob row of one stepped slot (test export)
+__global__ void k_full_row(const float* __restrict__ T, const float* __restrict__ Wo32, const float* __restrict__ bo,
+                           const float* __restrict__ logZ, int slot, int Ep, int V, float* out) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= V) return;
+  const float* t = T + (int64_t)slot * Ep;
+  const float* wo = Wo32 + (int64_t)w * Ep;
+  float s = 0.f;
+  for (int k = lane; k < Ep; k += 32) s = fmaf(t[k], wo[k], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[w] = s + bo[w] - logZ[slot];
+}
+
+void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, float* T, float* logZ, int* amax,
+                      int R_max, cudaStream_t st) {
+  if (R_max <= 0) return;
+  const int g = R_max < 4096 ? R_max : 4096;
+  switch (which) {
+    case EW_GATHER: k_gather_state<<<g, 256, 0, st>>>(d, S); break;
+    case EW_GRU1: k_gru1<<<g, 256, 0, st>>>(d, S); break;
+    case EW_ATTN: {
+      constexpr int RPB = 4;
+      const int nthr = d.Cp / 8;
+      const size_t smem = (size_t)((nthr / 32 > 0 ? nthr / 32 : 1) * RPB + RPB) * a.Tx * sizeof(float);
+      k_attention<RPB><<<(R_max + RPB - 1) / RPB, nthr, smem, st>>>(d, a);
+      break;
+    }
+    case EW_GRU2: k_gru2<<<g, 256, 0, st>>>(d, S); break;
+    case EW_READOUT: k_readout<<<g, 128, 0, st>>>(d, T); break;
+    case EW_FINALIZE: k_finalize<<<(R_max * 32 + 255) / 256, 256, 0, st>>>(d, logZ, amax); break;
+  }
+  CK(cudaGetLastError());
+}
+
+void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const float* bo, int Ep, float* out_logp,
+                int* out_child32, long long* out_child64, int* out_argmax, cudaStream_t st) {
+  if (io.n_cand > 0) {
+    k_gather_dot<<<(io.n_cand * 32 + 255) / 256, 256, 0, st>>>(c, io, Wo32, bo, Ep, out_logp, out_child32,
+                                                                 out_child64);
+    CK(cudaGetLastError());
+  }
+  if (out_argmax && io.n_par > 0) {
+    k_argmax_out<<<(io.n_par + 255) / 256, 256, 0, st>>>(c, io, out_argmax);
+    CK(cudaGetLastError());
+  }
+}
+
+void full_row(const float* T, const float* Wo32, const float* bo, const float* logZ, int slot, int Ep, int V,
+              float* out, cudaStream_t st) {
+  k_full_row<<<(V * 32 + 255) / 256, 256, 0, st>>>(T, Wo32, bo, logZ, slot, Ep, V, out);
+  CK(cudaGetLastError());
+}
+
+// ===================================================================================== encoder
+// E1: gather source embeddings into the split bf16 A operand of the input projections.
+__global__ void k_enc_gather(const float* __restrict__ Wemb, const int* __restrict__ src, int Tx, int E, int Ep,
+                             __nv_bfloat16* X) {
+  const int j = blockIdx.x;
+  if (j >= Tx) return;
+  const float* e = Wemb + (int64_t)src[j] * E;
+  for (int k = threadIdx.x; k < E; k += blockDim.x) store_split(X + (int64_t)j * 2 * Ep + k, Ep, e[k]);
+}
+void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, __nv_bfloat16* X, cudaStream_t st) {
+  k_enc_gather<<<Tx, 128, 0, st>>>(Wemb, src, Tx, E, Ep, X);
+  CK(cudaGetLastError());
+}
+
+// E3/E4: persistent bidirectional GRU recurrence.  CTAs [0, NB) run the forward direction,
+// [NB, 2NB) the backward one; each CTA keeps its UPC units' slice of [U | Ux] (fp32) resident in
+// shared memory and the directions synchronise per time step through a global counter barrier.
+// Pin = x.[W|Wx] + [b|bx] for both directions (GEMM E2), layout [Tx][dir*3Hp + gate*Hp + j].
+__global__ void __launch_bounds__(256, 1) k_enc_recur(EncDev e, int Tx) {
+  extern __shared__ float sm[];
+  const int NB = e.NB, UPC = e.UPC, H = e.H, Hp = e.Hp;
+  const int dir = blockIdx.x / NB, cb = blockIdx.x % NB;
+  const int u0 = cb * UPC;
+  const int ncol = 3 * UPC;
+  float* W = sm;                 // [ncol][H]
+  float* hprev = W + ncol * H;   // [H]
+  float* dots = hprev + H;       // [ncol]
+  {
+    const float4* src = reinterpret_cast<const float4*>(e.Uarr + ((int64_t)(dir * NB + cb) * ncol) * H);
+    float4* dst = reinterpret_cast<float4*>(W);
+    for (int i = threadIdx.x; i < ncol * H / 4; i += blockDim.x) dst[i] = src[i];
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int t = 0; t < Tx; ++t) {
+    const int j = dir == 0 ? t : Tx - 1 - t;
+    if (t == 0) {
+      for (int k = threadIdx.x; k < H; k += blockDim.x) hprev[k] = 0.f;
+    } else {
+      const float* hb = e.hbuf + (dir * 2 + (t & 1)) * Hp;
+      for (int k = threadIdx.x; k < H; k += blockDim.x) hprev[k] = __ldcg(hb + k);
+    }
+    __syncthreads();
+    for (int c = warp; c < ncol; c += nw) {
+      const float* wr = W + (int64_t)c * H;
+      float s = 0.f;
+      for (int k = lane; k < H; k += 32) s = fmaf(wr[k], hprev[k], s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) dots[c] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < UPC) {
+      const int u = threadIdx.x, jj = u0 + u;
+      if (jj < H) {
+        const float* pin = e.Pin + (int64_t)j * 6 * Hp + dir * 3 * Hp;
+        const float rg = 1.f / (1.f + expf(-(pin[jj] + dots[u])));
+        const float ug = 1.f / (1.f + expf(-(pin[Hp + jj] + dots[UPC + u])));
+        const float ht = tanhf(rg * dots[2 * UPC + u] + pin[2 * Hp + jj]);
+        const float h = ug * hprev[jj] + (1.f - ug) * ht;
+        e.ctx[(int64_t)j * 2 * Hp + dir * Hp + jj] = h;
+        e.hbuf[(dir * 2 + ((t + 1) & 1)) * Hp + jj] = h;
+      }
+    }
+    // direction-wide barrier: all NB CTAs published h_t before anyone reads it
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&e.bar[dir], 1);
+      const int target = NB * (t + 1);
+      volatile int* vb = e.bar + dir;
+      while (*vb < target) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+}
+size_t enc_recur_smem(int UPC, int H) { return (size_t)(3 * UPC * H + H + 3 * UPC) * sizeof(float); }
+void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
+  const size_t smem = enc_recur_smem(e.UPC, e.H);
+  static size_t attr = 0;  // the attribute must cover the largest H seen in this process
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_enc_recur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  CK(cudaMemsetAsync(e.bar, 0, 2 * sizeof(int), st));
+  EncDev ee = e;
+  void* args[] = {&ee, &Tx};
+  CK(cudaLaunchCooperativeKernel((void*)k_enc_recur, dim3(2 * e.NB), dim3(256), args, smem, st));
+}
+
+// E5: s0 = tanh(mean_j ctx_j . W_init + b_init) -> arena slot 0; also the split copy of ctx for E7.
+__global__ void k_enc_init(EncDev e, int Tx, float* S0) {
+  extern __shared__ float mean[];  // [2H] real context indices
+  const int H = e.H, Hp = e.Hp, C = 2 * H;
+  for (int i = threadIdx.x; i < C; i += blockDim.x) {
+    const int ci = i < H ? i : Hp + i - H;
+    float s = 0.f;
+    for (int j = 0; j < Tx; ++j) s += e.ctx[(int64_t)j * 2 * Hp + ci];
+    mean[i] = s / (float)Tx;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __shared__ float red[8][32];
+  const int o = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (o < H)
+    for (int k = warp; k < C; k += nw) s = fmaf(mean[k], e.W_init[(int64_t)k * H + o], s);
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && o < H) {
+    float t = 0.f;
+    for (int w = 0; w < nw; ++w) t += red[w][lane];
+    S0[o] = tanhf(t + e.b_init[o]);
+  }
+  // split copy of ctx (rows < Tx) for the pctx GEMM
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)Tx * 2 * Hp;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i / (2 * Hp), c = i % (2 * Hp);
+    store_split(e.ctxbf + j * 4 * Hp + c, 2 * Hp, e.ctx[i]);
+  }
+}
+void enc_init(const EncDev& e, int Tx, float* S0, cudaStream_t st) {
+  const int grid = (e.H + 31) / 32;
+  k_enc_init<<<grid, 256, 2 * e.H * sizeof(float), st>>>(e, Tx, S0);
+  CK(cudaGetLastError());
+}
+
+}  // namespace nmt

@@ -1,0 +1,109 @@
+// kernels.h - device-side views and launchers of the non-GEMM kernels (kernels.cu).
+#pragma once
+#include "internal.h"
+
+namespace nmt {
+
+enum { CNT_NODES = 0, CNT_SLOTS = 1, CNT_ERR = 2, CNT_R = 3, CNT_N = 4 };
+enum { ERR_BAD_STATE = 1, ERR_TOKEN = 2, ERR_OFFSETS = 4 };
+
+// Per-context device arena + node table + (parent, word) -> child hash (the state cache).
+struct CtxDev {
+  int* counters;               // [CNT_N]
+  int* node_word;              // y_prev of each node's step (-1 BOS)
+  int* node_parent;            // -1 for the root / injected nodes
+  int* node_src;               // input slot of parentless nodes
+  int* node_slot;              // stepped output slot, -1 if not stepped
+  int* node_claim;             // scratch for deterministic parent dedup (INT_MAX when idle)
+  unsigned long long* hkeys;   // (parent << 32 | word), -1 empty
+  int* hvals;                  // child id (>= 0), or claim (< 0) during a call
+  uint64_t hmask;
+  float* S;                    // [slots][Hp] states (slot 0 = s0, slot 1 = scratch)
+  float* T;                    // [slots][Ep] readout outputs t
+  float* logZ;                 // [slots]
+  int* amax;                   // [slots]
+  int V, H, Hp, Ep;
+};
+
+// One call's request (device pointers) and planner scratch.
+struct PlanIO {
+  int n_par, n_cand;
+  const int* parents;   // [n_par]
+  const int* offsets;   // [n_par + 1]
+  const int* words;     // [n_cand]
+  int* cand_k;          // [n_cand] parent index of each candidate
+  int* cand_hslot;      // [n_cand] hash slot (-1 invalid)
+  int* row_src;         // [n_par] input slot of each stepped row
+  int* row_y;           // [n_par] previous word of each row
+  int* row_dst;         // [n_par] output slot of each row
+  int* row_node;        // [n_par] node id of each row
+};
+
+// Decoder-step workspace view (rows r < *R).
+struct StepDev {
+  const int* R;
+  const int* row_src;
+  const int* row_y;
+  const int* row_dst;
+  int V, H, Hp, Cp, E, Ep, ROp, maxout;
+  __nv_bfloat16* A_s; int lda_s, lo_s;   // [R][sf*Hp]
+  float* G1;                             // [R][3Hp]
+  const float* Ex;                       // [V+1][3Hp]
+  float* S1;                             // [R][Hp]
+  __nv_bfloat16* X; int ldx, lo_x;       // [R][sf*(Hp+Cp+Hp)]  [s1 | c | s2]
+  float* Q;                              // [R][Cp]
+  float* Cf;                             // [R][Cp]
+  float* alpha_out; int alpha_ld;        // [R][max_src_len] (may be null)
+  float* G2;                             // [R][4Hp]
+  const float* b_nl;                     // [2Hp]
+  const float* bx_nl;                    // [Hp]
+  float* RO;                             // [R][ROp]
+  const float* Eproj;                    // [V+1][ROp]
+  __nv_bfloat16* A_t; int lda_t, lo_t;   // [R][sf*Ep]
+  float4* part; int n_tiles;             // [R][n_tiles]
+};
+
+struct AttnCtx {
+  const float* pctx;   // [Tx][Cp]
+  const float* ctx;    // [Tx][Cp]
+  const float* U_att;  // [Cp]
+  float c_tt;
+  int Tx;
+};
+
+struct EncDev {
+  int H, Hp, NB, UPC;
+  const float* Uarr;     // [2][NB][3*UPC][H] recurrent weights per CTA
+  const float* Pin;      // [Tx][6Hp]
+  float* ctx;            // [Tx][2Hp]
+  float* hbuf;           // [2 dirs][2][Hp]
+  int* bar;              // [2]
+  const float* W_init;   // [2H][H]
+  const float* b_init;   // [H]
+  __nv_bfloat16* ctxbf;  // [Tx][4Hp] hi | lo
+};
+
+enum { EW_GATHER, EW_GRU1, EW_ATTN, EW_GRU2, EW_READOUT, EW_FINALIZE };
+
+void pack_T(const float* src, int ld_src, int K, int N, __nv_bfloat16* dst, int ld_dst, int row0, int col0, int rmap,
+            int kmap, int H, int Hp, int lo_off, cudaStream_t st);
+void pack_rows(const float* src, int ld_src, int rows, int K, __nv_bfloat16* dst, int ld_dst, int col0, int lo_off,
+               cudaStream_t st);
+void transpose_f32(const float* src, int K, int N, float* dst, int ld_dst, cudaStream_t st);
+void fill_i32(int* p, int64_t n, int v, cudaStream_t st);
+void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st);
+void rehash(const unsigned long long* okeys, const int* ovals, int64_t ocap, unsigned long long* nkeys, int* nvals,
+            uint64_t nmask, cudaStream_t st);
+void inject(const CtxDev& c, int n, const float* s, const int* y, int* out_ids, cudaStream_t st);
+void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, float* T, float* logZ, int* amax,
+                      int R_max, cudaStream_t st);
+void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const float* bo, int Ep, float* out_logp,
+                int* out_child32, long long* out_child64, int* out_argmax, cudaStream_t st);
+void full_row(const float* T, const float* Wo32, const float* bo, const float* logZ, int slot, int Ep, int V,
+              float* out, cudaStream_t st);
+void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, __nv_bfloat16* X, cudaStream_t st);
+size_t enc_recur_smem(int UPC, int H);
+void enc_recur(const EncDev& e, int Tx, cudaStream_t st);
+void enc_init(const EncDev& e, int Tx, float* S0, cudaStream_t st);
+
+}  // namespace nmt

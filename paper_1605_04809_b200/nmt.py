@@ -1,0 +1,245 @@
+"""Thin ctypes binding of libnmt.so (include/nmt.h).  Argument marshalling only: every step of the
+hot path runs in the library's CUDA kernels.  There is no fallback: if libnmt.so is missing or
+no sm_100 GPU is present the calls raise."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnmt.so")
+
+NMT_PREC_FP32CLASS = 0
+NMT_PREC_BF16 = 1
+PRECISIONS = {"fp32class": NMT_PREC_FP32CLASS, "bf16": NMT_PREC_BF16}
+
+STATUS = {0: "NMT_OK", 1: "NMT_ERR_INVALID_ARG", 2: "NMT_ERR_IO", 3: "NMT_ERR_FORMAT", 4: "NMT_ERR_MISSING_PARAM",
+          5: "NMT_ERR_SHAPE", 6: "NMT_ERR_EMPTY_SOURCE", 7: "NMT_ERR_TOKEN_RANGE", 8: "NMT_ERR_BAD_STATE",
+          9: "NMT_ERR_CAPACITY", 10: "NMT_ERR_CUDA", 11: "NMT_ERR_NCCL", 12: "NMT_ERR_OOM"}
+
+# every symbol include/nmt.h declares (checked by tests/test_abi.py)
+EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "nmt_model_free", "nmt_encode",
+           "nmt_root", "nmt_ctx_free", "nmt_score_batch", "nmt_score_batch_dev", "nmt_ctx_check", "nmt_ctx_stats",
+           "nmt_inject_states", "nmt_logprobs_full", "nmt_debug_encoder", "nmt_debug_intermediates",
+           "nmt_test_gemm", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
+           "nmt_ensemble_free"]
+
+
+class NmtError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class Dims(C.Structure):
+    _fields_ = [("dim_emb", C.c_int32), ("dim_hid", C.c_int32), ("vocab_src", C.c_int32), ("vocab_tgt", C.c_int32),
+                ("max_src_len", C.c_int32), ("readout", C.c_int32)]
+
+
+class Opts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("precision", C.c_int32), ("max_src_len", C.c_int32), ("stream", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built (run python -m paper_1605_04809_b200.build)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, f32p = C.c_void_p, C.c_int32, C.c_int64, C.c_void_p
+        sig = {
+            "nmt_last_error": (C.c_char_p, []),
+            "nmt_load": (i32, [C.c_char_p, C.POINTER(Opts), C.POINTER(vp)]),
+            "nmt_load_buffer": (i32, [vp, C.c_size_t, C.POINTER(Opts), C.POINTER(vp)]),
+            "nmt_model_dims": (i32, [vp, C.POINTER(Dims)]),
+            "nmt_model_free": (None, [vp]),
+            "nmt_encode": (i32, [vp, vp, i32, C.POINTER(vp)]),
+            "nmt_root": (i64, [vp]),
+            "nmt_ctx_free": (None, [vp]),
+            "nmt_score_batch": (i32, [vp, i32, vp, vp, vp, vp, vp, vp]),
+            "nmt_score_batch_dev": (i32, [vp, i32, vp, vp, i32, vp, vp, vp, vp]),
+            "nmt_ctx_check": (i32, [vp]),
+            "nmt_ctx_stats": (i32, [vp, C.POINTER(i64), C.POINTER(i64)]),
+            "nmt_inject_states": (i32, [vp, i32, vp, vp, vp]),
+            "nmt_logprobs_full": (i32, [vp, i64, vp]),
+            "nmt_debug_encoder": (i32, [vp, vp, vp, vp]),
+            "nmt_debug_intermediates": (i32, [vp, i64, vp, vp, vp, vp, vp, vp, vp]),
+            "nmt_test_gemm": (i32, [i32, i32, i32, i32, vp, vp, vp, vp]),
+            "nmt_ensemble_init": (i32, [i32, i32, vp, i32, C.POINTER(vp)]),
+            "nmt_ensemble_get_unique_id": (i32, [vp]),
+            "nmt_ensemble_combine": (i32, [vp, vp, i32, C.c_float, i32, i32, vp, vp]),
+            "nmt_ensemble_free": (None, [vp]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise NmtError(status, lib().nmt_last_error().decode(errors="replace"))
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _c(a, dtype) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a), dtype=dtype)
+
+
+class Model:
+    """nmt_load / nmt_load_buffer.  `params` is a path or the bytes of a params container."""
+
+    def __init__(self, params, precision: str = "bf16", device: int = 0, max_src_len: int = 64,
+                 stream: Optional[int] = None):
+        self._h = C.c_void_p()
+        opts = Opts(device, PRECISIONS[precision], max_src_len, stream)
+        if isinstance(params, (bytes, bytearray, memoryview)):
+            buf = (C.c_char * len(params)).from_buffer_copy(params)
+            _check(lib().nmt_load_buffer(C.cast(buf, C.c_void_p), len(params), C.byref(opts), C.byref(self._h)))
+        else:
+            _check(lib().nmt_load(str(params).encode(), C.byref(opts), C.byref(self._h)))
+        d = Dims()
+        _check(lib().nmt_model_dims(self._h, C.byref(d)))
+        self.dims = d
+        self.precision = precision
+
+    def encode(self, src_ids: Sequence[int]) -> "Context":
+        return Context(self, src_ids)
+
+    def close(self):
+        if self._h:
+            lib().nmt_model_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Context:
+    """nmt_encode: the source context and its state arena (root node = (s0, BOS))."""
+
+    def __init__(self, model: Model, src_ids: Sequence[int]):
+        self.model = model
+        src = _c(src_ids, np.int32)
+        self._h = C.c_void_p()
+        _check(lib().nmt_encode(model._h, _ptr(src), len(src), C.byref(self._h)))
+        self.Tx = len(src)
+        self.root = int(lib().nmt_root(self._h))
+
+    def score_batch(self, parents, cand_offsets, cand_words, with_argmax: bool = True
+                    ) -> Tuple[np.ndarray, np.ndarray, Optional[np.ndarray]]:
+        par = _c(parents, np.int64)
+        off = _c(cand_offsets, np.int32)
+        words = _c(cand_words, np.int32)
+        n = int(off[-1]) if len(off) else 0
+        logp = np.empty(n, np.float32)
+        child = np.empty(n, np.int64)
+        am = np.empty(len(par), np.int32) if with_argmax else None
+        _check(lib().nmt_score_batch(self._h, len(par), _ptr(par), _ptr(off), _ptr(words), _ptr(logp), _ptr(child),
+                                     _ptr(am)))
+        return logp, child, am
+
+    def score_batch_dev(self, n_parents: int, parents_ptr: int, offsets_ptr: int, n_cand: int, words_ptr: int,
+                        logp_ptr: int, child_ptr: int, argmax_ptr: Optional[int] = None) -> None:
+        """Device-resident variant (int32 device arrays, e.g. torch tensors' data_ptr())."""
+        _check(lib().nmt_score_batch_dev(self._h, n_parents, parents_ptr, offsets_ptr, n_cand, words_ptr, logp_ptr,
+                                         child_ptr, argmax_ptr))
+
+    def check(self) -> None:
+        _check(lib().nmt_ctx_check(self._h))
+
+    def stats(self) -> Tuple[int, int]:
+        a, b = C.c_int64(), C.c_int64()
+        _check(lib().nmt_ctx_stats(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def inject_states(self, s: np.ndarray, y_prev: Sequence[int]) -> np.ndarray:
+        s = _c(s, np.float32)
+        y = _c(y_prev, np.int32)
+        out = np.empty(len(y), np.int64)
+        _check(lib().nmt_inject_states(self._h, len(y), _ptr(s), _ptr(y), _ptr(out)))
+        return out
+
+    def logprobs_full(self, node: int) -> np.ndarray:
+        out = np.empty(self.model.dims.vocab_tgt, np.float32)
+        _check(lib().nmt_logprobs_full(self._h, int(node), _ptr(out)))
+        return out
+
+    def debug_encoder(self):
+        H = self.model.dims.dim_hid
+        ctx = np.empty((self.Tx, 2 * H), np.float32)
+        pctx = np.empty((self.Tx, 2 * H), np.float32)
+        s0 = np.empty(H, np.float32)
+        _check(lib().nmt_debug_encoder(self._h, _ptr(ctx), _ptr(pctx), _ptr(s0)))
+        return ctx, pctx, s0
+
+    def debug_intermediates(self, node: int) -> dict:
+        d = self.model.dims
+        H, E = d.dim_hid, d.dim_emb
+        out = dict(s1=np.empty(H, np.float32), alpha=np.empty(self.Tx, np.float32), c=np.empty(2 * H, np.float32),
+                   s2=np.empty(H, np.float32), t=np.empty(E, np.float32), logZ=np.empty(1, np.float32),
+                   argmax=np.empty(1, np.int32))
+        _check(lib().nmt_debug_intermediates(self._h, int(node), *[_ptr(out[k]) for k in
+                                                                    ("s1", "alpha", "c", "s2", "t", "logZ", "argmax")]))
+        return out
+
+    def close(self):
+        if self._h:
+            lib().nmt_ctx_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def test_gemm(A: np.ndarray, B: np.ndarray, bias: Optional[np.ndarray] = None, split: bool = False) -> np.ndarray:
+    A = _c(A, np.float32)
+    B = _c(B, np.float32)
+    M, K = A.shape
+    N = B.shape[1]
+    out = np.empty((M, N), np.float32)
+    b = None if bias is None else _c(bias, np.float32)
+    _check(lib().nmt_test_gemm(M, N, K, int(split), _ptr(A), _ptr(B), _ptr(b), _ptr(out)))
+    return out
+
+
+class Ensemble:
+    """nmt_ensemble_*: one member per GPU/process; NCCL reduce of per-word scores to the root."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_char * 128)()
+        _check(lib().nmt_ensemble_get_unique_id(C.cast(buf, C.c_void_p)))
+        return bytes(buf)
+
+    def __init__(self, n_members: int, rank: int, unique_id: bytes, device: int):
+        self._h = C.c_void_p()
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        _check(lib().nmt_ensemble_init(n_members, rank, C.cast(buf, C.c_void_p), device, C.byref(self._h)))
+
+    def combine(self, logp_ptr: int, n: int, weight: float, mode: int, root: int, out_ptr: Optional[int],
+                stream: Optional[int] = None) -> None:
+        _check(lib().nmt_ensemble_combine(self._h, logp_ptr, n, weight, mode, root, out_ptr, stream))
+
+    def close(self):
+        if self._h:
+            lib().nmt_ensemble_free(self._h)
+            self._h = C.c_void_p()
