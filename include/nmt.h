@@ -111,6 +111,10 @@ NMT_API void nmt_model_free(nmt_model* m);
  * -> NMT_ERR_CAPACITY.  The returned context owns a state arena whose root node is (s_0, BOS).  */
 NMT_API nmt_status nmt_encode(nmt_model* m, const int32_t* src_ids, int32_t len, nmt_ctx** out);
 NMT_API nmt_state nmt_root(const nmt_ctx* c);
+/* Same with src_ids [dev] (e.g. resident in HBM); token ids are validated on the device and an
+ * out-of-range id is reported by nmt_ctx_check().  Asynchronous on the model stream.            */
+NMT_API nmt_status nmt_encode_dev(nmt_model* m, const int32_t* src_ids, int32_t len, nmt_ctx** out);
+/* Releases the context; its arena is kept by the model for reuse by a later nmt_encode. */
 NMT_API void nmt_ctx_free(nmt_ctx* c);
 
 /* ---- batched scoring (Alg. 1; parent-indexed rows, DESIGN.md §2 A13) -----
@@ -142,6 +146,22 @@ NMT_API nmt_status nmt_ctx_stats(nmt_ctx* c, int64_t* n_nodes, int64_t* n_steppe
 /* ---- synthetic parents (bench / tests): n nodes with given input state s[n x H] [host] and
  * previous word y_prev[n] [host] (-1 = BOS), not children of any node.                         */
 NMT_API nmt_status nmt_inject_states(nmt_ctx* c, int32_t n, const float* s, const int32_t* y_prev, nmt_state* out);
+
+/* Device variant: s [dev, n x H floats], y_prev [dev, n], out [dev, n int32 node ids]; async.  */
+NMT_API nmt_status nmt_inject_states_dev(nmt_ctx* c, int32_t n, const float* s, const int32_t* y_prev, int32_t* out);
+
+/* ---- diagnostics (bench.py) -----------------------------------------------------------------
+ * nmt_launch_count: kernels this library has launched in the process so far.
+ * nmt_profile: 0 off, 1 CUDA events around the vocabulary GEMM only, 2 around every stage (on the
+ * model stream).  nmt_profile_read synchronises and returns the milliseconds and launch counts per
+ * stage accumulated since the previous read, stage order:
+ *   0 plan  1 gather  2 gemm_h1  3 gru1  4 gemm_q  5 attention  6 gemm_g2  7 gru2  8 gemm_ro
+ *   9 readout  10 vocab_gemm_lse  11 finalize  12 gather_dot  13 enc_gather  14 enc_gemm_in
+ *   15 enc_recurrence  16 enc_init  17 enc_pctx  18 inject                                        */
+#define NMT_N_STAGES 19
+NMT_API long long nmt_launch_count(void);
+NMT_API nmt_status nmt_profile(nmt_model* m, int32_t mode);
+NMT_API nmt_status nmt_profile_read(nmt_model* m, double* ms, int64_t* count);
 
 /* ---- test-only exports ----------------------------------------------------------------------- */
 /* full log-prob row of one node over the whole vocab (normalisation tests); steps the node if

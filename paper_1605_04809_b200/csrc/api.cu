@@ -18,6 +18,7 @@
 #include <memory>
 #include <mutex>
 #include <sstream>
+#include <tuple>
 #include <vector>
 
 #include "internal.h"
@@ -26,6 +27,19 @@
 using namespace nmt;
 
 static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+namespace nmt {
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace nmt
+
+// profiling stages (include/nmt.h NMT_N_STAGES)
+enum Stage {
+  ST_PLAN, ST_GATHER, ST_GEMM_H1, ST_GRU1, ST_GEMM_Q, ST_ATTN, ST_GEMM_G2, ST_GRU2, ST_GEMM_RO, ST_READOUT,
+  ST_VOCAB, ST_FINALIZE, ST_GATHERDOT, ST_ENC_GATHER, ST_ENC_GEMM, ST_ENC_RECUR, ST_ENC_INIT, ST_ENC_PCTX,
+  ST_INJECT, ST_N
+};
+static_assert(ST_N == NMT_N_STAGES, "stage table");
 
 namespace nmt {
 nmt_status set_error(nmt_status c, const std::string& m) {
@@ -117,6 +131,8 @@ struct nmt_model {
   float* Pin = nullptr;           // [Tpad][6Hp]
   __nv_bfloat16* ctxbf = nullptr; // [Tpad][4Hp]
   float* hbuf = nullptr;
+  float* enc_mean = nullptr;
+  float* enc_s0part = nullptr;
   int* bar = nullptr;
   int* d_src = nullptr;
   CUtensorMap tm_Xsrc, tm_ctxbf;
@@ -139,6 +155,24 @@ struct nmt_model {
   // lifetime: one reference held by the user handle plus one per live context, so that
   // nmt_model_free and nmt_ctx_free may be called in any order
   std::atomic<int> refs{1};
+  // released contexts kept for reuse (no cudaMalloc / memset per sentence)
+  std::vector<nmt_ctx*> pool;
+  // CUDA-event profiling of the stages (mode 0 off, 1 vocabulary GEMM only, 2 all)
+  int prof_mode = 0;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> prof_pending;
+  std::vector<cudaEvent_t> prof_free;
+  double prof_ms[ST_N] = {0};
+  long long prof_cnt[ST_N] = {0};
+  cudaEvent_t ev() {
+    if (prof_free.empty()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = prof_free.back();
+    prof_free.pop_back();
+    return e;
+  }
 
   ~nmt_model();
   void free_ws();
@@ -148,7 +182,7 @@ struct nmt_model {
 
 static void free_all_model(nmt_model* m) {
   for (float** p : {&m->Wemb_src, &m->benc, &m->Uarr, &m->W_init, &m->b_init, &m->b_att, &m->U_att, &m->Ex, &m->b_nl,
-                    &m->bx_nl, &m->Eproj, &m->W_o32, &m->b_o, &m->Pin, &m->hbuf})
+                    &m->bx_nl, &m->Eproj, &m->W_o32, &m->b_o, &m->Pin, &m->hbuf, &m->enc_mean, &m->enc_s0part})
     dfree(*p);
   for (__nv_bfloat16** p : {&m->Wenc, &m->Watt, &m->W_h1, &m->W_q, &m->W_g2, &m->W_ro, &m->W_o, &m->Xsrc, &m->ctxbf})
     dfree(*p);
@@ -159,9 +193,35 @@ static void free_all_model(nmt_model* m) {
   m->pin = nullptr;
 }
 
+struct ProfScope {  // CUDA events around one stage's launches on the model stream
+  nmt_model* m;
+  int stage;
+  cudaEvent_t a = nullptr;
+  ProfScope(nmt_model* m_, int s) : m(m_), stage(s) {
+    if (m->prof_mode == 2 || (m->prof_mode == 1 && s == ST_VOCAB)) {
+      a = m->ev();
+      CK(cudaEventRecord(a, m->st));
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = m->ev();
+      cudaEventRecord(b, m->st);
+      m->prof_pending.emplace_back(stage, a, b);
+    }
+  }
+};
+
 nmt_model::~nmt_model() {
   cudaSetDevice(device);
   if (st) cudaStreamSynchronize(st);
+  for (nmt_ctx* c : pool) delete c;
+  pool.clear();
+  for (auto& t : prof_pending) {
+    cudaEventDestroy(std::get<1>(t));
+    cudaEventDestroy(std::get<2>(t));
+  }
+  for (cudaEvent_t e : prof_free) cudaEventDestroy(e);
   free_all_model(this);
   if (own_stream && st) cudaStreamDestroy(st);
 }
@@ -454,9 +514,9 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   }
   m->Wenc = dalloc<__nv_bfloat16>((size_t)6 * Hp * 2 * Ep);
   std::vector<float> benc(6 * Hp, 0.f);
-  m->UPC = std::max(1, (H + 63) / 64);
+  m->UPC = std::max(1, (H + 73) / 74);  // <= 74 CTAs per direction: both directions fill the 148 SMs
   m->NB = (H + m->UPC - 1) / m->UPC;
-  std::vector<float> uarr((size_t)2 * m->NB * 3 * m->UPC * H, 0.f);
+  std::vector<float> uarr((size_t)2 * m->NB * 3 * m->UPC * Hp, 0.f);
   for (int d = 0; d < 2; ++d) {
     const std::string p = d ? "encoder_r" : "encoder";
     Upload W(A.at(p + "_W"), st), Wx(A.at(p + "_Wx"), st);
@@ -477,7 +537,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
         for (int u = 0; u < m->UPC; ++u) {
           const int jj = cb * m->UPC + u;
           if (jj >= H) continue;
-          float* dst = &uarr[(((size_t)(d * m->NB + cb) * 3 * m->UPC) + g * m->UPC + u) * H];
+          float* dst = &uarr[(((size_t)(d * m->NB + cb) * 3 * m->UPC) + g * m->UPC + u) * Hp];
           for (int k = 0; k < H; ++k) dst[k] = g < 2 ? U[(size_t)k * 2 * H + g * H + jj] : Ux[(size_t)k * H + jj];
         }
   }
@@ -625,6 +685,8 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   m->Pin = dalloc<float>((size_t)m->Tpad * 6 * Hp);
   m->ctxbf = dalloc<__nv_bfloat16>((size_t)m->Tpad * 4 * Hp);
   m->hbuf = dalloc<float>(4 * Hp);
+  m->enc_mean = dalloc<float>(2 * H);
+  m->enc_s0part = dalloc<float>(16 * H);
   m->bar = dalloc<int>(2);
   m->d_src = dalloc<int>(m->maxTx);
   m->tm_Xsrc = make_tmap_bf16(m->Xsrc, m->Tpad, 2 * Ep, 128);
@@ -776,12 +838,13 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
   const int* Rd = d.R;
   const int Hp = m->Hp, Cp = m->Cp, Ep = m->Ep;
   const bool sp = m->split;
-  step_elementwise(EW_GATHER, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
-  gemm_store(m->tm_As, m->tm_Wh1, gemm_shape(0, Rd, 3 * Hp, Hp, 0, sp, Hp, Hp), m->G1, 3 * Hp, nullptr, R_max, st);
-  step_elementwise(EW_GRU1, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
-  gemm_store(m->tm_X, m->tm_Wq, gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp), m->Q, Cp, nullptr, R_max, st);
-  step_elementwise(EW_ATTN, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
+  { ProfScope p_(m, ST_GATHER); step_elementwise(EW_GATHER, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
+  { ProfScope p_(m, ST_GEMM_H1); gemm_store(m->tm_As, m->tm_Wh1, gemm_shape(0, Rd, 3 * Hp, Hp, 0, sp, Hp, Hp), m->G1, 3 * Hp, nullptr, R_max, st); }
+  { ProfScope p_(m, ST_GRU1); step_elementwise(EW_GRU1, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
+  { ProfScope p_(m, ST_GEMM_Q); gemm_store(m->tm_X, m->tm_Wq, gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp), m->Q, Cp, nullptr, R_max, st); }
+  { ProfScope p_(m, ST_ATTN); step_elementwise(EW_ATTN, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   {
+    ProfScope p_(m, ST_GEMM_G2);
     GemmShape g = gemm_shape(0, Rd, 4 * Hp, Hp + Cp, 0, sp, 4 * Hp, Hp + Cp);
     g.nreg = 3;
     g.reg_n_end[0] = 2 * Hp, g.reg_k0[0] = 0, g.reg_k1[0] = Hp + Cp;  // gates: s1 U_nl + c Wc
@@ -789,12 +852,12 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
     g.reg_n_end[2] = 4 * Hp, g.reg_k0[2] = Hp, g.reg_k1[2] = Hp + Cp; // c Wcx
     gemm_store(m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, nullptr, R_max, st);
   }
-  step_elementwise(EW_GRU2, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
-  gemm_store(m->tm_X, m->tm_Wro, gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp), m->RO_buf, m->ROp,
-             nullptr, R_max, st);
-  step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
-  gemm_lse(m->tm_At, m->tm_Wo, gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep), m->part, m->V, R_max, st);
-  step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
+  { ProfScope p_(m, ST_GRU2); step_elementwise(EW_GRU2, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
+  { ProfScope p_(m, ST_GEMM_RO); gemm_store(m->tm_X, m->tm_Wro, gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp), m->RO_buf, m->ROp,
+             nullptr, R_max, st); }
+  { ProfScope p_(m, ST_READOUT); step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
+  { ProfScope p_(m, ST_VOCAB); gemm_lse(m->tm_At, m->tm_Wo, gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep), m->part, m->V, R_max, st); }
+  { ProfScope p_(m, ST_FINALIZE); step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
 }
 
 static PlanIO plan_io(nmt_model* m, int np, int nc, const int* par, const int* off, const int* words) {
@@ -816,8 +879,12 @@ static PlanIO plan_io(nmt_model* m, int np, int nc, const int* par, const int* o
 static void run_call(nmt_model* m, nmt_ctx* c, const PlanIO& io, float* out_logp, int* out_child,
                      long long* out_child64, int* out_amax) {
   const CtxDev cd = c->dev();
-  plan(cd, io, c->counters + CNT_R, m->st);
+  {
+    ProfScope p_(m, ST_PLAN);
+    plan(cd, io, c->counters + CNT_R, m->st);
+  }
   run_step(m, c, io.n_par);
+  ProfScope p_(m, ST_GATHERDOT);
   gather_dot(cd, io, m->W_o32, m->b_o, m->Ep, out_logp, out_child, out_child64, out_amax, m->st);
 }
 
@@ -891,6 +958,85 @@ nmt_status nmt_model_dims(const nmt_model* m, nmt_dims* out) {
 
 void nmt_model_free(nmt_model* m) { model_release(m); }
 
+// E1-E7 for one sentence; src ids either [host] (copied) or [dev] (validated on the device)
+static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t* src_dev, int len) {
+  CK(cudaSetDevice(m->device));
+  cudaStream_t st = m->st;
+  nmt_ctx* c = nullptr;
+  if (!m->pool.empty()) {  // reuse a released arena: reset its counters and hash table only
+    c = m->pool.back();
+    m->pool.pop_back();
+    c->m = m;
+    CK(cudaMemsetAsync(c->hkeys, 0xff, c->hcap * sizeof(unsigned long long), st));
+    fill_i32(c->hvals, c->hcap, INT32_MIN, st);
+  } else {
+    c = new nmt_ctx();
+    c->m = m;
+    c->ctx = dalloc<float>((size_t)m->maxTx * m->Cp);
+    c->pctx = dalloc<float>((size_t)m->maxTx * m->Cp);
+    c->counters = dalloc<int>(CNT_N);
+    c->grow_nodes(4096);
+    c->grow_slots(1024);
+  }
+  m->refs.fetch_add(1);
+  c->Tx = len;
+  std::unique_ptr<nmt_ctx> guard_c(c);
+  const int* d_src = src_dev;
+  if (src_host) {
+    CK(cudaMemcpyAsync(m->d_src, src_host, (size_t)len * 4, cudaMemcpyHostToDevice, st));
+    d_src = m->d_src;
+  }
+  static const int cnt[CNT_N] = {1, 2, 0, 0};  // static: source of an async copy
+  CK(cudaMemcpyAsync(c->counters, cnt, sizeof(cnt), cudaMemcpyHostToDevice, st));
+  {  // E1/E2: embeddings -> input projections of both directions (split bf16x3 GEMM)
+    {
+      ProfScope p_(m, ST_ENC_GATHER);
+      enc_gather(m->Wemb_src, d_src, len, m->E, m->Ep, m->Vs, m->Xsrc, c->counters + CNT_ERR, st);
+    }
+    ProfScope p_(m, ST_ENC_GEMM);
+    gemm_store(m->tm_Xsrc, m->tm_Wenc, gemm_shape(len, nullptr, 6 * m->Hp, m->Ep, 0, true, m->Ep, m->Ep), m->Pin,
+               6 * m->Hp, m->benc, len, st);
+  }
+  EncDev e{};
+  e.H = m->H;
+  e.Hp = m->Hp;
+  e.NB = m->NB;
+  e.UPC = m->UPC;
+  e.Uarr = m->Uarr;
+  e.Pin = m->Pin;
+  e.ctx = c->ctx;
+  e.hbuf = m->hbuf;
+  e.bar = m->bar;
+  e.W_init = m->W_init;
+  e.b_init = m->b_init;
+  e.ctxbf = m->ctxbf;
+  e.mean = m->enc_mean;
+  e.s0part = m->enc_s0part;
+  {  // E3/E4: recurrence
+    ProfScope p_(m, ST_ENC_RECUR);
+    enc_recur(e, len, st);
+  }
+  {  // E5: s0 into slot 0 (+ split copy of ctx)
+    ProfScope p_(m, ST_ENC_INIT);
+    enc_init(e, len, c->S, st);
+  }
+  {  // E7: pctx = ctx.Wc_att + b_att
+    ProfScope p_(m, ST_ENC_PCTX);
+    gemm_store(m->tm_ctxbf, m->tm_Watt, gemm_shape(len, nullptr, m->Cp, m->Cp, 0, true, m->Cp, m->Cp), c->pctx, m->Cp,
+               m->b_att, len, st);
+  }
+  // root node 0 = (s0, BOS): word -1, parent -1, src slot 0, not stepped
+  static const int root[3] = {-1, -1, 0};
+  CK(cudaMemcpyAsync(c->node_word, &root[0], 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->node_parent, &root[1], 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->node_src, &root[2], 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->node_slot, &root[0], 4, cudaMemcpyHostToDevice, st));
+  c->n_nodes = 1;
+  c->n_slots = 2;
+  c->stale = src_dev != nullptr;  // device ids are validated asynchronously
+  return guard_c.release();
+}
+
 nmt_status nmt_encode(nmt_model* m, const int32_t* src, int32_t len, nmt_ctx** out) {
   if (!m || !out) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
   if (len == 0) return fail(NMT_ERR_EMPTY_SOURCE, "empty source");
@@ -903,58 +1049,34 @@ nmt_status nmt_encode(nmt_model* m, const int32_t* src, int32_t len, nmt_ctx** o
                                            " outside [0, " + std::to_string(m->Vs) + ")");
   return guard([&] {
     std::lock_guard<std::mutex> lk(m->mu);
-    CK(cudaSetDevice(m->device));
-    cudaStream_t st = m->st;
-    std::unique_ptr<nmt_ctx> c(new nmt_ctx());
-    m->refs.fetch_add(1);
-    c->m = m;
-    c->Tx = len;
-    c->ctx = dalloc<float>((size_t)len * m->Cp);
-    c->pctx = dalloc<float>((size_t)len * m->Cp);
-    c->counters = dalloc<int>(CNT_N);
-    c->grow_nodes(4096);
-    c->grow_slots(1024);
-    // E1/E2: embeddings -> input projections of both directions (split bf16x3 GEMM)
-    CK(cudaMemcpyAsync(m->d_src, src, len * 4, cudaMemcpyHostToDevice, st));
-    enc_gather(m->Wemb_src, m->d_src, len, m->E, m->Ep, m->Xsrc, st);
-    gemm_store(m->tm_Xsrc, m->tm_Wenc, gemm_shape(len, nullptr, 6 * m->Hp, m->Ep, 0, true, m->Ep, m->Ep), m->Pin,
-               6 * m->Hp, m->benc, len, st);
-    // E3/E4: recurrence
-    EncDev e{};
-    e.H = m->H;
-    e.Hp = m->Hp;
-    e.NB = m->NB;
-    e.UPC = m->UPC;
-    e.Uarr = m->Uarr;
-    e.Pin = m->Pin;
-    e.ctx = c->ctx;
-    e.hbuf = m->hbuf;
-    e.bar = m->bar;
-    e.W_init = m->W_init;
-    e.b_init = m->b_init;
-    e.ctxbf = m->ctxbf;
-    enc_recur(e, len, st);
-    // E5: s0 into slot 0; E7: pctx = ctx.Wc_att + b_att
-    enc_init(e, len, c->S, st);
-    gemm_store(m->tm_ctxbf, m->tm_Watt, gemm_shape(len, nullptr, m->Cp, m->Cp, 0, true, m->Cp, m->Cp), c->pctx, m->Cp,
-               m->b_att, len, st);
-    // root node 0 = (s0, BOS)
-    const int cnt[CNT_N] = {1, 2, 0, 0};
-    const int w = -1, par = -1, srcslot = 0;
-    CK(cudaMemcpyAsync(c->counters, cnt, sizeof(cnt), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->node_word, &w, 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->node_parent, &par, 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(c->node_src, &srcslot, 4, cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));
-    c->n_nodes = 1;
-    c->n_slots = 2;
-    *out = c.release();
+    *out = encode_impl(m, src, nullptr, len);
+  });
+}
+
+nmt_status nmt_encode_dev(nmt_model* m, const int32_t* src, int32_t len, nmt_ctx** out) {
+  if (!m || !out) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
+  if (len == 0) return fail(NMT_ERR_EMPTY_SOURCE, "empty source");
+  if (len < 0 || !src) return fail(NMT_ERR_INVALID_ARG, "bad source");
+  if (len > m->maxTx)
+    return fail(NMT_ERR_CAPACITY, "source length " + std::to_string(len) + " > max_src_len " + std::to_string(m->maxTx));
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    *out = encode_impl(m, nullptr, src, len);
   });
 }
 
 nmt_state nmt_root(const nmt_ctx* c) { return c ? 0 : -1; }
 
-void nmt_ctx_free(nmt_ctx* c) { delete c; }
+void nmt_ctx_free(nmt_ctx* c) {
+  if (!c) return;
+  nmt_model* m = c->m;
+  {
+    std::lock_guard<std::mutex> lk(m->mu);
+    c->m = nullptr;  // pooled arenas hold no model reference; stream order protects their reuse
+    m->pool.push_back(c);
+  }
+  model_release(m);
+}
 
 nmt_status nmt_score_batch(nmt_ctx* c, int32_t np, const nmt_state* parents, const int32_t* off, const int32_t* words,
                            float* out_logp, nmt_state* out_child, int32_t* out_argmax) {
@@ -1088,13 +1210,64 @@ nmt_status nmt_inject_states(nmt_ctx* c, int32_t n, const float* s, const int32_
     // (in_s holds R_cap x H floats; the y and ids use the candidate scratch)
     CK(cudaMemcpyAsync(m->in_s, s, (size_t)n * m->H * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(m->in_words, y, (size_t)n * 4, cudaMemcpyHostToDevice, st));
-    inject(c->dev(), n, m->in_s, m->in_words, m->out_child, st);
+    {
+      ProfScope p_(m, ST_INJECT);
+      inject(c->dev(), n, m->in_s, m->in_words, m->out_child, st);
+    }
     std::vector<int> ids(n);
     CK(cudaMemcpyAsync(ids.data(), m->out_child, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     for (int i = 0; i < n; ++i) out[i] = ids[i];
     c->n_nodes += n;
     c->n_slots += n;
+  });
+}
+
+nmt_status nmt_inject_states_dev(nmt_ctx* c, int32_t n, const float* s, const int32_t* y, int32_t* out) {
+  if (!c || n < 0 || (n > 0 && (!s || !y || !out))) return fail(NMT_ERR_INVALID_ARG, "bad argument");
+  nmt_model* m = c->m;
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    if (n == 0) return;
+    c->ensure(n, n);
+    ProfScope p_(m, ST_INJECT);
+    inject(c->dev(), n, s, y, out, m->st);
+    c->n_nodes += n;
+    c->n_slots += n;
+  });
+}
+
+long long nmt_launch_count(void) { return g_launches.load(); }
+
+nmt_status nmt_profile(nmt_model* m, int32_t mode) {
+  if (!m || mode < 0 || mode > 2) return fail(NMT_ERR_INVALID_ARG, "bad argument");
+  std::lock_guard<std::mutex> lk(m->mu);
+  m->prof_mode = mode;
+  return NMT_OK;
+}
+
+nmt_status nmt_profile_read(nmt_model* m, double* ms, int64_t* count) {
+  if (!m) return fail(NMT_ERR_INVALID_ARG, "model is NULL");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    CK(cudaStreamSynchronize(m->st));
+    for (auto& t : m->prof_pending) {
+      float e = 0.f;
+      CK(cudaEventElapsedTime(&e, std::get<1>(t), std::get<2>(t)));
+      m->prof_ms[std::get<0>(t)] += e;
+      m->prof_cnt[std::get<0>(t)] += 1;
+      m->prof_free.push_back(std::get<1>(t));
+      m->prof_free.push_back(std::get<2>(t));
+    }
+    m->prof_pending.clear();
+    for (int i = 0; i < ST_N; ++i) {
+      if (ms) ms[i] = m->prof_ms[i];
+      if (count) count[i] = m->prof_cnt[i];
+      m->prof_ms[i] = 0;
+      m->prof_cnt[i] = 0;
+    }
   });
 }
 

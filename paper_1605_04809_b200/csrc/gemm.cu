@@ -267,7 +267,7 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& 
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
   if (grid <= 0) return;
   k_gemm<BN, STAGES, EPI><<<grid, 192, S::BYTES, st>>>(a, b, g, ep);
-  CK(cudaGetLastError());
+  CK_LAUNCH();
 }
 
 void gemm_validate(const GemmShape& g, int BN) {

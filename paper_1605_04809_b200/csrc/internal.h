@@ -25,6 +25,14 @@ struct NmtError {
                             std::string(#expr) + ": " + cudaGetErrorString(_e));                          \
   } while (0)
 
+// every kernel launch of the library goes through CK_LAUNCH (counted for the bench's gpu_launches)
+void note_launch();
+#define CK_LAUNCH()            \
+  do {                         \
+    ::nmt::note_launch();      \
+    CK(cudaGetLastError());    \
+  } while (0)
+
 // --------------------------------------------------------------------------- GEMM engine
 struct GemmShape {
   int M;             // rows (if M_dev == nullptr)

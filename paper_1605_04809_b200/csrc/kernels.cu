@@ -45,7 +45,7 @@ void pack_T(const float* src, int ld_src, int K, int N, __nv_bfloat16* dst, int 
   if (!n) return;
   k_pack_T<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, ld_src, K, N, dst, ld_dst, row0, col0, rmap, kmap, H, Hp,
                                                         lo_off);
-  CK(cudaGetLastError());
+  CK_LAUNCH();
 }
 
 // dst[r][col0 + k] = split(src[r * ld_src + k]) for r < rows, k < K (row-major copy)
@@ -61,7 +61,7 @@ void pack_rows(const float* src, int ld_src, int rows, int K, __nv_bfloat16* dst
   const int64_t n = (int64_t)rows * K;
   if (!n) return;
   k_pack_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, ld_src, rows, K, dst, ld_dst, col0, lo_off);
-  CK(cudaGetLastError());
+  CK_LAUNCH();
 }
 
 // fp32 [K x N] -> fp32 [N x ld_dst] transposed (W_o columns as contiguous per-word rows)
@@ -74,7 +74,7 @@ __global__ void k_transpose_f32(const float* __restrict__ src, int K, int N, flo
 void transpose_f32(const float* src, int K, int N, float* dst, int ld_dst, cudaStream_t st) {
   const int64_t n = (int64_t)K * N;
   k_transpose_f32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, K, N, dst, ld_dst);
-  CK(cudaGetLastError());
+  CK_LAUNCH();
 }
 
 // ===================================================================================== planner
@@ -227,10 +227,10 @@ void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st) {
   const int n = io.n_cand > io.n_par ? io.n_cand : io.n_par;
   if (n > 0) {
     k_plan_intern<<<(n + 255) / 256, 256, 0, st>>>(c, io);
-    CK(cudaGetLastError());
+    CK_LAUNCH();
   }
   k_plan_assign<<<1, 1024, 0, st>>>(c, io, R_dev);
-  CK(cudaGetLastError());
+  CK_LAUNCH();
 }
 
 // rehash all entries of an old table into a new (larger) one
@@ -246,7 +246,7 @@ __global__ void k_rehash(const unsigned long long* okeys, const int* ovals, int6
 void rehash(const unsigned long long* okeys, const int* ovals, int64_t ocap, unsigned long long* nkeys, int* nvals,
             uint64_t nmask, cudaStream_t st) {
   k_rehash<<<(unsigned)((ocap + 255) / 256), 256, 0, st>>>(okeys, ovals, ocap, nkeys, nvals, nmask);
-  CK(cudaGetLastError());
+  CK_LAUNCH();
 }
 
 __global__ void k_fill_i32(int* p, int64_t n, int v) {
@@ -256,7 +256,7 @@ __global__ void k_fill_i32(int* p, int64_t n, int v) {
 void fill_i32(int* p, int64_t n, int v, cudaStream_t st) {
   if (n <= 0) return;
   k_fill_i32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, n, v);
-  CK(cudaGetLastError());
+  CK_LAUNCH();
 }
 
 // inject parentless nodes with their own input slots (synthetic parents for bench/tests)
@@ -267,7 +267,12 @@ __global__ void k_inject(CtxDev c, int n, const float* s, const int* y, int* out
     for (int j = threadIdx.x; j < c.H; j += blockDim.x) c.S[(int64_t)slot * c.Hp + j] = s[(int64_t)i * c.H + j];
     if (threadIdx.x == 0) {
       const int id = n_nodes0 + i;
-      c.node_word[id] = y[i];
+      int yy = y[i];
+      if (yy < -1 || yy >= c.V) {
+        atomicOr(&c.counters[CNT_ERR], ERR_TOKEN);
+        yy = -1;
+      }
+      c.node_word[id] = yy;
       c.node_parent[id] = -1;
       c.node_src[id] = slot;
       c.node_slot[id] = -1;
@@ -282,9 +287,9 @@ __global__ void k_inject_commit(CtxDev c, int n) {
 }
 void inject(const CtxDev& c, int n, const float* s, const int* y, int* out_ids, cudaStream_t st) {
   k_inject<<<n < 1024 ? n : 1024, 256, 0, st>>>(c, n, s, y, out_ids);
-  CK(cudaGetLastError());
+  CK_LAUNCH();
   k_inject_commit<<<1, 1, 0, st>>>(c, n);
-  CK(cudaGetLastError());
+  CK_LAUNCH();
 }
 
 // ===================================================================================== step D1-D7
@@ -591,7 +596,7 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
     case EW_READOUT: k_readout<<<g, 128, 0, st>>>(d, T); break;
     case EW_FINALIZE: k_finalize<<<(R_max * 32 + 255) / 256, 256, 0, st>>>(d, logZ, amax); break;
   }
-  CK(cudaGetLastError());
+  CK_LAUNCH();
 }
 
 void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const float* bo, int Ep, float* out_logp,
@@ -599,69 +604,94 @@ void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const floa
   if (io.n_cand > 0) {
     k_gather_dot<<<(io.n_cand * 32 + 255) / 256, 256, 0, st>>>(c, io, Wo32, bo, Ep, out_logp, out_child32,
                                                                  out_child64);
-    CK(cudaGetLastError());
+    CK_LAUNCH();
   }
   if (out_argmax && io.n_par > 0) {
     k_argmax_out<<<(io.n_par + 255) / 256, 256, 0, st>>>(c, io, out_argmax);
-    CK(cudaGetLastError());
+    CK_LAUNCH();
   }
 }
 
 void full_row(const float* T, const float* Wo32, const float* bo, const float* logZ, int slot, int Ep, int V,
               float* out, cudaStream_t st) {
   k_full_row<<<(V * 32 + 255) / 256, 256, 0, st>>>(T, Wo32, bo, logZ, slot, Ep, V, out);
-  CK(cudaGetLastError());
+  CK_LAUNCH();
 }
 
 // ===================================================================================== encoder
 // E1: gather source embeddings into the split bf16 A operand of the input projections.
-__global__ void k_enc_gather(const float* __restrict__ Wemb, const int* __restrict__ src, int Tx, int E, int Ep,
-                             __nv_bfloat16* X) {
+__global__ void k_enc_gather(const float* __restrict__ Wemb, const int* __restrict__ src, int Tx, int E, int Ep, int Vs,
+                             __nv_bfloat16* X, int* err) {
   const int j = blockIdx.x;
   if (j >= Tx) return;
-  const float* e = Wemb + (int64_t)src[j] * E;
+  int id = src[j];
+  if (id < 0 || id >= Vs) {  // device-resident ids are validated here (reported by nmt_ctx_check)
+    if (threadIdx.x == 0) atomicOr(err, ERR_TOKEN);
+    id = 0;
+  }
+  const float* e = Wemb + (int64_t)id * E;
   for (int k = threadIdx.x; k < E; k += blockDim.x) store_split(X + (int64_t)j * 2 * Ep + k, Ep, e[k]);
 }
-void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, __nv_bfloat16* X, cudaStream_t st) {
-  k_enc_gather<<<Tx, 128, 0, st>>>(Wemb, src, Tx, E, Ep, X);
-  CK(cudaGetLastError());
+void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, int Vs, __nv_bfloat16* X, int* err,
+                cudaStream_t st) {
+  k_enc_gather<<<Tx, 128, 0, st>>>(Wemb, src, Tx, E, Ep, Vs, X, err);
+  CK_LAUNCH();
 }
 
 // E3/E4: persistent bidirectional GRU recurrence.  CTAs [0, NB) run the forward direction,
-// [NB, 2NB) the backward one; each CTA keeps its UPC units' slice of [U | Ux] (fp32) resident in
-// shared memory and the directions synchronise per time step through a global counter barrier.
+// [NB, 2NB) the backward one; each CTA keeps its UPC units' slice of [U | Ux] (fp32, rows of Hp)
+// resident in shared memory and the CTAs of a direction synchronise once per time step through a
+// release/acquire counter in global memory (cooperative launch guarantees co-residency).
 // Pin = x.[W|Wx] + [b|bx] for both directions (GEMM E2), layout [Tx][dir*3Hp + gate*Hp + j].
+constexpr int kRecurCPW = 6;  // max columns per warp (3*UPC <= 48 with 8 warps)
 __global__ void __launch_bounds__(256, 1) k_enc_recur(EncDev e, int Tx) {
-  extern __shared__ float sm[];
+  extern __shared__ float4 sm4[];
   const int NB = e.NB, UPC = e.UPC, H = e.H, Hp = e.Hp;
   const int dir = blockIdx.x / NB, cb = blockIdx.x % NB;
   const int u0 = cb * UPC;
   const int ncol = 3 * UPC;
-  float* W = sm;                 // [ncol][H]
-  float* hprev = W + ncol * H;   // [H]
-  float* dots = hprev + H;       // [ncol]
+  const int H4 = Hp / 4;
+  float4* W4 = sm4;                      // [ncol][Hp/4]
+  float4* h4 = W4 + (size_t)ncol * H4;   // [Hp/4]
+  float* hprev = reinterpret_cast<float*>(h4);
+  float* dots = reinterpret_cast<float*>(h4 + H4);  // [ncol]
   {
-    const float4* src = reinterpret_cast<const float4*>(e.Uarr + ((int64_t)(dir * NB + cb) * ncol) * H);
-    float4* dst = reinterpret_cast<float4*>(W);
-    for (int i = threadIdx.x; i < ncol * H / 4; i += blockDim.x) dst[i] = src[i];
+    const float4* src = reinterpret_cast<const float4*>(e.Uarr) + (size_t)(dir * NB + cb) * ncol * H4;
+    for (int i = threadIdx.x; i < ncol * H4; i += blockDim.x) W4[i] = src[i];
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  int* bar = e.bar + dir;
   for (int t = 0; t < Tx; ++t) {
     const int j = dir == 0 ? t : Tx - 1 - t;
     if (t == 0) {
-      for (int k = threadIdx.x; k < H; k += blockDim.x) hprev[k] = 0.f;
+      for (int k = threadIdx.x; k < H4; k += blockDim.x) h4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
-      const float* hb = e.hbuf + (dir * 2 + (t & 1)) * Hp;
-      for (int k = threadIdx.x; k < H; k += blockDim.x) hprev[k] = __ldcg(hb + k);
+      const float4* hb = reinterpret_cast<const float4*>(e.hbuf + (dir * 2 + (t & 1)) * Hp);
+      for (int k = threadIdx.x; k < H4; k += blockDim.x) h4[k] = __ldcg(hb + k);
     }
     __syncthreads();
-    for (int c = warp; c < ncol; c += nw) {
-      const float* wr = W + (int64_t)c * H;
-      float s = 0.f;
-      for (int k = lane; k < H; k += 32) s = fmaf(wr[k], hprev[k], s);
+    // dot products: warp w owns columns w, w+nw, ... (<= kRecurCPW), lanes split k as float4
+    float acc[kRecurCPW];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) dots[c] = s;
+    for (int q = 0; q < kRecurCPW; ++q) acc[q] = 0.f;
+#pragma unroll 2
+    for (int k = lane; k < H4; k += 32) {
+      const float4 h = h4[k];
+#pragma unroll
+      for (int q = 0; q < kRecurCPW; ++q) {
+        const int c = warp + q * nw;
+        if (c < ncol) {
+          const float4 w = W4[(size_t)c * H4 + k];
+          acc[q] = fmaf(w.x, h.x, fmaf(w.y, h.y, fmaf(w.z, h.z, fmaf(w.w, h.w, acc[q]))));
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kRecurCPW; ++q) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+      const int c = warp + q * nw;
+      if (lane == 0 && c < ncol) dots[c] = acc[q];
     }
     __syncthreads();
     if (threadIdx.x < UPC) {
@@ -676,23 +706,23 @@ __global__ void __launch_bounds__(256, 1) k_enc_recur(EncDev e, int Tx) {
         e.hbuf[(dir * 2 + ((t + 1) & 1)) * Hp + jj] = h;
       }
     }
-    // direction-wide barrier: all NB CTAs published h_t before anyone reads it
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(&e.bar[dir], 1);
-      const int target = NB * (t + 1);
-      volatile int* vb = e.bar + dir;
-      while (*vb < target) {
+    if (t + 1 < Tx) {  // direction-wide barrier: every CTA published h_t before anyone reads it
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(bar) : "memory");
+        const int target = NB * (t + 1);
+        int v;
+        do {
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
       }
-      __threadfence();
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
-size_t enc_recur_smem(int UPC, int H) { return (size_t)(3 * UPC * H + H + 3 * UPC) * sizeof(float); }
+size_t enc_recur_smem(int UPC, int Hp) { return (size_t)(3 * UPC * Hp + Hp + 3 * UPC + 4) * sizeof(float); }
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
-  const size_t smem = enc_recur_smem(e.UPC, e.H);
+  const size_t smem = enc_recur_smem(e.UPC, e.Hp);
   static size_t attr = 0;  // the attribute must cover the largest H seen in this process
   if (smem > attr) {
     CK(cudaFuncSetAttribute(k_enc_recur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -702,43 +732,65 @@ void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
   EncDev ee = e;
   void* args[] = {&ee, &Tx};
   CK(cudaLaunchCooperativeKernel((void*)k_enc_recur, dim3(2 * e.NB), dim3(256), args, smem, st));
+  note_launch();
 }
 
 // E5: s0 = tanh(mean_j ctx_j . W_init + b_init) -> arena slot 0; also the split copy of ctx for E7.
-__global__ void k_enc_init(EncDev e, int Tx, float* S0) {
-  extern __shared__ float mean[];  // [2H] real context indices
-  const int H = e.H, Hp = e.Hp, C = 2 * H;
-  for (int i = threadIdx.x; i < C; i += blockDim.x) {
-    const int ci = i < H ? i : Hp + i - H;
-    float s = 0.f;
-    for (int j = 0; j < Tx; ++j) s += e.ctx[(int64_t)j * 2 * Hp + ci];
-    mean[i] = s / (float)Tx;
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  __shared__ float red[8][32];
-  const int o = blockIdx.x * 32 + lane;
+// (a) column means + split copy, (b) K-split partial mat-vec, (c) ordered sum + tanh.
+__global__ void k_enc_mean(EncDev e, int Tx) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;  // padded context column
+  const int Hp = e.Hp, H = e.H;
+  if (c >= 2 * Hp) return;
   float s = 0.f;
-  if (o < H)
-    for (int k = warp; k < C; k += nw) s = fmaf(mean[k], e.W_init[(int64_t)k * H + o], s);
-  red[warp][lane] = s;
+  for (int j = 0; j < Tx; ++j) {
+    const float v = e.ctx[(int64_t)j * 2 * Hp + c];
+    s += v;
+    store_split(e.ctxbf + (int64_t)j * 4 * Hp + c, 2 * Hp, v);
+  }
+  const int real = c < Hp ? (c < H ? c : -1) : (c - Hp < H ? H + c - Hp : -1);
+  if (real >= 0) e.mean[real] = s / (float)Tx;
+}
+constexpr int kInitKS = 16;  // K splits of the s0 mat-vec
+__global__ void k_enc_s0_part(EncDev e) {
+  const int H = e.H, C = 2 * H;
+  const int o = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int kchunk = (C + kInitKS - 1) / kInitKS;
+  const int k0 = blockIdx.y * kchunk, k1 = min(C, k0 + kchunk);
+  __shared__ float red[8][32];
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if (o < H) {
+    int k = k0 + warp;
+    for (; k + 3 * nw < k1; k += 4 * nw) {
+      a0 = fmaf(e.mean[k], e.W_init[(int64_t)k * H + o], a0);
+      a1 = fmaf(e.mean[k + nw], e.W_init[(int64_t)(k + nw) * H + o], a1);
+      a2 = fmaf(e.mean[k + 2 * nw], e.W_init[(int64_t)(k + 2 * nw) * H + o], a2);
+      a3 = fmaf(e.mean[k + 3 * nw], e.W_init[(int64_t)(k + 3 * nw) * H + o], a3);
+    }
+    for (; k < k1; k += nw) a0 = fmaf(e.mean[k], e.W_init[(int64_t)k * H + o], a0);
+  }
+  red[warp][threadIdx.x & 31] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   if (warp == 0 && o < H) {
     float t = 0.f;
-    for (int w = 0; w < nw; ++w) t += red[w][lane];
-    S0[o] = tanhf(t + e.b_init[o]);
-  }
-  // split copy of ctx (rows < Tx) for the pctx GEMM
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)Tx * 2 * Hp;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = i / (2 * Hp), c = i % (2 * Hp);
-    store_split(e.ctxbf + j * 4 * Hp + c, 2 * Hp, e.ctx[i]);
+    for (int w = 0; w < nw; ++w) t += red[w][threadIdx.x];
+    e.s0part[blockIdx.y * H + o] = t;
   }
 }
+__global__ void k_enc_s0_final(EncDev e, float* S0) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= e.H) return;
+  float t = 0.f;
+  for (int ks = 0; ks < kInitKS; ++ks) t += e.s0part[ks * e.H + o];
+  S0[o] = tanhf(t + e.b_init[o]);
+}
 void enc_init(const EncDev& e, int Tx, float* S0, cudaStream_t st) {
-  const int grid = (e.H + 31) / 32;
-  k_enc_init<<<grid, 256, 2 * e.H * sizeof(float), st>>>(e, Tx, S0);
-  CK(cudaGetLastError());
+  k_enc_mean<<<(2 * e.Hp + 127) / 128, 128, 0, st>>>(e, Tx);
+  CK_LAUNCH();
+  k_enc_s0_part<<<dim3((e.H + 31) / 32, kInitKS), 256, 0, st>>>(e);
+  CK_LAUNCH();
+  k_enc_s0_final<<<(e.H + 127) / 128, 128, 0, st>>>(e, S0);
+  CK_LAUNCH();
 }
 
 }  // namespace nmt

@@ -73,13 +73,15 @@ struct AttnCtx {
 
 struct EncDev {
   int H, Hp, NB, UPC;
-  const float* Uarr;     // [2][NB][3*UPC][H] recurrent weights per CTA
+  const float* Uarr;     // [2][NB][3*UPC][Hp] recurrent weights per CTA (rows zero-padded to Hp)
   const float* Pin;      // [Tx][6Hp]
   float* ctx;            // [Tx][2Hp]
   float* hbuf;           // [2 dirs][2][Hp]
   int* bar;              // [2]
   const float* W_init;   // [2H][H]
   const float* b_init;   // [H]
+  float* mean;           // [2H] mean_j ctx_j (real indices)
+  float* s0part;         // [16][H] K-split partial sums
   __nv_bfloat16* ctxbf;  // [Tx][4Hp] hi | lo
 };
 
@@ -101,8 +103,9 @@ void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const floa
                 int* out_child32, long long* out_child64, int* out_argmax, cudaStream_t st);
 void full_row(const float* T, const float* Wo32, const float* bo, const float* logZ, int slot, int Ep, int V,
               float* out, cudaStream_t st);
-void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, __nv_bfloat16* X, cudaStream_t st);
-size_t enc_recur_smem(int UPC, int H);
+void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, int Vs, __nv_bfloat16* X, int* err,
+                cudaStream_t st);
+size_t enc_recur_smem(int UPC, int Hp);
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st);
 void enc_init(const EncDev& e, int Tx, float* S0, cudaStream_t st);
 

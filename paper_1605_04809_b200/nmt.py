@@ -24,8 +24,19 @@ STATUS = {0: "NMT_OK", 1: "NMT_ERR_INVALID_ARG", 2: "NMT_ERR_IO", 3: "NMT_ERR_FO
 EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "nmt_model_free", "nmt_encode",
            "nmt_root", "nmt_ctx_free", "nmt_score_batch", "nmt_score_batch_dev", "nmt_ctx_check", "nmt_ctx_stats",
            "nmt_inject_states", "nmt_logprobs_full", "nmt_debug_encoder", "nmt_debug_intermediates",
-           "nmt_test_gemm", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
+           "nmt_test_gemm", "nmt_encode_dev", "nmt_inject_states_dev", "nmt_launch_count", "nmt_profile",
+           "nmt_profile_read", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
            "nmt_ensemble_free"]
+
+
+N_STAGES = 19
+STAGES = ["plan", "gather", "gemm_h1", "gru1", "gemm_q", "attention", "gemm_g2", "gru2", "gemm_ro", "readout",
+          "vocab_gemm_lse", "finalize", "gather_dot", "enc_gather", "enc_gemm_in", "enc_recurrence", "enc_init",
+          "enc_pctx", "inject"]
+
+
+def launch_count() -> int:
+    return int(lib().nmt_launch_count())
 
 
 class NmtError(RuntimeError):
@@ -76,6 +87,11 @@ def lib() -> C.CDLL:
             "nmt_ensemble_get_unique_id": (i32, [vp]),
             "nmt_ensemble_combine": (i32, [vp, vp, i32, C.c_float, i32, i32, vp, vp]),
             "nmt_ensemble_free": (None, [vp]),
+            "nmt_encode_dev": (i32, [vp, vp, i32, C.POINTER(vp)]),
+            "nmt_inject_states_dev": (i32, [vp, i32, vp, vp, vp]),
+            "nmt_launch_count": (C.c_longlong, []),
+            "nmt_profile": (i32, [vp, i32]),
+            "nmt_profile_read": (i32, [vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -118,6 +134,19 @@ class Model:
     def encode(self, src_ids: Sequence[int]) -> "Context":
         return Context(self, src_ids)
 
+    def encode_dev(self, src_ptr: int, length: int) -> "Context":
+        """nmt_encode_dev: source ids already resident in device memory (int32)."""
+        return Context(self, None, dev=(src_ptr, length))
+
+    def profile(self, mode: int) -> None:
+        _check(lib().nmt_profile(self._h, mode))
+
+    def profile_read(self) -> Tuple[np.ndarray, np.ndarray]:
+        ms = np.zeros(N_STAGES, np.float64)
+        cnt = np.zeros(N_STAGES, np.int64)
+        _check(lib().nmt_profile_read(self._h, _ptr(ms), _ptr(cnt)))
+        return ms, cnt
+
     def close(self):
         if self._h:
             lib().nmt_model_free(self._h)
@@ -133,12 +162,16 @@ class Model:
 class Context:
     """nmt_encode: the source context and its state arena (root node = (s0, BOS))."""
 
-    def __init__(self, model: Model, src_ids: Sequence[int]):
+    def __init__(self, model: Model, src_ids: Optional[Sequence[int]], dev: Optional[Tuple[int, int]] = None):
         self.model = model
-        src = _c(src_ids, np.int32)
         self._h = C.c_void_p()
-        _check(lib().nmt_encode(model._h, _ptr(src), len(src), C.byref(self._h)))
-        self.Tx = len(src)
+        if dev is not None:
+            _check(lib().nmt_encode_dev(model._h, dev[0], dev[1], C.byref(self._h)))
+            self.Tx = dev[1]
+        else:
+            src = _c(src_ids, np.int32)
+            _check(lib().nmt_encode(model._h, _ptr(src), len(src), C.byref(self._h)))
+            self.Tx = len(src)
         self.root = int(lib().nmt_root(self._h))
 
     def score_batch(self, parents, cand_offsets, cand_words, with_argmax: bool = True
@@ -174,6 +207,9 @@ class Context:
         out = np.empty(len(y), np.int64)
         _check(lib().nmt_inject_states(self._h, len(y), _ptr(s), _ptr(y), _ptr(out)))
         return out
+
+    def inject_states_dev(self, n: int, s_ptr: int, y_ptr: int, out_ptr: int) -> None:
+        _check(lib().nmt_inject_states_dev(self._h, n, s_ptr, y_ptr, out_ptr))
 
     def logprobs_full(self, node: int) -> np.ndarray:
         out = np.empty(self.model.dims.vocab_tgt, np.float32)
