@@ -132,6 +132,7 @@ struct nmt_model {
   __nv_bfloat16* ctxbf = nullptr; // [Tpad][4Hp]
   float* hbuf = nullptr;
   float* enc_mean = nullptr;
+  float* ksplit_buf = nullptr;  // split-K partials of the encoder GEMMs
   float* enc_s0part = nullptr;
   int* bar = nullptr;
   int* d_src = nullptr;
@@ -182,7 +183,7 @@ struct nmt_model {
 
 static void free_all_model(nmt_model* m) {
   for (float** p : {&m->Wemb_src, &m->benc, &m->Uarr, &m->W_init, &m->b_init, &m->b_att, &m->U_att, &m->Ex, &m->b_nl,
-                    &m->bx_nl, &m->Eproj, &m->W_o32, &m->b_o, &m->Pin, &m->hbuf, &m->enc_mean, &m->enc_s0part})
+                    &m->bx_nl, &m->Eproj, &m->W_o32, &m->b_o, &m->Pin, &m->hbuf, &m->enc_mean, &m->enc_s0part, &m->ksplit_buf})
     dfree(*p);
   for (__nv_bfloat16** p : {&m->Wenc, &m->Watt, &m->W_h1, &m->W_q, &m->W_g2, &m->W_ro, &m->W_o, &m->Xsrc, &m->ctxbf})
     dfree(*p);
@@ -684,8 +685,9 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   m->Xsrc = dalloc<__nv_bfloat16>((size_t)m->Tpad * 2 * Ep);
   m->Pin = dalloc<float>((size_t)m->Tpad * 6 * Hp);
   m->ctxbf = dalloc<__nv_bfloat16>((size_t)m->Tpad * 4 * Hp);
-  m->hbuf = dalloc<float>(4 * Hp);
+  m->hbuf = dalloc<float>(8 * Hp);  // [2 dirs][2][Hp] 64-bit tagged words
   m->enc_mean = dalloc<float>(2 * H);
+  m->ksplit_buf = dalloc<float>(std::max((size_t)3 * m->Tpad * 6 * Hp, (size_t)8 * m->Tpad * Cp));
   m->enc_s0part = dalloc<float>(16 * H);
   m->bar = dalloc<int>(2);
   m->d_src = dalloc<int>(m->maxTx);
@@ -993,9 +995,12 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
       ProfScope p_(m, ST_ENC_GATHER);
       enc_gather(m->Wemb_src, d_src, len, m->E, m->Ep, m->Vs, m->Xsrc, c->counters + CNT_ERR, st);
     }
-    ProfScope p_(m, ST_ENC_GEMM);
-    gemm_store(m->tm_Xsrc, m->tm_Wenc, gemm_shape(len, nullptr, 6 * m->Hp, m->Ep, 0, true, m->Ep, m->Ep), m->Pin,
-               6 * m->Hp, m->benc, len, st);
+    ProfScope p_(m, ST_ENC_GEMM);  // small M: split K over the 3 precision passes to fill the SMs
+    GemmShape g = gemm_shape(len, nullptr, 6 * m->Hp, m->Ep, 0, true, m->Ep, m->Ep);
+    g.ksplit = 3;
+    const size_t stride = (size_t)m->Tpad * 6 * m->Hp;
+    gemm_store(m->tm_Xsrc, m->tm_Wenc, g, m->ksplit_buf, 6 * m->Hp, nullptr, len, st, stride);
+    splitk_reduce(m->ksplit_buf, 3, stride, len, 6 * m->Hp, 6 * m->Hp, m->benc, m->Pin, st);
   }
   EncDev e{};
   e.H = m->H;
@@ -1005,8 +1010,7 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
   e.Uarr = m->Uarr;
   e.Pin = m->Pin;
   e.ctx = c->ctx;
-  e.hbuf = m->hbuf;
-  e.bar = m->bar;
+  e.hx = reinterpret_cast<unsigned long long*>(m->hbuf);
   e.W_init = m->W_init;
   e.b_init = m->b_init;
   e.ctxbf = m->ctxbf;
@@ -1022,8 +1026,14 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
   }
   {  // E7: pctx = ctx.Wc_att + b_att
     ProfScope p_(m, ST_ENC_PCTX);
-    gemm_store(m->tm_ctxbf, m->tm_Watt, gemm_shape(len, nullptr, m->Cp, m->Cp, 0, true, m->Cp, m->Cp), c->pctx, m->Cp,
-               m->b_att, len, st);
+    GemmShape g = gemm_shape(len, nullptr, m->Cp, m->Cp, 0, true, m->Cp, m->Cp);
+    {  // ~8 splits, none empty
+      const int nkb = 3 * m->Cp / 64, chunk = (nkb + 7) / 8;
+      g.ksplit = (nkb + chunk - 1) / chunk;
+    }
+    const size_t stride = (size_t)m->Tpad * m->Cp;
+    gemm_store(m->tm_ctxbf, m->tm_Watt, g, m->ksplit_buf, m->Cp, nullptr, len, st, stride);
+    splitk_reduce(m->ksplit_buf, g.ksplit, stride, len, m->Cp, m->Cp, m->b_att, c->pctx, st);
   }
   // root node 0 = (s0, BOS): word -1, parent -1, src slot 0, not stepped
   static const int root[3] = {-1, -1, 0};

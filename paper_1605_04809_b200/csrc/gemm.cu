@@ -42,6 +42,13 @@ struct RegionK {
   int k0, k1;  // in units of BK blocks
 };
 
+struct TileCoord {
+  int m, n, s;
+};
+NMT_DEV TileCoord tile_of(int t, int num_m, int num_n) {
+  return TileCoord{t % num_m, (t / num_m) % num_n, t / (num_m * num_n)};
+}
+
 NMT_DEV RegionK region_of(const GemmShape& g, int n0) {
   int r = 0;
 #pragma unroll 1
@@ -69,7 +76,7 @@ __global__ void __launch_bounds__(192, 1)
   const int M = g.M_dev ? *g.M_dev : g.M;
   const int num_m = (M + BM - 1) / BM;
   const int num_n = g.N / BN;
-  const int total = num_m * num_n;
+  const int total = num_m * num_n * g.ksplit;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -95,20 +102,22 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int m = t % num_m, n = t / num_m;
-        const RegionK rk = region_of(g, n * BN);
-        for (int pass = 0; pass < g.passes; ++pass) {
+        const TileCoord tc = tile_of(t, num_m, num_n);
+        const RegionK rk = region_of(g, tc.n * BN);
+        const int nkbp = rk.k1 - rk.k0, nkb = g.passes * nkbp;
+        const int chunk = (nkb + g.ksplit - 1) / g.ksplit;
+        const int i1 = min(nkb, (tc.s + 1) * chunk);
+        for (int i = tc.s * chunk; i < i1; ++i) {
+          const int pass = i / nkbp, kb = rk.k0 + i % nkbp;
           const int aoff = g.a_col0 + (pass == 2 ? g.a_lo_off : 0);
           const int boff = (pass == 1 ? g.b_lo_off : 0);
-          for (int kb = rk.k0; kb < rk.k1; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES);
-            tma_load_2d(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, m * BM);
-            tma_load_2d(&tmB, &full[stage], sB + stage * S::B_BYTES, boff + kb * BK, n * BN);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES);
+          tma_load_2d(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, tc.m * BM);
+          tma_load_2d(&tmB, &full[stage], sB + stage * S::B_BYTES, boff + kb * BK, tc.n * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
@@ -120,14 +129,16 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-        const int n = t / num_m;
-        const RegionK rk = region_of(g, n * BN);
+        const TileCoord tc = tile_of(t, num_m, num_n);
+        const RegionK rk = region_of(g, tc.n * BN);
         const int acc = it & 1;
         const uint32_t aph = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
-        const int nkb = g.passes * (rk.k1 - rk.k0);
+        const int nkb_all = g.passes * (rk.k1 - rk.k0);
+        const int chunk = (nkb_all + g.ksplit - 1) / g.ksplit;
+        const int nkb = min(nkb_all, (tc.s + 1) * chunk) - tc.s * chunk;
         for (int i = 0; i < nkb; ++i) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -150,7 +161,8 @@ __global__ void __launch_bounds__(192, 1)
     const int row_in_tile = q * 32 + lane;
     int it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-      const int m = t % num_m, n = t / num_m;
+      const TileCoord tc = tile_of(t, num_m, num_n);
+      const int m = tc.m, n = tc.n;
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
@@ -159,7 +171,7 @@ __global__ void __launch_bounds__(192, 1)
       const bool valid = grow < M;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
       if constexpr (EPI == EPI_STORE) {
-        float* orow = ep.out + (size_t)grow * ep.ldc + n * BN;
+        float* orow = ep.out + (size_t)tc.s * ep.split_stride + (size_t)grow * ep.ldc + n * BN;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           float v[32];
@@ -263,7 +275,7 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& 
     CK(cudaFuncSetAttribute(k_gemm<BN, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
     attr_set = true;
   }
-  const int tiles = ((M_max + BM - 1) / BM) * (g.N / BN);
+  const int tiles = ((M_max + BM - 1) / BM) * (g.N / BN) * g.ksplit;
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
   if (grid <= 0) return;
   k_gemm<BN, STAGES, EPI><<<grid, 192, S::BYTES, st>>>(a, b, g, ep);
@@ -272,6 +284,12 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& 
 
 void gemm_validate(const GemmShape& g, int BN) {
   if (g.N % BN) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: N not a multiple of the N tile");
+  if (g.ksplit < 1) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: ksplit < 1");
+  for (int r = 0; r < g.nreg; ++r) {  // every split must own >= 1 k-block of every region
+    const int nkb = g.passes * (g.reg_k1[r] - g.reg_k0[r]) / BK;
+    const int chunk = (nkb + g.ksplit - 1) / g.ksplit;
+    if ((g.ksplit - 1) * chunk >= nkb) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: empty K split");
+  }
   for (int r = 0; r < g.nreg; ++r) {
     if (g.reg_k0[r] % BK || g.reg_k1[r] % BK || g.reg_k1[r] <= g.reg_k0[r])
       throw NmtError(NMT_ERR_INVALID_ARG, "gemm: bad K region");
@@ -281,12 +299,14 @@ void gemm_validate(const GemmShape& g, int BN) {
 
 // fp32 output GEMM; BN = 128 (more CTAs for the mid-size decoder GEMMs).
 void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc,
-                const float* bias, int M_max, cudaStream_t st) {
+                const float* bias, int M_max, cudaStream_t st, size_t split_stride) {
   gemm_validate(g, 128);
+  if (g.ksplit > 1 && (bias || !split_stride)) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: split-K partials take no bias");
   EpiParams ep{};
   ep.out = out;
   ep.ldc = ldc;
   ep.bias = bias;
+  ep.split_stride = split_stride;
   launch<128, 6, EPI_STORE>(a, b, g, ep, M_max, st);
 }
 

@@ -46,6 +46,7 @@ struct GemmShape {
   int reg_n_end[4];  // region r covers output columns [reg_n_end[r-1], reg_n_end[r])
   int reg_k0[4];     // K range [k0, k1) of region r (multiples of 64, relative to a_col0 / 0)
   int reg_k1[4];
+  int ksplit;        // split-K factor: split s writes its partial sum to out + s * split_stride
 };
 
 struct EpiParams {
@@ -55,11 +56,15 @@ struct EpiParams {
   float4* part;
   int n_valid;
   int n_tiles;
+  size_t split_stride;
 };
 
 CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc,
-                const float* bias, int M_max, cudaStream_t st);
+                const float* bias, int M_max, cudaStream_t st, size_t split_stride = 0);
+// out[r][c] = bias[c] + sum_s part[s * stride + r * ldc + c]  (fixed order: deterministic)
+void splitk_reduce(const float* part, int ksplit, size_t stride, int M, int N, int ldc, const float* bias, float* out,
+                   cudaStream_t st);
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
               cudaStream_t st);
 
@@ -77,6 +82,7 @@ inline GemmShape gemm_shape(int M, const int* M_dev, int N, int K, int a_col0, b
   g.reg_n_end[0] = N;
   g.reg_k0[0] = 0;
   g.reg_k1[0] = K;
+  g.ksplit = 1;
   return g;
 }
 

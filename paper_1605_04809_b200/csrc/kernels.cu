@@ -77,6 +77,24 @@ void transpose_f32(const float* src, int K, int N, float* dst, int ld_dst, cudaS
   CK_LAUNCH();
 }
 
+// split-K partial sums -> output (+bias), in fixed split order
+__global__ void k_splitk_reduce(const float* __restrict__ part, int ksplit, size_t stride, int M, int N, int ldc,
+                                const float* __restrict__ bias, float* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)M * N) return;
+  const int r = (int)(i / N), c = (int)(i % N);
+  float s = bias ? bias[c] : 0.f;
+  for (int k = 0; k < ksplit; ++k) s += part[k * stride + (size_t)r * ldc + c];
+  out[(size_t)r * ldc + c] = s;
+}
+void splitk_reduce(const float* part, int ksplit, size_t stride, int M, int N, int ldc, const float* bias, float* out,
+                   cudaStream_t st) {
+  const int64_t n = (int64_t)M * N;
+  if (n <= 0) return;
+  k_splitk_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, ksplit, stride, M, N, ldc, bias, out);
+  CK_LAUNCH();
+}
+
 // ===================================================================================== planner
 // Device-side state cache (SURVEY §8(a) D0; PAPER.md:109 "collapsed edges", :121 "Cache state
 // pointers and probabilities at target nodes").  Keys (parent, word) -> child id in an open-
@@ -639,116 +657,156 @@ void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, int Vs
 }
 
 // E3/E4: persistent bidirectional GRU recurrence.  CTAs [0, NB) run the forward direction,
-// [NB, 2NB) the backward one; each CTA keeps its UPC units' slice of [U | Ux] (fp32, rows of Hp)
-// resident in shared memory and the CTAs of a direction synchronise once per time step through a
-// release/acquire counter in global memory (cooperative launch guarantees co-residency).
+// [NB, 2NB) the backward one (both fill the 148 SMs).  Each CTA owns UPC hidden units; the
+// 3*UPC columns of [U | Ux] it needs live in REGISTERS for the whole sentence (warp w owns
+// columns w, w+12, w+24, w+36; lane l holds the float4s k = l + 32 i of each), so a time step
+// reads no weights at all.  h_t is exchanged through global memory as 64-bit (value, tag = t+1)
+// words: a reader polls until every word carries the tag of the step it needs, which merges the
+// grid-wide barrier into the data read (one L2 round trip per step).  Double-buffered by parity:
+// a writer can be at most one step ahead of the slowest reader.
 // Pin = x.[W|Wx] + [b|bx] for both directions (GEMM E2), layout [Tx][dir*3Hp + gate*Hp + j].
-constexpr int kRecurCPW = 6;  // max columns per warp (3*UPC <= 48 with 8 warps)
-__global__ void __launch_bounds__(256, 1) k_enc_recur(EncDev e, int Tx) {
-  extern __shared__ float4 sm4[];
-  const int NB = e.NB, UPC = e.UPC, H = e.H, Hp = e.Hp;
+constexpr int kRecurThreads = 384, kRecurWarps = 12, kRecurCPW = 4;
+template <int KI>  // Hp = 128 * KI
+__global__ void __launch_bounds__(kRecurThreads, 1) k_enc_recur(EncDev e, int Tx) {
+  constexpr int Hp = 128 * KI, H4 = Hp / 4;
+  __shared__ float4 h4[H4];
+  __shared__ float dots[3 * 16];
+  const int NB = e.NB, UPC = e.UPC, H = e.H;
   const int dir = blockIdx.x / NB, cb = blockIdx.x % NB;
   const int u0 = cb * UPC;
   const int ncol = 3 * UPC;
-  const int H4 = Hp / 4;
-  float4* W4 = sm4;                      // [ncol][Hp/4]
-  float4* h4 = W4 + (size_t)ncol * H4;   // [Hp/4]
-  float* hprev = reinterpret_cast<float*>(h4);
-  float* dots = reinterpret_cast<float*>(h4 + H4);  // [ncol]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4 w[kRecurCPW][KI];
   {
     const float4* src = reinterpret_cast<const float4*>(e.Uarr) + (size_t)(dir * NB + cb) * ncol * H4;
-    for (int i = threadIdx.x; i < ncol * H4; i += blockDim.x) W4[i] = src[i];
+#pragma unroll
+    for (int q = 0; q < kRecurCPW; ++q) {
+      const int c = warp + q * kRecurWarps;
+#pragma unroll
+      for (int i = 0; i < KI; ++i)
+        w[q][i] = c < ncol ? src[(size_t)c * H4 + lane + 32 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  int* bar = e.bar + dir;
+  unsigned long long* hx = e.hx + (size_t)dir * 2 * Hp;  // [2][Hp] tagged words of this direction
+  const bool gate = threadIdx.x < UPC && u0 + (int)threadIdx.x < H;
+  const int jj = u0 + threadIdx.x;
+  float hself = 0.f;
   for (int t = 0; t < Tx; ++t) {
     const int j = dir == 0 ? t : Tx - 1 - t;
+    float p_r = 0.f, p_u = 0.f, p_x = 0.f;
+    if (gate) {  // input projections of this step (independent of h): issue early
+      const float* pin = e.Pin + (int64_t)j * 6 * Hp + dir * 3 * Hp;
+      p_r = pin[jj];
+      p_u = pin[Hp + jj];
+      p_x = pin[2 * Hp + jj];
+    }
     if (t == 0) {
-      for (int k = threadIdx.x; k < H4; k += blockDim.x) h4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k = threadIdx.x; k < H4; k += kRecurThreads) h4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
-      const float4* hb = reinterpret_cast<const float4*>(e.hbuf + (dir * 2 + (t & 1)) * Hp);
-      for (int k = threadIdx.x; k < H4; k += blockDim.x) h4[k] = __ldcg(hb + k);
+      const unsigned long long* src = hx + (size_t)(t & 1) * Hp;
+      const unsigned tag = (unsigned)t;  // h_{t-1} was written with tag (t-1)+1
+      for (int k = threadIdx.x; k < H4; k += kRecurThreads) {
+        if (4 * k >= H) {  // padded units (H < Hp) are never written: they stay 0
+          h4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          continue;
+        }
+        // units >= H inside this float4 carry no tag: accept them as 0
+        const unsigned need = (4 * k + 3 < H) ? 0xFu : ((1u << (H - 4 * k)) - 1u);
+        unsigned long long a, b, c, d;
+        const long long t0 = clock64();
+        while (true) {
+          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(src + 4 * k) : "memory");
+          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(c), "=l"(d) : "l"(src + 4 * k + 2) : "memory");
+          const unsigned ok = ((unsigned)(a >> 32) == tag) | (((unsigned)(b >> 32) == tag) << 1) |
+                              (((unsigned)(c >> 32) == tag) << 2) | (((unsigned)(d >> 32) == tag) << 3);
+          if ((ok & need) == need) break;
+          if (clock64() - t0 > (1ll << 32)) asm volatile("trap;");  // watchdog (~2 s): fail, never hang
+        }
+        h4[k] = make_float4((need & 1) ? __uint_as_float((unsigned)a) : 0.f, (need & 2) ? __uint_as_float((unsigned)b) : 0.f,
+                            (need & 4) ? __uint_as_float((unsigned)c) : 0.f, (need & 8) ? __uint_as_float((unsigned)d) : 0.f);
+      }
     }
     __syncthreads();
-    // dot products: warp w owns columns w, w+nw, ... (<= kRecurCPW), lanes split k as float4
     float acc[kRecurCPW];
 #pragma unroll
     for (int q = 0; q < kRecurCPW; ++q) acc[q] = 0.f;
-#pragma unroll 2
-    for (int k = lane; k < H4; k += 32) {
-      const float4 h = h4[k];
 #pragma unroll
-      for (int q = 0; q < kRecurCPW; ++q) {
-        const int c = warp + q * nw;
-        if (c < ncol) {
-          const float4 w = W4[(size_t)c * H4 + k];
-          acc[q] = fmaf(w.x, h.x, fmaf(w.y, h.y, fmaf(w.z, h.z, fmaf(w.w, h.w, acc[q]))));
-        }
-      }
+    for (int i = 0; i < KI; ++i) {
+      const float4 h = h4[lane + 32 * i];
+#pragma unroll
+      for (int q = 0; q < kRecurCPW; ++q)
+        acc[q] = fmaf(w[q][i].x, h.x, fmaf(w[q][i].y, h.y, fmaf(w[q][i].z, h.z, fmaf(w[q][i].w, h.w, acc[q]))));
     }
 #pragma unroll
     for (int q = 0; q < kRecurCPW; ++q) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
-      const int c = warp + q * nw;
+      const int c = warp + q * kRecurWarps;
       if (lane == 0 && c < ncol) dots[c] = acc[q];
     }
     __syncthreads();
-    if (threadIdx.x < UPC) {
-      const int u = threadIdx.x, jj = u0 + u;
-      if (jj < H) {
-        const float* pin = e.Pin + (int64_t)j * 6 * Hp + dir * 3 * Hp;
-        const float rg = 1.f / (1.f + expf(-(pin[jj] + dots[u])));
-        const float ug = 1.f / (1.f + expf(-(pin[Hp + jj] + dots[UPC + u])));
-        const float ht = tanhf(rg * dots[2 * UPC + u] + pin[2 * Hp + jj]);
-        const float h = ug * hprev[jj] + (1.f - ug) * ht;
-        e.ctx[(int64_t)j * 2 * Hp + dir * Hp + jj] = h;
-        e.hbuf[(dir * 2 + ((t + 1) & 1)) * Hp + jj] = h;
-      }
-    }
-    if (t + 1 < Tx) {  // direction-wide barrier: every CTA published h_t before anyone reads it
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(bar) : "memory");
-        const int target = NB * (t + 1);
-        int v;
-        do {
-          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-        } while (v < target);
-      }
-      __syncthreads();
+    if (gate) {
+      const int u = threadIdx.x;
+      const float rg = 1.f / (1.f + expf(-(p_r + dots[u])));
+      const float ug = 1.f / (1.f + expf(-(p_u + dots[UPC + u])));
+      const float ht = tanhf(rg * dots[2 * UPC + u] + p_x);
+      hself = ug * hself + (1.f - ug) * ht;
+      e.ctx[(int64_t)j * 2 * Hp + dir * Hp + jj] = hself;
+      const unsigned long long word = ((unsigned long long)(unsigned)(t + 1) << 32) | __float_as_uint(hself);
+      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(hx + (size_t)((t + 1) & 1) * Hp + jj), "l"(word)
+                   : "memory");
     }
   }
 }
-size_t enc_recur_smem(int UPC, int Hp) { return (size_t)(3 * UPC * Hp + Hp + 3 * UPC + 4) * sizeof(float); }
-void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
-  const size_t smem = enc_recur_smem(e.UPC, e.Hp);
-  static size_t attr = 0;  // the attribute must cover the largest H seen in this process
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_enc_recur, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
-  CK(cudaMemsetAsync(e.bar, 0, 2 * sizeof(int), st));
+
+template <int KI>
+static void launch_recur(const EncDev& e, int Tx, cudaStream_t st) {
   EncDev ee = e;
   void* args[] = {&ee, &Tx};
-  CK(cudaLaunchCooperativeKernel((void*)k_enc_recur, dim3(2 * e.NB), dim3(256), args, smem, st));
+  CK(cudaLaunchCooperativeKernel((void*)k_enc_recur<KI>, dim3(2 * e.NB), dim3(kRecurThreads), args, 0, st));
   note_launch();
+}
+void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
+  if (3 * e.UPC > kRecurWarps * kRecurCPW || 3 * e.UPC > 48) throw NmtError(NMT_ERR_SHAPE, "encoder: UPC too large");
+  // tags of both directions and parities start at 0 (never a valid tag)
+  CK(cudaMemsetAsync(e.hx, 0, (size_t)2 * 2 * e.Hp * sizeof(unsigned long long), st));
+  switch (e.Hp / 128) {
+    case 1: launch_recur<1>(e, Tx, st); break;
+    case 2: launch_recur<2>(e, Tx, st); break;
+    case 3: launch_recur<3>(e, Tx, st); break;
+    case 4: launch_recur<4>(e, Tx, st); break;
+    case 5: launch_recur<5>(e, Tx, st); break;
+    case 6: launch_recur<6>(e, Tx, st); break;
+    case 7: launch_recur<7>(e, Tx, st); break;
+    case 8: launch_recur<8>(e, Tx, st); break;
+    default: throw NmtError(NMT_ERR_SHAPE, "encoder: dim_hid > 1024");
+  }
 }
 
 // E5: s0 = tanh(mean_j ctx_j . W_init + b_init) -> arena slot 0; also the split copy of ctx for E7.
 // (a) column means + split copy, (b) K-split partial mat-vec, (c) ordered sum + tanh.
 __global__ void k_enc_mean(EncDev e, int Tx) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;  // padded context column
+  __shared__ float red[8][33];
   const int Hp = e.Hp, H = e.H;
-  if (c >= 2 * Hp) return;
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);  // padded context column
+  const int jl = threadIdx.x >> 5;                      // 8 row lanes
   float s = 0.f;
-  for (int j = 0; j < Tx; ++j) {
-    const float v = e.ctx[(int64_t)j * 2 * Hp + c];
-    s += v;
-    store_split(e.ctxbf + (int64_t)j * 4 * Hp + c, 2 * Hp, v);
+  if (c < 2 * Hp) {
+#pragma unroll 4
+    for (int j = jl; j < Tx; j += 8) {
+      const float v = e.ctx[(int64_t)j * 2 * Hp + c];
+      s += v;
+      store_split(e.ctxbf + (int64_t)j * 4 * Hp + c, 2 * Hp, v);
+    }
   }
-  const int real = c < Hp ? (c < H ? c : -1) : (c - Hp < H ? H + c - Hp : -1);
-  if (real >= 0) e.mean[real] = s / (float)Tx;
+  red[jl][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (jl == 0 && c < 2 * Hp) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x];
+    const int real = c < Hp ? (c < H ? c : -1) : (c - Hp < H ? H + c - Hp : -1);
+    if (real >= 0) e.mean[real] = t / (float)Tx;
+  }
 }
 constexpr int kInitKS = 16;  // K splits of the s0 mat-vec
 __global__ void k_enc_s0_part(EncDev e) {
@@ -785,7 +843,7 @@ __global__ void k_enc_s0_final(EncDev e, float* S0) {
   S0[o] = tanhf(t + e.b_init[o]);
 }
 void enc_init(const EncDev& e, int Tx, float* S0, cudaStream_t st) {
-  k_enc_mean<<<(2 * e.Hp + 127) / 128, 128, 0, st>>>(e, Tx);
+  k_enc_mean<<<(2 * e.Hp + 31) / 32, 256, 0, st>>>(e, Tx);
   CK_LAUNCH();
   k_enc_s0_part<<<dim3((e.H + 31) / 32, kInitKS), 256, 0, st>>>(e);
   CK_LAUNCH();

@@ -76,8 +76,7 @@ struct EncDev {
   const float* Uarr;     // [2][NB][3*UPC][Hp] recurrent weights per CTA (rows zero-padded to Hp)
   const float* Pin;      // [Tx][6Hp]
   float* ctx;            // [Tx][2Hp]
-  float* hbuf;           // [2 dirs][2][Hp]
-  int* bar;              // [2]
+  unsigned long long* hx;  // [2 dirs][2 parities][Hp] (tag << 32 | float bits)
   const float* W_init;   // [2H][H]
   const float* b_init;   // [H]
   float* mean;           // [2H] mean_j ctx_j (real indices)
@@ -105,7 +104,6 @@ void full_row(const float* T, const float* Wo32, const float* bo, const float* l
               float* out, cudaStream_t st);
 void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, int Vs, __nv_bfloat16* X, int* err,
                 cudaStream_t st);
-size_t enc_recur_smem(int UPC, int Hp);
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st);
 void enc_init(const EncDev& e, int Tx, float* S0, cudaStream_t st);
 

@@ -1,0 +1,45 @@
+"""Summarise an ncu launch list (gpu__time_duration.sum per launch) of bench.py into per-step shares.
+The list is cold-cache and serialised: compare SHARES of the step, not absolute times."""
+import csv
+import json
+import re
+import sys
+from collections import OrderedDict
+
+
+def short(name: str) -> str:
+    m = re.search(r"nmt::(k_\w+)(<[^>]*>)?", name)
+    if not m:
+        return "torch:" + re.sub(r"\(.*", "", name)[-40:]
+    base = m.group(1)
+    if base == "k_gemm":
+        base += m.group(2).replace("(int)", "")
+    return base
+
+
+def main(path: str, out_json: str) -> None:
+    lines = [ln for ln in open(path) if ln.startswith('"')]  # drop ==PROF== / ==WARNING== lines
+    rows = list(csv.DictReader(lines))
+    launches = [(short(r["Kernel Name"]), float(r["Metric Value"]) / 1000.0) for r in rows
+                if r["Metric Name"] == "gpu__time_duration.sum"]
+    # a step starts at k_enc_gather; keep the last complete step
+    starts = [i for i, (n, _) in enumerate(launches) if n == "k_enc_gather"]
+    i0 = starts[-2] if len(starts) >= 2 else starts[-1]
+    i1 = starts[-1] if len(starts) >= 2 else len(launches)
+    step = [x for x in launches[i0:i1] if not x[0].startswith("torch:")]
+    tot = sum(t for _, t in step)
+    agg = OrderedDict()
+    for n, t in step:
+        agg.setdefault(n, [0.0, 0])
+        agg[n][0] += t
+        agg[n][1] += 1
+    table = [{"kernel": n, "launches": c, "us": round(t, 2), "share": round(t / tot, 4)} for n, (t, c) in agg.items()]
+    res = {"source": path, "step_kernels": len(step), "step_us_serialised": round(tot, 1), "table": table}
+    json.dump(res, open(out_json, "w"), indent=1)
+    for r in sorted(table, key=lambda r: -r["us"]):
+        print(f'{r["kernel"]:34s} {r["launches"]:3d} {r["us"]:9.2f} us  {100 * r["share"]:5.1f} %')
+    print(f"step: {len(step)} launches, {tot:.1f} us serialised")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2])
