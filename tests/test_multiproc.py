@@ -1,0 +1,54 @@
+"""World-size-2 gloo checks (CPU) of the multi-GPU host logic of bench.py: sentence sharding gives
+disjoint per-rank inputs (weak scaling, no data-path collective) and the job time is the max over
+ranks while the word-score count is the sum (bench.py reduce_max / reduce_sum)."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    import synth
+    t = bench.reduce_max(1.0 + rank, dist)
+    n = bench.reduce_sum(100.0 * (rank + 1), dist)
+    src = synth.make_source(50000, 49, seed=bench.shard_seed(rank, 0))
+    q.put((rank, t, n, src.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_reductions_and_sharding_gloo():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(r[1] == 2.0 for r in res)          # max over ranks
+    assert all(r[2] == 300.0 for r in res)        # total work over ranks
+    assert res[0][3] != res[1][3]                 # each rank scores its own sentences
+
+
+def test_shard_seeds_disjoint():
+    import bench
+    seeds = {bench.shard_seed(r, s) for r in range(8) for s in range(1000)}
+    assert len(seeds) == 8000
