@@ -271,7 +271,7 @@ void nmt_model::ensure_ws(int R, int NC) {
   G2 = dalloc<float>((size_t)R_cap * 4 * Hp);
   RO_buf = dalloc<float>((size_t)R_cap * ROp);
   A_t = dalloc<__nv_bfloat16>((size_t)R_cap * sf * Ep);
-  part = dalloc<float4>((size_t)R_cap * (Vp / 256));
+  part = dalloc<float4>((size_t)R_cap * 2 * (Vp / 256));
   row_src = dalloc<int>(R_cap);
   row_y = dalloc<int>(R_cap);
   row_dst = dalloc<int>(R_cap);

@@ -30,6 +30,8 @@ namespace nmt {
 
 constexpr int BM = 128, BK = 64;
 constexpr int EPI_STORE = 0, EPI_LSE = 1;
+constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant, each owning half of the tile's columns
+constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
 template <int BN, int STAGES>
 struct GemmSmem {
@@ -57,7 +59,7 @@ NMT_DEV RegionK region_of(const GemmShape& g, int n0) {
 }
 
 template <int BN, int STAGES, int EPI>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmShape g,
            EpiParams ep) {
   using S = GemmSmem<BN, STAGES>;
@@ -73,10 +75,6 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int M = g.M_dev ? *g.M_dev : g.M;
-  const int num_m = (M + BM - 1) / BM;
-  const int num_n = g.N / BN;
-  const int total = num_m * num_n * g.ksplit;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -87,7 +85,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], EPI_WARPS);
     }
     fence_barrier_init();
   }
@@ -96,6 +94,11 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_enter();  // prologue above overlaps the previous kernel; inputs (and M_dev) are read below
+  const int M = g.M_dev ? *g.M_dev : g.M;
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = g.N / BN;
+  const int total = num_m * num_n * g.ksplit;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -156,8 +159,10 @@ __global__ void __launch_bounds__(192, 1)
         mma_commit(&tfull[acc]);
       }
     }
-  } else {  // ---------------- epilogue warps 2..5
-    const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
+  } else {  // ---------------- epilogue warps 2..9
+    const int q = warp & 3;               // TMEM lane quadrant accessible to this warp
+    const int half = (warp - 2) >> 2;     // which half of the tile's columns
+    constexpr int COLS = BN / 2;
     const int row_in_tile = q * 32 + lane;
     int it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
@@ -169,55 +174,83 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const int grow = m * BM + row_in_tile;
       const bool valid = grow < M;
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + half * COLS;
+      const int colbase = n * BN + half * COLS;
       if constexpr (EPI == EPI_STORE) {
-        float* orow = ep.out + (size_t)tc.s * ep.split_stride + (size_t)grow * ep.ldc + n * BN;
+        float* orow = ep.out + (size_t)tc.s * ep.split_stride + (size_t)grow * ep.ldc + colbase;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          float v[32];
-          tmem_ld32(tbase + c * 32, v);
+        for (int c = 0; c < COLS; c += 64) {
+          float v[64];
+          tmem_ld32_nowait(tbase + c, v);
+          tmem_ld32_nowait(tbase + c + 32, v + 32);
+          tmem_wait_ld_dep(v);
+          reg_dep32(v + 32);
           if (valid) {
             if (ep.bias) {
-              const float* b = ep.bias + n * BN + c * 32;
+              const float4* b = reinterpret_cast<const float4*>(ep.bias + colbase + c);
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] += __ldg(b + j);
+              for (int j = 0; j < 16; ++j) {
+                const float4 bb = __ldg(b + j);
+                v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
+              }
             }
-            float4* o = reinterpret_cast<float4*>(orow + c * 32);
+            float4* o = reinterpret_cast<float4*>(orow + c);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            for (int j = 0; j < 16; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
         }
-      } else {  // EPI_LSE: online (max, sum exp, argmax) over this tile's BN logits of the row
+      } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
         constexpr float LOG2E = 1.4426950408889634f;
-        float mx = -INFINITY, sm = 0.f;
+        float mx = -INFINITY, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
         int am = 0;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          float v[32];
-          tmem_ld32(tbase + c * 32, v);
-          const int col0 = n * BN + c * 32;
-          float cm = -INFINITY;
-          int ci = 0;
+        for (int c = 0; c < COLS; c += 64) {
+          float v[64];
+          tmem_ld32_nowait(tbase + c, v);
+          tmem_ld32_nowait(tbase + c + 32, v + 32);
+          tmem_wait_ld_dep(v);
+          reg_dep32(v + 32);
+          const int col0 = colbase + c;
+          if (col0 + 64 > ep.n_valid) {  // padded vocabulary columns (last tile only)
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (col0 + j >= ep.n_valid) v[j] = -INFINITY;
-            if (v[j] > cm) {
-              cm = v[j];
-              ci = j;
-            }
+            for (int j = 0; j < 64; ++j)
+              if (col0 + j >= ep.n_valid) v[j] = -INFINITY;
           }
-          if (cm > mx) {  // strict: earlier (lower id) wins ties
-            sm = sm * ex2_approx((mx - cm) * LOG2E);
+          float t32[32];  // tree max
+#pragma unroll
+          for (int j = 0; j < 32; ++j) t32[j] = fmaxf(v[j], v[j + 32]);
+#pragma unroll
+          for (int w = 16; w > 0; w >>= 1)
+#pragma unroll
+            for (int j = 0; j < w; ++j) t32[j] = fmaxf(t32[j], t32[j + w]);
+          const float cm = t32[0];
+          if (cm > mx) {  // new running max: first (lowest) index of it in this chunk; rescale the sums
+            int ix[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ix[j] = v[j] == cm ? j : (v[j + 32] == cm ? j + 32 : 64);
+#pragma unroll
+            for (int w = 16; w > 0; w >>= 1)
+#pragma unroll
+              for (int j = 0; j < w; ++j) ix[j] = min(ix[j], ix[j + w]);
+            const float f = ex2_approx((mx - cm) * LOG2E);
+            s0 *= f; s1 *= f; s2 *= f; s3 *= f;
             mx = cm;
-            am = col0 + ci;
+            am = col0 + ix[0];
           }
-          if (cm > -INFINITY) {
+          if (mx > -INFINITY) {
             const float mb = mx * LOG2E;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) sm += ex2_approx(fmaf(v[j], LOG2E, -mb));
+            for (int j = 0; j < 64; j += 4) {
+              s0 += ex2_approx(fmaf(v[j], LOG2E, -mb));
+              s1 += ex2_approx(fmaf(v[j + 1], LOG2E, -mb));
+              s2 += ex2_approx(fmaf(v[j + 2], LOG2E, -mb));
+              s3 += ex2_approx(fmaf(v[j + 3], LOG2E, -mb));
+            }
           }
         }
-        if (valid) ep.part[(size_t)grow * ep.n_tiles + n] = make_float4(mx, sm, __int_as_float(am), 0.f);
+        if (valid)
+          ep.part[((size_t)grow * ep.n_tiles + n) * 2 + half] =
+              make_float4(mx, (s0 + s1) + (s2 + s3), __int_as_float(am), 0.f);
       }
       tc_fence_before();
       __syncwarp();
@@ -278,7 +311,7 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& 
   const int tiles = ((M_max + BM - 1) / BM) * (g.N / BN) * g.ksplit;
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
   if (grid <= 0) return;
-  k_gemm<BN, STAGES, EPI><<<grid, 192, S::BYTES, st>>>(a, b, g, ep);
+  launch_pdl(k_gemm<BN, STAGES, EPI>, grid, GEMM_THREADS, S::BYTES, st, a, b, g, ep);
   CK_LAUNCH();
 }
 

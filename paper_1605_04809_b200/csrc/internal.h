@@ -33,6 +33,23 @@ void note_launch();
     CK(cudaGetLastError());    \
   } while (0)
 
+// Launch with the programmatic-stream-serialization attribute (PDL): the kernel may start while the
+// previous kernel of the stream drains; every kernel calls pdl_wait() before touching its inputs.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 // --------------------------------------------------------------------------- GEMM engine
 struct GemmShape {
   int M;             // rows (if M_dev == nullptr)
@@ -64,7 +81,7 @@ void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, 
                 const float* bias, int M_max, cudaStream_t st, size_t split_stride = 0);
 // out[r][c] = bias[c] + sum_s part[s * stride + r * ldc + c]  (fixed order: deterministic)
 void splitk_reduce(const float* part, int ksplit, size_t stride, int M, int N, int ldc, const float* bias, float* out,
-                   cudaStream_t st);
+                   cudaStream_t st, __nv_bfloat16* out16 = nullptr);
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
               cudaStream_t st);
 

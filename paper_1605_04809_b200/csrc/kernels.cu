@@ -32,6 +32,7 @@ NMT_DEV void store_split(__nv_bfloat16* hi_ptr, int lo_off, float x) {
 // into an N x K K-major bf16 operand; lo half at +lo_off columns if lo_off > 0)
 __global__ void k_pack_T(const float* __restrict__ src, int ld_src, int K, int N, __nv_bfloat16* dst, int ld_dst,
                          int row0, int col0, int rmap, int kmap, int H, int Hp, int lo_off) {
+  pdl_enter();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)K * N) return;
   const int k = (int)(idx / N), n = (int)(idx % N);
@@ -43,7 +44,7 @@ void pack_T(const float* src, int ld_src, int K, int N, __nv_bfloat16* dst, int 
             int kmap, int H, int Hp, int lo_off, cudaStream_t st) {
   const int64_t n = (int64_t)K * N;
   if (!n) return;
-  k_pack_T<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, ld_src, K, N, dst, ld_dst, row0, col0, rmap, kmap, H, Hp,
+  launch_pdl(k_pack_T, (unsigned)((n + 255) / 256), 256, 0, st, src, ld_src, K, N, dst, ld_dst, row0, col0, rmap, kmap, H, Hp,
                                                         lo_off);
   CK_LAUNCH();
 }
@@ -51,6 +52,7 @@ void pack_T(const float* src, int ld_src, int K, int N, __nv_bfloat16* dst, int 
 // dst[r][col0 + k] = split(src[r * ld_src + k]) for r < rows, k < K (row-major copy)
 __global__ void k_pack_rows(const float* __restrict__ src, int ld_src, int rows, int K, __nv_bfloat16* dst,
                             int ld_dst, int col0, int lo_off) {
+  pdl_enter();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)rows * K) return;
   const int r = (int)(idx / K), k = (int)(idx % K);
@@ -60,12 +62,13 @@ void pack_rows(const float* src, int ld_src, int rows, int K, __nv_bfloat16* dst
                cudaStream_t st) {
   const int64_t n = (int64_t)rows * K;
   if (!n) return;
-  k_pack_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, ld_src, rows, K, dst, ld_dst, col0, lo_off);
+  launch_pdl(k_pack_rows, (unsigned)((n + 255) / 256), 256, 0, st, src, ld_src, rows, K, dst, ld_dst, col0, lo_off);
   CK_LAUNCH();
 }
 
 // fp32 [K x N] -> fp32 [N x ld_dst] transposed (W_o columns as contiguous per-word rows)
 __global__ void k_transpose_f32(const float* __restrict__ src, int K, int N, float* dst, int ld_dst) {
+  pdl_enter();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)K * N) return;
   const int k = (int)(idx / N), n = (int)(idx % N);
@@ -73,25 +76,27 @@ __global__ void k_transpose_f32(const float* __restrict__ src, int K, int N, flo
 }
 void transpose_f32(const float* src, int K, int N, float* dst, int ld_dst, cudaStream_t st) {
   const int64_t n = (int64_t)K * N;
-  k_transpose_f32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(src, K, N, dst, ld_dst);
+  launch_pdl(k_transpose_f32, (unsigned)((n + 255) / 256), 256, 0, st, src, K, N, dst, ld_dst);
   CK_LAUNCH();
 }
 
 // split-K partial sums -> output (+bias), in fixed split order
 __global__ void k_splitk_reduce(const float* __restrict__ part, int ksplit, size_t stride, int M, int N, int ldc,
-                                const float* __restrict__ bias, float* out) {
+                                const float* __restrict__ bias, float* out, __nv_bfloat16* out16) {
+  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)M * N) return;
   const int r = (int)(i / N), c = (int)(i % N);
   float s = bias ? bias[c] : 0.f;
   for (int k = 0; k < ksplit; ++k) s += part[k * stride + (size_t)r * ldc + c];
   out[(size_t)r * ldc + c] = s;
+  if (out16) out16[(size_t)r * ldc + c] = __float2bfloat16_rn(s);
 }
 void splitk_reduce(const float* part, int ksplit, size_t stride, int M, int N, int ldc, const float* bias, float* out,
-                   cudaStream_t st) {
+                   cudaStream_t st, __nv_bfloat16* out16) {
   const int64_t n = (int64_t)M * N;
   if (n <= 0) return;
-  k_splitk_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, ksplit, stride, M, N, ldc, bias, out);
+  launch_pdl(k_splitk_reduce, (unsigned)((n + 255) / 256), 256, 0, st, part, ksplit, stride, M, N, ldc, bias, out, out16);
   CK_LAUNCH();
 }
 
@@ -121,6 +126,7 @@ NMT_DEV int hash_insert(unsigned long long* keys, uint64_t mask, int64_t key) {
 }
 
 __global__ void k_plan_intern(CtxDev c, PlanIO io) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int n_nodes = c.counters[CNT_NODES];
   if (i < io.n_cand) {
@@ -181,6 +187,7 @@ NMT_DEV int block_scan_excl(int v, int* smem32, int& total) {
 
 // single-CTA pass: new node ids (first appearances), row list of parents to step.
 __global__ void __launch_bounds__(1024) k_plan_assign(CtxDev c, PlanIO io, int* R_out) {
+  pdl_enter();
   __shared__ int sm[32];
   const int n_nodes0 = c.counters[CNT_NODES];
   const int n_slots0 = c.counters[CNT_SLOTS];
@@ -244,16 +251,17 @@ __global__ void __launch_bounds__(1024) k_plan_assign(CtxDev c, PlanIO io, int* 
 void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st) {
   const int n = io.n_cand > io.n_par ? io.n_cand : io.n_par;
   if (n > 0) {
-    k_plan_intern<<<(n + 255) / 256, 256, 0, st>>>(c, io);
+    launch_pdl(k_plan_intern, (n + 255) / 256, 256, 0, st, c, io);
     CK_LAUNCH();
   }
-  k_plan_assign<<<1, 1024, 0, st>>>(c, io, R_dev);
+  launch_pdl(k_plan_assign, 1, 1024, 0, st, c, io, R_dev);
   CK_LAUNCH();
 }
 
 // rehash all entries of an old table into a new (larger) one
 __global__ void k_rehash(const unsigned long long* okeys, const int* ovals, int64_t ocap, unsigned long long* nkeys,
                          int* nvals, uint64_t nmask) {
+  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ocap) return;
   const int64_t key = (int64_t)okeys[i];
@@ -263,22 +271,24 @@ __global__ void k_rehash(const unsigned long long* okeys, const int* ovals, int6
 }
 void rehash(const unsigned long long* okeys, const int* ovals, int64_t ocap, unsigned long long* nkeys, int* nvals,
             uint64_t nmask, cudaStream_t st) {
-  k_rehash<<<(unsigned)((ocap + 255) / 256), 256, 0, st>>>(okeys, ovals, ocap, nkeys, nvals, nmask);
+  launch_pdl(k_rehash, (unsigned)((ocap + 255) / 256), 256, 0, st, okeys, ovals, ocap, nkeys, nvals, nmask);
   CK_LAUNCH();
 }
 
 __global__ void k_fill_i32(int* p, int64_t n, int v) {
+  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
 }
 void fill_i32(int* p, int64_t n, int v, cudaStream_t st) {
   if (n <= 0) return;
-  k_fill_i32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, n, v);
+  launch_pdl(k_fill_i32, (unsigned)((n + 255) / 256), 256, 0, st, p, n, v);
   CK_LAUNCH();
 }
 
 // inject parentless nodes with their own input slots (synthetic parents for bench/tests)
 __global__ void k_inject(CtxDev c, int n, const float* s, const int* y, int* out_ids) {
+  pdl_enter();
   const int n_nodes0 = c.counters[CNT_NODES], n_slots0 = c.counters[CNT_SLOTS];
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
     const int slot = n_slots0 + i;
@@ -300,19 +310,21 @@ __global__ void k_inject(CtxDev c, int n, const float* s, const int* y, int* out
   }
 }
 __global__ void k_inject_commit(CtxDev c, int n) {
+  pdl_enter();
   c.counters[CNT_NODES] += n;
   c.counters[CNT_SLOTS] += n;
 }
 void inject(const CtxDev& c, int n, const float* s, const int* y, int* out_ids, cudaStream_t st) {
-  k_inject<<<n < 1024 ? n : 1024, 256, 0, st>>>(c, n, s, y, out_ids);
+  launch_pdl(k_inject, n < 1024 ? n : 1024, 256, 0, st, c, n, s, y, out_ids);
   CK_LAUNCH();
-  k_inject_commit<<<1, 1, 0, st>>>(c, n);
+  launch_pdl(k_inject_commit, 1, 1, 0, st, c, n);
   CK_LAUNCH();
 }
 
 // ===================================================================================== step D1-D7
 // D1: gather the parents' input states into the bf16 A operand of GRU1's recurrent GEMM
 __global__ void k_gather_state(StepDev d, const float* __restrict__ S) {
+  pdl_enter();
   const int R = *d.R;
   for (int r = blockIdx.x; r < R; r += gridDim.x) {
     const float* src = S + (int64_t)d.row_src[r] * d.Hp;
@@ -323,6 +335,7 @@ __global__ void k_gather_state(StepDev d, const float* __restrict__ S) {
 
 // D2: GRU1 gates.  G1 = s.[U|Ux] (GEMM), Ex[y] = e.[W|Wx] + [b|bx] (precomputed per word).
 __global__ void k_gru1(StepDev d, const float* __restrict__ S) {
+  pdl_enter();
   const int R = *d.R;
   const int H = d.H, Hp = d.Hp;
   for (int r = blockIdx.x; r < R; r += gridDim.x) {
@@ -342,70 +355,118 @@ __global__ void k_gru1(StepDev d, const float* __restrict__ S) {
 }
 
 // D4+D5: MLP attention energies (MUFU tanh), softmax over source positions, context vector.
-// One CTA = RPB rows of the same sentence; thread owns 8 consecutive context columns.
+// One CTA = RPB rows of the same sentence; thread owns 8 consecutive context columns (q of its
+// rows in registers).  pctx_j and ctx_j slices stream through a per-thread cp.async ring in
+// shared memory (NST positions in flight).  Energies of 8 positions x RPB rows are reduced across
+// the warp with a 32-value butterfly reduce-scatter (31 shuffles instead of 5 per value).
+NMT_DEV void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+NMT_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+NMT_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// v[0..31] are 32 values per lane; returns sum over the warp of v[lane] (lane i gets the total of
+// value i).  5 stages, 16+8+4+2+1 shuffles.
+NMT_DEV float warp_reduce_scatter32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int st = 16; st >= 1; st >>= 1) {
+    const bool upper = (lane & st) != 0;
+#pragma unroll
+    for (int i = 0; i < st; ++i) {
+      const float send = upper ? v[i] : v[i + st];
+      const float keep = upper ? v[i + st] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+    }
+  }
+  return v[0];
+}
+
 template <int RPB>
-__global__ void k_attention(StepDev d, AttnCtx a) {
+__global__ void __launch_bounds__(256) k_attention(StepDev d, AttnCtx a) {
+  pdl_enter();
+  static_assert(RPB == 4, "the 32-value reduce-scatter covers 8 positions x 4 rows");
+  constexpr int NST = 8;  // positions in flight
   const int R = *d.R;
   const int r0 = blockIdx.x * RPB;
   if (r0 >= R) return;
   const int Cp = d.Cp, Tx = a.Tx;
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = threadIdx.x * 8;
-  extern __shared__ float sm[];
-  float* red = sm;                     // [nw][RPB][Tx]
-  float* alpha = sm + nw * RPB * Tx;   // [RPB][Tx]
+  extern __shared__ float4 smq[];
+  float4* ring = smq;                                                   // [NST][blockDim][2] float4
+  float* red = reinterpret_cast<float*>(ring + NST * blockDim.x * 2);  // [nw][RPB][Tx8]
+  const int Tx8 = (Tx + 7) & ~7;
+  float* alpha = red + nw * RPB * Tx8;                                  // [RPB][Tx]
+  float4* mine = ring + threadIdx.x * 2;
+  const int rstride = blockDim.x * 2;
   float q[RPB][8], u[8];
 #pragma unroll
   for (int rr = 0; rr < RPB; ++rr) {
     const bool ok = r0 + rr < R;
     const float4* qp = reinterpret_cast<const float4*>(d.Q + (int64_t)(r0 + rr) * Cp + c0);
-    float4 x0 = ok ? qp[0] : make_float4(0, 0, 0, 0), x1 = ok ? qp[1] : make_float4(0, 0, 0, 0);
+    const float4 x0 = ok ? qp[0] : make_float4(0, 0, 0, 0), x1 = ok ? qp[1] : make_float4(0, 0, 0, 0);
     q[rr][0] = x0.x; q[rr][1] = x0.y; q[rr][2] = x0.z; q[rr][3] = x0.w;
     q[rr][4] = x1.x; q[rr][5] = x1.y; q[rr][6] = x1.z; q[rr][7] = x1.w;
   }
   {
     const float4* up = reinterpret_cast<const float4*>(a.U_att + c0);
-    float4 x0 = up[0], x1 = up[1];
+    const float4 x0 = up[0], x1 = up[1];
     u[0] = x0.x; u[1] = x0.y; u[2] = x0.z; u[3] = x0.w; u[4] = x1.x; u[5] = x1.y; u[6] = x1.z; u[7] = x1.w;
   }
-  for (int j = 0; j < Tx; ++j) {
-    const float4* pp = reinterpret_cast<const float4*>(a.pctx + (int64_t)j * Cp + c0);
-    const float4 p0 = pp[0], p1 = pp[1];
-    const float p[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-    float acc[RPB];
+  const float* pg = a.pctx + c0;
+  // prologue: positions 0..NST-1 in flight (one commit group per position, possibly empty)
 #pragma unroll
-    for (int rr = 0; rr < RPB; ++rr) {
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) s = fmaf(tanh_approx(p[k] + q[rr][k]), u[k], s);
-      acc[rr] = s;
+  for (int i = 0; i < NST; ++i) {
+    if (i < Tx) {
+      cp_async16(mine + i * rstride, pg + (int64_t)i * Cp);
+      cp_async16(mine + i * rstride + 1, pg + (int64_t)i * Cp + 4);
     }
-#pragma unroll
-    for (int rr = 0; rr < RPB; ++rr) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], o);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int rr = 0; rr < RPB; ++rr) red[(warp * RPB + rr) * Tx + j] = acc[rr];
-    }
+    cp_async_commit();
   }
+  for (int j0 = 0; j0 < Tx; j0 += 8) {
+    float e[32];  // e[jj * 4 + rr] partial energies of positions j0..j0+7
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int j = j0 + jj;
+      const int slot = j % NST;
+      cp_async_wait<NST - 1>();
+      const float4 n0 = mine[slot * rstride], n1 = mine[slot * rstride + 1];
+      // refill this slot with position j + NST
+      if (j + NST < Tx) {
+        cp_async16(mine + slot * rstride, pg + (int64_t)(j + NST) * Cp);
+        cp_async16(mine + slot * rstride + 1, pg + (int64_t)(j + NST) * Cp + 4);
+      }
+      cp_async_commit();
+      const float p[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+#pragma unroll
+      for (int rr = 0; rr < RPB; ++rr) {
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s = fmaf(tanh_approx(p[k] + q[rr][k]), u[k], s);
+        e[jj * 4 + rr] = j < Tx ? s : 0.f;
+      }
+    }
+    const float tot = warp_reduce_scatter32(e, lane);  // lane = jj * 4 + rr
+    red[(warp * RPB + (lane & 3)) * Tx8 + j0 + (lane >> 2)] = tot;
+  }
+  cp_async_wait<0>();
   __syncthreads();
   for (int rr = warp; rr < RPB; rr += nw) {  // softmax over j for row rr
     float mx = -INFINITY;
     for (int j = lane; j < Tx; j += 32) {
-      float e = a.c_tt;
-      for (int w = 0; w < nw; ++w) e += red[(w * RPB + rr) * Tx + j];
-      alpha[rr * Tx + j] = e;
-      mx = fmaxf(mx, e);
+      float ev = a.c_tt;
+      for (int w = 0; w < nw; ++w) ev += red[(w * RPB + rr) * Tx8 + j];
+      alpha[rr * Tx + j] = ev;
+      mx = fmaxf(mx, ev);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     float sum = 0.f;
     for (int j = lane; j < Tx; j += 32) {
-      const float e = expf(alpha[rr * Tx + j] - mx);
-      alpha[rr * Tx + j] = e;
-      sum += e;
+      const float ev = expf(alpha[rr * Tx + j] - mx);
+      alpha[rr * Tx + j] = ev;
+      sum += ev;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -416,14 +477,30 @@ __global__ void k_attention(StepDev d, AttnCtx a) {
     }
   }
   __syncthreads();
+  // context c = sum_j alpha_j ctx_j, ctx slices through the same ring
+  const float* cg = a.ctx + c0;
+#pragma unroll
+  for (int i = 0; i < NST; ++i) {
+    if (i < Tx) {
+      cp_async16(mine + i * rstride, cg + (int64_t)i * Cp);
+      cp_async16(mine + i * rstride + 1, cg + (int64_t)i * Cp + 4);
+    }
+    cp_async_commit();
+  }
   float cacc[RPB][8];
 #pragma unroll
   for (int rr = 0; rr < RPB; ++rr)
 #pragma unroll
     for (int k = 0; k < 8; ++k) cacc[rr][k] = 0.f;
   for (int j = 0; j < Tx; ++j) {
-    const float4* cp = reinterpret_cast<const float4*>(a.ctx + (int64_t)j * Cp + c0);
-    const float4 x0 = cp[0], x1 = cp[1];
+    const int slot = j % NST;
+    cp_async_wait<NST - 1>();
+    const float4 x0 = mine[slot * rstride], x1 = mine[slot * rstride + 1];
+    if (j + NST < Tx) {
+      cp_async16(mine + slot * rstride, cg + (int64_t)(j + NST) * Cp);
+      cp_async16(mine + slot * rstride + 1, cg + (int64_t)(j + NST) * Cp + 4);
+    }
+    cp_async_commit();
     const float cv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
     for (int rr = 0; rr < RPB; ++rr) {
@@ -432,6 +509,7 @@ __global__ void k_attention(StepDev d, AttnCtx a) {
       for (int k = 0; k < 8; ++k) cacc[rr][k] = fmaf(al, cv[k], cacc[rr][k]);
     }
   }
+  cp_async_wait<0>();
 #pragma unroll
   for (int rr = 0; rr < RPB; ++rr) {
     const int r = r0 + rr;
@@ -447,6 +525,7 @@ __global__ void k_attention(StepDev d, AttnCtx a) {
 
 // D6: GRU2 gates.  G2 = [s1 U_nl + c Wc | s1 Ux_nl | c Wcx] (one region GEMM).
 __global__ void k_gru2(StepDev d, float* __restrict__ S) {
+  pdl_enter();
   const int R = *d.R;
   const int H = d.H, Hp = d.Hp;
   for (int r = blockIdx.x; r < R; r += gridDim.x) {
@@ -468,6 +547,7 @@ __global__ void k_gru2(StepDev d, float* __restrict__ S) {
 // Writes t (fp32) to the arena and the bf16 A operand of the vocabulary GEMM with the two
 // bias columns (b_o folded into the GEMM as hi + lo).
 __global__ void k_readout(StepDev d, float* __restrict__ T) {
+  pdl_enter();
   const int R = *d.R;
   const int E = d.E, Ep = d.Ep;
   for (int r = blockIdx.x; r < R; r += gridDim.x) {
@@ -495,13 +575,15 @@ __global__ void k_readout(StepDev d, float* __restrict__ T) {
 
 // D9a: combine the per-tile (max, sum, argmax) partials of each row in fixed tile order.
 __global__ void k_finalize(StepDev d, float* __restrict__ logZ, int* __restrict__ amax) {
+  pdl_enter();
   const int R = *d.R;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= R) return;
-  const float4* p = d.part + (int64_t)warp * d.n_tiles;
+  const int np = 2 * d.n_tiles;  // (tile, half) partials in column order
+  const float4* p = d.part + (int64_t)warp * np;
   float m = -INFINITY, s = 0.f;
   int am = 0x7fffffff;
-  for (int i = lane; i < d.n_tiles; i += 32) {
+  for (int i = lane; i < np; i += 32) {
     const float4 v = p[i];
     if (v.x > m) {
       s = s * expf(m - v.x) + v.y;
@@ -536,6 +618,7 @@ __global__ void k_finalize(StepDev d, float* __restrict__ logZ, int* __restrict_
 // D9b: per candidate log p = t . W_o[:,w] + b_o[w] - logZ (fp32 gather-dot; also serves cache hits)
 __global__ void k_gather_dot(CtxDev c, PlanIO io, const float* __restrict__ Wo32, const float* __restrict__ bo,
                              int Ep, float* out_logp, int* out_child32, long long* out_child64) {
+  pdl_enter();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= io.n_cand) return;
   const int hs = io.cand_hslot[warp];
@@ -571,6 +654,7 @@ __global__ void k_gather_dot(CtxDev c, PlanIO io, const float* __restrict__ Wo32
 }
 
 __global__ void k_argmax_out(CtxDev c, PlanIO io, int* out) {
+  pdl_enter();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= io.n_par) return;
   const int p = io.parents[k];
@@ -585,6 +669,7 @@ __global__ void k_argmax_out(CtxDev c, PlanIO io, int* out) {
 // full log-prob row of one stepped slot (test export)
 __global__ void k_full_row(const float* __restrict__ T, const float* __restrict__ Wo32, const float* __restrict__ bo,
                            const float* __restrict__ logZ, int slot, int Ep, int V, float* out) {
+  pdl_enter();
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= V) return;
   const float* t = T + (int64_t)slot * Ep;
@@ -601,18 +686,25 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
   if (R_max <= 0) return;
   const int g = R_max < 4096 ? R_max : 4096;
   switch (which) {
-    case EW_GATHER: k_gather_state<<<g, 256, 0, st>>>(d, S); break;
-    case EW_GRU1: k_gru1<<<g, 256, 0, st>>>(d, S); break;
+    case EW_GATHER: launch_pdl(k_gather_state, g, 256, 0, st, d, S); break;
+    case EW_GRU1: launch_pdl(k_gru1, g, 256, 0, st, d, S); break;
     case EW_ATTN: {
       constexpr int RPB = 4;
       const int nthr = d.Cp / 8;
-      const size_t smem = (size_t)((nthr / 32 > 0 ? nthr / 32 : 1) * RPB + RPB) * a.Tx * sizeof(float);
-      k_attention<RPB><<<(R_max + RPB - 1) / RPB, nthr, smem, st>>>(d, a);
+      const int nw = nthr / 32 > 0 ? nthr / 32 : 1;
+      const int Tx8 = (a.Tx + 7) & ~7;
+      const size_t smem = (size_t)8 * nthr * 2 * sizeof(float4) + (size_t)(nw * RPB * Tx8 + RPB * a.Tx) * sizeof(float);
+      static size_t attr = 0;  // > 48 KB of dynamic shared memory needs the opt-in
+      if (smem > attr) {
+        CK(cudaFuncSetAttribute(k_attention<RPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+      }
+      launch_pdl(k_attention<RPB>, (R_max + RPB - 1) / RPB, nthr, smem, st, d, a);
       break;
     }
-    case EW_GRU2: k_gru2<<<g, 256, 0, st>>>(d, S); break;
-    case EW_READOUT: k_readout<<<g, 128, 0, st>>>(d, T); break;
-    case EW_FINALIZE: k_finalize<<<(R_max * 32 + 255) / 256, 256, 0, st>>>(d, logZ, amax); break;
+    case EW_GRU2: launch_pdl(k_gru2, g, 256, 0, st, d, S); break;
+    case EW_READOUT: launch_pdl(k_readout, g, 128, 0, st, d, T); break;
+    case EW_FINALIZE: launch_pdl(k_finalize, (R_max * 32 + 255) / 256, 256, 0, st, d, logZ, amax); break;
   }
   CK_LAUNCH();
 }
@@ -620,19 +712,19 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
 void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const float* bo, int Ep, float* out_logp,
                 int* out_child32, long long* out_child64, int* out_argmax, cudaStream_t st) {
   if (io.n_cand > 0) {
-    k_gather_dot<<<(io.n_cand * 32 + 255) / 256, 256, 0, st>>>(c, io, Wo32, bo, Ep, out_logp, out_child32,
+    launch_pdl(k_gather_dot, (io.n_cand * 32 + 255) / 256, 256, 0, st, c, io, Wo32, bo, Ep, out_logp, out_child32,
                                                                  out_child64);
     CK_LAUNCH();
   }
   if (out_argmax && io.n_par > 0) {
-    k_argmax_out<<<(io.n_par + 255) / 256, 256, 0, st>>>(c, io, out_argmax);
+    launch_pdl(k_argmax_out, (io.n_par + 255) / 256, 256, 0, st, c, io, out_argmax);
     CK_LAUNCH();
   }
 }
 
 void full_row(const float* T, const float* Wo32, const float* bo, const float* logZ, int slot, int Ep, int V,
               float* out, cudaStream_t st) {
-  k_full_row<<<(V * 32 + 255) / 256, 256, 0, st>>>(T, Wo32, bo, logZ, slot, Ep, V, out);
+  launch_pdl(k_full_row, (V * 32 + 255) / 256, 256, 0, st, T, Wo32, bo, logZ, slot, Ep, V, out);
   CK_LAUNCH();
 }
 
@@ -640,6 +732,7 @@ void full_row(const float* T, const float* Wo32, const float* bo, const float* l
 // E1: gather source embeddings into the split bf16 A operand of the input projections.
 __global__ void k_enc_gather(const float* __restrict__ Wemb, const int* __restrict__ src, int Tx, int E, int Ep, int Vs,
                              __nv_bfloat16* X, int* err) {
+  pdl_enter();
   const int j = blockIdx.x;
   if (j >= Tx) return;
   int id = src[j];
@@ -652,7 +745,7 @@ __global__ void k_enc_gather(const float* __restrict__ Wemb, const int* __restri
 }
 void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, int Vs, __nv_bfloat16* X, int* err,
                 cudaStream_t st) {
-  k_enc_gather<<<Tx, 128, 0, st>>>(Wemb, src, Tx, E, Ep, Vs, X, err);
+  launch_pdl(k_enc_gather, Tx, 128, 0, st, Wemb, src, Tx, E, Ep, Vs, X, err);
   CK_LAUNCH();
 }
 
@@ -668,6 +761,7 @@ void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, int Vs
 constexpr int kRecurThreads = 384, kRecurWarps = 12, kRecurCPW = 4;
 template <int KI>  // Hp = 128 * KI
 __global__ void __launch_bounds__(kRecurThreads, 1) k_enc_recur(EncDev e, int Tx) {
+  pdl_wait();  // (no early trigger: the cooperative grid must not lose SMs to dependents)
   constexpr int Hp = 128 * KI, H4 = Hp / 4;
   __shared__ float4 h4[H4];
   __shared__ float dots[3 * 16];
@@ -786,6 +880,7 @@ void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
 // E5: s0 = tanh(mean_j ctx_j . W_init + b_init) -> arena slot 0; also the split copy of ctx for E7.
 // (a) column means + split copy, (b) K-split partial mat-vec, (c) ordered sum + tanh.
 __global__ void k_enc_mean(EncDev e, int Tx) {
+  pdl_enter();
   __shared__ float red[8][33];
   const int Hp = e.Hp, H = e.H;
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);  // padded context column
@@ -810,6 +905,7 @@ __global__ void k_enc_mean(EncDev e, int Tx) {
 }
 constexpr int kInitKS = 16;  // K splits of the s0 mat-vec
 __global__ void k_enc_s0_part(EncDev e) {
+  pdl_enter();
   const int H = e.H, C = 2 * H;
   const int o = blockIdx.x * 32 + (threadIdx.x & 31);
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -836,6 +932,7 @@ __global__ void k_enc_s0_part(EncDev e) {
   }
 }
 __global__ void k_enc_s0_final(EncDev e, float* S0) {
+  pdl_enter();
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= e.H) return;
   float t = 0.f;
@@ -843,11 +940,11 @@ __global__ void k_enc_s0_final(EncDev e, float* S0) {
   S0[o] = tanhf(t + e.b_init[o]);
 }
 void enc_init(const EncDev& e, int Tx, float* S0, cudaStream_t st) {
-  k_enc_mean<<<(2 * e.Hp + 31) / 32, 256, 0, st>>>(e, Tx);
+  launch_pdl(k_enc_mean, (2 * e.Hp + 31) / 32, 256, 0, st, e, Tx);
   CK_LAUNCH();
-  k_enc_s0_part<<<dim3((e.H + 31) / 32, kInitKS), 256, 0, st>>>(e);
+  launch_pdl(k_enc_s0_part, dim3((e.H + 31) / 32, kInitKS), 256, 0, st, e);
   CK_LAUNCH();
-  k_enc_s0_final<<<(e.H + 127) / 128, 128, 0, st>>>(e, S0);
+  launch_pdl(k_enc_s0_final, (e.H + 127) / 128, 128, 0, st, e, S0);
   CK_LAUNCH();
 }
 

@@ -176,6 +176,7 @@ def test_enru_ragged_batch_vs_oracle(enru, prec):
     rl, rc, ra = sess.score_batch(oids, off, words)
     assert list(ch) == list(rc)
     err = np.abs(lp.astype(np.float64) - rl)
+    print(f"\n[parity] En->Ru R={R} {prec}: max|dlogp| = {err.max():.3e}, mean = {err.mean():.3e}")
     assert err.max() < TOL[prec], float(err.max())
     zrows = []
     for i in range(0, R, 10):  # top-1 margin rule on a sample of rows
@@ -206,5 +207,6 @@ def test_enru_bench_config_sampled(enru):
         for i in range(off[r], off[r + 1]):
             worst = max(worst, abs(float(lp[i]) - lsm[words[i]]))
         assert lsm[am[r]] >= lsm.max() - 2 * TOL["bf16"]
+    print(f"\n[parity] bench config R=1024 bf16 (sampled rows): max|dlogp| = {worst:.3e}")
     assert worst < TOL["bf16"], worst
     assert len(set(ch.tolist())) == len(ch)
