@@ -142,6 +142,7 @@ struct nmt_model {
   __nv_bfloat16 *A_s = nullptr, *X = nullptr, *A_t = nullptr;
   float *G1 = nullptr, *S1 = nullptr, *Q = nullptr, *Cf = nullptr, *G2 = nullptr, *RO_buf = nullptr, *alpha = nullptr;
   float4* part = nullptr;
+  int* lse_cpm = nullptr;  // [1] runs per m-tile of the last vocabulary GEMM
   int *row_src = nullptr, *row_y = nullptr, *row_dst = nullptr, *row_node = nullptr;
   int *cand_k = nullptr, *cand_hslot = nullptr;
   int *in_par = nullptr, *in_off = nullptr, *in_words = nullptr;
@@ -231,7 +232,7 @@ void nmt_model::free_ws() {
   for (__nv_bfloat16** p : {&A_s, &X, &A_t}) dfree(*p);
   for (float** p : {&G1, &S1, &Q, &Cf, &G2, &RO_buf, &alpha, &out_logp, &in_s}) dfree(*p);
   dfree(part);
-  for (int** p : {&row_src, &row_y, &row_dst, &row_node, &cand_k, &cand_hslot, &in_par, &in_off, &in_words,
+  for (int** p : {&lse_cpm, &row_src, &row_y, &row_dst, &row_node, &cand_k, &cand_hslot, &in_par, &in_off, &in_words,
                   &out_child, &out_amax})
     dfree(*p);
   R_cap = NC_cap = 0;
@@ -271,7 +272,8 @@ void nmt_model::ensure_ws(int R, int NC) {
   G2 = dalloc<float>((size_t)R_cap * 4 * Hp);
   RO_buf = dalloc<float>((size_t)R_cap * ROp);
   A_t = dalloc<__nv_bfloat16>((size_t)R_cap * sf * Ep);
-  part = dalloc<float4>((size_t)R_cap * 2 * (Vp / 256));
+  part = dalloc<float4>((size_t)R_cap * 2 * kNumSMs);  // <= 2 x (CTAs per m-tile) partials per row
+  lse_cpm = dalloc<int>(1);
   row_src = dalloc<int>(R_cap);
   row_y = dalloc<int>(R_cap);
   row_dst = dalloc<int>(R_cap);
@@ -829,6 +831,7 @@ static StepDev step_view(nmt_model* m, nmt_ctx* c) {
   d.lo_t = m->split ? m->Ep : 0;
   d.part = m->part;
   d.n_tiles = m->Vp / 256;
+  d.cpm = m->lse_cpm;
   return d;
 }
 
@@ -858,7 +861,7 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
   { ProfScope p_(m, ST_GEMM_RO); gemm_store(m->tm_X, m->tm_Wro, gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp), m->RO_buf, m->ROp,
              nullptr, R_max, st); }
   { ProfScope p_(m, ST_READOUT); step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  { ProfScope p_(m, ST_VOCAB); gemm_lse(m->tm_At, m->tm_Wo, gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep), m->part, m->V, R_max, st); }
+  { ProfScope p_(m, ST_VOCAB); gemm_lse(m->tm_At, m->tm_Wo, gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep), m->part, m->V, R_max, st, m->lse_cpm); }
   { ProfScope p_(m, ST_FINALIZE); step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
 }
 

@@ -12,8 +12,6 @@
 
 namespace nmt {
 
-constexpr int kNumSMs = 148;
-
 NMT_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
 NMT_DEV uint32_t lane_id() { uint32_t r; asm volatile("mov.u32 %0, %%laneid;" : "=r"(r)); return r; }

@@ -50,6 +50,41 @@ struct TileCoord {
 NMT_DEV TileCoord tile_of(int t, int num_m, int num_n) {
   return TileCoord{t % num_m, (t / num_m) % num_n, t / (num_m * num_n)};
 }
+// Work items: EPI_STORE -> one tile per item (m fastest, so concurrent CTAs share B tiles in L2).
+// EPI_LSE -> item = (m-tile, contiguous run of n-tiles): the CTA keeps each row's running
+// (max, sum, argmax) across its run and emits ONE partial per row and run half.
+struct Item {
+  int m, s, n0, n1, c;
+};
+struct Sched {
+  int num_m, num_n, ksplit, cpm, chunk, items;
+  NMT_DEV Item item(int i) const {
+    if (cpm == 0) {
+      const TileCoord t = tile_of(i, num_m, num_n);
+      return Item{t.m, t.s, t.n, t.n + 1, 0};
+    }
+    const int m = i / cpm, c = i % cpm;
+    const int n0 = min(num_n, c * chunk);
+    return Item{m, 0, n0, min(num_n, n0 + chunk), c};
+  }
+};
+template <int EPI>
+NMT_DEV Sched make_sched(int M, int N, int BN, int ksplit) {
+  Sched s;
+  s.num_m = (M + BM - 1) / BM;
+  s.num_n = N / BN;
+  s.ksplit = ksplit;
+  if (EPI == 1) {  // EPI_LSE
+    s.cpm = max(1, (int)gridDim.x / max(1, s.num_m));
+    s.chunk = (s.num_n + s.cpm - 1) / s.cpm;
+    s.items = s.num_m * s.cpm;
+  } else {
+    s.cpm = 0;
+    s.chunk = 1;
+    s.items = s.num_m * s.num_n * ksplit;
+  }
+  return s;
+}
 
 NMT_DEV RegionK region_of(const GemmShape& g, int n0) {
   int r = 0;
@@ -96,31 +131,33 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_enter();  // prologue above overlaps the previous kernel; inputs (and M_dev) are read below
   const int M = g.M_dev ? *g.M_dev : g.M;
-  const int num_m = (M + BM - 1) / BM;
-  const int num_n = g.N / BN;
-  const int total = num_m * num_n * g.ksplit;
+  const Sched sc = make_sched<EPI>(M, g.N, BN, g.ksplit);
+  if (EPI == EPI_LSE && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileCoord tc = tile_of(t, num_m, num_n);
-        const RegionK rk = region_of(g, tc.n * BN);
-        const int nkbp = rk.k1 - rk.k0, nkb = g.passes * nkbp;
-        const int chunk = (nkb + g.ksplit - 1) / g.ksplit;
-        const int i1 = min(nkb, (tc.s + 1) * chunk);
-        for (int i = tc.s * chunk; i < i1; ++i) {
-          const int pass = i / nkbp, kb = rk.k0 + i % nkbp;
-          const int aoff = g.a_col0 + (pass == 2 ? g.a_lo_off : 0);
-          const int boff = (pass == 1 ? g.b_lo_off : 0);
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES);
-          tma_load_2d(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, tc.m * BM);
-          tma_load_2d(&tmB, &full[stage], sB + stage * S::B_BYTES, boff + kb * BK, tc.n * BN);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+      for (int w = blockIdx.x; w < sc.items; w += gridDim.x) {
+        const Item itm = sc.item(w);
+        for (int n = itm.n0; n < itm.n1; ++n) {
+          const TileCoord tc{itm.m, n, itm.s};
+          const RegionK rk = region_of(g, tc.n * BN);
+          const int nkbp = rk.k1 - rk.k0, nkb = g.passes * nkbp;
+          const int chunk = (nkb + g.ksplit - 1) / g.ksplit;
+          const int i1 = min(nkb, (tc.s + 1) * chunk);
+          for (int i = tc.s * chunk; i < i1; ++i) {
+            const int pass = i / nkbp, kb = rk.k0 + i % nkbp;
+            const int aoff = g.a_col0 + (pass == 2 ? g.a_lo_off : 0);
+            const int boff = (pass == 1 ? g.b_lo_off : 0);
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES);
+            tma_load_2d(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, tc.m * BM);
+            tma_load_2d(&tmB, &full[stage], sB + stage * S::B_BYTES, boff + kb * BK, tc.n * BN);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -131,32 +168,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-        const TileCoord tc = tile_of(t, num_m, num_n);
-        const RegionK rk = region_of(g, tc.n * BN);
-        const int acc = it & 1;
-        const uint32_t aph = (it >> 1) & 1;
-        mbar_wait(&tempty[acc], aph ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
-        const int nkb_all = g.passes * (rk.k1 - rk.k0);
-        const int chunk = (nkb_all + g.ksplit - 1) / g.ksplit;
-        const int nkb = min(nkb_all, (tc.s + 1) * chunk) - tc.s * chunk;
-        for (int i = 0; i < nkb; ++i) {
-          mbar_wait(&full[stage], phase);
+      for (int w = blockIdx.x; w < sc.items; w += gridDim.x) {
+        const Item itm = sc.item(w);
+        for (int n = itm.n0; n < itm.n1; ++n, ++it) {
+          const TileCoord tc{itm.m, n, itm.s};
+          const RegionK rk = region_of(g, tc.n * BN);
+          const int acc = it & 1;
+          const uint32_t aph = (it >> 1) & 1;
+          mbar_wait(&tempty[acc], aph ^ 1);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * S::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * S::B_BYTES);
+          const uint32_t d = tmem + acc * BN;
+          const int nkb_all = g.passes * (rk.k1 - rk.k0);
+          const int chunk = (nkb_all + g.ksplit - 1) / g.ksplit;
+          const int nkb = min(nkb_all, (tc.s + 1) * chunk) - tc.s * chunk;
+          for (int i = 0; i < nkb; ++i) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + stage * S::A_BYTES);
+            const uint32_t b0 = smem_u32(sB + stage * S::B_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma_bf16(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
-          mma_commit(&empty[stage]);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
+            mma_commit(&empty[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
+          mma_commit(&tfull[acc]);
         }
-        mma_commit(&tfull[acc]);
       }
     }
   } else {  // ---------------- epilogue warps 2..9
@@ -165,96 +205,99 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     constexpr int COLS = BN / 2;
     const int row_in_tile = q * 32 + lane;
     int it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-      const TileCoord tc = tile_of(t, num_m, num_n);
-      const int m = tc.m, n = tc.n;
-      const int acc = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
-      const int grow = m * BM + row_in_tile;
+    for (int w = blockIdx.x; w < sc.items; w += gridDim.x) {
+      const Item itm = sc.item(w);
+      const int grow = itm.m * BM + row_in_tile;
       const bool valid = grow < M;
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + half * COLS;
-      const int colbase = n * BN + half * COLS;
-      if constexpr (EPI == EPI_STORE) {
-        float* orow = ep.out + (size_t)tc.s * ep.split_stride + (size_t)grow * ep.ldc + colbase;
+      constexpr float LOG2E = 1.4426950408889634f;
+      float mx = -INFINITY, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // LSE running state (per run)
+      int am = 0;
+      for (int n = itm.n0; n < itm.n1; ++n, ++it) {
+        const int acc = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + half * COLS;
+        const int colbase = n * BN + half * COLS;
+        if constexpr (EPI == EPI_STORE) {
+          float* orow = ep.out + (size_t)itm.s * ep.split_stride + (size_t)grow * ep.ldc + colbase;
 #pragma unroll 1
-        for (int c = 0; c < COLS; c += 64) {
-          float v[64];
-          tmem_ld32_nowait(tbase + c, v);
-          tmem_ld32_nowait(tbase + c + 32, v + 32);
-          tmem_wait_ld_dep(v);
-          reg_dep32(v + 32);
-          if (valid) {
-            if (ep.bias) {
-              const float4* b = reinterpret_cast<const float4*>(ep.bias + colbase + c);
+          for (int c = 0; c < COLS; c += 64) {
+            float v[64];
+            tmem_ld32_nowait(tbase + c, v);
+            tmem_ld32_nowait(tbase + c + 32, v + 32);
+            tmem_wait_ld_dep(v);
+            reg_dep32(v + 32);
+            if (valid) {
+              if (ep.bias) {
+                const float4* b = reinterpret_cast<const float4*>(ep.bias + colbase + c);
 #pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const float4 bb = __ldg(b + j);
-                v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
+                for (int j = 0; j < 16; ++j) {
+                  const float4 bb = __ldg(b + j);
+                  v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
+                }
+              }
+              float4* o = reinterpret_cast<float4*>(orow + c);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+          }
+        } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
+#pragma unroll 1
+          for (int c = 0; c < COLS; c += 64) {
+            float v[64];
+            tmem_ld32_nowait(tbase + c, v);
+            tmem_ld32_nowait(tbase + c + 32, v + 32);
+            tmem_wait_ld_dep(v);
+            reg_dep32(v + 32);
+            const int col0 = colbase + c;
+            if (col0 + 64 > ep.n_valid) {  // padded vocabulary columns (last tile only)
+#pragma unroll
+              for (int j = 0; j < 64; ++j)
+                if (col0 + j >= ep.n_valid) v[j] = -INFINITY;
+            }
+            float t32[32];  // tree max
+#pragma unroll
+            for (int j = 0; j < 32; ++j) t32[j] = fmaxf(v[j], v[j + 32]);
+#pragma unroll
+            for (int k = 16; k > 0; k >>= 1)
+#pragma unroll
+              for (int j = 0; j < k; ++j) t32[j] = fmaxf(t32[j], t32[j + k]);
+            const float cm = t32[0];
+            if (cm > mx) {  // new running max (rare after the first chunks): lowest index of it
+              int ix[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) ix[j] = v[j] == cm ? j : (v[j + 32] == cm ? j + 32 : 64);
+#pragma unroll
+              for (int k = 16; k > 0; k >>= 1)
+#pragma unroll
+                for (int j = 0; j < k; ++j) ix[j] = min(ix[j], ix[j + k]);
+              const float f = ex2_approx((mx - cm) * LOG2E);
+              s0 *= f; s1 *= f; s2 *= f; s3 *= f;
+              mx = cm;
+              am = col0 + ix[0];
+            }
+            if (mx > -INFINITY) {
+              const float mb = mx * LOG2E;
+#pragma unroll
+              for (int j = 0; j < 64; j += 4) {
+                s0 += ex2_approx(fmaf(v[j], LOG2E, -mb));
+                s1 += ex2_approx(fmaf(v[j + 1], LOG2E, -mb));
+                s2 += ex2_approx(fmaf(v[j + 2], LOG2E, -mb));
+                s3 += ex2_approx(fmaf(v[j + 3], LOG2E, -mb));
               }
             }
-            float4* o = reinterpret_cast<float4*>(orow + c);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
         }
-      } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
-        constexpr float LOG2E = 1.4426950408889634f;
-        float mx = -INFINITY, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        int am = 0;
-#pragma unroll 1
-        for (int c = 0; c < COLS; c += 64) {
-          float v[64];
-          tmem_ld32_nowait(tbase + c, v);
-          tmem_ld32_nowait(tbase + c + 32, v + 32);
-          tmem_wait_ld_dep(v);
-          reg_dep32(v + 32);
-          const int col0 = colbase + c;
-          if (col0 + 64 > ep.n_valid) {  // padded vocabulary columns (last tile only)
-#pragma unroll
-            for (int j = 0; j < 64; ++j)
-              if (col0 + j >= ep.n_valid) v[j] = -INFINITY;
-          }
-          float t32[32];  // tree max
-#pragma unroll
-          for (int j = 0; j < 32; ++j) t32[j] = fmaxf(v[j], v[j + 32]);
-#pragma unroll
-          for (int w = 16; w > 0; w >>= 1)
-#pragma unroll
-            for (int j = 0; j < w; ++j) t32[j] = fmaxf(t32[j], t32[j + w]);
-          const float cm = t32[0];
-          if (cm > mx) {  // new running max: first (lowest) index of it in this chunk; rescale the sums
-            int ix[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) ix[j] = v[j] == cm ? j : (v[j + 32] == cm ? j + 32 : 64);
-#pragma unroll
-            for (int w = 16; w > 0; w >>= 1)
-#pragma unroll
-              for (int j = 0; j < w; ++j) ix[j] = min(ix[j], ix[j + w]);
-            const float f = ex2_approx((mx - cm) * LOG2E);
-            s0 *= f; s1 *= f; s2 *= f; s3 *= f;
-            mx = cm;
-            am = col0 + ix[0];
-          }
-          if (mx > -INFINITY) {
-            const float mb = mx * LOG2E;
-#pragma unroll
-            for (int j = 0; j < 64; j += 4) {
-              s0 += ex2_approx(fmaf(v[j], LOG2E, -mb));
-              s1 += ex2_approx(fmaf(v[j + 1], LOG2E, -mb));
-              s2 += ex2_approx(fmaf(v[j + 2], LOG2E, -mb));
-              s3 += ex2_approx(fmaf(v[j + 3], LOG2E, -mb));
-            }
-          }
-        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
+      if constexpr (EPI == EPI_LSE) {  // one partial per (row, run, half); empty runs give (-inf, 0)
         if (valid)
-          ep.part[((size_t)grow * ep.n_tiles + n) * 2 + half] =
+          ep.part[((size_t)grow * sc.cpm + itm.c) * 2 + half] =
               make_float4(mx, (s0 + s1) + (s2 + s3), __int_as_float(am), 0.f);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   __syncthreads();
@@ -345,12 +388,13 @@ void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, 
 
 // fused vocabulary GEMM + online log-sum-exp partials; BN = 256.
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
-              cudaStream_t st) {
+              cudaStream_t st, int* cpm_out) {
   gemm_validate(g, 256);
   EpiParams ep{};
   ep.part = part;
   ep.n_valid = n_valid;
   ep.n_tiles = g.N / 256;
+  ep.cpm_out = cpm_out;
   launch<256, 4, EPI_LSE>(a, b, g, ep, M_max, st);
 }
 

@@ -11,6 +11,8 @@
 
 namespace nmt {
 
+constexpr int kNumSMs = 148;  // B200
+
 struct NmtError {
   nmt_status code;
   std::string msg;
@@ -74,6 +76,7 @@ struct EpiParams {
   int n_valid;
   int n_tiles;
   size_t split_stride;
+  int* cpm_out;  // EPI_LSE: runs per m-tile (partials per row = 2 * cpm), written by CTA 0
 };
 
 CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
@@ -83,7 +86,7 @@ void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, 
 void splitk_reduce(const float* part, int ksplit, size_t stride, int M, int N, int ldc, const float* bias, float* out,
                    cudaStream_t st, __nv_bfloat16* out16 = nullptr);
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
-              cudaStream_t st);
+              cudaStream_t st, int* cpm_out);
 
 inline GemmShape gemm_shape(int M, const int* M_dev, int N, int K, int a_col0, bool split, int a_lo_off,
                             int b_lo_off) {

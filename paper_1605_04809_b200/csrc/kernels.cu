@@ -322,36 +322,58 @@ void inject(const CtxDev& c, int n, const float* s, const int* y, int* out_ids, 
 }
 
 // ===================================================================================== step D1-D7
+// Elementwise step kernels: one thread per (row, 4 consecutive hidden units), float4 loads all
+// issued before any math (latency-bound otherwise); rows r >= *R exit.
+NMT_DEV float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+NMT_DEV void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+NMT_DEV uint32_t pk_bf16(float a, float b) {
+  uint32_t y;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(y) : "f"(b), "f"(a));
+  return y;
+}
+// write 4 values as bf16 hi (and the bf16 lo residuals at +lo_off) - 8-byte stores
+NMT_DEV void store_split4(__nv_bfloat16* hi, int lo_off, float4 v) {
+  const uint32_t h01 = pk_bf16(v.x, v.y), h23 = pk_bf16(v.z, v.w);
+  *reinterpret_cast<uint2*>(hi) = make_uint2(h01, h23);
+  if (lo_off > 0) {
+    const float r0 = v.x - __uint_as_float(h01 << 16), r1 = v.y - __uint_as_float(h01 & 0xffff0000u);
+    const float r2 = v.z - __uint_as_float(h23 << 16), r3 = v.w - __uint_as_float(h23 & 0xffff0000u);
+    *reinterpret_cast<uint2*>(hi + lo_off) = make_uint2(pk_bf16(r0, r1), pk_bf16(r2, r3));
+  }
+}
+NMT_DEV float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+
 // D1: gather the parents' input states into the bf16 A operand of GRU1's recurrent GEMM
 __global__ void k_gather_state(StepDev d, const float* __restrict__ S) {
   pdl_enter();
-  const int R = *d.R;
-  for (int r = blockIdx.x; r < R; r += gridDim.x) {
-    const float* src = S + (int64_t)d.row_src[r] * d.Hp;
-    __nv_bfloat16* dst = d.A_s + (int64_t)r * d.lda_s;
-    for (int k = threadIdx.x; k < d.H; k += blockDim.x) store_split(dst + k, d.lo_s, src[k]);
-  }
+  const int H4 = (d.H + 3) / 4;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = idx / H4, j = (idx % H4) * 4;
+  if (r >= *d.R) return;
+  const float4 v = ld4(S + (int64_t)d.row_src[r] * d.Hp + j);
+  store_split4(d.A_s + (int64_t)r * d.lda_s + j, d.lo_s, v);
 }
 
 // D2: GRU1 gates.  G1 = s.[U|Ux] (GEMM), Ex[y] = e.[W|Wx] + [b|bx] (precomputed per word).
 __global__ void k_gru1(StepDev d, const float* __restrict__ S) {
   pdl_enter();
-  const int R = *d.R;
-  const int H = d.H, Hp = d.Hp;
-  for (int r = blockIdx.x; r < R; r += gridDim.x) {
-    const int y = d.row_y[r];
-    const float* g = d.G1 + (int64_t)r * 3 * Hp;
-    const float* ex = d.Ex + (int64_t)(y < 0 ? d.V : y) * 3 * Hp;
-    const float* s = S + (int64_t)d.row_src[r] * Hp;
-    for (int j = threadIdx.x; j < H; j += blockDim.x) {
-      const float rg = 1.f / (1.f + expf(-(ex[j] + g[j])));
-      const float ug = 1.f / (1.f + expf(-(ex[Hp + j] + g[Hp + j])));
-      const float ht = tanhf(rg * g[2 * Hp + j] + ex[2 * Hp + j]);
-      const float s1 = ug * s[j] + (1.f - ug) * ht;
-      d.S1[(int64_t)r * Hp + j] = s1;
-      store_split(d.X + (int64_t)r * d.ldx + j, d.lo_x, s1);
-    }
-  }
+  const int Hp = d.Hp, H4 = (d.H + 3) / 4;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = idx / H4, j = (idx % H4) * 4;
+  if (r >= *d.R) return;
+  const int y = d.row_y[r];
+  const float* g = d.G1 + (int64_t)r * 3 * Hp + j;
+  const float* ex = d.Ex + (int64_t)(y < 0 ? d.V : y) * 3 * Hp + j;
+  const float4 gr = ld4(g), gu = ld4(g + Hp), gc = ld4(g + 2 * Hp);
+  const float4 er = ld4(ex), eu = ld4(ex + Hp), ec = ld4(ex + 2 * Hp);
+  const float4 sv = ld4(S + (int64_t)d.row_src[r] * Hp + j);
+  float4 o;
+#define NMT_GRU1(c) { const float rg = sigm(er.c + gr.c), ug = sigm(eu.c + gu.c); \
+                      o.c = ug * sv.c + (1.f - ug) * tanhf(rg * gc.c + ec.c); }
+  NMT_GRU1(x) NMT_GRU1(y) NMT_GRU1(z) NMT_GRU1(w)
+#undef NMT_GRU1
+  st4(d.S1 + (int64_t)r * Hp + j, o);
+  store_split4(d.X + (int64_t)r * d.ldx + j, d.lo_x, o);
 }
 
 // D4+D5: MLP attention energies (MUFU tanh), softmax over source positions, context vector.
@@ -526,71 +548,104 @@ __global__ void __launch_bounds__(256) k_attention(StepDev d, AttnCtx a) {
 // D6: GRU2 gates.  G2 = [s1 U_nl + c Wc | s1 Ux_nl | c Wcx] (one region GEMM).
 __global__ void k_gru2(StepDev d, float* __restrict__ S) {
   pdl_enter();
-  const int R = *d.R;
-  const int H = d.H, Hp = d.Hp;
-  for (int r = blockIdx.x; r < R; r += gridDim.x) {
-    const float* g = d.G2 + (int64_t)r * 4 * Hp;
-    const float* s1 = d.S1 + (int64_t)r * Hp;
-    float* s2o = S + (int64_t)d.row_dst[r] * Hp;
-    for (int j = threadIdx.x; j < H; j += blockDim.x) {
-      const float rg = 1.f / (1.f + expf(-(g[j] + d.b_nl[j])));
-      const float ug = 1.f / (1.f + expf(-(g[Hp + j] + d.b_nl[Hp + j])));
-      const float ht = tanhf(rg * (g[2 * Hp + j] + d.bx_nl[j]) + g[3 * Hp + j]);
-      const float s2 = ug * s1[j] + (1.f - ug) * ht;
-      s2o[j] = s2;
-      store_split(d.X + (int64_t)r * d.ldx + d.Hp + d.Cp + j, d.lo_x, s2);
-    }
-  }
+  const int Hp = d.Hp, H4 = (d.H + 3) / 4;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = idx / H4, j = (idx % H4) * 4;
+  if (r >= *d.R) return;
+  const float* g = d.G2 + (int64_t)r * 4 * Hp + j;
+  const float4 gr = ld4(g), gu = ld4(g + Hp), gh = ld4(g + 2 * Hp), gc = ld4(g + 3 * Hp);
+  const float4 br = ld4(d.b_nl + j), bu = ld4(d.b_nl + Hp + j), bx = ld4(d.bx_nl + j);
+  const float4 s1 = ld4(d.S1 + (int64_t)r * Hp + j);
+  float4 o;
+#define NMT_GRU2(c) { const float rg = sigm(gr.c + br.c), ug = sigm(gu.c + bu.c); \
+                      o.c = ug * s1.c + (1.f - ug) * tanhf(rg * (gh.c + bx.c) + gc.c); }
+  NMT_GRU2(x) NMT_GRU2(y) NMT_GRU2(z) NMT_GRU2(w)
+#undef NMT_GRU2
+  st4(S + (int64_t)d.row_dst[r] * Hp + j, o);
+  store_split4(d.X + (int64_t)r * d.ldx + d.Hp + d.Cp + j, d.lo_x, o);
 }
 
 // D7: readout activation.  RO = c W_ctx + s2 W_l (GEMM), Ep[y] = e W_p + b_p + b_l + b_ctx.
 // Writes t (fp32) to the arena and the bf16 A operand of the vocabulary GEMM with the two
-// bias columns (b_o folded into the GEMM as hi + lo).
+// bias columns (b_o folded into the GEMM as hi + lo).  Thread per (row, 4 outputs).
 __global__ void k_readout(StepDev d, float* __restrict__ T) {
   pdl_enter();
-  const int R = *d.R;
-  const int E = d.E, Ep = d.Ep;
-  for (int r = blockIdx.x; r < R; r += gridDim.x) {
-    const int y = d.row_y[r];
-    const float* pre = d.RO + (int64_t)r * d.ROp;
-    const float* epr = d.Eproj + (int64_t)(y < 0 ? d.V : y) * d.ROp;
-    float* to = T + (int64_t)d.row_dst[r] * Ep;
-    __nv_bfloat16* at = d.A_t + (int64_t)r * d.lda_t;
-    for (int k = threadIdx.x; k < Ep; k += blockDim.x) {
-      float t;
-      if (k < E) {
-        if (d.maxout) t = fmaxf(pre[2 * k] + epr[2 * k], pre[2 * k + 1] + epr[2 * k + 1]);
-        else t = tanhf(pre[k] + epr[k]);
-        to[k] = t;
-        store_split(at + k, d.lo_t, t);
-      } else {
-        // bias columns: bf16 path A[E] = A[E+1] = 1 (b_hi, b_lo in B); split path hi[E] = 1, lo[E] = 0
-        const float one = (k == E || (k == E + 1 && d.lo_t == 0)) ? 1.f : 0.f;
-        at[k] = __float2bfloat16_rn(one);
-        if (d.lo_t > 0) at[k + d.lo_t] = __float2bfloat16_rn(0.f);
-      }
+  const int E = d.E, Ep = d.Ep, E4 = Ep / 4;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = idx / E4, k = (idx % E4) * 4;
+  if (r >= *d.R) return;
+  const int y = d.row_y[r];
+  const float* pre = d.RO + (int64_t)r * d.ROp;
+  const float* epr = d.Eproj + (int64_t)(y < 0 ? d.V : y) * d.ROp;
+  float t[4];
+  if (d.maxout) {
+    if (2 * k + 7 < d.ROp) {
+      const float4 a0 = ld4(pre + 2 * k), a1 = ld4(pre + 2 * k + 4);
+      const float4 b0 = ld4(epr + 2 * k), b1 = ld4(epr + 2 * k + 4);
+      t[0] = fmaxf(a0.x + b0.x, a0.y + b0.y);
+      t[1] = fmaxf(a0.z + b0.z, a0.w + b0.w);
+      t[2] = fmaxf(a1.x + b1.x, a1.y + b1.y);
+      t[3] = fmaxf(a1.z + b1.z, a1.w + b1.w);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        t[i] = k + i < E ? fmaxf(pre[2 * (k + i)] + epr[2 * (k + i)], pre[2 * (k + i) + 1] + epr[2 * (k + i) + 1]) : 0.f;
     }
+  } else {
+    if (k + 3 < d.ROp) {
+      const float4 a = ld4(pre + k), b = ld4(epr + k);
+      t[0] = tanhf(a.x + b.x); t[1] = tanhf(a.y + b.y); t[2] = tanhf(a.z + b.z); t[3] = tanhf(a.w + b.w);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) t[i] = k + i < E ? tanhf(pre[k + i] + epr[k + i]) : 0.f;
+    }
+  }
+  float4 tv, av;  // tv -> arena (zero past E), av -> GEMM operand (bias columns at E, E+1)
+  float* tp = &tv.x;
+  float* ap = &av.x;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int kk = k + i;
+    tp[i] = kk < E ? t[i] : 0.f;
+    ap[i] = kk < E ? t[i] : ((kk == E || (kk == E + 1 && d.lo_t == 0)) ? 1.f : 0.f);
+  }
+  st4(T + (int64_t)d.row_dst[r] * Ep + k, tv);
+  __nv_bfloat16* at = d.A_t + (int64_t)r * d.lda_t + k;
+  if (k + 3 < E || d.lo_t == 0) {
+    store_split4(at, d.lo_t, av);
+  } else {  // split path, bias columns: hi = 1 at E, lo part of the bias columns = 0
+    store_split4(at, 0, av);
+    const float4 lo4 = make_float4(k < E ? tp[0] - __bfloat162float(__float2bfloat16_rn(tp[0])) : 0.f,
+                                   k + 1 < E ? tp[1] - __bfloat162float(__float2bfloat16_rn(tp[1])) : 0.f,
+                                   k + 2 < E ? tp[2] - __bfloat162float(__float2bfloat16_rn(tp[2])) : 0.f,
+                                   k + 3 < E ? tp[3] - __bfloat162float(__float2bfloat16_rn(tp[3])) : 0.f);
+    const uint32_t l01 = pk_bf16(lo4.x, lo4.y), l23 = pk_bf16(lo4.z, lo4.w);
+    *reinterpret_cast<uint2*>(at + d.lo_t) = make_uint2(l01, l23);
   }
 }
 
-// D9a: combine the per-tile (max, sum, argmax) partials of each row in fixed tile order.
+// D9a: combine the per-run (max, sum, argmax) partials of each row in fixed column order.
 __global__ void k_finalize(StepDev d, float* __restrict__ logZ, int* __restrict__ amax) {
   pdl_enter();
   const int R = *d.R;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= R) return;
-  const int np = 2 * d.n_tiles;  // (tile, half) partials in column order
+  const int np = 2 * *d.cpm;  // (run, half) partials in column order
   const float4* p = d.part + (int64_t)warp * np;
+  float4 v[10];  // np <= 2 * 148: all loads in flight before combining
+#pragma unroll
+  for (int i = 0; i < 10; ++i) v[i] = lane + 32 * i < np ? p[lane + 32 * i] : make_float4(-INFINITY, 0.f, 0.f, 0.f);
   float m = -INFINITY, s = 0.f;
   int am = 0x7fffffff;
-  for (int i = lane; i < np; i += 32) {
-    const float4 v = p[i];
-    if (v.x > m) {
-      s = s * expf(m - v.x) + v.y;
-      m = v.x;
-      am = __float_as_int(v.z);
-    } else if (v.x > -INFINITY) {
-      s += v.y * expf(v.x - m);
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    if (v[i].x > m) {
+      s = s * expf(m - v[i].x) + v[i].y;
+      m = v[i].x;
+      am = __float_as_int(v[i].z);
+    } else if (v[i].x > -INFINITY) {
+      s += v[i].y * expf(v[i].x - m);
+      if (v[i].x == m) am = min(am, __float_as_int(v[i].z));  // runs/halves interleave columns
     }
   }
 #pragma unroll
@@ -685,9 +740,13 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
                       int R_max, cudaStream_t st) {
   if (R_max <= 0) return;
   const int g = R_max < 4096 ? R_max : 4096;
+  const int H4 = (d.H + 3) / 4;
+  const unsigned gh = (unsigned)(((int64_t)R_max * H4 + 255) / 256);
+  const unsigned ge = (unsigned)(((int64_t)R_max * (d.Ep / 4) + 255) / 256);
+  (void)g;
   switch (which) {
-    case EW_GATHER: launch_pdl(k_gather_state, g, 256, 0, st, d, S); break;
-    case EW_GRU1: launch_pdl(k_gru1, g, 256, 0, st, d, S); break;
+    case EW_GATHER: launch_pdl(k_gather_state, gh, 256, 0, st, d, S); break;
+    case EW_GRU1: launch_pdl(k_gru1, gh, 256, 0, st, d, S); break;
     case EW_ATTN: {
       constexpr int RPB = 4;
       const int nthr = d.Cp / 8;
@@ -702,8 +761,8 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
       launch_pdl(k_attention<RPB>, (R_max + RPB - 1) / RPB, nthr, smem, st, d, a);
       break;
     }
-    case EW_GRU2: launch_pdl(k_gru2, g, 256, 0, st, d, S); break;
-    case EW_READOUT: launch_pdl(k_readout, g, 128, 0, st, d, T); break;
+    case EW_GRU2: launch_pdl(k_gru2, gh, 256, 0, st, d, S); break;
+    case EW_READOUT: launch_pdl(k_readout, ge, 256, 0, st, d, T); break;
     case EW_FINALIZE: launch_pdl(k_finalize, (R_max * 32 + 255) / 256, 256, 0, st, d, logZ, amax); break;
   }
   CK_LAUNCH();

@@ -60,7 +60,8 @@ struct StepDev {
   float* RO;                             // [R][ROp]
   const float* Eproj;                    // [V+1][ROp]
   __nv_bfloat16* A_t; int lda_t, lo_t;   // [R][sf*Ep]
-  float4* part; int n_tiles;             // [R][n_tiles]
+  float4* part; int n_tiles;             // [R][2 * cpm] LSE partials of the vocabulary GEMM
+  const int* cpm;                        // runs per m-tile (device, written by the GEMM)
 };
 
 struct AttnCtx {
