@@ -178,6 +178,12 @@ NMT_API nmt_status nmt_debug_intermediates(nmt_ctx* c, nmt_state node, float* s1
 NMT_API nmt_status nmt_test_gemm(int32_t M, int32_t N, int32_t K, int32_t split, const float* A, const float* B,
                          const float* bias, float* C);
 
+/* GEMM engine micro-benchmark on device-resident random operands: average ms of `iters` launches
+ * of C[M x N] = A[M x K].B[K x N] (epi 0: fp32 store, N % 128 == 0; epi 1: vocabulary online
+ * log-sum-exp, N % 256 == 0), split = bf16x3, ksplit = split-K factor (epi 0).                 */
+NMT_API nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_t epi, int32_t ksplit,
+                                  int32_t iters, float* ms_out);
+
 /* ---- ensemble hook (models as separately weighted features; north_star NCCL reduce)
  * One member per GPU/process.  nccl_unique_id points to the 128-byte ncclUniqueId broadcast by the
  * harness (torch process group).  combine: out = sum over members of (mode 0) weight*logp or

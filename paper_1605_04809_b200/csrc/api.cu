@@ -101,12 +101,10 @@ struct nmt_model {
   int E, H, Vs, V, RO, maxout, maxTx;
   int Ep, Hp, Cp, Vp, ROp, sf;
   // encoder
-  float* Wemb_src = nullptr;   // [Vs][E]
-  __nv_bfloat16* Wenc = nullptr;  // [6Hp][2Ep]
-  float* benc = nullptr;       // [6Hp]
+  float* EncIn = nullptr;      // [Vs][6Hp] precomputed Wemb.[W|Wx] + [b|bx] of both directions
   int NB = 0, UPC = 0;
-  float* Uarr = nullptr;       // [2][NB][3UPC][H]
-  float* W_init = nullptr;     // [2H][H]
+  float* Uarr = nullptr;       // [2][NB][3UPC][Hp]
+  float* W_initT = nullptr;    // [H][2H] ff_state_W transposed
   float* b_init = nullptr;     // [H]
   __nv_bfloat16* Watt = nullptr;  // [Cp][2Cp]
   float* b_att = nullptr;      // [Cp]
@@ -124,19 +122,17 @@ struct nmt_model {
   __nv_bfloat16* W_o = nullptr;   // [Vp][sf Ep]
   float* W_o32 = nullptr;         // [V][Ep]
   float* b_o = nullptr;           // [V]
-  CUtensorMap tm_Wenc, tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo;
+  int g2_bn = 256;  // N tile of the GRU2 region GEMM (256 when the regions are 256-aligned)
+  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo;
   // encoder workspace
   int Tpad = 0;
-  __nv_bfloat16* Xsrc = nullptr;  // [Tpad][2Ep]
-  float* Pin = nullptr;           // [Tpad][6Hp]
   __nv_bfloat16* ctxbf = nullptr; // [Tpad][4Hp]
   float* hbuf = nullptr;
   float* enc_mean = nullptr;
-  float* ksplit_buf = nullptr;  // split-K partials of the encoder GEMMs
-  float* enc_s0part = nullptr;
+  float* ksplit_buf = nullptr;  // split-K partials of the pctx GEMM
   int* bar = nullptr;
   int* d_src = nullptr;
-  CUtensorMap tm_Xsrc, tm_ctxbf;
+  CUtensorMap tm_ctxbf;
   // step workspace
   int R_cap = 0, NC_cap = 0;
   __nv_bfloat16 *A_s = nullptr, *X = nullptr, *A_t = nullptr;
@@ -183,11 +179,10 @@ struct nmt_model {
 };
 
 static void free_all_model(nmt_model* m) {
-  for (float** p : {&m->Wemb_src, &m->benc, &m->Uarr, &m->W_init, &m->b_init, &m->b_att, &m->U_att, &m->Ex, &m->b_nl,
-                    &m->bx_nl, &m->Eproj, &m->W_o32, &m->b_o, &m->Pin, &m->hbuf, &m->enc_mean, &m->enc_s0part, &m->ksplit_buf})
+  for (float** p : {&m->EncIn, &m->Uarr, &m->W_initT, &m->b_init, &m->b_att, &m->U_att, &m->Ex, &m->b_nl, &m->bx_nl,
+                    &m->Eproj, &m->W_o32, &m->b_o, &m->hbuf, &m->enc_mean, &m->ksplit_buf})
     dfree(*p);
-  for (__nv_bfloat16** p : {&m->Wenc, &m->Watt, &m->W_h1, &m->W_q, &m->W_g2, &m->W_ro, &m->W_o, &m->Xsrc, &m->ctxbf})
-    dfree(*p);
+  for (__nv_bfloat16** p : {&m->Watt, &m->W_h1, &m->W_q, &m->W_g2, &m->W_ro, &m->W_o, &m->ctxbf}) dfree(*p);
   dfree(m->bar);
   dfree(m->d_src);
   m->free_ws();
@@ -509,44 +504,64 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   auto cmap = [&](int i) { return i < H ? i : Hp + i - H; };
   auto hv = [&](const char* n) { return A.at(n).h; };
 
-  // ---- encoder
+  // ---- encoder: per-source-word input projections of both directions (always bf16x3):
+  //      EncIn[w] = Wemb[w].[W_f|Wx_f|W_b|Wx_b] + [b_f|bx_f|b_b|bx_b]  -> E1+E2 become a gather
   {
-    Upload w(A.at("Wemb"), st);
-    m->Wemb_src = w.d;
-    w.d = nullptr;
+    __nv_bfloat16* Wenc = dalloc<__nv_bfloat16>((size_t)6 * Hp * 2 * Ep);
+    std::vector<float> benc(6 * Hp, 0.f);
+    for (int d = 0; d < 2; ++d) {
+      const std::string p = d ? "encoder_r" : "encoder";
+      Upload W(A.at(p + "_W"), st), Wx(A.at(p + "_Wx"), st);
+      for (int g = 0; g < 2; ++g)
+        pack_T(W.d + g * H, 2 * H, E, H, Wenc, 2 * Ep, d * 3 * Hp + g * Hp, 0, 0, 0, H, Hp, Ep, st);
+      pack_T(Wx.d, H, E, H, Wenc, 2 * Ep, d * 3 * Hp + 2 * Hp, 0, 0, 0, H, Hp, Ep, st);
+      const float* b = hv((p + "_b").c_str());
+      const float* bx = hv((p + "_bx").c_str());
+      for (int j = 0; j < H; ++j) {
+        benc[d * 3 * Hp + j] = b[j];
+        benc[d * 3 * Hp + Hp + j] = b[H + j];
+        benc[d * 3 * Hp + 2 * Hp + j] = bx[j];
+      }
+    }
+    float* dbenc = upload_vec(benc, st);
+    const int Vr = round_up(Vs, 128);
+    __nv_bfloat16* Aemb = dalloc<__nv_bfloat16>((size_t)Vr * 2 * Ep);
+    {
+      Upload e(A.at("Wemb"), st);
+      pack_rows(e.d, E, Vs, E, Aemb, 2 * Ep, 0, Ep, st);
+    }
+    m->EncIn = dalloc<float>((size_t)Vs * 6 * Hp);
+    CUtensorMap ta = make_tmap_bf16(Aemb, Vr, 2 * Ep, 128), tb = make_tmap_bf16(Wenc, 6 * Hp, 2 * Ep, 128);
+    gemm_store(ta, tb, gemm_shape(Vs, nullptr, 6 * Hp, Ep, 0, true, Ep, Ep), m->EncIn, 6 * Hp, dbenc, Vs, st);
+    CK(cudaStreamSynchronize(st));
+    dfree(Wenc);
+    dfree(Aemb);
+    dfree(dbenc);
   }
-  m->Wenc = dalloc<__nv_bfloat16>((size_t)6 * Hp * 2 * Ep);
-  std::vector<float> benc(6 * Hp, 0.f);
   m->UPC = std::max(1, (H + 73) / 74);  // <= 74 CTAs per direction: both directions fill the 148 SMs
   m->NB = (H + m->UPC - 1) / m->UPC;
-  std::vector<float> uarr((size_t)2 * m->NB * 3 * m->UPC * Hp, 0.f);
-  for (int d = 0; d < 2; ++d) {
-    const std::string p = d ? "encoder_r" : "encoder";
-    Upload W(A.at(p + "_W"), st), Wx(A.at(p + "_Wx"), st);
-    for (int g = 0; g < 2; ++g)
-      pack_T(W.d + g * H, 2 * H, E, H, m->Wenc, 2 * Ep, d * 3 * Hp + g * Hp, 0, 0, 0, H, Hp, Ep, st);
-    pack_T(Wx.d, H, E, H, m->Wenc, 2 * Ep, d * 3 * Hp + 2 * Hp, 0, 0, 0, H, Hp, Ep, st);
-    const float* b = hv((p + "_b").c_str());
-    const float* bx = hv((p + "_bx").c_str());
-    for (int j = 0; j < H; ++j) {
-      benc[d * 3 * Hp + j] = b[j];
-      benc[d * 3 * Hp + Hp + j] = b[H + j];
-      benc[d * 3 * Hp + 2 * Hp + j] = bx[j];
+  {
+    std::vector<float> uarr((size_t)2 * m->NB * 3 * m->UPC * Hp, 0.f);
+    for (int d = 0; d < 2; ++d) {
+      const std::string p = d ? "encoder_r" : "encoder";
+      const float* U = hv((p + "_U").c_str());
+      const float* Ux = hv((p + "_Ux").c_str());
+      for (int cb = 0; cb < m->NB; ++cb)
+        for (int g = 0; g < 3; ++g)
+          for (int u = 0; u < m->UPC; ++u) {
+            const int jj = cb * m->UPC + u;
+            if (jj >= H) continue;
+            float* dst = &uarr[(((size_t)(d * m->NB + cb) * 3 * m->UPC) + g * m->UPC + u) * Hp];
+            for (int k = 0; k < H; ++k) dst[k] = g < 2 ? U[(size_t)k * 2 * H + g * H + jj] : Ux[(size_t)k * H + jj];
+          }
     }
-    const float* U = hv((p + "_U").c_str());
-    const float* Ux = hv((p + "_Ux").c_str());
-    for (int cb = 0; cb < m->NB; ++cb)
-      for (int g = 0; g < 3; ++g)
-        for (int u = 0; u < m->UPC; ++u) {
-          const int jj = cb * m->UPC + u;
-          if (jj >= H) continue;
-          float* dst = &uarr[(((size_t)(d * m->NB + cb) * 3 * m->UPC) + g * m->UPC + u) * Hp];
-          for (int k = 0; k < H; ++k) dst[k] = g < 2 ? U[(size_t)k * 2 * H + g * H + jj] : Ux[(size_t)k * H + jj];
-        }
+    m->Uarr = upload_vec(uarr, st);
+    std::vector<float> wt((size_t)H * C);
+    const float* wi = hv("ff_state_W");
+    for (int k = 0; k < C; ++k)
+      for (int o = 0; o < H; ++o) wt[(size_t)o * C + k] = wi[(size_t)k * H + o];
+    m->W_initT = upload_vec(wt, st);
   }
-  m->benc = upload_vec(benc, st);
-  m->Uarr = upload_vec(uarr, st);
-  m->W_init = upload_vec(std::vector<float>(hv("ff_state_W"), hv("ff_state_W") + (size_t)C * H), st);
   m->b_init = upload_vec(std::vector<float>(hv("ff_state_b"), hv("ff_state_b") + H), st);
   m->Watt = dalloc<__nv_bfloat16>((size_t)Cp * 2 * Cp);
   {
@@ -674,26 +689,22 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   }
 
   // ---- tensor maps of the weight operands
-  m->tm_Wenc = make_tmap_bf16(m->Wenc, 6 * Hp, 2 * Ep, 128);
   m->tm_Watt = make_tmap_bf16(m->Watt, Cp, 2 * Cp, 128);
   m->tm_Wh1 = make_tmap_bf16(m->W_h1, 3 * Hp, sf * Hp, 128);
   m->tm_Wq = make_tmap_bf16(m->W_q, Cp, sf * Hp, 128);
-  m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, 128);
+  m->g2_bn = Hp % 256 == 0 ? 256 : 128;  // region boundaries (2Hp, 3Hp) must be tile aligned
+  m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, m->g2_bn);
   m->tm_Wro = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 128);
   m->tm_Wo = make_tmap_bf16(m->W_o, Vp, sf * Ep, 256);
 
   // ---- encoder workspace
   m->Tpad = round_up(m->maxTx, 128);
-  m->Xsrc = dalloc<__nv_bfloat16>((size_t)m->Tpad * 2 * Ep);
-  m->Pin = dalloc<float>((size_t)m->Tpad * 6 * Hp);
   m->ctxbf = dalloc<__nv_bfloat16>((size_t)m->Tpad * 4 * Hp);
   m->hbuf = dalloc<float>(8 * Hp);  // [2 dirs][2][Hp] 64-bit tagged words
   m->enc_mean = dalloc<float>(2 * H);
-  m->ksplit_buf = dalloc<float>(std::max((size_t)3 * m->Tpad * 6 * Hp, (size_t)8 * m->Tpad * Cp));
-  m->enc_s0part = dalloc<float>(16 * H);
+  m->ksplit_buf = dalloc<float>((size_t)8 * m->Tpad * Cp);
   m->bar = dalloc<int>(2);
   m->d_src = dalloc<int>(m->maxTx);
-  m->tm_Xsrc = make_tmap_bf16(m->Xsrc, m->Tpad, 2 * Ep, 128);
   m->tm_ctxbf = make_tmap_bf16(m->ctxbf, m->Tpad, 4 * Hp, 128);
   CK(cudaStreamSynchronize(st));
 }
@@ -855,7 +866,8 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
     g.reg_n_end[0] = 2 * Hp, g.reg_k0[0] = 0, g.reg_k1[0] = Hp + Cp;  // gates: s1 U_nl + c Wc
     g.reg_n_end[1] = 3 * Hp, g.reg_k0[1] = 0, g.reg_k1[1] = Hp;       // s1 Ux_nl
     g.reg_n_end[2] = 4 * Hp, g.reg_k0[2] = Hp, g.reg_k1[2] = Hp + Cp; // c Wcx
-    gemm_store(m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, nullptr, R_max, st);
+    if (m->g2_bn == 256) gemm_store256(m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, nullptr, R_max, st);
+    else gemm_store(m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, nullptr, R_max, st);
   }
   { ProfScope p_(m, ST_GRU2); step_elementwise(EW_GRU2, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   { ProfScope p_(m, ST_GEMM_RO); gemm_store(m->tm_X, m->tm_Wro, gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp), m->RO_buf, m->ROp,
@@ -993,39 +1005,27 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
   }
   static const int cnt[CNT_N] = {1, 2, 0, 0};  // static: source of an async copy
   CK(cudaMemcpyAsync(c->counters, cnt, sizeof(cnt), cudaMemcpyHostToDevice, st));
-  {  // E1/E2: embeddings -> input projections of both directions (split bf16x3 GEMM)
-    {
-      ProfScope p_(m, ST_ENC_GATHER);
-      enc_gather(m->Wemb_src, d_src, len, m->E, m->Ep, m->Vs, m->Xsrc, c->counters + CNT_ERR, st);
-    }
-    ProfScope p_(m, ST_ENC_GEMM);  // small M: split K over the 3 precision passes to fill the SMs
-    GemmShape g = gemm_shape(len, nullptr, 6 * m->Hp, m->Ep, 0, true, m->Ep, m->Ep);
-    g.ksplit = 3;
-    const size_t stride = (size_t)m->Tpad * 6 * m->Hp;
-    gemm_store(m->tm_Xsrc, m->tm_Wenc, g, m->ksplit_buf, 6 * m->Hp, nullptr, len, st, stride);
-    splitk_reduce(m->ksplit_buf, 3, stride, len, 6 * m->Hp, 6 * m->Hp, m->benc, m->Pin, st);
-  }
-  EncDev e{};
-  e.H = m->H;
-  e.Hp = m->Hp;
-  e.NB = m->NB;
-  e.UPC = m->UPC;
-  e.Uarr = m->Uarr;
-  e.Pin = m->Pin;
-  e.ctx = c->ctx;
-  e.hx = reinterpret_cast<unsigned long long*>(m->hbuf);
-  e.W_init = m->W_init;
-  e.b_init = m->b_init;
-  e.ctxbf = m->ctxbf;
-  e.mean = m->enc_mean;
-  e.s0part = m->enc_s0part;
-  {  // E3/E4: recurrence
+  {  // E1-E6: gather of the precomputed input projections, bi-GRU recurrence, means, s0, ctx hi|lo
+    EncDev e{};
+    e.H = m->H;
+    e.Hp = m->Hp;
+    e.NB = m->NB;
+    e.UPC = m->UPC;
+    e.Vs = m->Vs;
+    e.Uarr = m->Uarr;
+    e.src = d_src;
+    e.encin = m->EncIn;
+    e.ctx = c->ctx;
+    e.ctxbf = m->ctxbf;
+    e.hx = reinterpret_cast<unsigned long long*>(m->hbuf);
+    e.mean = m->enc_mean;
+    e.bar = m->bar;
+    e.err = c->counters + CNT_ERR;
+    e.W_initT = m->W_initT;
+    e.b_init = m->b_init;
+    e.S0 = c->S;
     ProfScope p_(m, ST_ENC_RECUR);
     enc_recur(e, len, st);
-  }
-  {  // E5: s0 into slot 0 (+ split copy of ctx)
-    ProfScope p_(m, ST_ENC_INIT);
-    enc_init(e, len, c->S, st);
   }
   {  // E7: pctx = ctx.Wc_att + b_att
     ProfScope p_(m, ST_ENC_PCTX);
@@ -1350,6 +1350,56 @@ nmt_status nmt_debug_intermediates(nmt_ctx* c, nmt_state node, float* s1, float*
     if (t) std::memcpy(t, ht.data(), m->E * 4);
     if (logZ) *logZ = z;
     if (argmax) *argmax = am;
+  });
+}
+
+nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_t epi, int32_t ksplit, int32_t iters,
+                          float* ms_out) {
+  if (M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || !ms_out || (epi == 0 && N % 128) || (epi >= 1 && N % 256))
+    return fail(NMT_ERR_INVALID_ARG, "nmt_bench_gemm: bad shape");
+  return guard([&] {
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const int sf = split ? 2 : 1, Mp = round_up(M, 128);
+    __nv_bfloat16* a = dalloc<__nv_bfloat16>((size_t)Mp * sf * K);
+    __nv_bfloat16* b = dalloc<__nv_bfloat16>((size_t)N * sf * K);
+    float* c = dalloc<float>((size_t)ksplit * Mp * N);
+    float4* part = dalloc<float4>((size_t)Mp * 2 * kNumSMs);
+    int* cpm = dalloc<int>(1);
+    {  // small random operands (values do not matter for timing)
+      std::vector<__nv_bfloat16> h((size_t)Mp * sf * K);
+      for (size_t i = 0; i < h.size(); ++i) h[i] = __float2bfloat16_rn((float)((i * 2654435761u) % 1000) * 1e-3f - 0.5f);
+      CK(cudaMemcpy(a, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+      std::vector<__nv_bfloat16> hb((size_t)N * sf * K);
+      for (size_t i = 0; i < hb.size(); ++i) hb[i] = __float2bfloat16_rn((float)((i * 40503u) % 1000) * 1e-3f - 0.5f);
+      CK(cudaMemcpy(b, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice));
+    }
+    CUtensorMap ta = make_tmap_bf16(a, Mp, sf * K, 128), tb = make_tmap_bf16(b, N, sf * K, epi >= 1 ? 256 : 128);
+    GemmShape g = gemm_shape(M, nullptr, N, K, 0, split != 0, K, K);
+    g.ksplit = ksplit;
+    auto run = [&] {
+      if (epi == 1) gemm_lse(ta, tb, g, part, N, M, st, cpm);
+      else if (epi == 2) gemm_store256(ta, tb, g, c, N, nullptr, M, st, (size_t)Mp * N);
+      else gemm_store(ta, tb, g, c, N, nullptr, M, st, (size_t)Mp * N);
+    };
+    for (int i = 0; i < 3; ++i) run();
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    for (int i = 0; i < iters; ++i) run();
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(ms_out, e0, e1));
+    *ms_out /= iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    dfree(a);
+    dfree(b);
+    dfree(c);
+    dfree(part);
+    dfree(cpm);
+    cudaStreamDestroy(st);
   });
 }
 

@@ -386,6 +386,19 @@ void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, 
   launch<128, 6, EPI_STORE>(a, b, g, ep, M_max, st);
 }
 
+// fp32 output GEMM with 128 x 256 tiles (A reuse x2; fewer tiles)
+void gemm_store256(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc,
+                   const float* bias, int M_max, cudaStream_t st, size_t split_stride) {
+  gemm_validate(g, 256);
+  if (g.ksplit > 1 && (bias || !split_stride)) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: split-K partials take no bias");
+  EpiParams ep{};
+  ep.out = out;
+  ep.ldc = ldc;
+  ep.bias = bias;
+  ep.split_stride = split_stride;
+  launch<256, 4, EPI_STORE>(a, b, g, ep, M_max, st);
+}
+
 // fused vocabulary GEMM + online log-sum-exp partials; BN = 256.
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
               cudaStream_t st, int* cpm_out) {

@@ -788,35 +788,17 @@ void full_row(const float* T, const float* Wo32, const float* bo, const float* l
 }
 
 // ===================================================================================== encoder
-// E1: gather source embeddings into the split bf16 A operand of the input projections.
-__global__ void k_enc_gather(const float* __restrict__ Wemb, const int* __restrict__ src, int Tx, int E, int Ep, int Vs,
-                             __nv_bfloat16* X, int* err) {
-  pdl_enter();
-  const int j = blockIdx.x;
-  if (j >= Tx) return;
-  int id = src[j];
-  if (id < 0 || id >= Vs) {  // device-resident ids are validated here (reported by nmt_ctx_check)
-    if (threadIdx.x == 0) atomicOr(err, ERR_TOKEN);
-    id = 0;
-  }
-  const float* e = Wemb + (int64_t)id * E;
-  for (int k = threadIdx.x; k < E; k += blockDim.x) store_split(X + (int64_t)j * 2 * Ep + k, Ep, e[k]);
-}
-void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, int Vs, __nv_bfloat16* X, int* err,
-                cudaStream_t st) {
-  launch_pdl(k_enc_gather, Tx, 128, 0, st, Wemb, src, Tx, E, Ep, Vs, X, err);
-  CK_LAUNCH();
-}
-
-// E3/E4: persistent bidirectional GRU recurrence.  CTAs [0, NB) run the forward direction,
+// E1-E6 in one persistent cooperative kernel.  CTAs [0, NB) run the forward direction,
 // [NB, 2NB) the backward one (both fill the 148 SMs).  Each CTA owns UPC hidden units; the
 // 3*UPC columns of [U | Ux] it needs live in REGISTERS for the whole sentence (warp w owns
 // columns w, w+12, w+24, w+36; lane l holds the float4s k = l + 32 i of each), so a time step
-// reads no weights at all.  h_t is exchanged through global memory as 64-bit (value, tag = t+1)
-// words: a reader polls until every word carries the tag of the step it needs, which merges the
-// grid-wide barrier into the data read (one L2 round trip per step).  Double-buffered by parity:
-// a writer can be at most one step ahead of the slowest reader.
-// Pin = x.[W|Wx] + [b|bx] for both directions (GEMM E2), layout [Tx][dir*3Hp + gate*Hp + j].
+// reads no weights at all.  The input projections x_j.[W|Wx] + [b|bx] are rows of a table
+// precomputed per source word at load (E1+E2 become a gather).  h_t is exchanged through global
+// memory as 64-bit (value, tag = t+1) words: a reader polls until every word carries the tag of
+// the step it needs, which merges the grid-wide barrier into the data read (one L2 round trip
+// per step).  Double-buffered by parity: a writer is at most one step ahead of the slowest reader.
+// Tail (E5): each CTA publishes the time-mean of its units, one grid barrier, then the CTAs split
+// s0 = tanh(mean . W_init + b_init) and write the bf16 hi|lo copy of ctx for the pctx GEMM (E7).
 constexpr int kRecurThreads = 384, kRecurWarps = 12, kRecurCPW = 4;
 template <int KI>  // Hp = 128 * KI
 __global__ void __launch_bounds__(kRecurThreads, 1) k_enc_recur(EncDev e, int Tx) {
@@ -843,16 +825,26 @@ __global__ void __launch_bounds__(kRecurThreads, 1) k_enc_recur(EncDev e, int Tx
   unsigned long long* hx = e.hx + (size_t)dir * 2 * Hp;  // [2][Hp] tagged words of this direction
   const bool gate = threadIdx.x < UPC && u0 + (int)threadIdx.x < H;
   const int jj = u0 + threadIdx.x;
-  float hself = 0.f;
+  float hself = 0.f, hsum = 0.f;
+  // input projections (independent of h) are fetched one step ahead: the table rows live in HBM
+  auto fetch_pin = [&](int t, float& r_, float& u_, float& x_) {
+    const int j = dir == 0 ? t : Tx - 1 - t;
+    int id = e.src[j];
+    if (id < 0 || id >= e.Vs) {  // device-resident ids are validated here (nmt_ctx_check)
+      atomicOr(e.err, ERR_TOKEN);
+      id = 0;
+    }
+    const float* pin = e.encin + (int64_t)id * 6 * Hp + dir * 3 * Hp;
+    r_ = __ldg(pin + jj);
+    u_ = __ldg(pin + Hp + jj);
+    x_ = __ldg(pin + 2 * Hp + jj);
+  };
+  float n_r = 0.f, n_u = 0.f, n_x = 0.f;
+  if (gate) fetch_pin(0, n_r, n_u, n_x);
   for (int t = 0; t < Tx; ++t) {
     const int j = dir == 0 ? t : Tx - 1 - t;
-    float p_r = 0.f, p_u = 0.f, p_x = 0.f;
-    if (gate) {  // input projections of this step (independent of h): issue early
-      const float* pin = e.Pin + (int64_t)j * 6 * Hp + dir * 3 * Hp;
-      p_r = pin[jj];
-      p_u = pin[Hp + jj];
-      p_x = pin[2 * Hp + jj];
-    }
+    const float p_r = n_r, p_u = n_u, p_x = n_x;
+    if (gate && t + 1 < Tx) fetch_pin(t + 1, n_r, n_u, n_x);
     if (t == 0) {
       for (int k = threadIdx.x; k < H4; k += kRecurThreads) h4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
@@ -904,11 +896,62 @@ __global__ void __launch_bounds__(kRecurThreads, 1) k_enc_recur(EncDev e, int Tx
       const float ug = 1.f / (1.f + expf(-(p_u + dots[UPC + u])));
       const float ht = tanhf(rg * dots[2 * UPC + u] + p_x);
       hself = ug * hself + (1.f - ug) * ht;
-      e.ctx[(int64_t)j * 2 * Hp + dir * Hp + jj] = hself;
+      hsum += hself;
       const unsigned long long word = ((unsigned long long)(unsigned)(t + 1) << 32) | __float_as_uint(hself);
       asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(hx + (size_t)((t + 1) & 1) * Hp + jj), "l"(word)
                    : "memory");
+      const int cidx = dir * Hp + jj;  // padded context column
+      e.ctx[(int64_t)j * 2 * Hp + cidx] = hself;
+      __nv_bfloat16 hi, lo;
+      split_bf16(hself, hi, lo);
+      e.ctxbf[(int64_t)j * 4 * Hp + cidx] = hi;
+      e.ctxbf[(int64_t)j * 4 * Hp + 2 * Hp + cidx] = lo;
     }
+  }
+  // ---- E5: time means -> grid barrier -> s0 slices
+  if (gate) e.mean[dir * H + jj] = hsum / (float)Tx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(e.bar) : "memory");
+    int v;
+    const long long t0 = clock64();
+    do {
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(e.bar) : "memory");
+      if (clock64() - t0 > (1ll << 32)) asm volatile("trap;");
+    } while (v < (int)gridDim.x);
+  }
+  __syncthreads();
+  const int C = 2 * H;
+  float* msm = reinterpret_cast<float*>(h4);  // reuse the h buffer (2H <= 2Hp... staged in two halves)
+  const int per = (H + gridDim.x - 1) / gridDim.x;
+  float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+  const int o = blockIdx.x * per + warp;  // warp per output; W_initT rows are contiguous
+  for (int half = 0; half < 2; ++half) {
+    const int k0 = half * Hp;
+    const int kn = min(Hp, C - k0);
+    for (int k = threadIdx.x; k < Hp; k += kRecurThreads) msm[k] = k < kn ? __ldcg(e.mean + k0 + k) : 0.f;
+    __syncthreads();
+    if (warp < per && o < H) {
+      const float* wr = e.W_initT + (int64_t)o * C + k0;
+      for (int k = 4 * lane; k < kn; k += 128) {  // kn is a multiple of 4 except in tiny models
+        if (k + 3 < kn) {
+          const float4 wv = *reinterpret_cast<const float4*>(wr + k);
+          acc0 = fmaf(msm[k], wv.x, acc0);
+          acc1 = fmaf(msm[k + 1], wv.y, acc1);
+          acc2 = fmaf(msm[k + 2], wv.z, acc2);
+          acc3 = fmaf(msm[k + 3], wv.w, acc3);
+        } else {
+          for (int kk = k; kk < kn; ++kk) acc0 = fmaf(msm[kk], wr[kk], acc0);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (warp < per && o < H) {
+    float s = (acc0 + acc1) + (acc2 + acc3);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) e.S0[o] = tanhf(s + e.b_init[o]);
   }
 }
 
@@ -921,8 +964,9 @@ static void launch_recur(const EncDev& e, int Tx, cudaStream_t st) {
 }
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
   if (3 * e.UPC > kRecurWarps * kRecurCPW || 3 * e.UPC > 48) throw NmtError(NMT_ERR_SHAPE, "encoder: UPC too large");
-  // tags of both directions and parities start at 0 (never a valid tag)
+  // tags of both directions and parities start at 0 (never a valid tag); the tail barrier at 0
   CK(cudaMemsetAsync(e.hx, 0, (size_t)2 * 2 * e.Hp * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(e.bar, 0, sizeof(int), st));
   switch (e.Hp / 128) {
     case 1: launch_recur<1>(e, Tx, st); break;
     case 2: launch_recur<2>(e, Tx, st); break;
@@ -934,77 +978,6 @@ void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
     case 8: launch_recur<8>(e, Tx, st); break;
     default: throw NmtError(NMT_ERR_SHAPE, "encoder: dim_hid > 1024");
   }
-}
-
-// E5: s0 = tanh(mean_j ctx_j . W_init + b_init) -> arena slot 0; also the split copy of ctx for E7.
-// (a) column means + split copy, (b) K-split partial mat-vec, (c) ordered sum + tanh.
-__global__ void k_enc_mean(EncDev e, int Tx) {
-  pdl_enter();
-  __shared__ float red[8][33];
-  const int Hp = e.Hp, H = e.H;
-  const int c = blockIdx.x * 32 + (threadIdx.x & 31);  // padded context column
-  const int jl = threadIdx.x >> 5;                      // 8 row lanes
-  float s = 0.f;
-  if (c < 2 * Hp) {
-#pragma unroll 4
-    for (int j = jl; j < Tx; j += 8) {
-      const float v = e.ctx[(int64_t)j * 2 * Hp + c];
-      s += v;
-      store_split(e.ctxbf + (int64_t)j * 4 * Hp + c, 2 * Hp, v);
-    }
-  }
-  red[jl][threadIdx.x & 31] = s;
-  __syncthreads();
-  if (jl == 0 && c < 2 * Hp) {
-    float t = 0.f;
-    for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x];
-    const int real = c < Hp ? (c < H ? c : -1) : (c - Hp < H ? H + c - Hp : -1);
-    if (real >= 0) e.mean[real] = t / (float)Tx;
-  }
-}
-constexpr int kInitKS = 16;  // K splits of the s0 mat-vec
-__global__ void k_enc_s0_part(EncDev e) {
-  pdl_enter();
-  const int H = e.H, C = 2 * H;
-  const int o = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int kchunk = (C + kInitKS - 1) / kInitKS;
-  const int k0 = blockIdx.y * kchunk, k1 = min(C, k0 + kchunk);
-  __shared__ float red[8][32];
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-  if (o < H) {
-    int k = k0 + warp;
-    for (; k + 3 * nw < k1; k += 4 * nw) {
-      a0 = fmaf(e.mean[k], e.W_init[(int64_t)k * H + o], a0);
-      a1 = fmaf(e.mean[k + nw], e.W_init[(int64_t)(k + nw) * H + o], a1);
-      a2 = fmaf(e.mean[k + 2 * nw], e.W_init[(int64_t)(k + 2 * nw) * H + o], a2);
-      a3 = fmaf(e.mean[k + 3 * nw], e.W_init[(int64_t)(k + 3 * nw) * H + o], a3);
-    }
-    for (; k < k1; k += nw) a0 = fmaf(e.mean[k], e.W_init[(int64_t)k * H + o], a0);
-  }
-  red[warp][threadIdx.x & 31] = (a0 + a1) + (a2 + a3);
-  __syncthreads();
-  if (warp == 0 && o < H) {
-    float t = 0.f;
-    for (int w = 0; w < nw; ++w) t += red[w][threadIdx.x];
-    e.s0part[blockIdx.y * H + o] = t;
-  }
-}
-__global__ void k_enc_s0_final(EncDev e, float* S0) {
-  pdl_enter();
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= e.H) return;
-  float t = 0.f;
-  for (int ks = 0; ks < kInitKS; ++ks) t += e.s0part[ks * e.H + o];
-  S0[o] = tanhf(t + e.b_init[o]);
-}
-void enc_init(const EncDev& e, int Tx, float* S0, cudaStream_t st) {
-  launch_pdl(k_enc_mean, (2 * e.Hp + 31) / 32, 256, 0, st, e, Tx);
-  CK_LAUNCH();
-  launch_pdl(k_enc_s0_part, dim3((e.H + 31) / 32, kInitKS), 256, 0, st, e);
-  CK_LAUNCH();
-  launch_pdl(k_enc_s0_final, (e.H + 127) / 128, 128, 0, st, e, S0);
-  CK_LAUNCH();
 }
 
 }  // namespace nmt

@@ -73,16 +73,19 @@ struct AttnCtx {
 };
 
 struct EncDev {
-  int H, Hp, NB, UPC;
+  int H, Hp, NB, UPC, Vs;
   const float* Uarr;     // [2][NB][3*UPC][Hp] recurrent weights per CTA (rows zero-padded to Hp)
-  const float* Pin;      // [Tx][6Hp]
+  const int* src;        // [Tx] source ids (device)
+  const float* encin;    // [Vs][6Hp] precomputed x.[W|Wx] + [b|bx] of both directions per source word
   float* ctx;            // [Tx][2Hp]
+  __nv_bfloat16* ctxbf;  // [Tx][4Hp] hi | lo copy for the pctx GEMM
   unsigned long long* hx;  // [2 dirs][2 parities][Hp] (tag << 32 | float bits)
-  const float* W_init;   // [2H][H]
-  const float* b_init;   // [H]
   float* mean;           // [2H] mean_j ctx_j (real indices)
-  float* s0part;         // [16][H] K-split partial sums
-  __nv_bfloat16* ctxbf;  // [Tx][4Hp] hi | lo
+  int* bar;              // [1] tail grid barrier
+  int* err;              // validation flags of the context
+  const float* W_initT;  // [H][2H] ff_state_W transposed (contiguous per output)
+  const float* b_init;   // [H]
+  float* S0;             // [H] arena slot 0
 };
 
 enum { EW_GATHER, EW_GRU1, EW_ATTN, EW_GRU2, EW_READOUT, EW_FINALIZE };
@@ -103,9 +106,6 @@ void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const floa
                 int* out_child32, long long* out_child64, int* out_argmax, cudaStream_t st);
 void full_row(const float* T, const float* Wo32, const float* bo, const float* logZ, int slot, int Ep, int V,
               float* out, cudaStream_t st);
-void enc_gather(const float* Wemb, const int* src, int Tx, int E, int Ep, int Vs, __nv_bfloat16* X, int* err,
-                cudaStream_t st);
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st);
-void enc_init(const EncDev& e, int Tx, float* S0, cudaStream_t st);
 
 }  // namespace nmt

@@ -25,7 +25,7 @@ EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "n
            "nmt_root", "nmt_ctx_free", "nmt_score_batch", "nmt_score_batch_dev", "nmt_ctx_check", "nmt_ctx_stats",
            "nmt_inject_states", "nmt_logprobs_full", "nmt_debug_encoder", "nmt_debug_intermediates",
            "nmt_test_gemm", "nmt_encode_dev", "nmt_inject_states_dev", "nmt_launch_count", "nmt_profile",
-           "nmt_profile_read", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
+           "nmt_profile_read", "nmt_bench_gemm", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
            "nmt_ensemble_free"]
 
 
@@ -92,6 +92,7 @@ def lib() -> C.CDLL:
             "nmt_launch_count": (C.c_longlong, []),
             "nmt_profile": (i32, [vp, i32]),
             "nmt_profile_read": (i32, [vp, vp, vp]),
+            "nmt_bench_gemm": (i32, [i32, i32, i32, i32, i32, i32, i32, C.POINTER(C.c_float)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -255,6 +256,13 @@ def test_gemm(A: np.ndarray, B: np.ndarray, bias: Optional[np.ndarray] = None, s
     b = None if bias is None else _c(bias, np.float32)
     _check(lib().nmt_test_gemm(M, N, K, int(split), _ptr(A), _ptr(B), _ptr(b), _ptr(out)))
     return out
+
+
+def bench_gemm(M: int, N: int, K: int, split: bool = False, epi: int = 0, ksplit: int = 1, iters: int = 20) -> float:
+    """Average milliseconds of the tcgen05 GEMM engine on device-resident operands (tuning aid)."""
+    ms = C.c_float()
+    _check(lib().nmt_bench_gemm(M, N, K, int(split), epi, ksplit, iters, C.byref(ms)))
+    return ms.value
 
 
 class Ensemble:
