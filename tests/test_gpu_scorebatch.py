@@ -1,0 +1,102 @@
+"""ScoreBatch forest driver (Alg. 1) on the GPU path vs the float64 oracle, the Fig. 1 worked
+example (tests/golden/fig1_forest.txt), C3-style stack-decoding batches and the
+ensemble hook with a single-rank NCCL communicator."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = {"fp32class": 1e-3, "bf16": 2e-2}
+
+
+def _fig1():
+    hyps, info = {}, {}
+    for ln in open(os.path.join(GOLD, "fig1_forest.txt")):
+        ln = ln.strip()
+        if not ln or ln.startswith("#"):
+            continue
+        if ln.startswith("hyp"):
+            h, rest = ln[4:].split(":")
+            hyps[int(h)] = [tuple(int(w[1:]) + 2 for w in ph.split()) for ph in rest.split("|")]
+        else:
+            k, *v = ln.split()
+            info[k] = v
+    return [(h, t) for h in sorted(hyps) for t in hyps[h]], info
+
+
+@pytest.mark.parametrize("prec", ["fp32class", "bf16"])
+def test_fig1_through_the_gpu_driver(prec):
+    from paper_1605_04809_b200 import nmt, scorebatch
+    pairs, info = _fig1()
+    d = synth.Dims(8, 16, 50, 50, "tanh")
+    p = synth.make_model(d, 21)
+    M = nmt.Model(synth.params_bytes(d, p), precision=prec)
+    src = synth.make_source(d.vocab_src, 5, seed=6)
+    ctx = M.encode(src)
+    rng = np.random.default_rng(1)
+    s = np.tanh(rng.standard_normal((2, d.dim_hid))).astype(np.float32)
+    hyps = ctx.inject_states(s, [4, 9])
+    out, st = scorebatch.score_batch(ctx, hyps, pairs)
+    assert st.steps == int(info["steps"][0])
+    assert st.edges_per_depth == [int(x) for x in info["edges_per_depth"]]
+    assert st.rows_per_depth == [int(x) for x in info["parent_rows_per_depth"]]
+    assert st.naive_words == int(info["naive_words"][0])
+    sess = O.Session(O.Model(d, p), src)
+    oh = [sess.inject_state(s[i], y) for i, y in enumerate([4, 9])]
+    ref = O.score_forest(sess, oh, pairs)
+    for k, (lp, _) in out.items():
+        assert abs(lp - ref[k]) < TOL[prec] * len(k[1])
+
+
+@pytest.mark.parametrize("prec", ["fp32class", "bf16"])
+def test_stack_batch_dedup_tiny(prec):
+    """C3-style stack: distinct (h, t) expansions over zipf parents, phrase lengths 1..5,
+    branching shrinking with depth.  Ids and scores must match the oracle; the
+    number of stepped rows is bounded by the edges, and a re-scored stack steps nothing."""
+    from paper_1605_04809_b200 import nmt, scorebatch
+    d = synth.Dims(8, 16, 50, 50, "maxout")
+    p = synth.make_model(d, 1605)
+    M = nmt.Model(synth.params_bytes(d, p), precision=prec)
+    src = synth.make_source(d.vocab_src, 12, seed=1606)
+    ctx = M.encode(src)
+    sess = O.Session(O.Model(d, p), src)
+    H = 16
+    s, y = synth.make_states(H, d.dim_hid, d.vocab_tgt, seed=1607)
+    gh = ctx.inject_states(s, y)
+    oh = [sess.inject_state(s[i], int(y[i])) for i in range(H)]
+    pairs = synth.make_stack_expansions(120, H, d.vocab_tgt, seed=1608)
+    out, st = scorebatch.score_batch(ctx, gh, pairs)
+    ref = O.score_forest(sess, oh, pairs)
+    worst = max(abs(out[k][0] - ref[k]) / len(k[1]) for k in out)
+    assert worst < TOL[prec]
+    assert sum(st.rows_per_depth) <= sum(st.edges_per_depth) <= st.naive_words
+    assert st.steps == max(len(t) for _, t in pairs)
+    n0 = ctx.stats()
+    out2, st2 = scorebatch.score_batch(ctx, gh, pairs)  # cache: no new rows, identical values
+    assert ctx.stats() == n0 and sum(st2.rows_per_depth) == 0
+    assert all(out2[k] == out[k] for k in out)
+
+
+def test_ensemble_single_rank_nccl():
+    """nmt_ensemble_combine with one member (NCCL communicator of size 1) reproduces the oracle's
+    combine of a single model: mode 0 = weight * logp, mode 1 = log(weight * p)."""
+    import torch
+    from paper_1605_04809_b200 import nmt
+    uid = nmt.Ensemble.unique_id()
+    ens = nmt.Ensemble(1, 0, uid, 0)
+    rng = np.random.default_rng(0)
+    lp = np.log(rng.dirichlet(np.ones(64), size=1)[0]).astype(np.float32)
+    d_in = torch.from_numpy(lp).cuda()
+    d_out = torch.empty_like(d_in)
+    st = torch.cuda.current_stream().cuda_stream
+    for mode, w in [(0, 1.0), (0, 0.25), (1, 1.0), (1, 0.5)]:
+        ens.combine(d_in.data_ptr(), 64, w, mode, 0, d_out.data_ptr(), st)
+        torch.cuda.synchronize()
+        ref = O.ensemble_combine([lp.astype(np.float64)], [w], mode)
+        assert np.max(np.abs(d_out.cpu().numpy() - ref)) < 1e-5
+    ens.close()

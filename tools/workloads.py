@@ -1,0 +1,126 @@
+"""Secondary workloads of BASELINE.json:configs (not the bench.py headline line):
+
+  c3     Ru->En shape (V_t 50k, V_s 100k): per sentence (L ~ U[10,50]) one stack of 4096 distinct
+         (hypothesis, phrase) expansions over 1024 hypothesis states, scored with the ScoreBatch
+         forest driver (one nmt_score_batch per depth) - word-scores/s, rows/s and the dedup ratio
+         naive words : collapsed edges (word-scores) : stepped rows.
+  sweep  C2 model (V_t 100k): hypothesis batch-size sweep R in 64..16384 (x3 candidates) through the
+         device-resident C ABI - word-scores/s and the vocabulary GEMM's TFLOP/s / fraction of the
+         measured bf16 peak per R (HBM-bound W_o stream at small R, tensor-bound at large R).
+Prints one JSON line per measurement point.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+
+
+def peaks():
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    return json.load(open(p)) if os.path.exists(p) else {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
+
+
+def c3(a):
+    import torch
+    from paper_1605_04809_b200 import nmt, scorebatch
+    d = synth.Dims(500, 1024, 100000, 50000, a.readout)
+    M = nmt.Model(synth.params_bytes(d, synth.make_model(d, 1605)), precision=a.precision)
+    rng = np.random.default_rng(1605)
+    tot_t = tot_e = tot_r = tot_n = 0
+    for k in range(a.sentences + 1):
+        L = int(rng.integers(10, 51))
+        src = synth.make_source(d.vocab_src, L, seed=1605 + k)
+        s, y = synth.make_states(1024, d.dim_hid, d.vocab_tgt, seed=3000 + k)
+        pairs = synth.make_stack_expansions(4096, 1024, d.vocab_tgt, seed=4000 + k)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx = M.encode(src)
+        hyps = ctx.inject_states(s, y)
+        out, st = scorebatch.score_batch(ctx, hyps, pairs)
+        ctx.close()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if k == 0:
+            continue  # warm-up sentence
+        tot_t += dt
+        tot_e += sum(st.edges_per_depth)
+        tot_r += sum(st.rows_per_depth)
+        tot_n += st.naive_words
+        print(json.dumps({"workload": "c3", "sentence": k, "src_len": L + 1, "ms": 1000 * dt,
+                          "steps": st.steps, "edges_per_depth": st.edges_per_depth,
+                          "rows_per_depth": st.rows_per_depth, "naive_words": st.naive_words}), flush=True)
+    print(json.dumps({"workload": "c3 summary", "precision": a.precision, "readout": a.readout,
+                      "sentences": a.sentences, "word_scores_per_s": tot_e / tot_t, "rows_per_s": tot_r / tot_t,
+                      "dedup naive:edges:rows": [1.0, tot_e / tot_n, tot_r / tot_n],
+                      "timing": "host wall clock around encode + inject + ScoreBatch driver (host C ABI), "
+                                "synchronized"}), flush=True)
+
+
+def sweep(a):
+    import torch
+    from paper_1605_04809_b200 import nmt
+    d = synth.Dims(500, 1024, 50000, 100000, a.readout)
+    st = torch.cuda.Stream()
+    torch.cuda.set_stream(st)
+    M = nmt.Model(synth.params_bytes(d, synth.make_model(d, 2016)), precision=a.precision, stream=st.cuda_stream)
+    pk = peaks()
+    src = torch.from_numpy(synth.make_source(d.vocab_src, 49, seed=1)).cuda()
+    flush = torch.empty(256 * 2**20 // 4, device="cuda")
+    vi = nmt.STAGES.index("vocab_gemm_lse")
+    for R in [64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384]:
+        s, y = synth.make_states(R, d.dim_hid, d.vocab_tgt, seed=R)
+        off, w = synth.make_candidates(R, 3, d.vocab_tgt, seed=R + 1)
+        ds, dy, doff, dw = (torch.from_numpy(x).cuda() for x in (s, y, off, w))
+        ids = torch.empty(R, dtype=torch.int32, device="cuda")
+        lp = torch.empty(3 * R, device="cuda")
+        ch = torch.empty(3 * R, dtype=torch.int32, device="cuda")
+        ctx = M.encode_dev(src.data_ptr(), 50)
+        ctx.inject_states_dev(R, ds.data_ptr(), dy.data_ptr(), ids.data_ptr())
+
+        def score():  # re-score fresh parents every iteration: inject new nodes each time
+            ctx.inject_states_dev(R, ds.data_ptr(), dy.data_ptr(), ids.data_ptr())
+            ctx.score_batch_dev(R, ids.data_ptr(), doff.data_ptr(), 3 * R, dw.data_ptr(), lp.data_ptr(),
+                                ch.data_ptr(), None)
+        for _ in range(3):
+            score()
+        M.profile(1)
+        M.profile_read()
+        ev = []
+        for _ in range(a.iters):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            score()
+            e1.record(st)
+            ev.append((e0, e1))
+        torch.cuda.synchronize()
+        ms, cnt = M.profile_read()
+        M.profile(0)
+        t = sum(e0.elapsed_time(e1) for e0, e1 in ev) / a.iters
+        vms = ms[vi] / cnt[vi]
+        tf = 2 * R * d.vocab_tgt * d.dim_emb / (vms / 1000) / 1e12
+        wo_gbs = 2 * 512 * 100096 / (vms / 1000) / 1e9
+        ctx.close()
+        print(json.dumps({"workload": "sweep", "R": R, "ms_per_batch": t, "word_scores_per_s": 3 * R / (t / 1000),
+                          "rows_per_s": R / (t / 1000), "vocab_ms": vms, "vocab_tflops": tf,
+                          "vocab_frac_bf16_peak": tf / pk["bf16_tflops"], "W_o_stream_GBps": wo_gbs,
+                          "W_o_frac_hbm": wo_gbs / pk["hbm_gbs"],
+                          "note": "per batch: inject R parents + nmt_score_batch_dev (no encode), L2 flushed"}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("what", choices=["c3", "sweep"])
+    ap.add_argument("--precision", default="bf16")
+    ap.add_argument("--readout", default="tanh")
+    ap.add_argument("--sentences", type=int, default=5)
+    ap.add_argument("--iters", type=int, default=10)
+    a = ap.parse_args()
+    c3(a) if a.what == "c3" else sweep(a)
