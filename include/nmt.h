@@ -138,6 +138,18 @@ NMT_API nmt_status nmt_score_batch(nmt_ctx* c, int32_t n_parents, const nmt_stat
 NMT_API nmt_status nmt_score_batch_dev(nmt_ctx* c, int32_t n_parents, const int32_t* parents,
                                const int32_t* cand_offsets, int32_t n_cand, const int32_t* cand_words,
                                float* out_logprob, int32_t* out_child, int32_t* out_argmax);
+/* ScoreBatch (Alg. 1) in one call.  Pair i expands hypothesis state hyp_states[i]
+ * [host] by the phrase phrase_words[phrase_offsets[i] .. phrase_offsets[i+1]) [host] (1..16 words;
+ * an empty phrase -> NMT_ERR_INVALID_ARG "empty expansion").  The library builds the
+ * forest of per-hypothesis prefix trees, runs ONE batched step per tree depth
+ * (shared prefixes collapse, states are cached for later calls) and
+ * returns out_logp[i] = sum of the phrase's word log-probs and out_state[i] = the state after the
+ * phrase [host, n_pairs each].  stats [host, 33 int32, may be NULL]: [0] = steps (= the longest
+ * phrase), [1..16] = collapsed edges (word-scores) per depth, [17..32] = decoder
+ * rows stepped per depth.                                                                        */
+NMT_API nmt_status nmt_score_forest(nmt_ctx* c, int32_t n_pairs, const nmt_state* hyp_states,
+                                    const int32_t* phrase_offsets, const int32_t* phrase_words, float* out_logp,
+                                    nmt_state* out_state, int32_t* stats);
 /* Waits for the model stream and reports a device-side validation error of earlier _dev calls. */
 NMT_API nmt_status nmt_ctx_check(nmt_ctx* c);
 /* Number of nodes and stepped nodes in the context's arena (synchronises the stream). */

@@ -19,6 +19,7 @@
 #include <mutex>
 #include <sstream>
 #include <tuple>
+#include <unordered_map>
 #include <vector>
 
 #include "internal.h"
@@ -146,6 +147,11 @@ struct nmt_model {
   int *out_child = nullptr, *out_amax = nullptr;
   float* in_s = nullptr;
   CUtensorMap tm_As, tm_X, tm_At;
+  // ScoreBatch forest workspace (nmt_score_forest)
+  int* fws_i = nullptr;
+  size_t fws_i_cap = 0;
+  float* fws_f = nullptr;
+  size_t fws_f_cap = 0;
   // pinned host staging
   void* pin = nullptr;
   size_t pin_bytes = 0;
@@ -186,6 +192,8 @@ static void free_all_model(nmt_model* m) {
   dfree(m->bar);
   dfree(m->d_src);
   m->free_ws();
+  dfree(m->fws_i);
+  dfree(m->fws_f);
   if (m->pin) cudaFreeHost(m->pin);
   m->pin = nullptr;
 }
@@ -1172,6 +1180,189 @@ nmt_status nmt_score_batch_dev(nmt_ctx* c, int32_t np, const int32_t* parents, c
     c->n_nodes += nc;  // upper bounds until the next sync
     c->n_slots += np;
     c->stale = true;
+  });
+}
+
+// ScoreBatch (Alg. 1) in one call: host prefix-tree forest, one H2D, one
+// device step per depth (parents of depth d+1 gathered on the device from depth d's children),
+// per-pair path sums on the device, one D2H.
+nmt_status nmt_score_forest(nmt_ctx* c, int32_t n_pairs, const nmt_state* hyp, const int32_t* poff,
+                            const int32_t* pwords, float* out_logp, nmt_state* out_state, int32_t* stats) {
+  if (!c || n_pairs < 0) return fail(NMT_ERR_INVALID_ARG, "bad argument");
+  if (n_pairs == 0) {
+    if (stats) std::memset(stats, 0, 33 * sizeof(int32_t));
+    return NMT_OK;
+  }
+  if (!hyp || !poff || !pwords || !out_logp || !out_state) return fail(NMT_ERR_INVALID_ARG, "NULL array");
+  nmt_model* m = c->m;
+  if (poff[0] != 0) return fail(NMT_ERR_INVALID_ARG, "phrase_offsets[0] != 0");
+  for (int i = 0; i < n_pairs; ++i) {
+    if (poff[i + 1] <= poff[i]) return fail(NMT_ERR_INVALID_ARG, "empty expansion (pair " + std::to_string(i) + ")");
+    if (poff[i + 1] - poff[i] > 16) return fail(NMT_ERR_CAPACITY, "phrase longer than 16 words");
+  }
+  for (int k = 0; k < poff[n_pairs]; ++k)
+    if (pwords[k] < 0 || pwords[k] >= m->V)
+      return fail(NMT_ERR_TOKEN_RANGE, "phrase_words[" + std::to_string(k) + "] outside [0, " + std::to_string(m->V) + ")");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    cudaStream_t st = m->st;
+    if (c->stale) c->sync_counters();
+    for (int i = 0; i < n_pairs; ++i)
+      if (hyp[i] < 0 || hyp[i] >= c->n_nodes) throw NmtError(NMT_ERR_BAD_STATE, "unknown state " + std::to_string(hyp[i]));
+    // ---- host prefix-tree forest: tnodes, one per distinct (hypothesis, prefix)
+    std::vector<int> t_parent, t_word, t_depth;
+    std::vector<int> roots;  // device node ids of the distinct hypotheses (first appearance)
+    std::unordered_map<int64_t, int> root_t;
+    std::unordered_map<uint64_t, int> kids;
+    kids.reserve((size_t)poff[n_pairs] * 2);
+    std::vector<int> path_t(poff[n_pairs]);
+    int maxd = 0;
+    for (int i = 0; i < n_pairs; ++i) {
+      auto it = root_t.find(hyp[i]);
+      int cur;
+      if (it == root_t.end()) {
+        cur = (int)t_parent.size();
+        t_parent.push_back((int)roots.size());  // roots keep their root index here
+        t_word.push_back(-1);
+        t_depth.push_back(0);
+        root_t.emplace(hyp[i], cur);
+        roots.push_back((int)hyp[i]);
+      } else {
+        cur = it->second;
+      }
+      for (int k = poff[i]; k < poff[i + 1]; ++k) {
+        const uint64_t key = ((uint64_t)(uint32_t)cur << 32) | (uint32_t)pwords[k];
+        auto kt = kids.find(key);
+        int nx;
+        if (kt == kids.end()) {
+          nx = (int)t_parent.size();
+          t_parent.push_back(cur);
+          t_word.push_back(pwords[k]);
+          t_depth.push_back(t_depth[cur] + 1);
+          kids.emplace(key, nx);
+        } else {
+          nx = kt->second;
+        }
+        path_t[k] = nx;
+        cur = nx;
+      }
+      maxd = std::max(maxd, poff[i + 1] - poff[i]);
+    }
+    const int nt = (int)t_parent.size();
+    std::vector<std::vector<int>> by_depth(maxd + 1);
+    for (int t = 0; t < nt; ++t) by_depth[t_depth[t]].push_back(t);
+    std::vector<int> pos_of(nt, 0);
+    for (size_t r = 0; r < by_depth[0].size(); ++r) pos_of[by_depth[0][r]] = t_parent[by_depth[0][r]];
+    // staging (int32): roots | per depth: gidx, offsets, words | path_off | path_pos
+    std::vector<int> npar(maxd + 1), nedge(maxd + 1), base(maxd + 2, 0);
+    std::vector<int> host;
+    host.insert(host.end(), roots.begin(), roots.end());
+    std::vector<size_t> o_gidx(maxd + 1), o_off(maxd + 1), o_words(maxd + 1);
+    for (int d = 1; d <= maxd; ++d) {
+      std::vector<int>& E = by_depth[d];
+      std::stable_sort(E.begin(), E.end(), [&](int a, int b) { return pos_of[t_parent[a]] < pos_of[t_parent[b]]; });
+      std::vector<int> gidx, off{0}, words;
+      int last = -1;
+      for (size_t e = 0; e < E.size(); ++e) {
+        pos_of[E[e]] = (int)e;
+        const int pp = pos_of[t_parent[E[e]]];
+        if (pp != last) {
+          if (last >= 0) off.push_back((int)e);
+          gidx.push_back(pp);
+          last = pp;
+        }
+        words.push_back(t_word[E[e]]);
+      }
+      off.push_back((int)E.size());
+      npar[d] = (int)gidx.size();
+      nedge[d] = (int)E.size();
+      base[d + 1] = base[d] + nedge[d];
+      o_gidx[d] = host.size();
+      host.insert(host.end(), gidx.begin(), gidx.end());
+      o_off[d] = host.size();
+      host.insert(host.end(), off.begin(), off.end());
+      o_words[d] = host.size();
+      host.insert(host.end(), words.begin(), words.end());
+    }
+    const size_t o_poff = host.size();
+    host.insert(host.end(), poff, poff + n_pairs + 1);
+    const size_t o_ppos = host.size();
+    for (int k = 0; k < poff[n_pairs]; ++k) host.push_back(base[t_depth[path_t[k]]] + pos_of[path_t[k]]);
+    const int total_e = base[maxd + 1];
+    int max_np = 0, max_ne = 0, total_np = 0;
+    for (int d = 1; d <= maxd; ++d) {
+      max_np = std::max(max_np, npar[d]);
+      max_ne = std::max(max_ne, nedge[d]);
+      total_np += npar[d];
+    }
+    // ---- capacity and device buffers
+    m->ensure_ws(max_np, max_ne);
+    c->ensure(total_e, total_np);
+    const size_t need_i = host.size() + (size_t)total_e /*child*/ + (size_t)max_np /*parents*/ + n_pairs /*state*/ +
+                          (size_t)maxd + 16;
+    const size_t need_f = (size_t)total_e + n_pairs;
+    if (need_i > m->fws_i_cap || need_f > m->fws_f_cap) {
+      CK(cudaStreamSynchronize(st));
+      if (need_i > m->fws_i_cap) {
+        dfree(m->fws_i);
+        m->fws_i_cap = std::max(need_i, m->fws_i_cap * 2);
+        m->fws_i = dalloc<int>(m->fws_i_cap);
+      }
+      if (need_f > m->fws_f_cap) {
+        dfree(m->fws_f);
+        m->fws_f_cap = std::max(need_f, m->fws_f_cap * 2);
+        m->fws_f = dalloc<float>(m->fws_f_cap);
+      }
+    }
+    int* dh = m->fws_i;
+    int* child_all = dh + host.size();
+    int* par = child_all + total_e;
+    int* dstate = par + max_np;
+    int* drows = dstate + n_pairs;
+    float* logp_all = m->fws_f;
+    float* dlogp = logp_all + total_e;
+    int* hp = static_cast<int*>(m->pinned(std::max(host.size(), (size_t)2 * n_pairs + maxd + 8) * 4));
+    std::memcpy(hp, host.data(), host.size() * 4);
+    CK(cudaMemcpyAsync(dh, hp, host.size() * 4, cudaMemcpyHostToDevice, st));
+    for (int d = 1; d <= maxd; ++d) {
+      const int* parents = dh;  // depth 1: the roots (distinct hypotheses, in order)
+      if (d > 1) {
+        gather_idx(child_all + base[d - 1], dh + o_gidx[d], npar[d], par, st);
+        parents = par;
+      }
+      const PlanIO io = plan_io(m, npar[d], nedge[d], parents, dh + o_off[d], dh + o_words[d]);
+      run_call(m, c, io, logp_all + base[d], child_all + base[d], nullptr, nullptr);
+      CK(cudaMemcpyAsync(drows + d, c->counters + CNT_R, 4, cudaMemcpyDeviceToDevice, st));
+    }
+    path_sum(logp_all, child_all, dh + o_poff, dh + o_ppos, n_pairs, dlogp, dstate, st);
+    float* rl = reinterpret_cast<float*>(hp);
+    int* rs = hp + n_pairs;
+    int* rr = rs + n_pairs;
+    int* rc = rr + maxd + 1;
+    CK(cudaStreamSynchronize(st));  // (the staging buffer is reused for the results)
+    CK(cudaMemcpyAsync(rl, dlogp, (size_t)n_pairs * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rs, dstate, (size_t)n_pairs * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rr, drows, (size_t)(maxd + 1) * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rc, c->counters, CNT_N * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (rc[CNT_ERR]) {
+      const int z = 0;
+      CK(cudaMemcpy(c->counters + CNT_ERR, &z, 4, cudaMemcpyHostToDevice));
+      throw NmtError(NMT_ERR_BAD_STATE, "device-side validation failed (flags " + std::to_string(rc[CNT_ERR]) + ")");
+    }
+    c->n_nodes = rc[CNT_NODES];
+    c->n_slots = rc[CNT_SLOTS];
+    std::memcpy(out_logp, rl, (size_t)n_pairs * 4);
+    for (int i = 0; i < n_pairs; ++i) out_state[i] = rs[i];
+    if (stats) {
+      std::memset(stats, 0, 33 * sizeof(int32_t));
+      stats[0] = maxd;
+      for (int d = 1; d <= maxd; ++d) {
+        stats[d] = nedge[d];
+        stats[16 + d] = rr[d];
+      }
+    }
   });
 }
 

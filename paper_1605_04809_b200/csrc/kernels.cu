@@ -721,6 +721,35 @@ __global__ void k_argmax_out(CtxDev c, PlanIO io, int* out) {
   out[k] = v;
 }
 
+// ScoreBatch forest helpers: parents of depth d+1 = children of depth d gathered by edge position;
+// per pair, the sum of its phrase's word log-probs along its path of edges and the final state.
+__global__ void k_gather_idx(const int* __restrict__ src, const int* __restrict__ idx, int n, int* out) {
+  pdl_enter();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = src[idx[i]];
+}
+void gather_idx(const int* src, const int* idx, int n, int* out, cudaStream_t st) {
+  if (n <= 0) return;
+  launch_pdl(k_gather_idx, (n + 255) / 256, 256, 0, st, src, idx, n, out);
+  CK_LAUNCH();
+}
+__global__ void k_path_sum(const float* __restrict__ logp, const int* __restrict__ child, const int* __restrict__ off,
+                           const int* __restrict__ pos, int n, float* out_logp, int* out_state) {
+  pdl_enter();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float s = 0.f;
+  for (int k = off[i]; k < off[i + 1]; ++k) s += logp[pos[k]];  // depth order
+  out_logp[i] = s;
+  out_state[i] = child[pos[off[i + 1] - 1]];
+}
+void path_sum(const float* logp, const int* child, const int* off, const int* pos, int n, float* out_logp,
+              int* out_state, cudaStream_t st) {
+  if (n <= 0) return;
+  launch_pdl(k_path_sum, (n + 255) / 256, 256, 0, st, logp, child, off, pos, n, out_logp, out_state);
+  CK_LAUNCH();
+}
+
 // full log-prob row of one stepped slot (test export)
 __global__ void k_full_row(const float* __restrict__ T, const float* __restrict__ Wo32, const float* __restrict__ bo,
                            const float* __restrict__ logZ, int slot, int Ep, int V, float* out) {

@@ -104,6 +104,9 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
                       int R_max, cudaStream_t st);
 void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const float* bo, int Ep, float* out_logp,
                 int* out_child32, long long* out_child64, int* out_argmax, cudaStream_t st);
+void gather_idx(const int* src, const int* idx, int n, int* out, cudaStream_t st);
+void path_sum(const float* logp, const int* child, const int* off, const int* pos, int n, float* out_logp,
+              int* out_state, cudaStream_t st);
 void full_row(const float* T, const float* Wo32, const float* bo, const float* logZ, int slot, int Ep, int V,
               float* out, cudaStream_t st);
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st);

@@ -22,7 +22,7 @@ STATUS = {0: "NMT_OK", 1: "NMT_ERR_INVALID_ARG", 2: "NMT_ERR_IO", 3: "NMT_ERR_FO
 
 # every symbol include/nmt.h declares (checked by tests/test_abi.py)
 EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "nmt_model_free", "nmt_encode",
-           "nmt_root", "nmt_ctx_free", "nmt_score_batch", "nmt_score_batch_dev", "nmt_ctx_check", "nmt_ctx_stats",
+           "nmt_root", "nmt_ctx_free", "nmt_score_batch", "nmt_score_forest", "nmt_score_batch_dev", "nmt_ctx_check", "nmt_ctx_stats",
            "nmt_inject_states", "nmt_logprobs_full", "nmt_debug_encoder", "nmt_debug_intermediates",
            "nmt_test_gemm", "nmt_encode_dev", "nmt_inject_states_dev", "nmt_launch_count", "nmt_profile",
            "nmt_profile_read", "nmt_bench_gemm", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
@@ -76,6 +76,7 @@ def lib() -> C.CDLL:
             "nmt_ctx_free": (None, [vp]),
             "nmt_score_batch": (i32, [vp, i32, vp, vp, vp, vp, vp, vp]),
             "nmt_score_batch_dev": (i32, [vp, i32, vp, vp, i32, vp, vp, vp, vp]),
+            "nmt_score_forest": (i32, [vp, i32, vp, vp, vp, vp, vp, vp]),
             "nmt_ctx_check": (i32, [vp]),
             "nmt_ctx_stats": (i32, [vp, C.POINTER(i64), C.POINTER(i64)]),
             "nmt_inject_states": (i32, [vp, i32, vp, vp, vp]),
@@ -193,6 +194,21 @@ class Context:
         """Device-resident variant (int32 device arrays, e.g. torch tensors' data_ptr())."""
         _check(lib().nmt_score_batch_dev(self._h, n_parents, parents_ptr, offsets_ptr, n_cand, words_ptr, logp_ptr,
                                          child_ptr, argmax_ptr))
+
+    def score_forest(self, hyp_states, phrase_offsets, phrase_words):
+        """nmt_score_forest: ScoreBatch over (hypothesis, phrase) pairs in one call.
+        Returns (summed log-probs [n], final states [n], stats dict)."""
+        hs = _c(hyp_states, np.int64)
+        off = _c(phrase_offsets, np.int32)
+        w = _c(phrase_words, np.int32)
+        n = len(hs)
+        lp = np.empty(n, np.float32)
+        st = np.empty(n, np.int64)
+        stats = np.zeros(33, np.int32)
+        _check(lib().nmt_score_forest(self._h, n, _ptr(hs), _ptr(off), _ptr(w), _ptr(lp), _ptr(st), _ptr(stats)))
+        steps = int(stats[0])
+        return lp, st, {"steps": steps, "edges_per_depth": stats[1:1 + steps].tolist(),
+                        "rows_per_depth": stats[17:17 + steps].tolist()}
 
     def check(self) -> None:
         _check(lib().nmt_ctx_check(self._h))

@@ -100,3 +100,62 @@ def test_ensemble_single_rank_nccl():
         ref = O.ensemble_combine([lp.astype(np.float64)], [w], mode)
         assert np.max(np.abs(d_out.cpu().numpy() - ref)) < 1e-5
     ens.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32class", "bf16"])
+def test_native_score_forest_matches_oracle_and_driver(prec):
+    """nmt_score_forest (native ScoreBatch) == oracle per-pair sums; Fig. 1 step structure; a second
+    call on the same pairs is served from the state cache (no new rows, identical results)."""
+    from paper_1605_04809_b200 import nmt, scorebatch
+    d = synth.Dims(8, 16, 50, 50, "tanh")
+    p = synth.make_model(d, 21)
+    M = nmt.Model(synth.params_bytes(d, p), precision=prec)
+    src = synth.make_source(d.vocab_src, 5, seed=6)
+    rng = np.random.default_rng(1)
+    s = np.tanh(rng.standard_normal((2, d.dim_hid))).astype(np.float32)
+    pairs, info = _fig1()
+    hs_idx = [h for h, _ in pairs]
+    off = np.cumsum([0] + [len(t) for _, t in pairs]).astype(np.int32)
+    words = np.array([w for _, t in pairs for w in t], np.int32)
+    ctx = M.encode(src)
+    hyps = ctx.inject_states(s, [4, 9])
+    lp, stt, st = ctx.score_forest([hyps[h] for h in hs_idx], off, words)
+    assert st["steps"] == 4 and st["edges_per_depth"] == [4, 5, 3, 1] and st["rows_per_depth"] == [2, 3, 3, 1]
+    sess = O.Session(O.Model(d, p), src)
+    oh = [sess.inject_state(s[i], y) for i, y in enumerate([4, 9])]
+    ref = O.score_forest(sess, oh, pairs)
+    for i, k in enumerate(pairs):
+        assert abs(lp[i] - ref[k]) < TOL[prec] * len(k[1])
+    lp2, st2, s2 = ctx.score_forest([hyps[h] for h in hs_idx], off, words)
+    assert s2["rows_per_depth"] == [0, 0, 0, 0] and np.array_equal(lp, lp2) and np.array_equal(stt, st2)
+    # the python driver on a fresh context gives the same numbers
+    ctx2 = M.encode(src)
+    hyps2 = ctx2.inject_states(s, [4, 9])
+    out, _ = scorebatch.score_batch(ctx2, hyps2, pairs)
+    for i, k in enumerate(pairs):
+        assert abs(out[k][0] - lp[i]) < 1e-5
+    with pytest.raises(nmt.NmtError) as e:
+        ctx.score_forest([hyps[0]], [0, 0], np.zeros(0, np.int32))
+    assert "empty expansion" in str(e.value)
+
+
+def test_native_score_forest_c3_stack_tiny():
+    from paper_1605_04809_b200 import nmt
+    d = synth.Dims(8, 16, 50, 50, "maxout")
+    p = synth.make_model(d, 1605)
+    M = nmt.Model(synth.params_bytes(d, p), precision="fp32class")
+    src = synth.make_source(d.vocab_src, 12, seed=1606)
+    ctx = M.encode(src)
+    sess = O.Session(O.Model(d, p), src)
+    H = 16
+    s, y = synth.make_states(H, d.dim_hid, d.vocab_tgt, seed=1607)
+    gh = ctx.inject_states(s, y)
+    oh = [sess.inject_state(s[i], int(y[i])) for i in range(H)]
+    pairs = synth.make_stack_expansions(200, H, d.vocab_tgt, seed=1609)
+    off = np.cumsum([0] + [len(t) for _, t in pairs]).astype(np.int32)
+    words = np.array([w for _, t in pairs for w in t], np.int32)
+    lp, _, st = ctx.score_forest([gh[h] for h, _ in pairs], off, words)
+    ref = O.score_forest(sess, oh, pairs)
+    worst = max(abs(lp[i] - ref[k]) / len(k[1]) for i, k in enumerate(pairs))
+    assert worst < TOL["fp32class"]
+    assert st["rows_per_depth"] == sess.rows_per_step
