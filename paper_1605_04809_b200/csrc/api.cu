@@ -141,7 +141,8 @@ struct nmt_model {
   float4* part = nullptr;
   int* lse_cpm = nullptr;  // [1] runs per m-tile of the last vocabulary GEMM
   int *row_src = nullptr, *row_y = nullptr, *row_dst = nullptr, *row_node = nullptr;
-  int *cand_k = nullptr, *cand_hslot = nullptr;
+  int *cand_k = nullptr, *cand_hslot = nullptr, *cflag = nullptr, *pflag = nullptr, *bcount = nullptr,
+      *snap = nullptr;
   int *in_par = nullptr, *in_off = nullptr, *in_words = nullptr;
   float* out_logp = nullptr;
   int *out_child = nullptr, *out_amax = nullptr;
@@ -235,7 +236,8 @@ void nmt_model::free_ws() {
   for (__nv_bfloat16** p : {&A_s, &X, &A_t}) dfree(*p);
   for (float** p : {&G1, &S1, &Q, &Cf, &G2, &RO_buf, &alpha, &out_logp, &in_s}) dfree(*p);
   dfree(part);
-  for (int** p : {&lse_cpm, &row_src, &row_y, &row_dst, &row_node, &cand_k, &cand_hslot, &in_par, &in_off, &in_words,
+  for (int** p : {&lse_cpm, &row_src, &row_y, &row_dst, &row_node, &cand_k, &cand_hslot, &cflag, &pflag, &bcount, &snap,
+                  &in_par, &in_off, &in_words,
                   &out_child, &out_amax})
     dfree(*p);
   R_cap = NC_cap = 0;
@@ -287,6 +289,10 @@ void nmt_model::ensure_ws(int R, int NC) {
   in_s = dalloc<float>((size_t)R_cap * H);
   cand_k = dalloc<int>(NC_cap);
   cand_hslot = dalloc<int>(NC_cap);
+  cflag = dalloc<int>(NC_cap);
+  pflag = dalloc<int>(R_cap);
+  bcount = dalloc<int>((NC_cap + R_cap) / 256 + 4);
+  snap = dalloc<int>(4);
   in_words = dalloc<int>(NC_cap);
   out_logp = dalloc<float>(NC_cap);
   out_child = dalloc<int>(NC_cap);
@@ -540,7 +546,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
     }
     m->EncIn = dalloc<float>((size_t)Vs * 6 * Hp);
     CUtensorMap ta = make_tmap_bf16(Aemb, Vr, 2 * Ep, 128), tb = make_tmap_bf16(Wenc, 6 * Hp, 2 * Ep, 128);
-    gemm_store(ta, tb, gemm_shape(Vs, nullptr, 6 * Hp, Ep, 0, true, Ep, Ep), m->EncIn, 6 * Hp, dbenc, Vs, st);
+    gemm_store(ta, tb, gemm_shape(Vs, nullptr, 6 * Hp, Ep, 0, true, Ep, Ep), m->EncIn, 6 * Hp, Vs, dbenc, Vs, st);
     CK(cudaStreamSynchronize(st));
     dfree(Wenc);
     dfree(Aemb);
@@ -672,7 +678,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
     float* db1 = upload_vec(b1, st);
     m->Ex = dalloc<float>((size_t)(V + 1) * 3 * Hp);
     CUtensorMap tmB1 = make_tmap_bf16(B1, 3 * Hp, 2 * Ep, 128);
-    gemm_store(tmE, tmB1, gemm_shape(V, nullptr, 3 * Hp, Ep, 0, true, Ep, Ep), m->Ex, 3 * Hp, db1, V, st);
+    gemm_store(tmE, tmB1, gemm_shape(V, nullptr, 3 * Hp, Ep, 0, true, Ep, Ep), m->Ex, 3 * Hp, V + 1, db1, V, st);
     CK(cudaMemcpyAsync(m->Ex + (size_t)V * 3 * Hp, db1, 3 * Hp * 4, cudaMemcpyDeviceToDevice, st));
 
     __nv_bfloat16* Bp = dalloc<__nv_bfloat16>((size_t)ROp * 2 * Ep);
@@ -686,7 +692,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
     float* dbs = upload_vec(bsum, st);
     m->Eproj = dalloc<float>((size_t)(V + 1) * ROp);
     CUtensorMap tmBp = make_tmap_bf16(Bp, ROp, 2 * Ep, 128);
-    gemm_store(tmE, tmBp, gemm_shape(V, nullptr, ROp, Ep, 0, true, Ep, Ep), m->Eproj, ROp, dbs, V, st);
+    gemm_store(tmE, tmBp, gemm_shape(V, nullptr, ROp, Ep, 0, true, Ep, Ep), m->Eproj, ROp, V + 1, dbs, V, st);
     CK(cudaMemcpyAsync(m->Eproj + (size_t)V * ROp, dbs, ROp * 4, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));
     dfree(Aemb);
@@ -863,9 +869,9 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
   const int Hp = m->Hp, Cp = m->Cp, Ep = m->Ep;
   const bool sp = m->split;
   { ProfScope p_(m, ST_GATHER); step_elementwise(EW_GATHER, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  { ProfScope p_(m, ST_GEMM_H1); gemm_store(m->tm_As, m->tm_Wh1, gemm_shape(0, Rd, 3 * Hp, Hp, 0, sp, Hp, Hp), m->G1, 3 * Hp, nullptr, R_max, st); }
+  { ProfScope p_(m, ST_GEMM_H1); gemm_store(m->tm_As, m->tm_Wh1, gemm_shape(0, Rd, 3 * Hp, Hp, 0, sp, Hp, Hp), m->G1, 3 * Hp, m->R_cap, nullptr, R_max, st); }
   { ProfScope p_(m, ST_GRU1); step_elementwise(EW_GRU1, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  { ProfScope p_(m, ST_GEMM_Q); gemm_store(m->tm_X, m->tm_Wq, gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp), m->Q, Cp, nullptr, R_max, st); }
+  { ProfScope p_(m, ST_GEMM_Q); gemm_store(m->tm_X, m->tm_Wq, gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp), m->Q, Cp, m->R_cap, nullptr, R_max, st); }
   { ProfScope p_(m, ST_ATTN); step_elementwise(EW_ATTN, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   {
     ProfScope p_(m, ST_GEMM_G2);
@@ -874,12 +880,12 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
     g.reg_n_end[0] = 2 * Hp, g.reg_k0[0] = 0, g.reg_k1[0] = Hp + Cp;  // gates: s1 U_nl + c Wc
     g.reg_n_end[1] = 3 * Hp, g.reg_k0[1] = 0, g.reg_k1[1] = Hp;       // s1 Ux_nl
     g.reg_n_end[2] = 4 * Hp, g.reg_k0[2] = Hp, g.reg_k1[2] = Hp + Cp; // c Wcx
-    if (m->g2_bn == 256) gemm_store256(m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, nullptr, R_max, st);
-    else gemm_store(m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, nullptr, R_max, st);
+    if (m->g2_bn == 256) gemm_store256(m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, m->R_cap, nullptr, R_max, st);
+    else gemm_store(m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, m->R_cap, nullptr, R_max, st);
   }
   { ProfScope p_(m, ST_GRU2); step_elementwise(EW_GRU2, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   { ProfScope p_(m, ST_GEMM_RO); gemm_store(m->tm_X, m->tm_Wro, gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp), m->RO_buf, m->ROp,
-             nullptr, R_max, st); }
+             m->R_cap, nullptr, R_max, st); }
   { ProfScope p_(m, ST_READOUT); step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   { ProfScope p_(m, ST_VOCAB); gemm_lse(m->tm_At, m->tm_Wo, gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep), m->part, m->V, R_max, st, m->lse_cpm); }
   { ProfScope p_(m, ST_FINALIZE); step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
@@ -898,6 +904,10 @@ static PlanIO plan_io(nmt_model* m, int np, int nc, const int* par, const int* o
   io.row_y = m->row_y;
   io.row_dst = m->row_dst;
   io.row_node = m->row_node;
+  io.cflag = m->cflag;
+  io.pflag = m->pflag;
+  io.bcount = m->bcount;
+  io.snap = m->snap;
   return io;
 }
 
@@ -1043,7 +1053,7 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
       g.ksplit = (nkb + chunk - 1) / chunk;
     }
     const size_t stride = (size_t)m->Tpad * m->Cp;
-    gemm_store(m->tm_ctxbf, m->tm_Watt, g, m->ksplit_buf, m->Cp, nullptr, len, st, stride);
+    gemm_store(m->tm_ctxbf, m->tm_Watt, g, m->ksplit_buf, m->Cp, g.ksplit * m->Tpad, nullptr, len, st, stride);
     splitk_reduce(m->ksplit_buf, g.ksplit, stride, len, m->Cp, m->Cp, m->b_att, c->pctx, st);
   }
   // root node 0 = (s0, BOS): word -1, parent -1, src slot 0, not stepped
@@ -1570,8 +1580,8 @@ nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_
     g.ksplit = ksplit;
     auto run = [&] {
       if (epi == 1) gemm_lse(ta, tb, g, part, N, M, st, cpm);
-      else if (epi == 2) gemm_store256(ta, tb, g, c, N, nullptr, M, st, (size_t)Mp * N);
-      else gemm_store(ta, tb, g, c, N, nullptr, M, st, (size_t)Mp * N);
+      else if (epi == 2) gemm_store256(ta, tb, g, c, N, ksplit * Mp, nullptr, M, st, (size_t)Mp * N);
+      else gemm_store(ta, tb, g, c, N, ksplit * Mp, nullptr, M, st, (size_t)Mp * N);
     };
     for (int i = 0; i < 3; ++i) run();
     cudaEvent_t e0, e1;
@@ -1615,7 +1625,7 @@ nmt_status nmt_test_gemm(int32_t M, int32_t N, int32_t K, int32_t split, const f
     pack_rows(dA, K, M, K, a, sf * K, 0, split ? K : 0, st);
     pack_T(dB, N, K, N, b, sf * K, 0, 0, 0, 0, 1, 1, split ? K : 0, st);
     CUtensorMap ta = make_tmap_bf16(a, Mp, sf * K, 128), tb = make_tmap_bf16(b, N, sf * K, 128);
-    gemm_store(ta, tb, gemm_shape(M, nullptr, N, K, 0, split != 0, K, K), dC, N, db, M, st);
+    gemm_store(ta, tb, gemm_shape(M, nullptr, N, K, 0, split != 0, K, K), dC, N, M, db, M, st);
     CK(cudaStreamSynchronize(st));
     CK(cudaMemcpy(C, dC, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
     dfree(dA);

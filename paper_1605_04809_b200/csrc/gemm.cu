@@ -19,7 +19,9 @@
 // the logits never leave the chip (PAPER.md:120 computes P_i explicitly; we never do).
 #include <cuda.h>
 
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <stdexcept>
 #include <string>
 
@@ -33,11 +35,13 @@ constexpr int EPI_STORE = 0, EPI_LSE = 1;
 constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant, each owning half of the tile's columns
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EPI>
 struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int BYTES = 1024 + STAGES * (A_BYTES + B_BYTES) + (2 * STAGES + 4) * 8 + 16;
+  // EPI_STORE: per epilogue warp two 32 x 32 fp32 staging tiles (128B-swizzled) for TMA stores
+  static constexpr int C_BYTES = EPI == 0 ? EPI_WARPS * 2 * 4096 : 0;
+  static constexpr int BYTES = 1024 + STAGES * (A_BYTES + B_BYTES) + C_BYTES + (2 * STAGES + 4) * 8 + 16;
 };
 
 struct RegionK {
@@ -95,14 +99,15 @@ NMT_DEV RegionK region_of(const GemmShape& g, int n0) {
 
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmShape g,
-           EpiParams ep) {
-  using S = GemmSmem<BN, STAGES>;
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const __grid_constant__ CUtensorMap tmC, GemmShape g, EpiParams ep) {
+  using S = GemmSmem<BN, STAGES, EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * S::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * S::B_BYTES);
+  uint8_t* sC = sB + STAGES * S::B_BYTES;  // (1024-aligned: A/B stage sizes are multiples of 1 KB)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sC + S::C_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -114,6 +119,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (EPI == EPI_STORE) tma_prefetch(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -220,26 +226,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + half * COLS;
         const int colbase = n * BN + half * COLS;
         if constexpr (EPI == EPI_STORE) {
-          float* orow = ep.out + (size_t)itm.s * ep.split_stride + (size_t)grow * ep.ldc + colbase;
+          // TMEM -> registers (+bias) -> 128B-swizzled 32x32 smem tile -> TMA store (coalesced)
+          uint8_t* stile = sC + (size_t)(warp - 2) * 2 * 4096;
+          const int row0 = itm.s * ep.rows_per_split + itm.m * BM + q * 32;
 #pragma unroll 1
-          for (int c = 0; c < COLS; c += 64) {
-            float v[64];
+          for (int c = 0; c < COLS; c += 32) {
+            uint8_t* buf = stile + ((c >> 5) & 1) * 4096;
+            if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer has read it
+            __syncwarp();
+            float v[32];
             tmem_ld32_nowait(tbase + c, v);
-            tmem_ld32_nowait(tbase + c + 32, v + 32);
             tmem_wait_ld_dep(v);
-            reg_dep32(v + 32);
-            if (valid) {
-              if (ep.bias) {
-                const float4* b = reinterpret_cast<const float4*>(ep.bias + colbase + c);
+            if (ep.bias) {
+              const float4* b = reinterpret_cast<const float4*>(ep.bias + colbase + c);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                  const float4 bb = __ldg(b + j);
-                  v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
-                }
+              for (int j = 0; j < 8; ++j) {
+                const float4 bb = __ldg(b + j);
+                v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
               }
-              float4* o = reinterpret_cast<float4*>(orow + c);
+            }
 #pragma unroll
-              for (int j = 0; j < 16; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            for (int j = 0; j < 8; ++j) {
+              float4* dst = reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
+              *dst = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmC, buf, colbase + c, row0);
+              bulk_commit();
             }
           }
         } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
@@ -300,6 +315,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   }
+  if (EPI == EPI_STORE && warp >= 2 && lane == 0) bulk_wait_all();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -342,10 +358,33 @@ CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint3
   return m;
 }
 
+// fp32 output map for the TMA-store epilogue: box 32 x 32, 128B swizzle; cached per buffer
+static CUtensorMap make_tmap_f32_out(const void* base, uint64_t rows, uint64_t cols) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw NmtError(NMT_ERR_CUDA, "cuTensorMapEncodeTiled (fp32 out) failed");
+  return m;
+}
+static const CUtensorMap& out_map(const float* out, uint64_t rows, uint64_t ldc) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, uint64_t, uint64_t>, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple((const void*)out, rows, ldc);
+  auto it = cache.find(key);
+  if (it == cache.end()) it = cache.emplace(key, make_tmap_f32_out(out, rows, ldc)).first;
+  return it->second;
+}
+
 template <int BN, int STAGES, int EPI>
-static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, const EpiParams& ep, int M_max,
-                   cudaStream_t st) {
-  using S = GemmSmem<BN, STAGES>;
+static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmShape& g,
+                   const EpiParams& ep, int M_max, cudaStream_t st) {
+  using S = GemmSmem<BN, STAGES, EPI>;
   static bool attr_set = false;  // per template instance; set once per process (single device use)
   if (!attr_set) {
     CK(cudaFuncSetAttribute(k_gemm<BN, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
@@ -354,7 +393,7 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& 
   const int tiles = ((M_max + BM - 1) / BM) * (g.N / BN) * g.ksplit;
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
   if (grid <= 0) return;
-  launch_pdl(k_gemm<BN, STAGES, EPI>, grid, GEMM_THREADS, S::BYTES, st, a, b, g, ep);
+  launch_pdl(k_gemm<BN, STAGES, EPI>, grid, GEMM_THREADS, S::BYTES, st, a, b, c, g, ep);
   CK_LAUNCH();
 }
 
@@ -373,30 +412,33 @@ void gemm_validate(const GemmShape& g, int BN) {
   }
 }
 
-// fp32 output GEMM; BN = 128 (more CTAs for the mid-size decoder GEMMs).
-void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc,
-                const float* bias, int M_max, cudaStream_t st, size_t split_stride) {
-  gemm_validate(g, 128);
+// fp32 output GEMM (TMA-store epilogue); BN = 128 (more CTAs for the mid-size decoder GEMMs).
+// out_rows = rows of the output allocation (stores are clipped there); split-K partial s goes to
+// rows s * split_stride / ldc + r of the same 2-D map.
+static EpiParams store_params(const GemmShape& g, int BN, float* out, int ldc, const float* bias,
+                              size_t split_stride) {
+  gemm_validate(g, BN);
   if (g.ksplit > 1 && (bias || !split_stride)) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: split-K partials take no bias");
+  if (split_stride % ldc) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: split stride not a whole number of rows");
   EpiParams ep{};
   ep.out = out;
   ep.ldc = ldc;
   ep.bias = bias;
   ep.split_stride = split_stride;
-  launch<128, 6, EPI_STORE>(a, b, g, ep, M_max, st);
+  ep.rows_per_split = (int)(split_stride / ldc);
+  return ep;
+}
+void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc, int out_rows,
+                const float* bias, int M_max, cudaStream_t st, size_t split_stride) {
+  const EpiParams ep = store_params(g, 128, out, ldc, bias, split_stride);
+  launch<128, 4, EPI_STORE>(a, b, out_map(out, out_rows, ldc), g, ep, M_max, st);
 }
 
 // fp32 output GEMM with 128 x 256 tiles (A reuse x2; fewer tiles)
-void gemm_store256(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc,
+void gemm_store256(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc, int out_rows,
                    const float* bias, int M_max, cudaStream_t st, size_t split_stride) {
-  gemm_validate(g, 256);
-  if (g.ksplit > 1 && (bias || !split_stride)) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: split-K partials take no bias");
-  EpiParams ep{};
-  ep.out = out;
-  ep.ldc = ldc;
-  ep.bias = bias;
-  ep.split_stride = split_stride;
-  launch<256, 4, EPI_STORE>(a, b, g, ep, M_max, st);
+  const EpiParams ep = store_params(g, 256, out, ldc, bias, split_stride);
+  launch<256, 3, EPI_STORE>(a, b, out_map(out, out_rows, ldc), g, ep, M_max, st);
 }
 
 // fused vocabulary GEMM + online log-sum-exp partials; BN = 256.
@@ -408,7 +450,7 @@ void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, fl
   ep.n_valid = n_valid;
   ep.n_tiles = g.N / 256;
   ep.cpm_out = cpm_out;
-  launch<256, 4, EPI_LSE>(a, b, g, ep, M_max, st);
+  launch<256, 4, EPI_LSE>(a, b, b /*unused*/, g, ep, M_max, st);
 }
 
 }  // namespace nmt

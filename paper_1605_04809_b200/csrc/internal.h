@@ -77,12 +77,13 @@ struct EpiParams {
   int n_tiles;
   size_t split_stride;
   int* cpm_out;  // EPI_LSE: runs per m-tile (partials per row = 2 * cpm), written by CTA 0
+  int rows_per_split;  // EPI_STORE: row offset of split-K partial s is s * rows_per_split
 };
 
 CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
-void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc,
+void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc, int out_rows,
                 const float* bias, int M_max, cudaStream_t st, size_t split_stride = 0);
-void gemm_store256(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc,
+void gemm_store256(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc, int out_rows,
                    const float* bias, int M_max, cudaStream_t st, size_t split_stride = 0);
 // out[r][c] = bias[c] + sum_s part[s * stride + r * ldc + c]  (fixed order: deterministic)
 void splitk_reduce(const float* part, int ksplit, size_t stride, int M, int N, int ldc, const float* bias, float* out,

@@ -125,15 +125,24 @@ NMT_DEV int hash_insert(unsigned long long* keys, uint64_t mask, int64_t key) {
   }
 }
 
+constexpr int kPlanSmemOffsets = 8192;  // offsets staged in shared memory up to this many parents
 __global__ void k_plan_intern(CtxDev c, PlanIO io) {
   pdl_enter();
+  __shared__ int soff[kPlanSmemOffsets + 1];
+  const bool use_smem = io.n_par + 1 <= kPlanSmemOffsets + 1;
+  const int* offs = io.offsets;
+  if (use_smem) {
+    for (int k = threadIdx.x; k <= io.n_par; k += blockDim.x) soff[k] = io.offsets[k];
+    __syncthreads();
+    offs = soff;
+  }
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int n_nodes = c.counters[CNT_NODES];
   if (i < io.n_cand) {
     int lo = 0, hi = io.n_par;  // find k with offsets[k] <= i < offsets[k+1]
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (io.offsets[mid] <= i) lo = mid; else hi = mid;
+      if (offs[mid] <= i) lo = mid; else hi = mid;
     }
     const int k = lo;
     io.cand_k[i] = k;
@@ -151,7 +160,7 @@ __global__ void k_plan_intern(CtxDev c, PlanIO io) {
   }
   if (i < io.n_par) {
     const int p = io.parents[i];
-    const int o0 = io.offsets[i], o1 = io.offsets[i + 1];
+    const int o0 = offs[i], o1 = offs[i + 1];
     if (o1 < o0) atomicOr(&c.counters[CNT_ERR], ERR_OFFSETS);
     if (p < 0 || p >= n_nodes) atomicOr(&c.counters[CNT_ERR], ERR_BAD_STATE);
     else if (o1 > o0) atomicMin(&c.node_claim[p], i);
@@ -185,66 +194,116 @@ NMT_DEV int block_scan_excl(int v, int* smem32, int& total) {
   return warp_prefix + x - v;
 }
 
-// single-CTA pass: new node ids (first appearances), row list of parents to step.
-__global__ void __launch_bounds__(1024) k_plan_assign(CtxDev c, PlanIO io, int* R_out) {
+// Multi-CTA assignment (blocks [0, Bc) = candidates, [Bc, Bc + Bp) = parents, 256 threads each):
+//  k_plan_flags : first-appearance flags of new (parent, word) keys / parents that must be stepped,
+//                 one count per block, and a snapshot of the node/slot counters;
+//  k_plan_assign: block prefix from the counts + in-block scan -> node ids in first-appearance
+//                 order (deterministic), row list of the parents to step (in request order).
+constexpr int kPlanBlock = 256;
+NMT_DEV int block_count(int v, int* red) {  // sum over a 256-thread block
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = __reduce_add_sync(0xffffffffu, v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  int t = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+  return t;
+}
+__global__ void __launch_bounds__(kPlanBlock) k_plan_flags(CtxDev c, PlanIO io, int Bc) {
   pdl_enter();
-  __shared__ int sm[32];
-  const int n_nodes0 = c.counters[CNT_NODES];
-  const int n_slots0 = c.counters[CNT_SLOTS];
-  int base = 0;
-  for (int i0 = 0; i0 < io.n_cand; i0 += blockDim.x) {
-    const int i = i0 + threadIdx.x;
-    int hs = -1, flag = 0;
+  __shared__ int red[8];
+  const int b = blockIdx.x;
+  int f = 0;
+  if (b < Bc) {
+    const int i = b * kPlanBlock + threadIdx.x;
     if (i < io.n_cand) {
-      hs = io.cand_hslot[i];
-      flag = hs >= 0 && c.hvals[hs] == -2 - i;
+      const int hs = io.cand_hslot[i];
+      f = hs >= 0 && c.hvals[hs] == -2 - i;
+      io.cflag[i] = f;
     }
-    int tot;
-    const int ex = block_scan_excl(flag, sm, tot);
-    if (flag) {
-      const int id = n_nodes0 + base + ex;
-      const int k = io.cand_k[i];
-      c.node_word[id] = io.words[i];
+  } else {
+    const int k = (b - Bc) * kPlanBlock + threadIdx.x;
+    const int n_nodes0 = c.counters[CNT_NODES];
+    if (k < io.n_par) {
+      const int p = io.parents[k];
+      f = p >= 0 && p < n_nodes0 && io.offsets[k + 1] > io.offsets[k] && c.node_slot[p] < 0 && c.node_claim[p] == k;
+      io.pflag[k] = f;
+    }
+  }
+  const int t = block_count(f, red);
+  if (threadIdx.x == 0) {
+    io.bcount[b] = t;
+    if (b == 0) {
+      io.snap[0] = c.counters[CNT_NODES];
+      io.snap[1] = c.counters[CNT_SLOTS];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPlanBlock) k_plan_assign(CtxDev c, PlanIO io, int Bc, int Bp, int* R_out) {
+  pdl_enter();
+  __shared__ int red[32];
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool cand = b < Bc;
+  const int b0 = cand ? 0 : Bc, bi = cand ? b : b - Bc;
+  // prefix of the earlier blocks of the same kind (warp 0), totals (block 0 only)
+  if (warp == 0) {
+    int pre = 0;
+    for (int q = lane; q < bi; q += 32) pre += io.bcount[b0 + q];
+    pre = __reduce_add_sync(0xffffffffu, pre);
+    if (lane == 0) red[16] = pre;
+    if (b == 0) {
+      int tc = 0, tp = 0;
+      for (int q = lane; q < Bc; q += 32) tc += io.bcount[q];
+      for (int q = lane; q < Bp; q += 32) tp += io.bcount[Bc + q];
+      tc = __reduce_add_sync(0xffffffffu, tc);
+      tp = __reduce_add_sync(0xffffffffu, tp);
+      if (lane == 0) {
+        c.counters[CNT_NODES] = io.snap[0] + tc;
+        c.counters[CNT_SLOTS] = io.snap[1] + tp;
+        *R_out = tp;
+      }
+    }
+  }
+  const int e = bi * kPlanBlock + threadIdx.x;
+  const int n = cand ? io.n_cand : io.n_par;
+  const int f = e < n ? (cand ? io.cflag[e] : io.pflag[e]) : 0;
+  // in-block exclusive scan
+  int x = f;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) red[warp] = x;
+  __syncthreads();
+  int wpre = 0;
+  for (int w = 0; w < warp; ++w) wpre += red[w];
+  const int pos = red[16] + wpre + x - f;
+  if (cand) {
+    if (f) {
+      const int id = io.snap[0] + pos;
+      const int k = io.cand_k[e];
+      c.node_word[id] = io.words[e];
       c.node_parent[id] = io.parents[k];
       c.node_slot[id] = -1;
       c.node_claim[id] = INT32_MAX;
-      c.hvals[hs] = id;
+      c.hvals[io.cand_hslot[e]] = id;
     }
-    base += tot;
-  }
-  const int n_new = base;
-  base = 0;
-  for (int k0 = 0; k0 < io.n_par; k0 += blockDim.x) {
-    const int k = k0 + threadIdx.x;
-    int need = 0, p = -1;
-    if (k < io.n_par) {
-      p = io.parents[k];
-      need = p >= 0 && p < n_nodes0 && io.offsets[k + 1] > io.offsets[k] && c.node_slot[p] < 0 &&
-             c.node_claim[p] == k;
-    }
-    int tot;
-    const int ex = block_scan_excl(need, sm, tot);
-    if (need) {
-      const int r = base + ex;
+  } else if (e < n) {
+    const int p = io.parents[e];
+    if (f) {
+      const int r = pos;
       const int par = c.node_parent[p];
-      io.row_src[r] = par >= 0 ? c.node_slot[par] : c.node_src[p];
+      io.row_src[r] = par >= 0 ? c.node_slot[par] : c.node_src[p];  // parents stepped in earlier calls
       io.row_y[r] = c.node_word[p];
-      io.row_dst[r] = n_slots0 + r;
+      io.row_dst[r] = io.snap[1] + r;
       io.row_node[r] = p;
+      c.node_slot[p] = io.snap[1] + r;
     }
-    __syncthreads();
-    if (need) c.node_slot[p] = n_slots0 + base + ex;
-    base += tot;
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < io.n_par; k += blockDim.x) {  // release claims
-    const int p = io.parents[k];
-    if (p >= 0 && p < n_nodes0) c.node_claim[p] = INT32_MAX;
-  }
-  if (threadIdx.x == 0) {
-    c.counters[CNT_NODES] = n_nodes0 + n_new;
-    c.counters[CNT_SLOTS] = n_slots0 + base;
-    *R_out = base;
+    if (p >= 0 && p < io.snap[0]) c.node_claim[p] = INT32_MAX;  // release claims
   }
 }
 
@@ -254,7 +313,11 @@ void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st) {
     launch_pdl(k_plan_intern, (n + 255) / 256, 256, 0, st, c, io);
     CK_LAUNCH();
   }
-  launch_pdl(k_plan_assign, 1, 1024, 0, st, c, io, R_dev);
+  const int Bc = (io.n_cand + kPlanBlock - 1) / kPlanBlock, Bp = (io.n_par + kPlanBlock - 1) / kPlanBlock;
+  const int B = Bc + Bp > 0 ? Bc + Bp : 1;
+  launch_pdl(k_plan_flags, B, kPlanBlock, 0, st, c, io, Bc);
+  CK_LAUNCH();
+  launch_pdl(k_plan_assign, B, kPlanBlock, 0, st, c, io, Bc, Bp, R_dev);
   CK_LAUNCH();
 }
 

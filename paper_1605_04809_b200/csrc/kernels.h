@@ -37,6 +37,10 @@ struct PlanIO {
   int* row_y;           // [n_par] previous word of each row
   int* row_dst;         // [n_par] output slot of each row
   int* row_node;        // [n_par] node id of each row
+  int* cflag;           // [n_cand] first appearance of a new key
+  int* pflag;           // [n_par] parent must be stepped
+  int* bcount;          // [blocks] per-block flag counts
+  int* snap;            // [2] node / slot counters at plan start
 };
 
 // Decoder-step workspace view (rows r < *R).

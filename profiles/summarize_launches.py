@@ -14,6 +14,8 @@ def short(name: str) -> str:
     base = m.group(1)
     if base == "k_gemm":
         base += m.group(2).replace("(int)", "")
+    if base == "k_enc_recur":
+        base = "k_enc_recur"
     return base
 
 
@@ -23,10 +25,11 @@ def main(path: str, out_json: str) -> None:
     launches = [(short(r["Kernel Name"]), float(r["Metric Value"]) / 1000.0) for r in rows
                 if r["Metric Name"] == "gpu__time_duration.sum"]
     # a step starts at k_enc_gather; keep the last complete step
-    starts = [i for i, (n, _) in enumerate(launches) if n == "k_enc_gather"]
+    starts = [i for i, (n, _) in enumerate(launches) if n.startswith("k_enc_recur")]
     i0 = starts[-2] if len(starts) >= 2 else starts[-1]
     i1 = starts[-1] if len(starts) >= 2 else len(launches)
-    step = [x for x in launches[i0:i1] if not x[0].startswith("torch:")]
+    # a step = the launches from one encoder recurrence to the next (encode + inject + score)
+    step = [x for x in launches[i0 - 1:i1 - 1] if not x[0].startswith("torch:")]
     tot = sum(t for _, t in step)
     agg = OrderedDict()
     for n, t in step:
