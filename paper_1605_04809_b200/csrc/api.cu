@@ -124,7 +124,8 @@ struct nmt_model {
   float* W_o32 = nullptr;         // [V][Ep]
   float* b_o = nullptr;           // [V]
   int g2_bn = 256;  // N tile of the GRU2 region GEMM (256 when the regions are 256-aligned)
-  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo;
+  bool use_pair_vocab = true;  // CTA-pair (cta_group::2) vocabulary GEMM on the bf16 path (NMT_PAIR_VOCAB=0 disables)
+  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128;
   // encoder workspace
   int Tpad = 0;
   __nv_bfloat16* ctxbf = nullptr; // [Tpad][4Hp]
@@ -710,6 +711,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, m->g2_bn);
   m->tm_Wro = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 128);
   m->tm_Wo = make_tmap_bf16(m->W_o, Vp, sf * Ep, 256);
+  m->tm_Wo128 = make_tmap_bf16(m->W_o, Vp, sf * Ep, 128);  // CTA-pair vocabulary GEMM: half tiles
 
   // ---- encoder workspace
   m->Tpad = round_up(m->maxTx, 128);
@@ -801,6 +803,7 @@ static void parse_and_build(const char* buf, size_t len, const nmt_opts* opts, n
     m->own_stream = true;
   }
   m->split = o.precision == NMT_PREC_FP32CLASS;
+  if (const char* ev = getenv("NMT_PAIR_VOCAB")) m->use_pair_vocab = atoi(ev) != 0;
   m->sf = m->split ? 2 : 1;
   m->E = E;
   m->H = H;
@@ -887,7 +890,12 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
   { ProfScope p_(m, ST_GEMM_RO); gemm_store(m->tm_X, m->tm_Wro, gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp), m->RO_buf, m->ROp,
              m->R_cap, nullptr, R_max, st); }
   { ProfScope p_(m, ST_READOUT); step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  { ProfScope p_(m, ST_VOCAB); gemm_lse(m->tm_At, m->tm_Wo, gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep), m->part, m->V, R_max, st, m->lse_cpm); }
+  {
+    ProfScope p_(m, ST_VOCAB);
+    const GemmShape g = gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep);
+    if (!sp && m->use_pair_vocab) gemm_lse_pair(m->tm_At, m->tm_Wo128, g, m->part, m->V, st, m->lse_cpm);
+    else gemm_lse(m->tm_At, m->tm_Wo, g, m->part, m->V, R_max, st, m->lse_cpm);
+  }
   { ProfScope p_(m, ST_FINALIZE); step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
 }
 
@@ -1556,7 +1564,7 @@ nmt_status nmt_debug_intermediates(nmt_ctx* c, nmt_state node, float* s1, float*
 
 nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_t epi, int32_t ksplit, int32_t iters,
                           float* ms_out) {
-  if (M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || !ms_out || (epi == 0 && N % 128) || (epi >= 1 && N % 256))
+  if (M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || !ms_out || (epi == 0 && N % 128) || (epi >= 1 && N % 256) || epi > 4)
     return fail(NMT_ERR_INVALID_ARG, "nmt_bench_gemm: bad shape");
   return guard([&] {
     cudaStream_t st;
@@ -1576,10 +1584,12 @@ nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_
       CK(cudaMemcpy(b, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice));
     }
     CUtensorMap ta = make_tmap_bf16(a, Mp, sf * K, 128), tb = make_tmap_bf16(b, N, sf * K, epi >= 1 ? 256 : 128);
+    CUtensorMap tb128 = make_tmap_bf16(b, N, sf * K, 128);
     GemmShape g = gemm_shape(M, nullptr, N, K, 0, split != 0, K, K);
     g.ksplit = ksplit;
     auto run = [&] {
       if (epi == 1) gemm_lse(ta, tb, g, part, N, M, st, cpm);
+      else if (epi == 4) gemm_lse_pair(ta, tb128, g, part, N, st, cpm);
       else if (epi == 2) gemm_store256(ta, tb, g, c, N, ksplit * Mp, nullptr, M, st, (size_t)Mp * N);
       else gemm_store(ta, tb, g, c, N, ksplit * Mp, nullptr, M, st, (size_t)Mp * N);
     };

@@ -323,6 +323,207 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------------------------- CTA-pair vocab GEMM
+// cta_group::2 variant of the fused vocabulary kernel: a cluster of 2 CTAs computes 256 x BN tiles
+// (M = 256 across the pair, each CTA holds its 128 rows of A and HALF of the B tile), so per SM a
+// k-block moves 32 KB (16 KB A + 16 KB B) for 512 MMA cycles instead of 48 KB, and 6 stages fit.
+// Protocol (as CUTLASS' 2SM kernels): both CTAs TMA into their own smem and count bytes on the
+// leader's full barrier (+1 remote arrive from the peer); the leader issues the MMAs and commits
+// with multicast to both CTAs' empty / tfull barriers; every epilogue warp of both CTAs arrives on
+// the leader's tempty barrier.  Epilogue = EPI_LSE of k_gemm (per row running max/sum/argmax).
+template <int BN, int STAGES>
+struct PairSmem {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int BYTES = 1024 + STAGES * (A_BYTES + B_BYTES) + (2 * STAGES + 4) * 8 + 16;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    k_gemm_pair_lse(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmShape g,
+                    EpiParams ep) {
+  using S = PairSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * S::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * S::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 2);   // leader's expect_tx arrive + the peer's remote arrive
+      mbar_init(&empty[s], 1);  // the leader's multicast commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * EPI_WARPS);  // epilogue warps of both CTAs (used on the leader)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 2 * BN);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_enter();
+  const int M = g.M_dev ? *g.M_dev : g.M;
+  const int num_m2 = (M + 2 * BM - 1) / (2 * BM), num_n = g.N / BN;
+  const int ncl = gridDim.x / 2, cid = blockIdx.x / 2;
+  const int cpm = max(1, ncl / max(1, num_m2));
+  const int chunk = (num_n + cpm - 1) / cpm;
+  const int items = num_m2 * cpm;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = cpm;
+  const int nkb = (g.reg_k1[0] - g.reg_k0[0]) / BK, kb0 = g.reg_k0[0] / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      const uint32_t full0 = mapa_shared(smem_u32(full), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = cid; w < items; w += ncl) {
+        const int m2 = w / cpm, c = w % cpm;
+        const int n0 = min(num_n, c * chunk), n1 = min(num_n, n0 + chunk);
+        for (int n = n0; n < n1; ++n) {
+          for (int kb = kb0; kb < kb0 + nkb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (S::A_BYTES + S::B_BYTES));
+            else mbar_arrive_cluster(full0 + stage * 8);
+            tma_load_2d_pair(&tmA, &full[stage], sA + stage * S::A_BYTES, g.a_col0 + kb * BK, m2 * 2 * BM + rank * BM);
+            tma_load_2d_pair(&tmB, &full[stage], sB + stage * S::B_BYTES, kb * BK, n * BN + rank * (BN / 2));
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only)
+      constexpr uint32_t idesc = idesc_bf16(2 * BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int w = cid; w < items; w += ncl) {
+        const int c = w % cpm;
+        const int n0 = min(num_n, c * chunk), n1 = min(num_n, n0 + chunk);
+        for (int n = n0; n < n1; ++n, ++it) {
+          const int acc = it & 1;
+          const uint32_t aph = (it >> 1) & 1;
+          mbar_wait(&tempty[acc], aph ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + acc * BN;
+          for (int i = 0; i < nkb; ++i) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + stage * S::A_BYTES);
+            const uint32_t b0 = smem_u32(sB + stage * S::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_pair(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
+            mma_commit_pair(&empty[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          mma_commit_pair(&tfull[acc]);
+        }
+      }
+    }
+  } else {  // ---------------- epilogue warps 2..9 (both CTAs): EPI_LSE over this CTA's 128 rows
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    constexpr int COLS = BN / 2;
+    const int row_in_tile = q * 32 + lane;
+    const uint32_t tempty0 = mapa_shared(smem_u32(tempty), 0);
+    constexpr float LOG2E = 1.4426950408889634f;
+    int it = 0;
+    for (int w = cid; w < items; w += ncl) {
+      const int m2 = w / cpm, c = w % cpm;
+      const int n0 = min(num_n, c * chunk), n1 = min(num_n, n0 + chunk);
+      const int grow = m2 * 2 * BM + rank * BM + row_in_tile;
+      const bool valid = grow < M;
+      float mx = -INFINITY, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      int am = 0;
+      for (int n = n0; n < n1; ++n, ++it) {
+        const int acc = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + half * COLS;
+        const int colbase = n * BN + half * COLS;
+#pragma unroll 1
+        for (int cc = 0; cc < COLS; cc += 64) {
+          float v[64];
+          tmem_ld32_nowait(tbase + cc, v);
+          tmem_ld32_nowait(tbase + cc + 32, v + 32);
+          tmem_wait_ld_dep(v);
+          reg_dep32(v + 32);
+          const int col0 = colbase + cc;
+          if (col0 + 64 > ep.n_valid) {
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (col0 + j >= ep.n_valid) v[j] = -INFINITY;
+          }
+          float t32[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) t32[j] = fmaxf(v[j], v[j + 32]);
+#pragma unroll
+          for (int k = 16; k > 0; k >>= 1)
+#pragma unroll
+            for (int j = 0; j < k; ++j) t32[j] = fmaxf(t32[j], t32[j + k]);
+          const float cm = t32[0];
+          if (cm > mx) {
+            int ix[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ix[j] = v[j] == cm ? j : (v[j + 32] == cm ? j + 32 : 64);
+#pragma unroll
+            for (int k = 16; k > 0; k >>= 1)
+#pragma unroll
+              for (int j = 0; j < k; ++j) ix[j] = min(ix[j], ix[j + k]);
+            const float f = ex2_approx((mx - cm) * LOG2E);
+            s0 *= f; s1 *= f; s2 *= f; s3 *= f;
+            mx = cm;
+            am = col0 + ix[0];
+          }
+          if (mx > -INFINITY) {
+            const float mb = mx * LOG2E;
+#pragma unroll
+            for (int j = 0; j < 64; j += 4) {
+              s0 += ex2_approx(fmaf(v[j], LOG2E, -mb));
+              s1 += ex2_approx(fmaf(v[j + 1], LOG2E, -mb));
+              s2 += ex2_approx(fmaf(v[j + 2], LOG2E, -mb));
+              s3 += ex2_approx(fmaf(v[j + 3], LOG2E, -mb));
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[acc]);
+          else mbar_arrive_cluster(tempty0 + acc * 8);
+        }
+      }
+      if (valid) ep.part[((size_t)grow * cpm + c) * 2 + half] = make_float4(mx, (s0 + s1) + (s2 + s3), __int_as_float(am), 0.f);
+    }
+  }
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 2 * BN);
+  }
+}
+
 // ------------------------------------------------------------------------------------- host side
 typedef CUresult (*PFN_tmapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -451,6 +652,41 @@ void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, fl
   ep.n_tiles = g.N / 256;
   ep.cpm_out = cpm_out;
   launch<256, 4, EPI_LSE>(a, b, b /*unused*/, g, ep, M_max, st);
+}
+
+// CTA-pair vocabulary GEMM (single pass, single region): `b_half` must be a tensor map of B with a
+// 128-row box (each CTA of a pair loads half of the 256-column tile).
+void gemm_lse_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float4* part, int n_valid,
+                   cudaStream_t st, int* cpm_out) {
+  gemm_validate(g, 256);
+  if (g.passes != 1 || g.nreg != 1 || g.ksplit != 1) throw NmtError(NMT_ERR_INVALID_ARG, "gemm_lse_pair: bad shape");
+  EpiParams ep{};
+  ep.part = part;
+  ep.n_valid = n_valid;
+  ep.n_tiles = g.N / 256;
+  ep.cpm_out = cpm_out;
+  using S = PairSmem<256, 6>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_gemm_pair_lse<256, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kNumSMs);  // 74 CTA pairs, persistent
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = S::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  CK(cudaLaunchKernelEx(&cfg, k_gemm_pair_lse<256, 6>, a, b_half, g, ep));
+  CK_LAUNCH();
 }
 
 }  // namespace nmt
