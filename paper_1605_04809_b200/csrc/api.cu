@@ -123,8 +123,7 @@ struct nmt_model {
   __nv_bfloat16* W_o = nullptr;   // [Vp][sf Ep]
   float* W_o32 = nullptr;         // [V][Ep]
   float* b_o = nullptr;           // [V]
-  int g2_bn = 256;  // N tile of the GRU2 region GEMM (256 when the regions are 256-aligned)
-  bool use_pair_vocab = true;  // CTA-pair (cta_group::2) vocabulary GEMM on the bf16 path (NMT_PAIR_VOCAB=0 disables)
+  bool use_pair = true;  // CTA-pair (cta_group::2) GEMMs where the shapes allow (NMT_PAIR=0 disables)
   CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128;
   // encoder workspace
   int Tpad = 0;
@@ -707,8 +706,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   m->tm_Watt = make_tmap_bf16(m->Watt, Cp, 2 * Cp, 128);
   m->tm_Wh1 = make_tmap_bf16(m->W_h1, 3 * Hp, sf * Hp, 128);
   m->tm_Wq = make_tmap_bf16(m->W_q, Cp, sf * Hp, 128);
-  m->g2_bn = Hp % 256 == 0 ? 256 : 128;  // region boundaries (2Hp, 3Hp) must be tile aligned
-  m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, m->g2_bn);
+  m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, 128);
   m->tm_Wro = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 128);
   m->tm_Wo = make_tmap_bf16(m->W_o, Vp, sf * Ep, 256);
   m->tm_Wo128 = make_tmap_bf16(m->W_o, Vp, sf * Ep, 128);  // CTA-pair vocabulary GEMM: half tiles
@@ -803,7 +801,7 @@ static void parse_and_build(const char* buf, size_t len, const nmt_opts* opts, n
     m->own_stream = true;
   }
   m->split = o.precision == NMT_PREC_FP32CLASS;
-  if (const char* ev = getenv("NMT_PAIR_VOCAB")) m->use_pair_vocab = atoi(ev) != 0;
+  if (const char* ev = getenv("NMT_PAIR")) m->use_pair = atoi(ev) != 0;
   m->sf = m->split ? 2 : 1;
   m->E = E;
   m->H = H;
@@ -863,6 +861,16 @@ static StepDev step_view(nmt_model* m, nmt_ctx* c) {
   return d;
 }
 
+// fp32-output GEMM: CTA pairs with 256 x 256 tiles when N and the region boundaries are multiples of
+// 256, else single-CTA 128 x 128 tiles.  `b128` = weight tensor map with a 128-row box.
+static void gemm_auto(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b128, const GemmShape& g, float* out,
+                      int ldc, int out_rows, const float* bias, int M_max, cudaStream_t st) {
+  bool aligned = g.N % 256 == 0;
+  for (int r = 0; r < g.nreg - 1; ++r) aligned = aligned && g.reg_n_end[r] % 256 == 0;
+  if (m->use_pair && aligned) gemm_store_pair(a, b128, g, out, ldc, out_rows, bias, M_max, st);
+  else gemm_store(a, b128, g, out, ldc, out_rows, bias, M_max, st);
+}
+
 // one decoder forward step over the rows planned in m->row_* (count at c->counters[CNT_R])
 static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
   cudaStream_t st = m->st;
@@ -872,9 +880,9 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
   const int Hp = m->Hp, Cp = m->Cp, Ep = m->Ep;
   const bool sp = m->split;
   { ProfScope p_(m, ST_GATHER); step_elementwise(EW_GATHER, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  { ProfScope p_(m, ST_GEMM_H1); gemm_store(m->tm_As, m->tm_Wh1, gemm_shape(0, Rd, 3 * Hp, Hp, 0, sp, Hp, Hp), m->G1, 3 * Hp, m->R_cap, nullptr, R_max, st); }
+  { ProfScope p_(m, ST_GEMM_H1); gemm_auto(m, m->tm_As, m->tm_Wh1, gemm_shape(0, Rd, 3 * Hp, Hp, 0, sp, Hp, Hp), m->G1, 3 * Hp, m->R_cap, nullptr, R_max, st); }
   { ProfScope p_(m, ST_GRU1); step_elementwise(EW_GRU1, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  { ProfScope p_(m, ST_GEMM_Q); gemm_store(m->tm_X, m->tm_Wq, gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp), m->Q, Cp, m->R_cap, nullptr, R_max, st); }
+  { ProfScope p_(m, ST_GEMM_Q); gemm_auto(m, m->tm_X, m->tm_Wq, gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp), m->Q, Cp, m->R_cap, nullptr, R_max, st); }
   { ProfScope p_(m, ST_ATTN); step_elementwise(EW_ATTN, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   {
     ProfScope p_(m, ST_GEMM_G2);
@@ -883,17 +891,16 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
     g.reg_n_end[0] = 2 * Hp, g.reg_k0[0] = 0, g.reg_k1[0] = Hp + Cp;  // gates: s1 U_nl + c Wc
     g.reg_n_end[1] = 3 * Hp, g.reg_k0[1] = 0, g.reg_k1[1] = Hp;       // s1 Ux_nl
     g.reg_n_end[2] = 4 * Hp, g.reg_k0[2] = Hp, g.reg_k1[2] = Hp + Cp; // c Wcx
-    if (m->g2_bn == 256) gemm_store256(m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, m->R_cap, nullptr, R_max, st);
-    else gemm_store(m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, m->R_cap, nullptr, R_max, st);
+    gemm_auto(m, m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, m->R_cap, nullptr, R_max, st);
   }
   { ProfScope p_(m, ST_GRU2); step_elementwise(EW_GRU2, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  { ProfScope p_(m, ST_GEMM_RO); gemm_store(m->tm_X, m->tm_Wro, gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp), m->RO_buf, m->ROp,
+  { ProfScope p_(m, ST_GEMM_RO); gemm_auto(m, m->tm_X, m->tm_Wro, gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp), m->RO_buf, m->ROp,
              m->R_cap, nullptr, R_max, st); }
   { ProfScope p_(m, ST_READOUT); step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   {
     ProfScope p_(m, ST_VOCAB);
     const GemmShape g = gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep);
-    if (!sp && m->use_pair_vocab) gemm_lse_pair(m->tm_At, m->tm_Wo128, g, m->part, m->V, st, m->lse_cpm);
+    if (m->use_pair) gemm_lse_pair(m->tm_At, m->tm_Wo128, g, m->part, m->V, st, m->lse_cpm);
     else gemm_lse(m->tm_At, m->tm_Wo, g, m->part, m->V, R_max, st, m->lse_cpm);
   }
   { ProfScope p_(m, ST_FINALIZE); step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }

@@ -35,10 +35,17 @@ constexpr int EPI_STORE = 0, EPI_LSE = 1;
 constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant, each owning half of the tile's columns
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
-template <int BN, int STAGES, int EPI>
+// PAIR (cta_group::2): a cluster of 2 CTAs computes 256 x BN tiles - M = 256 across the pair, each
+// CTA holds its 128 rows of A and HALF of the B tile, so per SM a k-block moves (16 + BN/8) KB for
+// the MMA work of a 128 x BN tile.  Protocol (as CUTLASS' 2SM kernels): both CTAs TMA into their own
+// smem and count bytes on the leader's full barrier (+1 remote arrive from the peer); the leader
+// issues the MMAs and commits with multicast to both CTAs' empty / tfull barriers; every epilogue
+// warp of both CTAs arrives on the leader's tempty barrier.
+template <int BN, int STAGES, int EPI, bool PAIR>
 struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_ROWS = PAIR ? BN / 2 : BN;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
   // EPI_STORE: per epilogue warp two 32 x 32 fp32 staging tiles (128B-swizzled) for TMA stores
   static constexpr int C_BYTES = EPI == 0 ? EPI_WARPS * 2 * 4096 : 0;
   static constexpr int BYTES = 1024 + STAGES * (A_BYTES + B_BYTES) + C_BYTES + (2 * STAGES + 4) * 8 + 16;
@@ -54,8 +61,9 @@ struct TileCoord {
 NMT_DEV TileCoord tile_of(int t, int num_m, int num_n) {
   return TileCoord{t % num_m, (t / num_m) % num_n, t / (num_m * num_n)};
 }
-// Work items: EPI_STORE -> one tile per item (m fastest, so concurrent CTAs share B tiles in L2).
-// EPI_LSE -> item = (m-tile, contiguous run of n-tiles): the CTA keeps each row's running
+// Work items over m-tiles of CM = 128 (or 256 rows for a CTA pair) and n-tiles of BN:
+// EPI_STORE -> one tile per item (m fastest, so concurrent units share B tiles in L2).
+// EPI_LSE -> item = (m-tile, contiguous run of n-tiles): the unit keeps each row's running
 // (max, sum, argmax) across its run and emits ONE partial per row and run half.
 struct Item {
   int m, s, n0, n1, c;
@@ -73,13 +81,13 @@ struct Sched {
   }
 };
 template <int EPI>
-NMT_DEV Sched make_sched(int M, int N, int BN, int ksplit) {
+NMT_DEV Sched make_sched(int M, int CM, int N, int BN, int ksplit, int units) {
   Sched s;
-  s.num_m = (M + BM - 1) / BM;
+  s.num_m = (M + CM - 1) / CM;
   s.num_n = N / BN;
   s.ksplit = ksplit;
   if (EPI == 1) {  // EPI_LSE
-    s.cpm = max(1, (int)gridDim.x / max(1, s.num_m));
+    s.cpm = max(1, units / max(1, s.num_m));
     s.chunk = (s.num_n + s.cpm - 1) / s.cpm;
     s.items = s.num_m * s.cpm;
   } else {
@@ -97,11 +105,12 @@ NMT_DEV RegionK region_of(const GemmShape& g, int n0) {
   return RegionK{g.reg_k0[r] / BK, g.reg_k1[r] / BK};
 }
 
-template <int BN, int STAGES, int EPI>
+template <int BN, int STAGES, int EPI, bool PAIR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmC, GemmShape g, EpiParams ep) {
-  using S = GemmSmem<BN, STAGES, EPI>;
+  using S = GemmSmem<BN, STAGES, EPI, PAIR>;
+  constexpr int CM = PAIR ? 2 * BM : BM;  // rows of a tile (per CTA pair)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -115,36 +124,44 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if (EPI == EPI_STORE) tma_prefetch(&tmC);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], PAIR ? 2 : 1);  // (pair: the leader's expect_tx arrive + the peer's remote arrive)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_WARPS);
+      mbar_init(&tempty[a], (PAIR ? 2 : 1) * EPI_WARPS);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_pair(tmem_slot, 2 * BN);
+    else tmem_alloc(tmem_slot, 2 * BN);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_enter();  // prologue above overlaps the previous kernel; inputs (and M_dev) are read below
   const int M = g.M_dev ? *g.M_dev : g.M;
-  const Sched sc = make_sched<EPI>(M, g.N, BN, g.ksplit);
+  const int unit = PAIR ? blockIdx.x / 2 : blockIdx.x, nunits = PAIR ? gridDim.x / 2 : gridDim.x;
+  const Sched sc = make_sched<EPI>(M, CM, g.N, BN, g.ksplit, nunits);
   if (EPI == EPI_LSE && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs of a pair)
+      const uint32_t full0 = PAIR ? mapa_shared(smem_u32(full), 0) : 0;
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = blockIdx.x; w < sc.items; w += gridDim.x) {
+      for (int w = unit; w < sc.items; w += nunits) {
         const Item itm = sc.item(w);
         for (int n = itm.n0; n < itm.n1; ++n) {
           const TileCoord tc{itm.m, n, itm.s};
@@ -157,9 +174,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int aoff = g.a_col0 + (pass == 2 ? g.a_lo_off : 0);
             const int boff = (pass == 1 ? g.b_lo_off : 0);
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES);
-            tma_load_2d(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, tc.m * BM);
-            tma_load_2d(&tmB, &full[stage], sB + stage * S::B_BYTES, boff + kb * BK, tc.n * BN);
+            const int arow = tc.m * CM + rank * BM, brow = tc.n * BN + rank * S::B_ROWS;
+            if constexpr (PAIR) {
+              if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (S::A_BYTES + S::B_BYTES));
+              else mbar_arrive_cluster(full0 + stage * 8);
+              tma_load_2d_pair(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, arow);
+              tma_load_2d_pair(&tmB, &full[stage], sB + stage * S::B_BYTES, boff + kb * BK, brow);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES);
+              tma_load_2d(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, arow);
+              tma_load_2d(&tmB, &full[stage], sB + stage * S::B_BYTES, boff + kb * BK, brow);
+            }
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -169,12 +194,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      constexpr uint32_t idesc = idesc_bf16(BM, BN);
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (the pair's leader)
+      constexpr uint32_t idesc = idesc_bf16(CM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int w = blockIdx.x; w < sc.items; w += gridDim.x) {
+      for (int w = unit; w < sc.items; w += nunits) {
         const Item itm = sc.item(w);
         for (int n = itm.n0; n < itm.n1; ++n, ++it) {
           const TileCoord tc{itm.m, n, itm.s};
@@ -193,27 +218,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint32_t a0 = smem_u32(sA + stage * S::A_BYTES);
             const uint32_t b0 = smem_u32(sB + stage * S::B_BYTES);
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              mma_bf16(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
-            mma_commit(&empty[stage]);
+            for (int k = 0; k < BK / 16; ++k) {
+              if constexpr (PAIR)
+                mma_bf16_pair(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
+              else
+                mma_bf16(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
+            }
+            if constexpr (PAIR) mma_commit_pair(&empty[stage]);
+            else mma_commit(&empty[stage]);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
           }
-          mma_commit(&tfull[acc]);
+          if constexpr (PAIR) mma_commit_pair(&tfull[acc]);
+          else mma_commit(&tfull[acc]);
         }
       }
     }
-  } else {  // ---------------- epilogue warps 2..9
+  } else {  // ---------------- epilogue warps 2..9 (each CTA: its 128 rows of the tile)
     const int q = warp & 3;               // TMEM lane quadrant accessible to this warp
     const int half = (warp - 2) >> 2;     // which half of the tile's columns
     constexpr int COLS = BN / 2;
     const int row_in_tile = q * 32 + lane;
+    const uint32_t tempty0 = PAIR ? mapa_shared(smem_u32(tempty), 0) : 0;
     int it = 0;
-    for (int w = blockIdx.x; w < sc.items; w += gridDim.x) {
+    for (int w = unit; w < sc.items; w += nunits) {
       const Item itm = sc.item(w);
-      const int grow = itm.m * BM + row_in_tile;
+      const int grow = itm.m * CM + rank * BM + row_in_tile;
       const bool valid = grow < M;
       constexpr float LOG2E = 1.4426950408889634f;
       float mx = -INFINITY, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // LSE running state (per run)
@@ -228,7 +260,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if constexpr (EPI == EPI_STORE) {
           // TMEM -> registers (+bias) -> 128B-swizzled 32x32 smem tile -> TMA store (coalesced)
           uint8_t* stile = sC + (size_t)(warp - 2) * 2 * 4096;
-          const int row0 = itm.s * ep.rows_per_split + itm.m * BM + q * 32;
+          const int row0 = itm.s * ep.rows_per_split + itm.m * CM + rank * BM + q * 32;
 #pragma unroll 1
           for (int c = 0; c < COLS; c += 32) {
             uint8_t* buf = stile + ((c >> 5) & 1) * 4096;
@@ -306,7 +338,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[acc]);
+          else mbar_arrive_cluster(tempty0 + acc * 8);
+        }
       }
       if constexpr (EPI == EPI_LSE) {  // one partial per (row, run, half); empty runs give (-inf, 0)
         if (valid)
@@ -317,210 +352,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
   if (EPI == EPI_STORE && warp >= 2 && lane == 0) bulk_wait_all();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 2 * BN);
-  }
-}
-
-// ------------------------------------------------------------------------------------- CTA-pair vocab GEMM
-// cta_group::2 variant of the fused vocabulary kernel: a cluster of 2 CTAs computes 256 x BN tiles
-// (M = 256 across the pair, each CTA holds its 128 rows of A and HALF of the B tile), so per SM a
-// k-block moves 32 KB (16 KB A + 16 KB B) for 512 MMA cycles instead of 48 KB, and 6 stages fit.
-// Protocol (as CUTLASS' 2SM kernels): both CTAs TMA into their own smem and count bytes on the
-// leader's full barrier (+1 remote arrive from the peer); the leader issues the MMAs and commits
-// with multicast to both CTAs' empty / tfull barriers; every epilogue warp of both CTAs arrives on
-// the leader's tempty barrier.  Epilogue = EPI_LSE of k_gemm (per row running max/sum/argmax).
-template <int BN, int STAGES>
-struct PairSmem {
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = (BN / 2) * BK * 2;
-  static constexpr int BYTES = 1024 + STAGES * (A_BYTES + B_BYTES) + (2 * STAGES + 4) * 8 + 16;
-};
-
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-    k_gemm_pair_lse(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmShape g,
-                    EpiParams ep) {
-  using S = PairSmem<BN, STAGES>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * S::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * S::B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 2);   // leader's expect_tx arrive + the peer's remote arrive
-      mbar_init(&empty[s], 1);  // the leader's multicast commit
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * EPI_WARPS);  // epilogue warps of both CTAs (used on the leader)
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc_pair(tmem_slot, 2 * BN);
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_enter();
-  const int M = g.M_dev ? *g.M_dev : g.M;
-  const int num_m2 = (M + 2 * BM - 1) / (2 * BM), num_n = g.N / BN;
-  const int ncl = gridDim.x / 2, cid = blockIdx.x / 2;
-  const int cpm = max(1, ncl / max(1, num_m2));
-  const int chunk = (num_n + cpm - 1) / cpm;
-  const int items = num_m2 * cpm;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = cpm;
-  const int nkb = (g.reg_k1[0] - g.reg_k0[0]) / BK, kb0 = g.reg_k0[0] / BK;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
-      const uint32_t full0 = mapa_shared(smem_u32(full), 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int w = cid; w < items; w += ncl) {
-        const int m2 = w / cpm, c = w % cpm;
-        const int n0 = min(num_n, c * chunk), n1 = min(num_n, n0 + chunk);
-        for (int n = n0; n < n1; ++n) {
-          for (int kb = kb0; kb < kb0 + nkb; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (S::A_BYTES + S::B_BYTES));
-            else mbar_arrive_cluster(full0 + stage * 8);
-            tma_load_2d_pair(&tmA, &full[stage], sA + stage * S::A_BYTES, g.a_col0 + kb * BK, m2 * 2 * BM + rank * BM);
-            tma_load_2d_pair(&tmB, &full[stage], sB + stage * S::B_BYTES, kb * BK, n * BN + rank * (BN / 2));
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only)
-      constexpr uint32_t idesc = idesc_bf16(2 * BM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int w = cid; w < items; w += ncl) {
-        const int c = w % cpm;
-        const int n0 = min(num_n, c * chunk), n1 = min(num_n, n0 + chunk);
-        for (int n = n0; n < n1; ++n, ++it) {
-          const int acc = it & 1;
-          const uint32_t aph = (it >> 1) & 1;
-          mbar_wait(&tempty[acc], aph ^ 1);
-          tc_fence_after();
-          const uint32_t d = tmem + acc * BN;
-          for (int i = 0; i < nkb; ++i) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + stage * S::A_BYTES);
-            const uint32_t b0 = smem_u32(sB + stage * S::B_BYTES);
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              mma_bf16_pair(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
-            mma_commit_pair(&empty[stage]);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-          mma_commit_pair(&tfull[acc]);
-        }
-      }
-    }
-  } else {  // ---------------- epilogue warps 2..9 (both CTAs): EPI_LSE over this CTA's 128 rows
-    const int q = warp & 3;
-    const int half = (warp - 2) >> 2;
-    constexpr int COLS = BN / 2;
-    const int row_in_tile = q * 32 + lane;
-    const uint32_t tempty0 = mapa_shared(smem_u32(tempty), 0);
-    constexpr float LOG2E = 1.4426950408889634f;
-    int it = 0;
-    for (int w = cid; w < items; w += ncl) {
-      const int m2 = w / cpm, c = w % cpm;
-      const int n0 = min(num_n, c * chunk), n1 = min(num_n, n0 + chunk);
-      const int grow = m2 * 2 * BM + rank * BM + row_in_tile;
-      const bool valid = grow < M;
-      float mx = -INFINITY, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-      int am = 0;
-      for (int n = n0; n < n1; ++n, ++it) {
-        const int acc = it & 1;
-        const uint32_t aph = (it >> 1) & 1;
-        mbar_wait(&tfull[acc], aph);
-        tc_fence_after();
-        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + half * COLS;
-        const int colbase = n * BN + half * COLS;
-#pragma unroll 1
-        for (int cc = 0; cc < COLS; cc += 64) {
-          float v[64];
-          tmem_ld32_nowait(tbase + cc, v);
-          tmem_ld32_nowait(tbase + cc + 32, v + 32);
-          tmem_wait_ld_dep(v);
-          reg_dep32(v + 32);
-          const int col0 = colbase + cc;
-          if (col0 + 64 > ep.n_valid) {
-#pragma unroll
-            for (int j = 0; j < 64; ++j)
-              if (col0 + j >= ep.n_valid) v[j] = -INFINITY;
-          }
-          float t32[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) t32[j] = fmaxf(v[j], v[j + 32]);
-#pragma unroll
-          for (int k = 16; k > 0; k >>= 1)
-#pragma unroll
-            for (int j = 0; j < k; ++j) t32[j] = fmaxf(t32[j], t32[j + k]);
-          const float cm = t32[0];
-          if (cm > mx) {
-            int ix[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) ix[j] = v[j] == cm ? j : (v[j + 32] == cm ? j + 32 : 64);
-#pragma unroll
-            for (int k = 16; k > 0; k >>= 1)
-#pragma unroll
-              for (int j = 0; j < k; ++j) ix[j] = min(ix[j], ix[j + k]);
-            const float f = ex2_approx((mx - cm) * LOG2E);
-            s0 *= f; s1 *= f; s2 *= f; s3 *= f;
-            mx = cm;
-            am = col0 + ix[0];
-          }
-          if (mx > -INFINITY) {
-            const float mb = mx * LOG2E;
-#pragma unroll
-            for (int j = 0; j < 64; j += 4) {
-              s0 += ex2_approx(fmaf(v[j], LOG2E, -mb));
-              s1 += ex2_approx(fmaf(v[j + 1], LOG2E, -mb));
-              s2 += ex2_approx(fmaf(v[j + 2], LOG2E, -mb));
-              s3 += ex2_approx(fmaf(v[j + 3], LOG2E, -mb));
-            }
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive(&tempty[acc]);
-          else mbar_arrive_cluster(tempty0 + acc * 8);
-        }
-      }
-      if (valid) ep.part[((size_t)grow * cpm + c) * 2 + half] = make_float4(mx, (s0 + s1) + (s2 + s3), __int_as_float(am), 0.f);
-    }
-  }
-  __syncthreads();
-  cluster_sync();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc_pair(tmem, 2 * BN);
+    if constexpr (PAIR) tmem_dealloc_pair(tmem, 2 * BN);
+    else tmem_dealloc(tmem, 2 * BN);
   }
 }
 
@@ -582,19 +418,36 @@ static const CUtensorMap& out_map(const float* out, uint64_t rows, uint64_t ldc)
   return it->second;
 }
 
-template <int BN, int STAGES, int EPI>
+template <int BN, int STAGES, int EPI, bool PAIR>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmShape& g,
                    const EpiParams& ep, int M_max, cudaStream_t st) {
-  using S = GemmSmem<BN, STAGES, EPI>;
+  using S = GemmSmem<BN, STAGES, EPI, PAIR>;
+  static_assert(S::BYTES <= 232448, "shared memory budget");
   static bool attr_set = false;  // per template instance; set once per process (single device use)
   if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_gemm<BN, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
+    CK(cudaFuncSetAttribute(k_gemm<BN, STAGES, EPI, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
     attr_set = true;
   }
-  const int tiles = ((M_max + BM - 1) / BM) * (g.N / BN) * g.ksplit;
-  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  const int CM = PAIR ? 2 * BM : BM;
+  const int tiles = ((M_max + CM - 1) / CM) * (g.N / BN) * g.ksplit;
+  int grid = (PAIR ? 2 : 1) * tiles;
+  if (EPI == EPI_LSE || grid > kNumSMs) grid = kNumSMs;  // persistent (LSE runs use every unit)
   if (grid <= 0) return;
-  launch_pdl(k_gemm<BN, STAGES, EPI>, grid, GEMM_THREADS, S::BYTES, st, a, b, c, g, ep);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = S::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = PAIR ? 2 : 1;
+  CK(cudaLaunchKernelEx(&cfg, k_gemm<BN, STAGES, EPI, PAIR>, a, b, c, g, ep));
   CK_LAUNCH();
 }
 
@@ -632,14 +485,21 @@ static EpiParams store_params(const GemmShape& g, int BN, float* out, int ldc, c
 void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc, int out_rows,
                 const float* bias, int M_max, cudaStream_t st, size_t split_stride) {
   const EpiParams ep = store_params(g, 128, out, ldc, bias, split_stride);
-  launch<128, 4, EPI_STORE>(a, b, out_map(out, out_rows, ldc), g, ep, M_max, st);
+  launch<128, 4, EPI_STORE, false>(a, b, out_map(out, out_rows, ldc), g, ep, M_max, st);
 }
 
 // fp32 output GEMM with 128 x 256 tiles (A reuse x2; fewer tiles)
 void gemm_store256(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc, int out_rows,
                    const float* bias, int M_max, cudaStream_t st, size_t split_stride) {
   const EpiParams ep = store_params(g, 256, out, ldc, bias, split_stride);
-  launch<256, 3, EPI_STORE>(a, b, out_map(out, out_rows, ldc), g, ep, M_max, st);
+  launch<256, 3, EPI_STORE, false>(a, b, out_map(out, out_rows, ldc), g, ep, M_max, st);
+}
+
+// fp32 output GEMM on CTA pairs: 256 x 256 tiles; `b_half` = tensor map of B with a 128-row box
+void gemm_store_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float* out, int ldc,
+                     int out_rows, const float* bias, int M_max, cudaStream_t st, size_t split_stride) {
+  const EpiParams ep = store_params(g, 256, out, ldc, bias, split_stride);
+  launch<256, 5, EPI_STORE, true>(a, b_half, out_map(out, out_rows, ldc), g, ep, M_max, st);
 }
 
 // fused vocabulary GEMM + online log-sum-exp partials; BN = 256.
@@ -651,42 +511,19 @@ void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, fl
   ep.n_valid = n_valid;
   ep.n_tiles = g.N / 256;
   ep.cpm_out = cpm_out;
-  launch<256, 4, EPI_LSE>(a, b, b /*unused*/, g, ep, M_max, st);
+  launch<256, 4, EPI_LSE, false>(a, b, b /*unused*/, g, ep, M_max, st);
 }
 
-// CTA-pair vocabulary GEMM (single pass, single region): `b_half` must be a tensor map of B with a
-// 128-row box (each CTA of a pair loads half of the 256-column tile).
+// vocabulary GEMM + LSE on CTA pairs; `b_half` = tensor map of B with a 128-row box
 void gemm_lse_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float4* part, int n_valid,
                    cudaStream_t st, int* cpm_out) {
   gemm_validate(g, 256);
-  if (g.passes != 1 || g.nreg != 1 || g.ksplit != 1) throw NmtError(NMT_ERR_INVALID_ARG, "gemm_lse_pair: bad shape");
   EpiParams ep{};
   ep.part = part;
   ep.n_valid = n_valid;
   ep.n_tiles = g.N / 256;
   ep.cpm_out = cpm_out;
-  using S = PairSmem<256, 6>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_gemm_pair_lse<256, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
-    attr_set = true;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(kNumSMs);  // 74 CTA pairs, persistent
-  cfg.blockDim = dim3(GEMM_THREADS);
-  cfg.dynamicSmemBytes = S::BYTES;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  CK(cudaLaunchKernelEx(&cfg, k_gemm_pair_lse<256, 6>, a, b_half, g, ep));
-  CK_LAUNCH();
+  launch<256, 6, EPI_LSE, true>(a, b_half, b_half /*unused*/, g, ep, kNumSMs * BM, st);
 }
 
 }  // namespace nmt

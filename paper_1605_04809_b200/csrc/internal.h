@@ -88,6 +88,8 @@ void gemm_store256(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& 
 // out[r][c] = bias[c] + sum_s part[s * stride + r * ldc + c]  (fixed order: deterministic)
 void splitk_reduce(const float* part, int ksplit, size_t stride, int M, int N, int ldc, const float* bias, float* out,
                    cudaStream_t st, __nv_bfloat16* out16 = nullptr);
+void gemm_store_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float* out, int ldc,
+                     int out_rows, const float* bias, int M_max, cudaStream_t st, size_t split_stride = 0);
 void gemm_lse_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float4* part, int n_valid,
                    cudaStream_t st, int* cpm_out);
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
