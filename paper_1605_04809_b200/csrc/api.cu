@@ -651,6 +651,13 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
     CK(cudaMemcpy2DAsync(m->W_o + E, pitch, bh.data(), 2, 2, V, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpy2DAsync(m->W_o + (m->split ? Ep + E : E + 1), pitch, bl.data(), 2, 2, V, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
+    // re-lay W_o^T as k-block panels [sf*Ep/64][Vp][64]: each TMA box of the vocabulary GEMM is
+    // then one contiguous chunk of HBM
+    __nv_bfloat16* panels = dalloc<__nv_bfloat16>((size_t)Vp * sf * Ep);
+    to_panels(m->W_o, Vp, sf * Ep, panels, st);
+    CK(cudaStreamSynchronize(st));
+    dfree(m->W_o);
+    m->W_o = panels;
   }
 
   // ---- precomputed target-embedding projections (always bf16x3): Ex = e.[W|Wx] + [b|bx],
@@ -708,8 +715,8 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   m->tm_Wq = make_tmap_bf16(m->W_q, Cp, sf * Hp, 128);
   m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, 128);
   m->tm_Wro = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 128);
-  m->tm_Wo = make_tmap_bf16(m->W_o, Vp, sf * Ep, 256);
-  m->tm_Wo128 = make_tmap_bf16(m->W_o, Vp, sf * Ep, 128);  // CTA-pair vocabulary GEMM: half tiles
+  m->tm_Wo = make_tmap_bf16(m->W_o, (uint64_t)Vp * sf * Ep / 64, 64, 256);     // panel layout
+  m->tm_Wo128 = make_tmap_bf16(m->W_o, (uint64_t)Vp * sf * Ep / 64, 64, 128);  // CTA-pair vocabulary GEMM: half tiles
 
   // ---- encoder workspace
   m->Tpad = round_up(m->maxTx, 128);
@@ -899,7 +906,8 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
   { ProfScope p_(m, ST_READOUT); step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   {
     ProfScope p_(m, ST_VOCAB);
-    const GemmShape g = gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep);
+    GemmShape g = gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep);
+    g.b_panel_rows = m->Vp;
     if (m->use_pair) gemm_lse_pair(m->tm_At, m->tm_Wo128, g, m->part, m->V, st, m->lse_cpm);
     else gemm_lse(m->tm_At, m->tm_Wo, g, m->part, m->V, R_max, st, m->lse_cpm);
   }

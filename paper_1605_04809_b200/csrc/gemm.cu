@@ -175,15 +175,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int boff = (pass == 1 ? g.b_lo_off : 0);
             mbar_wait(&empty[stage], phase ^ 1);
             const int arow = tc.m * CM + rank * BM, brow = tc.n * BN + rank * S::B_ROWS;
+            const int bx = g.b_panel_rows ? 0 : boff + kb * BK;
+            const int by = g.b_panel_rows ? (boff / BK + kb) * g.b_panel_rows + brow : brow;
             if constexpr (PAIR) {
               if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (S::A_BYTES + S::B_BYTES));
               else mbar_arrive_cluster(full0 + stage * 8);
               tma_load_2d_pair(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, arow);
-              tma_load_2d_pair(&tmB, &full[stage], sB + stage * S::B_BYTES, boff + kb * BK, brow);
+              tma_load_2d_pair(&tmB, &full[stage], sB + stage * S::B_BYTES, bx, by);
             } else {
               mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES);
               tma_load_2d(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, arow);
-              tma_load_2d(&tmB, &full[stage], sB + stage * S::B_BYTES, boff + kb * BK, brow);
+              tma_load_2d(&tmB, &full[stage], sB + stage * S::B_BYTES, bx, by);
             }
             if (++stage == STAGES) {
               stage = 0;

@@ -66,6 +66,8 @@ struct GemmShape {
   int reg_k0[4];     // K range [k0, k1) of region r (multiples of 64, relative to a_col0 / 0)
   int reg_k1[4];
   int ksplit;        // split-K factor: split s writes its partial sum to out + s * split_stride
+  int b_panel_rows;  // 0: B is [N][K] row-major; else B is stored as k-block panels [K/64][b_panel_rows][64]
+                     // (every TMA box is one contiguous chunk): coordinate (0, kb * b_panel_rows + row)
 };
 
 struct EpiParams {
@@ -110,6 +112,7 @@ inline GemmShape gemm_shape(int M, const int* M_dev, int N, int K, int a_col0, b
   g.reg_k0[0] = 0;
   g.reg_k1[0] = K;
   g.ksplit = 1;
+  g.b_panel_rows = 0;
   return g;
 }
 

@@ -66,6 +66,20 @@ void pack_rows(const float* src, int ld_src, int rows, int K, __nv_bfloat16* dst
   CK_LAUNCH();
 }
 
+// row-major bf16 [rows][cols] -> k-block panels [cols/64][rows][64] (contiguous TMA boxes)
+__global__ void k_to_panels(const __nv_bfloat16* __restrict__ src, int rows, int cols, __nv_bfloat16* dst) {
+  pdl_enter();
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)rows * cols) return;
+  const int r = (int)(idx / cols), k = (int)(idx % cols);
+  dst[((int64_t)(k / 64) * rows + r) * 64 + (k % 64)] = src[idx];
+}
+void to_panels(const __nv_bfloat16* src, int rows, int cols, __nv_bfloat16* dst, cudaStream_t st) {
+  const int64_t n = (int64_t)rows * cols;
+  launch_pdl(k_to_panels, (unsigned)((n + 255) / 256), 256, 0, st, src, rows, cols, dst);
+  CK_LAUNCH();
+}
+
 // fp32 [K x N] -> fp32 [N x ld_dst] transposed (W_o columns as contiguous per-word rows)
 __global__ void k_transpose_f32(const float* __restrict__ src, int K, int N, float* dst, int ld_dst) {
   pdl_enter();

@@ -98,6 +98,7 @@ void pack_T(const float* src, int ld_src, int K, int N, __nv_bfloat16* dst, int 
             int kmap, int H, int Hp, int lo_off, cudaStream_t st);
 void pack_rows(const float* src, int ld_src, int rows, int K, __nv_bfloat16* dst, int ld_dst, int col0, int lo_off,
                cudaStream_t st);
+void to_panels(const __nv_bfloat16* src, int rows, int cols, __nv_bfloat16* dst, cudaStream_t st);
 void transpose_f32(const float* src, int K, int N, float* dst, int ld_dst, cudaStream_t st);
 void fill_i32(int* p, int64_t n, int v, cudaStream_t st);
 void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st);

@@ -186,11 +186,20 @@ def test_enru_ragged_batch_vs_oracle(enru, prec):
     check_top1(zrows, am[::10], TOL[prec])
 
 
-def test_enru_bench_config_sampled(enru):
-    """The bench.py launch configuration (R = 1024 parents x 3 candidates, bf16) checked on a sample of
-    rows the oracle computes one by one (rows are independent)."""
-    d, p, blob, om = enru
-    M = nmt().Model(blob, precision="bf16")
+@pytest.fixture(scope="module")
+def bench_model():
+    """Exactly the bench.py model: E 500, H 1024, V_s 50k, V_t 100k, MAXOUT readout, seed 2016."""
+    d = synth.Dims(500, 1024, 50000, 100000, "maxout")
+    p = synth.make_model(d, 2016)
+    return d, p, synth.params_bytes(d, p), O.Model(d, p)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32class"])
+def test_bench_config_sampled(bench_model, prec):
+    """The bench.py launch configuration (R = 1024 parents x 3 candidates, maxout, Tx = 50) checked on
+    a sample of rows the oracle computes one by one (rows are independent)."""
+    d, p, blob, om = bench_model
+    M = nmt().Model(blob, precision=prec)
     src = synth.make_source(d.vocab_src, 49, seed=2016)
     c = M.encode(src)
     R = 1024
@@ -206,7 +215,7 @@ def test_enru_bench_config_sampled(enru):
         lsm = O.log_softmax(out["z"][j])
         for i in range(off[r], off[r + 1]):
             worst = max(worst, abs(float(lp[i]) - lsm[words[i]]))
-        assert lsm[am[r]] >= lsm.max() - 2 * TOL["bf16"]
-    print(f"\n[parity] bench config R=1024 bf16 (sampled rows): max|dlogp| = {worst:.3e}")
-    assert worst < TOL["bf16"], worst
+        assert lsm[am[r]] >= lsm.max() - 2 * TOL[prec]
+    print(f"\n[parity] bench config R=1024 maxout {prec} (sampled rows): max|dlogp| = {worst:.3e}")
+    assert worst < TOL[prec], worst
     assert len(set(ch.tolist())) == len(ch)
