@@ -140,6 +140,7 @@ struct nmt_model {
   float *G1 = nullptr, *S1 = nullptr, *Q = nullptr, *Cf = nullptr, *G2 = nullptr, *RO_buf = nullptr, *alpha = nullptr;
   float4* part = nullptr;
   int* lse_cpm = nullptr;  // [1] runs per m-tile of the last vocabulary GEMM
+  int* inject_done = nullptr;  // [1] block counter of k_inject (reset by its last block)
   int *row_src = nullptr, *row_y = nullptr, *row_dst = nullptr, *row_node = nullptr;
   int *cand_k = nullptr, *cand_hslot = nullptr, *cflag = nullptr, *pflag = nullptr, *bcount = nullptr,
       *snap = nullptr;
@@ -156,6 +157,7 @@ struct nmt_model {
   // pinned host staging
   void* pin = nullptr;
   size_t pin_bytes = 0;
+  cudaEvent_t pin2_ev = nullptr;  // H2D of nmt_inject_states from page-locked caller memory
   std::mutex mu;
   // lifetime: one reference held by the user handle plus one per live context, so that
   // nmt_model_free and nmt_ctx_free may be called in any order
@@ -197,6 +199,8 @@ static void free_all_model(nmt_model* m) {
   dfree(m->fws_f);
   if (m->pin) cudaFreeHost(m->pin);
   m->pin = nullptr;
+  if (m->pin2_ev) cudaEventDestroy(m->pin2_ev);
+  m->pin2_ev = nullptr;
 }
 
 struct ProfScope {  // CUDA events around one stage's launches on the model stream
@@ -236,7 +240,7 @@ void nmt_model::free_ws() {
   for (__nv_bfloat16** p : {&A_s, &X, &A_t}) dfree(*p);
   for (float** p : {&G1, &S1, &Q, &Cf, &G2, &RO_buf, &alpha, &out_logp, &in_s}) dfree(*p);
   dfree(part);
-  for (int** p : {&lse_cpm, &row_src, &row_y, &row_dst, &row_node, &cand_k, &cand_hslot, &cflag, &pflag, &bcount, &snap,
+  for (int** p : {&lse_cpm, &inject_done, &row_src, &row_y, &row_dst, &row_node, &cand_k, &cand_hslot, &cflag, &pflag, &bcount, &snap,
                   &in_par, &in_off, &in_words,
                   &out_child, &out_amax})
     dfree(*p);
@@ -279,6 +283,7 @@ void nmt_model::ensure_ws(int R, int NC) {
   A_t = dalloc<__nv_bfloat16>((size_t)R_cap * sf * Ep);
   part = dalloc<float4>((size_t)R_cap * 2 * kNumSMs);  // <= 2 x (CTAs per m-tile) partials per row
   lse_cpm = dalloc<int>(1);
+  inject_done = dalloc<int>(1);
   row_src = dalloc<int>(R_cap);
   row_y = dalloc<int>(R_cap);
   row_dst = dalloc<int>(R_cap);
@@ -1445,16 +1450,25 @@ nmt_status nmt_inject_states(nmt_ctx* c, int32_t n, const float* s, const int32_
     m->ensure_ws(n, n);
     c->ensure(n, n);
     // (in_s holds R_cap x H floats; the y and ids use the candidate scratch)
+    // copy straight from the caller's arrays; for page-locked sources the call waits for the DMA
+    // only (not for the kernel), so the caller may reuse its buffers on return - pageable sources
+    // are staged synchronously by cudaMemcpyAsync itself
+    if (!m->pin2_ev) CK(cudaEventCreateWithFlags(&m->pin2_ev, cudaEventDisableTiming));
     CK(cudaMemcpyAsync(m->in_s, s, (size_t)n * m->H * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(m->in_words, y, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, s) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+      CK(cudaEventRecord(m->pin2_ev, st));
+      CK(cudaEventSynchronize(m->pin2_ev));
+    }
+    cudaGetLastError();  // (clear a possible "invalid value" from cudaPointerGetAttributes)
     {
       ProfScope p_(m, ST_INJECT);
-      inject(c->dev(), n, m->in_s, m->in_words, m->out_child, st);
+      inject(c->dev(), n, m->in_s, m->in_words, m->out_child, m->inject_done, st);
     }
-    std::vector<int> ids(n);
-    CK(cudaMemcpyAsync(ids.data(), m->out_child, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    for (int i = 0; i < n; ++i) out[i] = ids[i];
+    // injected nodes take the next n ids in order; the host mirror is exact here (synced above when
+    // stale), so no device round trip is needed
+    for (int i = 0; i < n; ++i) out[i] = c->n_nodes + i;
     c->n_nodes += n;
     c->n_slots += n;
   });
@@ -1467,9 +1481,10 @@ nmt_status nmt_inject_states_dev(nmt_ctx* c, int32_t n, const float* s, const in
     std::lock_guard<std::mutex> lk(m->mu);
     CK(cudaSetDevice(m->device));
     if (n == 0) return;
+    m->ensure_ws(1, 1);  // (workspace holds the inject block counter)
     c->ensure(n, n);
     ProfScope p_(m, ST_INJECT);
-    inject(c->dev(), n, s, y, out, m->st);
+    inject(c->dev(), n, s, y, out, m->inject_done, m->st);
     c->n_nodes += n;
     c->n_slots += n;
   });

@@ -363,8 +363,9 @@ void fill_i32(int* p, int64_t n, int v, cudaStream_t st) {
   CK_LAUNCH();
 }
 
-// inject parentless nodes with their own input slots (synthetic parents for bench/tests)
-__global__ void k_inject(CtxDev c, int n, const float* s, const int* y, int* out_ids) {
+// inject parentless nodes with their own input slots (synthetic parents for bench/tests); the last
+// block to finish publishes the new node/slot counts (every block has read them by then)
+__global__ void k_inject(CtxDev c, int n, const float* s, const int* y, int* out_ids, int* done) {
   pdl_enter();
   const int n_nodes0 = c.counters[CNT_NODES], n_slots0 = c.counters[CNT_SLOTS];
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
@@ -385,16 +386,18 @@ __global__ void k_inject(CtxDev c, int n, const float* s, const int* y, int* out
       out_ids[i] = id;
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1) == (int)gridDim.x - 1) {
+      c.counters[CNT_NODES] = n_nodes0 + n;
+      c.counters[CNT_SLOTS] = n_slots0 + n;
+      *done = 0;
+    }
+  }
 }
-__global__ void k_inject_commit(CtxDev c, int n) {
-  pdl_enter();
-  c.counters[CNT_NODES] += n;
-  c.counters[CNT_SLOTS] += n;
-}
-void inject(const CtxDev& c, int n, const float* s, const int* y, int* out_ids, cudaStream_t st) {
-  launch_pdl(k_inject, n < 1024 ? n : 1024, 256, 0, st, c, n, s, y, out_ids);
-  CK_LAUNCH();
-  launch_pdl(k_inject_commit, 1, 1, 0, st, c, n);
+void inject(const CtxDev& c, int n, const float* s, const int* y, int* out_ids, int* done, cudaStream_t st) {
+  launch_pdl(k_inject, n < 1024 ? n : 1024, 256, 0, st, c, n, s, y, out_ids, done);
   CK_LAUNCH();
 }
 
@@ -747,10 +750,24 @@ __global__ void k_finalize(StepDev d, float* __restrict__ logZ, int* __restrict_
   }
 }
 
-// D9b: per candidate log p = t . W_o[:,w] + b_o[w] - logZ (fp32 gather-dot; also serves cache hits)
+// D9b: per candidate log p = t . W_o[:,w] + b_o[w] - logZ (fp32 gather-dot; also serves cache hits);
+// the trailing blocks write each parent's argmax.
 __global__ void k_gather_dot(CtxDev c, PlanIO io, const float* __restrict__ Wo32, const float* __restrict__ bo,
-                             int Ep, float* out_logp, int* out_child32, long long* out_child64) {
+                             int Ep, float* out_logp, int* out_child32, long long* out_child64, int* out_argmax,
+                             int cand_blocks) {
   pdl_enter();
+  if ((int)blockIdx.x >= cand_blocks) {  // parents' argmax
+    const int k = (blockIdx.x - cand_blocks) * blockDim.x + threadIdx.x;
+    if (k >= io.n_par) return;
+    const int p = io.parents[k];
+    int v = -1;
+    if (p >= 0 && p < c.counters[CNT_NODES]) {
+      const int slot = c.node_slot[p];
+      if (slot >= 0) v = c.amax[slot];
+    }
+    out_argmax[k] = v;
+    return;
+  }
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= io.n_cand) return;
   const int hs = io.cand_hslot[warp];
@@ -783,19 +800,6 @@ __global__ void k_gather_dot(CtxDev c, PlanIO io, const float* __restrict__ Wo32
     if (out_child32) out_child32[warp] = ch;
     if (out_child64) out_child64[warp] = ch;
   }
-}
-
-__global__ void k_argmax_out(CtxDev c, PlanIO io, int* out) {
-  pdl_enter();
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= io.n_par) return;
-  const int p = io.parents[k];
-  int v = -1;
-  if (p >= 0 && p < c.counters[CNT_NODES]) {
-    const int slot = c.node_slot[p];
-    if (slot >= 0) v = c.amax[slot];
-  }
-  out[k] = v;
 }
 
 // ScoreBatch forest helpers: parents of depth d+1 = children of depth d gathered by edge position;
@@ -876,15 +880,12 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
 
 void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const float* bo, int Ep, float* out_logp,
                 int* out_child32, long long* out_child64, int* out_argmax, cudaStream_t st) {
-  if (io.n_cand > 0) {
-    launch_pdl(k_gather_dot, (io.n_cand * 32 + 255) / 256, 256, 0, st, c, io, Wo32, bo, Ep, out_logp, out_child32,
-                                                                 out_child64);
-    CK_LAUNCH();
-  }
-  if (out_argmax && io.n_par > 0) {
-    launch_pdl(k_argmax_out, (io.n_par + 255) / 256, 256, 0, st, c, io, out_argmax);
-    CK_LAUNCH();
-  }
+  const int cb = (io.n_cand * 32 + 255) / 256;
+  const int pb = out_argmax ? (io.n_par + 255) / 256 : 0;
+  if (cb + pb == 0) return;
+  launch_pdl(k_gather_dot, cb + pb, 256, 0, st, c, io, Wo32, bo, Ep, out_logp, out_child32, out_child64, out_argmax,
+             cb);
+  CK_LAUNCH();
 }
 
 void full_row(const float* T, const float* Wo32, const float* bo, const float* logZ, int slot, int Ep, int V,

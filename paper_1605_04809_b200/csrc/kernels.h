@@ -104,7 +104,7 @@ void fill_i32(int* p, int64_t n, int v, cudaStream_t st);
 void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st);
 void rehash(const unsigned long long* okeys, const int* ovals, int64_t ocap, unsigned long long* nkeys, int* nvals,
             uint64_t nmask, cudaStream_t st);
-void inject(const CtxDev& c, int n, const float* s, const int* y, int* out_ids, cudaStream_t st);
+void inject(const CtxDev& c, int n, const float* s, const int* y, int* out_ids, int* done, cudaStream_t st);
 void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, float* T, float* logZ, int* amax,
                       int R_max, cudaStream_t st);
 void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const float* bo, int Ep, float* out_logp,
