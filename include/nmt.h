@@ -80,7 +80,7 @@ typedef struct {
 typedef struct {
   int32_t device;          /* CUDA device ordinal */
   nmt_precision precision; /* GEMM recipe, see above */
-  int32_t max_src_len;     /* 0 -> 64 */
+  int32_t max_src_len;     /* 0 -> 64; at most 65534 (else NMT_ERR_INVALID_ARG) */
   void* stream;            /* cudaStream_t the model's work is issued on; NULL -> a private stream */
 } nmt_opts;
 

@@ -132,6 +132,7 @@ struct nmt_model {
   float* enc_mean = nullptr;
   float* ksplit_buf = nullptr;  // split-K partials of the pctx GEMM
   int* bar = nullptr;
+  unsigned enc_epoch = 0;      // encodes since the last reset of hbuf / bar (k_enc_recur tags)
   int* d_src = nullptr;
   CUtensorMap tm_ctxbf;
   // step workspace
@@ -822,6 +823,8 @@ static void parse_and_build(const char* buf, size_t len, const nmt_opts* opts, n
   m->RO = RO;
   m->maxout = maxout;
   m->maxTx = o.max_src_len > 0 ? o.max_src_len : 64;
+  if (m->maxTx > 65534)  // the encoder's exchange tags carry t + 1 in 16 bits
+    throw NmtError(NMT_ERR_INVALID_ARG, "max_src_len > 65534");
   m->Ep = round_up(E + 2, 64);
   m->Hp = round_up(H, 128);
   m->Cp = 2 * m->Hp;
@@ -1030,8 +1033,6 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
     c = m->pool.back();
     m->pool.pop_back();
     c->m = m;
-    CK(cudaMemsetAsync(c->hkeys, 0xff, c->hcap * sizeof(unsigned long long), st));
-    fill_i32(c->hvals, c->hcap, INT32_MIN, st);
   } else {
     c = new nmt_ctx();
     c->m = m;
@@ -1044,13 +1045,12 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
   m->refs.fetch_add(1);
   c->Tx = len;
   std::unique_ptr<nmt_ctx> guard_c(c);
+  ctx_reset(c->dev(), c->hcap, st);  // counters, root node, empty hash table
   const int* d_src = src_dev;
   if (src_host) {
     CK(cudaMemcpyAsync(m->d_src, src_host, (size_t)len * 4, cudaMemcpyHostToDevice, st));
     d_src = m->d_src;
   }
-  static const int cnt[CNT_N] = {1, 2, 0, 0};  // static: source of an async copy
-  CK(cudaMemcpyAsync(c->counters, cnt, sizeof(cnt), cudaMemcpyHostToDevice, st));
   {  // E1-E6: gather of the precomputed input projections, bi-GRU recurrence, means, s0, ctx hi|lo
     EncDev e{};
     e.H = m->H;
@@ -1071,7 +1071,40 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
     e.b_init = m->b_init;
     e.S0 = c->S;
     ProfScope p_(m, ST_ENC_RECUR);
+    { const char* pm = getenv("NMT_ENC_POLL"); e.poll = pm ? atoi(pm) : 0; }
+    if (++m->enc_epoch > 65535) {  // tags carry a 16-bit epoch: reset them before it repeats
+      CK(cudaMemsetAsync(m->hbuf, 0, (size_t)8 * m->Hp * sizeof(float), st));
+      CK(cudaMemsetAsync(m->bar, 0, sizeof(int), st));
+      m->enc_epoch = 1;
+    }
+    e.epoch = m->enc_epoch;
+    const bool trace = getenv("NMT_ENC_TRACE") != nullptr;  // diagnostic: per-step phase stamps
+    if (trace) CK(cudaMalloc(&e.trace, (size_t)(len + 1) * 8 * sizeof(long long)));
     enc_recur(e, len, st);
+    if (trace) {
+      std::vector<long long> tv((size_t)(len + 1) * 8);
+      CK(cudaMemcpyAsync(tv.data(), e.trace, tv.size() * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      cudaFree(e.trace);
+      double ph[6] = {0, 0, 0, 0, 0, 0};
+      for (int t = 2; t < len - 1; ++t) {
+        const long long* r = &tv[(size_t)t * 8];
+        ph[0] += r[1] - r[0];        // fetch issue
+        ph[1] += r[2] - r[1];        // own polls
+        ph[2] += r[3] - r[2];        // barrier
+        ph[3] += r[4] - r[3];        // matvec + reduction
+        ph[4] += r[5] - r[4];        // gate + stores
+        ph[5] += r[8] - r[5];        // loop back
+      }
+      const double n = std::max(1, len - 3);
+      fprintf(stderr, "[enc_trace] Tx=%d cycles/step: fetch %.0f poll %.0f bar %.0f mv %.0f gate %.0f loop %.0f total %.0f polls/step %.2f\n",
+              len, ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, ph[4] / n, ph[5] / n,
+              (double)(tv[(size_t)(len - 1) * 8] - tv[16]) / (len - 3), (double)tv[(size_t)(len - 1) * 8 + 6] / len);
+      const long long* f = &tv[(size_t)len * 8];
+      fprintf(stderr, "[enc_trace] fixed cycles: weights %lld  to-first-step %lld  loop %lld  barrier %lld  s0 %lld"
+              "  | CTA0 %.1f us, %.0f MHz\n", f[1] - f[0], tv[0] - f[1], f[2] - tv[0], f[3] - f[2], f[4] - f[3],
+              (f[6] - f[5]) / 1000.0, (double)(f[4] - f[0]) / ((f[6] - f[5]) / 1000.0));
+    }
   }
   {  // E7: pctx = ctx.Wc_att + b_att
     ProfScope p_(m, ST_ENC_PCTX);
@@ -1084,12 +1117,6 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
     gemm_store(m->tm_ctxbf, m->tm_Watt, g, m->ksplit_buf, m->Cp, g.ksplit * m->Tpad, nullptr, len, st, stride);
     splitk_reduce(m->ksplit_buf, g.ksplit, stride, len, m->Cp, m->Cp, m->b_att, c->pctx, st);
   }
-  // root node 0 = (s0, BOS): word -1, parent -1, src slot 0, not stepped
-  static const int root[3] = {-1, -1, 0};
-  CK(cudaMemcpyAsync(c->node_word, &root[0], 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->node_parent, &root[1], 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->node_src, &root[2], 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->node_slot, &root[0], 4, cudaMemcpyHostToDevice, st));
   c->n_nodes = 1;
   c->n_slots = 2;
   c->stale = src_dev != nullptr;  // device ids are validated asynchronously

@@ -363,6 +363,32 @@ void fill_i32(int* p, int64_t n, int v, cudaStream_t st) {
   CK_LAUNCH();
 }
 
+// context (re)initialisation for nmt_encode, one launch: the hash table is emptied, the counters and
+// the root node 0 = (s0, BOS) (word -1, parent -1, state in slot 0, not stepped) are written
+__global__ void k_ctx_reset(CtxDev c, int64_t hcap) {
+  pdl_enter();
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = i0; i < hcap; i += (int64_t)gridDim.x * blockDim.x) {
+    c.hkeys[i] = ~0ull;
+    c.hvals[i] = INT32_MIN;
+  }
+  if (i0 == 0) {
+    c.counters[CNT_NODES] = 1;
+    c.counters[CNT_SLOTS] = 2;  // slot 0 = s0, slot 1 = scratch
+    c.counters[CNT_ERR] = 0;
+    c.counters[CNT_R] = 0;
+    c.node_word[0] = -1;
+    c.node_parent[0] = -1;
+    c.node_src[0] = 0;
+    c.node_slot[0] = -1;
+  }
+}
+void ctx_reset(const CtxDev& c, int64_t hcap, cudaStream_t st) {
+  const int64_t b = std::min<int64_t>((hcap + 255) / 256, 4 * kNumSMs);
+  launch_pdl(k_ctx_reset, (unsigned)std::max<int64_t>(b, 1), 256, 0, st, c, hcap);
+  CK_LAUNCH();
+}
+
 // inject parentless nodes with their own input slots (synthetic parents for bench/tests); the last
 // block to finish publishes the new node/slot counts (every block has read them by then)
 __global__ void k_inject(CtxDev c, int n, const float* s, const int* y, int* out_ids, int* done) {
@@ -896,49 +922,89 @@ void full_row(const float* T, const float* Wo32, const float* bo, const float* l
 
 // ===================================================================================== encoder
 // E1-E6 in one persistent cooperative kernel.  CTAs [0, NB) run the forward direction,
-// [NB, 2NB) the backward one (both fill the 148 SMs).  Each CTA owns UPC hidden units; the
-// 3*UPC columns of [U | Ux] it needs live in REGISTERS for the whole sentence (warp w owns
-// columns w, w+12, w+24, w+36; lane l holds the float4s k = l + 32 i of each), so a time step
-// reads no weights at all.  The input projections x_j.[W|Wx] + [b|bx] are rows of a table
-// precomputed per source word at load (E1+E2 become a gather).  h_t is exchanged through global
-// memory as 64-bit (value, tag = t+1) words: a reader polls until every word carries the tag of
-// the step it needs, which merges the grid-wide barrier into the data read (one L2 round trip
-// per step).  Double-buffered by parity: a writer is at most one step ahead of the slowest reader.
+// [NB, 2NB) the backward one (both fill the 148 SMs).  Each CTA owns UPC hidden units, one WARP
+// per unit: the warp keeps the unit's three columns of [U | Ux] (r, u and candidate gates) in
+// REGISTERS for the whole sentence (lane l holds the float4s k = l + 32 i of each), so a time step
+// reads no weights at all, and the warp's butterfly reduction leaves the three dot products in
+// every lane, which evaluates the GRU update itself (no shared-memory hop, one barrier per step).
+// The dot products use packed FFMA2.  The input projections x_j.[W|Wx] + [b|bx] are rows of a
+// table precomputed per source word at load (E1+E2 become a gather, fetched one step ahead).
+// h_t is exchanged through global memory as 64-bit (value, tag = epoch:t+1) words: a reader polls until
+// every word carries the tag of the step it needs, which merges the grid-wide barrier into the
+// data read (one L2 round trip per step).  Double-buffered by parity: a writer is at most one step
+// ahead of the slowest reader.  The 16-bit encode epoch in the tag (and a barrier counter that only
+// grows) means no buffer is reset between calls.
 // Tail (E5): each CTA publishes the time-mean of its units, one grid barrier, then the CTAs split
-// s0 = tanh(mean . W_init + b_init) and write the bf16 hi|lo copy of ctx for the pctx GEMM (E7).
-constexpr int kRecurThreads = 384, kRecurWarps = 12, kRecurCPW = 4;
+// s0 = tanh(mean . W_init + b_init); their W_init rows are prefetched into shared memory at start.
+// The kernel also writes the bf16 hi|lo copy of ctx (E7 input) and the new context's counters.
+__device__ __forceinline__ void ffma2(float2& acc, float2 a, float2 b) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&acc)));
+  acc = *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float sigmoid_fast(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+__device__ __forceinline__ float tanh_fast(float x) {  // |err| ~ 1e-7 (not tanh.approx)
+  const float e = __expf(2.f * fminf(fmaxf(x, -15.f), 15.f));
+  return 1.f - __fdividef(2.f, e + 1.f);
+}
 template <int KI>  // Hp = 128 * KI
-__global__ void __launch_bounds__(kRecurThreads, 1) k_enc_recur(EncDev e, int Tx) {
+__global__ void __launch_bounds__(512, 1) k_enc_recur(EncDev e, int Tx) {
   pdl_wait();  // (no early trigger: the cooperative grid must not lose SMs to dependents)
   constexpr int Hp = 128 * KI, H4 = Hp / 4;
-  __shared__ float4 h4[H4];
-  __shared__ float dots[3 * 16];
+  __shared__ float4 h4buf[2][H4];  // by step parity: a warp reading step t never races the poll of t+1
   const int NB = e.NB, UPC = e.UPC, H = e.H;
+  const int nthr = blockDim.x;
   const int dir = blockIdx.x / NB, cb = blockIdx.x % NB;
-  const int u0 = cb * UPC;
-  const int ncol = 3 * UPC;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float4 w[kRecurCPW][KI];
+  const int jj = cb * UPC + warp;  // this warp's hidden unit
+  const bool unit = jj < H;
+  long long* tr = (e.trace && blockIdx.x == 0 && threadIdx.x == 0) ? e.trace : nullptr;
+  if (tr) {
+    tr[Tx * 8 + 0] = clock64();
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    tr[Tx * 8 + 5] = (long long)g;
+  }
+  const int C = 2 * H;
+  const int per = (H + gridDim.x - 1) / gridDim.x;  // s0 outputs of this CTA (tail)
+  extern __shared__ __align__(16) float wsm[];       // [per][C] rows of W_init^T (tail)
+  __shared__ __align__(8) uint64_t wbar;  // completion of their bulk copy
+  const int o_first = blockIdx.x * per, n_out = max(0, min(per, H - o_first));
+  const bool bulk = (C % 4) == 0;  // 16-byte rows: one bulk copy per row, in flight during the loop
+  if (bulk && threadIdx.x == 0) {
+    mbar_init(&wbar, 1);
+    fence_barrier_init();
+    mbar_arrive_expect_tx(&wbar, (uint32_t)(n_out * C * 4));
+    for (int r = 0; r < n_out; ++r)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(wsm + r * C)), "l"(e.W_initT + (int64_t)(o_first + r) * C), "r"(C * 4),
+                   "r"(smem_u32(&wbar)) : "memory");
+  }
+  float4 wr[KI], wu[KI], wx[KI];
   {
-    const float4* src = reinterpret_cast<const float4*>(e.Uarr) + (size_t)(dir * NB + cb) * ncol * H4;
+    const float4* src = reinterpret_cast<const float4*>(e.Uarr) + (size_t)(dir * NB + cb) * 3 * UPC * H4;
 #pragma unroll
-    for (int q = 0; q < kRecurCPW; ++q) {
-      const int c = warp + q * kRecurWarps;
-#pragma unroll
-      for (int i = 0; i < KI; ++i)
-        w[q][i] = c < ncol ? src[(size_t)c * H4 + lane + 32 * i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = 0; i < KI; ++i) {
+      wr[i] = src[(size_t)warp * H4 + lane + 32 * i];
+      wu[i] = src[(size_t)(UPC + warp) * H4 + lane + 32 * i];
+      wx[i] = src[(size_t)(2 * UPC + warp) * H4 + lane + 32 * i];
     }
   }
+  if (!bulk)
+    for (int i = threadIdx.x; i < n_out * C; i += nthr) wsm[i] = __ldg(e.W_initT + (int64_t)o_first * C + i);
   unsigned long long* hx = e.hx + (size_t)dir * 2 * Hp;  // [2][Hp] tagged words of this direction
-  const bool gate = threadIdx.x < UPC && u0 + (int)threadIdx.x < H;
-  const int jj = u0 + threadIdx.x;
+  const unsigned ep = e.epoch << 16;
+  bool bad = false;
   float hself = 0.f, hsum = 0.f;
   // input projections (independent of h) are fetched one step ahead: the table rows live in HBM
-  auto fetch_pin = [&](int t, float& r_, float& u_, float& x_) {
-    const int j = dir == 0 ? t : Tx - 1 - t;
-    int id = e.src[j];
+  // and the source id one step before that, so no dependent load sits on the step's critical path
+  auto load_id = [&](int t) { return t < Tx ? __ldg(e.src + (dir == 0 ? t : Tx - 1 - t)) : 0; };
+  auto fetch_pin = [&](int id, float& r_, float& u_, float& x_) {
     if (id < 0 || id >= e.Vs) {  // device-resident ids are validated here (nmt_ctx_check)
-      atomicOr(e.err, ERR_TOKEN);
+      bad = true;
       id = 0;
     }
     const float* pin = e.encin + (int64_t)id * 6 * Hp + dir * 3 * Hp;
@@ -947,76 +1013,107 @@ __global__ void __launch_bounds__(kRecurThreads, 1) k_enc_recur(EncDev e, int Tx
     x_ = __ldg(pin + 2 * Hp + jj);
   };
   float n_r = 0.f, n_u = 0.f, n_x = 0.f;
-  if (gate) fetch_pin(0, n_r, n_u, n_x);
+  int id_next = load_id(1);
+  if (unit) fetch_pin(load_id(0), n_r, n_u, n_x);
+  if (tr) {
+    // (weights are in registers once used: force completion for the stamp with a dependent read)
+    tr[Tx * 8 + 1] = clock64() + (long long)(wr[KI - 1].w == 12345.f) + (long long)(wx[0].x == 12345.f);
+  }
+  int npolls = 0;
   for (int t = 0; t < Tx; ++t) {
+    if (tr) tr[t * 8 + 0] = clock64();
     const int j = dir == 0 ? t : Tx - 1 - t;
     const float p_r = n_r, p_u = n_u, p_x = n_x;
-    if (gate && t + 1 < Tx) fetch_pin(t + 1, n_r, n_u, n_x);
-    if (t == 0) {
-      for (int k = threadIdx.x; k < H4; k += kRecurThreads) h4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    } else {
+    if (unit && t + 1 < Tx) fetch_pin(id_next, n_r, n_u, n_x);
+    id_next = load_id(t + 2);
+    if (tr) tr[t * 8 + 1] = clock64();
+    float2 ar0 = make_float2(0.f, 0.f), au0 = ar0, ax0 = ar0, ar1 = ar0, au1 = ar0, ax1 = ar0;
+    if (t > 0) {
       const unsigned long long* src = hx + (size_t)(t & 1) * Hp;
-      const unsigned tag = (unsigned)t;  // h_{t-1} was written with tag (t-1)+1
-      for (int k = threadIdx.x; k < H4; k += kRecurThreads) {
-        if (4 * k >= H) {  // padded units (H < Hp) are never written: they stay 0
-          h4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-          continue;
+      const unsigned tag = ep | (unsigned)t;  // h_{t-1} was written with tag (t-1)+1
+      float4* h4 = h4buf[t & 1];
+      const int npoll = (e.poll & 2) ? 64 : nthr;  // threads that poll
+      if ((int)threadIdx.x < npoll) {
+        for (int k = threadIdx.x; k < H4; k += npoll) {
+          if (4 * k >= H) {  // padded units (H < Hp) are never written: they stay 0
+            h4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            continue;
+          }
+          // units >= H inside this float4 carry no tag: accept them as 0
+          const unsigned need = (4 * k + 3 < H) ? 0xFu : ((1u << (H - 4 * k)) - 1u);
+          unsigned long long a, b, c, d;
+          const long long t0 = clock64();
+          while (true) {  // one 256-bit load: 4 tagged words
+            asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                         : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(src + 4 * k) : "memory");
+            const unsigned ok = ((unsigned)(a >> 32) == tag) | (((unsigned)(b >> 32) == tag) << 1) |
+                                (((unsigned)(c >> 32) == tag) << 2) | (((unsigned)(d >> 32) == tag) << 3);
+            ++npolls;
+            if ((ok & need) == need || (e.poll & 4)) break;  // (4: timing only, no wait)
+            if (e.poll & 1) __nanosleep(64);
+            if (clock64() - t0 > (1ll << 32)) asm volatile("trap;");  // watchdog (~2 s): fail, never hang
+          }
+          h4[k] = make_float4((need & 1) ? __uint_as_float((unsigned)a) : 0.f, (need & 2) ? __uint_as_float((unsigned)b) : 0.f,
+                              (need & 4) ? __uint_as_float((unsigned)c) : 0.f, (need & 8) ? __uint_as_float((unsigned)d) : 0.f);
         }
-        // units >= H inside this float4 carry no tag: accept them as 0
-        const unsigned need = (4 * k + 3 < H) ? 0xFu : ((1u << (H - 4 * k)) - 1u);
-        unsigned long long a, b, c, d;
-        const long long t0 = clock64();
-        while (true) {
-          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(src + 4 * k) : "memory");
-          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(c), "=l"(d) : "l"(src + 4 * k + 2) : "memory");
-          const unsigned ok = ((unsigned)(a >> 32) == tag) | (((unsigned)(b >> 32) == tag) << 1) |
-                              (((unsigned)(c >> 32) == tag) << 2) | (((unsigned)(d >> 32) == tag) << 3);
-          if ((ok & need) == need) break;
-          if (clock64() - t0 > (1ll << 32)) asm volatile("trap;");  // watchdog (~2 s): fail, never hang
+      }
+      if (tr) tr[t * 8 + 2] = clock64();
+      __syncthreads();  // (the only barrier of a step: buffer t&1 is rewritten at t+2, after t+1's barrier)
+      if (tr) tr[t * 8 + 3] = clock64();
+#pragma unroll
+      for (int i = 0; i < KI; ++i) {
+        const float4 h = h4[lane + 32 * i];
+        const float2 hlo = make_float2(h.x, h.y), hhi = make_float2(h.z, h.w);
+        if (i & 1) {
+          ffma2(ar1, make_float2(wr[i].x, wr[i].y), hlo); ffma2(ar1, make_float2(wr[i].z, wr[i].w), hhi);
+          ffma2(au1, make_float2(wu[i].x, wu[i].y), hlo); ffma2(au1, make_float2(wu[i].z, wu[i].w), hhi);
+          ffma2(ax1, make_float2(wx[i].x, wx[i].y), hlo); ffma2(ax1, make_float2(wx[i].z, wx[i].w), hhi);
+        } else {
+          ffma2(ar0, make_float2(wr[i].x, wr[i].y), hlo); ffma2(ar0, make_float2(wr[i].z, wr[i].w), hhi);
+          ffma2(au0, make_float2(wu[i].x, wu[i].y), hlo); ffma2(au0, make_float2(wu[i].z, wu[i].w), hhi);
+          ffma2(ax0, make_float2(wx[i].x, wx[i].y), hlo); ffma2(ax0, make_float2(wx[i].z, wx[i].w), hhi);
         }
-        h4[k] = make_float4((need & 1) ? __uint_as_float((unsigned)a) : 0.f, (need & 2) ? __uint_as_float((unsigned)b) : 0.f,
-                            (need & 4) ? __uint_as_float((unsigned)c) : 0.f, (need & 8) ? __uint_as_float((unsigned)d) : 0.f);
       }
     }
-    __syncthreads();
-    float acc[kRecurCPW];
+    // (h_0 = 0: the dot products are 0 at t = 0)
+    float dr = (ar0.x + ar0.y) + (ar1.x + ar1.y);
+    float du = (au0.x + au0.y) + (au1.x + au1.y);
+    float dx = (ax0.x + ax0.y) + (ax1.x + ax1.y);
 #pragma unroll
-    for (int q = 0; q < kRecurCPW; ++q) acc[q] = 0.f;
-#pragma unroll
-    for (int i = 0; i < KI; ++i) {
-      const float4 h = h4[lane + 32 * i];
-#pragma unroll
-      for (int q = 0; q < kRecurCPW; ++q)
-        acc[q] = fmaf(w[q][i].x, h.x, fmaf(w[q][i].y, h.y, fmaf(w[q][i].z, h.z, fmaf(w[q][i].w, h.w, acc[q]))));
+    for (int o = 16; o > 0; o >>= 1) {  // butterfly: every lane ends with the same sums
+      dr += __shfl_xor_sync(0xffffffffu, dr, o);
+      du += __shfl_xor_sync(0xffffffffu, du, o);
+      dx += __shfl_xor_sync(0xffffffffu, dx, o);
     }
-#pragma unroll
-    for (int q = 0; q < kRecurCPW; ++q) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
-      const int c = warp + q * kRecurWarps;
-      if (lane == 0 && c < ncol) dots[c] = acc[q];
-    }
-    __syncthreads();
-    if (gate) {
-      const int u = threadIdx.x;
-      const float rg = 1.f / (1.f + expf(-(p_r + dots[u])));
-      const float ug = 1.f / (1.f + expf(-(p_u + dots[UPC + u])));
-      const float ht = tanhf(rg * dots[2 * UPC + u] + p_x);
+    if (tr) tr[t * 8 + 4] = clock64();
+    if (unit) {
+      const float rg = sigmoid_fast(p_r + dr);
+      const float ug = sigmoid_fast(p_u + du);
+      const float ht = tanh_fast(rg * dx + p_x);
       hself = ug * hself + (1.f - ug) * ht;
       hsum += hself;
-      const unsigned long long word = ((unsigned long long)(unsigned)(t + 1) << 32) | __float_as_uint(hself);
-      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(hx + (size_t)((t + 1) & 1) * Hp + jj), "l"(word)
-                   : "memory");
       const int cidx = dir * Hp + jj;  // padded context column
-      e.ctx[(int64_t)j * 2 * Hp + cidx] = hself;
-      __nv_bfloat16 hi, lo;
-      split_bf16(hself, hi, lo);
-      e.ctxbf[(int64_t)j * 4 * Hp + cidx] = hi;
-      e.ctxbf[(int64_t)j * 4 * Hp + 2 * Hp + cidx] = lo;
+      if (lane == 0) {
+        const unsigned long long word = ((unsigned long long)(ep | (unsigned)(t + 1)) << 32) | __float_as_uint(hself);
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(hx + (size_t)((t + 1) & 1) * Hp + jj), "l"(word)
+                     : "memory");
+      } else if (lane == 1) {
+        e.ctx[(int64_t)j * 2 * Hp + cidx] = hself;
+      } else if (lane == 2) {
+        __nv_bfloat16 hi, lo;
+        split_bf16(hself, hi, lo);
+        e.ctxbf[(int64_t)j * 4 * Hp + cidx] = hi;
+        e.ctxbf[(int64_t)j * 4 * Hp + 2 * Hp + cidx] = lo;
+      }
+    }
+    if (tr) {
+      tr[t * 8 + 5] = clock64();
+      tr[t * 8 + 6] = npolls;
     }
   }
   // ---- E5: time means -> grid barrier -> s0 slices
-  if (gate) e.mean[dir * H + jj] = hsum / (float)Tx;
+  if (tr) tr[Tx * 8 + 2] = clock64();
+  if (unit && lane == 0) e.mean[dir * H + jj] = hsum / (float)Tx;
   __syncthreads();
   if (threadIdx.x == 0) {
     asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(e.bar) : "memory");
@@ -1025,40 +1122,41 @@ __global__ void __launch_bounds__(kRecurThreads, 1) k_enc_recur(EncDev e, int Tx
     do {
       asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(e.bar) : "memory");
       if (clock64() - t0 > (1ll << 32)) asm volatile("trap;");
-    } while (v < (int)gridDim.x);
+    } while (v < (int)(e.epoch * gridDim.x));
   }
   __syncthreads();
-  const int C = 2 * H;
-  float* msm = reinterpret_cast<float*>(h4);  // reuse the h buffer (2H <= 2Hp... staged in two halves)
-  const int per = (H + gridDim.x - 1) / gridDim.x;
-  float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-  const int o = blockIdx.x * per + warp;  // warp per output; W_initT rows are contiguous
-  for (int half = 0; half < 2; ++half) {
-    const int k0 = half * Hp;
-    const int kn = min(Hp, C - k0);
-    for (int k = threadIdx.x; k < Hp; k += kRecurThreads) msm[k] = k < kn ? __ldcg(e.mean + k0 + k) : 0.f;
-    __syncthreads();
-    if (warp < per && o < H) {
-      const float* wr = e.W_initT + (int64_t)o * C + k0;
-      for (int k = 4 * lane; k < kn; k += 128) {  // kn is a multiple of 4 except in tiny models
-        if (k + 3 < kn) {
-          const float4 wv = *reinterpret_cast<const float4*>(wr + k);
-          acc0 = fmaf(msm[k], wv.x, acc0);
-          acc1 = fmaf(msm[k + 1], wv.y, acc1);
-          acc2 = fmaf(msm[k + 2], wv.z, acc2);
-          acc3 = fmaf(msm[k + 3], wv.w, acc3);
-        } else {
-          for (int kk = k; kk < kn; ++kk) acc0 = fmaf(msm[kk], wr[kk], acc0);
-        }
+  if (tr) tr[Tx * 8 + 3] = clock64();
+  if (bad && lane == 0) atomicOr(e.err, ERR_TOKEN);
+  // all 2H means at once (C <= 2Hp floats = the two h buffers), then a warp per s0 output
+  float* msm = reinterpret_cast<float*>(h4buf);
+  for (int k = threadIdx.x; k < C; k += nthr) msm[k] = __ldcg(e.mean + k);
+  __syncthreads();
+  if (warp < n_out) {
+    if (bulk) mbar_wait(&wbar, 0);
+    const int o = o_first + warp;
+    const float* wrow = wsm + warp * C;
+    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+    if (bulk) {
+      for (int k = 4 * lane; k < C; k += 128) {
+        const float4 mv = *reinterpret_cast<const float4*>(msm + k), wv = *reinterpret_cast<const float4*>(wrow + k);
+        acc0 = fmaf(mv.x, wv.x, acc0);
+        acc1 = fmaf(mv.y, wv.y, acc1);
+        acc2 = fmaf(mv.z, wv.z, acc2);
+        acc3 = fmaf(mv.w, wv.w, acc3);
       }
+    } else {
+      for (int k = lane; k < C; k += 32) acc0 = fmaf(msm[k], wrow[k], acc0);
     }
-    __syncthreads();
-  }
-  if (warp < per && o < H) {
-    float s = (acc0 + acc1) + (acc2 + acc3);
+    float sacc = (acc0 + acc1) + (acc2 + acc3);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) e.S0[o] = tanhf(s + e.b_init[o]);
+    for (int off = 16; off > 0; off >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, off);
+    if (lane == 0) e.S0[o] = tanhf(sacc + e.b_init[o]);
+  }
+  if (tr) {
+    tr[Tx * 8 + 4] = clock64();
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    tr[Tx * 8 + 6] = (long long)g;
   }
 }
 
@@ -1066,14 +1164,18 @@ template <int KI>
 static void launch_recur(const EncDev& e, int Tx, cudaStream_t st) {
   EncDev ee = e;
   void* args[] = {&ee, &Tx};
-  CK(cudaLaunchCooperativeKernel((void*)k_enc_recur<KI>, dim3(2 * e.NB), dim3(kRecurThreads), args, 0, st));
+  const size_t smem = (size_t)((e.H + 2 * e.NB - 1) / (2 * e.NB)) * 2 * e.H * sizeof(float);
+  static size_t attr = 0;  // > 48 KB of dynamic shared memory needs the opt-in
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_enc_recur<KI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  CK(cudaLaunchCooperativeKernel((void*)k_enc_recur<KI>, dim3(2 * e.NB), dim3(32 * e.UPC), args, smem, st));
   note_launch();
 }
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
-  if (3 * e.UPC > kRecurWarps * kRecurCPW || 3 * e.UPC > 48) throw NmtError(NMT_ERR_SHAPE, "encoder: UPC too large");
-  // tags of both directions and parities start at 0 (never a valid tag); the tail barrier at 0
-  CK(cudaMemsetAsync(e.hx, 0, (size_t)2 * 2 * e.Hp * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(e.bar, 0, sizeof(int), st));
+  if (e.UPC > 16) throw NmtError(NMT_ERR_SHAPE, "encoder: UPC too large");
+  // (the caller resets the tags and the barrier counter when the 16-bit epoch wraps)
   switch (e.Hp / 128) {
     case 1: launch_recur<1>(e, Tx, st); break;
     case 2: launch_recur<2>(e, Tx, st); break;

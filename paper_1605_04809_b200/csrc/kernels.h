@@ -78,6 +78,9 @@ struct AttnCtx {
 
 struct EncDev {
   int H, Hp, NB, UPC, Vs;
+  int poll;              // h-exchange polling variant (diagnostic: NMT_ENC_POLL)
+  unsigned epoch;        // 1..65535, per encode: tags and the tail barrier need no reset between calls
+  long long* trace;      // diagnostic (NMT_ENC_TRACE): [Tx][8] clock64 phase stamps of CTA 0, thread 0
   const float* Uarr;     // [2][NB][3*UPC][Hp] recurrent weights per CTA (rows zero-padded to Hp)
   const int* src;        // [Tx] source ids (device)
   const float* encin;    // [Vs][6Hp] precomputed x.[W|Wx] + [b|bx] of both directions per source word
@@ -100,6 +103,7 @@ void pack_rows(const float* src, int ld_src, int rows, int K, __nv_bfloat16* dst
                cudaStream_t st);
 void to_panels(const __nv_bfloat16* src, int rows, int cols, __nv_bfloat16* dst, cudaStream_t st);
 void transpose_f32(const float* src, int K, int N, float* dst, int ld_dst, cudaStream_t st);
+void ctx_reset(const CtxDev& c, int64_t hcap, cudaStream_t st);
 void fill_i32(int* p, int64_t n, int v, cudaStream_t st);
 void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st);
 void rehash(const unsigned long long* okeys, const int* ovals, int64_t ocap, unsigned long long* nkeys, int* nvals,
