@@ -1,3 +1,4 @@
+#include <climits>
 // api.cu - host runtime behind the C ABI of include/nmt.h: params loading + device re-layout,
 // per-context arenas, the orchestration of the encoder and of one batched decoder step.
 //
@@ -41,6 +42,21 @@ enum Stage {
   ST_INJECT, ST_N
 };
 static_assert(ST_N == NMT_N_STAGES, "stage table");
+// diagnostic only: NMT_SKIP = comma-separated stage indices whose (numeric) kernels are not launched,
+// to measure a stage's in-situ cost with the rest of the step (and its PDL overlap) intact
+static bool stage_skipped(int st) {
+  static const unsigned mask = [] {
+    unsigned mk = 0;
+    if (const char* e = getenv("NMT_SKIP"))
+      for (const char* p = e; *p;) {
+        mk |= 1u << atoi(p);
+        while (*p && *p != ',') ++p;
+        if (*p == ',') ++p;
+      }
+    return mk;
+  }();
+  return (mask >> st) & 1u;
+}
 
 namespace nmt {
 nmt_status set_error(nmt_status c, const std::string& m) {
@@ -137,6 +153,7 @@ struct nmt_model {
   CUtensorMap tm_ctxbf;
   // step workspace
   int R_cap = 0, NC_cap = 0;
+  int P_rows = 0;  // rows of G1 / Q / G2 / RO_buf: room for the split-K partials of a step
   __nv_bfloat16 *A_s = nullptr, *X = nullptr, *A_t = nullptr;
   float *G1 = nullptr, *S1 = nullptr, *Q = nullptr, *Cf = nullptr, *G2 = nullptr, *RO_buf = nullptr, *alpha = nullptr;
   float4* part = nullptr;
@@ -273,14 +290,15 @@ void nmt_model::ensure_ws(int R, int NC) {
   R_cap = nR;
   NC_cap = nNC;
   A_s = dalloc<__nv_bfloat16>((size_t)R_cap * sf * Hp);
-  G1 = dalloc<float>((size_t)R_cap * 3 * Hp);
+  P_rows = round_up(std::max(R_cap, 4096), 256);  // split-K partial rows (small batches split K up to 4 ways)
+  G1 = dalloc<float>((size_t)P_rows * 3 * Hp);
   S1 = dalloc<float>((size_t)R_cap * Hp);
   X = dalloc<__nv_bfloat16>((size_t)R_cap * sf * 4 * Hp);
-  Q = dalloc<float>((size_t)R_cap * Cp);
+  Q = dalloc<float>((size_t)P_rows * Cp);
   Cf = dalloc<float>((size_t)R_cap * Cp);
   alpha = dalloc<float>((size_t)R_cap * maxTx);
-  G2 = dalloc<float>((size_t)R_cap * 4 * Hp);
-  RO_buf = dalloc<float>((size_t)R_cap * ROp);
+  G2 = dalloc<float>((size_t)P_rows * 4 * Hp);
+  RO_buf = dalloc<float>((size_t)P_rows * ROp);
   A_t = dalloc<__nv_bfloat16>((size_t)R_cap * sf * Ep);
   part = dalloc<float4>((size_t)R_cap * 2 * kNumSMs);  // <= 2 x (CTAs per m-tile) partials per row
   lse_cpm = dalloc<int>(1);
@@ -727,7 +745,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   // ---- encoder workspace
   m->Tpad = round_up(m->maxTx, 128);
   m->ctxbf = dalloc<__nv_bfloat16>((size_t)m->Tpad * 4 * Hp);
-  m->hbuf = dalloc<float>(8 * Hp);  // [2 dirs][2][Hp] 64-bit tagged words
+  m->hbuf = dalloc<float>(2 * 2 * 131072);  // [2 dirs][stride >= 2Hp] 64-bit tagged words (1 MB)
   m->enc_mean = dalloc<float>(2 * H);
   m->ksplit_buf = dalloc<float>((size_t)8 * m->Tpad * Cp);
   m->bar = dalloc<int>(2);
@@ -876,50 +894,121 @@ static StepDev step_view(nmt_model* m, nmt_ctx* c) {
   return d;
 }
 
-// fp32-output GEMM: CTA pairs with 256 x 256 tiles when N and the region boundaries are multiples of
-// 256, else single-CTA 128 x 128 tiles.  `b128` = weight tensor map with a 128-row box.
-static void gemm_auto(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b128, const GemmShape& g, float* out,
-                      int ldc, int out_rows, const float* bias, int M_max, cudaStream_t st) {
+// Per-region split-K factors (<= max_ks) for a decoder GEMM at M_max rows on `units` parallel units
+// with CM x BN tiles.  At the bench batch (R = 1024) the plain tile count leaves most SMs idle (e.g.
+// the readout GEMM has 16 CTA-pair tiles of 48 k-blocks); splitting K evens the work per unit.
+// Cost model: waves x k-blocks of the largest item; regions get the split that brings their items
+// closest to a common chunk.  The partial sums are added by the kernel that consumes the output.
+static void pick_splits(GemmShape& g, int M_max, int CM, int BN, int units, int max_ks) {
+  const int num_m = (M_max + CM - 1) / CM;
+  int nt[4], nkb[4], maxnkb = 1;
+  for (int r = 0, n0 = 0; r < g.nreg; ++r) {
+    const int n1 = r < g.nreg - 1 ? g.reg_n_end[r] : g.N;
+    nt[r] = (n1 - n0) / BN;
+    nkb[r] = g.passes * (g.reg_k1[r] - g.reg_k0[r]) / 64;
+    maxnkb = std::max(maxnkb, nkb[r]);
+    n0 = n1;
+  }
+  long best_cost = LONG_MAX, best_items = LONG_MAX;
+  int best[4] = {1, 1, 1, 1};
+  for (int c = maxnkb; c >= 1; --c) {  // target k-blocks per item
+    int ks[4];
+    long items = 0;
+    int chunk_max = 1;
+    for (int r = 0; r < g.nreg; ++r) {
+      int k = std::min(max_ks, (nkb[r] + c - 1) / c);
+      while (k > 1 && (k - 1) * ((nkb[r] + k - 1) / k) >= nkb[r]) --k;  // no empty split
+      ks[r] = std::max(1, k);
+      items += (long)num_m * nt[r] * ks[r];
+      chunk_max = std::max(chunk_max, (nkb[r] + ks[r] - 1) / ks[r]);
+    }
+    const long cost = ((items + units - 1) / units) * chunk_max;
+    if (cost < best_cost || (cost == best_cost && items < best_items)) {
+      best_cost = cost;
+      best_items = items;
+      std::copy(ks, ks + g.nreg, best);
+    }
+  }
+  int kmax = 1;
+  for (int r = 0; r < g.nreg; ++r) {
+    g.reg_ks[r] = best[r];
+    kmax = std::max(kmax, best[r]);
+  }
+  g.ksplit = kmax;
+}
+
+// fp32-output decoder GEMM: CTA pairs with 256 x 256 tiles when N and the region boundaries are
+// multiples of 256, else single-CTA 128 x 128 tiles.  `b128` = weight tensor map with a 128-row box.
+// Split-K partial s is written at rows [s * rps, (s + 1) * rps) of `out` (rps = rows per split;
+// out has m->P_rows rows); the chosen per-region factors are left in g.reg_ks.
+static void gemm_auto(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b128, GemmShape& g, float* out,
+                      int ldc, int rps, int M_max, cudaStream_t st) {
   bool aligned = g.N % 256 == 0;
   for (int r = 0; r < g.nreg - 1; ++r) aligned = aligned && g.reg_n_end[r] % 256 == 0;
-  if (m->use_pair && aligned) gemm_store_pair(a, b128, g, out, ldc, out_rows, bias, M_max, st);
-  else gemm_store(a, b128, g, out, ldc, out_rows, bias, M_max, st);
+  const bool pair = m->use_pair && aligned;
+  static const int ks_cap = getenv("NMT_MAX_KS") ? std::max(1, atoi(getenv("NMT_MAX_KS"))) : 4;  // (diagnostic)
+  const int max_ks = std::max(1, std::min(ks_cap, m->P_rows / rps));
+  if (pair) pick_splits(g, M_max, 256, 256, kNumSMs / 2, max_ks);
+  else pick_splits(g, M_max, 128, 128, kNumSMs, max_ks);
+  const size_t stride = (size_t)rps * ldc;
+  if (pair) gemm_store_pair(a, b128, g, out, ldc, m->P_rows, nullptr, M_max, st, stride);
+  else gemm_store(a, b128, g, out, ldc, m->P_rows, nullptr, M_max, st, stride);
 }
 
 // one decoder forward step over the rows planned in m->row_* (count at c->counters[CNT_R])
 static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
   cudaStream_t st = m->st;
-  const StepDev d = step_view(m, c);
+  StepDev d = step_view(m, c);
   AttnCtx a{c->pctx, c->ctx, m->U_att, m->c_tt, c->Tx};
   const int* Rd = d.R;
   const int Hp = m->Hp, Cp = m->Cp, Ep = m->Ep;
   const bool sp = m->split;
+  const int rps = round_up(std::max(R_max, 1), 256);  // rows per split-K partial
   { ProfScope p_(m, ST_GATHER); step_elementwise(EW_GATHER, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  { ProfScope p_(m, ST_GEMM_H1); gemm_auto(m, m->tm_As, m->tm_Wh1, gemm_shape(0, Rd, 3 * Hp, Hp, 0, sp, Hp, Hp), m->G1, 3 * Hp, m->R_cap, nullptr, R_max, st); }
-  { ProfScope p_(m, ST_GRU1); step_elementwise(EW_GRU1, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  { ProfScope p_(m, ST_GEMM_Q); gemm_auto(m, m->tm_X, m->tm_Wq, gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp), m->Q, Cp, m->R_cap, nullptr, R_max, st); }
-  { ProfScope p_(m, ST_ATTN); step_elementwise(EW_ATTN, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  {
+  if (!stage_skipped(ST_GEMM_H1)) {
+    ProfScope p_(m, ST_GEMM_H1);
+    GemmShape g = gemm_shape(0, Rd, 3 * Hp, Hp, 0, sp, Hp, Hp);
+    gemm_auto(m, m->tm_As, m->tm_Wh1, g, m->G1, 3 * Hp, rps, R_max, st);
+    d.ks_g1 = g.reg_ks[0];
+    d.ps_g1 = (int64_t)rps * 3 * Hp;
+  }
+  if (!stage_skipped(ST_GRU1)) { ProfScope p_(m, ST_GRU1); step_elementwise(EW_GRU1, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
+  if (!stage_skipped(ST_GEMM_Q)) {
+    ProfScope p_(m, ST_GEMM_Q);
+    GemmShape g = gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp);
+    gemm_auto(m, m->tm_X, m->tm_Wq, g, m->Q, Cp, rps, R_max, st);
+    d.ks_q = g.reg_ks[0];
+    d.ps_q = (int64_t)rps * Cp;
+  }
+  if (!stage_skipped(ST_ATTN)) { ProfScope p_(m, ST_ATTN); step_elementwise(EW_ATTN, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
+  if (!stage_skipped(ST_GEMM_G2)) {
     ProfScope p_(m, ST_GEMM_G2);
     GemmShape g = gemm_shape(0, Rd, 4 * Hp, Hp + Cp, 0, sp, 4 * Hp, Hp + Cp);
     g.nreg = 3;
     g.reg_n_end[0] = 2 * Hp, g.reg_k0[0] = 0, g.reg_k1[0] = Hp + Cp;  // gates: s1 U_nl + c Wc
     g.reg_n_end[1] = 3 * Hp, g.reg_k0[1] = 0, g.reg_k1[1] = Hp;       // s1 Ux_nl
     g.reg_n_end[2] = 4 * Hp, g.reg_k0[2] = Hp, g.reg_k1[2] = Hp + Cp; // c Wcx
-    gemm_auto(m, m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, m->R_cap, nullptr, R_max, st);
+    gemm_auto(m, m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, rps, R_max, st);
+    for (int r = 0; r < 3; ++r) d.ks_g2[r] = g.reg_ks[r];
+    d.ps_g2 = (int64_t)rps * 4 * Hp;
   }
-  { ProfScope p_(m, ST_GRU2); step_elementwise(EW_GRU2, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  { ProfScope p_(m, ST_GEMM_RO); gemm_auto(m, m->tm_X, m->tm_Wro, gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp), m->RO_buf, m->ROp,
-             m->R_cap, nullptr, R_max, st); }
-  { ProfScope p_(m, ST_READOUT); step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  {
+  if (!stage_skipped(ST_GRU2)) { ProfScope p_(m, ST_GRU2); step_elementwise(EW_GRU2, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
+  if (!stage_skipped(ST_GEMM_RO)) {
+    ProfScope p_(m, ST_GEMM_RO);
+    GemmShape g = gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp);
+    gemm_auto(m, m->tm_X, m->tm_Wro, g, m->RO_buf, m->ROp, rps, R_max, st);
+    d.ks_ro = g.reg_ks[0];
+    d.ps_ro = (int64_t)rps * m->ROp;
+  }
+  if (!stage_skipped(ST_READOUT)) { ProfScope p_(m, ST_READOUT); step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
+  if (!stage_skipped(ST_VOCAB)) {
     ProfScope p_(m, ST_VOCAB);
     GemmShape g = gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep);
     g.b_panel_rows = m->Vp;
     if (m->use_pair) gemm_lse_pair(m->tm_At, m->tm_Wo128, g, m->part, m->V, st, m->lse_cpm);
     else gemm_lse(m->tm_At, m->tm_Wo, g, m->part, m->V, R_max, st, m->lse_cpm);
   }
-  { ProfScope p_(m, ST_FINALIZE); step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
+  if (!stage_skipped(ST_FINALIZE)) { ProfScope p_(m, ST_FINALIZE); step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
 }
 
 static PlanIO plan_io(nmt_model* m, int np, int nc, const int* par, const int* off, const int* words) {
@@ -1071,18 +1160,26 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
     e.b_init = m->b_init;
     e.S0 = c->S;
     ProfScope p_(m, ST_ENC_RECUR);
-    { const char* pm = getenv("NMT_ENC_POLL"); e.poll = pm ? atoi(pm) : 0; }
     if (++m->enc_epoch > 65535) {  // tags carry a 16-bit epoch: reset them before it repeats
-      CK(cudaMemsetAsync(m->hbuf, 0, (size_t)8 * m->Hp * sizeof(float), st));
+      CK(cudaMemsetAsync(m->hbuf, 0, (size_t)2 * 2 * 131072 * sizeof(float), st));
       CK(cudaMemsetAsync(m->bar, 0, sizeof(int), st));
       m->enc_epoch = 1;
     }
     e.epoch = m->enc_epoch;
+    {
+      const char* sw = getenv("NMT_ENC_HXSWAP");
+      const char* sd = getenv("NMT_ENC_HXSTRIDE");
+      const char* rp = getenv("NMT_ENC_HXREP");  // (diagnostic)
+      e.hx_rep = rp ? std::max(1, std::min(8, atoi(rp))) : 1;  // (measured: replicas only add store work)
+      e.hx_swap = sw ? atoi(sw) & 1 : 0;
+      e.hx_stride = sd ? std::max<int64_t>(2 * e.hx_rep * m->Hp, std::min<int64_t>(atoll(sd), 65536))
+                       : 2 * e.hx_rep * m->Hp;
+    }
     const bool trace = getenv("NMT_ENC_TRACE") != nullptr;  // diagnostic: per-step phase stamps
-    if (trace) CK(cudaMalloc(&e.trace, (size_t)(len + 1) * 8 * sizeof(long long)));
-    enc_recur(e, len, st);
+    if (trace) CK(cudaMalloc(&e.trace, ((size_t)(len + 1) * 8 + 2 * 2 * m->NB) * sizeof(long long)));
+    if (!stage_skipped(ST_ENC_RECUR)) enc_recur(e, len, st);
     if (trace) {
-      std::vector<long long> tv((size_t)(len + 1) * 8);
+      std::vector<long long> tv((size_t)(len + 1) * 8 + 2 * 2 * m->NB);
       CK(cudaMemcpyAsync(tv.data(), e.trace, tv.size() * 8, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       cudaFree(e.trace);
@@ -1104,9 +1201,22 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
       fprintf(stderr, "[enc_trace] fixed cycles: weights %lld  to-first-step %lld  loop %lld  barrier %lld  s0 %lld"
               "  | CTA0 %.1f us, %.0f MHz\n", f[1] - f[0], tv[0] - f[1], f[2] - tv[0], f[3] - f[2], f[4] - f[3],
               (f[6] - f[5]) / 1000.0, (double)(f[4] - f[0]) / ((f[6] - f[5]) / 1000.0));
+      for (int dd = 0; dd < 2; ++dd) {  // per direction: loop cycles and barrier waits over the CTAs
+        const long long* q = &tv[(size_t)(len + 1) * 8 + 2 * dd * m->NB];
+        long long lmin = LLONG_MAX, lmax = 0, wmin = LLONG_MAX, wmax = 0;
+        int amin = 0, amax = 0;
+        for (int b = 0; b < m->NB; ++b) {
+          if (q[2 * b] < lmin) lmin = q[2 * b];
+          if (q[2 * b] > lmax) lmax = q[2 * b];
+          if (q[2 * b + 1] < wmin) { wmin = q[2 * b + 1]; amin = b; }
+          if (q[2 * b + 1] > wmax) { wmax = q[2 * b + 1]; amax = b; }
+        }
+        fprintf(stderr, "[enc_trace] dir %d: loop cycles %lld..%lld, poll+barrier wait %lld (cta %d) .. %lld (cta %d)\n",
+                dd, lmin, lmax, wmin, amin, wmax, amax);
+      }
     }
   }
-  {  // E7: pctx = ctx.Wc_att + b_att
+  if (!stage_skipped(ST_ENC_PCTX)) {  // E7: pctx = ctx.Wc_att + b_att
     ProfScope p_(m, ST_ENC_PCTX);
     GemmShape g = gemm_shape(len, nullptr, m->Cp, m->Cp, 0, true, m->Cp, m->Cp);
     {  // ~8 splits, none empty

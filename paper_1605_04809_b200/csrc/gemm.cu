@@ -53,6 +53,7 @@ struct GemmSmem {
 
 struct RegionK {
   int k0, k1;  // in units of BK blocks
+  int ks;      // split-K factor of the region
 };
 
 struct TileCoord {
@@ -68,12 +69,22 @@ NMT_DEV TileCoord tile_of(int t, int num_m, int num_n) {
 struct Item {
   int m, s, n0, n1, c;
 };
+// EPI_STORE items go region by region; inside a region m is fastest, then n, then the K split.
 struct Sched {
-  int num_m, num_n, ksplit, cpm, chunk, items;
+  int num_m, num_n, cpm, chunk, items;
+  int nreg, nt_end[4], ks[4], it_end[4];  // per region: n-tile end, split count, cumulative items
   NMT_DEV Item item(int i) const {
     if (cpm == 0) {
-      const TileCoord t = tile_of(i, num_m, num_n);
-      return Item{t.m, t.s, t.n, t.n + 1, 0};
+      int r = 0, nt0 = 0, i0 = 0;
+#pragma unroll 1
+      while (r < nreg - 1 && i >= it_end[r]) {
+        nt0 = nt_end[r];
+        i0 = it_end[r];
+        ++r;
+      }
+      const int li = i - i0, ntr = nt_end[r] - nt0;
+      const int rest = li / num_m, n = nt0 + rest % ntr;
+      return Item{li % num_m, rest / ntr, n, n + 1, 0};
     }
     const int m = i / cpm, c = i % cpm;
     const int n0 = min(num_n, c * chunk);
@@ -81,11 +92,11 @@ struct Sched {
   }
 };
 template <int EPI>
-NMT_DEV Sched make_sched(int M, int CM, int N, int BN, int ksplit, int units) {
+NMT_DEV Sched make_sched(const GemmShape& g, int M, int CM, int BN, int units) {
   Sched s;
   s.num_m = (M + CM - 1) / CM;
-  s.num_n = N / BN;
-  s.ksplit = ksplit;
+  s.num_n = g.N / BN;
+  s.nreg = g.nreg;
   if (EPI == 1) {  // EPI_LSE
     s.cpm = max(1, units / max(1, s.num_m));
     s.chunk = (s.num_n + s.cpm - 1) / s.cpm;
@@ -93,7 +104,16 @@ NMT_DEV Sched make_sched(int M, int CM, int N, int BN, int ksplit, int units) {
   } else {
     s.cpm = 0;
     s.chunk = 1;
-    s.items = s.num_m * s.num_n * ksplit;
+    int nt0 = 0, acc = 0;
+    for (int r = 0; r < g.nreg; ++r) {
+      const int nt1 = r < g.nreg - 1 ? g.reg_n_end[r] / BN : s.num_n;
+      s.ks[r] = g.reg_ks[r] > 0 ? g.reg_ks[r] : g.ksplit;
+      acc += s.num_m * (nt1 - nt0) * s.ks[r];
+      s.nt_end[r] = nt1;
+      s.it_end[r] = acc;
+      nt0 = nt1;
+    }
+    s.items = acc;
   }
   return s;
 }
@@ -102,7 +122,7 @@ NMT_DEV RegionK region_of(const GemmShape& g, int n0) {
   int r = 0;
 #pragma unroll 1
   while (r < g.nreg - 1 && n0 >= g.reg_n_end[r]) ++r;
-  return RegionK{g.reg_k0[r] / BK, g.reg_k1[r] / BK};
+  return RegionK{g.reg_k0[r] / BK, g.reg_k1[r] / BK, g.reg_ks[r] > 0 ? g.reg_ks[r] : g.ksplit};
 }
 
 template <int BN, int STAGES, int EPI, bool PAIR>
@@ -153,7 +173,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   pdl_enter();  // prologue above overlaps the previous kernel; inputs (and M_dev) are read below
   const int M = g.M_dev ? *g.M_dev : g.M;
   const int unit = PAIR ? blockIdx.x / 2 : blockIdx.x, nunits = PAIR ? gridDim.x / 2 : gridDim.x;
-  const Sched sc = make_sched<EPI>(M, CM, g.N, BN, g.ksplit, nunits);
+  const Sched sc = make_sched<EPI>(g, M, CM, BN, nunits);
   if (EPI == EPI_LSE && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
 
   if (warp == 0) {
@@ -167,7 +187,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const TileCoord tc{itm.m, n, itm.s};
           const RegionK rk = region_of(g, tc.n * BN);
           const int nkbp = rk.k1 - rk.k0, nkb = g.passes * nkbp;
-          const int chunk = (nkb + g.ksplit - 1) / g.ksplit;
+          const int chunk = (nkb + rk.ks - 1) / rk.ks;
           const int i1 = min(nkb, (tc.s + 1) * chunk);
           for (int i = tc.s * chunk; i < i1; ++i) {
             const int pass = i / nkbp, kb = rk.k0 + i % nkbp;
@@ -212,7 +232,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tc_fence_after();
           const uint32_t d = tmem + acc * BN;
           const int nkb_all = g.passes * (rk.k1 - rk.k0);
-          const int chunk = (nkb_all + g.ksplit - 1) / g.ksplit;
+          const int chunk = (nkb_all + rk.ks - 1) / rk.ks;
           const int nkb = min(nkb_all, (tc.s + 1) * chunk) - tc.s * chunk;
           for (int i = 0; i < nkb; ++i) {
             mbar_wait(&full[stage], phase);
@@ -431,7 +451,12 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
     attr_set = true;
   }
   const int CM = PAIR ? 2 * BM : BM;
-  const int tiles = ((M_max + CM - 1) / CM) * (g.N / BN) * g.ksplit;
+  int tiles = 0;  // work items at M_max rows (EPI_STORE: per region, with its split count)
+  for (int r = 0, nt0 = 0; r < g.nreg; ++r) {
+    const int nt1 = r < g.nreg - 1 ? g.reg_n_end[r] / BN : g.N / BN;
+    tiles += ((M_max + CM - 1) / CM) * (nt1 - nt0) * gemm_ks(g, r);
+    nt0 = nt1;
+  }
   int grid = (PAIR ? 2 : 1) * tiles;
   if (EPI == EPI_LSE || grid > kNumSMs) grid = kNumSMs;  // persistent (LSE runs use every unit)
   if (grid <= 0) return;
@@ -456,10 +481,12 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
 void gemm_validate(const GemmShape& g, int BN) {
   if (g.N % BN) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: N not a multiple of the N tile");
   if (g.ksplit < 1) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: ksplit < 1");
-  for (int r = 0; r < g.nreg; ++r) {  // every split must own >= 1 k-block of every region
+  for (int r = 0; r < g.nreg; ++r) {  // every split must own >= 1 k-block of its region
+    const int ks = gemm_ks(g, r);
+    if (ks < 1) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: region split < 1");
     const int nkb = g.passes * (g.reg_k1[r] - g.reg_k0[r]) / BK;
-    const int chunk = (nkb + g.ksplit - 1) / g.ksplit;
-    if ((g.ksplit - 1) * chunk >= nkb) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: empty K split");
+    const int chunk = (nkb + ks - 1) / ks;
+    if ((ks - 1) * chunk >= nkb) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: empty K split");
   }
   for (int r = 0; r < g.nreg; ++r) {
     if (g.reg_k0[r] % BK || g.reg_k1[r] % BK || g.reg_k1[r] <= g.reg_k0[r])
@@ -474,7 +501,8 @@ void gemm_validate(const GemmShape& g, int BN) {
 static EpiParams store_params(const GemmShape& g, int BN, float* out, int ldc, const float* bias,
                               size_t split_stride) {
   gemm_validate(g, BN);
-  if (g.ksplit > 1 && (bias || !split_stride)) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: split-K partials take no bias");
+  if (gemm_ks_max(g) > 1 && (bias || !split_stride))
+    throw NmtError(NMT_ERR_INVALID_ARG, "gemm: split-K partials take no bias");
   if (split_stride % ldc) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: split stride not a whole number of rows");
   EpiParams ep{};
   ep.out = out;

@@ -66,6 +66,8 @@ struct GemmShape {
   int reg_k0[4];     // K range [k0, k1) of region r (multiples of 64, relative to a_col0 / 0)
   int reg_k1[4];
   int ksplit;        // split-K factor: split s writes its partial sum to out + s * split_stride
+  int reg_ks[4];     // per-region split-K factor (0: ksplit); regions may split differently so that
+                     // every work item carries about the same number of k-blocks
   int b_panel_rows;  // 0: B is [N][K] row-major; else B is stored as k-block panels [K/64][b_panel_rows][64]
                      // (every TMA box is one contiguous chunk): coordinate (0, kb * b_panel_rows + row)
 };
@@ -114,6 +116,12 @@ inline GemmShape gemm_shape(int M, const int* M_dev, int N, int K, int a_col0, b
   g.ksplit = 1;
   g.b_panel_rows = 0;
   return g;
+}
+inline int gemm_ks(const GemmShape& g, int r) { return g.reg_ks[r] > 0 ? g.reg_ks[r] : g.ksplit; }
+inline int gemm_ks_max(const GemmShape& g) {
+  int k = 1;
+  for (int r = 0; r < g.nreg; ++r) k = k > gemm_ks(g, r) ? k : gemm_ks(g, r);
+  return k;
 }
 
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }

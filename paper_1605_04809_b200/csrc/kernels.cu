@@ -450,6 +450,21 @@ NMT_DEV void store_split4(__nv_bfloat16* hi, int lo_off, float4 v) {
 NMT_DEV float sigm(float x) { return 1.f / (1.f + expf(-x)); }
 
 // D1: gather the parents' input states into the bf16 A operand of GRU1's recurrent GEMM
+// sum of the split-K partials of a decoder GEMM output, in split order (deterministic)
+NMT_DEV float4 ld4_sum(const float* p, int ks, int64_t stride) {
+  float4 a = ld4(p);
+  for (int s = 1; s < ks; ++s) {
+    const float4 b = ld4(p + s * stride);
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+  }
+  return a;
+}
+NMT_DEV float ld_sum(const float* p, int ks, int64_t stride) {
+  float a = p[0];
+  for (int s = 1; s < ks; ++s) a += p[s * stride];
+  return a;
+}
+
 __global__ void k_gather_state(StepDev d, const float* __restrict__ S) {
   pdl_enter();
   const int H4 = (d.H + 3) / 4;
@@ -470,7 +485,8 @@ __global__ void k_gru1(StepDev d, const float* __restrict__ S) {
   const int y = d.row_y[r];
   const float* g = d.G1 + (int64_t)r * 3 * Hp + j;
   const float* ex = d.Ex + (int64_t)(y < 0 ? d.V : y) * 3 * Hp + j;
-  const float4 gr = ld4(g), gu = ld4(g + Hp), gc = ld4(g + 2 * Hp);
+  const float4 gr = ld4_sum(g, d.ks_g1, d.ps_g1), gu = ld4_sum(g + Hp, d.ks_g1, d.ps_g1),
+               gc = ld4_sum(g + 2 * Hp, d.ks_g1, d.ps_g1);
   const float4 er = ld4(ex), eu = ld4(ex + Hp), ec = ld4(ex + 2 * Hp);
   const float4 sv = ld4(S + (int64_t)d.row_src[r] * Hp + j);
   float4 o;
@@ -513,8 +529,9 @@ NMT_DEV float warp_reduce_scatter32(float (&v)[32], int lane) {
 template <int RPB>
 __global__ void __launch_bounds__(256) k_attention(StepDev d, AttnCtx a) {
   pdl_enter();
-  static_assert(RPB == 4, "the 32-value reduce-scatter covers 8 positions x 4 rows");
-  constexpr int NST = 8;  // positions in flight
+  static_assert(RPB >= 1 && RPB <= 8, "rows per CTA");
+  constexpr int JB = RPB <= 4 ? 8 : 4;  // positions per reduce-scatter: JB x RPB <= 32 values
+  constexpr int NST = 8;                // positions in flight
   const int R = *d.R;
   const int r0 = blockIdx.x * RPB;
   if (r0 >= R) return;
@@ -532,8 +549,9 @@ __global__ void __launch_bounds__(256) k_attention(StepDev d, AttnCtx a) {
 #pragma unroll
   for (int rr = 0; rr < RPB; ++rr) {
     const bool ok = r0 + rr < R;
-    const float4* qp = reinterpret_cast<const float4*>(d.Q + (int64_t)(r0 + rr) * Cp + c0);
-    const float4 x0 = ok ? qp[0] : make_float4(0, 0, 0, 0), x1 = ok ? qp[1] : make_float4(0, 0, 0, 0);
+    const float* qp = d.Q + (int64_t)(r0 + rr) * Cp + c0;
+    const float4 x0 = ok ? ld4_sum(qp, d.ks_q, d.ps_q) : make_float4(0, 0, 0, 0),
+                 x1 = ok ? ld4_sum(qp + 4, d.ks_q, d.ps_q) : make_float4(0, 0, 0, 0);
     q[rr][0] = x0.x; q[rr][1] = x0.y; q[rr][2] = x0.z; q[rr][3] = x0.w;
     q[rr][4] = x1.x; q[rr][5] = x1.y; q[rr][6] = x1.z; q[rr][7] = x1.w;
   }
@@ -552,10 +570,12 @@ __global__ void __launch_bounds__(256) k_attention(StepDev d, AttnCtx a) {
     }
     cp_async_commit();
   }
-  for (int j0 = 0; j0 < Tx; j0 += 8) {
-    float e[32];  // e[jj * 4 + rr] partial energies of positions j0..j0+7
+  for (int j0 = 0; j0 < Tx; j0 += JB) {
+    float e[32];  // e[jj * RPB + rr] partial energies of positions j0..j0+JB-1 (zero padded)
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
+    for (int i = JB * RPB; i < 32; ++i) e[i] = 0.f;
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj) {
       const int j = j0 + jj;
       const int slot = j % NST;
       cp_async_wait<NST - 1>();
@@ -572,11 +592,11 @@ __global__ void __launch_bounds__(256) k_attention(StepDev d, AttnCtx a) {
         float s = 0.f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) s = fmaf(tanh_approx(p[k] + q[rr][k]), u[k], s);
-        e[jj * 4 + rr] = j < Tx ? s : 0.f;
+        e[jj * RPB + rr] = j < Tx ? s : 0.f;
       }
     }
-    const float tot = warp_reduce_scatter32(e, lane);  // lane = jj * 4 + rr
-    red[(warp * RPB + (lane & 3)) * Tx8 + j0 + (lane >> 2)] = tot;
+    const float tot = warp_reduce_scatter32(e, lane);  // lane = jj * RPB + rr
+    if (lane < JB * RPB) red[(warp * RPB + lane % RPB) * Tx8 + j0 + lane / RPB] = tot;
   }
   cp_async_wait<0>();
   __syncthreads();
@@ -659,7 +679,8 @@ __global__ void k_gru2(StepDev d, float* __restrict__ S) {
   const int r = idx / H4, j = (idx % H4) * 4;
   if (r >= *d.R) return;
   const float* g = d.G2 + (int64_t)r * 4 * Hp + j;
-  const float4 gr = ld4(g), gu = ld4(g + Hp), gh = ld4(g + 2 * Hp), gc = ld4(g + 3 * Hp);
+  const float4 gr = ld4_sum(g, d.ks_g2[0], d.ps_g2), gu = ld4_sum(g + Hp, d.ks_g2[0], d.ps_g2),
+               gh = ld4_sum(g + 2 * Hp, d.ks_g2[1], d.ps_g2), gc = ld4_sum(g + 3 * Hp, d.ks_g2[2], d.ps_g2);
   const float4 br = ld4(d.b_nl + j), bu = ld4(d.b_nl + Hp + j), bx = ld4(d.bx_nl + j);
   const float4 s1 = ld4(d.S1 + (int64_t)r * Hp + j);
   float4 o;
@@ -686,7 +707,7 @@ __global__ void k_readout(StepDev d, float* __restrict__ T) {
   float t[4];
   if (d.maxout) {
     if (2 * k + 7 < d.ROp) {
-      const float4 a0 = ld4(pre + 2 * k), a1 = ld4(pre + 2 * k + 4);
+      const float4 a0 = ld4_sum(pre + 2 * k, d.ks_ro, d.ps_ro), a1 = ld4_sum(pre + 2 * k + 4, d.ks_ro, d.ps_ro);
       const float4 b0 = ld4(epr + 2 * k), b1 = ld4(epr + 2 * k + 4);
       t[0] = fmaxf(a0.x + b0.x, a0.y + b0.y);
       t[1] = fmaxf(a0.z + b0.z, a0.w + b0.w);
@@ -695,15 +716,16 @@ __global__ void k_readout(StepDev d, float* __restrict__ T) {
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        t[i] = k + i < E ? fmaxf(pre[2 * (k + i)] + epr[2 * (k + i)], pre[2 * (k + i) + 1] + epr[2 * (k + i) + 1]) : 0.f;
+        t[i] = k + i < E ? fmaxf(ld_sum(pre + 2 * (k + i), d.ks_ro, d.ps_ro) + epr[2 * (k + i)],
+                                 ld_sum(pre + 2 * (k + i) + 1, d.ks_ro, d.ps_ro) + epr[2 * (k + i) + 1]) : 0.f;
     }
   } else {
     if (k + 3 < d.ROp) {
-      const float4 a = ld4(pre + k), b = ld4(epr + k);
+      const float4 a = ld4_sum(pre + k, d.ks_ro, d.ps_ro), b = ld4(epr + k);
       t[0] = tanhf(a.x + b.x); t[1] = tanhf(a.y + b.y); t[2] = tanhf(a.z + b.z); t[3] = tanhf(a.w + b.w);
     } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) t[i] = k + i < E ? tanhf(pre[k + i] + epr[k + i]) : 0.f;
+      for (int i = 0; i < 4; ++i) t[i] = k + i < E ? tanhf(ld_sum(pre + k + i, d.ks_ro, d.ps_ro) + epr[k + i]) : 0.f;
     }
   }
   float4 tv, av;  // tv -> arena (zero past E), av -> GEMM operand (bias columns at E, E+1)
@@ -872,6 +894,20 @@ __global__ void k_full_row(const float* __restrict__ T, const float* __restrict_
   if (lane == 0) out[w] = s + bo[w] - logZ[slot];
 }
 
+template <int RPB>
+static void launch_attention(const StepDev& d, const AttnCtx& a, int R_max, cudaStream_t st) {
+  const int nthr = d.Cp / 8;
+  const int nw = nthr / 32 > 0 ? nthr / 32 : 1;
+  const int Tx8 = (a.Tx + 7) & ~7;  // (as in the kernel: JB divides 8)
+  const size_t smem = (size_t)8 * nthr * 2 * sizeof(float4) + (size_t)(nw * RPB * Tx8 + RPB * a.Tx) * sizeof(float);
+  static size_t attr = 0;  // > 48 KB of dynamic shared memory needs the opt-in
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_attention<RPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  launch_pdl(k_attention<RPB>, (R_max + RPB - 1) / RPB, nthr, smem, st, d, a);
+}
+
 void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, float* T, float* logZ, int* amax,
                       int R_max, cudaStream_t st) {
   if (R_max <= 0) return;
@@ -884,17 +920,21 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
     case EW_GATHER: launch_pdl(k_gather_state, gh, 256, 0, st, d, S); break;
     case EW_GRU1: launch_pdl(k_gru1, gh, 256, 0, st, d, S); break;
     case EW_ATTN: {
-      constexpr int RPB = 4;
-      const int nthr = d.Cp / 8;
-      const int nw = nthr / 32 > 0 ? nthr / 32 : 1;
-      const int Tx8 = (a.Tx + 7) & ~7;
-      const size_t smem = (size_t)8 * nthr * 2 * sizeof(float4) + (size_t)(nw * RPB * Tx8 + RPB * a.Tx) * sizeof(float);
-      static size_t attr = 0;  // > 48 KB of dynamic shared memory needs the opt-in
-      if (smem > attr) {
-        CK(cudaFuncSetAttribute(k_attention<RPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
+      // one wave: rows per CTA = ceil(R / SMs) (<= 8), so every SM carries the same number of rows
+      static const int rpb_env = getenv("NMT_ATTN_RPB") ? atoi(getenv("NMT_ATTN_RPB")) : 0;  // (diagnostic)
+      // rows per CTA: ceil(R / SMs), at most 4 (measured in the step at R = 1024: 4 rows x 256 CTAs is
+      // ~28 us faster than one wave of 7-row CTAs, whose single CTA per SM hides less latency)
+      const int rpb = rpb_env > 0 ? std::min(8, rpb_env) : std::max(1, std::min(4, (R_max + kNumSMs - 1) / kNumSMs));
+      switch (rpb) {
+        case 1: launch_attention<1>(d, a, R_max, st); break;
+        case 2: launch_attention<2>(d, a, R_max, st); break;
+        case 3: launch_attention<3>(d, a, R_max, st); break;
+        case 4: launch_attention<4>(d, a, R_max, st); break;
+        case 5: launch_attention<5>(d, a, R_max, st); break;
+        case 6: launch_attention<6>(d, a, R_max, st); break;
+        case 7: launch_attention<7>(d, a, R_max, st); break;
+        default: launch_attention<8>(d, a, R_max, st); break;
       }
-      launch_pdl(k_attention<RPB>, (R_max + RPB - 1) / RPB, nthr, smem, st, d, a);
       break;
     }
     case EW_GRU2: launch_pdl(k_gru2, gh, 256, 0, st, d, S); break;
@@ -950,8 +990,9 @@ __device__ __forceinline__ float tanh_fast(float x) {  // |err| ~ 1e-7 (not tanh
   const float e = __expf(2.f * fminf(fmaxf(x, -15.f), 15.f));
   return 1.f - __fdividef(2.f, e + 1.f);
 }
-template <int KI>  // Hp = 128 * KI
-__global__ void __launch_bounds__(512, 1) k_enc_recur(EncDev e, int Tx) {
+constexpr int kPinMax = 512;  // sources up to this length have their input projections staged in smem
+template <int KI, bool TRACE>  // Hp = 128 * KI; TRACE: clock64 phase stamps (diagnostic build of the kernel)
+__global__ void __launch_bounds__(448, 1) k_enc_recur(EncDev e, int Tx) {  // UPC <= 14 warps (<= 4 per SMSP: 128 regs)
   pdl_wait();  // (no early trigger: the cooperative grid must not lose SMs to dependents)
   constexpr int Hp = 128 * KI, H4 = Hp / 4;
   __shared__ float4 h4buf[2][H4];  // by step parity: a warp reading step t never races the poll of t+1
@@ -961,8 +1002,8 @@ __global__ void __launch_bounds__(512, 1) k_enc_recur(EncDev e, int Tx) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int jj = cb * UPC + warp;  // this warp's hidden unit
   const bool unit = jj < H;
-  long long* tr = (e.trace && blockIdx.x == 0 && threadIdx.x == 0) ? e.trace : nullptr;
-  if (tr) {
+  long long* tr = (TRACE && blockIdx.x == 0 && threadIdx.x == 0) ? e.trace : nullptr;
+  if (TRACE && tr) {
     tr[Tx * 8 + 0] = clock64();
     unsigned long long g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -995,98 +1036,141 @@ __global__ void __launch_bounds__(512, 1) k_enc_recur(EncDev e, int Tx) {
   }
   if (!bulk)
     for (int i = threadIdx.x; i < n_out * C; i += nthr) wsm[i] = __ldg(e.W_initT + (int64_t)o_first * C + i);
-  unsigned long long* hx = e.hx + (size_t)dir * 2 * Hp;  // [2][Hp] tagged words of this direction
+  unsigned long long* hx = e.hx + (size_t)(dir ^ e.hx_swap) * e.hx_stride;  // [2][Hp] tagged words of this direction
   const unsigned ep = e.epoch << 16;
-  bool bad = false;
   float hself = 0.f, hsum = 0.f;
-  // input projections (independent of h) are fetched one step ahead: the table rows live in HBM
-  // and the source id one step before that, so no dependent load sits on the step's critical path
-  auto load_id = [&](int t) { return t < Tx ? __ldg(e.src + (dir == 0 ? t : Tx - 1 - t)) : 0; };
-  auto fetch_pin = [&](int id, float& r_, float& u_, float& x_) {
-    if (id < 0 || id >= e.Vs) {  // device-resident ids are validated here (nmt_ctx_check)
-      bad = true;
-      id = 0;
-    }
-    const float* pin = e.encin + (int64_t)id * 6 * Hp + dir * 3 * Hp;
-    r_ = __ldg(pin + jj);
-    u_ = __ldg(pin + Hp + jj);
-    x_ = __ldg(pin + 2 * Hp + jj);
-  };
+  // input projections (independent of h) are fetched one step ahead: the table rows live in HBM;
+  // the source id one step before that, so no dependent load sits on the step's critical path
+  const int* srcp = e.src;
+  const int sdir = dir == 0 ? 1 : -1, s0 = dir == 0 ? 0 : Tx - 1;  // position of step t = s0 + sdir t
+  const float* encin = e.encin + dir * 3 * Hp + jj;
+  const int Vs = e.Vs;
+#define NMT_FETCH_PIN(ID, R_, U_, X_)                                              \
+  {                                                                                \
+    int id_ = (ID);                                                                \
+    if (id_ < 0 || id_ >= Vs) { /* device-resident ids are validated here */      \
+      if (lane == 0) atomicOr(e.err, ERR_TOKEN);  /* (nmt_ctx_check reports it) */ \
+      id_ = 0;                                                                     \
+    }                                                                              \
+    const float* pin_ = encin + (int64_t)id_ * 6 * Hp;                             \
+    R_ = __ldg(pin_);                                                              \
+    U_ = __ldg(pin_ + Hp);                                                         \
+    X_ = __ldg(pin_ + 2 * Hp);                                                     \
+  }
+  // Tx <= kPinMax: the whole sentence's projections of this CTA's units are gathered into shared
+  // memory at start (ids first, then 4-byte cp.async gathers that overlap the weight loads), so a
+  // step reads them with LDS; longer sources fetch one step ahead from HBM (NMT_FETCH_PIN).
+  const bool pre = Tx <= kPinMax;
+  float* pin_s = wsm + per * C;                                     // [Tx][3][UPC]
+  int* ids_s = reinterpret_cast<int*>(pin_s + (pre ? Tx * 3 * UPC : 0));  // [Tx]
   float n_r = 0.f, n_u = 0.f, n_x = 0.f;
-  int id_next = load_id(1);
-  if (unit) fetch_pin(load_id(0), n_r, n_u, n_x);
-  if (tr) {
+  int id_next = 0;
+  if (pre) {
+    for (int t = threadIdx.x; t < Tx; t += nthr) {
+      int id = __ldg(srcp + s0 + sdir * t);
+      if (id < 0 || id >= Vs) {  // device-resident ids are validated here (nmt_ctx_check)
+        atomicOr(e.err, ERR_TOKEN);
+        id = 0;
+      }
+      ids_s[t] = id;
+    }
+    __syncthreads();
+    const int per_t = 3 * UPC;
+    for (int i = threadIdx.x; i < Tx * per_t; i += nthr) {
+      const int t = i / per_t, g = (i % per_t) / UPC, u = i % UPC;
+      const int unit_j = cb * UPC + u;
+      if (unit_j < H)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(pin_s + i)),
+                     "l"(e.encin + (int64_t)ids_s[t] * 6 * Hp + dir * 3 * Hp + g * Hp + unit_j) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  } else {
+    id_next = Tx > 1 ? __ldg(srcp + s0 + sdir) : 0;
+    if (unit) NMT_FETCH_PIN(__ldg(srcp + s0), n_r, n_u, n_x);
+  }
+  if (TRACE && tr) {
     // (weights are in registers once used: force completion for the stamp with a dependent read)
     tr[Tx * 8 + 1] = clock64() + (long long)(wr[KI - 1].w == 12345.f) + (long long)(wx[0].x == 12345.f);
   }
+  // polling: thread k < Hp/4 owns the 4 tagged words of units 4k..4k+3 (one 256-bit load)
+  const int kq = threadIdx.x;
+  const bool poller = kq < H4 && 4 * kq < H;
+  const unsigned need = (4 * kq + 3 < H) ? 0xFu : ((1u << max(0, min(4, H - 4 * kq))) - 1u);  // real units only
+  if (pre) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();  // (the gathered projections are visible to every warp)
+  }
   int npolls = 0;
+  long long cyc_poll = 0, cyc_loop0 = TRACE ? clock64() : 0;
   for (int t = 0; t < Tx; ++t) {
-    if (tr) tr[t * 8 + 0] = clock64();
-    const int j = dir == 0 ? t : Tx - 1 - t;
-    const float p_r = n_r, p_u = n_u, p_x = n_x;
-    if (unit && t + 1 < Tx) fetch_pin(id_next, n_r, n_u, n_x);
-    id_next = load_id(t + 2);
-    if (tr) tr[t * 8 + 1] = clock64();
-    float2 ar0 = make_float2(0.f, 0.f), au0 = ar0, ax0 = ar0, ar1 = ar0, au1 = ar0, ax1 = ar0;
+    if (TRACE && tr) tr[t * 8 + 0] = clock64();
+    const int j = s0 + sdir * t;
+    float p_r = n_r, p_u = n_u, p_x = n_x;
+    if (!pre) {
+      if (unit && t + 1 < Tx) NMT_FETCH_PIN(id_next, n_r, n_u, n_x);
+      if (t + 2 < Tx) id_next = __ldg(srcp + s0 + sdir * (t + 2));
+    }
+    // (measured: issuing the poll before the fetch above is ~20% slower per step)
+    unsigned long long a = 0, b = 0, c = 0, d = 0;
+    const unsigned long long* hsrc = hx + (size_t)(t & 1) * Hp + 4 * kq;
+    if (t > 0 && poller)
+      asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                   : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(hsrc) : "memory");
+    if (TRACE && tr) tr[t * 8 + 1] = clock64();
+    float2 ar = make_float2(0.f, 0.f), au = ar, ax = ar;  // (3 chains: the 96 weight registers leave room for no more)
     if (t > 0) {
-      const unsigned long long* src = hx + (size_t)(t & 1) * Hp;
       const unsigned tag = ep | (unsigned)t;  // h_{t-1} was written with tag (t-1)+1
       float4* h4 = h4buf[t & 1];
-      const int npoll = (e.poll & 2) ? 64 : nthr;  // threads that poll
-      if ((int)threadIdx.x < npoll) {
-        for (int k = threadIdx.x; k < H4; k += npoll) {
-          if (4 * k >= H) {  // padded units (H < Hp) are never written: they stay 0
-            h4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-            continue;
-          }
-          // units >= H inside this float4 carry no tag: accept them as 0
-          const unsigned need = (4 * k + 3 < H) ? 0xFu : ((1u << (H - 4 * k)) - 1u);
-          unsigned long long a, b, c, d;
-          const long long t0 = clock64();
-          while (true) {  // one 256-bit load: 4 tagged words
-            asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
-                         : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(src + 4 * k) : "memory");
-            const unsigned ok = ((unsigned)(a >> 32) == tag) | (((unsigned)(b >> 32) == tag) << 1) |
-                                (((unsigned)(c >> 32) == tag) << 2) | (((unsigned)(d >> 32) == tag) << 3);
-            ++npolls;
-            if ((ok & need) == need || (e.poll & 4)) break;  // (4: timing only, no wait)
-            if (e.poll & 1) __nanosleep(64);
-            if (clock64() - t0 > (1ll << 32)) asm volatile("trap;");  // watchdog (~2 s): fail, never hang
-          }
-          h4[k] = make_float4((need & 1) ? __uint_as_float((unsigned)a) : 0.f, (need & 2) ? __uint_as_float((unsigned)b) : 0.f,
-                              (need & 4) ? __uint_as_float((unsigned)c) : 0.f, (need & 8) ? __uint_as_float((unsigned)d) : 0.f);
+      if (poller) {
+        const long long t0 = clock64();
+        while (true) {
+          ++npolls;
+          const unsigned ok = ((unsigned)(a >> 32) == tag) | (((unsigned)(b >> 32) == tag) << 1) |
+                              (((unsigned)(c >> 32) == tag) << 2) | (((unsigned)(d >> 32) == tag) << 3);
+          if ((ok & need) == need) break;
+          if (clock64() - t0 > (1ll << 32)) asm volatile("trap;");  // watchdog (~2 s): fail, never hang
+          asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                       : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(hsrc) : "memory");
         }
+        // units >= H inside this float4 carry no tag: they are 0
+        h4[kq] = make_float4((need & 1) ? __uint_as_float((unsigned)a) : 0.f, (need & 2) ? __uint_as_float((unsigned)b) : 0.f,
+                             (need & 4) ? __uint_as_float((unsigned)c) : 0.f, (need & 8) ? __uint_as_float((unsigned)d) : 0.f);
+      } else if (kq < H4) {
+        h4[kq] = make_float4(0.f, 0.f, 0.f, 0.f);  // padded units (H < Hp) are never written
       }
-      if (tr) tr[t * 8 + 2] = clock64();
+      if (TRACE && tr) tr[t * 8 + 2] = clock64();
+      const long long cb0 = TRACE ? clock64() : 0;
       __syncthreads();  // (the only barrier of a step: buffer t&1 is rewritten at t+2, after t+1's barrier)
-      if (tr) tr[t * 8 + 3] = clock64();
+      if (TRACE && tr) tr[t * 8 + 3] = clock64();
+      if (TRACE) cyc_poll += clock64() - cb0;  // (barrier wait: this CTA's pollers waiting for h)
 #pragma unroll
       for (int i = 0; i < KI; ++i) {
         const float4 h = h4[lane + 32 * i];
         const float2 hlo = make_float2(h.x, h.y), hhi = make_float2(h.z, h.w);
-        if (i & 1) {
-          ffma2(ar1, make_float2(wr[i].x, wr[i].y), hlo); ffma2(ar1, make_float2(wr[i].z, wr[i].w), hhi);
-          ffma2(au1, make_float2(wu[i].x, wu[i].y), hlo); ffma2(au1, make_float2(wu[i].z, wu[i].w), hhi);
-          ffma2(ax1, make_float2(wx[i].x, wx[i].y), hlo); ffma2(ax1, make_float2(wx[i].z, wx[i].w), hhi);
-        } else {
-          ffma2(ar0, make_float2(wr[i].x, wr[i].y), hlo); ffma2(ar0, make_float2(wr[i].z, wr[i].w), hhi);
-          ffma2(au0, make_float2(wu[i].x, wu[i].y), hlo); ffma2(au0, make_float2(wu[i].z, wu[i].w), hhi);
-          ffma2(ax0, make_float2(wx[i].x, wx[i].y), hlo); ffma2(ax0, make_float2(wx[i].z, wx[i].w), hhi);
-        }
+        ffma2(ar, make_float2(wr[i].x, wr[i].y), hlo);
+        ffma2(au, make_float2(wu[i].x, wu[i].y), hlo);
+        ffma2(ax, make_float2(wx[i].x, wx[i].y), hlo);
+        ffma2(ar, make_float2(wr[i].z, wr[i].w), hhi);
+        ffma2(au, make_float2(wu[i].z, wu[i].w), hhi);
+        ffma2(ax, make_float2(wx[i].z, wx[i].w), hhi);
       }
     }
     // (h_0 = 0: the dot products are 0 at t = 0)
-    float dr = (ar0.x + ar0.y) + (ar1.x + ar1.y);
-    float du = (au0.x + au0.y) + (au1.x + au1.y);
-    float dx = (ax0.x + ax0.y) + (ax1.x + ax1.y);
+    float dr = ar.x + ar.y, du = au.x + au.y, dx = ax.x + ax.y;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {  // butterfly: every lane ends with the same sums
       dr += __shfl_xor_sync(0xffffffffu, dr, o);
       du += __shfl_xor_sync(0xffffffffu, du, o);
       dx += __shfl_xor_sync(0xffffffffu, dx, o);
     }
-    if (tr) tr[t * 8 + 4] = clock64();
+    if (TRACE && tr) tr[t * 8 + 4] = clock64();
     if (unit) {
+      if (pre) {
+        const float* pt = pin_s + t * 3 * UPC + warp;
+        p_r = pt[0];
+        p_u = pt[UPC];
+        p_x = pt[2 * UPC];
+      }
       const float rg = sigmoid_fast(p_r + dr);
       const float ug = sigmoid_fast(p_u + du);
       const float ht = tanh_fast(rg * dx + p_x);
@@ -1106,13 +1190,18 @@ __global__ void __launch_bounds__(512, 1) k_enc_recur(EncDev e, int Tx) {
         e.ctxbf[(int64_t)j * 4 * Hp + 2 * Hp + cidx] = lo;
       }
     }
-    if (tr) {
+    if (TRACE && tr) {
       tr[t * 8 + 5] = clock64();
       tr[t * 8 + 6] = npolls;
     }
   }
+#undef NMT_FETCH_PIN
   // ---- E5: time means -> grid barrier -> s0 slices
-  if (tr) tr[Tx * 8 + 2] = clock64();
+  if (TRACE && tr) tr[Tx * 8 + 2] = clock64();
+  if (TRACE && threadIdx.x == 0) {  // per-CTA: [loop cycles, barrier-wait cycles] after the CTA-0 trace
+    e.trace[(Tx + 1) * 8 + 2 * blockIdx.x] = clock64() - cyc_loop0;
+    e.trace[(Tx + 1) * 8 + 2 * blockIdx.x + 1] = cyc_poll;
+  }
   if (unit && lane == 0) e.mean[dir * H + jj] = hsum / (float)Tx;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1125,8 +1214,7 @@ __global__ void __launch_bounds__(512, 1) k_enc_recur(EncDev e, int Tx) {
     } while (v < (int)(e.epoch * gridDim.x));
   }
   __syncthreads();
-  if (tr) tr[Tx * 8 + 3] = clock64();
-  if (bad && lane == 0) atomicOr(e.err, ERR_TOKEN);
+  if (TRACE && tr) tr[Tx * 8 + 3] = clock64();
   // all 2H means at once (C <= 2Hp floats = the two h buffers), then a warp per s0 output
   float* msm = reinterpret_cast<float*>(h4buf);
   for (int k = threadIdx.x; k < C; k += nthr) msm[k] = __ldcg(e.mean + k);
@@ -1152,7 +1240,7 @@ __global__ void __launch_bounds__(512, 1) k_enc_recur(EncDev e, int Tx) {
     for (int off = 16; off > 0; off >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, off);
     if (lane == 0) e.S0[o] = tanhf(sacc + e.b_init[o]);
   }
-  if (tr) {
+  if (TRACE && tr) {
     tr[Tx * 8 + 4] = clock64();
     unsigned long long g;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -1160,31 +1248,328 @@ __global__ void __launch_bounds__(512, 1) k_enc_recur(EncDev e, int Tx) {
   }
 }
 
-template <int KI>
+// Variant with TWO units per warp (UPC <= 14 -> <= 7 warps): the warp keeps 6 weight columns in
+// registers (192 per lane, up to 255 allowed at 224 threads), so half as many warps read h from
+// shared memory each step (the bound of the 1-unit layout: 14 warps x 4 KB per step), with six
+// independent FFMA2 chains per lane.  Lanes 0-15 finish unit 2w, lanes 16-31 unit 2w+1.
+template <int KI, bool TRACE>
+__global__ void __launch_bounds__(224, 1) k_enc_recur2(EncDev e, int Tx) {
+  pdl_wait();  // (no early trigger: the cooperative grid must not lose SMs to dependents)
+  constexpr int Hp = 128 * KI, H4 = Hp / 4;
+  __shared__ float4 h4buf[2][H4];  // by step parity: a warp reading step t never races the poll of t+1
+  const int NB = e.NB, UPC = e.UPC, H = e.H;
+  const int nthr = blockDim.x;
+  const int dir = blockIdx.x / NB, cb = blockIdx.x % NB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ua = 2 * warp, ub = 2 * warp + 1;                 // the warp's units (CTA-local)
+  const int side = lane >> 4;                                  // 0: lanes finish unit ua, 1: ub
+  const int uloc = ua + side;
+  const int jj = cb * UPC + uloc;                              // this lane's finishing unit (global)
+  const bool unit = uloc < UPC && jj < H;
+  long long* tr = (TRACE && blockIdx.x == 0 && threadIdx.x == 0) ? e.trace : nullptr;
+  if (TRACE && tr) {
+    tr[Tx * 8 + 0] = clock64();
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    tr[Tx * 8 + 5] = (long long)g;
+  }
+  const int C = 2 * H;
+  const int per = (H + gridDim.x - 1) / gridDim.x;  // s0 outputs of this CTA (tail)
+  extern __shared__ __align__(16) float wsm[];       // [per][C] rows of W_init^T (tail) | pin | ids
+  __shared__ __align__(8) uint64_t wbar;             // completion of their bulk copy
+  const int o_first = blockIdx.x * per, n_out = max(0, min(per, H - o_first));
+  const bool bulk = (C % 4) == 0;
+  if (bulk && threadIdx.x == 0) {
+    mbar_init(&wbar, 1);
+    fence_barrier_init();
+    mbar_arrive_expect_tx(&wbar, (uint32_t)(n_out * C * 4));
+    for (int r = 0; r < n_out; ++r)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(wsm + r * C)), "l"(e.W_initT + (int64_t)(o_first + r) * C), "r"(C * 4),
+                   "r"(smem_u32(&wbar)) : "memory");
+  }
+  // weights: columns g * UPC + u of this CTA's [3 UPC][Hp] block (zero rows for u >= UPC)
+  float4 wra[KI], wua[KI], wxa[KI], wrb[KI], wub[KI], wxb[KI];
+  {
+    const float4* src = reinterpret_cast<const float4*>(e.Uarr) + (size_t)(dir * NB + cb) * 3 * UPC * H4;
+    const bool hb = ub < UPC;
+#pragma unroll
+    for (int i = 0; i < KI; ++i) {
+      const int k = lane + 32 * i;
+      wra[i] = src[(size_t)ua * H4 + k];
+      wua[i] = src[(size_t)(UPC + ua) * H4 + k];
+      wxa[i] = src[(size_t)(2 * UPC + ua) * H4 + k];
+      wrb[i] = hb ? src[(size_t)ub * H4 + k] : make_float4(0.f, 0.f, 0.f, 0.f);
+      wub[i] = hb ? src[(size_t)(UPC + ub) * H4 + k] : make_float4(0.f, 0.f, 0.f, 0.f);
+      wxb[i] = hb ? src[(size_t)(2 * UPC + ub) * H4 + k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  if (!bulk)
+    for (int i = threadIdx.x; i < n_out * C; i += nthr) wsm[i] = __ldg(e.W_initT + (int64_t)o_first * C + i);
+  unsigned long long* hx = e.hx + (size_t)(dir ^ e.hx_swap) * e.hx_stride;  // [2][Hp] tagged words
+  const unsigned ep = e.epoch << 16;
+  const int sdir = dir == 0 ? 1 : -1, s0 = dir == 0 ? 0 : Tx - 1;  // position of step t = s0 + sdir t
+  // input projections of all steps (Tx <= kPinMax): ids, then 4-byte cp.async gathers
+  const bool pre = Tx <= kPinMax;
+  float* pin_s = wsm + per * C;                                          // [Tx][3][UPC]
+  int* ids_s = reinterpret_cast<int*>(pin_s + (pre ? Tx * 3 * UPC : 0));  // [Tx]
+  if (pre) {
+    for (int t = threadIdx.x; t < Tx; t += nthr) {
+      int id = __ldg(e.src + s0 + sdir * t);
+      if (id < 0 || id >= e.Vs) {  // device-resident ids are validated here (nmt_ctx_check)
+        atomicOr(e.err, ERR_TOKEN);
+        id = 0;
+      }
+      ids_s[t] = id;
+    }
+    __syncthreads();
+    const int per_t = 3 * UPC;
+    for (int i = threadIdx.x; i < Tx * per_t; i += nthr) {
+      const int t = i / per_t, g = (i % per_t) / UPC, u = i % UPC;
+      const int uj = cb * UPC + u;
+      if (uj < H)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(pin_s + i)),
+                     "l"(e.encin + (int64_t)ids_s[t] * 6 * Hp + dir * 3 * Hp + g * Hp + uj) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+  }
+  if (TRACE && tr)
+    tr[Tx * 8 + 1] = clock64() + (long long)(wra[KI - 1].w == 12345.f) + (long long)(wxb[0].x == 12345.f);
+  float hself = 0.f, hsum = 0.f;
+  int npolls = 0;
+  long long cyc_poll = 0, cyc_loop0 = TRACE ? clock64() : 0;
+  for (int t = 0; t < Tx; ++t) {
+    if (TRACE && tr) tr[t * 8 + 0] = clock64();
+    const int j = s0 + sdir * t;
+    float p_r = 0.f, p_u = 0.f, p_x = 0.f;
+    if (unit) {
+      if (pre) {
+        const float* pt = pin_s + t * 3 * UPC + uloc;
+        p_r = pt[0];
+        p_u = pt[UPC];
+        p_x = pt[2 * UPC];
+      } else {
+        int id = __ldg(e.src + j);
+        if (id < 0 || id >= e.Vs) {
+          if ((lane & 15) == 0) atomicOr(e.err, ERR_TOKEN);
+          id = 0;
+        }
+        const float* pin = e.encin + (int64_t)id * 6 * Hp + dir * 3 * Hp + jj;
+        p_r = __ldg(pin);
+        p_u = __ldg(pin + Hp);
+        p_x = __ldg(pin + 2 * Hp);
+      }
+    }
+    if (TRACE && tr) tr[t * 8 + 1] = clock64();
+    float2 ara = make_float2(0.f, 0.f), aua = ara, axa = ara, arb = ara, aub = ara, axb = ara;
+    if (t > 0) {
+      const unsigned tag = ep | (unsigned)t;  // h_{t-1} was written with tag (t-1)+1
+      float4* h4 = h4buf[t & 1];
+      const unsigned long long* hsrc = hx + ((size_t)(t & 1) * e.hx_rep + cb % e.hx_rep) * Hp;
+      // <= 2 positions per thread (host-checked): both 256-bit loads are in flight before any wait
+      const int k0 = threadIdx.x, k1 = threadIdx.x + nthr;
+      const bool h0 = k0 < H4 && 4 * k0 < H, h1 = k1 < H4 && 4 * k1 < H;
+      const unsigned need0 = (4 * k0 + 3 < H) ? 0xFu : ((1u << max(0, H - 4 * k0)) - 1u);  // real units only
+      const unsigned need1 = (4 * k1 + 3 < H) ? 0xFu : ((1u << max(0, H - 4 * k1)) - 1u);
+      unsigned long long a0 = 0, b0 = 0, c0 = 0, d0 = 0, a1 = 0, b1 = 0, c1 = 0, d1 = 0;
+      if (h0)
+        asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                     : "=l"(a0), "=l"(b0), "=l"(c0), "=l"(d0) : "l"(hsrc + 4 * k0) : "memory");
+      if (h1)
+        asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                     : "=l"(a1), "=l"(b1), "=l"(c1), "=l"(d1) : "l"(hsrc + 4 * k1) : "memory");
+      auto settle = [&](bool has, int k, unsigned need, unsigned long long& a, unsigned long long& b,
+                        unsigned long long& c, unsigned long long& d) {
+        if (!has) {
+          if (k < H4) h4[k] = make_float4(0.f, 0.f, 0.f, 0.f);  // padded units (H < Hp) are never written
+          return;
+        }
+        const long long tw = clock64();
+        while (true) {
+          ++npolls;
+          const unsigned ok = ((unsigned)(a >> 32) == tag) | (((unsigned)(b >> 32) == tag) << 1) |
+                              (((unsigned)(c >> 32) == tag) << 2) | (((unsigned)(d >> 32) == tag) << 3);
+          if ((ok & need) == need) break;
+          if (clock64() - tw > (1ll << 32)) asm volatile("trap;");  // watchdog (~2 s): fail, never hang
+          asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                       : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(hsrc + 4 * k) : "memory");
+        }
+        h4[k] = make_float4((need & 1) ? __uint_as_float((unsigned)a) : 0.f, (need & 2) ? __uint_as_float((unsigned)b) : 0.f,
+                            (need & 4) ? __uint_as_float((unsigned)c) : 0.f, (need & 8) ? __uint_as_float((unsigned)d) : 0.f);
+      };
+      settle(h0, k0, need0, a0, b0, c0, d0);
+      settle(h1, k1, need1, a1, b1, c1, d1);
+      if (TRACE && tr) tr[t * 8 + 2] = clock64();
+      const long long cb0 = TRACE ? clock64() : 0;
+      __syncthreads();  // (the only barrier of a step: buffer t&1 is rewritten at t+2, after t+1's barrier)
+      if (TRACE && tr) tr[t * 8 + 3] = clock64();
+      if (TRACE) cyc_poll += clock64() - cb0;
+#pragma unroll
+      for (int i = 0; i < KI; ++i) {
+        const float4 h = h4[lane + 32 * i];
+        const float2 hlo = make_float2(h.x, h.y), hhi = make_float2(h.z, h.w);
+        ffma2(ara, make_float2(wra[i].x, wra[i].y), hlo);
+        ffma2(aua, make_float2(wua[i].x, wua[i].y), hlo);
+        ffma2(axa, make_float2(wxa[i].x, wxa[i].y), hlo);
+        ffma2(arb, make_float2(wrb[i].x, wrb[i].y), hlo);
+        ffma2(aub, make_float2(wub[i].x, wub[i].y), hlo);
+        ffma2(axb, make_float2(wxb[i].x, wxb[i].y), hlo);
+        ffma2(ara, make_float2(wra[i].z, wra[i].w), hhi);
+        ffma2(aua, make_float2(wua[i].z, wua[i].w), hhi);
+        ffma2(axa, make_float2(wxa[i].z, wxa[i].w), hhi);
+        ffma2(arb, make_float2(wrb[i].z, wrb[i].w), hhi);
+        ffma2(aub, make_float2(wub[i].z, wub[i].w), hhi);
+        ffma2(axb, make_float2(wxb[i].z, wxb[i].w), hhi);
+      }
+    }
+    // (h_0 = 0: the dot products are 0 at t = 0)
+    float dra = ara.x + ara.y, dua = aua.x + aua.y, dxa = axa.x + axa.y;
+    float drb = arb.x + arb.y, dub = aub.x + aub.y, dxb = axb.x + axb.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // butterfly: every lane ends with all six sums
+      dra += __shfl_xor_sync(0xffffffffu, dra, o);
+      dua += __shfl_xor_sync(0xffffffffu, dua, o);
+      dxa += __shfl_xor_sync(0xffffffffu, dxa, o);
+      drb += __shfl_xor_sync(0xffffffffu, drb, o);
+      dub += __shfl_xor_sync(0xffffffffu, dub, o);
+      dxb += __shfl_xor_sync(0xffffffffu, dxb, o);
+    }
+    if (TRACE && tr) tr[t * 8 + 4] = clock64();
+    if (unit) {
+      const float dr = side ? drb : dra, du = side ? dub : dua, dx = side ? dxb : dxa;
+      const float rg = sigmoid_fast(p_r + dr);
+      const float ug = sigmoid_fast(p_u + du);
+      const float ht = tanh_fast(rg * dx + p_x);
+      hself = ug * hself + (1.f - ug) * ht;
+      hsum += hself;
+      const int cidx = dir * Hp + jj;  // padded context column
+      const int role = lane & 15;
+      if (role >= 3 + 0 && role < 3 + e.hx_rep) {  // lanes 3.. publish h_t to every replica (one store each)
+        const unsigned long long word = ((unsigned long long)(ep | (unsigned)(t + 1)) << 32) | __float_as_uint(hself);
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;"
+                     ::"l"(hx + ((size_t)((t + 1) & 1) * e.hx_rep + (role - 3)) * Hp + jj), "l"(word) : "memory");
+      } else if (role == 1) {
+        e.ctx[(int64_t)j * 2 * Hp + cidx] = hself;
+      } else if (role == 2) {
+        __nv_bfloat16 hi, lo;
+        split_bf16(hself, hi, lo);
+        e.ctxbf[(int64_t)j * 4 * Hp + cidx] = hi;
+        e.ctxbf[(int64_t)j * 4 * Hp + 2 * Hp + cidx] = lo;
+      }
+    }
+    if (TRACE && tr) {
+      tr[t * 8 + 5] = clock64();
+      tr[t * 8 + 6] = npolls;
+    }
+  }
+  // ---- E5: time means -> grid barrier -> s0 slices
+  if (TRACE && tr) tr[Tx * 8 + 2] = clock64();
+  if (TRACE && threadIdx.x == 0) {
+    e.trace[(Tx + 1) * 8 + 2 * blockIdx.x] = clock64() - cyc_loop0;
+    e.trace[(Tx + 1) * 8 + 2 * blockIdx.x + 1] = cyc_poll;
+  }
+  if (unit && (lane & 15) == 0) e.mean[dir * H + jj] = hsum / (float)Tx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(e.bar) : "memory");
+    int v;
+    const long long t0 = clock64();
+    do {
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(e.bar) : "memory");
+      if (clock64() - t0 > (1ll << 32)) asm volatile("trap;");
+    } while (v < (int)(e.epoch * gridDim.x));
+  }
+  __syncthreads();
+  if (TRACE && tr) tr[Tx * 8 + 3] = clock64();
+  // all 2H means at once (C <= 2Hp floats = the two h buffers), then a warp per s0 output
+  float* msm = reinterpret_cast<float*>(h4buf);
+  for (int k = threadIdx.x; k < C; k += nthr) msm[k] = __ldcg(e.mean + k);
+  __syncthreads();
+  const int nwarps = nthr >> 5;
+  for (int w = warp; w < n_out; w += nwarps) {
+    if (bulk) mbar_wait(&wbar, 0);
+    const int o = o_first + w;
+    const float* wrow = wsm + w * C;
+    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+    if (bulk) {
+      for (int k = 4 * lane; k < C; k += 128) {
+        const float4 mv = *reinterpret_cast<const float4*>(msm + k), wv = *reinterpret_cast<const float4*>(wrow + k);
+        acc0 = fmaf(mv.x, wv.x, acc0);
+        acc1 = fmaf(mv.y, wv.y, acc1);
+        acc2 = fmaf(mv.z, wv.z, acc2);
+        acc3 = fmaf(mv.w, wv.w, acc3);
+      }
+    } else {
+      for (int k = lane; k < C; k += 32) acc0 = fmaf(msm[k], wrow[k], acc0);
+    }
+    float sacc = (acc0 + acc1) + (acc2 + acc3);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, off);
+    if (lane == 0) e.S0[o] = tanhf(sacc + e.b_init[o]);
+  }
+  if (TRACE && tr) {
+    tr[Tx * 8 + 4] = clock64();
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    tr[Tx * 8 + 6] = (long long)g;
+  }
+}
+
+template <int KI, bool TRACE>
+static void launch_recur2(const EncDev& e, int Tx, cudaStream_t st) {
+  EncDev ee = e;
+  void* args[] = {&ee, &Tx};
+  const size_t smem = (size_t)((e.H + 2 * e.NB - 1) / (2 * e.NB)) * 2 * e.H * sizeof(float) +
+                      (Tx <= kPinMax ? (size_t)Tx * (3 * e.UPC + 1) * sizeof(float) : 0);
+  static size_t attr = 0;  // > 48 KB of dynamic shared memory needs the opt-in
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_enc_recur2<KI, TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  CK(cudaLaunchCooperativeKernel((void*)k_enc_recur2<KI, TRACE>, dim3(2 * e.NB), dim3(32 * ((e.UPC + 1) / 2)), args,
+                                 smem, st));
+  note_launch();
+}
+
+template <int KI, bool TRACE>
 static void launch_recur(const EncDev& e, int Tx, cudaStream_t st) {
   EncDev ee = e;
   void* args[] = {&ee, &Tx};
-  const size_t smem = (size_t)((e.H + 2 * e.NB - 1) / (2 * e.NB)) * 2 * e.H * sizeof(float);
+  const size_t smem = (size_t)((e.H + 2 * e.NB - 1) / (2 * e.NB)) * 2 * e.H * sizeof(float) +
+                      (Tx <= kPinMax ? (size_t)Tx * (3 * e.UPC + 1) * sizeof(float) : 0);
   static size_t attr = 0;  // > 48 KB of dynamic shared memory needs the opt-in
   if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_enc_recur<KI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_enc_recur<KI, TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  CK(cudaLaunchCooperativeKernel((void*)k_enc_recur<KI>, dim3(2 * e.NB), dim3(32 * e.UPC), args, smem, st));
+  CK(cudaLaunchCooperativeKernel((void*)k_enc_recur<KI, TRACE>, dim3(2 * e.NB), dim3(32 * e.UPC), args, smem, st));
   note_launch();
 }
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
-  if (e.UPC > 16) throw NmtError(NMT_ERR_SHAPE, "encoder: UPC too large");
+  if (e.UPC > 14) throw NmtError(NMT_ERR_SHAPE, "encoder: UPC too large");
   // (the caller resets the tags and the barrier counter when the 16-bit epoch wraps)
+  static const bool v1 = getenv("NMT_ENC_V") && atoi(getenv("NMT_ENC_V")) == 1;  // (diagnostic: 1-unit warps)
+  if (v1 && 32 * e.UPC < e.Hp / 4) throw NmtError(NMT_ERR_SHAPE, "encoder: fewer threads than polled words");
+  if (!v1 && 2 * 32 * ((e.UPC + 1) / 2) < e.Hp / 4) throw NmtError(NMT_ERR_SHAPE, "encoder: > 2 polled words per thread");
   switch (e.Hp / 128) {
-    case 1: launch_recur<1>(e, Tx, st); break;
-    case 2: launch_recur<2>(e, Tx, st); break;
-    case 3: launch_recur<3>(e, Tx, st); break;
-    case 4: launch_recur<4>(e, Tx, st); break;
-    case 5: launch_recur<5>(e, Tx, st); break;
-    case 6: launch_recur<6>(e, Tx, st); break;
-    case 7: launch_recur<7>(e, Tx, st); break;
-    case 8: launch_recur<8>(e, Tx, st); break;
+    case 1: v1 ? (e.trace ? launch_recur<1, true>(e, Tx, st) : launch_recur<1, false>(e, Tx, st))
+            : (e.trace ? launch_recur2<1, true>(e, Tx, st) : launch_recur2<1, false>(e, Tx, st)); break;
+    case 2: v1 ? (e.trace ? launch_recur<2, true>(e, Tx, st) : launch_recur<2, false>(e, Tx, st))
+            : (e.trace ? launch_recur2<2, true>(e, Tx, st) : launch_recur2<2, false>(e, Tx, st)); break;
+    case 3: v1 ? (e.trace ? launch_recur<3, true>(e, Tx, st) : launch_recur<3, false>(e, Tx, st))
+            : (e.trace ? launch_recur2<3, true>(e, Tx, st) : launch_recur2<3, false>(e, Tx, st)); break;
+    case 4: v1 ? (e.trace ? launch_recur<4, true>(e, Tx, st) : launch_recur<4, false>(e, Tx, st))
+            : (e.trace ? launch_recur2<4, true>(e, Tx, st) : launch_recur2<4, false>(e, Tx, st)); break;
+    case 5: v1 ? (e.trace ? launch_recur<5, true>(e, Tx, st) : launch_recur<5, false>(e, Tx, st))
+            : (e.trace ? launch_recur2<5, true>(e, Tx, st) : launch_recur2<5, false>(e, Tx, st)); break;
+    case 6: v1 ? (e.trace ? launch_recur<6, true>(e, Tx, st) : launch_recur<6, false>(e, Tx, st))
+            : (e.trace ? launch_recur2<6, true>(e, Tx, st) : launch_recur2<6, false>(e, Tx, st)); break;
+    case 7: v1 ? (e.trace ? launch_recur<7, true>(e, Tx, st) : launch_recur<7, false>(e, Tx, st))
+            : (e.trace ? launch_recur2<7, true>(e, Tx, st) : launch_recur2<7, false>(e, Tx, st)); break;
+    case 8: v1 ? (e.trace ? launch_recur<8, true>(e, Tx, st) : launch_recur<8, false>(e, Tx, st))
+            : (e.trace ? launch_recur2<8, true>(e, Tx, st) : launch_recur2<8, false>(e, Tx, st)); break;
     default: throw NmtError(NMT_ERR_SHAPE, "encoder: dim_hid > 1024");
   }
 }

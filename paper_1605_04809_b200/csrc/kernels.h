@@ -51,21 +51,23 @@ struct StepDev {
   const int* row_dst;
   int V, H, Hp, Cp, E, Ep, ROp, maxout;
   __nv_bfloat16* A_s; int lda_s, lo_s;   // [R][sf*Hp]
-  float* G1;                             // [R][3Hp]
+  float* G1;                             // [ks_g1][R..][3Hp] split-K partials (stride ps_g1 floats)
   const float* Ex;                       // [V+1][3Hp]
   float* S1;                             // [R][Hp]
   __nv_bfloat16* X; int ldx, lo_x;       // [R][sf*(Hp+Cp+Hp)]  [s1 | c | s2]
-  float* Q;                              // [R][Cp]
+  float* Q;                              // [ks_q][R..][Cp]
   float* Cf;                             // [R][Cp]
   float* alpha_out; int alpha_ld;        // [R][max_src_len] (may be null)
-  float* G2;                             // [R][4Hp]
+  float* G2;                             // [..][R..][4Hp]: ks_g2[0] | [1] | [2] partials of gates | hUx | cWcx
   const float* b_nl;                     // [2Hp]
   const float* bx_nl;                    // [Hp]
-  float* RO;                             // [R][ROp]
+  float* RO;                             // [ks_ro][R..][ROp]
   const float* Eproj;                    // [V+1][ROp]
   __nv_bfloat16* A_t; int lda_t, lo_t;   // [R][sf*Ep]
   float4* part; int n_tiles;             // [R][2 * cpm] LSE partials of the vocabulary GEMM
   const int* cpm;                        // runs per m-tile (device, written by the GEMM)
+  int ks_g1, ks_q, ks_g2[3], ks_ro;      // split-K partial counts of the decoder GEMM outputs
+  int64_t ps_g1, ps_q, ps_g2, ps_ro;     // floats between consecutive partials
 };
 
 struct AttnCtx {
@@ -78,7 +80,9 @@ struct AttnCtx {
 
 struct EncDev {
   int H, Hp, NB, UPC, Vs;
-  int poll;              // h-exchange polling variant (diagnostic: NMT_ENC_POLL)
+  int hx_swap;           // diagnostic: direction -> exchange buffer mapping (NMT_ENC_HXSWAP)
+  int64_t hx_stride;     // u64 words between the two directions' exchange buffers (>= 2 rep Hp)
+  int hx_rep;            // replicas of the exchange buffer (readers spread over them: less L2 contention)
   unsigned epoch;        // 1..65535, per encode: tags and the tail barrier need no reset between calls
   long long* trace;      // diagnostic (NMT_ENC_TRACE): [Tx][8] clock64 phase stamps of CTA 0, thread 0
   const float* Uarr;     // [2][NB][3*UPC][Hp] recurrent weights per CTA (rows zero-padded to Hp)

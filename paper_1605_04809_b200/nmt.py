@@ -10,7 +10,7 @@ from typing import Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnmt.so")
+LIB_PATH = os.environ.get("NMT_LIB_PATH") or os.path.join(_HERE, "libnmt.so")  # (override: A/B builds)
 
 NMT_PREC_FP32CLASS = 0
 NMT_PREC_BF16 = 1

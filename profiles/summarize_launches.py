@@ -37,12 +37,16 @@ def main(path: str, out_json: str) -> None:
         agg[n][0] += t
         agg[n][1] += 1
     table = [{"kernel": n, "launches": c, "us": round(t, 2), "share": round(t / tot, 4)} for n, (t, c) in agg.items()]
-    res = {"source": path, "step_kernels": len(step), "step_us_serialised": round(tot, 1), "table": table}
+    res = {"source": path, "step_kernels": len(step), "step_us_serialised": round(tot, 1), "table": table,
+           "sequence": [[n, round(t, 2)] for n, t in step]}
     json.dump(res, open(out_json, "w"), indent=1)
     for r in sorted(table, key=lambda r: -r["us"]):
         print(f'{r["kernel"]:34s} {r["launches"]:3d} {r["us"]:9.2f} us  {100 * r["share"]:5.1f} %')
     print(f"step: {len(step)} launches, {tot:.1f} us serialised")
+    if "--seq" in sys.argv:
+        for n, t in step:
+            print(f"  {n:34s} {t:8.2f}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2])  # [--seq]: also print the step's launches in order

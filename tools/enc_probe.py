@@ -9,9 +9,7 @@ from paper_1605_04809_b200 import nmt
 d = synth.Dims(500, 1024, 50000, 100000, "maxout")
 M = nmt.Model(synth.params_bytes(d, synth.make_model(d, 2016)), precision="bf16")
 ri = nmt.STAGES.index("enc_recurrence")
-modes = [int(x) for x in os.environ.get("PROBE_MODES", "0").split(",")]
-for mode, Tx in [(m, t) for m in modes for t in ([1, 2, 5, 10, 25, 50, 64] if len(modes) == 1 else [10, 50])]:
-    os.environ["NMT_ENC_POLL"] = str(mode)
+for Tx in [1, 2, 5, 10, 25, 50, 64]:
     src = synth.make_source(d.vocab_src, Tx - 1, seed=Tx)
     for _ in range(3):
         M.encode(src).close()
@@ -21,4 +19,4 @@ for mode, Tx in [(m, t) for m in modes for t in ([1, 2, 5, 10, 25, 50, 64] if le
         M.encode(src).close()
     ms, cnt = M.profile_read()
     M.profile(0)
-    print(f"poll={mode} Tx={Tx:3d}  recurrence {1000 * ms[ri] / cnt[ri]:8.1f} us   pctx {1000 * ms[ri + 1] / cnt[ri + 1]:6.1f} us")
+    print(f"Tx={Tx:3d}  recurrence {1000 * ms[ri] / cnt[ri]:8.1f} us")

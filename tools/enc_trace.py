@@ -14,8 +14,5 @@ if "--plain" in sys.argv:  # (for ncu: no trace stamps)
     M.encode(src).close()
     sys.exit(0)
 os.environ["NMT_ENC_TRACE"] = "1"
-for mode in [0, 4]:
-    os.environ["NMT_ENC_POLL"] = str(mode)
-    print("poll mode", mode, flush=True)
-    for _ in range(3):
-        M.encode(src).close()
+for _ in range(3):
+    M.encode(src).close()
