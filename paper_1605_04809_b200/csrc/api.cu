@@ -1218,9 +1218,11 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
   }
   if (!stage_skipped(ST_ENC_PCTX)) {  // E7: pctx = ctx.Wc_att + b_att
     ProfScope p_(m, ST_ENC_PCTX);
-    GemmShape g = gemm_shape(len, nullptr, m->Cp, m->Cp, 0, true, m->Cp, m->Cp);
+    // the attention keys follow the step's precision: single-pass bf16 in NMT_PREC_BF16 (like the
+    // decoder's query GEMM), bf16x3 in NMT_PREC_FP32CLASS
+    GemmShape g = gemm_shape(len, nullptr, m->Cp, m->Cp, 0, m->split, m->Cp, m->Cp);
     {  // ~8 splits, none empty
-      const int nkb = 3 * m->Cp / 64, chunk = (nkb + 7) / 8;
+      const int nkb = g.passes * m->Cp / 64, chunk = (nkb + 7) / 8;
       g.ksplit = (nkb + chunk - 1) / chunk;
     }
     const size_t stride = (size_t)m->Tpad * m->Cp;

@@ -45,7 +45,11 @@ def test_tiny_encoder(tiny):
     ctx, pctx, s0 = M.encode(src).debug_encoder()
     ref = O.encode(om, src)
     assert np.max(np.abs(ctx - ref.ctx)) < 1e-4
-    assert np.max(np.abs(pctx - ref.pctx)) < 1e-4
+    if prec == "fp32class":
+        assert np.max(np.abs(pctx - ref.pctx)) < 1e-4
+    else:  # single-pass bf16 keys: both operands rounded to bf16 (2^-9 each), fp32 accumulation
+        bound = 2.0 ** -8 * (np.abs(ref.ctx) @ np.abs(p["decoder_Wc_att"])) + 1e-5
+        assert np.all(np.abs(pctx - ref.pctx) <= bound)
     assert np.max(np.abs(s0 - ref.s0)) < 1e-4
 
 
