@@ -100,6 +100,15 @@ typedef int64_t nmt_state;
 NMT_API nmt_status nmt_load(const char* params_path, const nmt_opts* opts, nmt_model** out);
 NMT_API nmt_status nmt_load_buffer(const void* buf /*[host]*/, size_t len, const nmt_opts* opts, nmt_model** out);
 NMT_API nmt_status nmt_model_dims(const nmt_model* m, nmt_dims* out);
+/* Checkpoint averaging (NMT-k-Avg: "the element-wise average of all model weights in
+ * the NMT ensembles", saved as a new model).  bufs[n] / lens[n] [host] are n params containers with
+ * IDENTICAL headers (dims, readout, array names and shapes; else NMT_ERR_SHAPE naming the first
+ * difference, NMT_ERR_FORMAT for a malformed container); out [host] receives a container of the
+ * same layout (out_len must equal lens[0], else NMT_ERR_INVALID_ARG) whose payload is, per element,
+ * fp32(sum_i x_i / n) with the sum taken in fp64 in member order on `device`.  Load it with
+ * nmt_load_buffer.  Synchronous; the caller owns every buffer.                                   */
+NMT_API nmt_status nmt_params_average(int32_t n, const void* const* bufs, const size_t* lens, int32_t device,
+                                      void* out, size_t out_len);
 /* Releases the caller's handle; the device memory goes when the last context of the model is freed
  * too (models and contexts may be freed in any order). */
 NMT_API void nmt_model_free(nmt_model* m);

@@ -283,6 +283,16 @@ def ensemble_combine(member_logp: Sequence[np.ndarray], weights: Sequence[float]
     return np.log((w * np.exp(L)).sum(axis=0))
 
 
+def average_params(members: Sequence[Dict[str, np.ndarray]]) -> Dict[str, np.ndarray]:
+    """Checkpoint averaging, NMT-k-Avg ("the element-wise average of all model weights
+    in the NMT ensembles and saved the resulting model"): every array is mean_i W_i, in float64."""
+    names = list(members[0].keys())
+    for m in members[1:]:
+        if list(m.keys()) != names or any(m[k].shape != members[0][k].shape for k in names):
+            raise ValueError("average_params: members differ in names or shapes")
+    return {k: np.mean(np.stack([np.asarray(m[k], np.float64) for m in members]), axis=0) for k in names}
+
+
 # ---------------------------------------------------------------------------------------------
 # ScoreBatch forest driver (Alg. 1) expressed on top of Session.score_batch:
 # one call per tree depth.  Used to pin the Fig. 1 structure (tests/golden/fig1_forest.txt).

@@ -363,6 +363,24 @@ void fill_i32(int* p, int64_t n, int v, cudaStream_t st) {
   CK_LAUNCH();
 }
 
+// checkpoint averaging: acc += x in fp64 (member order), out = fp32(acc / n)
+__global__ void k_avg_accum(double* __restrict__ acc, const float* __restrict__ x, int64_t n, int first) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) acc[i] = first ? (double)x[i] : acc[i] + (double)x[i];
+}
+__global__ void k_avg_finish(float* __restrict__ out, const double* __restrict__ acc, int64_t n, double members) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (float)(acc[i] / members);
+}
+void avg_accum(double* acc, const float* x, int64_t n, bool first, cudaStream_t st) {
+  k_avg_accum<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(acc, x, n, first ? 1 : 0);
+  CK_LAUNCH();
+}
+void avg_finish(float* out, const double* acc, int64_t n, int members, cudaStream_t st) {
+  k_avg_finish<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, acc, n, (double)members);
+  CK_LAUNCH();
+}
+
 // context (re)initialisation for nmt_encode, one launch: the hash table is emptied, the counters and
 // the root node 0 = (s0, BOS) (word -1, parent -1, state in slot 0, not stepped) are written
 __global__ void k_ctx_reset(CtxDev c, int64_t hcap) {

@@ -107,6 +107,8 @@ void pack_rows(const float* src, int ld_src, int rows, int K, __nv_bfloat16* dst
                cudaStream_t st);
 void to_panels(const __nv_bfloat16* src, int rows, int cols, __nv_bfloat16* dst, cudaStream_t st);
 void transpose_f32(const float* src, int K, int N, float* dst, int ld_dst, cudaStream_t st);
+void avg_accum(double* acc, const float* x, int64_t n, bool first, cudaStream_t st);
+void avg_finish(float* out, const double* acc, int64_t n, int members, cudaStream_t st);
 void ctx_reset(const CtxDev& c, int64_t hcap, cudaStream_t st);
 void fill_i32(int* p, int64_t n, int v, cudaStream_t st);
 void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st);

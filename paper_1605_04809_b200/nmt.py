@@ -26,7 +26,7 @@ EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "n
            "nmt_inject_states", "nmt_logprobs_full", "nmt_debug_encoder", "nmt_debug_intermediates",
            "nmt_test_gemm", "nmt_encode_dev", "nmt_inject_states_dev", "nmt_launch_count", "nmt_profile",
            "nmt_profile_read", "nmt_bench_gemm", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
-           "nmt_ensemble_free"]
+           "nmt_ensemble_free", "nmt_params_average"]
 
 
 N_STAGES = 19
@@ -37,6 +37,18 @@ STAGES = ["plan", "gather", "gemm_h1", "gru1", "gemm_q", "attention", "gemm_g2",
 
 def launch_count() -> int:
     return int(lib().nmt_launch_count())
+
+
+def params_average(blobs, device: int = 0) -> bytes:
+    """nmt_params_average: element-wise average of n params containers (NMT-k-Avg)."""
+    blobs = [bytes(b) for b in blobs]
+    n = len(blobs)
+    bufs = (C.c_char_p * n)(*blobs)
+    lens = (C.c_size_t * n)(*[len(b) for b in blobs])
+    out = C.create_string_buffer(len(blobs[0]) if n else 0)
+    _check(lib().nmt_params_average(n, C.cast(bufs, C.c_void_p), C.cast(lens, C.c_void_p), device, out,
+                                    len(blobs[0]) if n else 0))
+    return out.raw
 
 
 class NmtError(RuntimeError):
@@ -94,6 +106,7 @@ def lib() -> C.CDLL:
             "nmt_profile": (i32, [vp, i32]),
             "nmt_profile_read": (i32, [vp, vp, vp]),
             "nmt_bench_gemm": (i32, [i32, i32, i32, i32, i32, i32, i32, C.POINTER(C.c_float)]),
+            "nmt_params_average": (i32, [i32, vp, vp, i32, vp, C.c_size_t]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

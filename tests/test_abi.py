@@ -110,3 +110,22 @@ def test_scorebatch_forest_levels_fig1():
     lv = scorebatch.forest_levels(pairs)
     assert [len(l) for l in lv] == [4, 5, 3, 1]
     assert [w for _, w in lv[0]] == [0, 1, 1, 2] and [src[0] for src, _ in lv[0]] == [0, 0, 1, 1]
+
+
+def test_params_average_validates_before_device_work():
+    """nmt_params_average: headers must match; errors are named, no GPU needed."""
+    from paper_1605_04809_b200 import nmt
+    import synth
+    d = synth.TINY
+    a = synth.params_bytes(d, synth.make_model(d, 3))
+    other = synth.Dims(8, 16, 50, 50, "maxout")
+    b = synth.params_bytes(other, synth.make_model(other, 4))
+    with pytest.raises(nmt.NmtError) as e:
+        nmt.params_average([a, b])
+    assert e.value.name == "NMT_ERR_SHAPE" and "member 1" in str(e.value) and "readout" in str(e.value)
+    with pytest.raises(nmt.NmtError) as e:
+        nmt.params_average([a, a[:-4]])
+    assert e.value.name == "NMT_ERR_FORMAT"
+    with pytest.raises(nmt.NmtError) as e:
+        nmt.params_average([])
+    assert e.value.name == "NMT_ERR_INVALID_ARG"

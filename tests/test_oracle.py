@@ -359,6 +359,22 @@ def test_ensemble_combine_invariants():
     assert np.max(np.abs(a - ref)) < 1e-14
 
 
+def test_average_params_is_the_elementwise_mean():
+    """NMT-k-Avg: identities of the element-wise mean pin the oracle's averaging."""
+    d = synth.TINY
+    a, b, c = (synth.make_model(d, s) for s in (3, 4, 5))
+    one = O.average_params([a])
+    assert all(np.array_equal(one[k], a[k].astype(np.float64)) for k in a)          # k = 1: the model itself
+    same = O.average_params([a, a, a, a])
+    assert all(np.array_equal(same[k], a[k].astype(np.float64)) for k in a)         # identical members
+    two = O.average_params([a, b])
+    assert all(np.array_equal(two[k], (a[k].astype(np.float64) + b[k]) / 2) for k in a)  # exact in fp64
+    p1, p2 = O.average_params([a, b, c]), O.average_params([c, a, b])               # order independent
+    assert all(np.max(np.abs(p1[k] - p2[k])) <= 1e-15 * (1 + np.max(np.abs(p1[k]))) for k in a)
+    with pytest.raises(ValueError):
+        O.average_params([a, {k: v for k, v in b.items() if k != "decoder_U"}])
+
+
 # ------------------------------------------------------------------ Fig. 1 worked example (golden)
 def _read_fig1():
     hyps, info = {}, {}
