@@ -147,6 +147,17 @@ NMT_API nmt_status nmt_score_batch(nmt_ctx* c, int32_t n_parents, const nmt_stat
 NMT_API nmt_status nmt_score_batch_dev(nmt_ctx* c, int32_t n_parents, const int32_t* parents,
                                const int32_t* cand_offsets, int32_t n_cand, const int32_t* cand_words,
                                float* out_logprob, int32_t* out_child, int32_t* out_argmax);
+/* ---- beam step (pure-NMT beam search on the same step) ----
+ * For each parent (steps it first if it was never stepped), the k highest log-prob next words over
+ * the WHOLE target vocabulary.  parents [host] n_parents state handles; out_words [host] int32,
+ * out_logprob [host] float and out_child [host] state handles, each [n_parents * k], row-major by
+ * parent, descending log-prob (ties: lower word id).  The k words are chosen from the vocabulary
+ * GEMM's logits (a top-k epilogue, no logits in HBM), in the model's precision; their log-probs and
+ * child states are exactly those nmt_score_batch returns for the same (parent, word).
+ * 1 <= k <= NMT_TOPK_MAX (else NMT_ERR_INVALID_ARG); unknown parent -> NMT_ERR_BAD_STATE.        */
+#define NMT_TOPK_MAX 8
+NMT_API nmt_status nmt_beam_step(nmt_ctx* c, int32_t n_parents, const nmt_state* parents, int32_t k,
+                                 int32_t* out_words, float* out_logprob, nmt_state* out_child);
 /* ScoreBatch (Alg. 1) in one call.  Pair i expands hypothesis state hyp_states[i]
  * [host] by the phrase phrase_words[phrase_offsets[i] .. phrase_offsets[i+1]) [host] (1..16 words;
  * an empty phrase -> NMT_ERR_INVALID_ARG "empty expansion").  The library builds the

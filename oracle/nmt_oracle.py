@@ -253,10 +253,23 @@ class Session:
         out = step(self.m, self.c, n.s_in[None, :], [n.word])
         return log_softmax(out["z"][0])
 
+    def beam_step(self, parents: Sequence[int], k: int) -> Tuple[np.ndarray, np.ndarray]:
+        """Pure-NMT beam step: for each parent, the k words of
+        largest log p(w | parent) over the whole vocabulary -> (words [n, k], logp [n, k])."""
+        rows = [self.logprobs_full(int(p)) for p in parents]
+        words = np.array([topk_words(r, k) for r in rows], np.int64).reshape(len(rows), k)
+        return words, np.array([r[w] for r, w in zip(rows, words)]).reshape(len(rows), k)
+
     def intermediates(self, node: int) -> Dict[str, np.ndarray]:
         n = self.nodes[node]
         out = step(self.m, self.c, n.s_in[None, :], [n.word])
         return {k: v[0] for k, v in out.items()}
+
+
+def topk_words(logp: np.ndarray, k: int) -> np.ndarray:
+    """The k indices of largest value, by value descending then index ascending (a stable sort of
+    -logp): the definition of a beam step's expansion set."""
+    return np.argsort(-np.asarray(logp, np.float64), kind="stable")[:k]
 
 
 def score_sequence(m: Model, c: Context, words: Sequence[int], s: Optional[np.ndarray] = None,

@@ -157,6 +157,8 @@ struct nmt_model {
   __nv_bfloat16 *A_s = nullptr, *X = nullptr, *A_t = nullptr;
   float *G1 = nullptr, *S1 = nullptr, *Q = nullptr, *Cf = nullptr, *G2 = nullptr, *RO_buf = nullptr, *alpha = nullptr;
   float4* part = nullptr;
+  float2* topk_part = nullptr;  // [R][2 cpm][kTopK] beam-step top-k partials (allocated on first use)
+  int topk_rows = 0;
   int* lse_cpm = nullptr;  // [1] runs per m-tile of the last vocabulary GEMM
   int* inject_done = nullptr;  // [1] block counter of k_inject (reset by its last block)
   int *row_src = nullptr, *row_y = nullptr, *row_dst = nullptr, *row_node = nullptr;
@@ -258,6 +260,8 @@ void nmt_model::free_ws() {
   for (__nv_bfloat16** p : {&A_s, &X, &A_t}) dfree(*p);
   for (float** p : {&G1, &S1, &Q, &Cf, &G2, &RO_buf, &alpha, &out_logp, &in_s}) dfree(*p);
   dfree(part);
+  dfree(topk_part);
+  topk_rows = 0;
   for (int** p : {&lse_cpm, &inject_done, &row_src, &row_y, &row_dst, &row_node, &cand_k, &cand_hslot, &cflag, &pflag, &bcount, &snap,
                   &in_par, &in_off, &in_words,
                   &out_child, &out_amax})
@@ -1366,6 +1370,100 @@ void nmt_ctx_free(nmt_ctx* c) {
     m->pool.push_back(c);
   }
   model_release(m);
+}
+
+// Beam step (pure-NMT decoding on the same step):
+// 1. step every listed parent that is not yet stepped (planner with step_all, one run_step);
+// 2. rebuild the parents' vocabulary operand rows from the cached t and run the vocabulary GEMM
+//    with the top-k epilogue; merge the per-run lists into each row's k best words;
+// 3. score those words as candidates (planner + gather-dot, no new rows): log-probs and child ids
+//    are exactly what nmt_score_batch returns for the same (parent, word).
+nmt_status nmt_beam_step(nmt_ctx* c, int32_t np, const nmt_state* parents, int32_t k, int32_t* out_words,
+                         float* out_logp, nmt_state* out_child) {
+  if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");
+  if (np < 0) return fail(NMT_ERR_INVALID_ARG, "n_parents < 0");
+  if (k < 1 || k > kTopK) return fail(NMT_ERR_INVALID_ARG, "k outside [1, " + std::to_string(kTopK) + "]");
+  if (np > 0 && (!parents || !out_words || !out_logp || !out_child)) return fail(NMT_ERR_INVALID_ARG, "NULL array");
+  nmt_model* m = c->m;
+  if (k > m->V) return fail(NMT_ERR_INVALID_ARG, "k > vocab_tgt");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    cudaStream_t st = m->st;
+    if (c->stale) c->sync_counters();
+    for (int q = 0; q < np; ++q)
+      if (parents[q] < 0 || parents[q] >= c->n_nodes)
+        throw NmtError(NMT_ERR_BAD_STATE, "unknown state " + std::to_string(parents[q]) + " (parents[" +
+                                              std::to_string(q) + "])");
+    if (np == 0) return;
+    const int nc = np * k;
+    m->ensure_ws(np, nc);
+    c->ensure(nc, np);
+    if (m->topk_rows < m->R_cap) {  // partial lists: up to 2 x 148 runs per row
+      dfree(m->topk_part);
+      m->topk_part = dalloc<float2>((size_t)m->R_cap * 2 * kNumSMs * kTopK);
+      m->topk_rows = m->R_cap;
+    }
+    int* h = static_cast<int*>(m->pinned((size_t)(2 * np + 1) * 4 + (size_t)nc * 16 + CNT_N * 4 + 64));
+    int* hp = h;
+    int* ho = hp + np;
+    for (int q = 0; q < np; ++q) hp[q] = (int)parents[q];
+    for (int q = 0; q <= np; ++q) ho[q] = q * k;
+    CK(cudaMemcpyAsync(m->in_par, hp, (size_t)np * 4, cudaMemcpyHostToDevice, st));
+    const CtxDev cd = c->dev();
+    {  // 1. step the parents that are not yet stepped (no candidates: offsets all 0)
+      CK(cudaMemsetAsync(m->in_off, 0, (size_t)(np + 1) * 4, st));
+      PlanIO io = plan_io(m, np, 0, m->in_par, m->in_off, m->in_words);
+      io.step_all = 1;
+      {
+        ProfScope p_(m, ST_PLAN);
+        plan(cd, io, c->counters + CNT_R, st);
+      }
+      run_step(m, c, np);
+    }
+    {  // 2. top-k words of every parent row over the whole vocabulary
+      const StepDev d = step_view(m, c);
+      beam_gather(d, c->dev(), m->in_par, np, st);
+      GemmShape g = gemm_shape(np, nullptr, m->Vp, m->Ep, 0, m->split, m->Ep, m->Ep);
+      g.b_panel_rows = m->Vp;
+      gemm_topk_pair(m->tm_At, m->tm_Wo128, g, m->topk_part, m->V, st, m->lse_cpm);
+      topk_merge(m->topk_part, m->lse_cpm, np, k, m->in_words, st);
+    }
+    {  // 3. the k words as candidates: children interned, exact log-probs by the gather-dot
+      CK(cudaMemcpyAsync(m->in_off, ho, (size_t)(np + 1) * 4, cudaMemcpyHostToDevice, st));
+      const CtxDev cd3 = c->dev();  // (arena pointers may have changed in step 1)
+      const PlanIO io = plan_io(m, np, nc, m->in_par, m->in_off, m->in_words);
+      plan(cd3, io, c->counters + CNT_R, st);
+      gather_dot(cd3, io, m->W_o32, m->b_o, m->Ep, m->out_logp, m->out_child, nullptr, nullptr, st);
+    }
+    int* rw = ho + np + 1;
+    float* rl = reinterpret_cast<float*>(rw + nc);
+    int* rc = reinterpret_cast<int*>(rl + nc);
+    int* rcnt = rc + nc;
+    CK(cudaMemcpyAsync(rw, m->in_words, (size_t)nc * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rl, m->out_logp, (size_t)nc * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rc, m->out_child, (size_t)nc * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rcnt, c->counters, CNT_N * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (rcnt[CNT_ERR]) {
+      const int z = 0;
+      CK(cudaMemcpy(c->counters + CNT_ERR, &z, 4, cudaMemcpyHostToDevice));
+      throw NmtError(NMT_ERR_BAD_STATE, "device-side validation failed (flags " + std::to_string(rcnt[CNT_ERR]) + ")");
+    }
+    c->n_nodes = rcnt[CNT_NODES];
+    c->n_slots = rcnt[CNT_SLOTS];
+    // per parent: descending exact log-prob, ties -> lower word id (selection itself is by the GEMM logits)
+    std::vector<int> ord(k);
+    for (int q = 0; q < np; ++q) {
+      for (int i = 0; i < k; ++i) ord[i] = q * k + i;
+      std::sort(ord.begin(), ord.end(), [&](int a, int b) { return rl[a] > rl[b] || (rl[a] == rl[b] && rw[a] < rw[b]); });
+      for (int i = 0; i < k; ++i) {
+        out_words[q * k + i] = rw[ord[i]];
+        out_logp[q * k + i] = rl[ord[i]];
+        out_child[q * k + i] = rc[ord[i]];
+      }
+    }
+  });
 }
 
 nmt_status nmt_score_batch(nmt_ctx* c, int32_t np, const nmt_state* parents, const int32_t* off, const int32_t* words,

@@ -31,7 +31,7 @@
 namespace nmt {
 
 constexpr int BM = 128, BK = 64;
-constexpr int EPI_STORE = 0, EPI_LSE = 1;
+constexpr int EPI_STORE = 0, EPI_LSE = 1, EPI_TOPK = 2;  // TOPK: runs like LSE, keeps the kTopK best logits
 constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant, each owning half of the tile's columns
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
@@ -97,7 +97,7 @@ NMT_DEV Sched make_sched(const GemmShape& g, int M, int CM, int BN, int units) {
   s.num_m = (M + CM - 1) / CM;
   s.num_n = g.N / BN;
   s.nreg = g.nreg;
-  if (EPI == 1) {  // EPI_LSE
+  if (EPI >= 1) {  // EPI_LSE / EPI_TOPK: (m-tile, n-run) items
     s.cpm = max(1, units / max(1, s.num_m));
     s.chunk = (s.num_n + s.cpm - 1) / s.cpm;
     s.items = s.num_m * s.cpm;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int M = g.M_dev ? *g.M_dev : g.M;
   const int unit = PAIR ? blockIdx.x / 2 : blockIdx.x, nunits = PAIR ? gridDim.x / 2 : gridDim.x;
   const Sched sc = make_sched<EPI>(g, M, CM, BN, nunits);
-  if (EPI == EPI_LSE && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
+  if (EPI != EPI_STORE && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs of a pair)
@@ -272,6 +272,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       constexpr float LOG2E = 1.4426950408889634f;
       float mx = -INFINITY, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // LSE running state (per run)
       int am = 0;
+      float tv[EPI == EPI_TOPK ? kTopK : 1];  // TOPK: best logits of the run, descending (ties: lower column)
+      int ti[EPI == EPI_TOPK ? kTopK : 1];
+      if constexpr (EPI == EPI_TOPK) {
+#pragma unroll
+        for (int q = 0; q < kTopK; ++q) {
+          tv[q] = -INFINITY;
+          ti[q] = INT32_MAX;
+        }
+      }
       for (int n = itm.n0; n < itm.n1; ++n, ++it) {
         const int acc = it & 1;
         const uint32_t aph = (it >> 1) & 1;
@@ -309,6 +318,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (lane == 0) {
               tma_store_2d(&tmC, buf, colbase + c, row0);
               bulk_commit();
+            }
+          }
+        } else if constexpr (EPI == EPI_TOPK) {  // running top-kTopK of this warp's COLS logits of the row
+#pragma unroll 1
+          for (int c = 0; c < COLS; c += 32) {
+            float v[32];
+            tmem_ld32_nowait(tbase + c, v);
+            tmem_wait_ld_dep(v);
+            const int col0 = colbase + c;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (v[j] > tv[kTopK - 1] && col0 + j < ep.n_valid) {  // (rare once the list is full)
+                float x = v[j];
+                int xi = col0 + j;
+#pragma unroll
+                for (int q = 0; q < kTopK; ++q) {  // sorted insert; an equal value stays behind
+                  if (x > tv[q]) {
+                    const float tx = tv[q];
+                    const int txi = ti[q];
+                    tv[q] = x;
+                    ti[q] = xi;
+                    x = tx;
+                    xi = txi;
+                  }
+                }
+              }
             }
           }
         } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
@@ -369,6 +404,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (valid)
           ep.part[((size_t)grow * sc.cpm + itm.c) * 2 + half] =
               make_float4(mx, (s0 + s1) + (s2 + s3), __int_as_float(am), 0.f);
+      }
+      if constexpr (EPI == EPI_TOPK) {  // kTopK (logit, column) per (row, run, half)
+        if (valid) {
+          float2* dst = ep.topk + (((size_t)grow * sc.cpm + itm.c) * 2 + half) * kTopK;
+#pragma unroll
+          for (int q = 0; q < kTopK; ++q) dst[q] = make_float2(tv[q], __int_as_float(ti[q]));
+        }
       }
     }
   }
@@ -458,7 +500,7 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
     nt0 = nt1;
   }
   int grid = (PAIR ? 2 : 1) * tiles;
-  if (EPI == EPI_LSE || grid > kNumSMs) grid = kNumSMs;  // persistent (LSE runs use every unit)
+  if (EPI != EPI_STORE || grid > kNumSMs) grid = kNumSMs;  // persistent (LSE / TOPK runs use every unit)
   if (grid <= 0) return;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -545,6 +587,18 @@ void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, fl
 }
 
 // vocabulary GEMM + LSE on CTA pairs; `b_half` = tensor map of B with a 128-row box
+// vocabulary GEMM with the top-kTopK epilogue (beam step) on CTA pairs; partials [R][2 cpm][kTopK]
+void gemm_topk_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float2* topk, int n_valid,
+                    cudaStream_t st, int* cpm_out) {
+  gemm_validate(g, 256);
+  EpiParams ep{};
+  ep.topk = topk;
+  ep.n_valid = n_valid;
+  ep.n_tiles = g.N / 256;
+  ep.cpm_out = cpm_out;
+  launch<256, 6, EPI_TOPK, true>(a, b_half, b_half /*unused*/, g, ep, kNumSMs * BM, st);
+}
+
 void gemm_lse_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float4* part, int n_valid,
                    cudaStream_t st, int* cpm_out) {
   gemm_validate(g, 256);

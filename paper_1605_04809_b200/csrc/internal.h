@@ -82,7 +82,9 @@ struct EpiParams {
   size_t split_stride;
   int* cpm_out;  // EPI_LSE: runs per m-tile (partials per row = 2 * cpm), written by CTA 0
   int rows_per_split;  // EPI_STORE: row offset of split-K partial s is s * rows_per_split
+  float2* topk;        // EPI_TOPK: [R][2 cpm][kTopK] (logit, column) per (row, run, half), descending
 };
+constexpr int kTopK = 8;  // NMT_TOPK_MAX: words per row kept by the top-k vocabulary epilogue
 
 CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 void gemm_store(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float* out, int ldc, int out_rows,
@@ -94,6 +96,8 @@ void splitk_reduce(const float* part, int ksplit, size_t stride, int M, int N, i
                    cudaStream_t st, __nv_bfloat16* out16 = nullptr);
 void gemm_store_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float* out, int ldc,
                      int out_rows, const float* bias, int M_max, cudaStream_t st, size_t split_stride = 0);
+void gemm_topk_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float2* topk, int n_valid,
+                    cudaStream_t st, int* cpm_out);
 void gemm_lse_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float4* part, int n_valid,
                    cudaStream_t st, int* cpm_out);
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,

@@ -177,7 +177,7 @@ __global__ void k_plan_intern(CtxDev c, PlanIO io) {
     const int o0 = offs[i], o1 = offs[i + 1];
     if (o1 < o0) atomicOr(&c.counters[CNT_ERR], ERR_OFFSETS);
     if (p < 0 || p >= n_nodes) atomicOr(&c.counters[CNT_ERR], ERR_BAD_STATE);
-    else if (o1 > o0) atomicMin(&c.node_claim[p], i);
+    else if (o1 > o0 || io.step_all) atomicMin(&c.node_claim[p], i);
   }
 }
 
@@ -241,7 +241,8 @@ __global__ void __launch_bounds__(kPlanBlock) k_plan_flags(CtxDev c, PlanIO io, 
     const int n_nodes0 = c.counters[CNT_NODES];
     if (k < io.n_par) {
       const int p = io.parents[k];
-      f = p >= 0 && p < n_nodes0 && io.offsets[k + 1] > io.offsets[k] && c.node_slot[p] < 0 && c.node_claim[p] == k;
+      f = p >= 0 && p < n_nodes0 && (io.step_all || io.offsets[k + 1] > io.offsets[k]) && c.node_slot[p] < 0 &&
+          c.node_claim[p] == k;
       io.pflag[k] = f;
     }
   }
@@ -710,6 +711,32 @@ __global__ void k_gru2(StepDev d, float* __restrict__ S) {
   store_split4(d.X + (int64_t)r * d.ldx + d.Hp + d.Cp + j, d.lo_x, o);
 }
 
+// Row r, columns k..k+3 of the bf16 A operand of the vocabulary GEMM from t (zero past E): the two
+// bias columns (b_o folded into the GEMM as hi + lo) are 1 at E (and E+1 in single pass); in split
+// mode the lo half carries t - bf16(t) and 0 in the bias columns.
+NMT_DEV void write_vocab_operand(const StepDev& d, int r, int k, const float (&tp)[4]) {
+  const int E = d.E;
+  float4 av;
+  float* ap = &av.x;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int kk = k + i;
+    ap[i] = kk < E ? tp[i] : ((kk == E || (kk == E + 1 && d.lo_t == 0)) ? 1.f : 0.f);
+  }
+  __nv_bfloat16* at = d.A_t + (int64_t)r * d.lda_t + k;
+  if (k + 3 < E || d.lo_t == 0) {
+    store_split4(at, d.lo_t, av);
+  } else {  // split path, bias columns: hi = 1 at E, lo part of the bias columns = 0
+    store_split4(at, 0, av);
+    const float4 lo4 = make_float4(k < E ? tp[0] - __bfloat162float(__float2bfloat16_rn(tp[0])) : 0.f,
+                                   k + 1 < E ? tp[1] - __bfloat162float(__float2bfloat16_rn(tp[1])) : 0.f,
+                                   k + 2 < E ? tp[2] - __bfloat162float(__float2bfloat16_rn(tp[2])) : 0.f,
+                                   k + 3 < E ? tp[3] - __bfloat162float(__float2bfloat16_rn(tp[3])) : 0.f);
+    const uint32_t l01 = pk_bf16(lo4.x, lo4.y), l23 = pk_bf16(lo4.z, lo4.w);
+    *reinterpret_cast<uint2*>(at + d.lo_t) = make_uint2(l01, l23);
+  }
+}
+
 // D7: readout activation.  RO = c W_ctx + s2 W_l (GEMM), Ep[y] = e W_p + b_p + b_l + b_ctx.
 // Writes t (fp32) to the arena and the bf16 A operand of the vocabulary GEMM with the two
 // bias columns (b_o folded into the GEMM as hi + lo).  Thread per (row, 4 outputs).
@@ -746,28 +773,11 @@ __global__ void k_readout(StepDev d, float* __restrict__ T) {
       for (int i = 0; i < 4; ++i) t[i] = k + i < E ? tanhf(ld_sum(pre + k + i, d.ks_ro, d.ps_ro) + epr[k + i]) : 0.f;
     }
   }
-  float4 tv, av;  // tv -> arena (zero past E), av -> GEMM operand (bias columns at E, E+1)
-  float* tp = &tv.x;
-  float* ap = &av.x;
+  float tp[4];  // t -> arena (zero past E)
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int kk = k + i;
-    tp[i] = kk < E ? t[i] : 0.f;
-    ap[i] = kk < E ? t[i] : ((kk == E || (kk == E + 1 && d.lo_t == 0)) ? 1.f : 0.f);
-  }
-  st4(T + (int64_t)d.row_dst[r] * Ep + k, tv);
-  __nv_bfloat16* at = d.A_t + (int64_t)r * d.lda_t + k;
-  if (k + 3 < E || d.lo_t == 0) {
-    store_split4(at, d.lo_t, av);
-  } else {  // split path, bias columns: hi = 1 at E, lo part of the bias columns = 0
-    store_split4(at, 0, av);
-    const float4 lo4 = make_float4(k < E ? tp[0] - __bfloat162float(__float2bfloat16_rn(tp[0])) : 0.f,
-                                   k + 1 < E ? tp[1] - __bfloat162float(__float2bfloat16_rn(tp[1])) : 0.f,
-                                   k + 2 < E ? tp[2] - __bfloat162float(__float2bfloat16_rn(tp[2])) : 0.f,
-                                   k + 3 < E ? tp[3] - __bfloat162float(__float2bfloat16_rn(tp[3])) : 0.f);
-    const uint32_t l01 = pk_bf16(lo4.x, lo4.y), l23 = pk_bf16(lo4.z, lo4.w);
-    *reinterpret_cast<uint2*>(at + d.lo_t) = make_uint2(l01, l23);
-  }
+  for (int i = 0; i < 4; ++i) tp[i] = k + i < E ? t[i] : 0.f;
+  st4(T + (int64_t)d.row_dst[r] * Ep + k, make_float4(tp[0], tp[1], tp[2], tp[3]));
+  write_vocab_operand(d, r, k, tp);
 }
 
 // D9a: combine the per-run (max, sum, argmax) partials of each row in fixed column order.
@@ -959,6 +969,78 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
     case EW_READOUT: launch_pdl(k_readout, ge, 256, 0, st, d, T); break;
     case EW_FINALIZE: launch_pdl(k_finalize, (R_max * 32 + 255) / 256, 256, 0, st, d, logZ, amax); break;
   }
+  CK_LAUNCH();
+}
+
+// Beam step: the vocabulary operand rows of already-stepped parents, rebuilt
+// from the t cached in the arena (bit-identical to what k_readout wrote when they were stepped).
+__global__ void k_beam_gather(StepDev d, CtxDev c, const int* __restrict__ parents, int n) {
+  pdl_enter();
+  const int E4 = d.Ep / 4;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = idx / E4, k = (idx % E4) * 4;
+  if (r >= n) return;
+  const int p = parents[r];
+  const int slot = (p >= 0) ? c.node_slot[p] : -1;
+  float tp[4] = {0.f, 0.f, 0.f, 0.f};
+  if (slot >= 0) {
+    const float4 t4 = ld4(c.T + (int64_t)slot * d.Ep + k);
+    tp[0] = t4.x; tp[1] = t4.y; tp[2] = t4.z; tp[3] = t4.w;
+  } else if (k == 0) {
+    atomicOr(&c.counters[CNT_ERR], ERR_BAD_STATE);
+  }
+  write_vocab_operand(d, r, k, tp);
+}
+// merge the 2 cpm (logit, column) lists of each row into its k best columns: descending logit,
+// ties -> lower column (the order a single sorted scan of the row would give).  Warp per row.
+__global__ void k_topk_merge(const float2* __restrict__ topk, const int* __restrict__ cpm_dev, int n, int k,
+                             int* __restrict__ out_words) {
+  pdl_enter();
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const int nc = 2 * (*cpm_dev) * kTopK;
+  const float2* L = topk + (size_t)row * nc;
+  int taken[kTopK];
+#pragma unroll
+  for (int q = 0; q < kTopK; ++q) taken[q] = -1;
+  for (int q = 0; q < k; ++q) {
+    float bv = -INFINITY;
+    int bi = INT32_MAX;
+    for (int i = lane; i < nc; i += 32) {
+      const float2 e = L[i];
+      const int col = __float_as_int(e.y);
+      bool used = false;
+#pragma unroll
+      for (int u = 0; u < kTopK; ++u) used |= (u < q && taken[u] == col);
+      if (!used && col != INT32_MAX && (e.x > bv || (e.x == bv && col < bi))) {
+        bv = e.x;
+        bi = col;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kTopK; ++u)
+      if (u == q) taken[u] = bi;
+    if (lane == 0) out_words[(size_t)row * k + q] = bi == INT32_MAX ? 0 : bi;
+  }
+}
+void beam_gather(const StepDev& d, const CtxDev& c, const int* parents, int n, cudaStream_t st) {
+  const int64_t tot = (int64_t)n * (d.Ep / 4);
+  if (tot <= 0) return;
+  launch_pdl(k_beam_gather, (unsigned)((tot + 255) / 256), 256, 0, st, d, c, parents, n);
+  CK_LAUNCH();
+}
+void topk_merge(const float2* topk, const int* cpm_dev, int n, int k, int* out_words, cudaStream_t st) {
+  if (n <= 0) return;
+  launch_pdl(k_topk_merge, (unsigned)((n * 32 + 255) / 256), 256, 0, st, topk, cpm_dev, n, k, out_words);
   CK_LAUNCH();
 }
 

@@ -41,6 +41,7 @@ struct PlanIO {
   int* pflag;           // [n_par] parent must be stepped
   int* bcount;          // [blocks] per-block flag counts
   int* snap;            // [2] node / slot counters at plan start
+  int step_all;         // 1: step every listed parent not yet stepped, candidates or not (beam step)
 };
 
 // Decoder-step workspace view (rows r < *R).
@@ -109,6 +110,8 @@ void to_panels(const __nv_bfloat16* src, int rows, int cols, __nv_bfloat16* dst,
 void transpose_f32(const float* src, int K, int N, float* dst, int ld_dst, cudaStream_t st);
 void avg_accum(double* acc, const float* x, int64_t n, bool first, cudaStream_t st);
 void avg_finish(float* out, const double* acc, int64_t n, int members, cudaStream_t st);
+void beam_gather(const StepDev& d, const CtxDev& c, const int* parents, int n, cudaStream_t st);
+void topk_merge(const float2* topk, const int* cpm_dev, int n, int k, int* out_words, cudaStream_t st);
 void ctx_reset(const CtxDev& c, int64_t hcap, cudaStream_t st);
 void fill_i32(int* p, int64_t n, int v, cudaStream_t st);
 void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st);

@@ -26,7 +26,7 @@ EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "n
            "nmt_inject_states", "nmt_logprobs_full", "nmt_debug_encoder", "nmt_debug_intermediates",
            "nmt_test_gemm", "nmt_encode_dev", "nmt_inject_states_dev", "nmt_launch_count", "nmt_profile",
            "nmt_profile_read", "nmt_bench_gemm", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
-           "nmt_ensemble_free", "nmt_params_average"]
+           "nmt_ensemble_free", "nmt_params_average", "nmt_beam_step"]
 
 
 N_STAGES = 19
@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
             "nmt_profile_read": (i32, [vp, vp, vp]),
             "nmt_bench_gemm": (i32, [i32, i32, i32, i32, i32, i32, i32, C.POINTER(C.c_float)]),
             "nmt_params_average": (i32, [i32, vp, vp, i32, vp, C.c_size_t]),
+            "nmt_beam_step": (i32, [vp, i32, vp, i32, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -201,6 +202,17 @@ class Context:
         _check(lib().nmt_score_batch(self._h, len(par), _ptr(par), _ptr(off), _ptr(words), _ptr(logp), _ptr(child),
                                      _ptr(am)))
         return logp, child, am
+
+    def beam_step(self, parents, k: int) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """nmt_beam_step: the k best next words of each parent over the whole vocabulary
+        -> (words [n, k], logprob [n, k], child [n, k]), descending log-prob per parent."""
+        par = _c(parents, np.int64)
+        n = len(par)
+        words = np.empty((n, k), np.int32)
+        logp = np.empty((n, k), np.float32)
+        child = np.empty((n, k), np.int64)
+        _check(lib().nmt_beam_step(self._h, n, _ptr(par), k, _ptr(words), _ptr(logp), _ptr(child)))
+        return words, logp, child
 
     def score_batch_dev(self, n_parents: int, parents_ptr: int, offsets_ptr: int, n_cand: int, words_ptr: int,
                         logp_ptr: int, child_ptr: int, argmax_ptr: Optional[int] = None) -> None:

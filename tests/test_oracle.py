@@ -375,6 +375,34 @@ def test_average_params_is_the_elementwise_mean():
         O.average_params([a, {k: v for k, v in b.items() if k != "decoder_U"}])
 
 
+def test_topk_words_definition():
+    """Beam expansion set (NEXT-3): brute force over every k-subset on tiny rows, ties -> lower id."""
+    rng = np.random.default_rng(3)
+    for trial in range(30):
+        v = rng.integers(0, 4, size=7).astype(np.float64)  # many ties
+        k = int(rng.integers(1, 7))
+        got = list(O.topk_words(v, k))
+        # brute force: the lexicographically smallest (by -value, index) k-subset ordering
+        best = sorted(range(7), key=lambda i: (-v[i], i))[:k]
+        assert got == best
+        assert all(v[got[i]] >= v[got[i + 1]] for i in range(k - 1))
+        worst_in = min(v[i] for i in got)
+        assert all(v[j] <= worst_in for j in set(range(7)) - set(got))   # nothing outside beats the set
+    v = rng.standard_normal(50)
+    assert O.topk_words(v, 1)[0] == int(np.argmax(v))                    # k = 1 is the argmax
+    assert list(O.topk_words(v, 50)) == list(np.argsort(-v))             # k = V is the full ranking
+
+
+def test_beam_step_matches_full_rows():
+    d = synth.TINY
+    p = synth.make_model(d, 7)
+    sess = O.Session(O.Model(d, p), synth.make_source(d.vocab_src, 4, seed=1))
+    w, lp = sess.beam_step([sess.root], 5)
+    full = sess.logprobs_full(sess.root)
+    assert list(w[0]) == list(np.argsort(-full, kind="stable")[:5])
+    assert np.allclose(lp[0], np.sort(full)[::-1][:5], rtol=0, atol=1e-15)
+
+
 # ------------------------------------------------------------------ Fig. 1 worked example (golden)
 def _read_fig1():
     hyps, info = {}, {}
