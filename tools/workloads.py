@@ -7,6 +7,11 @@
   sweep  C2 model (V_t 100k): hypothesis batch-size sweep R in 64..16384 (x3 candidates) through the
          device-resident C ABI - word-scores/s and the vocabulary GEMM's TFLOP/s / fraction of the
          measured bf16 peak per R (HBM-bound W_o stream at small R, tensor-bound at large R).
+  beam   C2 model: nmt_beam_step over R fresh injected parents, k = 8 -
+         expansions/s (R x k per call, host C ABI, synchronised) for R in 256..4096.
+  avg    NMT-k-Avg vs the k-ensemble ("four times smaller and four times faster"):
+         one C2 batch (R = 1024 x 3) scored by 4 member models in turn (+ log-linear combine on
+         the host) vs by their nmt_params_average model, on one GPU.
 Prints one JSON line per measurement point.
 """
 import argparse
@@ -122,12 +127,74 @@ def sweep(a):
               flush=True)
 
 
+def beam(a):
+    from paper_1605_04809_b200 import nmt
+    d = synth.Dims(500, 1024, 50000, 100000, a.readout)
+    M = nmt.Model(synth.params_bytes(d, synth.make_model(d, 2016)), precision=a.precision)
+    src = synth.make_source(d.vocab_src, 49, seed=1)
+    for R in [256, 1024, 4096]:
+        s, y = synth.make_states(R, d.dim_hid, d.vocab_tgt, seed=R)
+        ctx = M.encode(src)
+        for _ in range(3):  # warm-up (arena growth)
+            ctx.beam_step(ctx.inject_states(s, y), 8)
+        ts = []
+        for _ in range(a.iters):
+            hy = ctx.inject_states(s, y)
+            t0 = time.perf_counter()
+            ctx.beam_step(hy, 8)
+            ts.append(time.perf_counter() - t0)
+        ctx.close()
+        t = float(np.median(ts))
+        print(json.dumps({"workload": "beam", "R": R, "k": 8, "precision": a.precision, "ms_per_call": 1000 * t,
+                          "expansions_per_s": R * 8 / t, "rows_per_s": R / t,
+                          "timing": "host wall clock around nmt_beam_step (parents injected outside), median"}),
+              flush=True)
+
+
+def avg(a):
+    from paper_1605_04809_b200 import nmt
+    d = synth.Dims(500, 1024, 50000, 100000, a.readout)
+    blobs = [synth.params_bytes(d, synth.make_model(d, 2016 + i)) for i in range(4)]
+    members = [nmt.Model(b, precision=a.precision) for b in blobs]
+    avg_model = nmt.Model(nmt.params_average(blobs), precision=a.precision)
+    src = synth.make_source(d.vocab_src, 49, seed=1)
+    s, y = synth.make_states(1024, d.dim_hid, d.vocab_tgt, seed=5)
+    off, w = synth.make_candidates(1024, 3, d.vocab_tgt, seed=6)
+
+    def run(models):
+        out = []
+        for M in models:
+            ctx = M.encode(src)
+            lp, _, _ = ctx.score_batch(ctx.inject_states(s, y), off, w, with_argmax=False)
+            ctx.close()
+            out.append(lp)
+        return np.mean(np.stack(out), axis=0) if len(out) > 1 else out[0]  # log-linear, lambda = 1/4
+    for _ in range(2):
+        run(members)
+        run([avg_model])
+    te, ta = [], []
+    for _ in range(a.iters):
+        t0 = time.perf_counter()
+        run(members)
+        te.append(time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        run([avg_model])
+        ta.append(time.perf_counter() - t0)
+    e, v = float(np.median(te)), float(np.median(ta))
+    print(json.dumps({"workload": "avg", "members": 4, "precision": a.precision,
+                      "ensemble_ms_per_batch": 1000 * e, "average_ms_per_batch": 1000 * v,
+                      "speedup_average_vs_ensemble": e / v,
+                      "batch": "1 source (Tx=50) + 1024 injected parents x 3 words, host C ABI, one GPU",
+                      "note": "PAPER.md:305 reports the averaged model four times faster than the 4-ensemble"}),
+          flush=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["c3", "sweep"])
+    ap.add_argument("what", choices=["c3", "sweep", "beam", "avg"])
     ap.add_argument("--precision", default="bf16")
     ap.add_argument("--readout", default="tanh")
     ap.add_argument("--sentences", type=int, default=10)
     ap.add_argument("--iters", type=int, default=10)
     a = ap.parse_args()
-    c3(a) if a.what == "c3" else sweep(a)
+    {"c3": c3, "sweep": sweep, "beam": beam, "avg": avg}[a.what](a)
