@@ -168,6 +168,9 @@ struct nmt_model {
   float* out_logp = nullptr;
   int *out_child = nullptr, *out_amax = nullptr;
   float* in_s = nullptr;
+  int* in_y = nullptr;              // [R_cap] y_prev staging of nmt_inject_states
+  cudaStream_t cst = nullptr;       // copy stream of nmt_inject_states (overlaps the encoder)
+  cudaEvent_t inj_copy_ev = nullptr, inj_done_ev = nullptr;
   CUtensorMap tm_As, tm_X, tm_At;
   // ScoreBatch forest workspace (nmt_score_forest)
   int* fws_i = nullptr;
@@ -221,6 +224,13 @@ static void free_all_model(nmt_model* m) {
   m->pin = nullptr;
   if (m->pin2_ev) cudaEventDestroy(m->pin2_ev);
   m->pin2_ev = nullptr;
+  if (m->cst) {
+    cudaStreamSynchronize(m->cst);
+    cudaStreamDestroy(m->cst);
+    cudaEventDestroy(m->inj_copy_ev);
+    cudaEventDestroy(m->inj_done_ev);
+    m->cst = nullptr;
+  }
 }
 
 struct ProfScope {  // CUDA events around one stage's launches on the model stream
@@ -258,7 +268,9 @@ nmt_model::~nmt_model() {
 
 void nmt_model::free_ws() {
   for (__nv_bfloat16** p : {&A_s, &X, &A_t}) dfree(*p);
+  if (cst) cudaStreamSynchronize(cst);  // (a copy may still target in_s / in_y)
   for (float** p : {&G1, &S1, &Q, &Cf, &G2, &RO_buf, &alpha, &out_logp, &in_s}) dfree(*p);
+  dfree(in_y);
   dfree(part);
   dfree(topk_part);
   topk_rows = 0;
@@ -315,6 +327,7 @@ void nmt_model::ensure_ws(int R, int NC) {
   in_off = dalloc<int>(R_cap + 1);
   out_amax = dalloc<int>(R_cap);
   in_s = dalloc<float>((size_t)R_cap * H);
+  in_y = dalloc<int>(R_cap);
   cand_k = dalloc<int>(NC_cap);
   cand_hslot = dalloc<int>(NC_cap);
   cflag = dalloc<int>(NC_cap);
@@ -1778,23 +1791,30 @@ nmt_status nmt_inject_states(nmt_ctx* c, int32_t n, const float* s, const int32_
     if (c->stale) c->sync_counters();
     m->ensure_ws(n, n);
     c->ensure(n, n);
-    // (in_s holds R_cap x H floats; the y and ids use the candidate scratch)
-    // copy straight from the caller's arrays; for page-locked sources the call waits for the DMA
-    // only (not for the kernel), so the caller may reuse its buffers on return - pageable sources
-    // are staged synchronously by cudaMemcpyAsync itself
-    if (!m->pin2_ev) CK(cudaEventCreateWithFlags(&m->pin2_ev, cudaEventDisableTiming));
-    CK(cudaMemcpyAsync(m->in_s, s, (size_t)n * m->H * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(m->in_words, y, (size_t)n * 4, cudaMemcpyHostToDevice, st));
-    cudaPointerAttributes pa;
-    if (cudaPointerGetAttributes(&pa, s) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
-      CK(cudaEventRecord(m->pin2_ev, st));
-      CK(cudaEventSynchronize(m->pin2_ev));
+    // The upload runs on a copy stream: it depends only on the previous inject kernel having read
+    // the staging buffers, not on the work queued before it (e.g. the encoder of this sentence), so
+    // the DMA overlaps that work.  Copies come straight from the caller's arrays; for page-locked
+    // sources the call waits for the DMA only (not for any kernel), so the caller may reuse its
+    // buffers on return - pageable sources are staged synchronously by cudaMemcpyAsync itself.
+    if (!m->cst) {
+      CK(cudaStreamCreateWithFlags(&m->cst, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&m->inj_copy_ev, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&m->inj_done_ev, cudaEventDisableTiming));
     }
+    CK(cudaStreamWaitEvent(m->cst, m->inj_done_ev, 0));
+    CK(cudaMemcpyAsync(m->in_s, s, (size_t)n * m->H * 4, cudaMemcpyHostToDevice, m->cst));
+    CK(cudaMemcpyAsync(m->in_y, y, (size_t)n * 4, cudaMemcpyHostToDevice, m->cst));
+    CK(cudaEventRecord(m->inj_copy_ev, m->cst));
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, s) == cudaSuccess && pa.type == cudaMemoryTypeHost)
+      CK(cudaEventSynchronize(m->inj_copy_ev));
     cudaGetLastError();  // (clear a possible "invalid value" from cudaPointerGetAttributes)
+    CK(cudaStreamWaitEvent(st, m->inj_copy_ev, 0));
     {
       ProfScope p_(m, ST_INJECT);
-      inject(c->dev(), n, m->in_s, m->in_words, m->out_child, m->inject_done, st);
+      inject(c->dev(), n, m->in_s, m->in_y, m->out_child, m->inject_done, st);
     }
+    CK(cudaEventRecord(m->inj_done_ev, st));
     // injected nodes take the next n ids in order; the host mirror is exact here (synced above when
     // stale), so no device round trip is needed
     for (int i = 0; i < n; ++i) out[i] = c->n_nodes + i;
