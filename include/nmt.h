@@ -96,7 +96,8 @@ typedef int64_t nmt_state;
  *   then the arrays row-major float32 LE in header order.  Every required name must be present
  *   (NMT_ERR_MISSING_PARAM), shapes must agree with dims (NMT_ERR_SHAPE), the payload length must
  *   be exact (NMT_ERR_FORMAT).  Weights are re-laid out on the device at load (bf16 K-major
- *   tiles, hi/lo splits, precomputed embedding projections); the host copy is not kept.        */
+ *   tiles, hi/lo splits, precomputed embedding projections); the model also keeps the container
+ *   bytes on the host so that nmt_save_params can write them back unchanged.                   */
 NMT_API nmt_status nmt_load(const char* params_path, const nmt_opts* opts, nmt_model** out);
 NMT_API nmt_status nmt_load_buffer(const void* buf /*[host]*/, size_t len, const nmt_opts* opts, nmt_model** out);
 NMT_API nmt_status nmt_model_dims(const nmt_model* m, nmt_dims* out);
@@ -109,6 +110,24 @@ NMT_API nmt_status nmt_model_dims(const nmt_model* m, nmt_dims* out);
  * nmt_load_buffer.  Synchronous; the caller owns every buffer.                                   */
 NMT_API nmt_status nmt_params_average(int32_t n, const void* const* bufs, const size_t* lens, int32_t device,
                                       void* out, size_t out_len);
+/* Writes the model's params container to `path`, byte-identical to the container it was loaded or
+ * generated from (SPEC.md:192 round trip).  NMT_ERR_IO if the file cannot be written.           */
+NMT_API nmt_status nmt_save_params(const nmt_model* m, const char* path);
+/* The same bytes into out [host]: out == NULL -> *len = size needed; *len < size ->
+ * NMT_ERR_CAPACITY (and *len = size).                                                           */
+NMT_API nmt_status nmt_params_bytes(const nmt_model* m, void* out, size_t* len);
+/* Seeded synthetic model (SURVEY §8(d) generator): embeddings N(0,1), linear maps
+ * N(0, 1/fan_in), orthogonal recurrent blocks (Haar, DL4MT ortho_weight), biases N(0, 0.1^2),
+ * U_att N(0, (2/sqrt(2H))^2), W_o scaled so that std(t.W_o) ~ logit_std, b_o[w] = -ln(w+1).
+ * Counter-based draws (splitmix64 + Box-Muller, keyed by seed and array name): the same
+ * (dims, seed, logit_std) always gives the same bytes; it does NOT reproduce synth/'s numpy
+ * stream.  nmt_random_params is host-only (no GPU needed): out == NULL -> *len = size; otherwise
+ * writes the container (NMT_ERR_CAPACITY if *len is too small).  nmt_create_random = generate +
+ * nmt_load_buffer (dims->max_src_len is used when opts->max_src_len == 0).  Bad dims or
+ * logit_std <= 0 -> NMT_ERR_INVALID_ARG.                                                         */
+NMT_API nmt_status nmt_random_params(const nmt_dims* d, uint64_t seed, float logit_std, void* out, size_t* len);
+NMT_API nmt_status nmt_create_random(const nmt_dims* d, uint64_t seed, float logit_std, const nmt_opts* opts,
+                                     nmt_model** out);
 /* Releases the caller's handle; the device memory goes when the last context of the model is freed
  * too (models and contexts may be freed in any order). */
 NMT_API void nmt_model_free(nmt_model* m);
@@ -123,6 +142,16 @@ NMT_API nmt_state nmt_root(const nmt_ctx* c);
 /* Same with src_ids [dev] (e.g. resident in HBM); token ids are validated on the device and an
  * out-of-range id is reported by nmt_ctx_check().  Asynchronous on the model stream.            */
 NMT_API nmt_status nmt_encode_dev(nmt_model* m, const int32_t* src_ids, int32_t len, nmt_ctx** out);
+/* n sources at once (one context per sentence): ids [host] holds the
+ * sentences back to back, offsets [host, n+1] (offsets[0] = 0, non-decreasing) delimits them, and
+ * outs[n] [host] receives one context per sentence in input order.  The recurrences of all
+ * sentences advance together, one tensor-core GEMM per time step over the sentences still running
+ * (tensor-bound when hundreds of sentences are batched); results agree with
+ * nmt_encode within the precision's tolerance, not bit for bit.  Errors as nmt_encode, checked for
+ * every sentence before any work (the message names the sentence); on error no context is created.
+ * n == 0 is a no-op.  Asynchronous on the model stream.                                         */
+NMT_API nmt_status nmt_encode_batch(nmt_model* m, int32_t n, const int32_t* ids, const int32_t* offsets,
+                                    nmt_ctx** outs);
 /* Releases the context; its arena is kept by the model for reuse by a later nmt_encode. */
 NMT_API void nmt_ctx_free(nmt_ctx* c);
 
@@ -147,6 +176,14 @@ NMT_API nmt_status nmt_score_batch(nmt_ctx* c, int32_t n_parents, const nmt_stat
 NMT_API nmt_status nmt_score_batch_dev(nmt_ctx* c, int32_t n_parents, const int32_t* parents,
                                const int32_t* cand_offsets, int32_t n_cand, const int32_t* cand_words,
                                float* out_logprob, int32_t* out_child, int32_t* out_argmax);
+/* Several sentences in one call: parent k is a state of ctx_per_parent[k] [host,
+ * n_parents; all contexts of one model, else NMT_ERR_INVALID_ARG]; every other argument, output
+ * and error as nmt_score_batch, in input order (child handles belong to their parent's context).
+ * Parents are grouped by context in first-appearance order; the groups' steps are issued back to
+ * back on the model stream with one host synchronisation for the whole call.                     */
+NMT_API nmt_status nmt_score_batch_multi(int32_t n_parents, nmt_ctx* const* ctx_per_parent, const nmt_state* parents,
+                                         const int32_t* cand_offsets, const int32_t* cand_words, float* out_logprob,
+                                         nmt_state* out_child, int32_t* out_argmax);
 /* ---- beam step (pure-NMT beam search on the same step) ----
  * For each parent (steps it first if it was never stepped), the k highest log-prob next words over
  * the WHOLE target vocabulary.  parents [host] n_parents state handles; out_words [host] int32,
@@ -205,6 +242,14 @@ NMT_API nmt_status nmt_debug_encoder(nmt_ctx* c, float* ctx, float* pctx, float*
  * t[E], logZ[1], argmax[1]; any pointer may be NULL [host]                                       */
 NMT_API nmt_status nmt_debug_intermediates(nmt_ctx* c, nmt_state node, float* s1, float* alpha, float* ctxv,
                                    float* s2, float* t, float* logZ, int32_t* argmax);
+/* The vocabulary stage alone (D8 + D9, SURVEY §8(b) "minimum slice"): R rows of readout outputs
+ * t [host, R x dim_emb] -> out_logZ [host, R] = logsumexp_v(t.W_o + b_o), out_argmax [host, R or
+ * NULL] (lowest id on ties) and, for the CSR candidates cand_offsets [R+1] / cand_words [N_cand],
+ * out_logprob [host, N_cand] = t.W_o[:,w] + b_o[w] - logZ.  Same kernels as a step (vocabulary
+ * GEMM with the fused log-sum-exp, finalize, gather-dot), run on a scratch context.             */
+NMT_API nmt_status nmt_debug_vocab(nmt_model* m, int32_t R, const float* t, const int32_t* cand_offsets,
+                                   const int32_t* cand_words, float* out_logprob, float* out_logZ,
+                                   int32_t* out_argmax);
 /* GEMM engine unit test: C[M x N] = A[M x K] . B[K x N] (+ bias[N]) with the tcgen05 kernel;
  * split = 1 -> bf16x3.  A, B, bias, C are [host] fp32 row-major; N % 128 == 0, K % 64 == 0.     */
 NMT_API nmt_status nmt_test_gemm(int32_t M, int32_t N, int32_t K, int32_t split, const float* A, const float* B,

@@ -151,6 +151,21 @@ struct nmt_model {
   unsigned enc_epoch = 0;      // encodes since the last reset of hbuf / bar (k_enc_recur tags)
   int* d_src = nullptr;
   CUtensorMap tm_ctxbf;
+  // batched encoder (nmt_encode_batch): block-diagonal recurrent operand [6Hp][4Hp] (rows fwd r|u|x,
+  // bwd r|u|x; K = [h_fwd | h_bwd], lo at +2Hp) and W_init [Hp][2Cp] (K = ctx, lo at +Cp), bf16
+  __nv_bfloat16* W_encb = nullptr;
+  __nv_bfloat16* W_initb = nullptr;
+  CUtensorMap tm_Wencb, tm_Winitb;
+  struct EncBatchWS {
+    int n_cap = 0, tok_cap = 0;
+    size_t g_floats = 0, p_floats = 0;
+    __nv_bfloat16 *A = nullptr, *ctxbf = nullptr, *Am = nullptr;
+    float *h = nullptr, *G = nullptr, *P = nullptr;
+    int* ints = nullptr;       // src | tok_off | row_b
+    void* blob = nullptr;      // pointer tables | CtxDev[] | hcaps[]
+    size_t ints_cap = 0, blob_cap = 0;
+    CUtensorMap tm_A, tm_ctxbf, tm_Am;
+  } eb;
   // step workspace
   int R_cap = 0, NC_cap = 0;
   int P_rows = 0;  // rows of G1 / Q / G2 / RO_buf: room for the split-K partials of a step
@@ -182,6 +197,7 @@ struct nmt_model {
   size_t pin_bytes = 0;
   cudaEvent_t pin2_ev = nullptr;  // H2D of nmt_inject_states from page-locked caller memory
   std::mutex mu;
+  std::vector<char> raw;  // the params container this model was built from (nmt_save_params)
   // lifetime: one reference held by the user handle plus one per live context, so that
   // nmt_model_free and nmt_ctx_free may be called in any order
   std::atomic<int> refs{1};
@@ -217,6 +233,13 @@ static void free_all_model(nmt_model* m) {
   for (__nv_bfloat16** p : {&m->Watt, &m->W_h1, &m->W_q, &m->W_g2, &m->W_ro, &m->W_o, &m->ctxbf}) dfree(*p);
   dfree(m->bar);
   dfree(m->d_src);
+  dfree(m->W_encb);
+  dfree(m->W_initb);
+  for (__nv_bfloat16** p : {&m->eb.A, &m->eb.ctxbf, &m->eb.Am}) dfree(*p);
+  for (float** p : {&m->eb.h, &m->eb.G, &m->eb.P}) dfree(*p);
+  dfree(m->eb.ints);
+  if (m->eb.blob) cudaFree(m->eb.blob);
+  m->eb.blob = nullptr;
   m->free_ws();
   dfree(m->fws_i);
   dfree(m->fws_f);
@@ -617,6 +640,20 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
       for (int o = 0; o < H; ++o) wt[(size_t)o * C + k] = wi[(size_t)k * H + o];
     m->W_initT = upload_vec(wt, st);
   }
+  {  // batched-encoder operands (nmt_encode_batch): always stored hi | lo, the GEMM takes 1 or 3 passes
+    m->W_encb = dalloc<__nv_bfloat16>((size_t)6 * Hp * 4 * Hp);
+    for (int d = 0; d < 2; ++d) {
+      const std::string p = d ? "encoder_r" : "encoder";
+      Upload U(A.at(p + "_U"), st), Ux(A.at(p + "_Ux"), st);
+      for (int g = 0; g < 2; ++g)
+        pack_T(U.d + g * H, 2 * H, H, H, m->W_encb, 4 * Hp, d * 3 * Hp + g * Hp, d * Hp, 0, 0, H, Hp, 2 * Hp, st);
+      pack_T(Ux.d, H, H, H, m->W_encb, 4 * Hp, d * 3 * Hp + 2 * Hp, d * Hp, 0, 0, H, Hp, 2 * Hp, st);
+    }
+    m->W_initb = dalloc<__nv_bfloat16>((size_t)Hp * 2 * Cp);
+    Upload Wi(A.at("ff_state_W"), st);
+    pack_T(Wi.d, H, C, H, m->W_initb, 2 * Cp, 0, 0, 0, 1, H, Hp, Cp, st);
+    CK(cudaStreamSynchronize(st));
+  }
   m->b_init = upload_vec(std::vector<float>(hv("ff_state_b"), hv("ff_state_b") + H), st);
   m->Watt = dalloc<__nv_bfloat16>((size_t)Cp * 2 * Cp);
   {
@@ -752,6 +789,8 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
 
   // ---- tensor maps of the weight operands
   m->tm_Watt = make_tmap_bf16(m->Watt, Cp, 2 * Cp, 128);
+  m->tm_Wencb = make_tmap_bf16(m->W_encb, 6 * Hp, 4 * Hp, 128);
+  m->tm_Winitb = make_tmap_bf16(m->W_initb, Hp, 2 * Cp, 128);
   m->tm_Wh1 = make_tmap_bf16(m->W_h1, 3 * Hp, sf * Hp, 128);
   m->tm_Wq = make_tmap_bf16(m->W_q, Cp, sf * Hp, 128);
   m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, 128);
@@ -866,6 +905,7 @@ static void parse_and_build(const char* buf, size_t len, const nmt_opts* opts, n
   m->Vp = round_up(V, 256);
   m->ROp = round_up(RO, 128);
   build_model(m.get(), A);
+  m->raw.assign(buf, buf + len);
   *out = m.release();
 }
 
@@ -958,18 +998,25 @@ static void pick_splits(GemmShape& g, int M_max, int CM, int BN, int units, int 
 // multiples of 256, else single-CTA 128 x 128 tiles.  `b128` = weight tensor map with a 128-row box.
 // Split-K partial s is written at rows [s * rps, (s + 1) * rps) of `out` (rps = rows per split;
 // out has m->P_rows rows); the chosen per-region factors are left in g.reg_ks.
-static void gemm_auto(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b128, GemmShape& g, float* out,
-                      int ldc, int rps, int M_max, cudaStream_t st) {
+// fp32-output GEMM with split-K partial s at rows [s * rps, (s + 1) * rps) of `out` (out_rows rows in
+// all); the per-region factors (<= max_ks) are left in g.reg_ks
+static void gemm_split(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b128, GemmShape& g, float* out,
+                       int ldc, int rps, int out_rows, int M_max, int max_ks, cudaStream_t st) {
   bool aligned = g.N % 256 == 0;
   for (int r = 0; r < g.nreg - 1; ++r) aligned = aligned && g.reg_n_end[r] % 256 == 0;
   const bool pair = m->use_pair && aligned;
-  static const int ks_cap = getenv("NMT_MAX_KS") ? std::max(1, atoi(getenv("NMT_MAX_KS"))) : 4;  // (diagnostic)
-  const int max_ks = std::max(1, std::min(ks_cap, m->P_rows / rps));
   if (pair) pick_splits(g, M_max, 256, 256, kNumSMs / 2, max_ks);
   else pick_splits(g, M_max, 128, 128, kNumSMs, max_ks);
   const size_t stride = (size_t)rps * ldc;
-  if (pair) gemm_store_pair(a, b128, g, out, ldc, m->P_rows, nullptr, M_max, st, stride);
-  else gemm_store(a, b128, g, out, ldc, m->P_rows, nullptr, M_max, st, stride);
+  if (pair) gemm_store_pair(a, b128, g, out, ldc, out_rows, nullptr, M_max, st, stride);
+  else gemm_store(a, b128, g, out, ldc, out_rows, nullptr, M_max, st, stride);
+}
+
+static void gemm_auto(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b128, GemmShape& g, float* out,
+                      int ldc, int rps, int M_max, cudaStream_t st) {
+  static const int ks_cap = getenv("NMT_MAX_KS") ? std::max(1, atoi(getenv("NMT_MAX_KS"))) : 4;  // (diagnostic)
+  const int max_ks = std::max(1, std::min(ks_cap, m->P_rows / rps));
+  gemm_split(m, a, b128, g, out, ldc, rps, m->P_rows, M_max, max_ks, st);
 }
 
 // one decoder forward step over the rows planned in m->row_* (count at c->counters[CNT_R])
@@ -1117,6 +1164,46 @@ nmt_status nmt_load(const char* path, const nmt_opts* opts, nmt_model** out) {
   return nmt_load_buffer(buf.data(), buf.size(), opts, out);
 }
 
+nmt_status nmt_save_params(const nmt_model* m, const char* path) {
+  if (!m || !path) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
+  std::ofstream f(path, std::ios::binary | std::ios::trunc);
+  if (!f) return fail(NMT_ERR_IO, std::string("cannot open ") + path + " for writing");
+  f.write(m->raw.data(), (std::streamsize)m->raw.size());
+  f.close();
+  if (!f) return fail(NMT_ERR_IO, std::string("cannot write ") + path);
+  return NMT_OK;
+}
+
+nmt_status nmt_params_bytes(const nmt_model* m, void* out, size_t* len) {
+  if (!m || !len) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
+  if (!out) {
+    *len = m->raw.size();
+    return NMT_OK;
+  }
+  if (*len < m->raw.size()) {
+    *len = m->raw.size();
+    return fail(NMT_ERR_CAPACITY, "buffer smaller than the params container");
+  }
+  std::memcpy(out, m->raw.data(), m->raw.size());
+  *len = m->raw.size();
+  return NMT_OK;
+}
+
+nmt_status nmt_create_random(const nmt_dims* d, uint64_t seed, float logit_std, const nmt_opts* opts,
+                             nmt_model** out) {
+  if (!d || !out) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
+  size_t len = 0;
+  if (nmt_random_params(d, seed, logit_std, nullptr, &len) != NMT_OK)
+    return fail(NMT_ERR_INVALID_ARG, "bad dims or logit_std");
+  std::vector<char> buf(len);
+  if (nmt_random_params(d, seed, logit_std, buf.data(), &len) != NMT_OK)
+    return fail(NMT_ERR_INVALID_ARG, "bad dims or logit_std");
+  nmt_opts o{};
+  if (opts) o = *opts;
+  if (d->max_src_len > 0 && o.max_src_len <= 0) o.max_src_len = d->max_src_len;
+  return nmt_load_buffer(buf.data(), buf.size(), &o, out);
+}
+
 // header of a params container: [0, payload offset) and the payload size (format checks only)
 static size_t params_payload_offset(const char* buf, size_t len, size_t* payload) {
   size_t pos = 0;
@@ -1222,27 +1309,37 @@ nmt_status nmt_model_dims(const nmt_model* m, nmt_dims* out) {
 
 void nmt_model_free(nmt_model* m) { model_release(m); }
 
-// E1-E7 for one sentence; src ids either [host] (copied) or [dev] (validated on the device)
-static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t* src_dev, int len) {
-  CK(cudaSetDevice(m->device));
-  cudaStream_t st = m->st;
+// a context for a source of `len` tokens: a released arena from the model's pool, else a new one
+// (holds one model reference; the caller owns it)
+static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
   nmt_ctx* c = nullptr;
   if (!m->pool.empty()) {  // reuse a released arena: reset its counters and hash table only
     c = m->pool.back();
     m->pool.pop_back();
     c->m = m;
+    m->refs.fetch_add(1);
   } else {
     c = new nmt_ctx();
     c->m = m;
+    m->refs.fetch_add(1);
+    std::unique_ptr<nmt_ctx> g(c);
     c->ctx = dalloc<float>((size_t)m->maxTx * m->Cp);
     c->pctx = dalloc<float>((size_t)m->maxTx * m->Cp);
     c->counters = dalloc<int>(CNT_N);
     c->grow_nodes(4096);
     c->grow_slots(1024);
+    g.release();
   }
-  m->refs.fetch_add(1);
   c->Tx = len;
-  std::unique_ptr<nmt_ctx> guard_c(c);
+  return c;
+}
+
+// E1-E7 for one sentence; src ids either [host] (copied) or [dev] (validated on the device)
+static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t* src_dev, int len) {
+  CK(cudaSetDevice(m->device));
+  cudaStream_t st = m->st;
+  std::unique_ptr<nmt_ctx> guard_c(acquire_ctx(m, len));
+  nmt_ctx* c = guard_c.get();
   ctx_reset(c->dev(), c->hcap, st);  // counters, root node, empty hash table
   const int* d_src = src_dev;
   if (src_host) {
@@ -1344,6 +1441,158 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
   return guard_c.release();
 }
 
+// E1-E7 for n sentences at once (nmt_encode_batch).  The recurrences of all sentences advance
+// together: per time step one tensor-core GEMM [h_fwd | h_bwd] . blockdiag([U|Ux]_fwd, [U|Ux]_bwd)
+// over the sentences still running (sorted by length, a row prefix) and one gate kernel.  Then the
+// means, one s0 GEMM for all sentences, one pctx GEMM over all tokens and the scatters into the
+// per-sentence contexts.  2 Tx_max + 7 launches for the whole batch.
+static void encode_batch_impl(nmt_model* m, int n, const int32_t* ids, const int32_t* offs, nmt_ctx** outs) {
+  CK(cudaSetDevice(m->device));
+  cudaStream_t st = m->st;
+  const int Hp = m->Hp, Cp = m->Cp;
+  const bool sp = m->split;
+  std::vector<int> ord(n);
+  for (int i = 0; i < n; ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return offs[a + 1] - offs[a] > offs[b + 1] - offs[b]; });
+  std::vector<int> tok_off(n + 1, 0);
+  for (int i = 0; i < n; ++i) tok_off[i + 1] = tok_off[i] + (offs[ord[i] + 1] - offs[ord[i]]);
+  const int n_tok = tok_off[n], Tmax = tok_off[1];
+  // ---- contexts (sorted order); released again if anything below throws
+  std::vector<std::unique_ptr<nmt_ctx>> cs(n);
+  for (int i = 0; i < n; ++i) cs[i].reset(acquire_ctx(m, tok_off[i + 1] - tok_off[i]));
+  // ---- workspace (grow-only)
+  auto& w = m->eb;
+  const int n_cap = round_up(n, 256), tok_cap = round_up(n_tok, 256);
+  const int pks_max = std::max(1, std::min(8, 16384 / tok_cap));
+  const size_t g_need = (size_t)4 * n_cap * 6 * Hp, p_need = (size_t)pks_max * tok_cap * Cp;
+  if (n_cap > w.n_cap || tok_cap > w.tok_cap || g_need > w.g_floats || p_need > w.p_floats) {
+    CK(cudaStreamSynchronize(st));
+    if (n_cap > w.n_cap || g_need > w.g_floats) {
+      dfree(w.A);
+      dfree(w.Am);
+      dfree(w.h);
+      dfree(w.G);
+      w.n_cap = std::max(n_cap, w.n_cap);
+      w.g_floats = (size_t)4 * w.n_cap * 6 * Hp;
+      w.A = dalloc<__nv_bfloat16>((size_t)w.n_cap * 4 * Hp);
+      w.Am = dalloc<__nv_bfloat16>((size_t)w.n_cap * 2 * Cp);
+      w.h = dalloc<float>((size_t)w.n_cap * 2 * Hp);
+      w.G = dalloc<float>(w.g_floats);
+      w.tm_A = make_tmap_bf16(w.A, w.n_cap, 4 * Hp, 128);
+      w.tm_Am = make_tmap_bf16(w.Am, w.n_cap, 2 * Cp, 128);
+    }
+    if (tok_cap > w.tok_cap || p_need > w.p_floats) {
+      dfree(w.ctxbf);
+      dfree(w.P);
+      w.tok_cap = std::max(tok_cap, w.tok_cap);
+      w.p_floats = std::max(p_need, w.p_floats);
+      w.ctxbf = dalloc<__nv_bfloat16>((size_t)w.tok_cap * 2 * Cp);
+      w.P = dalloc<float>(w.p_floats);
+      w.tm_ctxbf = make_tmap_bf16(w.ctxbf, w.tok_cap, 2 * Cp, 128);
+    }
+  }
+  // ---- request upload: ids | tok_off | row_b, and the per-sentence tables
+  const size_t n_ints = (size_t)2 * n_tok + n + 1;
+  if (n_ints > w.ints_cap) {
+    CK(cudaStreamSynchronize(st));
+    dfree(w.ints);
+    w.ints_cap = std::max(n_ints, w.ints_cap * 2);
+    w.ints = dalloc<int>(w.ints_cap);
+  }
+  std::vector<int> hi(n_ints);
+  for (int i = 0; i < n; ++i) {
+    const int b = ord[i], L = tok_off[i + 1] - tok_off[i];
+    std::memcpy(&hi[tok_off[i]], ids + offs[b], (size_t)L * 4);
+    for (int j = 0; j < L; ++j) hi[(size_t)n_tok + n + 1 + tok_off[i] + j] = i;
+  }
+  std::memcpy(&hi[n_tok], tok_off.data(), (size_t)(n + 1) * 4);
+  const size_t blob_bytes = (size_t)3 * n * sizeof(float*) + (size_t)n * sizeof(CtxDev) + (size_t)n * 8;
+  if (blob_bytes > w.blob_cap) {
+    CK(cudaStreamSynchronize(st));
+    if (w.blob) cudaFree(w.blob);
+    w.blob = nullptr;
+    w.blob_cap = std::max(blob_bytes, w.blob_cap * 2);
+    CK(cudaMalloc(&w.blob, w.blob_cap));
+  }
+  std::vector<char> hb(blob_bytes);
+  float** tp = reinterpret_cast<float**>(hb.data());
+  CtxDev* tc = reinterpret_cast<CtxDev*>(hb.data() + (size_t)3 * n * sizeof(float*));
+  int64_t* th = reinterpret_cast<int64_t*>(hb.data() + (size_t)3 * n * sizeof(float*) + (size_t)n * sizeof(CtxDev));
+  int64_t hcap_max = 1;
+  for (int i = 0; i < n; ++i) {
+    tp[i] = cs[i]->ctx;
+    tp[n + i] = cs[i]->pctx;
+    tp[2 * n + i] = cs[i]->S;
+    tc[i] = cs[i]->dev();
+    th[i] = cs[i]->hcap;
+    hcap_max = std::max(hcap_max, cs[i]->hcap);
+  }
+  CK(cudaMemcpyAsync(w.ints, hi.data(), n_ints * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(w.blob, hb.data(), blob_bytes, cudaMemcpyHostToDevice, st));
+  char* db = static_cast<char*>(w.blob);
+  ctx_reset_many(reinterpret_cast<const CtxDev*>(db + (size_t)3 * n * sizeof(float*)),
+                 reinterpret_cast<const int64_t*>(db + (size_t)3 * n * sizeof(float*) + (size_t)n * sizeof(CtxDev)), n,
+                 hcap_max, st);
+  EncBatchDev e{};
+  e.n = n;
+  e.H = m->H;
+  e.Hp = Hp;
+  e.src = w.ints;
+  e.tok_off = w.ints + n_tok;
+  e.row_b = w.ints + n_tok + n + 1;
+  e.encin = m->EncIn;
+  e.G = w.G;
+  e.ps = (int64_t)n_cap * 6 * Hp;
+  e.h = w.h;
+  e.A = w.A;
+  e.lo_a = sp ? 2 * Hp : 0;
+  e.ctxbf = w.ctxbf;
+  e.Am = w.Am;
+  float* const* dtp = reinterpret_cast<float* const*>(db);
+  e.ctx = dtp;
+  e.pctx = dtp + n;
+  e.S0 = dtp + 2 * n;
+  e.b_init = m->b_init;
+  e.b_att = m->b_att;
+  {  // E3/E4: the recurrences, h_{-1} = h_{Tx} = 0
+    ProfScope p_(m, ST_ENC_RECUR);
+    CK(cudaMemsetAsync(w.A, 0, (size_t)n * 4 * Hp * sizeof(__nv_bfloat16), st));
+    CK(cudaMemsetAsync(w.h, 0, (size_t)n * 2 * Hp * sizeof(float), st));
+    int active = n;
+    for (int t = 0; t < Tmax; ++t) {
+      while (active > 0 && tok_off[active] - tok_off[active - 1] <= t) --active;
+      GemmShape g = gemm_shape(active, nullptr, 6 * Hp, 2 * Hp, 0, sp, 2 * Hp, 2 * Hp);
+      g.nreg = 2;
+      g.reg_n_end[0] = 3 * Hp, g.reg_k0[0] = 0, g.reg_k1[0] = Hp;        // forward: h_fwd . [U|Ux]_fwd
+      g.reg_n_end[1] = 6 * Hp, g.reg_k0[1] = Hp, g.reg_k1[1] = 2 * Hp;   // backward: h_bwd . [U|Ux]_bwd
+      gemm_split(m, w.tm_A, m->tm_Wencb, g, w.G, 6 * Hp, n_cap, 4 * n_cap, active, 4, st);
+      if (gemm_ks(g, 0) != gemm_ks(g, 1)) throw NmtError(NMT_ERR_CUDA, "encode_batch: asymmetric split-K");
+      e.ks = gemm_ks(g, 0);
+      encb_gates(e, t, active, st);
+    }
+  }
+  {  // E5/E6: s0 = tanh(mean_j ctx_j . W_init + b_init)
+    ProfScope p_(m, ST_ENC_INIT);
+    encb_mean(e, st);
+    GemmShape g = gemm_shape(n, nullptr, Hp, Cp, 0, sp, Cp, Cp);
+    gemm_split(m, w.tm_Am, m->tm_Winitb, g, w.G, Hp, n_cap, 24 * n_cap, n, 8, st);
+    encb_s0(e, w.G, gemm_ks(g, 0), (int64_t)n_cap * Hp, st);
+  }
+  {  // E7: pctx = ctx . Wc_att + b_att over all tokens
+    ProfScope p_(m, ST_ENC_PCTX);
+    GemmShape g = gemm_shape(n_tok, nullptr, Cp, Cp, 0, sp, Cp, Cp);
+    gemm_split(m, w.tm_ctxbf, m->tm_Watt, g, w.P, Cp, tok_cap, pks_max * tok_cap, n_tok, pks_max, st);
+    encb_pctx(e, w.P, gemm_ks(g, 0), (int64_t)tok_cap * Cp, n_tok, st);
+  }
+  for (int i = 0; i < n; ++i) {
+    nmt_ctx* c = cs[i].release();
+    c->n_nodes = 1;
+    c->n_slots = 2;
+    c->stale = false;
+    outs[ord[i]] = c;
+  }
+}
+
 nmt_status nmt_encode(nmt_model* m, const int32_t* src, int32_t len, nmt_ctx** out) {
   if (!m || !out) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
   if (len == 0) return fail(NMT_ERR_EMPTY_SOURCE, "empty source");
@@ -1369,6 +1618,29 @@ nmt_status nmt_encode_dev(nmt_model* m, const int32_t* src, int32_t len, nmt_ctx
   return guard([&] {
     std::lock_guard<std::mutex> lk(m->mu);
     *out = encode_impl(m, nullptr, src, len);
+  });
+}
+
+nmt_status nmt_encode_batch(nmt_model* m, int32_t n, const int32_t* ids, const int32_t* offsets, nmt_ctx** outs) {
+  if (!m || (n > 0 && (!ids || !offsets || !outs))) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
+  if (n < 0) return fail(NMT_ERR_INVALID_ARG, "n < 0");
+  if (n == 0) return NMT_OK;
+  if (offsets[0] != 0) return fail(NMT_ERR_INVALID_ARG, "offsets[0] != 0");
+  for (int b = 0; b < n; ++b) {
+    const int len = offsets[b + 1] - offsets[b];
+    if (len < 0) return fail(NMT_ERR_INVALID_ARG, "offsets decrease at " + std::to_string(b));
+    if (len == 0) return fail(NMT_ERR_EMPTY_SOURCE, "empty source (sentence " + std::to_string(b) + ")");
+    if (len > m->maxTx)
+      return fail(NMT_ERR_CAPACITY, "sentence " + std::to_string(b) + ": source length " + std::to_string(len) +
+                                        " > max_src_len " + std::to_string(m->maxTx));
+  }
+  for (int i = 0; i < offsets[n]; ++i)
+    if (ids[i] < 0 || ids[i] >= m->Vs)
+      return fail(NMT_ERR_TOKEN_RANGE, "source token " + std::to_string(ids[i]) + " at " + std::to_string(i) +
+                                           " outside [0, " + std::to_string(m->Vs) + ")");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    encode_batch_impl(m, n, ids, offsets, outs);
   });
 }
 
@@ -1540,6 +1812,212 @@ nmt_status nmt_score_batch(nmt_ctx* c, int32_t np, const nmt_state* parents, con
     if (nc) std::memcpy(out_logp, rl, (size_t)nc * 4);
     for (int i = 0; i < nc; ++i) out_child[i] = rc[i];
     if (out_argmax) std::memcpy(out_argmax, ra, (size_t)np * 4);
+  });
+}
+
+// D8 + D9 alone on caller-given readout outputs t (the minimum slice, SURVEY §8(b) test-only):
+// t rows go into a scratch context as R stepped nodes; then exactly the step's vocabulary path runs
+// (operand rows from the cached t, GEMM with the fused log-sum-exp, finalize, gather-dot).
+nmt_status nmt_debug_vocab(nmt_model* m, int32_t R, const float* t, const int32_t* off, const int32_t* words,
+                           float* out_logp, float* out_logZ, int32_t* out_argmax) {
+  if (!m || R < 0) return fail(NMT_ERR_INVALID_ARG, "bad arguments");
+  if (R == 0) return NMT_OK;
+  if (!t || !off || !out_logZ) return fail(NMT_ERR_INVALID_ARG, "NULL array");
+  if (off[0] != 0) return fail(NMT_ERR_INVALID_ARG, "cand_offsets[0] != 0");
+  for (int k = 0; k < R; ++k)
+    if (off[k + 1] < off[k]) return fail(NMT_ERR_INVALID_ARG, "cand_offsets decrease at " + std::to_string(k));
+  const int nc = off[R];
+  if (nc > 0 && (!words || !out_logp)) return fail(NMT_ERR_INVALID_ARG, "NULL candidate/output array");
+  for (int i = 0; i < nc; ++i)
+    if (words[i] < 0 || words[i] >= m->V) return fail(NMT_ERR_TOKEN_RANGE, "cand_words[" + std::to_string(i) + "]");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    cudaStream_t st = m->st;
+    std::unique_ptr<nmt_ctx> cg(acquire_ctx(m, 1));
+    nmt_ctx* c = cg.get();
+    c->n_nodes = 1;
+    c->n_slots = 2;
+    c->stale = false;
+    c->ensure((int64_t)R + nc + 1, (int64_t)R + 2);
+    ctx_reset(c->dev(), c->hcap, st);
+    m->ensure_ws(R, std::max(nc, 1));
+    const int Ep = m->Ep, E = m->E;
+    // nodes 1..R: parentless, stepped into slots 2..R+1 whose t is the caller's
+    std::vector<float> tp((size_t)R * Ep, 0.f);
+    for (int r = 0; r < R; ++r) std::memcpy(&tp[(size_t)r * Ep], t + (size_t)r * E, (size_t)E * 4);
+    std::vector<int> nodes(R), slots(R), minus1(R, -1), zero(R, 0);
+    for (int r = 0; r < R; ++r) {
+      nodes[r] = r + 1;
+      slots[r] = r + 2;
+    }
+    CK(cudaMemcpyAsync(c->T + (size_t)2 * Ep, tp.data(), tp.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->node_slot + 1, slots.data(), (size_t)R * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->node_word + 1, minus1.data(), (size_t)R * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->node_parent + 1, minus1.data(), (size_t)R * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(c->node_src + 1, zero.data(), (size_t)R * 4, cudaMemcpyHostToDevice, st));
+    const int cnt[CNT_N] = {R + 1, R + 2, 0, R};
+    CK(cudaMemcpyAsync(c->counters, cnt, sizeof(cnt), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m->in_par, nodes.data(), (size_t)R * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m->row_dst, slots.data(), (size_t)R * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // (pageable sources above)
+    c->n_nodes = R + 1;
+    c->n_slots = R + 2;
+    StepDev d = step_view(m, c);
+    beam_gather(d, c->dev(), m->in_par, R, st);  // vocabulary operand rows [t | 1 (| lo)] from the arena
+    {
+      ProfScope p_(m, ST_VOCAB);
+      GemmShape g = gemm_shape(0, d.R, m->Vp, Ep, 0, m->split, Ep, Ep);
+      g.b_panel_rows = m->Vp;
+      if (m->use_pair) gemm_lse_pair(m->tm_At, m->tm_Wo128, g, m->part, m->V, st, m->lse_cpm);
+      else gemm_lse(m->tm_At, m->tm_Wo, g, m->part, m->V, R, st, m->lse_cpm);
+    }
+    AttnCtx a{c->pctx, c->ctx, m->U_att, m->c_tt, 1};
+    step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R, st);
+    std::vector<float> lz(R);
+    std::vector<int> am(R);
+    if (nc > 0) {
+      std::vector<int> rq(off, off + R + 1);
+      CK(cudaMemcpyAsync(m->in_off, rq.data(), (size_t)(R + 1) * 4, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(m->in_words, words, (size_t)nc * 4, cudaMemcpyHostToDevice, st));
+      const PlanIO io = plan_io(m, R, nc, m->in_par, m->in_off, m->in_words);
+      plan(c->dev(), io, c->counters + CNT_R, st);  // every parent is stepped: no rows, children interned
+      gather_dot(c->dev(), io, m->W_o32, m->b_o, Ep, m->out_logp, m->out_child, nullptr, nullptr, st);
+      CK(cudaMemcpyAsync(out_logp, m->out_logp, (size_t)nc * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaMemcpyAsync(lz.data(), c->logZ + 2, (size_t)R * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(am.data(), c->amax + 2, (size_t)R * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::memcpy(out_logZ, lz.data(), (size_t)R * 4);
+    if (out_argmax) std::memcpy(out_argmax, am.data(), (size_t)R * 4);
+    // the scratch arena goes back to the pool
+    nmt_ctx* cc = cg.release();
+    cc->m = nullptr;
+    m->pool.push_back(cc);
+    m->refs.fetch_sub(1);
+  });
+}
+
+// Several contexts in one call: parent k belongs to ctx_per_parent[k]; candidates,
+// outputs and errors as nmt_score_batch, in input order.  Parents are grouped by context (stable)
+// and each group runs the step on the model stream with no host synchronisation in between; one
+// synchronisation at the end.
+nmt_status nmt_score_batch_multi(int32_t np, nmt_ctx* const* cpp, const nmt_state* parents, const int32_t* off,
+                                 const int32_t* words, float* out_logp, nmt_state* out_child, int32_t* out_argmax) {
+  if (np < 0) return fail(NMT_ERR_INVALID_ARG, "n_parents < 0");
+  if (np == 0) return NMT_OK;
+  if (!cpp || !parents || !off) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
+  nmt_model* m = cpp[0] ? cpp[0]->m : nullptr;
+  for (int k = 0; k < np; ++k) {
+    if (!cpp[k]) return fail(NMT_ERR_INVALID_ARG, "ctx_per_parent[" + std::to_string(k) + "] is NULL");
+    if (cpp[k]->m != m) return fail(NMT_ERR_INVALID_ARG, "contexts of different models in one call");
+  }
+  if (!m) return fail(NMT_ERR_BAD_STATE, "freed context");
+  if (off[0] != 0) return fail(NMT_ERR_INVALID_ARG, "cand_offsets[0] != 0");
+  for (int k = 0; k < np; ++k)
+    if (off[k + 1] < off[k]) return fail(NMT_ERR_INVALID_ARG, "cand_offsets decrease at " + std::to_string(k));
+  const int nc = off[np];
+  if (nc > 0 && (!words || !out_logp || !out_child)) return fail(NMT_ERR_INVALID_ARG, "NULL candidate/output array");
+  for (int i = 0; i < nc; ++i)
+    if (words[i] < 0 || words[i] >= m->V)
+      return fail(NMT_ERR_TOKEN_RANGE, "cand_words[" + std::to_string(i) + "] = " + std::to_string(words[i]) +
+                                           " outside [0, " + std::to_string(m->V) + ")");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    cudaStream_t st = m->st;
+    // groups in first-appearance order of their context
+    std::vector<nmt_ctx*> ctxs;
+    std::unordered_map<nmt_ctx*, int> gi;
+    std::vector<int> grp(np);
+    for (int k = 0; k < np; ++k) {
+      auto it = gi.find(cpp[k]);
+      if (it == gi.end()) it = gi.emplace(cpp[k], (int)ctxs.size()).first, ctxs.push_back(cpp[k]);
+      grp[k] = it->second;
+    }
+    const int G = (int)ctxs.size();
+    for (nmt_ctx* c : ctxs)
+      if (c->stale) c->sync_counters();
+    for (int k = 0; k < np; ++k)
+      if (parents[k] < 0 || parents[k] >= cpp[k]->n_nodes)
+        throw NmtError(NMT_ERR_BAD_STATE, "unknown state " + std::to_string(parents[k]) + " (parents[" +
+                                              std::to_string(k) + "])");
+    // per group: parents | offsets | words, concatenated; positions back into the input order
+    std::vector<std::vector<int>> gpar(G), gcand(G);
+    for (int k = 0; k < np; ++k) gpar[grp[k]].push_back(k);
+    int max_np = 0, max_nc = 0;
+    for (int g = 0; g < G; ++g) {
+      int n = 0;
+      for (int k : gpar[g]) n += off[k + 1] - off[k];
+      max_np = std::max(max_np, (int)gpar[g].size());
+      max_nc = std::max(max_nc, n);
+    }
+    m->ensure_ws(np + G, nc);  // one slice per group, each at its own offset (G + np offsets)
+    for (int g = 0; g < G; ++g) {
+      int n = 0;
+      for (int k : gpar[g]) n += off[k + 1] - off[k];
+      ctxs[g]->ensure(n, (int64_t)gpar[g].size());
+    }
+    int* h = static_cast<int*>(m->pinned((size_t)(2 * np + G + nc) * 4 + (size_t)(2 * nc + np) * 4 + 64));
+    int* hp = h;
+    int* ho = hp + np;        // G + np offsets (each group's CSR starts at 0)
+    int* hw = ho + np + G;
+    std::vector<int> pbase(G + 1, 0), cbase(G + 1, 0), cpos;  // group slices; candidate positions
+    cpos.reserve(nc);
+    for (int g = 0, P = 0, Cc = 0; g < G; ++g) {
+      pbase[g] = P;
+      cbase[g] = Cc;
+      int o = 0;
+      ho[P + g] = 0;
+      for (int k : gpar[g]) {
+        hp[P++] = (int)parents[k];
+        for (int i = off[k]; i < off[k + 1]; ++i) {
+          hw[Cc++] = words[i];
+          cpos.push_back(i);
+        }
+        o += off[k + 1] - off[k];
+        ho[P + g] = o;
+      }
+      pbase[g + 1] = P;
+      cbase[g + 1] = Cc;
+    }
+    CK(cudaMemcpyAsync(m->in_par, hp, (size_t)np * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m->in_off, ho, (size_t)(np + G) * 4, cudaMemcpyHostToDevice, st));
+    if (nc) CK(cudaMemcpyAsync(m->in_words, hw, (size_t)nc * 4, cudaMemcpyHostToDevice, st));
+    for (int g = 0; g < G; ++g) {
+      const int gn = pbase[g + 1] - pbase[g], gc = cbase[g + 1] - cbase[g];
+      const PlanIO io = plan_io(m, gn, gc, m->in_par + pbase[g], m->in_off + pbase[g] + g, m->in_words + cbase[g]);
+      run_call(m, ctxs[g], io, m->out_logp + cbase[g], m->out_child + cbase[g], nullptr, m->out_amax + pbase[g]);
+    }
+    float* rl = reinterpret_cast<float*>(hw + nc);
+    int* rc = reinterpret_cast<int*>(rl + nc);
+    int* ra = rc + nc;
+    if (nc) {
+      CK(cudaMemcpyAsync(rl, m->out_logp, (size_t)nc * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(rc, m->out_child, (size_t)nc * 4, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaMemcpyAsync(ra, m->out_amax, (size_t)np * 4, cudaMemcpyDeviceToHost, st));
+    std::vector<int> cnt((size_t)G * CNT_N);
+    for (int g = 0; g < G; ++g)
+      CK(cudaMemcpyAsync(&cnt[(size_t)g * CNT_N], ctxs[g]->counters, CNT_N * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int g = 0; g < G; ++g)
+      if (cnt[(size_t)g * CNT_N + CNT_ERR]) {
+        const int z = 0;
+        CK(cudaMemcpy(ctxs[g]->counters + CNT_ERR, &z, 4, cudaMemcpyHostToDevice));
+        throw NmtError(NMT_ERR_BAD_STATE, "device-side validation failed");
+      }
+    for (int g = 0; g < G; ++g) {
+      ctxs[g]->n_nodes = cnt[(size_t)g * CNT_N + CNT_NODES];
+      ctxs[g]->n_slots = cnt[(size_t)g * CNT_N + CNT_SLOTS];
+    }
+    for (int j = 0; j < nc; ++j) {
+      out_logp[cpos[j]] = rl[j];
+      out_child[cpos[j]] = rc[j];
+    }
+    if (out_argmax)
+      for (int g = 0; g < G; ++g)
+        for (int q = 0; q < (int)gpar[g].size(); ++q) out_argmax[gpar[g][q]] = ra[pbase[g] + q];
   });
 }
 

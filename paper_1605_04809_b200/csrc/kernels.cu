@@ -1674,4 +1674,127 @@ void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
   }
 }
 
+
+// ===================================================================================== batched encoder
+// nmt_encode_batch ("tensor-bound when B >~ 300 sentences are batched"): the
+// recurrence of n sentences advances one time step per (GEMM, gate) pair.  Sentences are sorted by
+// length (descending), so the rows still running at step t are a prefix [0, active(t)).
+// GEMM of step t: [h_fwd | h_bwd] (bf16 hi|lo) . blockdiag([U|Ux]_fwd, [U|Ux]_bwd) -> G [n][6Hp];
+// this kernel adds the precomputed input projections (EncIn[tok] = x.[W|Wx] + [b|bx]) and applies
+// the DL4MT GRU: [r|u] = sigm(xW + b + hU); h~ = tanh(r*(hUx) + xWx + bx);
+// h' = u*h + (1-u)*h~.  The forward direction reads token t, the backward token L_b - 1 - t, so each
+// sentence's backward pass starts at its own last token (h_{Tx} = 0).
+__global__ void k_encb_gates(EncBatchDev e, int t, int active) {
+  pdl_enter();
+  const int Hp = e.Hp, Cp = 2 * Hp, H4 = Hp / 4;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = idx / (2 * H4), rem = idx % (2 * H4), dir = rem / H4, j = (rem % H4) * 4;
+  if (b >= active) return;
+  const int o0 = e.tok_off[b], L = e.tok_off[b + 1] - o0;
+  const int pos = dir ? L - 1 - t : t;
+  const int tok = e.src[o0 + pos];
+  const float* g = e.G + (int64_t)b * 6 * Hp + dir * 3 * Hp + j;
+  const float* x = e.encin + (int64_t)tok * 6 * Hp + dir * 3 * Hp + j;
+  const float4 gr = ld4_sum(g, e.ks, e.ps), gu = ld4_sum(g + Hp, e.ks, e.ps), gx = ld4_sum(g + 2 * Hp, e.ks, e.ps);
+  const float4 xr = ld4(x), xu = ld4(x + Hp), xx = ld4(x + 2 * Hp);
+  float* hp = e.h + (int64_t)b * Cp + dir * Hp + j;
+  const float4 hv = ld4(hp);
+  float4 o;
+#define NMT_GRUE(c) { const float rg = sigm(xr.c + gr.c), ug = sigm(xu.c + gu.c); \
+                      o.c = ug * hv.c + (1.f - ug) * tanhf(rg * gx.c + xx.c); }
+  NMT_GRUE(x) NMT_GRUE(y) NMT_GRUE(z) NMT_GRUE(w)
+#undef NMT_GRUE
+  st4(hp, o);
+  store_split4(e.A + (int64_t)b * 2 * Cp + dir * Hp + j, e.lo_a, o);
+  st4(e.ctx[b] + (int64_t)pos * Cp + dir * Hp + j, o);
+  store_split4(e.ctxbf + (int64_t)(o0 + pos) * 2 * Cp + dir * Hp + j, Cp, o);
+}
+
+// E5 input: mean_j ctx_j per sentence -> bf16 hi|lo operand of the s0 GEMM
+__global__ void k_encb_mean(EncBatchDev e) {
+  pdl_enter();
+  const int Cp = 2 * e.Hp, b = blockIdx.y, k = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (k >= Cp) return;
+  const int L = e.tok_off[b + 1] - e.tok_off[b];
+  const float* c = e.ctx[b] + k;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j = 0; j < L; ++j) {
+    const float4 v = ld4(c + (int64_t)j * Cp);
+    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  }
+  const float inv = 1.f / (float)L;
+  s.x *= inv; s.y *= inv; s.z *= inv; s.w *= inv;
+  store_split4(e.Am + (int64_t)b * 2 * Cp + k, Cp, s);
+}
+
+// E6: s0 = tanh(mean ctx . W_init + b_init) into slot 0 of each sentence's state arena
+__global__ void k_encb_s0(EncBatchDev e, const float* __restrict__ S0w, int ks, int64_t ps) {
+  pdl_enter();
+  const int b = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= e.Hp) return;
+  float v = 0.f;
+  if (j < e.H) v = tanhf(ld_sum(S0w + (int64_t)b * e.Hp + j, ks, ps) + e.b_init[j]);
+  e.S0[b][j] = v;
+}
+
+// E7 output: pctx rows of the token-major batch GEMM (+ b_att) scattered to each sentence's pctx
+__global__ void k_encb_pctx(EncBatchDev e, const float* __restrict__ P, int ks, int64_t ps, int n_tok) {
+  pdl_enter();
+  const int Cp = 2 * e.Hp, C4 = Cp / 4;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = (int)(idx / C4), k = (int)(idx % C4) * 4;
+  if (r >= n_tok) return;
+  const int b = e.row_b[r], pos = r - e.tok_off[b];
+  float4 v = ld4_sum(P + (int64_t)r * Cp + k, ks, ps);
+  const float4 bb = ld4(e.b_att + k);
+  v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
+  st4(e.pctx[b] + (int64_t)pos * Cp + k, v);
+}
+
+// context (re)initialisation of n arenas in one launch (k_ctx_reset per blockIdx.y)
+__global__ void k_ctx_reset_many(const CtxDev* __restrict__ cs, const int64_t* __restrict__ hcaps) {
+  pdl_enter();
+  const CtxDev c = cs[blockIdx.y];
+  const int64_t hcap = hcaps[blockIdx.y];
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = i0; i < hcap; i += (int64_t)gridDim.x * blockDim.x) {
+    c.hkeys[i] = ~0ull;
+    c.hvals[i] = INT32_MIN;
+  }
+  if (i0 == 0) {
+    c.counters[CNT_NODES] = 1;
+    c.counters[CNT_SLOTS] = 2;
+    c.counters[CNT_ERR] = 0;
+    c.counters[CNT_R] = 0;
+    c.node_word[0] = -1;
+    c.node_parent[0] = -1;
+    c.node_src[0] = 0;
+    c.node_slot[0] = -1;
+  }
+}
+
+void encb_gates(const EncBatchDev& e, int t, int active, cudaStream_t st) {
+  const int64_t n = (int64_t)active * 2 * (e.Hp / 4);
+  launch_pdl(k_encb_gates, (unsigned)((n + 255) / 256), 256, 0, st, e, t, active);
+  CK_LAUNCH();
+}
+void encb_mean(const EncBatchDev& e, cudaStream_t st) {
+  launch_pdl(k_encb_mean, dim3((2 * e.Hp / 4 + 127) / 128, e.n), 128, 0, st, e);
+  CK_LAUNCH();
+}
+void encb_s0(const EncBatchDev& e, const float* S0w, int ks, int64_t ps, cudaStream_t st) {
+  launch_pdl(k_encb_s0, dim3((e.Hp + 127) / 128, e.n), 128, 0, st, e, S0w, ks, ps);
+  CK_LAUNCH();
+}
+void encb_pctx(const EncBatchDev& e, const float* P, int ks, int64_t ps, int n_tok, cudaStream_t st) {
+  const int64_t n = (int64_t)n_tok * (2 * e.Hp / 4);
+  launch_pdl(k_encb_pctx, (unsigned)((n + 255) / 256), 256, 0, st, e, P, ks, ps, n_tok);
+  CK_LAUNCH();
+}
+void ctx_reset_many(const CtxDev* cs, const int64_t* hcaps, int n, int64_t hcap_max, cudaStream_t st) {
+  const int64_t b = std::min<int64_t>((hcap_max + 255) / 256, 64);
+  launch_pdl(k_ctx_reset_many, dim3((unsigned)std::max<int64_t>(b, 1), n), 256, 0, st, cs, hcaps);
+  CK_LAUNCH();
+}
+
 }  // namespace nmt

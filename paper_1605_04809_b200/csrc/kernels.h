@@ -100,6 +100,25 @@ struct EncDev {
   float* S0;             // [H] arena slot 0
 };
 
+// nmt_encode_batch: n sentences sorted by length (descending); token rows sentence-major
+struct EncBatchDev {
+  int n, H, Hp;
+  const int* src;        // [n_tok] source ids
+  const int* tok_off;    // [n + 1] first token row of each sentence
+  const int* row_b;      // [n_tok] sentence of each token row
+  const float* encin;    // [Vs][6Hp] precomputed input projections (EncDev::encin)
+  const float* G; int ks; int64_t ps;  // [n][6Hp] recurrent GEMM output (+ split-K partials)
+  float* h;              // [n][2Hp] fp32 states [fwd | bwd]
+  __nv_bfloat16* A; int lo_a;  // [n][4Hp] bf16 operand of the next step's GEMM (hi | lo at +2Hp)
+  __nv_bfloat16* ctxbf;  // [n_tok][4Hp] hi | lo copy of ctx (pctx GEMM operand)
+  __nv_bfloat16* Am;     // [n][4Hp] mean ctx hi | lo (s0 GEMM operand)
+  float* const* ctx;     // [n] per-sentence ctx [Tx][Cp]
+  float* const* pctx;    // [n] per-sentence pctx [Tx][Cp]
+  float* const* S0;      // [n] slot 0 of each sentence's state arena
+  const float* b_init;   // [H]
+  const float* b_att;    // [Cp]
+};
+
 enum { EW_GATHER, EW_GRU1, EW_ATTN, EW_GRU2, EW_READOUT, EW_FINALIZE };
 
 void pack_T(const float* src, int ld_src, int K, int N, __nv_bfloat16* dst, int ld_dst, int row0, int col0, int rmap,
@@ -128,5 +147,10 @@ void path_sum(const float* logp, const int* child, const int* off, const int* po
 void full_row(const float* T, const float* Wo32, const float* bo, const float* logZ, int slot, int Ep, int V,
               float* out, cudaStream_t st);
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st);
+void encb_gates(const EncBatchDev& e, int t, int active, cudaStream_t st);
+void encb_mean(const EncBatchDev& e, cudaStream_t st);
+void encb_s0(const EncBatchDev& e, const float* S0w, int ks, int64_t ps, cudaStream_t st);
+void encb_pctx(const EncBatchDev& e, const float* P, int ks, int64_t ps, int n_tok, cudaStream_t st);
+void ctx_reset_many(const CtxDev* cs, const int64_t* hcaps, int n, int64_t hcap_max, cudaStream_t st);
 
 }  // namespace nmt

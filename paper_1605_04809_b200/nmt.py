@@ -26,7 +26,9 @@ EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "n
            "nmt_inject_states", "nmt_logprobs_full", "nmt_debug_encoder", "nmt_debug_intermediates",
            "nmt_test_gemm", "nmt_encode_dev", "nmt_inject_states_dev", "nmt_launch_count", "nmt_profile",
            "nmt_profile_read", "nmt_bench_gemm", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
-           "nmt_ensemble_free", "nmt_params_average", "nmt_beam_step"]
+           "nmt_ensemble_free", "nmt_params_average", "nmt_beam_step",
+           "nmt_encode_batch", "nmt_save_params", "nmt_params_bytes", "nmt_random_params", "nmt_create_random",
+           "nmt_debug_vocab", "nmt_score_batch_multi"]
 
 
 N_STAGES = 19
@@ -49,6 +51,36 @@ def params_average(blobs, device: int = 0) -> bytes:
     _check(lib().nmt_params_average(n, C.cast(bufs, C.c_void_p), C.cast(lens, C.c_void_p), device, out,
                                     len(blobs[0]) if n else 0))
     return out.raw
+
+
+READOUTS = {"tanh": 0, "maxout": 1}
+
+
+def random_params(dim_emb: int, dim_hid: int, vocab_src: int, vocab_tgt: int, readout: str = "tanh",
+                  seed: int = 0, logit_std: float = 1.0) -> bytes:
+    """nmt_random_params: the seeded synthetic params container (host only, no GPU needed)."""
+    d = Dims(dim_emb, dim_hid, vocab_src, vocab_tgt, 0, READOUTS[readout])
+    n = C.c_size_t(0)
+    _check(lib().nmt_random_params(C.byref(d), seed, logit_std, None, C.byref(n)))
+    buf = C.create_string_buffer(n.value)
+    _check(lib().nmt_random_params(C.byref(d), seed, logit_std, C.cast(buf, C.c_void_p), C.byref(n)))
+    return buf.raw[:n.value]
+
+
+def score_batch_multi(contexts, parents, cand_offsets, cand_words, with_argmax: bool = True):
+    """nmt_score_batch_multi: parent k belongs to contexts[k] (all of one model)."""
+    n = len(parents)
+    hs = (C.c_void_p * max(n, 1))(*[c._h.value for c in contexts])
+    par = _c(parents, np.int64)
+    off = _c(cand_offsets, np.int32)
+    words = _c(cand_words, np.int32)
+    nc = int(off[-1]) if len(off) else 0
+    logp = np.empty(nc, np.float32)
+    child = np.empty(nc, np.int64)
+    am = np.empty(n, np.int32) if with_argmax else None
+    _check(lib().nmt_score_batch_multi(n, C.cast(hs, C.c_void_p), _ptr(par), _ptr(off), _ptr(words), _ptr(logp),
+                                       _ptr(child), _ptr(am)))
+    return logp, child, am
 
 
 class NmtError(RuntimeError):
@@ -108,6 +140,13 @@ def lib() -> C.CDLL:
             "nmt_bench_gemm": (i32, [i32, i32, i32, i32, i32, i32, i32, C.POINTER(C.c_float)]),
             "nmt_params_average": (i32, [i32, vp, vp, i32, vp, C.c_size_t]),
             "nmt_beam_step": (i32, [vp, i32, vp, i32, vp, vp, vp]),
+            "nmt_encode_batch": (i32, [vp, i32, vp, vp, vp]),
+            "nmt_save_params": (i32, [vp, C.c_char_p]),
+            "nmt_params_bytes": (i32, [vp, vp, C.POINTER(C.c_size_t)]),
+            "nmt_random_params": (i32, [C.POINTER(Dims), C.c_uint64, C.c_float, vp, C.POINTER(C.c_size_t)]),
+            "nmt_create_random": (i32, [C.POINTER(Dims), C.c_uint64, C.c_float, C.POINTER(Opts), C.POINTER(vp)]),
+            "nmt_debug_vocab": (i32, [vp, i32, vp, vp, vp, vp, vp, vp]),
+            "nmt_score_batch_multi": (i32, [i32, vp, vp, vp, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -150,6 +189,58 @@ class Model:
     def encode(self, src_ids: Sequence[int]) -> "Context":
         return Context(self, src_ids)
 
+    @classmethod
+    def create_random(cls, dim_emb: int, dim_hid: int, vocab_src: int, vocab_tgt: int, readout: str = "tanh",
+                      seed: int = 0, logit_std: float = 1.0, precision: str = "bf16", device: int = 0,
+                      max_src_len: int = 64) -> "Model":
+        """nmt_create_random: the seeded synthetic model generated and loaded by the library."""
+        m = cls.__new__(cls)
+        m._h = C.c_void_p()
+        d = Dims(dim_emb, dim_hid, vocab_src, vocab_tgt, max_src_len, READOUTS[readout])
+        opts = Opts(device, PRECISIONS[precision], max_src_len, None)
+        _check(lib().nmt_create_random(C.byref(d), seed, logit_std, C.byref(opts), C.byref(m._h)))
+        dd = Dims()
+        _check(lib().nmt_model_dims(m._h, C.byref(dd)))
+        m.dims = dd
+        m.precision = precision
+        return m
+
+    def save_params(self, path: str) -> None:
+        _check(lib().nmt_save_params(self._h, str(path).encode()))
+
+    def params_bytes(self) -> bytes:
+        n = C.c_size_t(0)
+        _check(lib().nmt_params_bytes(self._h, None, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _check(lib().nmt_params_bytes(self._h, C.cast(buf, C.c_void_p), C.byref(n)))
+        return buf.raw[:n.value]
+
+    def debug_vocab(self, t: np.ndarray, cand_offsets, cand_words):
+        """nmt_debug_vocab: the vocabulary stage alone on given readout outputs t [R x E]."""
+        t = _c(t, np.float32)
+        R = t.shape[0]
+        off = _c(cand_offsets, np.int32)
+        words = _c(cand_words, np.int32)
+        nc = int(off[-1]) if len(off) else 0
+        logp = np.empty(nc, np.float32)
+        logZ = np.empty(R, np.float32)
+        am = np.empty(R, np.int32)
+        _check(lib().nmt_debug_vocab(self._h, R, _ptr(t), _ptr(off), _ptr(words), _ptr(logp), _ptr(logZ), _ptr(am)))
+        return logp, logZ, am
+
+    def encode_batch(self, sources: Sequence[Sequence[int]]) -> list:
+        """nmt_encode_batch: one context per source, all recurrences advanced together."""
+        srcs = [_c(x, np.int32) for x in sources]
+        n = len(srcs)
+        if n == 0:
+            return []
+        ids = np.concatenate(srcs).astype(np.int32) if sum(len(x) for x in srcs) else np.zeros(1, np.int32)
+        off = np.zeros(n + 1, np.int32)
+        off[1:] = np.cumsum([len(x) for x in srcs])
+        hs = (C.c_void_p * n)()
+        _check(lib().nmt_encode_batch(self._h, n, _ptr(ids), _ptr(off), C.cast(hs, C.c_void_p)))
+        return [Context._wrap(self, hs[i], len(srcs[i])) for i in range(n)]
+
     def encode_dev(self, src_ptr: int, length: int) -> "Context":
         """nmt_encode_dev: source ids already resident in device memory (int32)."""
         return Context(self, None, dev=(src_ptr, length))
@@ -189,6 +280,15 @@ class Context:
             _check(lib().nmt_encode(model._h, _ptr(src), len(src), C.byref(self._h)))
             self.Tx = len(src)
         self.root = int(lib().nmt_root(self._h))
+
+    @classmethod
+    def _wrap(cls, model: Model, handle: int, Tx: int) -> "Context":
+        c = cls.__new__(cls)
+        c.model = model
+        c._h = C.c_void_p(handle)
+        c.Tx = Tx
+        c.root = int(lib().nmt_root(c._h))
+        return c
 
     def score_batch(self, parents, cand_offsets, cand_words, with_argmax: bool = True
                     ) -> Tuple[np.ndarray, np.ndarray, Optional[np.ndarray]]:

@@ -1,0 +1,158 @@
+"""GPU tests of the remaining SURVEY §8(b) boundary calls: nmt_save_params / nmt_params_bytes
+(byte-identical round trip), nmt_create_random (the library's generator, checked by
+exporting its container to the float64 oracle), nmt_debug_vocab (D8 + D9 alone on given t, bounded
+by the operand rounding of the vocabulary GEMM) and nmt_score_batch_multi (several sentences per
+call, identical to per-context nmt_score_batch)."""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32class": 1e-3, "bf16": 2e-2}
+CONFIGS = [("tanh", "fp32class"), ("tanh", "bf16"), ("maxout", "fp32class"), ("maxout", "bf16")]
+
+
+def nmt():
+    from paper_1605_04809_b200 import nmt as m
+    return m
+
+
+@pytest.mark.parametrize("readout", ["tanh", "maxout"])
+def test_save_params_round_trip(readout):
+    d = synth.Dims(8, 16, 50, 60, readout)
+    blob = synth.params_bytes(d, synth.make_model(d, 3))
+    M = nmt().Model(blob, precision="bf16")
+    assert M.params_bytes() == blob
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "m.params")
+        M.save_params(path)
+        assert open(path, "rb").read() == blob
+        M2 = nmt().Model(path, precision="bf16")  # and the saved file loads again
+        assert M2.params_bytes() == blob
+    with pytest.raises(nmt().NmtError) as e:
+        M.save_params("/nonexistent-dir/x.params")
+    assert e.value.name == "NMT_ERR_IO"
+
+
+@pytest.mark.parametrize("readout,prec", CONFIGS)
+def test_create_random_vs_oracle(readout, prec):
+    N = nmt()
+    M = N.Model.create_random(8, 16, 50, 50, readout, seed=21, logit_std=1.5, precision=prec)
+    blob = M.params_bytes()
+    assert blob == N.random_params(8, 16, 50, 50, readout, seed=21, logit_std=1.5)
+    d, p = synth.read_params(blob)
+    om = O.Model(d, p)
+    src = synth.make_source(d.vocab_src, 6, seed=4)
+    c = M.encode(src)
+    sess = O.Session(om, src)
+    lp, ch, _ = c.score_batch([0], [0, 5], [2, 3, 4, 0, 1])
+    rl, rc, _ = sess.score_batch([0], [0, 5], [2, 3, 4, 0, 1])
+    assert list(ch) == list(rc)
+    assert np.max(np.abs(lp - rl)) < TOL[prec]
+    parents = [int(x) for x in ch]
+    off = [0, 2, 4, 6, 8, 10]
+    words = [5, 6, 7, 8, 9, 10, 11, 12, 13, 14]
+    lp2, _, _ = c.score_batch(parents, off, words)
+    rl2, _, _ = sess.score_batch(parents, off, words)
+    assert np.max(np.abs(lp2 - rl2)) < TOL[prec]
+
+
+def _vocab_case(d, p, M, prec, R, n_cand, seed):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    scale = 1.0 if d.readout == "tanh" else 1.7
+    t = (np.tanh(rng.standard_normal((R, d.dim_emb))) * scale).astype(np.float32)
+    off = (np.arange(R + 1) * n_cand).astype(np.int32)
+    words = rng.integers(0, d.vocab_tgt, size=R * n_cand).astype(np.int32)
+    lp, lz, am = M.debug_vocab(t, off, words)
+    W = p["ff_logit_W"].astype(np.float64)
+    b = p["ff_logit_b"][0].astype(np.float64)
+    t64 = t.astype(np.float64)
+    z = t64 @ W + b
+    ref_lz = O.logsumexp(z)
+    # operand-rounding bound of the GEMM: bf16 t and W (2^-9 relative each) -> 2^-8 sum|t||W|;
+    # bf16x3 (fp32class) drops the lo.lo term: ~2^-16 relative
+    rel = 2.0 ** -8 if prec == "bf16" else 2.0 ** -15
+    B = rel * (np.abs(t64) @ np.abs(W)) + 2e-5
+    Bmax = B.max(axis=1)
+    assert np.all(np.abs(lz - ref_lz) <= Bmax + 1e-4), float(np.max(np.abs(lz - ref_lz) - Bmax))
+    for r in range(R):
+        assert z[r, am[r]] >= z[r].max() - 2 * Bmax[r], r
+    rows = np.repeat(np.arange(R), n_cand)
+    ref = z[rows, words] - ref_lz[rows]
+    err = np.abs(lp.astype(np.float64) - ref)
+    assert np.all(err <= B[rows, words] + Bmax[rows] + 1e-4), float(err.max())
+    return float(err.max()) if err.size else 0.0
+
+
+@pytest.mark.parametrize("readout,prec", CONFIGS)
+def test_debug_vocab_tiny(readout, prec):
+    d = synth.Dims(8, 16, 50, 50, readout)
+    p = synth.make_model(d, 7)
+    M = nmt().Model(synth.params_bytes(d, p), precision=prec)
+    _vocab_case(d, p, M, prec, 5, 4, seed=1)
+    _vocab_case(d, p, M, prec, 1, 0, seed=2)  # no candidates: logZ / argmax only
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32class"])
+def test_debug_vocab_enru(prec):
+    """D8 + D9 at the north-star shape (K = 500, V = 100k) on 300 rows (2 tiles + a ragged tail)."""
+    d = synth.EN_RU
+    p = synth.make_model(d, 2016)
+    M = nmt().Model(synth.params_bytes(d, p), precision=prec)
+    err = _vocab_case(d, p, M, prec, 300, 3, seed=3)
+    print(f"\n[debug_vocab] En->Ru {prec}: max|dlogp| = {err:.3e}")
+    assert err < TOL[prec]
+
+
+@pytest.mark.parametrize("readout,prec", CONFIGS)
+def test_score_batch_multi(readout, prec):
+    d = synth.Dims(8, 16, 50, 50, readout)
+    p = synth.make_model(d, 7)
+    om = O.Model(d, p)
+    N = nmt()
+    M = N.Model(synth.params_bytes(d, p), precision=prec)
+    srcs = [synth.make_source(d.vocab_src, L, seed=30 + L) for L in (3, 7, 5)]
+    cs = [M.encode(s) for s in srcs]
+    sess = [O.Session(om, s) for s in srcs]
+    # call 1: the three roots, interleaved with a repeated parent
+    ctxs = [cs[1], cs[0], cs[2], cs[1]]
+    par = [0, 0, 0, 0]
+    off = [0, 2, 5, 6, 8]
+    words = [4, 5, 6, 7, 8, 9, 4, 10]
+    lp, ch, am = N.score_batch_multi(ctxs, par, off, words)
+    idx = {id(c): i for i, c in enumerate(cs)}
+    for k, c in enumerate(ctxs):
+        s = sess[idx[id(c)]]
+        rl, rc, ra = s.score_batch([par[k]], [0, off[k + 1] - off[k]], words[off[k]:off[k + 1]])
+        assert list(ch[off[k]:off[k + 1]]) == list(rc)
+        assert np.max(np.abs(lp[off[k]:off[k + 1]] - rl)) < TOL[prec]
+    assert lp[0] == lp[6] and ch[0] == ch[6]  # same (ctx, parent, word): same handle, same bits
+    # the same request streams through per-context nmt_score_batch on fresh contexts: bit-identical
+    # (same kernels over the same rows)
+    fresh = [M.encode(s) for s in srcs]
+    f1 = fresh[1].score_batch([0, 0], [0, 2, 4], [4, 5, 4, 10])
+    f0 = fresh[0].score_batch([0], [0, 3], [6, 7, 8])
+    f2 = fresh[2].score_batch([0], [0, 1], [9])
+    assert np.array_equal(f1[0], lp[[0, 1, 6, 7]]) and np.array_equal(f1[1], ch[[0, 1, 6, 7]])
+    assert np.array_equal(f0[0], lp[2:5]) and np.array_equal(f2[0], lp[5:6])
+    assert list(am) == [f1[2][0], f0[2][0], f2[2][0], f1[2][1]]
+    # call 2: children of call 1 across contexts, against the oracle
+    ctxs2 = [cs[0], cs[2], cs[1], cs[0]]
+    par2 = [int(ch[2]), int(ch[5]), int(ch[0]), int(ch[3])]
+    off2 = [0, 3, 4, 6, 9]
+    words2 = [1, 2, 3, 4, 5, 6, 7, 8, 9]
+    lp2, ch2, _ = N.score_batch_multi(ctxs2, par2, off2, words2)
+    for k, c in enumerate(ctxs2):
+        s = sess[idx[id(c)]]
+        rl, rc, _ = s.score_batch([par2[k]], [0, off2[k + 1] - off2[k]], words2[off2[k]:off2[k + 1]])
+        assert list(ch2[off2[k]:off2[k + 1]]) == list(rc)
+        assert np.max(np.abs(lp2[off2[k]:off2[k + 1]] - rl)) < TOL[prec]
+    with pytest.raises(N.NmtError) as e:
+        N.score_batch_multi([cs[0]], [99], [0, 1], [3])
+    assert e.value.name == "NMT_ERR_BAD_STATE"
