@@ -12,6 +12,18 @@
   avg    NMT-k-Avg vs the k-ensemble ("four times smaller and four times faster"):
          one C2 batch (R = 1024 x 3) scored by 4 member models in turn (+ log-linear combine on
          the host) vs by their nmt_params_average model, on one GPU.
+  encb   nmt_encode_batch vs a loop of nmt_encode: n sentences of L ~ U[10,50] (+EOS) tokens, En->Ru
+         encoder (H 1024) - sentences/s, source tokens/s and the recurrence+pctx TFLOP/s per n.
+  c5     cube-pruning workload: sentences L ~ U[10,50]; per sentence one batched
+         encode (nmt_encode_batch over a chunk of sentences), B injected hypothesis states, then L
+         stacks, each a ScoreBatch (nmt_score_forest) of B (hypothesis, phrase) pairs with phrase
+         lengths 1..4 w.p. .4/.3/.2/.1 (rows per depth ~ B [1, .6, .3, .1]); stack s+1 expands the
+         final states of stack s.  Sweep B in 64..16384; the sentence count of a point is cut to a
+         fixed row budget (recorded).  Sentences are sharded over ranks by greedy LPT on L x B
+         under torchrun (no collective on the data path; max-over-ranks time).
+  ens    C4 ensemble: member m = rank (seed 2016 + m) scores the same C2 batch (R = 1024 x 3) and
+         the per-word scores are combined by nmt_ensemble_combine (NCCL reduce to rank 0, log-linear,
+         lambda = 1/M) - combined word-scores/s and the reduce's microseconds.  One GPU per member.
 Prints one JSON line per measurement point.
 """
 import argparse
@@ -189,12 +201,211 @@ def avg(a):
           flush=True)
 
 
+ENC_FLOP_PER_TOKEN = 2 * 2 * 1024 * 3072 + 2 * 2048 * 2048  # E3/E4 recurrence + E7 pctx
+ENC_FLOP_PER_SENTENCE = 2 * 2048 * 1024                   # E6 s0
+
+
+def encb(a):
+    import torch
+    from paper_1605_04809_b200 import nmt
+    d = synth.Dims(500, 1024, 50000, 100000, a.readout)
+    M = nmt.Model(synth.params_bytes(d, synth.make_model(d, 2016)), precision=a.precision, max_src_len=64)
+    rng = np.random.default_rng(3000)
+    for n in [1, 16, 64, 256, 1024, 3000]:
+        srcs = [synth.make_source(d.vocab_src, int(rng.integers(10, 51)), seed=7000 + i) for i in range(n)]
+        ntok = sum(len(x) for x in srcs)
+        for _ in range(2):
+            for c in M.encode_batch(srcs):
+                c.close()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(max(1, a.iters // 2)):
+            t0 = time.perf_counter()
+            cs = M.encode_batch(srcs)
+            cs[0].check()  # synchronises the model stream
+            ts.append(time.perf_counter() - t0)
+            for c in cs:
+                c.close()
+        tb = float(np.median(ts))
+        m_loop = min(n, 64)  # the single-sentence kernel, over the first sentences
+        for c in [M.encode(x) for x in srcs[:2]]:
+            c.close()
+        t0 = time.perf_counter()
+        cs = [M.encode(x) for x in srcs[:m_loop]]
+        cs[-1].check()
+        tl = (time.perf_counter() - t0) / m_loop
+        for c in cs:
+            c.close()
+        flop = ntok * ENC_FLOP_PER_TOKEN + n * ENC_FLOP_PER_SENTENCE
+        print(json.dumps({"workload": "encb", "n": n, "tokens": ntok, "precision": a.precision,
+                          "batch_ms": 1000 * tb, "sentences_per_s": n / tb, "tokens_per_s": ntok / tb,
+                          "tflops": flop / tb / 1e12, "single_encode_ms_per_sentence": 1000 * tl,
+                          "speedup_vs_single": tl * n / tb,
+                          "timing": "host wall clock around nmt_encode_batch + stream sync (median)"}), flush=True)
+
+
+def _dist():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+        return rank, world, dist
+    return 0, 1, None
+
+
+def lpt_shard(costs, world):
+    """Greedy LPT: sentences in descending cost to the least-loaded rank (deterministic)."""
+    load = [0.0] * world
+    out = [[] for _ in range(world)]
+    for i in sorted(range(len(costs)), key=lambda i: (-costs[i], i)):
+        r = min(range(world), key=lambda r: (load[r], r))
+        out[r].append(i)
+        load[r] += costs[i]
+    return [sorted(x) for x in out]
+
+
+def c5(a):
+    import torch
+    from paper_1605_04809_b200 import nmt
+    rank, world, dist = _dist()
+    d = synth.Dims(500, 1024, 50000, 100000, a.readout)
+    M = nmt.Model(synth.params_bytes(d, synth.make_model(d, 2016)), precision=a.precision, max_src_len=64)
+    rng = np.random.default_rng(3000)
+    lens = [int(x) for x in rng.integers(10, 51, size=3000)]
+    Bs = [int(x) for x in a.batches.split(",")]
+    for B in Bs:
+        n_sent = max(world, min(3000, int(a.row_budget // (2.0 * B * 30))))
+        costs = [lens[i] * B for i in range(n_sent)]
+        mine = lpt_shard(costs, world)[rank]
+
+        def run(sents, count):
+            edges = rows = naive = stacks = 0
+            for c0 in range(0, len(sents), a.enc_chunk):
+                chunk = sents[c0:c0 + a.enc_chunk]
+                srcs = [synth.make_source(d.vocab_src, lens[i], seed=9000 + i) for i in chunk]
+                ctxs = M.encode_batch(srcs)
+                for i, ctx in zip(chunk, ctxs):
+                    g = np.random.default_rng(100000 * B + i)
+                    s, y = synth.make_states(B, d.dim_hid, d.vocab_tgt, seed=50000 + i)
+                    hyps = ctx.inject_states(s, y)
+                    for stk in range(lens[i] + 1):  # one stack per target position (~L)
+                        L = g.choice(4, size=B, p=[.4, .3, .2, .1]).astype(np.int32) + 1
+                        off = np.zeros(B + 1, np.int32)
+                        off[1:] = np.cumsum(L)
+                        words = synth.zipf_ids(g, int(off[-1]), d.vocab_tgt)
+                        lp, fin, st = ctx.score_forest(hyps, off, words)
+                        hyps = fin
+                        if count:
+                            edges += sum(st["edges_per_depth"])
+                            rows += sum(st["rows_per_depth"])
+                            naive += int(off[-1])
+                            stacks += 1
+                    ctx.close()
+            return edges, rows, naive, stacks
+        run(mine[:1], False)  # warm-up (arena growth, workspace)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e, r, nv, ns = run(mine, True)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        tot = torch.tensor([e, r, nv, ns, len(mine)], dtype=torch.float64, device="cuda")
+        tmax = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(tot)
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        e, r, nv, ns, nsent = (float(x) for x in tot.tolist())
+        dt = float(tmax.item())
+        if rank == 0:
+            print(json.dumps({"workload": "c5", "B": B, "gpus": world, "precision": a.precision,
+                              "sentences": int(nsent), "stacks": int(ns), "word_scores_per_s": e / dt,
+                              "rows_per_s": r / dt, "naive_words": int(nv), "edges": int(e), "rows": int(r),
+                              "seconds": dt, "row_budget": a.row_budget,
+                              "timing": "host wall clock (max over ranks) around encode_batch + inject + "
+                                        "L stacks of nmt_score_forest per sentence, host C ABI, synchronized"}),
+                  flush=True)
+
+
+def ens(a):
+    import torch
+    from paper_1605_04809_b200 import nmt
+    rank, world, dist = _dist()
+    dev = torch.cuda.current_device()
+    d = synth.Dims(500, 1024, 50000, 100000, a.readout)
+    st = torch.cuda.Stream()
+    torch.cuda.set_stream(st)
+    M = nmt.Model(synth.params_bytes(d, synth.make_model(d, 2016 + rank)), precision=a.precision,
+                  stream=st.cuda_stream)
+    if dist:
+        obj = [nmt.Ensemble.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    else:
+        uid = nmt.Ensemble.unique_id()
+    E = nmt.Ensemble(world, rank, uid, dev)
+    R, Cn = 1024, 3
+    src = torch.from_numpy(synth.make_source(d.vocab_src, 49, seed=1)).cuda()
+    s, y = synth.make_states(R, d.dim_hid, d.vocab_tgt, seed=5)
+    off, w = synth.make_candidates(R, Cn, d.vocab_tgt, seed=6)
+    ds, dy, doff, dw = (torch.from_numpy(x).cuda() for x in (s, y, off, w))
+    ids = torch.empty(R, dtype=torch.int32, device="cuda")
+    lp = torch.empty(R * Cn, device="cuda")
+    ch = torch.empty(R * Cn, dtype=torch.int32, device="cuda")
+    out = torch.empty(R * Cn, device="cuda")
+
+    def step(combine=True):
+        ctx = M.encode_dev(src.data_ptr(), 50)
+        ctx.inject_states_dev(R, ds.data_ptr(), dy.data_ptr(), ids.data_ptr())
+        ctx.score_batch_dev(R, ids.data_ptr(), doff.data_ptr(), R * Cn, dw.data_ptr(), lp.data_ptr(),
+                            ch.data_ptr(), None)
+        if combine:
+            E.combine(lp.data_ptr(), R * Cn, 1.0 / world, 0, 0, out.data_ptr(), st.cuda_stream)
+        ctx.close()
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    e0.record(st)
+    for _ in range(a.iters):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.iters
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(st)
+    for _ in range(100):
+        E.combine(lp.data_ptr(), R * Cn, 1.0 / world, 0, 0, out.data_ptr(), st.cuda_stream)
+    c1.record(st)
+    torch.cuda.synchronize()
+    red_us = 1000 * c0.elapsed_time(c1) / 100
+    t = torch.tensor([ms, red_us], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, red_us = (float(x) for x in t.tolist())
+    if rank == 0:
+        print(json.dumps({"workload": "ens", "members": world, "gpus": world, "precision": a.precision,
+                          "ms_per_batch": ms, "combined_word_scores_per_s": R * Cn / (ms / 1000),
+                          "reduce_us": red_us, "message_bytes": 4 * R * Cn,
+                          "batch": "encode Tx=50 + 1024 injected parents x 3 words per member, device C ABI",
+                          "timing": "CUDA events on the model stream, max over ranks"}), flush=True)
+    E.close()
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["c3", "sweep", "beam", "avg"])
+    ap.add_argument("what", choices=["c3", "sweep", "beam", "avg", "encb", "c5", "ens"])
     ap.add_argument("--precision", default="bf16")
     ap.add_argument("--readout", default="tanh")
     ap.add_argument("--sentences", type=int, default=10)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--batches", default="64,256,1024,4096,16384")
+    ap.add_argument("--row_budget", type=float, default=2e6)
+    ap.add_argument("--enc_chunk", type=int, default=64)
     a = ap.parse_args()
-    {"c3": c3, "sweep": sweep, "beam": beam, "avg": avg}[a.what](a)
+    {"c3": c3, "sweep": sweep, "beam": beam, "avg": avg, "encb": encb, "c5": c5, "ens": ens}[a.what](a)
