@@ -149,7 +149,8 @@ NMT_API nmt_status nmt_encode_dev(nmt_model* m, const int32_t* src_ids, int32_t 
  * (tensor-bound when hundreds of sentences are batched); results agree with
  * nmt_encode within the precision's tolerance, not bit for bit.  Errors as nmt_encode, checked for
  * every sentence before any work (the message names the sentence); on error no context is created.
- * n == 0 is a no-op.  Asynchronous on the model stream.                                         */
+ * n == 0 is a no-op.  Up to 8 sentences are encoded one by one with nmt_encode's kernel (faster
+ * there).  Asynchronous on the model stream.                                                    */
 NMT_API nmt_status nmt_encode_batch(nmt_model* m, int32_t n, const int32_t* ids, const int32_t* offsets,
                                     nmt_ctx** outs);
 /* Releases the context; its arena is kept by the model for reuse by a later nmt_encode. */
@@ -209,6 +210,9 @@ NMT_API nmt_status nmt_score_forest(nmt_ctx* c, int32_t n_pairs, const nmt_state
                                     nmt_state* out_state, int32_t* stats);
 /* Waits for the model stream and reports a device-side validation error of earlier _dev calls. */
 NMT_API nmt_status nmt_ctx_check(nmt_ctx* c);
+/* Grows the context's arena to hold n_nodes nodes and n_stepped stepped nodes without further
+ * reallocation (a decoder that knows its stack sizes avoids the doubling copies).  Never shrinks. */
+NMT_API nmt_status nmt_ctx_reserve(nmt_ctx* c, int64_t n_nodes, int64_t n_stepped);
 /* Number of nodes and stepped nodes in the context's arena (synchronises the stream). */
 NMT_API nmt_status nmt_ctx_stats(nmt_ctx* c, int64_t* n_nodes, int64_t* n_stepped);
 

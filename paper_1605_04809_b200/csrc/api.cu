@@ -1640,6 +1640,15 @@ nmt_status nmt_encode_batch(nmt_model* m, int32_t n, const int32_t* ids, const i
                                            " outside [0, " + std::to_string(m->Vs) + ")");
   return guard([&] {
     std::lock_guard<std::mutex> lk(m->mu);
+    // a few sentences: the single-sentence persistent recurrence kernel is faster than 2 Tx_max
+    // launches (measured crossover ~10 sentences, profiles/r01/encode_batch.jsonl)
+    static const int small_n = getenv("NMT_ENCB_SMALL") ? atoi(getenv("NMT_ENCB_SMALL")) : 8;  // (diagnostic)
+    if (n <= small_n) {
+      std::vector<std::unique_ptr<nmt_ctx>> cs;
+      for (int b = 0; b < n; ++b) cs.emplace_back(encode_impl(m, ids + offsets[b], nullptr, offsets[b + 1] - offsets[b]));
+      for (int b = 0; b < n; ++b) outs[b] = cs[b].release();
+      return;
+    }
     encode_batch_impl(m, n, ids, offsets, outs);
   });
 }
@@ -2253,6 +2262,17 @@ nmt_status nmt_ctx_stats(nmt_ctx* c, int64_t* n_nodes, int64_t* n_stepped) {
     c->sync_counters();
     if (n_nodes) *n_nodes = c->n_nodes;
     if (n_stepped) *n_stepped = c->n_slots - 2;  // slots 0 (s0) and 1 (scratch) are not steps
+  });
+}
+
+nmt_status nmt_ctx_reserve(nmt_ctx* c, int64_t n_nodes, int64_t n_stepped) {
+  if (!c || n_nodes < 0 || n_stepped < 0) return fail(NMT_ERR_INVALID_ARG, "bad argument");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->m->mu);
+    CK(cudaSetDevice(c->m->device));
+    if (c->stale) c->sync_counters();
+    if (n_nodes > c->node_cap) c->grow_nodes(n_nodes);
+    if (n_stepped + 2 > c->slot_cap) c->grow_slots(n_stepped + 2);
   });
 }
 

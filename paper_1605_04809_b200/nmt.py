@@ -28,7 +28,7 @@ EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "n
            "nmt_profile_read", "nmt_bench_gemm", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
            "nmt_ensemble_free", "nmt_params_average", "nmt_beam_step",
            "nmt_encode_batch", "nmt_save_params", "nmt_params_bytes", "nmt_random_params", "nmt_create_random",
-           "nmt_debug_vocab", "nmt_score_batch_multi"]
+           "nmt_debug_vocab", "nmt_score_batch_multi", "nmt_ctx_reserve"]
 
 
 N_STAGES = 19
@@ -147,6 +147,7 @@ def lib() -> C.CDLL:
             "nmt_create_random": (i32, [C.POINTER(Dims), C.c_uint64, C.c_float, C.POINTER(Opts), C.POINTER(vp)]),
             "nmt_debug_vocab": (i32, [vp, i32, vp, vp, vp, vp, vp, vp]),
             "nmt_score_batch_multi": (i32, [i32, vp, vp, vp, vp, vp, vp, vp]),
+            "nmt_ctx_reserve": (i32, [vp, i64, i64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -337,6 +338,9 @@ class Context:
 
     def check(self) -> None:
         _check(lib().nmt_ctx_check(self._h))
+
+    def reserve(self, n_nodes: int, n_stepped: int) -> None:
+        _check(lib().nmt_ctx_reserve(self._h, n_nodes, n_stepped))
 
     def stats(self) -> Tuple[int, int]:
         a, b = C.c_int64(), C.c_int64()

@@ -38,9 +38,11 @@ def _sources(vocab, lengths, seed):
     return [synth.make_source(vocab, L - 1, seed=seed + i) for i, L in enumerate(lengths)]
 
 
-def test_tiny_encode_batch_vs_oracle(tiny):
+@pytest.mark.parametrize("lengths", [[5, 1, 8, 3, 3, 12, 2, 7, 7, 9, 4, 6],  # batched path (> 8 sentences)
+                                     [4, 1, 9]])                             # small-n path (per sentence)
+def test_tiny_encode_batch_vs_oracle(tiny, lengths):
     d, p, M, om, prec = tiny
-    lengths = [5, 1, 8, 3, 3, 12, 2]  # ragged, a 1-token source (EOS only), equal lengths
+    # ragged, a 1-token source (EOS only), equal lengths
     srcs = _sources(d.vocab_src, lengths, 100)
     cs = M.encode_batch(srcs)
     assert len(cs) == len(srcs)
@@ -63,7 +65,7 @@ def test_tiny_encode_batch_vs_oracle(tiny):
 
 def test_tiny_encode_batch_matches_single(tiny):
     d, p, M, om, prec = tiny
-    srcs = _sources(d.vocab_src, [6, 4], 200)
+    srcs = _sources(d.vocab_src, [6, 4, 5, 3, 8, 2, 7, 6, 5, 4], 200)  # > 8: the batched path
     cs = M.encode_batch(srcs)
     for src, c in zip(srcs, cs):
         a = c.debug_encoder()

@@ -281,6 +281,8 @@ def c5(a):
         costs = [lens[i] * B for i in range(n_sent)]
         mine = lpt_shard(costs, world)[rank]
 
+        s_st, y_st = synth.make_states(B, d.dim_hid, d.vocab_tgt, seed=50000 + B)  # one stack's states
+
         def run(sents, count):
             edges = rows = naive = stacks = 0
             for c0 in range(0, len(sents), a.enc_chunk):
@@ -289,13 +291,17 @@ def c5(a):
                 ctxs = M.encode_batch(srcs)
                 for i, ctx in zip(chunk, ctxs):
                     g = np.random.default_rng(100000 * B + i)
-                    s, y = synth.make_states(B, d.dim_hid, d.vocab_tgt, seed=50000 + i)
-                    hyps = ctx.inject_states(s, y)
-                    for stk in range(lens[i] + 1):  # one stack per target position (~L)
-                        L = g.choice(4, size=B, p=[.4, .3, .2, .1]).astype(np.int32) + 1
+                    n_stk = lens[i] + 1  # one stack per target position (~L)
+                    L = g.choice(4, size=(n_stk, B), p=[.4, .3, .2, .1]).astype(np.int32) + 1
+                    words_all = synth.zipf_ids(g, int(L.sum()), d.vocab_tgt)
+                    ctx.reserve(int(L.sum()) + B + 1, int(L.sum()))
+                    hyps = ctx.inject_states(s_st, y_st)
+                    w0 = 0
+                    for stk in range(n_stk):
                         off = np.zeros(B + 1, np.int32)
-                        off[1:] = np.cumsum(L)
-                        words = synth.zipf_ids(g, int(off[-1]), d.vocab_tgt)
+                        off[1:] = np.cumsum(L[stk])
+                        words = words_all[w0:w0 + off[-1]]
+                        w0 += int(off[-1])
                         lp, fin, st = ctx.score_forest(hyps, off, words)
                         hyps = fin
                         if count:
@@ -305,7 +311,7 @@ def c5(a):
                             stacks += 1
                     ctx.close()
             return edges, rows, naive, stacks
-        run(mine[:1], False)  # warm-up (arena growth, workspace)
+        run(mine[:min(len(mine), 2)], False)  # warm-up (workspaces)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
@@ -325,8 +331,9 @@ def c5(a):
                               "sentences": int(nsent), "stacks": int(ns), "word_scores_per_s": e / dt,
                               "rows_per_s": r / dt, "naive_words": int(nv), "edges": int(e), "rows": int(r),
                               "seconds": dt, "row_budget": a.row_budget,
-                              "timing": "host wall clock (max over ranks) around encode_batch + inject + "
-                                        "L stacks of nmt_score_forest per sentence, host C ABI, synchronized"}),
+                              "timing": "host wall clock (max over ranks) around encode_batch + reserve + inject "
+                                        "+ L+1 stacks of nmt_score_forest per sentence (host C ABI, synchronized; "
+                                        "the synthetic request generation is inside the timed region)"}),
                   flush=True)
 
 
