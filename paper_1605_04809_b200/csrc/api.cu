@@ -185,6 +185,11 @@ struct nmt_model {
   float* in_s = nullptr;
   int* in_y = nullptr;              // [R_cap] y_prev staging of nmt_inject_states
   cudaStream_t cst = nullptr;       // copy stream of nmt_inject_states (overlaps the encoder)
+  // encoder stream: E3-E7 of nmt_encode run here, joined into the model stream right before the
+  // context's first dependent kernel (the step's state gather), so that the work queued in between
+  // (nmt_inject_states, the planner) overlaps the latency-bound recurrence
+  cudaStream_t est = nullptr;
+  cudaEvent_t enc_start_ev = nullptr;
   cudaEvent_t inj_copy_ev = nullptr, inj_done_ev = nullptr;
   CUtensorMap tm_As, tm_X, tm_At;
   // ScoreBatch forest workspace (nmt_score_forest)
@@ -247,6 +252,12 @@ static void free_all_model(nmt_model* m) {
   m->pin = nullptr;
   if (m->pin2_ev) cudaEventDestroy(m->pin2_ev);
   m->pin2_ev = nullptr;
+  if (m->est) {
+    cudaStreamSynchronize(m->est);
+    cudaStreamDestroy(m->est);
+    cudaEventDestroy(m->enc_start_ev);
+    m->est = nullptr;
+  }
   if (m->cst) {
     cudaStreamSynchronize(m->cst);
     cudaStreamDestroy(m->cst);
@@ -382,6 +393,9 @@ struct nmt_ctx {
   // host mirror of the device counters (exact when !stale; otherwise upper bounds)
   int64_t n_nodes = 0, n_slots = 0;
   bool stale = false;
+  cudaEvent_t enc_ev = nullptr;  // end of this context's encoder work on the encoder stream
+  bool enc_pending = false;      // the model stream has not waited for enc_ev yet
+  void join_enc();
 
   CtxDev dev() const {
     CtxDev c{};
@@ -418,7 +432,16 @@ static T* grow_copy(T* old, size_t old_n, size_t new_n, cudaStream_t st) {
   return p;
 }
 
+// order the model stream after this context's encoder work (once)
+void nmt_ctx::join_enc() {
+  if (enc_pending) {
+    CK(cudaStreamWaitEvent(m->st, enc_ev, 0));
+    enc_pending = false;
+  }
+}
+
 void nmt_ctx::sync_counters() {
+  join_enc();
   int h[CNT_N];
   CK(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, m->st));
   CK(cudaStreamSynchronize(m->st));
@@ -485,6 +508,7 @@ void nmt_ctx::grow_slots(int64_t need) {
 
 void nmt_ctx::ensure(int64_t add_nodes, int64_t add_slots) {
   if (n_nodes + add_nodes > node_cap || n_slots + add_slots > slot_cap) {
+    join_enc();  // (the encoder writes slot 0 of S)
     if (stale) sync_counters();
     if (n_nodes + add_nodes > node_cap) grow_nodes(n_nodes + add_nodes);
     if (n_slots + add_slots > slot_cap) grow_slots(n_slots + add_slots);
@@ -500,6 +524,8 @@ nmt_ctx::~nmt_ctx() {
     cudaSetDevice(m->device);
     cudaStreamSynchronize(m->st);
   }
+  if (m && m->est) cudaStreamSynchronize(m->est);
+  if (enc_ev) cudaEventDestroy(enc_ev);
   for (int** p : {&counters, &node_word, &node_parent, &node_src, &node_slot, &node_claim, &hvals, &amax}) dfree(*p);
   dfree(hkeys);
   for (float** p : {&ctx, &pctx, &S, &T, &logZ}) dfree(*p);
@@ -887,6 +913,8 @@ static void parse_and_build(const char* buf, size_t len, const nmt_opts* opts, n
     CK(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
     m->own_stream = true;
   }
+  CK(cudaStreamCreateWithFlags(&m->est, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&m->enc_start_ev, cudaEventDisableTiming));
   m->split = o.precision == NMT_PREC_FP32CLASS;
   if (const char* ev = getenv("NMT_PAIR")) m->use_pair = atoi(ev) != 0;
   m->sf = m->split ? 2 : 1;
@@ -1028,6 +1056,7 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
   const int Hp = m->Hp, Cp = m->Cp, Ep = m->Ep;
   const bool sp = m->split;
   const int rps = round_up(std::max(R_max, 1), 256);  // rows per split-K partial
+  c->join_enc();  // s0 (slot 0), ctx and pctx come from the encoder
   { ProfScope p_(m, ST_GATHER); step_elementwise(EW_GATHER, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   if (!stage_skipped(ST_GEMM_H1)) {
     ProfScope p_(m, ST_GEMM_H1);
@@ -1326,6 +1355,7 @@ static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
     c->ctx = dalloc<float>((size_t)m->maxTx * m->Cp);
     c->pctx = dalloc<float>((size_t)m->maxTx * m->Cp);
     c->counters = dalloc<int>(CNT_N);
+    CK(cudaEventCreateWithFlags(&c->enc_ev, cudaEventDisableTiming));
     c->grow_nodes(4096);
     c->grow_slots(1024);
     g.release();
@@ -1341,9 +1371,17 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
   std::unique_ptr<nmt_ctx> guard_c(acquire_ctx(m, len));
   nmt_ctx* c = guard_c.get();
   ctx_reset(c->dev(), c->hcap, st);  // counters, root node, empty hash table
+  // E1-E7 on the encoder stream (ordered after everything queued on the model stream so far); the
+  // model stream joins it before the context's first dependent kernel (nmt_ctx::join_enc)
+  static const bool sep = !(getenv("NMT_ENC_STREAM") && atoi(getenv("NMT_ENC_STREAM")) == 0);  // (diagnostic)
+  const cudaStream_t es = (sep && m->prof_mode == 0) ? m->est : st;
+  if (es != st) {
+    CK(cudaEventRecord(m->enc_start_ev, st));
+    CK(cudaStreamWaitEvent(es, m->enc_start_ev, 0));
+  }
   const int* d_src = src_dev;
   if (src_host) {
-    CK(cudaMemcpyAsync(m->d_src, src_host, (size_t)len * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m->d_src, src_host, (size_t)len * 4, cudaMemcpyHostToDevice, es));
     d_src = m->d_src;
   }
   {  // E1-E6: gather of the precomputed input projections, bi-GRU recurrence, means, s0, ctx hi|lo
@@ -1367,8 +1405,8 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
     e.S0 = c->S;
     ProfScope p_(m, ST_ENC_RECUR);
     if (++m->enc_epoch > 65535) {  // tags carry a 16-bit epoch: reset them before it repeats
-      CK(cudaMemsetAsync(m->hbuf, 0, (size_t)2 * 2 * 131072 * sizeof(float), st));
-      CK(cudaMemsetAsync(m->bar, 0, sizeof(int), st));
+      CK(cudaMemsetAsync(m->hbuf, 0, (size_t)2 * 2 * 131072 * sizeof(float), es));
+      CK(cudaMemsetAsync(m->bar, 0, sizeof(int), es));
       m->enc_epoch = 1;
     }
     e.epoch = m->enc_epoch;
@@ -1383,11 +1421,11 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
     }
     const bool trace = getenv("NMT_ENC_TRACE") != nullptr;  // diagnostic: per-step phase stamps
     if (trace) CK(cudaMalloc(&e.trace, ((size_t)(len + 1) * 8 + 2 * 2 * m->NB) * sizeof(long long)));
-    if (!stage_skipped(ST_ENC_RECUR)) enc_recur(e, len, st);
+    if (!stage_skipped(ST_ENC_RECUR)) enc_recur(e, len, es);
     if (trace) {
       std::vector<long long> tv((size_t)(len + 1) * 8 + 2 * 2 * m->NB);
-      CK(cudaMemcpyAsync(tv.data(), e.trace, tv.size() * 8, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpyAsync(tv.data(), e.trace, tv.size() * 8, cudaMemcpyDeviceToHost, es));
+      CK(cudaStreamSynchronize(es));
       cudaFree(e.trace);
       double ph[6] = {0, 0, 0, 0, 0, 0};
       for (int t = 2; t < len - 1; ++t) {
@@ -1432,8 +1470,12 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
       g.ksplit = (nkb + chunk - 1) / chunk;
     }
     const size_t stride = (size_t)m->Tpad * m->Cp;
-    gemm_store(m->tm_ctxbf, m->tm_Watt, g, m->ksplit_buf, m->Cp, g.ksplit * m->Tpad, nullptr, len, st, stride);
-    splitk_reduce(m->ksplit_buf, g.ksplit, stride, len, m->Cp, m->Cp, m->b_att, c->pctx, st);
+    gemm_store(m->tm_ctxbf, m->tm_Watt, g, m->ksplit_buf, m->Cp, g.ksplit * m->Tpad, nullptr, len, es, stride);
+    splitk_reduce(m->ksplit_buf, g.ksplit, stride, len, m->Cp, m->Cp, m->b_att, c->pctx, es);
+  }
+  if (es != st) {
+    CK(cudaEventRecord(c->enc_ev, es));
+    c->enc_pending = true;
   }
   c->n_nodes = 1;
   c->n_slots = 2;
@@ -1660,6 +1702,11 @@ void nmt_ctx_free(nmt_ctx* c) {
   nmt_model* m = c->m;
   {
     std::lock_guard<std::mutex> lk(m->mu);
+    cudaSetDevice(m->device);
+    try {
+      c->join_enc();  // later model-stream work on the reused arena follows its encoder
+    } catch (...) {
+    }
     c->m = nullptr;  // pooled arenas hold no model reference; stream order protects their reuse
     m->pool.push_back(c);
   }
@@ -2238,6 +2285,7 @@ nmt_status nmt_ctx_check(nmt_ctx* c) {
   return guard([&] {
     std::lock_guard<std::mutex> lk(c->m->mu);
     CK(cudaSetDevice(c->m->device));
+    c->join_enc();
     int h[CNT_N];
     CK(cudaMemcpyAsync(h, c->counters, sizeof(h), cudaMemcpyDeviceToHost, c->m->st));
     CK(cudaStreamSynchronize(c->m->st));
@@ -2392,6 +2440,7 @@ nmt_status nmt_debug_encoder(nmt_ctx* c, float* ctx, float* pctx, float* s0) {
     std::lock_guard<std::mutex> lk(m->mu);
     CK(cudaSetDevice(m->device));
     const int H = m->H, Hp = m->Hp, Cp = m->Cp, Tx = c->Tx;
+    c->join_enc();
     std::vector<float> a((size_t)Tx * Cp), b((size_t)Tx * Cp), s(Hp);
     CK(cudaMemcpyAsync(a.data(), c->ctx, a.size() * 4, cudaMemcpyDeviceToHost, m->st));
     CK(cudaMemcpyAsync(b.data(), c->pctx, b.size() * 4, cudaMemcpyDeviceToHost, m->st));
