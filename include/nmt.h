@@ -217,7 +217,10 @@ NMT_API nmt_status nmt_ctx_reserve(nmt_ctx* c, int64_t n_nodes, int64_t n_steppe
 NMT_API nmt_status nmt_ctx_stats(nmt_ctx* c, int64_t* n_nodes, int64_t* n_stepped);
 
 /* ---- synthetic parents (bench / tests): n nodes with given input state s[n x H] [host] and
- * previous word y_prev[n] [host] (-1 = BOS), not children of any node.                         */
+ * previous word y_prev[n] [host] (-1 = BOS), not children of any node.  Pageable arrays are
+ * copied before the call returns; page-locked arrays are read asynchronously (the upload overlaps
+ * the encoder) and must stay unchanged until the next synchronising call on the context
+ * (nmt_score_batch, nmt_score_forest, nmt_beam_step, nmt_ctx_check, nmt_ctx_stats) returns.      */
 NMT_API nmt_status nmt_inject_states(nmt_ctx* c, int32_t n, const float* s, const int32_t* y_prev, nmt_state* out);
 
 /* Device variant: s [dev, n x H floats], y_prev [dev, n], out [dev, n int32 node ids]; async.  */

@@ -2339,9 +2339,7 @@ nmt_status nmt_inject_states(nmt_ctx* c, int32_t n, const float* s, const int32_
     c->ensure(n, n);
     // The upload runs on a copy stream: it depends only on the previous inject kernel having read
     // the staging buffers, not on the work queued before it (e.g. the encoder of this sentence), so
-    // the DMA overlaps that work.  Copies come straight from the caller's arrays; for page-locked
-    // sources the call waits for the DMA only (not for any kernel), so the caller may reuse its
-    // buffers on return - pageable sources are staged synchronously by cudaMemcpyAsync itself.
+    // the DMA overlaps that work - and, for page-locked sources, the host's queueing of the step.
     if (!m->cst) {
       CK(cudaStreamCreateWithFlags(&m->cst, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&m->inj_copy_ev, cudaEventDisableTiming));
@@ -2351,10 +2349,8 @@ nmt_status nmt_inject_states(nmt_ctx* c, int32_t n, const float* s, const int32_
     CK(cudaMemcpyAsync(m->in_s, s, (size_t)n * m->H * 4, cudaMemcpyHostToDevice, m->cst));
     CK(cudaMemcpyAsync(m->in_y, y, (size_t)n * 4, cudaMemcpyHostToDevice, m->cst));
     CK(cudaEventRecord(m->inj_copy_ev, m->cst));
-    cudaPointerAttributes pa;
-    if (cudaPointerGetAttributes(&pa, s) == cudaSuccess && pa.type == cudaMemoryTypeHost)
-      CK(cudaEventSynchronize(m->inj_copy_ev));
-    cudaGetLastError();  // (clear a possible "invalid value" from cudaPointerGetAttributes)
+    // (page-locked sources: no wait here - the caller keeps them unchanged until the next
+    // synchronising call, include/nmt.h; pageable ones were staged by cudaMemcpyAsync itself)
     CK(cudaStreamWaitEvent(st, m->inj_copy_ev, 0));
     {
       ProfScope p_(m, ST_INJECT);
