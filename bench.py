@@ -314,7 +314,7 @@ def run_ours(a, rank: int, world: int, dist) -> None:
     flops = 2.0 * R * d.vocab_tgt * d.dim_emb
     achieved = flops / (vocab_ms / 1000.0) / 1e12
     peaks = measured_peaks()
-    roof = {"kernel": "k_gemm<256,4,EPI_LSE> (vocab GEMM + online log-sum-exp)", "bound": "tensor",
+    roof = {"kernel": "k_gemm<256,6,EPI_LSE,pair> (CTA-pair vocab GEMM + online log-sum-exp)", "bound": "tensor",
             "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
             "frac": achieved / peaks["bf16_tflops"], "traffic": ncu_traffic(),
             "peak_source": peaks["source"] + " bf16 burst", "algorithmic_flops_per_launch": flops,
