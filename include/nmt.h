@@ -180,8 +180,11 @@ NMT_API nmt_status nmt_score_batch_dev(nmt_ctx* c, int32_t n_parents, const int3
 /* Several sentences in one call: parent k is a state of ctx_per_parent[k] [host,
  * n_parents; all contexts of one model, else NMT_ERR_INVALID_ARG]; every other argument, output
  * and error as nmt_score_batch, in input order (child handles belong to their parent's context).
- * Parents are grouped by context in first-appearance order; the groups' steps are issued back to
- * back on the model stream with one host synchronisation for the whole call.                     */
+ * All contexts' new rows go through ONE fused decoder step (each row attends over its own
+ * sentence and writes its own arena; every context's rows start at a multiple of 4), with one
+ * planner pass and one gather-dot over all contexts and one host synchronisation.  Child ids are
+ * those per-context nmt_score_batch calls would give; log-probs agree with them up to fp32
+ * summation order (split-K factors depend on the fused row count).                             */
 NMT_API nmt_status nmt_score_batch_multi(int32_t n_parents, nmt_ctx* const* ctx_per_parent, const nmt_state* parents,
                                          const int32_t* cand_offsets, const int32_t* cand_words, float* out_logprob,
                                          nmt_state* out_child, int32_t* out_argmax);

@@ -192,6 +192,12 @@ struct nmt_model {
   cudaEvent_t enc_start_ev = nullptr;
   cudaEvent_t inj_copy_ev = nullptr, inj_done_ev = nullptr;
   CUtensorMap tm_As, tm_X, tm_At;
+  // multi-context step workspace (nmt_score_batch_multi): ints (bcount | snap | R | row_grp) and
+  // the group descriptors (PlanDesc[G] | GrpStep[G])
+  int* mws_i = nullptr;
+  size_t mws_i_cap = 0;
+  char* mws_b = nullptr;
+  size_t mws_b_cap = 0;
   // ScoreBatch forest workspace (nmt_score_forest)
   int* fws_i = nullptr;
   size_t fws_i_cap = 0;
@@ -248,6 +254,8 @@ static void free_all_model(nmt_model* m) {
   m->free_ws();
   dfree(m->fws_i);
   dfree(m->fws_f);
+  dfree(m->mws_i);
+  dfree(m->mws_b);
   if (m->pin) cudaFreeHost(m->pin);
   m->pin = nullptr;
   if (m->pin2_ev) cudaEventDestroy(m->pin2_ev);
@@ -1047,16 +1055,31 @@ static void gemm_auto(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b12
   gemm_split(m, a, b128, g, out, ldc, rps, m->P_rows, M_max, max_ks, st);
 }
 
-// one decoder forward step over the rows planned in m->row_* (count at c->counters[CNT_R])
-static void run_step(nmt_model* m, nmt_ctx* c, int R_max) {
+// multi-context step (nmt_score_batch_multi): device row count, per-row group, per-group arenas
+struct MultiStep {
+  const int* R_dev;
+  const int* row_grp;
+  const GrpStep* gs;
+  int max_Tx;
+};
+
+// one decoder forward step over the rows planned in m->row_* (count at c->counters[CNT_R]; or, for
+// a multi-context step, *ms->R_dev rows of the contexts in ms->gs, dead rows flagged row_dst < 0)
+static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = nullptr) {
   cudaStream_t st = m->st;
   StepDev d = step_view(m, c);
   AttnCtx a{c->pctx, c->ctx, m->U_att, m->c_tt, c->Tx};
+  if (ms) {
+    d.R = ms->R_dev;
+    d.row_grp = ms->row_grp;
+    d.gs = ms->gs;
+    a.Tx = ms->max_Tx;  // (shared-memory sizing; each CTA takes its group's pctx, ctx and Tx)
+  }
   const int* Rd = d.R;
   const int Hp = m->Hp, Cp = m->Cp, Ep = m->Ep;
   const bool sp = m->split;
   const int rps = round_up(std::max(R_max, 1), 256);  // rows per split-K partial
-  c->join_enc();  // s0 (slot 0), ctx and pctx come from the encoder
+  if (!ms) c->join_enc();  // s0 (slot 0), ctx and pctx come from the encoder (multi: the caller joins)
   { ProfScope p_(m, ST_GATHER); step_elementwise(EW_GATHER, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   if (!stage_skipped(ST_GEMM_H1)) {
     ProfScope p_(m, ST_GEMM_H1);
@@ -1999,25 +2022,52 @@ nmt_status nmt_score_batch_multi(int32_t np, nmt_ctx* const* cpp, const nmt_stat
         throw NmtError(NMT_ERR_BAD_STATE, "unknown state " + std::to_string(parents[k]) + " (parents[" +
                                               std::to_string(k) + "])");
     // per group: parents | offsets | words, concatenated; positions back into the input order
-    std::vector<std::vector<int>> gpar(G), gcand(G);
+    std::vector<std::vector<int>> gpar(G);
     for (int k = 0; k < np; ++k) gpar[grp[k]].push_back(k);
+    // rows of the fused step: group g owns rows [rbase[g], rbase[g] + roundup(n_par_g, 4)) (attention
+    // CTAs never straddle two sentences); rows its planner does not fill stay dead (row_dst = -1)
+    std::vector<int> gnc(G, 0), rbase(G + 1, 0);
     int max_np = 0, max_nc = 0;
     for (int g = 0; g < G; ++g) {
-      int n = 0;
-      for (int k : gpar[g]) n += off[k + 1] - off[k];
+      for (int k : gpar[g]) gnc[g] += off[k + 1] - off[k];
       max_np = std::max(max_np, (int)gpar[g].size());
-      max_nc = std::max(max_nc, n);
+      max_nc = std::max(max_nc, gnc[g]);
+      rbase[g + 1] = rbase[g] + round_up((int)gpar[g].size(), 4);
     }
-    m->ensure_ws(np + G, nc);  // one slice per group, each at its own offset (G + np offsets)
-    for (int g = 0; g < G; ++g) {
-      int n = 0;
-      for (int k : gpar[g]) n += off[k + 1] - off[k];
-      ctxs[g]->ensure(n, (int64_t)gpar[g].size());
+    const int total_rows = rbase[G];
+    m->ensure_ws(std::max(total_rows, np + G), nc);  // (G + np offsets)
+    for (int g = 0; g < G; ++g) ctxs[g]->ensure(gnc[g], (int64_t)gpar[g].size());
+    for (nmt_ctx* c : ctxs) c->join_enc();
+    const int Bblk = (max_nc + 255) / 256 + std::max(1, (max_np + 255) / 256);
+    const size_t need_i = (size_t)G * Bblk + 4 * (size_t)G + 1 + total_rows;
+    const size_t need_b = (size_t)G * (sizeof(PlanDesc) + sizeof(GrpStep));
+    if (need_i > m->mws_i_cap || need_b > m->mws_b_cap) {
+      CK(cudaStreamSynchronize(st));
+      if (need_i > m->mws_i_cap) {
+        dfree(m->mws_i);
+        m->mws_i_cap = std::max(need_i, m->mws_i_cap * 2);
+        m->mws_i = dalloc<int>(m->mws_i_cap);
+      }
+      if (need_b > m->mws_b_cap) {
+        dfree(m->mws_b);
+        m->mws_b_cap = std::max(need_b, m->mws_b_cap * 2);
+        m->mws_b = dalloc<char>(m->mws_b_cap);
+      }
     }
-    int* h = static_cast<int*>(m->pinned((size_t)(2 * np + G + nc) * 4 + (size_t)(2 * nc + np) * 4 + 64));
-    int* hp = h;
-    int* ho = hp + np;        // G + np offsets (each group's CSR starts at 0)
+    int* d_bcount = m->mws_i;
+    int* d_snap = d_bcount + (size_t)G * Bblk;
+    int* d_R = d_snap + 4 * G;
+    int* d_rowgrp = d_R + 1;
+    PlanDesc* d_desc = reinterpret_cast<PlanDesc*>(m->mws_b);
+    GrpStep* d_gs = reinterpret_cast<GrpStep*>(m->mws_b + (size_t)G * sizeof(PlanDesc));
+    // host staging (pinned): parents | offsets (G + np) | words | R | row_grp | descriptors
+    const size_t ints = (size_t)np + np + G + nc + 1 + total_rows;
+    char* hbuf = static_cast<char*>(m->pinned(ints * 4 + need_b + (size_t)(2 * nc + np) * 4 + 256));
+    int* hp = reinterpret_cast<int*>(hbuf);
+    int* ho = hp + np;
     int* hw = ho + np + G;
+    int* hR = hw + nc;
+    int* hrg = hR + 1;
     std::vector<int> pbase(G + 1, 0), cbase(G + 1, 0), cpos;  // group slices; candidate positions
     cpos.reserve(nc);
     for (int g = 0, P = 0, Cc = 0; g < G; ++g) {
@@ -2036,15 +2086,54 @@ nmt_status nmt_score_batch_multi(int32_t np, nmt_ctx* const* cpp, const nmt_stat
       }
       pbase[g + 1] = P;
       cbase[g + 1] = Cc;
+      for (int r = rbase[g]; r < rbase[g + 1]; ++r) hrg[r] = g;
+    }
+    *hR = total_rows;
+    char* hdesc = hbuf + ((ints * 4 + 15) / 16) * 16;
+    PlanDesc* hd = reinterpret_cast<PlanDesc*>(hdesc);
+    GrpStep* hg = reinterpret_cast<GrpStep*>(hdesc + (size_t)G * sizeof(PlanDesc));
+    for (int g = 0; g < G; ++g) {
+      nmt_ctx* c = ctxs[g];
+      const int gn = pbase[g + 1] - pbase[g], gc = cbase[g + 1] - cbase[g], rb = rbase[g];
+      PlanIO io = plan_io(m, gn, gc, m->in_par + pbase[g], m->in_off + pbase[g] + g, m->in_words + cbase[g]);
+      io.cand_k += cbase[g];
+      io.cand_hslot += cbase[g];
+      io.cflag += cbase[g];
+      io.row_src += rb;
+      io.row_y += rb;
+      io.row_dst += rb;
+      io.row_node += rb;
+      io.pflag += rb;
+      io.bcount = d_bcount + (size_t)g * Bblk;
+      io.snap = d_snap + 4 * g;
+      hd[g].c = c->dev();
+      hd[g].io = io;
+      hd[g].R_out = c->counters + CNT_R;
+      hd[g].out_logp = m->out_logp + cbase[g];
+      hd[g].out_child = m->out_child + cbase[g];
+      hd[g].out_argmax = m->out_amax + pbase[g];
+      hg[g] = GrpStep{c->S, c->T, c->logZ, c->amax, c->pctx, c->ctx, c->Tx};
     }
     CK(cudaMemcpyAsync(m->in_par, hp, (size_t)np * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(m->in_off, ho, (size_t)(np + G) * 4, cudaMemcpyHostToDevice, st));
     if (nc) CK(cudaMemcpyAsync(m->in_words, hw, (size_t)nc * 4, cudaMemcpyHostToDevice, st));
-    for (int g = 0; g < G; ++g) {
-      const int gn = pbase[g + 1] - pbase[g], gc = cbase[g + 1] - cbase[g];
-      const PlanIO io = plan_io(m, gn, gc, m->in_par + pbase[g], m->in_off + pbase[g] + g, m->in_words + cbase[g]);
-      run_call(m, ctxs[g], io, m->out_logp + cbase[g], m->out_child + cbase[g], nullptr, m->out_amax + pbase[g]);
+    CK(cudaMemcpyAsync(d_R, hR, (size_t)(1 + total_rows) * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m->mws_b, hdesc, need_b, cudaMemcpyHostToDevice, st));
+    fill_i32(m->row_dst, total_rows, -1, st);
+    {
+      ProfScope p_(m, ST_PLAN);
+      plan_multi(d_desc, G, max_nc, max_np, st);
     }
+    int max_Tx = 1;
+    for (nmt_ctx* c : ctxs) max_Tx = std::max(max_Tx, c->Tx);
+    const MultiStep ms{d_R, d_rowgrp, d_gs, max_Tx};
+    run_step(m, ctxs[0], total_rows, &ms);
+    {
+      ProfScope p_(m, ST_GATHERDOT);
+      gather_dot_multi(d_desc, G, max_nc, max_np, m->W_o32, m->b_o, m->Ep, st);
+    }
+    char* hres = hdesc + need_b;
+    hw = reinterpret_cast<int*>(hres) - nc;  // (results follow the staging: rl = hw + nc below)
     float* rl = reinterpret_cast<float*>(hw + nc);
     int* rc = reinterpret_cast<int*>(rl + nc);
     int* ra = rc + nc;

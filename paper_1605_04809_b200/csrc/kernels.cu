@@ -140,8 +140,12 @@ NMT_DEV int hash_insert(unsigned long long* keys, uint64_t mask, int64_t key) {
 }
 
 constexpr int kPlanSmemOffsets = 8192;  // offsets staged in shared memory up to this many parents
-__global__ void k_plan_intern(CtxDev c, PlanIO io) {
+__global__ void k_plan_intern(CtxDev c, PlanIO io, const PlanDesc* __restrict__ gd) {
   pdl_enter();
+  if (gd) {  // multi-context call: this block row serves group blockIdx.y
+    c = gd[blockIdx.y].c;
+    io = gd[blockIdx.y].io;
+  }
   __shared__ int soff[kPlanSmemOffsets + 1];
   const bool use_smem = io.n_par + 1 <= kPlanSmemOffsets + 1;
   const int* offs = io.offsets;
@@ -224,10 +228,16 @@ NMT_DEV int block_count(int v, int* red) {  // sum over a 256-thread block
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
   return t;
 }
-__global__ void __launch_bounds__(kPlanBlock) k_plan_flags(CtxDev c, PlanIO io, int Bc) {
+__global__ void __launch_bounds__(kPlanBlock) k_plan_flags(CtxDev c, PlanIO io, int Bc, const PlanDesc* __restrict__ gd) {
   pdl_enter();
   __shared__ int red[8];
   const int b = blockIdx.x;
+  if (gd) {
+    c = gd[blockIdx.y].c;
+    io = gd[blockIdx.y].io;
+    Bc = (io.n_cand + kPlanBlock - 1) / kPlanBlock;
+    if (b >= Bc + max(1, (io.n_par + kPlanBlock - 1) / kPlanBlock)) return;
+  }
   int f = 0;
   if (b < Bc) {
     const int i = b * kPlanBlock + threadIdx.x;
@@ -256,10 +266,19 @@ __global__ void __launch_bounds__(kPlanBlock) k_plan_flags(CtxDev c, PlanIO io, 
   }
 }
 
-__global__ void __launch_bounds__(kPlanBlock) k_plan_assign(CtxDev c, PlanIO io, int Bc, int Bp, int* R_out) {
+__global__ void __launch_bounds__(kPlanBlock) k_plan_assign(CtxDev c, PlanIO io, int Bc, int Bp, int* R_out,
+                                                            const PlanDesc* __restrict__ gd) {
   pdl_enter();
   __shared__ int red[32];
   const int b = blockIdx.x;
+  if (gd) {
+    c = gd[blockIdx.y].c;
+    io = gd[blockIdx.y].io;
+    R_out = gd[blockIdx.y].R_out;
+    Bc = (io.n_cand + kPlanBlock - 1) / kPlanBlock;
+    Bp = max(1, (io.n_par + kPlanBlock - 1) / kPlanBlock);
+    if (b >= Bc + Bp) return;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool cand = b < Bc;
   const int b0 = cand ? 0 : Bc, bi = cand ? b : b - Bc;
@@ -324,15 +343,31 @@ __global__ void __launch_bounds__(kPlanBlock) k_plan_assign(CtxDev c, PlanIO io,
 
 void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st) {
   const int n = io.n_cand > io.n_par ? io.n_cand : io.n_par;
+  const PlanDesc* none = nullptr;
   if (n > 0) {
-    launch_pdl(k_plan_intern, (n + 255) / 256, 256, 0, st, c, io);
+    launch_pdl(k_plan_intern, (n + 255) / 256, 256, 0, st, c, io, none);
     CK_LAUNCH();
   }
   const int Bc = (io.n_cand + kPlanBlock - 1) / kPlanBlock, Bp = (io.n_par + kPlanBlock - 1) / kPlanBlock;
   const int B = Bc + Bp > 0 ? Bc + Bp : 1;
-  launch_pdl(k_plan_flags, B, kPlanBlock, 0, st, c, io, Bc);
+  launch_pdl(k_plan_flags, B, kPlanBlock, 0, st, c, io, Bc, none);
   CK_LAUNCH();
-  launch_pdl(k_plan_assign, B, kPlanBlock, 0, st, c, io, Bc, Bp, R_dev);
+  launch_pdl(k_plan_assign, B, kPlanBlock, 0, st, c, io, Bc, Bp, R_dev, none);
+  CK_LAUNCH();
+}
+void plan_multi(const PlanDesc* descs, int G, int max_cand, int max_par, cudaStream_t st) {
+  const CtxDev c{};
+  const PlanIO io{};
+  const int n = std::max(max_cand, max_par);
+  if (n > 0) {
+    launch_pdl(k_plan_intern, dim3((n + 255) / 256, G), 256, 0, st, c, io, descs);
+    CK_LAUNCH();
+  }
+  const int B = (max_cand + kPlanBlock - 1) / kPlanBlock + std::max(1, (max_par + kPlanBlock - 1) / kPlanBlock);
+  launch_pdl(k_plan_flags, dim3(B, G), kPlanBlock, 0, st, c, io, 0, descs);
+  CK_LAUNCH();
+  int* no_r = nullptr;
+  launch_pdl(k_plan_assign, dim3(B, G), kPlanBlock, 0, st, c, io, 0, 0, no_r, descs);
   CK_LAUNCH();
 }
 
@@ -490,7 +525,8 @@ __global__ void k_gather_state(StepDev d, const float* __restrict__ S) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = idx / H4, j = (idx % H4) * 4;
   if (r >= *d.R) return;
-  const float4 v = ld4(S + (int64_t)d.row_src[r] * d.Hp + j);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);  // dead rows of a multi-context step: zeros
+  if (d.row_dst[r] >= 0) v = ld4((d.gs ? d.gs[d.row_grp[r]].S : S) + (int64_t)d.row_src[r] * d.Hp + j);
   store_split4(d.A_s + (int64_t)r * d.lda_s + j, d.lo_s, v);
 }
 
@@ -501,13 +537,15 @@ __global__ void k_gru1(StepDev d, const float* __restrict__ S) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = idx / H4, j = (idx % H4) * 4;
   if (r >= *d.R) return;
-  const int y = d.row_y[r];
+  const bool live = d.row_dst[r] >= 0;
+  const int y = live ? d.row_y[r] : -1;
   const float* g = d.G1 + (int64_t)r * 3 * Hp + j;
   const float* ex = d.Ex + (int64_t)(y < 0 ? d.V : y) * 3 * Hp + j;
   const float4 gr = ld4_sum(g, d.ks_g1, d.ps_g1), gu = ld4_sum(g + Hp, d.ks_g1, d.ps_g1),
                gc = ld4_sum(g + 2 * Hp, d.ks_g1, d.ps_g1);
   const float4 er = ld4(ex), eu = ld4(ex + Hp), ec = ld4(ex + 2 * Hp);
-  const float4 sv = ld4(S + (int64_t)d.row_src[r] * Hp + j);
+  const float4 sv = live ? ld4((d.gs ? d.gs[d.row_grp[r]].S : S) + (int64_t)d.row_src[r] * Hp + j)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
   float4 o;
 #define NMT_GRU1(c) { const float rg = sigm(er.c + gr.c), ug = sigm(eu.c + gu.c); \
                       o.c = ug * sv.c + (1.f - ug) * tanhf(rg * gc.c + ec.c); }
@@ -554,6 +592,12 @@ __global__ void __launch_bounds__(256) k_attention(StepDev d, AttnCtx a) {
   const int R = *d.R;
   const int r0 = blockIdx.x * RPB;
   if (r0 >= R) return;
+  if (d.gs) {  // multi-context step: groups start at multiples of 4 rows and RPB divides 4
+    const GrpStep& g = d.gs[d.row_grp[r0]];
+    a.pctx = g.pctx;
+    a.ctx = g.ctx;
+    a.Tx = g.Tx;
+  }
   const int Cp = d.Cp, Tx = a.Tx;
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = threadIdx.x * 8;
@@ -707,7 +751,8 @@ __global__ void k_gru2(StepDev d, float* __restrict__ S) {
                       o.c = ug * s1.c + (1.f - ug) * tanhf(rg * (gh.c + bx.c) + gc.c); }
   NMT_GRU2(x) NMT_GRU2(y) NMT_GRU2(z) NMT_GRU2(w)
 #undef NMT_GRU2
-  st4(S + (int64_t)d.row_dst[r] * Hp + j, o);
+  const int dst = d.row_dst[r];
+  if (dst >= 0) st4((d.gs ? d.gs[d.row_grp[r]].S : S) + (int64_t)dst * Hp + j, o);
   store_split4(d.X + (int64_t)r * d.ldx + d.Hp + d.Cp + j, d.lo_x, o);
 }
 
@@ -746,7 +791,8 @@ __global__ void k_readout(StepDev d, float* __restrict__ T) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = idx / E4, k = (idx % E4) * 4;
   if (r >= *d.R) return;
-  const int y = d.row_y[r];
+  const int dst = d.row_dst[r];
+  const int y = dst >= 0 ? d.row_y[r] : -1;
   const float* pre = d.RO + (int64_t)r * d.ROp;
   const float* epr = d.Eproj + (int64_t)(y < 0 ? d.V : y) * d.ROp;
   float t[4];
@@ -776,7 +822,7 @@ __global__ void k_readout(StepDev d, float* __restrict__ T) {
   float tp[4];  // t -> arena (zero past E)
 #pragma unroll
   for (int i = 0; i < 4; ++i) tp[i] = k + i < E ? t[i] : 0.f;
-  st4(T + (int64_t)d.row_dst[r] * Ep + k, make_float4(tp[0], tp[1], tp[2], tp[3]));
+  if (dst >= 0) st4((d.gs ? d.gs[d.row_grp[r]].T : T) + (int64_t)dst * Ep + k, make_float4(tp[0], tp[1], tp[2], tp[3]));
   write_vocab_operand(d, r, k, tp);
 }
 
@@ -819,10 +865,16 @@ __global__ void k_finalize(StepDev d, float* __restrict__ logZ, int* __restrict_
     s = ns;
     am = na;
   }
-  if (lane == 0) {
-    const int slot = d.row_dst[warp];
-    logZ[slot] = m + logf(s);
-    amax[slot] = am;
+  const int slot = d.row_dst[warp];
+  if (lane == 0 && slot >= 0) {
+    if (d.gs) {
+      const GrpStep& g = d.gs[d.row_grp[warp]];
+      g.logZ[slot] = m + logf(s);
+      g.amax[slot] = am;
+    } else {
+      logZ[slot] = m + logf(s);
+      amax[slot] = am;
+    }
   }
 }
 
@@ -830,8 +882,18 @@ __global__ void k_finalize(StepDev d, float* __restrict__ logZ, int* __restrict_
 // the trailing blocks write each parent's argmax.
 __global__ void k_gather_dot(CtxDev c, PlanIO io, const float* __restrict__ Wo32, const float* __restrict__ bo,
                              int Ep, float* out_logp, int* out_child32, long long* out_child64, int* out_argmax,
-                             int cand_blocks) {
+                             int cand_blocks, const PlanDesc* __restrict__ gd) {
   pdl_enter();
+  if (gd) {  // multi-context call: group blockIdx.y, its own output slices
+    const PlanDesc& g = gd[blockIdx.y];
+    c = g.c;
+    io = g.io;
+    out_logp = g.out_logp;
+    out_child32 = g.out_child;
+    out_child64 = nullptr;
+    out_argmax = g.out_argmax;
+    if ((int)blockIdx.x >= cand_blocks && !out_argmax) return;
+  }
   if ((int)blockIdx.x >= cand_blocks) {  // parents' argmax
     const int k = (blockIdx.x - cand_blocks) * blockDim.x + threadIdx.x;
     if (k >= io.n_par) return;
@@ -952,7 +1014,8 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
       static const int rpb_env = getenv("NMT_ATTN_RPB") ? atoi(getenv("NMT_ATTN_RPB")) : 0;  // (diagnostic)
       // rows per CTA: ceil(R / SMs), at most 4 (measured in the step at R = 1024: 4 rows x 256 CTAs is
       // ~28 us faster than one wave of 7-row CTAs, whose single CTA per SM hides less latency)
-      const int rpb = rpb_env > 0 ? std::min(8, rpb_env) : std::max(1, std::min(4, (R_max + kNumSMs - 1) / kNumSMs));
+      int rpb = rpb_env > 0 ? std::min(8, rpb_env) : std::max(1, std::min(4, (R_max + kNumSMs - 1) / kNumSMs));
+      if (d.gs && (rpb == 3 || rpb > 4)) rpb = 4;  // multi-context rows: CTAs must not straddle a group
       switch (rpb) {
         case 1: launch_attention<1>(d, a, R_max, st); break;
         case 2: launch_attention<2>(d, a, R_max, st); break;
@@ -1049,8 +1112,22 @@ void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const floa
   const int cb = (io.n_cand * 32 + 255) / 256;
   const int pb = out_argmax ? (io.n_par + 255) / 256 : 0;
   if (cb + pb == 0) return;
+  const PlanDesc* none = nullptr;
   launch_pdl(k_gather_dot, cb + pb, 256, 0, st, c, io, Wo32, bo, Ep, out_logp, out_child32, out_child64, out_argmax,
-             cb);
+             cb, none);
+  CK_LAUNCH();
+}
+void gather_dot_multi(const PlanDesc* descs, int G, int max_cand, int max_par, const float* Wo32, const float* bo,
+                      int Ep, cudaStream_t st) {
+  const int cb = (max_cand * 32 + 255) / 256;
+  const int pb = (max_par + 255) / 256;
+  if (cb + pb == 0) return;
+  const CtxDev c{};
+  const PlanIO io{};
+  float* nf = nullptr;
+  int* ni = nullptr;
+  long long* nl = nullptr;
+  launch_pdl(k_gather_dot, dim3(cb + pb, G), 256, 0, st, c, io, Wo32, bo, Ep, nf, ni, nl, ni, cb, descs);
   CK_LAUNCH();
 }
 

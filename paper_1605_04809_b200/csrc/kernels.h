@@ -44,8 +44,31 @@ struct PlanIO {
   int step_all;         // 1: step every listed parent not yet stepped, candidates or not (beam step)
 };
 
+// One context of a multi-context step (nmt_score_batch_multi): its arena and attention source.
+struct GrpStep {
+  float* S;
+  float* T;
+  float* logZ;
+  int* amax;
+  const float* pctx;
+  const float* ctx;
+  int Tx;
+};
+
+// Planner / gather-dot descriptor of one context of a multi-context call (blockIdx.y = group).
+struct PlanDesc {
+  CtxDev c;
+  PlanIO io;          // request and planner scratch slices of this group
+  int* R_out;         // the group's stepped-row count
+  float* out_logp;    // outputs of this group's candidates / parents
+  int* out_child;
+  int* out_argmax;
+};
+
 // Decoder-step workspace view (rows r < *R).
 struct StepDev {
+  const int* row_grp;  // multi-context step: group of each row (else null); rows with row_dst < 0 are dead
+  const GrpStep* gs;   // multi-context step: per-group arenas (else null)
   const int* R;
   const int* row_src;
   const int* row_y;
@@ -134,6 +157,8 @@ void topk_merge(const float2* topk, const int* cpm_dev, int n, int k, int* out_w
 void ctx_reset(const CtxDev& c, int64_t hcap, cudaStream_t st);
 void fill_i32(int* p, int64_t n, int v, cudaStream_t st);
 void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st);
+// G groups at once: descs [dev, G]; max_cand / max_par = the largest group's counts
+void plan_multi(const PlanDesc* descs, int G, int max_cand, int max_par, cudaStream_t st);
 void rehash(const unsigned long long* okeys, const int* ovals, int64_t ocap, unsigned long long* nkeys, int* nvals,
             uint64_t nmask, cudaStream_t st);
 void inject(const CtxDev& c, int n, const float* s, const int* y, int* out_ids, int* done, cudaStream_t st);
@@ -141,6 +166,8 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
                       int R_max, cudaStream_t st);
 void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const float* bo, int Ep, float* out_logp,
                 int* out_child32, long long* out_child64, int* out_argmax, cudaStream_t st);
+void gather_dot_multi(const PlanDesc* descs, int G, int max_cand, int max_par, const float* Wo32, const float* bo,
+                      int Ep, cudaStream_t st);
 void gather_idx(const int* src, const int* idx, int n, int* out, cudaStream_t st);
 void path_sum(const float* logp, const int* child, const int* off, const int* pos, int n, float* out_logp,
               int* out_state, cudaStream_t st);
