@@ -2039,7 +2039,7 @@ nmt_status nmt_score_batch_multi(int32_t np, nmt_ctx* const* cpp, const nmt_stat
     for (int g = 0; g < G; ++g) ctxs[g]->ensure(gnc[g], (int64_t)gpar[g].size());
     for (nmt_ctx* c : ctxs) c->join_enc();
     const int Bblk = (max_nc + 255) / 256 + std::max(1, (max_np + 255) / 256);
-    const size_t need_i = (size_t)G * Bblk + 4 * (size_t)G + 1 + total_rows;
+    const size_t need_i = (size_t)G * Bblk + 4 * (size_t)G + 1 + total_rows + (size_t)G * CNT_N;
     const size_t need_b = (size_t)G * (sizeof(PlanDesc) + sizeof(GrpStep));
     if (need_i > m->mws_i_cap || need_b > m->mws_b_cap) {
       CK(cudaStreamSynchronize(st));
@@ -2058,11 +2058,12 @@ nmt_status nmt_score_batch_multi(int32_t np, nmt_ctx* const* cpp, const nmt_stat
     int* d_snap = d_bcount + (size_t)G * Bblk;
     int* d_R = d_snap + 4 * G;
     int* d_rowgrp = d_R + 1;
+    int* d_cnt = d_rowgrp + total_rows;
     PlanDesc* d_desc = reinterpret_cast<PlanDesc*>(m->mws_b);
     GrpStep* d_gs = reinterpret_cast<GrpStep*>(m->mws_b + (size_t)G * sizeof(PlanDesc));
     // host staging (pinned): parents | offsets (G + np) | words | R | row_grp | descriptors
     const size_t ints = (size_t)np + np + G + nc + 1 + total_rows;
-    char* hbuf = static_cast<char*>(m->pinned(ints * 4 + need_b + (size_t)(2 * nc + np) * 4 + 256));
+    char* hbuf = static_cast<char*>(m->pinned(ints * 4 + need_b + (size_t)(2 * nc + np + G * CNT_N) * 4 + 256));
     int* hp = reinterpret_cast<int*>(hbuf);
     int* ho = hp + np;
     int* hw = ho + np + G;
@@ -2142,9 +2143,9 @@ nmt_status nmt_score_batch_multi(int32_t np, nmt_ctx* const* cpp, const nmt_stat
       CK(cudaMemcpyAsync(rc, m->out_child, (size_t)nc * 4, cudaMemcpyDeviceToHost, st));
     }
     CK(cudaMemcpyAsync(ra, m->out_amax, (size_t)np * 4, cudaMemcpyDeviceToHost, st));
-    std::vector<int> cnt((size_t)G * CNT_N);
-    for (int g = 0; g < G; ++g)
-      CK(cudaMemcpyAsync(&cnt[(size_t)g * CNT_N], ctxs[g]->counters, CNT_N * 4, cudaMemcpyDeviceToHost, st));
+    int* cnt = ra + np;  // (pinned)
+    counters_multi(d_desc, G, d_cnt, st);
+    CK(cudaMemcpyAsync(cnt, d_cnt, (size_t)G * CNT_N * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     for (int g = 0; g < G; ++g)
       if (cnt[(size_t)g * CNT_N + CNT_ERR]) {

@@ -1117,6 +1117,15 @@ void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const floa
              cb, none);
   CK_LAUNCH();
 }
+__global__ void k_counters_multi(const PlanDesc* __restrict__ descs, int G, int* __restrict__ out) {
+  pdl_enter();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < G * CNT_N) out[i] = descs[i / CNT_N].c.counters[i % CNT_N];
+}
+void counters_multi(const PlanDesc* descs, int G, int* out, cudaStream_t st) {
+  launch_pdl(k_counters_multi, (G * CNT_N + 255) / 256, 256, 0, st, descs, G, out);
+  CK_LAUNCH();
+}
 void gather_dot_multi(const PlanDesc* descs, int G, int max_cand, int max_par, const float* Wo32, const float* bo,
                       int Ep, cudaStream_t st) {
   const int cb = (max_cand * 32 + 255) / 256;

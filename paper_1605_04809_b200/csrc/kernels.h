@@ -166,6 +166,8 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
                       int R_max, cudaStream_t st);
 void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const float* bo, int Ep, float* out_logp,
                 int* out_child32, long long* out_child64, int* out_argmax, cudaStream_t st);
+// the CNT_N counters of every group's context into out [dev, G x CNT_N] (one D2H for the call)
+void counters_multi(const PlanDesc* descs, int G, int* out, cudaStream_t st);
 void gather_dot_multi(const PlanDesc* descs, int G, int max_cand, int max_par, const float* Wo32, const float* bo,
                       int Ep, cudaStream_t st);
 void gather_idx(const int* src, const int* idx, int n, int* out, cudaStream_t st);

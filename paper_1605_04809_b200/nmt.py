@@ -70,7 +70,12 @@ def random_params(dim_emb: int, dim_hid: int, vocab_src: int, vocab_tgt: int, re
 def score_batch_multi(contexts, parents, cand_offsets, cand_words, with_argmax: bool = True):
     """nmt_score_batch_multi: parent k belongs to contexts[k] (all of one model)."""
     n = len(parents)
-    hs = (C.c_void_p * max(n, 1))(*[c._h.value for c in contexts])
+    if isinstance(contexts, np.ndarray):  # int64 handles (Context.handle), e.g. built with np.repeat
+        hs = np.ascontiguousarray(contexts, dtype=np.int64)
+        hs_ptr = _ptr(hs)
+    else:
+        hs = (C.c_void_p * max(n, 1))(*[c._h.value for c in contexts])
+        hs_ptr = C.cast(hs, C.c_void_p)
     par = _c(parents, np.int64)
     off = _c(cand_offsets, np.int32)
     words = _c(cand_words, np.int32)
@@ -78,7 +83,7 @@ def score_batch_multi(contexts, parents, cand_offsets, cand_words, with_argmax: 
     logp = np.empty(nc, np.float32)
     child = np.empty(nc, np.int64)
     am = np.empty(n, np.int32) if with_argmax else None
-    _check(lib().nmt_score_batch_multi(n, C.cast(hs, C.c_void_p), _ptr(par), _ptr(off), _ptr(words), _ptr(logp),
+    _check(lib().nmt_score_batch_multi(n, hs_ptr, _ptr(par), _ptr(off), _ptr(words), _ptr(logp),
                                        _ptr(child), _ptr(am)))
     return logp, child, am
 
@@ -281,6 +286,10 @@ class Context:
             _check(lib().nmt_encode(model._h, _ptr(src), len(src), C.byref(self._h)))
             self.Tx = len(src)
         self.root = int(lib().nmt_root(self._h))
+
+    @property
+    def handle(self) -> int:
+        return int(self._h.value)
 
     @classmethod
     def _wrap(cls, model: Model, handle: int, Tx: int) -> "Context":
