@@ -311,6 +311,10 @@ def c5(a):
                             stacks += 1
                     ctx.close()
             return edges, rows, naive, stacks
+        tcall = [0.0]  # seconds inside nmt_score_batch_multi (host wall, synchronised calls)
+        tphase = [0.0, 0.0, 0.0]  # encode_batch, reserve, inject
+        max_tot = [0]  # words of the largest sentence of this point (arena reservation)
+
         def prep_multi(sents):
             """synthetic requests of each chunk (outside the timed region): phrase lengths and words"""
             out = []
@@ -324,6 +328,7 @@ def c5(a):
                 L_all[np.arange(T)[None, :] >= nstk[:, None]] = 0  # sentences with fewer stacks
                 W_all = synth.zipf_ids(g, S * T * B * 4, d.vocab_tgt).reshape(S, T, B, 4)
                 srcs = [synth.make_source(d.vocab_src, lens[i], seed=9000 + i) for i in chunk]
+                max_tot[0] = max(max_tot[0], int(L_all.sum(axis=(1, 2)).max()))
                 out.append((chunk, nstk, L_all, W_all, srcs))
             return out
 
@@ -331,15 +336,24 @@ def c5(a):
             """a.concurrent sentences at a time: each (stack, depth) is ONE nmt_score_batch_multi over
             all of them (rows of different sentences share the fused decoder step)."""
             edges = stacks = 0
+            tcall[0] = 0.0
+            tphase[:] = [0.0, 0.0, 0.0]
             for chunk, nstk, L_all, W_all, srcs in prepped:
                 S, T = L_all.shape[0], L_all.shape[1]
+                tp0 = time.perf_counter()
                 ctxs = M.encode_batch(srcs)
+                tphase[0] += time.perf_counter() - tp0
                 hnd_pair = np.repeat(np.array([c.handle for c in ctxs], np.int64), B)
                 cur_h = np.empty(S * B, np.int64)
+                tp0 = time.perf_counter()
+                for ctx in ctxs:  # every arena sized for the largest sentence of the point: pooled arenas
+                    ctx.reserve(max_tot[0] + B + 1, max_tot[0])  # never grow inside the timed region
+                tp1 = time.perf_counter()
                 for q, ctx in enumerate(ctxs):
-                    tot = int(L_all[q].sum())
-                    ctx.reserve(tot + B + 1, tot)
                     cur_h[q * B:(q + 1) * B] = ctx.inject_states(s_st, y_st)
+                tp2 = time.perf_counter()
+                tphase[1] += tp1 - tp0
+                tphase[2] += tp2 - tp1
                 for stk in range(T):
                     L = L_all[:, stk, :].reshape(-1)
                     Wst = W_all[:, stk, :, :].reshape(-1, 4)
@@ -349,8 +363,10 @@ def c5(a):
                         if len(sel) == 0:
                             break
                         off = np.arange(len(sel) + 1, dtype=np.int32)
+                        tc0 = time.perf_counter()
                         lp, ch, _ = nmt.score_batch_multi(hnd_pair[sel], cur[sel], off, Wst[sel, dep],
                                                           with_argmax=False)
+                        tcall[0] += time.perf_counter() - tc0
                         cur[sel] = ch
                         if count:
                             edges += len(sel)
@@ -364,9 +380,9 @@ def c5(a):
             return edges, edges, edges, stacks
 
         if a.concurrent > 1:
-            warm = prep_multi(mine[:min(len(mine), a.concurrent)])
-            run_multi(warm, False)  # warm-up (workspaces, arenas)
             work = prep_multi(mine)
+            warm = prep_multi(mine[:min(len(mine), a.concurrent)])
+            run_multi(warm, False)  # warm-up (workspaces, arenas at the point's largest reservation)
             runner = lambda: run_multi(work, True)
         else:
             run(mine[:min(len(mine), 2)], False)  # warm-up (workspaces)
@@ -388,6 +404,8 @@ def c5(a):
         if rank == 0:
             print(json.dumps({"workload": "c5", "B": B, "gpus": world, "precision": a.precision,
                               "concurrent_sentences": a.concurrent,
+                              "seconds_in_score_calls": tcall[0] if a.concurrent > 1 else None,
+                              "seconds_encode_reserve_inject": list(tphase) if a.concurrent > 1 else None,
                               "sentences": int(nsent), "stacks": int(ns), "word_scores_per_s": e / dt,
                               "rows_per_s": r / dt, "naive_words": int(nv), "edges": int(e), "rows": int(r),
                               "seconds": dt, "row_budget": a.row_budget,
