@@ -52,3 +52,22 @@ def test_shard_seeds_disjoint():
     import bench
     seeds = {bench.shard_seed(r, s) for r in range(8) for s in range(1000)}
     assert len(seeds) == 8000
+
+
+def test_c5_lpt_sharding_partitions_and_balances():
+    """tools/workloads.py lpt_shard (C5 sentence sharding over ranks): a partition of
+    the sentences, deterministic, and within the greedy-LPT bound max load <= 4/3 OPT + 1 job."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import numpy as np
+    import workloads
+    rng = np.random.default_rng(0)
+    costs = [int(x) * 64 for x in rng.integers(11, 52, size=3000)]
+    for world in (1, 2, 4, 8):
+        sh = workloads.lpt_shard(costs, world)
+        assert sorted(i for s in sh for i in s) == list(range(len(costs)))
+        assert sh == workloads.lpt_shard(costs, world)
+        loads = [sum(costs[i] for i in s) for s in sh]
+        lower = max(sum(costs) / world, max(costs))
+        assert max(loads) <= 4 / 3 * lower + max(costs)
+        assert max(loads) - min(loads) <= max(costs)
