@@ -390,10 +390,13 @@ def c5(a):
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        t0 = time.perf_counter()
-        e, r, nv, ns = runner()
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
+        import bench  # (nvidia-smi clock / throttle sampler of the bench contract)
+        with bench.ClockSampler(torch.cuda.current_device()) as clk:
+            t0 = time.perf_counter()
+            e, r, nv, ns = runner()
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+        clocks = clk.summary()
         tot = torch.tensor([e, r, nv, ns, len(mine)], dtype=torch.float64, device="cuda")
         tmax = torch.tensor([dt], dtype=torch.float64, device="cuda")
         if dist:
@@ -406,6 +409,7 @@ def c5(a):
                               "concurrent_sentences": a.concurrent,
                               "seconds_in_score_calls": tcall[0] if a.concurrent > 1 else None,
                               "seconds_encode_reserve_inject": list(tphase) if a.concurrent > 1 else None,
+                              "clocks": clocks,
                               "sentences": int(nsent), "stacks": int(ns), "word_scores_per_s": e / dt,
                               "rows_per_s": r / dt, "naive_words": int(nv), "edges": int(e), "rows": int(r),
                               "seconds": dt, "row_budget": a.row_budget,
