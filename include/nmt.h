@@ -211,6 +211,13 @@ NMT_API nmt_status nmt_beam_step(nmt_ctx* c, int32_t n_parents, const nmt_state*
 NMT_API nmt_status nmt_score_forest(nmt_ctx* c, int32_t n_pairs, const nmt_state* hyp_states,
                                     const int32_t* phrase_offsets, const int32_t* phrase_words, float* out_logp,
                                     nmt_state* out_state, int32_t* stats);
+/* n-best forced rescoring (rescoring gives "the same as if they
+ * were produced at decode-time"): sequence i = words[offsets[i] .. offsets[i+1]) [host] (non-empty,
+ * any length; the caller appends EOS) is scored from the root: out_logp[i] = sum_j log p(w_j | w_<j)
+ * and out_state[i] = the state after it [host, n each].  All sequences form one prefix forest, so
+ * shared prefixes are stepped once and each depth is one batched step (as nmt_score_forest).    */
+NMT_API nmt_status nmt_score_sequences(nmt_ctx* c, int32_t n, const int32_t* offsets, const int32_t* words,
+                                       float* out_logp, nmt_state* out_state);
 /* Waits for the model stream and reports a device-side validation error of earlier _dev calls. */
 NMT_API nmt_status nmt_ctx_check(nmt_ctx* c);
 /* Grows the context's arena to hold n_nodes nodes and n_stepped stepped nodes without further

@@ -2190,8 +2190,29 @@ nmt_status nmt_score_batch_dev(nmt_ctx* c, int32_t np, const int32_t* parents, c
 // ScoreBatch (Alg. 1) in one call: host prefix-tree forest, one H2D, one
 // device step per depth (parents of depth d+1 gathered on the device from depth d's children),
 // per-pair path sums on the device, one D2H.
+static nmt_status score_forest_impl(nmt_ctx* c, int32_t n_pairs, const nmt_state* hyp, const int32_t* poff,
+                                    const int32_t* pwords, float* out_logp, nmt_state* out_state, int32_t* stats,
+                                    int max_len);
+
 nmt_status nmt_score_forest(nmt_ctx* c, int32_t n_pairs, const nmt_state* hyp, const int32_t* poff,
                             const int32_t* pwords, float* out_logp, nmt_state* out_state, int32_t* stats) {
+  return score_forest_impl(c, n_pairs, hyp, poff, pwords, out_logp, out_state, stats, 16);
+}
+
+// n-best forced rescoring ("the same as if they were produced at
+// decode-time"): every sequence is a phrase from the root, so all of them form one prefix forest
+// and each depth is one batched step; any length (no per-depth statistics).
+nmt_status nmt_score_sequences(nmt_ctx* c, int32_t n, const int32_t* offsets, const int32_t* words, float* out_logp,
+                               nmt_state* out_state) {
+  if (!c || n < 0) return fail(NMT_ERR_INVALID_ARG, "bad argument");
+  if (n == 0) return NMT_OK;
+  std::vector<nmt_state> roots((size_t)n, nmt_root(c));
+  return score_forest_impl(c, n, roots.data(), offsets, words, out_logp, out_state, nullptr, INT32_MAX);
+}
+
+static nmt_status score_forest_impl(nmt_ctx* c, int32_t n_pairs, const nmt_state* hyp, const int32_t* poff,
+                                    const int32_t* pwords, float* out_logp, nmt_state* out_state, int32_t* stats,
+                                    int max_len) {
   if (!c || n_pairs < 0) return fail(NMT_ERR_INVALID_ARG, "bad argument");
   if (n_pairs == 0) {
     if (stats) std::memset(stats, 0, 33 * sizeof(int32_t));
@@ -2202,7 +2223,7 @@ nmt_status nmt_score_forest(nmt_ctx* c, int32_t n_pairs, const nmt_state* hyp, c
   if (poff[0] != 0) return fail(NMT_ERR_INVALID_ARG, "phrase_offsets[0] != 0");
   for (int i = 0; i < n_pairs; ++i) {
     if (poff[i + 1] <= poff[i]) return fail(NMT_ERR_INVALID_ARG, "empty expansion (pair " + std::to_string(i) + ")");
-    if (poff[i + 1] - poff[i] > 16) return fail(NMT_ERR_CAPACITY, "phrase longer than 16 words");
+    if (poff[i + 1] - poff[i] > max_len) return fail(NMT_ERR_CAPACITY, "phrase longer than 16 words");
   }
   for (int k = 0; k < poff[n_pairs]; ++k)
     if (pwords[k] < 0 || pwords[k] >= m->V)

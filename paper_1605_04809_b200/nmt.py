@@ -28,7 +28,7 @@ EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "n
            "nmt_profile_read", "nmt_bench_gemm", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
            "nmt_ensemble_free", "nmt_params_average", "nmt_beam_step",
            "nmt_encode_batch", "nmt_save_params", "nmt_params_bytes", "nmt_random_params", "nmt_create_random",
-           "nmt_debug_vocab", "nmt_score_batch_multi", "nmt_ctx_reserve"]
+           "nmt_debug_vocab", "nmt_score_batch_multi", "nmt_ctx_reserve", "nmt_score_sequences"]
 
 
 N_STAGES = 19
@@ -153,6 +153,7 @@ def lib() -> C.CDLL:
             "nmt_debug_vocab": (i32, [vp, i32, vp, vp, vp, vp, vp, vp]),
             "nmt_score_batch_multi": (i32, [i32, vp, vp, vp, vp, vp, vp, vp]),
             "nmt_ctx_reserve": (i32, [vp, i64, i64]),
+            "nmt_score_sequences": (i32, [vp, i32, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -344,6 +345,18 @@ class Context:
         steps = int(stats[0])
         return lp, st, {"steps": steps, "edges_per_depth": stats[1:1 + steps].tolist(),
                         "rows_per_depth": stats[17:17 + steps].tolist()}
+
+    def score_sequences(self, sequences) -> Tuple[np.ndarray, np.ndarray]:
+        """nmt_score_sequences: n-best forced rescoring from the root; (sum log-prob, final state)."""
+        seqs = [_c(x, np.int32) for x in sequences]
+        n = len(seqs)
+        off = np.zeros(n + 1, np.int32)
+        off[1:] = np.cumsum([len(x) for x in seqs])
+        w = np.concatenate(seqs).astype(np.int32) if n else np.zeros(1, np.int32)
+        lp = np.empty(n, np.float32)
+        st = np.empty(n, np.int64)
+        _check(lib().nmt_score_sequences(self._h, n, _ptr(off), _ptr(w), _ptr(lp), _ptr(st)))
+        return lp, st
 
     def check(self) -> None:
         _check(lib().nmt_ctx_check(self._h))

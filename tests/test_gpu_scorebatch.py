@@ -159,3 +159,37 @@ def test_native_score_forest_c3_stack_tiny():
     worst = max(abs(lp[i] - ref[k]) / len(k[1]) for i, k in enumerate(pairs))
     assert worst < TOL["fp32class"]
     assert st["rows_per_depth"] == sess.rows_per_step
+
+
+@pytest.mark.parametrize("prec", ["fp32class", "bf16"])
+def test_score_sequences_nbest_vs_oracle(prec):
+    """n-best forced rescoring (nmt_score_sequences, §8(f) NEXT-1): sequences longer than
+    a phrase (up to 27 words + EOS) sharing prefixes, scored from the root in one forest; each total
+    equals the oracle's chained sequence score (oracle.score_sequence), and the returned state
+    continues exactly like the oracle state after the sequence."""
+    from paper_1605_04809_b200 import nmt
+    d = synth.Dims(8, 16, 50, 50, "tanh")
+    p = synth.make_model(d, 7)
+    M = nmt.Model(synth.params_bytes(d, p), precision=prec)
+    om = O.Model(d, p)
+    src = synth.make_source(d.vocab_src, 6, seed=3)
+    c = M.encode(src)
+    oc = O.encode(om, src)
+    rng = np.random.Generator(np.random.PCG64(9))
+    base = [int(x) for x in rng.integers(2, d.vocab_tgt, size=27)]
+    nbest = [base + [0], base[:20] + [5, 6, 0], base[:20] + [5, 7, 0], base[:3] + [0], [4, 0],
+             [int(x) for x in rng.integers(2, d.vocab_tgt, size=18)] + [0]]
+    lp, st = c.score_sequences(nbest)
+    tol = 1e-3 if prec == "fp32class" else 2e-2
+    for seq, g in zip(nbest, lp):
+        ref, _, _ = O.score_sequence(om, oc, seq)
+        assert abs(g - ref) < tol * len(seq) ** 0.5, (len(seq), g, ref)
+    # shared prefixes were collapsed: the arena holds one node per distinct prefix (+ the root)
+    prefixes = {tuple(s[:k]) for s in nbest for k in range(1, len(s) + 1)}
+    assert c.stats()[0] == 1 + len(prefixes)
+    # continuing from a returned state: same as the oracle from the state after the sequence
+    lp2, _, _ = c.score_batch([int(st[4])], [0, 2], [3, 9])
+    _, _, s_after = O.score_sequence(om, oc, nbest[4])
+    out = O.step(om, oc, s_after[None, :], [nbest[4][-1]])
+    ref2 = O.log_softmax(out["z"][0])[[3, 9]]
+    assert np.max(np.abs(lp2 - ref2)) < tol
