@@ -267,6 +267,12 @@ NMT_API nmt_status nmt_debug_intermediates(nmt_ctx* c, nmt_state node, float* s1
 NMT_API nmt_status nmt_debug_vocab(nmt_model* m, int32_t R, const float* t, const int32_t* cand_offsets,
                                    const int32_t* cand_words, float* out_logprob, float* out_logZ,
                                    int32_t* out_argmax);
+/* The vocab-parallel path of one step (nmt_vocab_shard) emulated on one GPU: the vocabulary is cut
+ * into n_slices 256-column-aligned slices computed one after the other, as ranks 0..n-1 would,
+ * and their per-row (max, sum exp, argmax) partials are merged by the same combine kernel that runs
+ * after the all-gather.  t, out_logZ, out_argmax as nmt_debug_vocab.                          */
+NMT_API nmt_status nmt_debug_vocab_shards(nmt_model* m, int32_t R, const float* t, int32_t n_slices, float* out_logZ,
+                                          int32_t* out_argmax);
 /* GEMM engine unit test: C[M x N] = A[M x K] . B[K x N] (+ bias[N]) with the tcgen05 kernel;
  * split = 1 -> bf16x3.  A, B, bias, C are [host] fp32 row-major; N % 128 == 0, K % 64 == 0.     */
 NMT_API nmt_status nmt_test_gemm(int32_t M, int32_t N, int32_t K, int32_t split, const float* A, const float* B,
@@ -277,6 +283,16 @@ NMT_API nmt_status nmt_test_gemm(int32_t M, int32_t N, int32_t K, int32_t split,
  * log-sum-exp, N % 256 == 0), split = bf16x3, ksplit = split-K factor (epi 0).                 */
 NMT_API nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_t epi, int32_t ksplit,
                                   int32_t iters, float* ms_out);
+
+/* ---- vocab-parallel scoring (PAPER.md:98 multi-GPU) ---------------------
+ * Every rank (one per GPU) holds the same model and issues the same calls; after this call the
+ * rank's vocabulary GEMM covers only its slice of the target vocabulary (the 256-column tiles
+ * [T*rank/world, T*(rank+1)/world)), each row's (max, sum exp, argmax) over the slice is exchanged
+ * with ONE all-gather per step on `comm` (an nmt_ensemble communicator of `world` ranks: 16 B per
+ * row per rank) and merged in rank order, so logZ, argmax and every log-prob equal the single-GPU
+ * result up to fp32 summation order.  The rest of the step is replicated.  world == 1 or
+ * comm == NULL restores the full vocabulary.  rank/world must match the communicator.             */
+NMT_API nmt_status nmt_vocab_shard(nmt_model* m, int32_t rank, int32_t world, nmt_ensemble* comm);
 
 /* ---- ensemble hook (models as separately weighted features; north_star NCCL reduce)
  * One member per GPU/process.  nccl_unique_id points to the 128-byte ncclUniqueId broadcast by the

@@ -209,6 +209,12 @@ struct nmt_model {
   cudaEvent_t pin2_ev = nullptr;  // H2D of nmt_inject_states from page-locked caller memory
   std::mutex mu;
   std::vector<char> raw;  // the params container this model was built from (nmt_save_params)
+  // vocab-parallel scoring (nmt_vocab_shard): this rank's vocabulary slice [vs_n0, vs_n1) and the
+  // exchange buffer xbuf [world][xrows] of per-row (max, sum exp, argmax) slice partials
+  int vs_world = 0, vs_rank = 0, vs_n0 = 0, vs_n1 = 0;
+  nmt_ensemble* vs_comm = nullptr;
+  float4* xbuf = nullptr;
+  int xrows = 0, xworld = 0;
   // lifetime: one reference held by the user handle plus one per live context, so that
   // nmt_model_free and nmt_ctx_free may be called in any order
   std::atomic<int> refs{1};
@@ -256,6 +262,7 @@ static void free_all_model(nmt_model* m) {
   dfree(m->fws_f);
   dfree(m->mws_i);
   dfree(m->mws_b);
+  dfree(m->xbuf);
   if (m->pin) cudaFreeHost(m->pin);
   m->pin = nullptr;
   if (m->pin2_ev) cudaEventDestroy(m->pin2_ev);
@@ -1055,6 +1062,31 @@ static void gemm_auto(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b12
   gemm_split(m, a, b128, g, out, ldc, rps, m->P_rows, M_max, max_ks, st);
 }
 
+namespace nmt {  // (ensemble.cu)
+int ens_world(const nmt_ensemble* e);
+int ens_rank(const nmt_ensemble* e);
+void ens_allgather(nmt_ensemble* e, const float* send, float* recv, size_t count, cudaStream_t st);
+}  // namespace nmt
+
+// the vocabulary GEMM with the fused log-sum-exp over columns [n0, n1) (a multiple of 256 wide)
+static void vocab_lse(nmt_model* m, const int* Rd, int R_max, int n0, int n1, cudaStream_t st) {
+  GemmShape g = gemm_shape(0, Rd, n1 - n0, m->Ep, 0, m->split, m->Ep, m->Ep);
+  g.b_panel_rows = m->Vp;
+  g.n_off = n0;
+  if (m->use_pair) gemm_lse_pair(m->tm_At, m->tm_Wo128, g, m->part, m->V, st, m->lse_cpm);
+  else gemm_lse(m->tm_At, m->tm_Wo, g, m->part, m->V, R_max, st, m->lse_cpm);
+}
+
+static void ensure_xbuf(nmt_model* m, int world) {
+  if (m->xrows < m->R_cap || m->xworld < world) {
+    CK(cudaStreamSynchronize(m->st));
+    dfree(m->xbuf);
+    m->xrows = m->R_cap;
+    m->xworld = std::max(world, m->xworld);
+    m->xbuf = dalloc<float4>((size_t)m->xworld * m->xrows);
+  }
+}
+
 // multi-context step (nmt_score_batch_multi): device row count, per-row group, per-group arenas
 struct MultiStep {
   const int* R_dev;
@@ -1117,12 +1149,24 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
     d.ps_ro = (int64_t)rps * m->ROp;
   }
   if (!stage_skipped(ST_READOUT)) { ProfScope p_(m, ST_READOUT); step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
+  if (m->vs_world > 1) {  // vocab-parallel (NEXT-2): this rank's slice, ONE all-gather, rank-order combine
+    ensure_xbuf(m, m->vs_world);
+    {
+      ProfScope p_(m, ST_VOCAB);
+      vocab_lse(m, Rd, R_max, m->vs_n0, m->vs_n1, st);
+    }
+    ProfScope p_(m, ST_FINALIZE);
+    d.xout = m->xbuf + (size_t)m->vs_rank * m->xrows;
+    step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R_max, st);
+    d.xout = nullptr;
+    ens_allgather(m->vs_comm, reinterpret_cast<const float*>(m->xbuf + (size_t)m->vs_rank * m->xrows),
+                  reinterpret_cast<float*>(m->xbuf), (size_t)m->xrows * 4, st);
+    shard_combine(d, m->xbuf, m->vs_world, m->xrows, c->logZ, c->amax, R_max, st);
+    return;
+  }
   if (!stage_skipped(ST_VOCAB)) {
     ProfScope p_(m, ST_VOCAB);
-    GemmShape g = gemm_shape(0, Rd, m->Vp, Ep, 0, sp, Ep, Ep);
-    g.b_panel_rows = m->Vp;
-    if (m->use_pair) gemm_lse_pair(m->tm_At, m->tm_Wo128, g, m->part, m->V, st, m->lse_cpm);
-    else gemm_lse(m->tm_At, m->tm_Wo, g, m->part, m->V, R_max, st, m->lse_cpm);
+    vocab_lse(m, Rd, R_max, 0, m->Vp, st);
   }
   if (!stage_skipped(ST_FINALIZE)) { ProfScope p_(m, ST_FINALIZE); step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
 }
@@ -1897,8 +1941,25 @@ nmt_status nmt_score_batch(nmt_ctx* c, int32_t np, const nmt_state* parents, con
 // D8 + D9 alone on caller-given readout outputs t (the minimum slice, SURVEY §8(b) test-only):
 // t rows go into a scratch context as R stepped nodes; then exactly the step's vocabulary path runs
 // (operand rows from the cached t, GEMM with the fused log-sum-exp, finalize, gather-dot).
+static nmt_status debug_vocab_impl(nmt_model* m, int32_t R, const float* t, const int32_t* off, const int32_t* words,
+                                   float* out_logp, float* out_logZ, int32_t* out_argmax, int n_slices);
+
 nmt_status nmt_debug_vocab(nmt_model* m, int32_t R, const float* t, const int32_t* off, const int32_t* words,
                            float* out_logp, float* out_logZ, int32_t* out_argmax) {
+  return debug_vocab_impl(m, R, t, off, words, out_logp, out_logZ, out_argmax, 0);
+}
+
+// the vocab-parallel path of one step emulated on one GPU: n_slices slices computed one after the
+// other (as ranks 0..n-1 would), partials combined by the same kernel as after the all-gather
+nmt_status nmt_debug_vocab_shards(nmt_model* m, int32_t R, const float* t, int32_t n_slices, float* out_logZ,
+                                  int32_t* out_argmax) {
+  if (!m || n_slices < 1 || n_slices > m->Vp / 256) return fail(NMT_ERR_INVALID_ARG, "bad n_slices");
+  std::vector<int32_t> off((size_t)std::max(R, 0) + 1, 0);
+  return debug_vocab_impl(m, R, t, off.data(), nullptr, nullptr, out_logZ, out_argmax, n_slices);
+}
+
+static nmt_status debug_vocab_impl(nmt_model* m, int32_t R, const float* t, const int32_t* off, const int32_t* words,
+                                   float* out_logp, float* out_logZ, int32_t* out_argmax, int n_slices) {
   if (!m || R < 0) return fail(NMT_ERR_INVALID_ARG, "bad arguments");
   if (R == 0) return NMT_OK;
   if (!t || !off || !out_logZ) return fail(NMT_ERR_INVALID_ARG, "NULL array");
@@ -1944,15 +2005,24 @@ nmt_status nmt_debug_vocab(nmt_model* m, int32_t R, const float* t, const int32_
     c->n_slots = R + 2;
     StepDev d = step_view(m, c);
     beam_gather(d, c->dev(), m->in_par, R, st);  // vocabulary operand rows [t | 1 (| lo)] from the arena
-    {
-      ProfScope p_(m, ST_VOCAB);
-      GemmShape g = gemm_shape(0, d.R, m->Vp, Ep, 0, m->split, Ep, Ep);
-      g.b_panel_rows = m->Vp;
-      if (m->use_pair) gemm_lse_pair(m->tm_At, m->tm_Wo128, g, m->part, m->V, st, m->lse_cpm);
-      else gemm_lse(m->tm_At, m->tm_Wo, g, m->part, m->V, R, st, m->lse_cpm);
-    }
     AttnCtx a{c->pctx, c->ctx, m->U_att, m->c_tt, 1};
-    step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R, st);
+    if (n_slices > 0) {  // vocab-parallel emulation: slice k as rank k of n_slices
+      ensure_xbuf(m, n_slices);
+      const int T = m->Vp / 256;
+      for (int k = 0; k < n_slices; ++k) {
+        vocab_lse(m, d.R, R, 256 * (T * k / n_slices), 256 * (T * (k + 1) / n_slices), st);
+        d.xout = m->xbuf + (size_t)k * m->xrows;
+        step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R, st);
+      }
+      d.xout = nullptr;
+      shard_combine(d, m->xbuf, n_slices, m->xrows, c->logZ, c->amax, R, st);
+    } else {
+      {
+        ProfScope p_(m, ST_VOCAB);
+        vocab_lse(m, d.R, R, 0, m->Vp, st);
+      }
+      step_elementwise(EW_FINALIZE, d, a, c->S, c->T, c->logZ, c->amax, R, st);
+    }
     std::vector<float> lz(R);
     std::vector<int> am(R);
     if (nc > 0) {
@@ -2421,6 +2491,29 @@ nmt_status nmt_ctx_stats(nmt_ctx* c, int64_t* n_nodes, int64_t* n_stepped) {
     c->sync_counters();
     if (n_nodes) *n_nodes = c->n_nodes;
     if (n_stepped) *n_stepped = c->n_slots - 2;  // slots 0 (s0) and 1 (scratch) are not steps
+  });
+}
+
+nmt_status nmt_vocab_shard(nmt_model* m, int32_t rank, int32_t world, nmt_ensemble* comm) {
+  if (!m || world < 1 || rank < 0 || rank >= world) return fail(NMT_ERR_INVALID_ARG, "bad rank/world");
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    CK(cudaSetDevice(m->device));
+    CK(cudaStreamSynchronize(m->st));
+    if (world == 1 || !comm) {
+      m->vs_world = 0;
+      m->vs_comm = nullptr;
+      return;
+    }
+    if (ens_world(comm) != world || ens_rank(comm) != rank)
+      throw NmtError(NMT_ERR_INVALID_ARG, "communicator rank/size differ from rank/world");
+    const int T = m->Vp / 256;
+    if (T < world) throw NmtError(NMT_ERR_INVALID_ARG, "fewer 256-column vocabulary tiles than ranks");
+    m->vs_world = world;
+    m->vs_rank = rank;
+    m->vs_comm = comm;
+    m->vs_n0 = 256 * (T * rank / world);
+    m->vs_n1 = 256 * (T * (rank + 1) / world);
   });
 }
 

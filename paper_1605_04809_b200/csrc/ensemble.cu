@@ -27,6 +27,7 @@ struct Nccl {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*reduce)(const void*, void*, size_t, int, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
   bool load() {
     if (h) return true;
@@ -40,6 +41,7 @@ struct Nccl {
     reduce = (decltype(reduce))dlsym(h, "ncclReduce");
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
     getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+    allGather = (decltype(allGather))dlsym(h, "ncclAllGather");
     return getUniqueId && commInitRank && reduce && commDestroy;
   }
 };
@@ -66,6 +68,15 @@ struct nmt_ensemble {
 extern "C" const char* nmt_last_error(void);
 namespace nmt {
 nmt_status set_error(nmt_status c, const std::string& m);
+
+// vocab-parallel exchange (api.cu): all-gather of `count` floats per rank on the communicator
+int ens_world(const nmt_ensemble* e) { return e->n; }
+int ens_rank(const nmt_ensemble* e) { return e->rank; }
+void ens_allgather(nmt_ensemble* e, const float* send, float* recv, size_t count, cudaStream_t st) {
+  if (!g_nccl.allGather) throw NmtError(NMT_ERR_NCCL, "ncclAllGather not found");
+  const ncclResult_t r = g_nccl.allGather(send, recv, count, kNcclFloat32, e->comm, st);
+  if (r) throw NmtError(NMT_ERR_NCCL, std::string("ncclAllGather: ") + g_nccl.getErrorString(r));
+}
 }
 
 extern "C" {

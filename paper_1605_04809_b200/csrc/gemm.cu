@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int aoff = g.a_col0 + (pass == 2 ? g.a_lo_off : 0);
             const int boff = (pass == 1 ? g.b_lo_off : 0);
             mbar_wait(&empty[stage], phase ^ 1);
-            const int arow = tc.m * CM + rank * BM, brow = tc.n * BN + rank * S::B_ROWS;
+            const int arow = tc.m * CM + rank * BM, brow = tc.n * BN + rank * S::B_ROWS + g.n_off;
             const int bx = g.b_panel_rows ? 0 : boff + kb * BK;
             const int by = g.b_panel_rows ? (boff / BK + kb) * g.b_panel_rows + brow : brow;
             if constexpr (PAIR) {
@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             float v[32];
             tmem_ld32_nowait(tbase + c, v);
             tmem_wait_ld_dep(v);
-            const int col0 = colbase + c;
+            const int col0 = colbase + c + g.n_off;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               if (v[j] > tv[kTopK - 1] && col0 + j < ep.n_valid) {  // (rare once the list is full)
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tmem_ld32_nowait(tbase + c + 32, v + 32);
             tmem_wait_ld_dep(v);
             reg_dep32(v + 32);
-            const int col0 = colbase + c;
+            const int col0 = colbase + c + g.n_off;
             if (col0 + 64 > ep.n_valid) {  // padded vocabulary columns (last tile only)
 #pragma unroll
               for (int j = 0; j < 64; ++j)

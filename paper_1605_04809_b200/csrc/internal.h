@@ -70,6 +70,8 @@ struct GemmShape {
                      // every work item carries about the same number of k-blocks
   int b_panel_rows;  // 0: B is [N][K] row-major; else B is stored as k-block panels [K/64][b_panel_rows][64]
                      // (every TMA box is one contiguous chunk): coordinate (0, kb * b_panel_rows + row)
+  int n_off;         // EPI_LSE / EPI_TOPK: first B row (= vocabulary column) of the GEMM's N range (vocab
+                     // slice of a vocab-parallel rank); reported columns are global
 };
 
 struct EpiParams {
@@ -119,6 +121,7 @@ inline GemmShape gemm_shape(int M, const int* M_dev, int N, int K, int a_col0, b
   g.reg_k1[0] = K;
   g.ksplit = 1;
   g.b_panel_rows = 0;
+  g.n_off = 0;
   return g;
 }
 inline int gemm_ks(const GemmShape& g, int r) { return g.reg_ks[r] > 0 ? g.reg_ks[r] : g.ksplit; }

@@ -865,6 +865,10 @@ __global__ void k_finalize(StepDev d, float* __restrict__ logZ, int* __restrict_
     s = ns;
     am = na;
   }
+  if (d.xout) {  // vocab-parallel: this rank's slice partial, combined after the all-gather
+    if (lane == 0) d.xout[warp] = make_float4(m, s, __int_as_float(am), 0.f);
+    return;
+  }
   const int slot = d.row_dst[warp];
   if (lane == 0 && slot >= 0) {
     if (d.gs) {
@@ -1115,6 +1119,39 @@ void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const floa
   const PlanDesc* none = nullptr;
   launch_pdl(k_gather_dot, cb + pb, 256, 0, st, c, io, Wo32, bo, Ep, out_logp, out_child32, out_child64, out_argmax,
              cb, none);
+  CK_LAUNCH();
+}
+__global__ void k_shard_combine(StepDev d, const float4* __restrict__ xall, int world, int stride,
+                                float* __restrict__ logZ, int* __restrict__ amax) {
+  pdl_enter();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= *d.R) return;
+  float m = -INFINITY, s = 0.f;
+  int am = 0x7fffffff;
+  for (int k = 0; k < world; ++k) {  // rank order = ascending vocabulary slices
+    const float4 v = xall[(int64_t)k * stride + r];
+    if (v.x > m) {
+      s = (m > -INFINITY ? s * expf(m - v.x) : 0.f) + v.y;
+      m = v.x;
+      am = __float_as_int(v.z);
+    } else if (v.x > -INFINITY) {
+      s += v.y * expf(v.x - m);
+    }
+  }
+  const int slot = d.row_dst[r];
+  if (slot < 0) return;
+  if (d.gs) {
+    const GrpStep& g = d.gs[d.row_grp[r]];
+    g.logZ[slot] = m + logf(s);
+    g.amax[slot] = am;
+  } else {
+    logZ[slot] = m + logf(s);
+    amax[slot] = am;
+  }
+}
+void shard_combine(const StepDev& d, const float4* xall, int world, int stride, float* logZ, int* amax, int R_max,
+                   cudaStream_t st) {
+  launch_pdl(k_shard_combine, (R_max + 127) / 128, 128, 0, st, d, xall, world, stride, logZ, amax);
   CK_LAUNCH();
 }
 __global__ void k_counters_multi(const PlanDesc* __restrict__ descs, int G, int* __restrict__ out) {

@@ -90,6 +90,8 @@ struct StepDev {
   __nv_bfloat16* A_t; int lda_t, lo_t;   // [R][sf*Ep]
   float4* part; int n_tiles;             // [R][2 * cpm] LSE partials of the vocabulary GEMM
   const int* cpm;                        // runs per m-tile (device, written by the GEMM)
+  float4* xout;                          // vocab-parallel: finalize writes each row's (max, sum exp,
+                                         // argmax) of this rank's vocabulary slice here (else null)
   int ks_g1, ks_q, ks_g2[3], ks_ro;      // split-K partial counts of the decoder GEMM outputs
   int64_t ps_g1, ps_q, ps_g2, ps_ro;     // floats between consecutive partials
 };
@@ -167,6 +169,10 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
 void gather_dot(const CtxDev& c, const PlanIO& io, const float* Wo32, const float* bo, int Ep, float* out_logp,
                 int* out_child32, long long* out_child64, int* out_argmax, cudaStream_t st);
 // the CNT_N counters of every group's context into out [dev, G x CNT_N] (one D2H for the call)
+// vocab-parallel combine: xall [world][stride] (max, sum exp, argmax) of each rank's slice, merged in
+// rank order (ties -> the lower rank's = lower word id) -> logZ, argmax of every row into the arena
+void shard_combine(const StepDev& d, const float4* xall, int world, int stride, float* logZ, int* amax, int R_max,
+                   cudaStream_t st);
 void counters_multi(const PlanDesc* descs, int G, int* out, cudaStream_t st);
 void gather_dot_multi(const PlanDesc* descs, int G, int max_cand, int max_par, const float* Wo32, const float* bo,
                       int Ep, cudaStream_t st);

@@ -28,7 +28,8 @@ EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "n
            "nmt_profile_read", "nmt_bench_gemm", "nmt_ensemble_init", "nmt_ensemble_get_unique_id", "nmt_ensemble_combine",
            "nmt_ensemble_free", "nmt_params_average", "nmt_beam_step",
            "nmt_encode_batch", "nmt_save_params", "nmt_params_bytes", "nmt_random_params", "nmt_create_random",
-           "nmt_debug_vocab", "nmt_score_batch_multi", "nmt_ctx_reserve", "nmt_score_sequences"]
+           "nmt_debug_vocab", "nmt_score_batch_multi", "nmt_ctx_reserve", "nmt_score_sequences",
+           "nmt_vocab_shard", "nmt_debug_vocab_shards"]
 
 
 N_STAGES = 19
@@ -154,6 +155,8 @@ def lib() -> C.CDLL:
             "nmt_score_batch_multi": (i32, [i32, vp, vp, vp, vp, vp, vp, vp]),
             "nmt_ctx_reserve": (i32, [vp, i64, i64]),
             "nmt_score_sequences": (i32, [vp, i32, vp, vp, vp, vp]),
+            "nmt_vocab_shard": (i32, [vp, i32, i32, vp]),
+            "nmt_debug_vocab_shards": (i32, [vp, i32, vp, i32, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -234,6 +237,19 @@ class Model:
         am = np.empty(R, np.int32)
         _check(lib().nmt_debug_vocab(self._h, R, _ptr(t), _ptr(off), _ptr(words), _ptr(logp), _ptr(logZ), _ptr(am)))
         return logp, logZ, am
+
+    def vocab_shard(self, rank: int, world: int, comm: Optional["Ensemble"]) -> None:
+        """nmt_vocab_shard: vocab-parallel scoring over `world` ranks (comm = an Ensemble communicator)."""
+        _check(lib().nmt_vocab_shard(self._h, rank, world, comm._h if comm is not None else None))
+
+    def debug_vocab_shards(self, t: np.ndarray, n_slices: int):
+        """nmt_debug_vocab_shards: the vocab-parallel combine emulated with n_slices slices."""
+        t = _c(t, np.float32)
+        R = t.shape[0]
+        logZ = np.empty(R, np.float32)
+        am = np.empty(R, np.int32)
+        _check(lib().nmt_debug_vocab_shards(self._h, R, _ptr(t), n_slices, _ptr(logZ), _ptr(am)))
+        return logZ, am
 
     def encode_batch(self, sources: Sequence[Sequence[int]]) -> list:
         """nmt_encode_batch: one context per source, all recurrences advanced together."""

@@ -129,3 +129,11 @@ def test_params_average_validates_before_device_work():
     with pytest.raises(nmt.NmtError) as e:
         nmt.params_average([])
     assert e.value.name == "NMT_ERR_INVALID_ARG"
+
+
+def test_no_unresolved_library_internal_symbols(libpath):
+    """every internal C++ symbol of the library is defined in it (an undefined nmt:: symbol would only
+    fail at dlopen time on the GPU box)"""
+    out = subprocess.run(["nm", "-D", "--undefined-only", libpath], capture_output=True, text=True).stdout
+    bad = [ln for ln in out.splitlines() if "nmt" in ln or "ens_" in ln]
+    assert not bad, bad

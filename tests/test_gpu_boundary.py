@@ -231,3 +231,61 @@ def test_score_batch_multi_enru(prec):
             worst = max(worst, float(np.max(np.abs(lp[off[q]:off[q + 1]] - rl))))
     print(f"\n[score_batch_multi] En->Ru 8 x 40 {prec}: max|dlogp| = {worst:.3e}")
     assert worst < TOL[prec]
+
+
+@pytest.mark.parametrize("prec", ["fp32class", "bf16"])
+def test_vocab_shards_emulated(prec):
+    """Vocab-parallel path (NEXT-2) emulated on one GPU: n slices of the vocabulary computed as ranks
+    0..n-1 and merged by the post-all-gather combine give the unsharded logZ (fp32 summation order)
+    and argmax, and logZ stays within the GEMM operand-rounding bound of the float64 oracle."""
+    d = synth.Dims(16, 32, 60, 1000, "maxout")  # Vp = 1024: 4 tiles of 256 columns
+    p = synth.make_model(d, 5)
+    M = nmt().Model(synth.params_bytes(d, p), precision=prec)
+    rng = np.random.Generator(np.random.PCG64(8))
+    t = (np.tanh(rng.standard_normal((37, d.dim_emb))) * 1.7).astype(np.float32)
+    _, lz_full, am_full = M.debug_vocab(t, np.zeros(38, np.int32), np.zeros(0, np.int32))
+    z = t.astype(np.float64) @ p["ff_logit_W"].astype(np.float64) + p["ff_logit_b"][0]
+    rel = 2.0 ** -8 if prec == "bf16" else 2.0 ** -15
+    B = (rel * (np.abs(t.astype(np.float64)) @ np.abs(p["ff_logit_W"].astype(np.float64)))).max(axis=1) + 1e-4
+    for n in (1, 2, 3, 4):
+        lz, am = M.debug_vocab_shards(t, n)
+        assert np.allclose(lz, lz_full, atol=1e-5, rtol=1e-6), n
+        assert np.array_equal(am, am_full), n
+        assert np.all(np.abs(lz - O.logsumexp(z)) <= B), n
+    with pytest.raises(nmt().NmtError):
+        M.debug_vocab_shards(t, 5)  # more slices than 256-column tiles
+
+
+def test_vocab_shards_emulated_enru():
+    d = synth.EN_RU
+    p = synth.make_model(d, 2016)
+    M = nmt().Model(synth.params_bytes(d, p), precision="bf16")
+    rng = np.random.Generator(np.random.PCG64(9))
+    t = (np.tanh(rng.standard_normal((300, d.dim_emb))) * 1.7).astype(np.float32)
+    _, lz_full, am_full = M.debug_vocab(t, np.zeros(301, np.int32), np.zeros(0, np.int32))
+    for n in (2, 8):
+        lz, am = M.debug_vocab_shards(t, n)
+        assert np.allclose(lz, lz_full, atol=1e-5, rtol=1e-6), n
+        assert np.array_equal(am, am_full), n
+
+
+def test_vocab_shard_single_rank_and_errors():
+    """world == 1 (single-rank NCCL communicator) keeps the full vocabulary; mismatched rank/world is
+    rejected."""
+    N = nmt()
+    d = synth.Dims(8, 16, 50, 50, "tanh")
+    p = synth.make_model(d, 7)
+    M = N.Model(synth.params_bytes(d, p), precision="fp32class")
+    uid = N.Ensemble.unique_id()
+    comm = N.Ensemble(1, 0, uid, 0)
+    src = synth.make_source(d.vocab_src, 4, seed=1)
+    ref = M.encode(src).score_batch([0], [0, 3], [5, 9, 2])[0]
+    M.vocab_shard(0, 1, comm)
+    got = M.encode(src).score_batch([0], [0, 3], [5, 9, 2])[0]
+    assert np.array_equal(ref, got)
+    with pytest.raises(N.NmtError) as e:
+        M.vocab_shard(1, 2, comm)  # the communicator has one rank
+    assert e.value.name == "NMT_ERR_INVALID_ARG"
+    with pytest.raises(N.NmtError):
+        M.vocab_shard(2, 2, None)
+    comm.close()
