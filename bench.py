@@ -171,6 +171,7 @@ def oracle_sample(om, d, a, rows: int, seed: int) -> tuple:
     lp, _, _ = sess.score_batch(ids, off, words)
     dt = time.perf_counter() - t0
     assert np.all(np.isfinite(lp))
+    oracle_sample.last = (src, s, y, off, words, lp)  # (inputs and result, for the parity check)
     return dt, rows * a.cands
 
 
@@ -200,20 +201,36 @@ def run_reference(a, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(a) -> dict:
+def cpu_baseline(a, M=None) -> tuple:
+    """(cpu_baseline dict, parity dict or None): the oracle timed on two full steps of the workload;
+    the same two steps through the GPU path (host C ABI) give the run's own max |dlogp|."""
     import oracle as O
     d = model_dims(a.readout)
     om = O.Model(d, synth.make_model(d, 2016))
     oracle_sample(om, d, a, 16, seed=7)  # warm BLAS
     rows = a.rows
     t, n = 0.0, 0
+    worst, cnt = 0.0, 0
     for k in range(2):
         dt, m = oracle_sample(om, d, a, rows, seed=shard_seed(0, 5000 + k))
         t += dt
         n += m
-    return {"value": n / t, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+        if M is not None:  # (untimed) the same inputs through the CUDA path
+            src, s, y, off, words, ref = oracle_sample.last
+            ctx = M.encode(src)
+            lp, _, _ = ctx.score_batch(ctx.inject_states(s, y), off, words, with_argmax=False)
+            ctx.close()
+            worst = max(worst, float(np.max(np.abs(lp.astype(np.float64) - ref))))
+            cnt += len(lp)
+    base = {"value": n / t, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
             "sample": f"2 full steps of the workload (encode Tx={a.src_len} + {rows} parents x {a.cands} words), "
                       f"float64 numpy oracle, {t:.1f} s"}
+    par = None
+    if M is not None:
+        tol = 2e-2 if a.precision == "bf16" else 1e-3
+        par = {"max_abs_dlogp": worst, "tol": tol, "ok": worst < tol, "word_scores": cnt,
+               "vs": "float64 oracle on the cpu_baseline sample (same inputs), host C ABI"}
+    return base, par
 
 
 # ------------------------------------------------------------------------------------- GPU arm
@@ -324,7 +341,8 @@ def run_ours(a, rank: int, world: int, dist) -> None:
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if a.precision == "bf16" else "bf16x3",
             "data": "synthetic (seeded random-init cGRU weights, Zipf ids, injected parent states)",
             "config": workload_config(a, world), "roofline": roof, "gpu_launches": int(launches),
-            "gpu_launches_per_step": launches / a.steps, "clocks": clocks}
+            "gpu_launches_per_step": launches / a.steps, "clocks": clocks,
+            "rows_per_s": value / a.cands}  # unique decoder steps (rows) per second
     # ---------------- optional per-stage breakdown (separate untimed pass)
     if a.stages:
         M.profile(2)
@@ -368,7 +386,7 @@ def run_ours(a, rank: int, world: int, dist) -> None:
                        "d2h_bytes_per_step": d2h,
                        "path": "nmt_encode + nmt_inject_states + nmt_score_batch (host arrays, pinned)"}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(a)
+        line["cpu_baseline"], line["parity"] = cpu_baseline(a, M)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
