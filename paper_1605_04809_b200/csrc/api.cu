@@ -440,13 +440,6 @@ struct nmt_ctx {
   ~nmt_ctx();
 };
 
-template <typename T>
-static T* grow_copy(T* old, size_t old_n, size_t new_n, cudaStream_t st) {
-  T* p = dalloc<T>(new_n);
-  if (old && old_n) CK(cudaMemcpyAsync(p, old, old_n * sizeof(T), cudaMemcpyDeviceToDevice, st));
-  return p;
-}
-
 // order the model stream after this context's encoder work (once)
 void nmt_ctx::join_enc() {
   if (enc_pending) {
@@ -465,15 +458,35 @@ void nmt_ctx::sync_counters() {
   stale = false;
 }
 
+// Arena growth is stream-ordered (cudaMallocAsync / copies / cudaFreeAsync on the model stream): no
+// host or device-wide synchronisation, so a growing context never stalls other work on the GPU.
+template <typename T>
+static T* salloc(size_t n, cudaStream_t st) {
+  void* p = nullptr;
+  CK(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st));
+  return static_cast<T*>(p);
+}
+template <typename T>
+static void sfree(T*& p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+  p = nullptr;
+}
+template <typename T>
+static T* grow_copy_async(T* old, size_t old_n, size_t new_n, cudaStream_t st) {
+  T* p = salloc<T>(new_n, st);
+  if (old && old_n) CK(cudaMemcpyAsync(p, old, old_n * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  if (new_n > old_n) CK(cudaMemsetAsync(p + old_n, 0, (new_n - old_n) * sizeof(T), st));
+  return p;
+}
+
 void nmt_ctx::grow_nodes(int64_t need) {
   int64_t nc = std::max<int64_t>(need, (int64_t)node_cap * 2);
   if (nc > INT32_MAX / 2) throw NmtError(NMT_ERR_CAPACITY, "state arena: too many nodes");
   cudaStream_t st = m->st;
-  CK(cudaStreamSynchronize(st));
   auto g = [&](int*& p, int fill) {
-    int* q = grow_copy(p, node_cap, nc, st);
+    int* q = grow_copy_async(p, node_cap, nc, st);
     fill_i32(q + node_cap, nc - node_cap, fill, st);
-    dfree(p);
+    sfree(p, st);
     p = q;
   };
   g(node_word, 0);
@@ -484,19 +497,17 @@ void nmt_ctx::grow_nodes(int64_t need) {
   int64_t nh = 1;
   while (nh < 2 * nc) nh <<= 1;
   if (nh != hcap) {
-    unsigned long long* nk = dalloc<unsigned long long>(nh);
-    int* nv = dalloc<int>(nh);
+    unsigned long long* nk = salloc<unsigned long long>(nh, st);
+    int* nv = salloc<int>(nh, st);
     CK(cudaMemsetAsync(nk, 0xff, nh * sizeof(unsigned long long), st));
     fill_i32(nv, nh, INT32_MIN, st);
     if (hkeys) rehash(hkeys, hvals, hcap, nk, nv, (uint64_t)nh - 1, st);
-    CK(cudaStreamSynchronize(st));
-    dfree(hkeys);
-    dfree(hvals);
+    sfree(hkeys, st);
+    sfree(hvals, st);
     hkeys = nk;
     hvals = nv;
     hcap = nh;
   }
-  CK(cudaStreamSynchronize(st));
   node_cap = (int)nc;
 }
 
@@ -504,16 +515,14 @@ void nmt_ctx::grow_slots(int64_t need) {
   int64_t nc = std::max<int64_t>(need, (int64_t)slot_cap * 2);
   if (nc > INT32_MAX / 2) throw NmtError(NMT_ERR_CAPACITY, "state arena: too many stepped nodes");
   cudaStream_t st = m->st;
-  CK(cudaStreamSynchronize(st));
-  float* nS = grow_copy(S, (size_t)slot_cap * m->Hp, (size_t)nc * m->Hp, st);
-  float* nT = grow_copy(T, (size_t)slot_cap * m->Ep, (size_t)nc * m->Ep, st);
-  float* nZ = grow_copy(logZ, slot_cap, nc, st);
-  int* nA = grow_copy(amax, slot_cap, nc, st);
-  CK(cudaStreamSynchronize(st));
-  dfree(S);
-  dfree(T);
-  dfree(logZ);
-  dfree(amax);
+  float* nS = grow_copy_async(S, (size_t)slot_cap * m->Hp, (size_t)nc * m->Hp, st);
+  float* nT = grow_copy_async(T, (size_t)slot_cap * m->Ep, (size_t)nc * m->Ep, st);
+  float* nZ = grow_copy_async(logZ, slot_cap, nc, st);
+  int* nA = grow_copy_async(amax, slot_cap, nc, st);
+  sfree(S, st);
+  sfree(T, st);
+  sfree(logZ, st);
+  sfree(amax, st);
   S = nS;
   T = nT;
   logZ = nZ;
@@ -930,6 +939,14 @@ static void parse_and_build(const char* buf, size_t len, const nmt_opts* opts, n
   }
   CK(cudaStreamCreateWithFlags(&m->est, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&m->enc_start_ev, cudaEventDisableTiming));
+  {  // arenas grow with cudaMallocAsync: keep released blocks in the device pool for reuse
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, o.device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
   m->split = o.precision == NMT_PREC_FP32CLASS;
   if (const char* ev = getenv("NMT_PAIR")) m->use_pair = atoi(ev) != 0;
   m->sf = m->split ? 2 : 1;
