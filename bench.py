@@ -168,10 +168,10 @@ def oracle_sample(om, d, a, rows: int, seed: int) -> tuple:
     t0 = time.perf_counter()
     sess = O.Session(om, src)
     ids = [sess.inject_state(s[i], int(y[i])) for i in range(rows)]
-    lp, _, _ = sess.score_batch(ids, off, words)
+    lp, _, am = sess.score_batch(ids, off, words)
     dt = time.perf_counter() - t0
     assert np.all(np.isfinite(lp))
-    oracle_sample.last = (src, s, y, off, words, lp)  # (inputs and result, for the parity check)
+    oracle_sample.last = (src, s, y, off, words, lp, am, sess, ids)  # (inputs and results, for the parity check)
     return dt, rows * a.cands
 
 
@@ -210,25 +210,32 @@ def cpu_baseline(a, M=None) -> tuple:
     oracle_sample(om, d, a, 16, seed=7)  # warm BLAS
     rows = a.rows
     t, n = 0.0, 0
-    worst, cnt = 0.0, 0
+    worst, cnt, top_same, top_rows, top_tie_ok = 0.0, 0, 0, 0, True
+    tol = 2e-2 if a.precision == "bf16" else 1e-3
     for k in range(2):
         dt, m = oracle_sample(om, d, a, rows, seed=shard_seed(0, 5000 + k))
         t += dt
         n += m
         if M is not None:  # (untimed) the same inputs through the CUDA path
-            src, s, y, off, words, ref = oracle_sample.last
+            src, s, y, off, words, ref, ref_am, sess, oids = oracle_sample.last
             ctx = M.encode(src)
-            lp, _, _ = ctx.score_batch(ctx.inject_states(s, y), off, words, with_argmax=False)
+            lp, _, am = ctx.score_batch(ctx.inject_states(s, y), off, words)
             ctx.close()
             worst = max(worst, float(np.max(np.abs(lp.astype(np.float64) - ref))))
             cnt += len(lp)
+            same = am == ref_am
+            top_same += int(same.sum())
+            top_rows += len(am)
+            for i in np.nonzero(~same)[0]:  # a different top-1 must lie in the oracle's tie set (A21)
+                row = sess.logprobs_full(oids[i])
+                top_tie_ok = top_tie_ok and bool(row[am[i]] >= row.max() - 2 * tol)
     base = {"value": n / t, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
             "sample": f"2 full steps of the workload (encode Tx={a.src_len} + {rows} parents x {a.cands} words), "
                       f"float64 numpy oracle, {t:.1f} s"}
     par = None
     if M is not None:
-        tol = 2e-2 if a.precision == "bf16" else 1e-3
-        par = {"max_abs_dlogp": worst, "tol": tol, "ok": worst < tol, "word_scores": cnt,
+        par = {"max_abs_dlogp": worst, "tol": tol, "ok": worst < tol and top_tie_ok, "word_scores": cnt,
+               "top1_identical": f"{top_same}/{top_rows}", "top1_in_oracle_tie_set": top_tie_ok,
                "vs": "float64 oracle on the cpu_baseline sample (same inputs), host C ABI"}
     return base, par
 
