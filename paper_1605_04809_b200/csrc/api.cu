@@ -410,7 +410,10 @@ struct nmt_ctx {
   bool stale = false;
   cudaEvent_t enc_ev = nullptr;  // end of this context's encoder work on the encoder stream
   bool enc_pending = false;      // the model stream has not waited for enc_ev yet
+  cudaEvent_t enc_s0_ev = nullptr;  // end of the recurrence (ctx, s0); the pctx GEMM follows
+  bool enc_s0_pending = false;
   void join_enc();
+  void join_enc_s0();
 
   CtxDev dev() const {
     CtxDev c{};
@@ -445,6 +448,14 @@ void nmt_ctx::join_enc() {
   if (enc_pending) {
     CK(cudaStreamWaitEvent(m->st, enc_ev, 0));
     enc_pending = false;
+    enc_s0_pending = false;
+  }
+}
+// only the recurrence (s0 in slot 0, ctx): the step's first kernels need s0, attention needs pctx
+void nmt_ctx::join_enc_s0() {
+  if (enc_s0_pending) {
+    CK(cudaStreamWaitEvent(m->st, enc_s0_ev, 0));
+    enc_s0_pending = false;
   }
 }
 
@@ -550,6 +561,7 @@ nmt_ctx::~nmt_ctx() {
   }
   if (m && m->est) cudaStreamSynchronize(m->est);
   if (enc_ev) cudaEventDestroy(enc_ev);
+  if (enc_s0_ev) cudaEventDestroy(enc_s0_ev);
   for (int** p : {&counters, &node_word, &node_parent, &node_src, &node_slot, &node_claim, &hvals, &amax}) dfree(*p);
   dfree(hkeys);
   for (float** p : {&ctx, &pctx, &S, &T, &logZ}) dfree(*p);
@@ -1128,7 +1140,7 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
   const int Hp = m->Hp, Cp = m->Cp, Ep = m->Ep;
   const bool sp = m->split;
   const int rps = round_up(std::max(R_max, 1), 256);  // rows per split-K partial
-  if (!ms) c->join_enc();  // s0 (slot 0), ctx and pctx come from the encoder (multi: the caller joins)
+  if (!ms) c->join_enc_s0();  // s0 (slot 0) comes from the encoder (multi: the caller joins)
   { ProfScope p_(m, ST_GATHER); step_elementwise(EW_GATHER, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   if (!stage_skipped(ST_GEMM_H1)) {
     ProfScope p_(m, ST_GEMM_H1);
@@ -1145,6 +1157,7 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
     d.ks_q = g.reg_ks[0];
     d.ps_q = (int64_t)rps * Cp;
   }
+  if (!ms) c->join_enc();  // ctx and pctx (the pctx GEMM overlapped the steps above)
   if (!stage_skipped(ST_ATTN)) { ProfScope p_(m, ST_ATTN); step_elementwise(EW_ATTN, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   if (!stage_skipped(ST_GEMM_G2)) {
     ProfScope p_(m, ST_GEMM_G2);
@@ -1440,6 +1453,7 @@ static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
     c->pctx = dalloc<float>((size_t)m->maxTx * m->Cp);
     c->counters = dalloc<int>(CNT_N);
     CK(cudaEventCreateWithFlags(&c->enc_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->enc_s0_ev, cudaEventDisableTiming));
     c->grow_nodes(4096);
     c->grow_slots(1024);
     g.release();
@@ -1543,6 +1557,10 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
                 dd, lmin, lmax, wmin, amin, wmax, amax);
       }
     }
+  }
+  if (es != st) {
+    CK(cudaEventRecord(c->enc_s0_ev, es));
+    c->enc_s0_pending = true;
   }
   if (!stage_skipped(ST_ENC_PCTX)) {  // E7: pctx = ctx.Wc_att + b_att
     ProfScope p_(m, ST_ENC_PCTX);
