@@ -129,6 +129,7 @@ struct nmt_model {
   float* U_att = nullptr;      // [Cp]
   float c_tt = 0.f;
   __nv_bfloat16* W_h1 = nullptr;  // [3Hp][sf Hp]
+  __nv_bfloat16* W_h1g = nullptr; // [4Hp][sf Hp] per 32-unit group [r | u | x | 0] (fused GRU1 epilogue)
   float* Ex = nullptr;            // [V+1][3Hp]
   __nv_bfloat16* W_q = nullptr;   // [Cp][sf Hp]
   __nv_bfloat16* W_g2 = nullptr;  // [4Hp][sf (Hp+Cp)]
@@ -140,7 +141,7 @@ struct nmt_model {
   float* W_o32 = nullptr;         // [V][Ep]
   float* b_o = nullptr;           // [V]
   bool use_pair = true;  // CTA-pair (cta_group::2) GEMMs where the shapes allow (NMT_PAIR=0 disables)
-  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128;
+  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128, tm_Wh1g;
   // encoder workspace
   int Tpad = 0;
   __nv_bfloat16* ctxbf = nullptr; // [Tpad][4Hp]
@@ -247,7 +248,7 @@ static void free_all_model(nmt_model* m) {
   for (float** p : {&m->EncIn, &m->Uarr, &m->W_initT, &m->b_init, &m->b_att, &m->U_att, &m->Ex, &m->b_nl, &m->bx_nl,
                     &m->Eproj, &m->W_o32, &m->b_o, &m->hbuf, &m->enc_mean, &m->ksplit_buf})
     dfree(*p);
-  for (__nv_bfloat16** p : {&m->Watt, &m->W_h1, &m->W_q, &m->W_g2, &m->W_ro, &m->W_o, &m->ctxbf}) dfree(*p);
+  for (__nv_bfloat16** p : {&m->W_h1g, &m->Watt, &m->W_h1, &m->W_q, &m->W_g2, &m->W_ro, &m->W_o, &m->ctxbf}) dfree(*p);
   dfree(m->bar);
   dfree(m->d_src);
   dfree(m->W_encb);
@@ -738,6 +739,24 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
     for (int g = 0; g < 2; ++g) pack_T(U.d + g * H, 2 * H, H, H, m->W_h1, sf * Hp, g * Hp, 0, 0, 0, H, Hp, lo_h, st);
     pack_T(Ux.d, H, H, H, m->W_h1, sf * Hp, 2 * Hp, 0, 0, 0, H, Hp, lo_h, st);
   }
+  {  // the same weights interleaved per 32-unit group for the fused GRU1 epilogue (EPI_GRU):
+     // B row (j / 32) * 128 + g * 32 + j % 32 = gate g (r, u, x) of unit j; rows 96..127 of a group 0
+    std::vector<float> wg((size_t)H * 4 * Hp, 0.f);
+    const float* U = hv("decoder_U");
+    const float* Ux = hv("decoder_Ux");
+    for (int k = 0; k < H; ++k)
+      for (int j = 0; j < H; ++j) {
+        const size_t col = (size_t)(j / 32) * 128 + j % 32;
+        wg[(size_t)k * 4 * Hp + col] = U[(size_t)k * 2 * H + j];
+        wg[(size_t)k * 4 * Hp + col + 32] = U[(size_t)k * 2 * H + H + j];
+        wg[(size_t)k * 4 * Hp + col + 64] = Ux[(size_t)k * H + j];
+      }
+    float* dwg = upload_vec(wg, st);
+    m->W_h1g = dalloc<__nv_bfloat16>((size_t)4 * Hp * sf * Hp);
+    pack_T(dwg, 4 * Hp, H, 4 * Hp, m->W_h1g, sf * Hp, 0, 0, 0, 0, H, Hp, lo_h, st);
+    CK(cudaStreamSynchronize(st));
+    dfree(dwg);
+  }
   m->W_q = dalloc<__nv_bfloat16>((size_t)Cp * sf * Hp);
   {
     Upload w(A.at("decoder_W_comb_att"), st);
@@ -854,6 +873,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   m->tm_Wencb = make_tmap_bf16(m->W_encb, 6 * Hp, 4 * Hp, 128);
   m->tm_Winitb = make_tmap_bf16(m->W_initb, Hp, 2 * Cp, 128);
   m->tm_Wh1 = make_tmap_bf16(m->W_h1, 3 * Hp, sf * Hp, 128);
+  m->tm_Wh1g = make_tmap_bf16(m->W_h1g, 4 * Hp, sf * Hp, 128);
   m->tm_Wq = make_tmap_bf16(m->W_q, Cp, sf * Hp, 128);
   m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, 128);
   m->tm_Wro = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 128);
@@ -1142,14 +1162,35 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
   const int rps = round_up(std::max(R_max, 1), 256);  // rows per split-K partial
   if (!ms) c->join_enc_s0();  // s0 (slot 0) comes from the encoder (multi: the caller joins)
   { ProfScope p_(m, ST_GATHER); step_elementwise(EW_GATHER, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  if (!stage_skipped(ST_GEMM_H1)) {
+  // D2: GEMM s.[U|Ux] with the GRU1 gates in its epilogue (one launch, no G1 round trip), or the
+  // split-K GEMM + k_gru1 (multi-context steps, 1-CTA mode, NMT_FUSE_GRU1=0)
+  static const bool fuse_env = !(getenv("NMT_FUSE_GRU1") && atoi(getenv("NMT_FUSE_GRU1")) == 0);  // (diagnostic)
+  if (fuse_env && !ms && m->use_pair && !stage_skipped(ST_GEMM_H1)) {
     ProfScope p_(m, ST_GEMM_H1);
-    GemmShape g = gemm_shape(0, Rd, 3 * Hp, Hp, 0, sp, Hp, Hp);
-    gemm_auto(m, m->tm_As, m->tm_Wh1, g, m->G1, 3 * Hp, rps, R_max, st);
-    d.ks_g1 = g.reg_ks[0];
-    d.ps_g1 = (int64_t)rps * 3 * Hp;
+    GemmShape g = gemm_shape(0, Rd, 4 * Hp, Hp, 0, sp, Hp, Hp);
+    EpiParams ep{};
+    ep.gx = m->Ex;
+    ep.gx_ld = 3 * Hp;
+    ep.row_y = m->row_y;
+    ep.y_bos = m->V;
+    ep.row_src = m->row_src;
+    ep.S = c->S;
+    ep.S1 = m->S1;
+    ep.X = m->X;
+    ep.ldx = d.ldx;
+    ep.lo_x = d.lo_x;
+    ep.Hp = Hp;
+    gemm_gru_pair(m->tm_As, m->tm_Wh1g, g, ep, R_max, st);
+  } else {
+    if (!stage_skipped(ST_GEMM_H1)) {
+      ProfScope p_(m, ST_GEMM_H1);
+      GemmShape g = gemm_shape(0, Rd, 3 * Hp, Hp, 0, sp, Hp, Hp);
+      gemm_auto(m, m->tm_As, m->tm_Wh1, g, m->G1, 3 * Hp, rps, R_max, st);
+      d.ks_g1 = g.reg_ks[0];
+      d.ps_g1 = (int64_t)rps * 3 * Hp;
+    }
+    if (!stage_skipped(ST_GRU1)) { ProfScope p_(m, ST_GRU1); step_elementwise(EW_GRU1, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   }
-  if (!stage_skipped(ST_GRU1)) { ProfScope p_(m, ST_GRU1); step_elementwise(EW_GRU1, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   if (!stage_skipped(ST_GEMM_Q)) {
     ProfScope p_(m, ST_GEMM_Q);
     GemmShape g = gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp);

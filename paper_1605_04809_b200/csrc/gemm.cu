@@ -32,6 +32,7 @@ namespace nmt {
 
 constexpr int BM = 128, BK = 64;
 constexpr int EPI_STORE = 0, EPI_LSE = 1, EPI_TOPK = 2;  // TOPK: runs like LSE, keeps the kTopK best logits
+constexpr int EPI_GRU = 3;  // fused GRU gates (one tile per item like EPI_STORE, no split-K)
 constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant, each owning half of the tile's columns
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
@@ -97,7 +98,7 @@ NMT_DEV Sched make_sched(const GemmShape& g, int M, int CM, int BN, int units) {
   s.num_m = (M + CM - 1) / CM;
   s.num_n = g.N / BN;
   s.nreg = g.nreg;
-  if (EPI >= 1) {  // EPI_LSE / EPI_TOPK: (m-tile, n-run) items
+  if (EPI == EPI_LSE || EPI == EPI_TOPK) {  // (m-tile, n-run) items
     s.cpm = max(1, units / max(1, s.num_m));
     s.chunk = (s.num_n + s.cpm - 1) / s.cpm;
     s.items = s.num_m * s.cpm;
@@ -123,6 +124,22 @@ NMT_DEV RegionK region_of(const GemmShape& g, int n0) {
 #pragma unroll 1
   while (r < g.nreg - 1 && n0 >= g.reg_n_end[r]) ++r;
   return RegionK{g.reg_k0[r] / BK, g.reg_k1[r] / BK, g.reg_ks[r] > 0 ? g.reg_ks[r] : g.ksplit};
+}
+
+NMT_DEV float gru_sigm(float x) { return 1.f / (1.f + expf(-x)); }
+NMT_DEV uint32_t gru_pk(float lo, float hi) {
+  uint32_t y;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(y) : "f"(hi), "f"(lo));
+  return y;
+}
+// 4 values as bf16 (and the bf16 residuals at +lo_off when lo_off > 0)
+NMT_DEV void gru_store4(__nv_bfloat16* p, int lo_off, float a, float b, float c, float d) {
+  const uint32_t h01 = gru_pk(a, b), h23 = gru_pk(c, d);
+  *reinterpret_cast<uint2*>(p) = make_uint2(h01, h23);
+  if (lo_off > 0)
+    *reinterpret_cast<uint2*>(p + lo_off) =
+        make_uint2(gru_pk(a - __uint_as_float(h01 << 16), b - __uint_as_float(h01 & 0xffff0000u)),
+                   gru_pk(c - __uint_as_float(h23 << 16), d - __uint_as_float(h23 & 0xffff0000u)));
 }
 
 template <int BN, int STAGES, int EPI, bool PAIR>
@@ -174,7 +191,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int M = g.M_dev ? *g.M_dev : g.M;
   const int unit = PAIR ? blockIdx.x / 2 : blockIdx.x, nunits = PAIR ? gridDim.x / 2 : gridDim.x;
   const Sched sc = make_sched<EPI>(g, M, CM, BN, nunits);
-  if (EPI != EPI_STORE && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
+  if ((EPI == EPI_LSE || EPI == EPI_TOPK) && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs of a pair)
@@ -346,6 +363,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               }
             }
           }
+        } else if constexpr (EPI == EPI_GRU) {
+          // this warp's COLS = 128 columns are one 32-unit group [r | u | h~ | pad] of its row
+          static_assert(BN / 2 == 128, "EPI_GRU: one 32-unit group per epilogue warp");
+          float vr[32], vu[32], vx[32];
+          tmem_ld32_nowait(tbase, vr);
+          tmem_ld32_nowait(tbase + 32, vu);
+          tmem_ld32_nowait(tbase + 64, vx);
+          tmem_wait_ld_dep(vr);
+          reg_dep32(vu);
+          reg_dep32(vx);
+          if (valid) {
+            const int j0 = (colbase >> 7) * 32, Hp = ep.Hp;
+            const int y = ep.row_y[grow];
+            const float* gxr = ep.gx + (int64_t)(y < 0 ? ep.y_bos : y) * ep.gx_ld + j0;
+            const float* sp = ep.S + (int64_t)ep.row_src[grow] * Hp + j0;
+            float* s1 = ep.S1 + (int64_t)grow * Hp + j0;
+            __nv_bfloat16* xo = ep.X + (int64_t)grow * ep.ldx + j0;
+#pragma unroll
+            for (int k = 0; k < 32; k += 4) {
+              const float4 er = __ldg(reinterpret_cast<const float4*>(gxr + k));
+              const float4 eu = __ldg(reinterpret_cast<const float4*>(gxr + Hp + k));
+              const float4 ec = __ldg(reinterpret_cast<const float4*>(gxr + 2 * Hp + k));
+              const float4 sv = *reinterpret_cast<const float4*>(sp + k);
+              float o[4];
+              const float erv[4] = {er.x, er.y, er.z, er.w}, euv[4] = {eu.x, eu.y, eu.z, eu.w};
+              const float ecv[4] = {ec.x, ec.y, ec.z, ec.w}, svv[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float rg = gru_sigm(erv[i] + vr[k + i]), ug = gru_sigm(euv[i] + vu[k + i]);
+                o[i] = ug * svv[i] + (1.f - ug) * tanhf(rg * vx[k + i] + ecv[i]);
+              }
+              *reinterpret_cast<float4*>(s1 + k) = make_float4(o[0], o[1], o[2], o[3]);
+              gru_store4(xo + k, ep.lo_x, o[0], o[1], o[2], o[3]);
+            }
+          }
         } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
 #pragma unroll 1
           for (int c = 0; c < COLS; c += 64) {
@@ -500,7 +552,7 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
     nt0 = nt1;
   }
   int grid = (PAIR ? 2 : 1) * tiles;
-  if (EPI != EPI_STORE || grid > kNumSMs) grid = kNumSMs;  // persistent (LSE / TOPK runs use every unit)
+  if (EPI == EPI_LSE || EPI == EPI_TOPK || grid > kNumSMs) grid = kNumSMs;  // persistent (LSE / TOPK runs use every unit)
   if (grid <= 0) return;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -575,6 +627,13 @@ void gemm_store_pair(const CUtensorMap& a, const CUtensorMap& b_half, const Gemm
 }
 
 // fused vocabulary GEMM + online log-sum-exp partials; BN = 256.
+void gemm_gru_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, const EpiParams& ep, int M_max,
+                   cudaStream_t st) {
+  gemm_validate(g, 256);
+  if (gemm_ks_max(g) != 1) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: the fused GRU epilogue needs the full K sum");
+  launch<256, 5, EPI_GRU, true>(a, b_half, b_half /*unused*/, g, ep, M_max, st);
+}
+
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
               cudaStream_t st, int* cpm_out) {
   gemm_validate(g, 256);

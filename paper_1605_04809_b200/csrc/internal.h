@@ -85,6 +85,17 @@ struct EpiParams {
   int* cpm_out;  // EPI_LSE: runs per m-tile (partials per row = 2 * cpm), written by CTA 0
   int rows_per_split;  // EPI_STORE: row offset of split-K partial s is s * rows_per_split
   float2* topk;        // EPI_TOPK: [R][2 cpm][kTopK] (logit, column) per (row, run, half), descending
+  // EPI_GRU (fused GRU gates, B rows interleaved per 32-unit group as [r | u | h~ | zero pad]):
+  //   h' = u*h + (1-u)*tanh(r*acc_x + gx_x) with r = sigm(gx_r + acc_r), u = sigm(gx_u + acc_u)
+  const float* gx;     // [.][gx_ld] input projections + biases, row gx_row(r): [r | u | x] blocks of Hp
+  int gx_ld;
+  const int* row_y;    // gx row of output row r: row_y[r] (< 0 -> y_bos)
+  int y_bos;
+  const int* row_src;  // previous state of output row r: S[row_src[r]]
+  const float* S;      // [.][Hp]
+  float* S1;           // [R][Hp] new state (fp32)
+  __nv_bfloat16* X;    // [R][ldx] new state as the next GEMM's bf16 operand (lo at +lo_x if > 0)
+  int ldx, lo_x, Hp;
 };
 constexpr int kTopK = 8;  // NMT_TOPK_MAX: words per row kept by the top-k vocabulary epilogue
 
@@ -102,6 +113,9 @@ void gemm_topk_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmS
                     cudaStream_t st, int* cpm_out);
 void gemm_lse_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float4* part, int n_valid,
                    cudaStream_t st, int* cpm_out);
+// GEMM s.[U|Ux] with the GRU gates fused into the epilogue (CTA pairs, no split-K); see EPI_GRU
+void gemm_gru_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, const EpiParams& ep, int M_max,
+                   cudaStream_t st);
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
               cudaStream_t st, int* cpm_out);
 
