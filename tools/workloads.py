@@ -63,6 +63,7 @@ def c3(a):
         words = np.array([w for _, t in pairs for w in t], np.int32)
         hidx = np.array([h for h, _ in pairs], np.int64)
         ctx = M.encode(src)
+        ctx.reserve(1024 + len(words) + 1, len(words))  # (pooled arena: grows during warm-up only)
         hyps = ctx.inject_states(s, y)
         lp, fin, st = ctx.score_forest(hyps[hidx], off, words)  # native ScoreBatch (one call)
         ctx.close()
@@ -105,6 +106,8 @@ def sweep(a):
         lp = torch.empty(3 * R, device="cuda")
         ch = torch.empty(3 * R, dtype=torch.int32, device="cuda")
         ctx = M.encode_dev(src.data_ptr(), 50)
+        n_inj = 1 + 3 + a.iters  # injections of R parents into this context (+ their 3R children)
+        ctx.reserve(4 * R * n_inj + 1, 2 * R * n_inj)  # steady state: no arena growth while timed
         ctx.inject_states_dev(R, ds.data_ptr(), dy.data_ptr(), ids.data_ptr())
 
         def score():  # re-score fresh parents every iteration: inject new nodes each time
@@ -135,7 +138,8 @@ def sweep(a):
                           "rows_per_s": R / (t / 1000), "vocab_ms": vms, "vocab_tflops": tf,
                           "vocab_frac_bf16_peak": tf / pk["bf16_tflops"], "W_o_stream_GBps": wo_gbs,
                           "W_o_frac_hbm": wo_gbs / pk["hbm_gbs"],
-                          "note": "per batch: inject R parents + nmt_score_batch_dev (no encode), L2 flushed"}),
+                          "note": "per batch: inject R parents + nmt_score_batch_dev (no encode), L2 flushed, "
+                                  "arena reserved up front (no growth while timed)"}),
               flush=True)
 
 
@@ -147,7 +151,9 @@ def beam(a):
     for R in [256, 1024, 4096]:
         s, y = synth.make_states(R, d.dim_hid, d.vocab_tgt, seed=R)
         ctx = M.encode(src)
-        for _ in range(3):  # warm-up (arena growth)
+        n_inj = 3 + a.iters
+        ctx.reserve(9 * R * n_inj + 1, 2 * R * n_inj)  # steady state: no arena growth while timed
+        for _ in range(3):  # warm-up
             ctx.beam_step(ctx.inject_states(s, y), 8)
         ts = []
         for _ in range(a.iters):
