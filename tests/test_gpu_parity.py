@@ -223,3 +223,42 @@ def test_bench_config_sampled(bench_model, prec):
     print(f"\n[parity] bench config R=1024 maxout {prec} (sampled rows): max|dlogp| = {worst:.3e}")
     assert worst < TOL[prec], worst
     assert len(set(ch.tolist())) == len(ch)
+
+
+def test_tiny_max_source_length(tiny):
+    """Tx = max_src_len (64 by default): the longest source the context accepts, encoded and scored
+    against the oracle (the attention softmax over 64 positions, the encoder's full smem staging)."""
+    d, p, M, om, prec = tiny
+    src = synth.make_source(d.vocab_src, 63, seed=64)
+    assert len(src) == 64
+    c = M.encode(src)
+    sess = O.Session(om, src)
+    lp, ch, _ = c.score_batch([0], [0, 4], [3, 7, 0, 1])
+    rl, rc, _ = sess.score_batch([0], [0, 4], [3, 7, 0, 1])
+    assert list(ch) == list(rc)
+    assert np.max(np.abs(lp - rl)) < TOL[prec]
+
+
+@pytest.mark.parametrize("prec", ["bf16"])
+def test_enru_large_batch_sampled(enru, prec):
+    """R = 8192 unique parents x 2 words at the En->Ru shape (the top of bench's batch sweep): a
+    sample of rows against the oracle, every log-prob finite and <= 0, child ids distinct."""
+    d, p, blob, om = enru
+    M = nmt().Model(blob, precision=prec)
+    src = synth.make_source(d.vocab_src, 29, seed=81)
+    c = M.encode(src)
+    R = 8192
+    s, y = synth.make_states(R, d.dim_hid, d.vocab_tgt, seed=82)
+    ids = c.inject_states(s, y)
+    off, words = synth.make_candidates(R, 2, d.vocab_tgt, seed=83)
+    lp, ch, am = c.score_batch(ids, off, words)
+    assert np.all(np.isfinite(lp)) and np.all(lp <= 0)
+    assert len(set(ch.tolist())) == len(ch)
+    sess = O.Session(om, src)
+    worst = 0.0
+    for i in (0, 1, 4095, 4096, 8190, 8191):
+        oid = sess.inject_state(s[i], int(y[i]))
+        rl, _, _ = sess.score_batch([oid], [0, 2], words[off[i]:off[i + 1]])
+        worst = max(worst, float(np.max(np.abs(lp[off[i]:off[i + 1]] - rl))))
+    print(f"\n[parity] En->Ru R={R} {prec}: sampled max|dlogp| = {worst:.3e}")
+    assert worst < TOL[prec]
