@@ -31,10 +31,14 @@ struct Nccl {
   const char* (*getErrorString)(ncclResult_t) = nullptr;
   bool load() {
     if (h) return true;
-    const char* cands[] = {"libnccl.so.2", "libnccl.so",
-                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    // The NCCL that torch itself links (nvidia/nccl/lib in the Python environment) comes first: the
+    // first libnccl.so.2 loaded in the process is the one every later user binds to by soname, so
+    // loading an older system copy before torch would break torch's own import.
+    const char* env = getenv("NMT_NCCL_LIB");  // set by the Python binding to torch's copy
+    const char* cands[] = {env ? env : "", "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2",
+                           "libnccl.so.2", "libnccl.so"};
     for (const char* c : cands)
-      if ((h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+      if (*c && (h = dlopen(c, RTLD_NOW | RTLD_LOCAL))) break;
     if (!h) return false;
     getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
     commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");

@@ -108,11 +108,29 @@ class Opts(C.Structure):
 _lib = None
 
 
+def _torch_nccl_path() -> Optional[str]:
+    """Path of the NCCL that torch links (pip package nvidia-nccl), found without importing torch."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            return p
+    return None
+
+
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} not built (run python -m paper_1605_04809_b200.build)")
+        if "NMT_NCCL_LIB" not in os.environ:  # ensemble hook: the same NCCL as torch (ensemble.cu)
+            p = _torch_nccl_path()
+            if p:
+                os.environ["NMT_NCCL_LIB"] = p
         L = C.CDLL(LIB_PATH)
         vp, i32, i64, f32p = C.c_void_p, C.c_int32, C.c_int64, C.c_void_p
         sig = {
