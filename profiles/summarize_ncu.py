@@ -12,7 +12,8 @@ KEYS = {
     "l2_to_sm_GB": "l1tex__m_xbar2l1tex_read_bytes.sum",
     "l2_to_sm_pct_peak": "l1tex__m_xbar2l1tex_read_bytes.sum.pct_of_peak_sustained_elapsed",
     "tensor_mem_cycles_pct": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
-    "tensor_pipe_realtime_pct": "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "tensor_mem_cycles_pct_elapsed": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "hmma_subpipe_active_cycles_realtime": "TPC.TriageCompute.sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
     "xu_pipe_pct": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
     "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "registers": "launch__registers_per_thread",
