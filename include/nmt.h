@@ -211,6 +211,15 @@ NMT_API nmt_status nmt_beam_step(nmt_ctx* c, int32_t n_parents, const nmt_state*
 NMT_API nmt_status nmt_score_forest(nmt_ctx* c, int32_t n_pairs, const nmt_state* hyp_states,
                                     const int32_t* phrase_offsets, const int32_t* phrase_words, float* out_logp,
                                     nmt_state* out_state, int32_t* stats);
+/* ScoreBatch over several sentences at once: pair i expands hyp_states[i], a state of
+ * ctx_per_pair[i] [host, n_pairs; contexts of one model], by its phrase (as nmt_score_forest, any
+ * length).  Each depth is ONE fused multi-context step (nmt_score_batch_multi), so the stacks of
+ * many sentences share the decoder GEMMs; shared prefixes collapse per context.  out_logp [host]
+ * = the phrase's summed log-prob, out_state [host] = the state after it (a state of that pair's
+ * context).  Errors as nmt_score_batch_multi; outputs are written only on success.             */
+NMT_API nmt_status nmt_score_forest_multi(int32_t n_pairs, nmt_ctx* const* ctx_per_pair, const nmt_state* hyp_states,
+                                          const int32_t* phrase_offsets, const int32_t* phrase_words,
+                                          float* out_logp, nmt_state* out_state);
 /* n-best forced rescoring (rescoring gives "the same as if they
  * were produced at decode-time"): sequence i = words[offsets[i] .. offsets[i+1]) [host] (non-empty,
  * any length; the caller appends EOS) is scored from the root: out_logp[i] = sum_j log p(w_j | w_<j)

@@ -2313,6 +2313,60 @@ nmt_status nmt_score_batch_multi(int32_t np, nmt_ctx* const* cpp, const nmt_stat
   });
 }
 
+// ScoreBatch over the expansions of SEVERAL sentences (Alg. 1, one forest per
+// context): depth by depth, every pair still running contributes (its current state, its next word)
+// to ONE fused multi-context step (nmt_score_batch_multi: shared prefixes collapse in the state
+// cache, rows of all sentences share the decoder GEMMs); the word log-probs are summed per pair.
+nmt_status nmt_score_forest_multi(int32_t n_pairs, nmt_ctx* const* ctx_per_pair, const nmt_state* hyp,
+                                  const int32_t* poff, const int32_t* pwords, float* out_logp, nmt_state* out_state) {
+  if (n_pairs < 0) return fail(NMT_ERR_INVALID_ARG, "n_pairs < 0");
+  if (n_pairs == 0) return NMT_OK;
+  if (!ctx_per_pair || !hyp || !poff || !pwords || !out_logp || !out_state)
+    return fail(NMT_ERR_INVALID_ARG, "NULL array");
+  if (poff[0] != 0) return fail(NMT_ERR_INVALID_ARG, "phrase_offsets[0] != 0");
+  int maxd = 0;
+  for (int i = 0; i < n_pairs; ++i) {
+    if (poff[i + 1] <= poff[i]) return fail(NMT_ERR_INVALID_ARG, "empty expansion (pair " + std::to_string(i) + ")");
+    maxd = std::max(maxd, poff[i + 1] - poff[i]);
+  }
+  std::vector<nmt_state> cur(hyp, hyp + n_pairs);
+  std::vector<double> sum((size_t)n_pairs, 0.0);
+  std::vector<nmt_ctx*> cp;
+  std::vector<nmt_state> par, child;
+  std::vector<int32_t> off, w, idx;
+  std::vector<float> lp;
+  for (int d = 0; d < maxd; ++d) {
+    cp.clear();
+    par.clear();
+    w.clear();
+    idx.clear();
+    for (int i = 0; i < n_pairs; ++i)
+      if (poff[i] + d < poff[i + 1]) {
+        cp.push_back(ctx_per_pair[i]);
+        par.push_back(cur[i]);
+        w.push_back(pwords[poff[i] + d]);
+        idx.push_back(i);
+      }
+    const int n = (int)idx.size();
+    off.resize(n + 1);
+    for (int k = 0; k <= n; ++k) off[k] = k;
+    lp.resize(n);
+    child.resize(n);
+    const nmt_status r =
+        nmt_score_batch_multi(n, cp.data(), par.data(), off.data(), w.data(), lp.data(), child.data(), nullptr);
+    if (r != NMT_OK) return r;
+    for (int k = 0; k < n; ++k) {
+      sum[idx[k]] += lp[k];
+      cur[idx[k]] = child[k];
+    }
+  }
+  for (int i = 0; i < n_pairs; ++i) {
+    out_logp[i] = (float)sum[i];
+    out_state[i] = cur[i];
+  }
+  return NMT_OK;
+}
+
 nmt_status nmt_score_batch_dev(nmt_ctx* c, int32_t np, const int32_t* parents, const int32_t* off, int32_t nc,
                                const int32_t* words, float* out_logp, int32_t* out_child, int32_t* out_argmax) {
   if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");

@@ -29,7 +29,7 @@ EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "n
            "nmt_ensemble_free", "nmt_params_average", "nmt_beam_step",
            "nmt_encode_batch", "nmt_save_params", "nmt_params_bytes", "nmt_random_params", "nmt_create_random",
            "nmt_debug_vocab", "nmt_score_batch_multi", "nmt_ctx_reserve", "nmt_score_sequences",
-           "nmt_vocab_shard", "nmt_debug_vocab_shards"]
+           "nmt_vocab_shard", "nmt_debug_vocab_shards", "nmt_score_forest_multi"]
 
 
 N_STAGES = 19
@@ -87,6 +87,23 @@ def score_batch_multi(contexts, parents, cand_offsets, cand_words, with_argmax: 
     _check(lib().nmt_score_batch_multi(n, hs_ptr, _ptr(par), _ptr(off), _ptr(words), _ptr(logp),
                                        _ptr(child), _ptr(am)))
     return logp, child, am
+
+
+def score_forest_multi(contexts, hyp_states, phrase_offsets, phrase_words):
+    """nmt_score_forest_multi: pair i expands hyp_states[i] of contexts[i] (Context objects or int64
+    handles) by its phrase; returns (summed log-probs [n], final states [n])."""
+    n = len(hyp_states)
+    if isinstance(contexts, np.ndarray):
+        hs = np.ascontiguousarray(contexts, dtype=np.int64)
+    else:
+        hs = np.array([c._h.value for c in contexts], np.int64)
+    st = _c(hyp_states, np.int64)
+    off = _c(phrase_offsets, np.int32)
+    w = _c(phrase_words, np.int32)
+    lp = np.empty(n, np.float32)
+    out = np.empty(n, np.int64)
+    _check(lib().nmt_score_forest_multi(n, _ptr(hs), _ptr(st), _ptr(off), _ptr(w), _ptr(lp), _ptr(out)))
+    return lp, out
 
 
 class NmtError(RuntimeError):
@@ -174,6 +191,7 @@ def lib() -> C.CDLL:
             "nmt_ctx_reserve": (i32, [vp, i64, i64]),
             "nmt_score_sequences": (i32, [vp, i32, vp, vp, vp, vp]),
             "nmt_vocab_shard": (i32, [vp, i32, i32, vp]),
+            "nmt_score_forest_multi": (i32, [i32, vp, vp, vp, vp, vp, vp]),
             "nmt_debug_vocab_shards": (i32, [vp, i32, vp, i32, vp, vp]),
         }
         for name, (res, args) in sig.items():

