@@ -221,6 +221,7 @@ struct nmt_model {
   std::atomic<int> refs{1};
   // released contexts kept for reuse (no cudaMalloc / memset per sentence)
   std::vector<nmt_ctx*> pool;
+  size_t pool_bytes = 0;  // arena bytes held by pooled contexts (trimmed above NMT_POOL_CAP_GB)
   // CUDA-event profiling of the stages (mode 0 off, 1 vocabulary GEMM only, 2 all)
   int prof_mode = 0;
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> prof_pending;
@@ -438,6 +439,10 @@ struct nmt_ctx {
     return c;
   }
   void sync_counters();
+  size_t arena_bytes() const {
+    return (size_t)slot_cap * (m->Hp + m->Ep + 2) * 4 + (size_t)node_cap * 5 * 4 + (size_t)hcap * 12;
+  }
+  void shrink();
   void grow_nodes(int64_t need);
   void grow_slots(int64_t need);
   void ensure(int64_t add_nodes, int64_t add_slots);
@@ -521,6 +526,19 @@ void nmt_ctx::grow_nodes(int64_t need) {
     hcap = nh;
   }
   node_cap = (int)nc;
+}
+
+// back to the initial arena (4096 nodes, 1024 slots), stream-ordered: a pooled context that grew
+// for one huge sentence does not keep GBs for the rest of the run
+void nmt_ctx::shrink() {
+  cudaStream_t st = m->st;
+  for (int** p : {&node_word, &node_parent, &node_src, &node_slot, &node_claim, &hvals, &amax}) sfree(*p, st);
+  sfree(hkeys, st);
+  for (float** p : {&S, &T, &logZ}) sfree(*p, st);
+  node_cap = slot_cap = 0;
+  hcap = 0;
+  grow_nodes(4096);
+  grow_slots(1024);
 }
 
 void nmt_ctx::grow_slots(int64_t need) {
@@ -1484,6 +1502,7 @@ static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
     c = m->pool.back();
     m->pool.pop_back();
     c->m = m;
+    m->pool_bytes -= std::min(m->pool_bytes, c->arena_bytes());
     m->refs.fetch_add(1);
   } else {
     c = new nmt_ctx();
@@ -1850,6 +1869,12 @@ void nmt_ctx_free(nmt_ctx* c) {
       c->join_enc();  // later model-stream work on the reused arena follows its encoder
     } catch (...) {
     }
+    static const double cap_gb = getenv("NMT_POOL_CAP_GB") ? atof(getenv("NMT_POOL_CAP_GB")) : 32.0;
+    try {
+      if ((double)(m->pool_bytes + c->arena_bytes()) > cap_gb * (1 << 30)) c->shrink();
+    } catch (...) {
+    }
+    m->pool_bytes += c->arena_bytes();
     c->m = nullptr;  // pooled arenas hold no model reference; stream order protects their reuse
     m->pool.push_back(c);
   }
