@@ -96,22 +96,6 @@ def test_params_errors_are_named():
     assert e.value.name == "NMT_ERR_IO"
 
 
-def test_scorebatch_forest_levels_fig1():
-    """The product's forest grouping (host driver) reproduces the paper's Fig. 1 step structure."""
-    import os
-    from paper_1605_04809_b200 import scorebatch
-    gold = os.path.join(os.path.dirname(__file__), "golden", "fig1_forest.txt")
-    hyps = {}
-    for ln in open(gold):
-        if ln.startswith("hyp"):
-            h, rest = ln[4:].split(":")
-            hyps[int(h)] = [tuple(int(w[1:]) for w in ph.split()) for ph in rest.split("|")]
-    pairs = [(h, t) for h in sorted(hyps) for t in hyps[h]]
-    lv = scorebatch.forest_levels(pairs)
-    assert [len(l) for l in lv] == [4, 5, 3, 1]
-    assert [w for _, w in lv[0]] == [0, 1, 1, 2] and [src[0] for src, _ in lv[0]] == [0, 0, 1, 1]
-
-
 def test_params_average_validates_before_device_work():
     """nmt_params_average: headers must match; errors are named, no GPU needed."""
     from paper_1605_04809_b200 import nmt

@@ -29,36 +29,18 @@ def _fig1():
     return [(h, t) for h in sorted(hyps) for t in hyps[h]], info
 
 
-@pytest.mark.parametrize("prec", ["fp32class", "bf16"])
-def test_fig1_through_the_gpu_driver(prec):
-    from paper_1605_04809_b200 import nmt, scorebatch
-    pairs, info = _fig1()
-    d = synth.Dims(8, 16, 50, 50, "tanh")
-    p = synth.make_model(d, 21)
-    M = nmt.Model(synth.params_bytes(d, p), precision=prec)
-    src = synth.make_source(d.vocab_src, 5, seed=6)
-    ctx = M.encode(src)
-    rng = np.random.default_rng(1)
-    s = np.tanh(rng.standard_normal((2, d.dim_hid))).astype(np.float32)
-    hyps = ctx.inject_states(s, [4, 9])
-    out, st = scorebatch.score_batch(ctx, hyps, pairs)
-    assert st.steps == int(info["steps"][0])
-    assert st.edges_per_depth == [int(x) for x in info["edges_per_depth"]]
-    assert st.rows_per_depth == [int(x) for x in info["parent_rows_per_depth"]]
-    assert st.naive_words == int(info["naive_words"][0])
-    sess = O.Session(O.Model(d, p), src)
-    oh = [sess.inject_state(s[i], y) for i, y in enumerate([4, 9])]
-    ref = O.score_forest(sess, oh, pairs)
-    for k, (lp, _) in out.items():
-        assert abs(lp - ref[k]) < TOL[prec] * len(k[1])
+def _forest_args(pairs):
+    off = np.cumsum([0] + [len(t) for _, t in pairs]).astype(np.int32)
+    words = np.array([w for _, t in pairs for w in t], np.int32)
+    return off, words
 
 
 @pytest.mark.parametrize("prec", ["fp32class", "bf16"])
 def test_stack_batch_dedup_tiny(prec):
-    """C3-style stack: distinct (h, t) expansions over zipf parents, phrase lengths 1..5,
-    branching shrinking with depth.  Ids and scores must match the oracle; the
+    """C3-style stack through nmt_score_forest: distinct (h, t) expansions over zipf parents, phrase
+    lengths 1..5, branching shrinking with depth.  Scores must match the oracle; the
     number of stepped rows is bounded by the edges, and a re-scored stack steps nothing."""
-    from paper_1605_04809_b200 import nmt, scorebatch
+    from paper_1605_04809_b200 import nmt
     d = synth.Dims(8, 16, 50, 50, "maxout")
     p = synth.make_model(d, 1605)
     M = nmt.Model(synth.params_bytes(d, p), precision=prec)
@@ -70,16 +52,18 @@ def test_stack_batch_dedup_tiny(prec):
     gh = ctx.inject_states(s, y)
     oh = [sess.inject_state(s[i], int(y[i])) for i in range(H)]
     pairs = synth.make_stack_expansions(120, H, d.vocab_tgt, seed=1608)
-    out, st = scorebatch.score_batch(ctx, gh, pairs)
+    off, words = _forest_args(pairs)
+    lp, fin, st = ctx.score_forest([gh[h] for h, _ in pairs], off, words)
     ref = O.score_forest(sess, oh, pairs)
-    worst = max(abs(out[k][0] - ref[k]) / len(k[1]) for k in out)
+    worst = max(abs(lp[i] - ref[k]) / len(k[1]) for i, k in enumerate(pairs))
     assert worst < TOL[prec]
-    assert sum(st.rows_per_depth) <= sum(st.edges_per_depth) <= st.naive_words
-    assert st.steps == max(len(t) for _, t in pairs)
+    assert sum(st["rows_per_depth"]) <= sum(st["edges_per_depth"]) <= len(words)
+    assert st["steps"] == max(len(t) for _, t in pairs)
+    assert st["rows_per_depth"] == sess.rows_per_step
     n0 = ctx.stats()
-    out2, st2 = scorebatch.score_batch(ctx, gh, pairs)  # cache: no new rows, identical values
-    assert ctx.stats() == n0 and sum(st2.rows_per_depth) == 0
-    assert all(out2[k] == out[k] for k in out)
+    lp2, fin2, st2 = ctx.score_forest([gh[h] for h, _ in pairs], off, words)  # cache: no new rows
+    assert ctx.stats() == n0 and sum(st2["rows_per_depth"]) == 0
+    assert np.array_equal(lp, lp2) and np.array_equal(fin, fin2)
 
 
 def test_ensemble_single_rank_nccl():
@@ -103,10 +87,12 @@ def test_ensemble_single_rank_nccl():
 
 
 @pytest.mark.parametrize("prec", ["fp32class", "bf16"])
-def test_native_score_forest_matches_oracle_and_driver(prec):
-    """nmt_score_forest (native ScoreBatch) == oracle per-pair sums; Fig. 1 step structure; a second
-    call on the same pairs is served from the state cache (no new rows, identical results)."""
-    from paper_1605_04809_b200 import nmt, scorebatch
+def test_native_score_forest_matches_oracle_fig1(prec):
+    """nmt_score_forest (native ScoreBatch) == oracle per-pair sums on the Fig. 1 worked example
+    (tests/golden/fig1_forest.txt); Fig. 1 step structure (steps, edges per depth, parent rows per
+    depth); a second call on the same pairs is served from the state cache (no new rows, identical
+    results)."""
+    from paper_1605_04809_b200 import nmt
     d = synth.Dims(8, 16, 50, 50, "tanh")
     p = synth.make_model(d, 21)
     M = nmt.Model(synth.params_bytes(d, p), precision=prec)
@@ -120,7 +106,9 @@ def test_native_score_forest_matches_oracle_and_driver(prec):
     ctx = M.encode(src)
     hyps = ctx.inject_states(s, [4, 9])
     lp, stt, st = ctx.score_forest([hyps[h] for h in hs_idx], off, words)
-    assert st["steps"] == 4 and st["edges_per_depth"] == [4, 5, 3, 1] and st["rows_per_depth"] == [2, 3, 3, 1]
+    assert st["steps"] == int(info["steps"][0])
+    assert st["edges_per_depth"] == [int(x) for x in info["edges_per_depth"]]
+    assert st["rows_per_depth"] == [int(x) for x in info["parent_rows_per_depth"]]
     sess = O.Session(O.Model(d, p), src)
     oh = [sess.inject_state(s[i], y) for i, y in enumerate([4, 9])]
     ref = O.score_forest(sess, oh, pairs)
@@ -128,12 +116,6 @@ def test_native_score_forest_matches_oracle_and_driver(prec):
         assert abs(lp[i] - ref[k]) < TOL[prec] * len(k[1])
     lp2, st2, s2 = ctx.score_forest([hyps[h] for h in hs_idx], off, words)
     assert s2["rows_per_depth"] == [0, 0, 0, 0] and np.array_equal(lp, lp2) and np.array_equal(stt, st2)
-    # the python driver on a fresh context gives the same numbers
-    ctx2 = M.encode(src)
-    hyps2 = ctx2.inject_states(s, [4, 9])
-    out, _ = scorebatch.score_batch(ctx2, hyps2, pairs)
-    for i, k in enumerate(pairs):
-        assert abs(out[k][0] - lp[i]) < 1e-5
     with pytest.raises(nmt.NmtError) as e:
         ctx.score_forest([hyps[0]], [0, 0], np.zeros(0, np.int32))
     assert "empty expansion" in str(e.value)

@@ -127,6 +127,123 @@ def test_gru_closed_form_zero_matrices():
     assert np.max(np.abs(h2 - (u2 * h1 + (1 - u2) * np.tanh(r2 * bx)))) < 1e-15
 
 
+# ------------------------------------------------------------------ cGRU composition (closed forms)
+# The conditional GRU of DL4MT (reading A4) is defined by WHERE s1 goes: the
+# attention query and the GRU2 state both come from s1, the output of GRU1, not from the input
+# state s.  With GRU1's matrices zero, s1 is known in closed form (u weights the old state, A2):
+#   s1 = u1*s + (1-u1)*tanh(bx),  u1 = sigm(b_u)
+# and it can be made to have the opposite sign of s on a chosen coordinate.  These tests fail if the
+# query or the GRU2 state is taken from s (tools/mutate_oracle.py checks exactly that).
+def _cgru_probe_model(H=16, E=8, V=50):
+    d = synth.Dims(E, H, 50, V, "tanh")
+    p = synth.make_model(d, 31)
+    for k in ("decoder_W", "decoder_U", "decoder_Wx", "decoder_Ux"):
+        p[k] = np.zeros_like(p[k])
+    return d, p
+
+
+def _s1_closed_form(p, s, H):
+    b = p["decoder_b"].astype(np.float64).reshape(-1)
+    bx = p["decoder_bx"].astype(np.float64).reshape(-1)
+    u1 = 1.0 / (1.0 + np.exp(-b[H:]))
+    return u1 * s + (1.0 - u1) * np.tanh(bx)
+
+
+def test_attention_query_comes_from_gru1_output():
+    d, p = _cgru_probe_model()
+    H, C, k, col, Tx, jstar = d.dim_hid, d.ctx_dim, 3, 5, 6, 2
+    p["decoder_b"] = p["decoder_b"].copy()
+    p["decoder_b"][0, H + k] = -30.0            # u1[k] ~ 0: s1[k] = tanh(bx[k])
+    p["decoder_bx"] = p["decoder_bx"].copy()
+    p["decoder_bx"][0, k] = 2.0                  # s1[k] = tanh(2) > 0
+    W = np.zeros((H, C), np.float32)
+    W[k, col] = 40.0                             # q[col] = 40 s1[k]: one-hot route of coordinate k
+    p["decoder_W_comb_att"] = W
+    ua = np.zeros((C, 1), np.float32)
+    ua[col, 0] = 8.0
+    p["decoder_U_att"] = ua
+    m = O.Model(d, p)
+    rng = np.random.default_rng(12)
+    ctx = rng.standard_normal((Tx, C))
+    pctx = np.full((Tx, C), -40.0)
+    pctx[jstar, :] = 0.0                         # position j* lights up only for a POSITIVE query
+    c = O.Context(ctx=ctx, pctx=pctx, s0=np.zeros(H))
+    s = np.zeros((1, H))
+    s[0, k] = -0.9                               # the input state has the opposite sign
+    out = O.step(m, c, s, [O.BOS])
+    s1 = _s1_closed_form(m.p, s[0], H)
+    assert s1[k] > 0.9 and s[0, k] < 0
+    # by hand: a_j = 8 tanh(pctx[j, col] + 40 s1[k]) + c_tt, alpha = softmax_j(a)
+    a = 8.0 * np.tanh(pctx[:, col] + 40.0 * s1[k])
+    alpha = np.exp(a - a.max())
+    alpha /= alpha.sum()
+    assert np.max(np.abs(out["s1"][0] - s1)) < 1e-15
+    assert np.max(np.abs(out["alpha"][0] - alpha)) < 1e-12
+    assert out["alpha"][0, jstar] > 0.99         # (a query from s would give uniform attention)
+    assert np.max(np.abs(out["c"][0] - alpha @ ctx)) < 1e-12
+
+
+def test_gru2_state_is_gru1_output():
+    d, p = _cgru_probe_model()
+    H = d.dim_hid
+    for k in ("decoder_U_nl", "decoder_Wc", "decoder_Ux_nl", "decoder_Wcx"):
+        p[k] = np.zeros_like(p[k])
+    p["decoder_b"] = p["decoder_b"].copy()
+    p["decoder_b"][0, H:] = -30.0                # u1 ~ 0: s1 = tanh(bx), independent of s
+    p["decoder_bx"] = np.full((1, H), 1.5, np.float32)
+    p["decoder_b_nl"] = np.zeros((1, 2 * H), np.float32)   # r2 = u2 = 1/2
+    m = O.Model(d, p)
+    c = O.encode(m, synth.make_source(d.vocab_src, 5, seed=3))
+    s = -np.tanh(np.abs(np.random.default_rng(4).standard_normal((2, H))))   # s < 0 everywhere
+    out = O.step(m, c, s, [7, O.BOS])
+    s1 = np.stack([_s1_closed_form(m.p, s[r], H) for r in range(2)])
+    bx_nl = m.p["decoder_bx_nl"]
+    s2 = 0.5 * s1 + 0.5 * np.tanh(0.5 * bx_nl)   # GRU2 with zero matrices: state s1, bx_nl inside r2
+    assert np.max(np.abs(out["s2"] - s2)) < 1e-15
+    assert np.min(s1) > 0.9                      # (a GRU2 state s < 0 would differ by >= 0.45)
+
+
+def test_encoder_closed_form_and_pctx_orientation():
+    """Zero encoder matrices: fwd_j = (1 - u_f^(j+1)) tanh(bx_f), bwd_j = (1 - u_b^(Tx-j)) tanh(bx_b)
+    (GRU closed form, h_{-1} = h_{Tx} = 0).  pctx = ctx Wc_att + b_att with a NON-symmetric
+    permutation Wc_att (pctx[:, pi(i)] = ctx[:, i]) pins the orientation of the product."""
+    d = synth.Dims(8, 16, 50, 50, "tanh")
+    p = synth.make_model(d, 41)
+    H, C = d.dim_hid, d.ctx_dim
+    for pre in ("encoder", "encoder_r"):
+        for s in ("W", "U", "Wx", "Ux"):
+            p[f"{pre}_{s}"] = np.zeros_like(p[f"{pre}_{s}"])
+    pi = np.random.default_rng(5).permutation(C)
+    P = np.zeros((C, C), np.float32)
+    P[np.arange(C), pi] = 1.0
+    assert not np.array_equal(P, P.T)
+    p["decoder_Wc_att"] = P
+    p["decoder_b_att"] = np.zeros((1, C), np.float32)
+    m = O.Model(d, p)
+    src = synth.make_source(d.vocab_src, 6, seed=9)
+    Tx = len(src)
+    c = O.encode(m, src)
+    sg = lambda x: 1.0 / (1.0 + np.exp(-x))
+    bf, bb = m.p["encoder_b"], m.p["encoder_r_b"]
+    for j in range(Tx):
+        fwd = (1 - sg(bf[H:]) ** (j + 1)) * np.tanh(m.p["encoder_bx"])
+        bwd = (1 - sg(bb[H:]) ** (Tx - j)) * np.tanh(m.p["encoder_r_bx"])
+        assert np.max(np.abs(c.ctx[j, :H] - fwd)) < 1e-14
+        assert np.max(np.abs(c.ctx[j, H:] - bwd)) < 1e-14
+    assert np.array_equal(c.pctx[:, pi], c.ctx)
+
+
+def test_ensemble_weighted_combine_hand_values():
+    """PAPER.md:92 (models as separately WEIGHTED features), reading A16, with unequal weights."""
+    L1 = np.log([0.5, 0.25, 0.25])
+    L2 = np.log([0.25, 0.25, 0.5])
+    ln2 = math.log(2.0)
+    got0 = O.ensemble_combine([L1, L2], [0.75, 0.25], 0)
+    assert np.max(np.abs(got0 - np.array([-1.25 * ln2, -2 * ln2, -1.75 * ln2]))) < 1e-15
+    got1 = O.ensemble_combine([L1, L2], [0.75, 0.25], 1)
+    assert np.max(np.abs(got1 - np.log([0.4375, 0.25, 0.3125]))) < 1e-15
+
+
 # ------------------------------------------------------------------ whole model / attention closed forms
 def test_zero_model_uniform():
     d = TINY

@@ -45,7 +45,7 @@ def peaks():
 
 def c3(a):
     import torch
-    from paper_1605_04809_b200 import nmt, scorebatch
+    from paper_1605_04809_b200 import nmt
     d = synth.Dims(500, 1024, 100000, 50000, a.readout)
     M = nmt.Model(synth.params_bytes(d, synth.make_model(d, 1605)), precision=a.precision)
     rng = np.random.default_rng(1605)
