@@ -7,19 +7,27 @@ inject R = 1024 synthetic parent states, and score R x 3 candidate words (3072 w
 nmt_score_batch (device planner -> GRU1 -> attention -> GRU2 -> readout -> vocab GEMM + fused
 log-softmax -> gather).  `value` times the device-resident C-ABI path (nmt_*_dev, inputs already in
 HBM); `e2e` times the host API (pinned host inputs copied in, results copied out) every step.
+Variants in the same line (`variants`): the primary C2 with 1 candidate per row, and the FP32CLASS
+precision (bf16x3, bound 1e-3), each with its own in-run parity against the float64 oracle.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-  N > 1: torchrun, one rank per GPU, sentences sharded (weak scaling, no collective on the data path).
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--ensemble M]
+  N > 1: one rank per GPU.  Without torchrun in the environment (WORLD_SIZE unset) bench.py starts
+  torchrun itself.  Sentences are sharded over ranks (weak scaling, no collective on the data path).
+  --ensemble M: C4, an M-member ensemble (seeds 2016..) whose per-word log-probs are combined to rank 0
+  of each member group (one member per GPU over NCCL when N >= M, groups of M ranks; all M members on
+  the one GPU over the in-process communicator when N == 1).
 """
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import statistics
 import subprocess
 import sys
 import tempfile
+import threading
 import time
 
 import numpy as np
@@ -45,8 +53,10 @@ def parse_args(argv=None):
     ap.add_argument("--rows", type=int, default=1024)
     ap.add_argument("--cands", type=int, default=3)
     ap.add_argument("--src-len", type=int, default=50)
+    ap.add_argument("--ensemble", type=int, default=0, help="C4: number of ensemble members (0: single model)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--stages", action="store_true", help="add a per-stage CUDA-event breakdown (untimed pass)")
     return ap.parse_args(argv)
 
@@ -56,12 +66,21 @@ def model_dims(readout: str) -> synth.Dims:
 
 
 def workload_config(a, n_gpus: int) -> dict:
-    return {"workload": f"C2 En->Ru: encode 1 source (Tx={a.src_len}) + score {a.rows} injected parents x "
-                        f"{a.cands} candidate words per step",
-            "dim_emb": 500, "dim_hid": 1024, "vocab_tgt": 100000, "src_len": a.src_len, "rows": a.rows,
-            "cands_per_row": a.cands, "precision": a.precision, "readout": a.readout,
-            "l2": "flushed before every timed step (256 MiB write)",
-            "parallelism": f"{n_gpus} GPU(s), sentence sharding, no collective on the data path"}
+    c = {"workload": f"C2 En->Ru: encode 1 source (Tx={a.src_len}) + score {a.rows} injected parents x "
+                     f"{a.cands} candidate words per step",
+         "dim_emb": 500, "dim_hid": 1024, "vocab_tgt": 100000, "src_len": a.src_len, "rows": a.rows,
+         "cands_per_row": a.cands, "precision": a.precision, "readout": a.readout,
+         "l2": "flushed before every timed step (256 MiB write)",
+         "parallelism": f"{n_gpus} GPU(s), sentence sharding, no collective on the data path"}
+    if a.ensemble:
+        c["workload"] = (f"C4 En->Ru ensemble of {a.ensemble} members: per member encode 1 source (Tx={a.src_len}) "
+                         f"+ score {a.rows} parents x {a.cands} words, combined log-probs (mode 0, lambda = 1/M)")
+        c["members"] = a.ensemble
+        c["l2"] = "not flushed: each step reads the weights of all members (> 4 x 0.3 GB), larger than L2"
+        c["parallelism"] = (f"{n_gpus} GPU(s): " + ("one member per GPU, NCCL all-gather + combine on the group's "
+                                                    "rank 0" if n_gpus >= a.ensemble else
+                                                    f"all {a.ensemble} members on one GPU (in-process communicator)"))
+    return c
 
 
 def shard_seed(rank: int, step: int) -> int:
@@ -90,6 +109,20 @@ def reduce_sum(value: float, dist) -> float:
     return float(t.item())
 
 
+def step_flops(rows: int, src_len: int, d: synth.Dims) -> dict:
+    """Algorithmic dense work of one bench step (multiply-add = 2 flops), SURVEY §8(a)/(d):
+    per decoder row: GRU1 s.[U|Ux] 2*H*3H, query s1.W_comb_att 2*H*2H, attention energies + context
+    4*Tx*2H, GRU2 2*(H+2H)*2H + 2*H*H + 2*2H*H, readout 2*(2H+H)*RO (RO = 2E maxout, E tanh), vocabulary
+    2*E*V; per source token: input projections 2*E*3H*2, recurrence 2*H*3H*2, keys pctx 2*2H*2H; per
+    sentence s0 2*2H*H.  (The embedding projections the library precomputes at load are counted.)"""
+    E, H, V = d.dim_emb, d.dim_hid, d.vocab_tgt
+    RO = 2 * E if d.readout == "maxout" else E
+    row = (2 * H * 3 * H + 2 * H * 2 * H + 4 * src_len * 2 * H + 2 * 3 * H * 2 * H + 2 * H * H + 2 * 2 * H * H
+           + 2 * 3 * H * RO + 2 * E * V + 2 * E * 3 * H + 2 * E * RO)
+    enc = src_len * (2 * E * 3 * H * 2 + 2 * H * 3 * H * 2 + 2 * 2 * H * 2 * H) + 2 * 2 * H * H
+    return {"per_row": row, "encoder": enc, "per_step": rows * row + enc}
+
+
 # ------------------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi clocks/throttle sampling DURING the timed region (B200_PROFILING.md recipe)."""
@@ -106,7 +139,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -159,12 +192,13 @@ def cpu_threads() -> int:
     return len(os.sched_getaffinity(0))
 
 
-def oracle_sample(om, d, a, rows: int, seed: int) -> tuple:
+def oracle_sample(om, d, a, rows: int, seed: int, cands: int | None = None) -> tuple:
     """One bounded sample of the step on the host: encode 1 source + `rows` parents x cands."""
     import oracle as O
+    cands = a.cands if cands is None else cands
     src = synth.make_source(d.vocab_src, a.src_len - 1, seed=seed)
     s, y = synth.make_states(rows, d.dim_hid, d.vocab_tgt, seed=seed + 1)
-    off, words = synth.make_candidates(rows, a.cands, d.vocab_tgt, seed=seed + 2)
+    off, words = synth.make_candidates(rows, cands, d.vocab_tgt, seed=seed + 2)
     t0 = time.perf_counter()
     sess = O.Session(om, src)
     ids = [sess.inject_state(s[i], int(y[i])) for i in range(rows)]
@@ -172,7 +206,7 @@ def oracle_sample(om, d, a, rows: int, seed: int) -> tuple:
     dt = time.perf_counter() - t0
     assert np.all(np.isfinite(lp))
     oracle_sample.last = (src, s, y, off, words, lp, am, sess, ids)  # (inputs and results, for the parity check)
-    return dt, rows * a.cands
+    return dt, rows * cands
 
 
 def run_reference(a, rank: int, world: int) -> None:
@@ -180,6 +214,11 @@ def run_reference(a, rank: int, world: int) -> None:
     if rank != 0:
         return
     import oracle as O
+    try:  # the box's host cores (torchrun sets OMP_NUM_THREADS=1 per rank)
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(len(os.sched_getaffinity(0)))
+    except Exception:
+        pass
     d = model_dims(a.readout)
     om = O.Model(d, synth.make_model(d, 2016))
     rows = 96  # per step: 1 encode + 96 parents x cands (~1 s of CPU work)
@@ -201,6 +240,32 @@ def run_reference(a, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def parity_vs_oracle(M, om, d, a, rows: int, seeds, cands: int, tol: float) -> tuple:
+    """(oracle seconds, word-scores, parity dict): oracle samples through the host C ABI and the oracle."""
+    t, n = 0.0, 0
+    worst, cnt, top_same, top_rows, top_tie_ok = 0.0, 0, 0, 0, True
+    for sd in seeds:
+        dt, m = oracle_sample(om, d, a, rows, seed=sd, cands=cands)
+        t += dt
+        n += m
+        src, s, y, off, words, ref, ref_am, sess, oids = oracle_sample.last
+        ctx = M.encode(src)
+        lp, _, am = ctx.score_batch(ctx.inject_states(s, y), off, words)
+        ctx.close()
+        worst = max(worst, float(np.max(np.abs(lp.astype(np.float64) - ref))))
+        cnt += len(lp)
+        same = am == ref_am
+        top_same += int(same.sum())
+        top_rows += len(am)
+        for i in np.nonzero(~same)[0]:  # a different top-1 must lie in the oracle's tie set (A21)
+            row = sess.logprobs_full(oids[i])
+            top_tie_ok = top_tie_ok and bool(row[am[i]] >= row.max() - 2 * tol)
+    par = {"max_abs_dlogp": worst, "tol": tol, "ok": worst < tol and top_tie_ok, "word_scores": cnt,
+           "top1_identical": f"{top_same}/{top_rows}", "top1_in_oracle_tie_set": top_tie_ok,
+           "vs": "float64 oracle, same inputs through the host C ABI"}
+    return t, n, par
+
+
 def cpu_baseline(a, M=None) -> tuple:
     """(cpu_baseline dict, parity dict or None): the oracle timed on two full steps of the workload;
     the same two steps through the GPU path (host C ABI) give the run's own max |dlogp|."""
@@ -208,36 +273,19 @@ def cpu_baseline(a, M=None) -> tuple:
     d = model_dims(a.readout)
     om = O.Model(d, synth.make_model(d, 2016))
     oracle_sample(om, d, a, 16, seed=7)  # warm BLAS
-    rows = a.rows
-    t, n = 0.0, 0
-    worst, cnt, top_same, top_rows, top_tie_ok = 0.0, 0, 0, 0, True
     tol = 2e-2 if a.precision == "bf16" else 1e-3
-    for k in range(2):
-        dt, m = oracle_sample(om, d, a, rows, seed=shard_seed(0, 5000 + k))
-        t += dt
-        n += m
-        if M is not None:  # (untimed) the same inputs through the CUDA path
-            src, s, y, off, words, ref, ref_am, sess, oids = oracle_sample.last
-            ctx = M.encode(src)
-            lp, _, am = ctx.score_batch(ctx.inject_states(s, y), off, words)
-            ctx.close()
-            worst = max(worst, float(np.max(np.abs(lp.astype(np.float64) - ref))))
-            cnt += len(lp)
-            same = am == ref_am
-            top_same += int(same.sum())
-            top_rows += len(am)
-            for i in np.nonzero(~same)[0]:  # a different top-1 must lie in the oracle's tie set (A21)
-                row = sess.logprobs_full(oids[i])
-                top_tie_ok = top_tie_ok and bool(row[am[i]] >= row.max() - 2 * tol)
+    if M is None:
+        t, n = 0.0, 0
+        for k in range(2):
+            dt, m = oracle_sample(om, d, a, a.rows, seed=shard_seed(0, 5000 + k))
+            t, n = t + dt, n + m
+        par = None
+    else:
+        t, n, par = parity_vs_oracle(M, om, d, a, a.rows, [shard_seed(0, 5000 + k) for k in range(2)], a.cands, tol)
     base = {"value": n / t, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
-            "sample": f"2 full steps of the workload (encode Tx={a.src_len} + {rows} parents x {a.cands} words), "
+            "sample": f"2 full steps of the workload (encode Tx={a.src_len} + {a.rows} parents x {a.cands} words), "
                       f"float64 numpy oracle, {t:.1f} s"}
-    par = None
-    if M is not None:
-        par = {"max_abs_dlogp": worst, "tol": tol, "ok": worst < tol and top_tie_ok, "word_scores": cnt,
-               "top1_identical": f"{top_same}/{top_rows}", "top1_in_oracle_tie_set": top_tie_ok,
-               "vs": "float64 oracle on the cpu_baseline sample (same inputs), host C ABI"}
-    return base, par
+    return base, par, om
 
 
 # ------------------------------------------------------------------------------------- GPU arm
@@ -246,62 +294,71 @@ def measured_peaks() -> dict:
     if os.path.exists(p):
         with open(p) as f:
             j = json.load(f)
-        return {"bf16_tflops": j.get("bf16_tflops"), "hbm_gbs": j.get("hbm_gbs"), "source": "measured"}
-    return {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+        return {"bf16_tflops": j.get("bf16_tflops"), "bf16_tflops_sustained": j.get("bf16_tflops_sustained"),
+                "hbm_gbs": j.get("hbm_gbs"), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": None, "hbm_gbs": 6650.0,
+            "source": "fallback (B200_PROFILING.md)"}
 
 
-def ncu_traffic() -> float | None:
-    p = os.path.join(ROOT, "profiles", "vocab_gemm_ncu.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            j = json.load(f)
-        return j.get("dram_bytes_per_launch")
-    return None
+def ncu_traffic() -> tuple:
+    """dram read + write bytes per launch of the vocab GEMM from the committed `ncu --set full` summary
+    (ncu cannot run inside the timed bench; the file names the capture)."""
+    for p in (os.path.join(ROOT, "profiles", "r02", "vocab_ncu.json"), os.path.join(ROOT, "profiles", "vocab_gemm_ncu.json")):
+        if os.path.exists(p):
+            with open(p) as f:
+                j = json.load(f)
+            return j.get("dram_bytes_per_launch"), os.path.relpath(p, ROOT)
+    return None, None
 
 
-def run_ours(a, rank: int, world: int, dist) -> None:
-    import torch
-    from paper_1605_04809_b200 import nmt
-
-    dev = int(os.environ.get("LOCAL_RANK", 0))
-    torch.cuda.set_device(dev)
-    stream = torch.cuda.Stream(device=dev)
-    torch.cuda.set_stream(stream)
-    d = model_dims(a.readout)
-    params = synth.params_bytes(d, synth.make_model(d, 2016))
-    M = nmt.Model(params, precision=a.precision, device=dev, max_src_len=64, stream=stream.cuda_stream)
-    del params
-    R, Cn, Tx = a.rows, a.cands, a.src_len
+class Workload:
+    """Seeded device-resident inputs of a rank's shard (NSETS batches) and the timed step."""
     NSETS = 4
-    # device-resident inputs (value leg): NSETS seeded batches of this rank's shard
-    srcs, states, ys, words = [], [], [], []
-    for i in range(NSETS):
-        sd = shard_seed(rank, i)
-        srcs.append(synth.make_source(d.vocab_src, Tx - 1, seed=sd))
-        s, y = synth.make_states(R, d.dim_hid, d.vocab_tgt, seed=sd + 1)
-        off, w = synth.make_candidates(R, Cn, d.vocab_tgt, seed=sd + 2)
-        states.append(s)
-        ys.append(y)
-        words.append(w)
-    dsrc = [torch.from_numpy(x).cuda() for x in srcs]
-    dstates = [torch.from_numpy(x).cuda() for x in states]
-    dy = [torch.from_numpy(x).cuda() for x in ys]
-    dwords = [torch.from_numpy(x).cuda() for x in words]
-    doff = torch.from_numpy(off).cuda()
-    ids = torch.empty(R, dtype=torch.int32, device="cuda")
-    logp = torch.empty(R * Cn, dtype=torch.float32, device="cuda")
-    child = torch.empty(R * Cn, dtype=torch.int32, device="cuda")
-    amax = torch.empty(R, dtype=torch.int32, device="cuda")
-    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
 
-    def step_dev(i: int) -> None:
-        j = i % NSETS
-        ctx = M.encode_dev(dsrc[j].data_ptr(), Tx)
-        ctx.inject_states_dev(R, dstates[j].data_ptr(), dy[j].data_ptr(), ids.data_ptr())
-        ctx.score_batch_dev(R, ids.data_ptr(), doff.data_ptr(), R * Cn, dwords[j].data_ptr(), logp.data_ptr(),
-                            child.data_ptr(), amax.data_ptr())
+    def __init__(self, M, d, a, rank, cands, torch):
+        self.M, self.d, self.R, self.Cn, self.Tx = M, d, a.rows, cands, a.src_len
+        self.srcs, self.states, self.ys, self.words, self.off = [], [], [], [], None
+        for i in range(self.NSETS):
+            sd = shard_seed(rank, i)
+            self.srcs.append(synth.make_source(d.vocab_src, self.Tx - 1, seed=sd))
+            s, y = synth.make_states(self.R, d.dim_hid, d.vocab_tgt, seed=sd + 1)
+            off, w = synth.make_candidates(self.R, cands, d.vocab_tgt, seed=sd + 2)
+            self.states.append(s)
+            self.ys.append(y)
+            self.words.append(w)
+            self.off = off
+        cu = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        self.dsrc = [cu(x) for x in self.srcs]
+        self.dstates = [cu(x) for x in self.states]
+        self.dy = [cu(x) for x in self.ys]
+        self.dwords = [cu(x) for x in self.words]
+        self.doff = cu(self.off)
+        R, nc = self.R, self.R * cands
+        self.ids = torch.empty(R, dtype=torch.int32, device="cuda")
+        self.logp = torch.empty(nc, dtype=torch.float32, device="cuda")
+        self.child = torch.empty(nc, dtype=torch.int32, device="cuda")
+        self.amax = torch.empty(R, dtype=torch.int32, device="cuda")
+
+    def step_dev(self, i: int) -> None:
+        j = i % self.NSETS
+        ctx = self.M.encode_dev(self.dsrc[j].data_ptr(), self.Tx)
+        ctx.inject_states_dev(self.R, self.dstates[j].data_ptr(), self.dy[j].data_ptr(), self.ids.data_ptr())
+        ctx.score_batch_dev(self.R, self.ids.data_ptr(), self.doff.data_ptr(), self.R * self.Cn,
+                            self.dwords[j].data_ptr(), self.logp.data_ptr(), self.child.data_ptr(),
+                            self.amax.data_ptr())
         ctx.close()
 
+    def step_host(self, j: int, pinned) -> tuple:
+        ctx = self.M.encode(pinned["src"][j])
+        pids = ctx.inject_states(pinned["s"][j], pinned["y"][j])
+        out = ctx.score_batch(pids, pinned["off"], pinned["w"][j])
+        ctx.close()
+        return out
+
+
+def timed_dev(wl, a, stream, flush, dist, torch, nmt):
+    """W warm-up steps, then K steps bracketed by barrier + synchronize, per-step CUDA events on the
+    model stream with an L2 flush (outside the events) before each step."""
     def barrier():
         torch.cuda.synchronize()
         if dist is not None:
@@ -309,109 +366,353 @@ def run_ours(a, rank: int, world: int, dist) -> None:
         torch.cuda.synchronize()
 
     for i in range(a.warmup):
-        step_dev(i)
+        wl.step_dev(i)
     torch.cuda.synchronize()
-    assert torch.isfinite(logp).all().item(), "non-finite log-probs"
-    # ---------------- timed region (value): per-step CUDA events on the model stream, L2 flushed between steps
-    M.profile(1)
-    M.profile_read()
+    assert torch.isfinite(wl.logp).all().item(), "non-finite log-probs"
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     barrier()
     n0 = nmt.launch_count()
-    with ClockSampler(dev) as clk:
-        for i in range(a.steps):
-            flush.zero_()
-            ev[i][0].record(stream)
-            step_dev(i)
-            ev[i][1].record(stream)
-        barrier()
+    for i in range(a.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        wl.step_dev(i)
+        ev[i][1].record(stream)
+    barrier()
     launches = nmt.launch_count() - n0
+    t_local = sum(e0.elapsed_time(e1) for e0, e1 in ev) / 1000.0
+    return t_local, launches
+
+
+def run_ours(a, rank: int, world: int, dist) -> None:
+    import torch
+    from paper_1605_04809_b200 import nmt
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    if dev >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{dev} but only {torch.cuda.device_count()} GPU(s) exist")
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    d = model_dims(a.readout)
+    params = synth.params_bytes(d, synth.make_model(d, 2016))
+    M = nmt.Model(params, precision=a.precision, device=dev, max_src_len=64, stream=stream.cuda_stream)
+    R, Cn, Tx = a.rows, a.cands, a.src_len
+    wl = Workload(M, d, a, rank, Cn, torch)
+    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
+    # ---------------- timed region (value): per-step CUDA events on the model stream, L2 flushed between steps
+    M.profile(1)
+    M.profile_read()
+    with ClockSampler(dev) as clk:
+        t_local, launches = timed_dev(wl, a, stream, flush, dist, torch, nmt)
     stage_ms, stage_cnt = M.profile_read()
     M.profile(0)
-    t_local = sum(e0.elapsed_time(e1) for e0, e1 in ev) / 1000.0
+    last_set = (a.steps - 1) % Workload.NSETS
+    dev_logp = wl.logp.cpu().numpy().copy()  # the last timed step's output (compared with the host path below)
     t_max = reduce_max(t_local, dist)
     total_scores = reduce_sum(float(R * Cn * a.steps), dist)
     value = total_scores / t_max
     clocks = clk.summary()
     # roofline of the dominant kernel (vocabulary GEMM + fused log-sum-exp), live from the timed region
-    vocab_ms = stage_ms[nmt.STAGES.index("vocab_gemm_lse")] / max(1, stage_cnt[nmt.STAGES.index("vocab_gemm_lse")])
+    vi = nmt.STAGES.index("vocab_gemm_lse")
+    vocab_ms = stage_ms[vi] / max(1, stage_cnt[vi])
     flops = 2.0 * R * d.vocab_tgt * d.dim_emb
     achieved = flops / (vocab_ms / 1000.0) / 1e12
     peaks = measured_peaks()
+    traffic, traffic_src = ncu_traffic()
     roof = {"kernel": "k_gemm<256,6,EPI_LSE,pair> (CTA-pair vocab GEMM + online log-sum-exp)", "bound": "tensor",
             "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-            "frac": achieved / peaks["bf16_tflops"], "traffic": ncu_traffic(),
+            "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
+            "traffic_source": f"ncu --set full capture summarised in {traffic_src} (not measured in this run)",
             "peak_source": peaks["source"] + " bf16 burst", "algorithmic_flops_per_launch": flops,
             "avg_launch_ms": vocab_ms, "share_of_step": vocab_ms / (1000.0 * t_local / a.steps)}
+    sf = step_flops(R, Tx, d)
+    ms_step = 1000.0 * t_max / a.steps
+    step_roof = {"algorithmic_flops_per_step": sf["per_step"], "per_row": sf["per_row"], "encoder": sf["encoder"],
+                 "achieved_tflops": sf["per_step"] / (ms_step / 1000.0) / 1e12,
+                 "frac_of_bf16_peak": sf["per_step"] / (ms_step / 1000.0) / 1e12 / peaks["bf16_tflops"],
+                 "note": "whole step (encoder + decoder + vocabulary) against the dense bf16 burst peak"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": 1000.0 * t_max / a.steps, "higher_is_better": True,
+            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if a.precision == "bf16" else "bf16x3",
             "data": "synthetic (seeded random-init cGRU weights, Zipf ids, injected parent states)",
-            "config": workload_config(a, world), "roofline": roof, "gpu_launches": int(launches),
-            "gpu_launches_per_step": launches / a.steps, "clocks": clocks,
-            "rows_per_s": value / a.cands}  # unique decoder steps (rows) per second
+            "config": workload_config(a, world), "roofline": roof, "step_roofline": step_roof,
+            "gpu_launches": int(launches), "gpu_launches_per_step": launches / a.steps, "clocks": clocks,
+            "rows_per_s": value / Cn}  # unique decoder steps (rows) per second
+    if dist is not None:
+        line["comm"] = comm_info(dist, torch)
     # ---------------- optional per-stage breakdown (separate untimed pass)
     if a.stages:
         M.profile(2)
         M.profile_read()
         for i in range(10):
-            step_dev(i)
+            wl.step_dev(i)
         ms, cnt = M.profile_read()
         M.profile(0)
         line["stages_ms_per_step"] = {n: ms[k] / 10 for k, n in enumerate(nmt.STAGES) if cnt[k]}
     # ---------------- e2e: the host C-ABI (pinned host inputs in, results out, every step)
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+    pinned = {"src": [pin(x) for x in wl.srcs], "s": [pin(x) for x in wl.states], "y": [pin(x) for x in wl.ys],
+              "w": [pin(x) for x in wl.words], "off": pin(wl.off)}
+    host_lp = wl.step_host(last_set, pinned)[0]
+    line["dev_vs_host"] = {"bitwise_equal": bool(np.array_equal(dev_logp.view(np.uint32), host_lp.view(np.uint32))),
+                           "what": "log-probs of the last timed device step vs the host C ABI on the same inputs"}
     if not a.no_e2e:
-        pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
-        hsrc = [pin(x) for x in srcs]
-        hstates = [pin(x) for x in states]
-        hy = [pin(x) for x in ys]
-        hwords = [pin(x) for x in words]
-        hoff = pin(off)
-
-        def step_host(i: int) -> int:
-            j = i % NSETS
-            ctx = M.encode(hsrc[j])
-            pids = ctx.inject_states(hstates[j], hy[j])
-            lp, ch, am = ctx.score_batch(pids, hoff, hwords[j])
-            ctx.close()
-            return int(np.isfinite(lp).sum())
-
         for i in range(a.warmup):
-            step_host(i)
+            wl.step_host(i % Workload.NSETS, pinned)
         ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
-        barrier()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
         for i in range(a.steps):
             flush.zero_()
             ev2[i][0].record(stream)
-            step_host(i)
+            wl.step_host(i % Workload.NSETS, pinned)
             ev2[i][1].record(stream)
-        barrier()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
         t2 = reduce_max(sum(e0.elapsed_time(e1) for e0, e1 in ev2) / 1000.0, dist)
         h2d = Tx * 4 + R * d.dim_hid * 4 + R * 4 + R * 8 + (R + 1) * 4 + R * Cn * 4
         d2h = R * 8 + R * Cn * 4 + R * Cn * 8 + R * 4
         line["e2e"] = {"value": total_scores / t2, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h,
                        "path": "nmt_encode + nmt_inject_states + nmt_score_batch (host arrays, pinned)"}
+    om = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        line["cpu_baseline"], line["parity"] = cpu_baseline(a, M)
+        line["cpu_baseline"], line["parity"], om = cpu_baseline(a, M)
+    # ---------------- variants: primary C2 (1 candidate per row) and FP32CLASS, each with its own parity
+    if not a.no_variants:
+        line["variants"] = variants(a, M, params, d, rank, world, dist, stream, flush, torch, nmt, om)
+    M.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
 
 
+def variants(a, M, params, d, rank, world, dist, stream, flush, torch, nmt, om) -> dict:
+    import copy
+    out = {}
+    steps = max(3, min(a.steps, 10))
+    for name, prec, cands in (("c2_1cand_bf16", "bf16", 1), ("fp32class", "fp32class", a.cands)):
+        if prec == a.precision and cands == a.cands:
+            continue
+        va = copy.copy(a)
+        va.steps, va.warmup, va.cands, va.precision = steps, max(3, min(a.warmup, 5)), cands, prec
+        Mv = M if prec == a.precision else nmt.Model(params, precision=prec, device=torch.cuda.current_device(),
+                                                       max_src_len=64, stream=stream.cuda_stream)
+        wl = Workload(Mv, d, va, rank, cands, torch)
+        t_local, launches = timed_dev(wl, va, stream, flush, dist, torch, nmt)
+        t_max = reduce_max(t_local, dist)
+        v = reduce_sum(float(va.rows * cands * steps), dist) / t_max
+        r = {"value": v, "unit": UNIT, "rows_per_s": v / cands, "ms_per_step": 1000.0 * t_max / steps,
+             "steps": steps, "warmup": va.warmup, "precision": prec, "cands_per_row": cands,
+             "dtype": "bf16" if prec == "bf16" else "bf16x3"}
+        if om is not None and rank == 0:
+            tol = 2e-2 if prec == "bf16" else 1e-3
+            _, _, r["parity"] = parity_vs_oracle(Mv, om, d, va, 256, [shard_seed(0, 7000)], cands, tol)
+            r["parity"]["sample"] = "256 parents of one step"
+        out[name] = r
+        if Mv is not M:
+            Mv.close()
+    return out
+
+
+def comm_info(dist, torch) -> dict:
+    """What the process group really is (rank count from the communicator, NCCL version, init lines)."""
+    info = {"backend": dist.get_backend(), "world_size": dist.get_world_size()}
+    try:
+        v = torch.cuda.nccl.version()
+        info["nccl_version"] = ".".join(str(x) for x in v) if isinstance(v, tuple) else str(v)
+    except Exception:
+        pass
+    lines = []
+    for f in sorted(glob.glob(os.environ.get("NMT_NCCL_LOG_GLOB", "/tmp/nmt_bench_nccl.*.log"))):
+        try:
+            lines += [ln.strip() for ln in open(f) if "nranks" in ln or "Init COMPLETE" in ln]
+        except OSError:
+            pass
+    info["nccl_init_lines"] = lines[:16]
+    return info
+
+
+# ------------------------------------------------------------------------------------- C4 ensemble
+def run_ensemble(a, rank: int, world: int, dist) -> None:
+    """C4: M members (seeds 2016..2016+M-1) score the same C2 batch; per-word log-probs are combined
+    (mode 0, lambda = 1/M) on member 0.  N >= M GPUs: groups of M ranks, one member per GPU, NCCL;
+    N == 1: all members on the GPU, one host thread each, in-process communicator."""
+    import torch
+    from paper_1605_04809_b200 import nmt
+    Mn = a.ensemble
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    d = model_dims(a.readout)
+    if world == 1:
+        members, group = list(range(Mn)), 0
+    elif world % Mn == 0:
+        members, group = [rank % Mn], rank // Mn
+    else:
+        raise SystemExit(f"--ensemble {Mn} needs 1 GPU or a multiple of {Mn} GPUs (got {world})")
+    streams = [torch.cuda.Stream(device=dev) for _ in members]
+    models = [nmt.Model(synth.params_bytes(d, synth.make_model(d, 2016 + m)), precision=a.precision, device=dev,
+                        max_src_len=64, stream=streams[i].cuda_stream) for i, m in enumerate(members)]
+    if world == 1:
+        comms = nmt.Ensemble.local(Mn)
+    else:
+        obj = [None] * world  # every group leader makes its NCCL id; the group's ranks take their leader's
+        dist.all_gather_object(obj, nmt.Ensemble.unique_id() if rank % Mn == 0 else None)
+        ids = obj[group * Mn]
+        comms = [nmt.Ensemble(Mn, rank % Mn, ids, dev)]
+    wls = []
+    for i, m in enumerate(members):
+        with torch.cuda.stream(streams[i]):
+            wls.append(Workload(models[i], d, a, group, a.cands, torch))  # the group's shard: same batch per member
+    nc = a.rows * a.cands
+    out = torch.empty(nc, dtype=torch.float32, device="cuda")
+
+    def member_steps(i, k0, n):
+        for k in range(k0, k0 + n):
+            wls[i].step_dev(k)
+            comms[i].combine(wls[i].logp.data_ptr(), nc, 1.0 / Mn, 0, 0,
+                             out.data_ptr() if comms[i].rank == 0 else None, streams[i].cuda_stream)
+
+    def run_all(k0, n):
+        if len(members) == 1:
+            member_steps(0, k0, n)
+            return
+        err = []
+
+        def body(i):
+            try:
+                torch.cuda.set_device(dev)
+                member_steps(i, k0, n)
+            except BaseException as e:  # noqa: BLE001
+                err.append(e)
+        ts = [threading.Thread(target=body, args=(i,)) for i in range(len(members))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if err:
+            raise err[0]
+
+    run_all(0, a.warmup)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in members]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in members]
+    n0 = nmt.launch_count()
+    with ClockSampler(dev) as clk:
+        for i in range(len(members)):
+            starts[i].record(streams[i])
+        run_all(a.warmup, a.steps)
+        for i in range(len(members)):
+            ends[i].record(streams[i])
+        torch.cuda.synchronize()
+    launches = nmt.launch_count() - n0
+    t_local = max(starts[0].elapsed_time(e) for e in ends) / 1000.0
+    t_max = reduce_max(t_local, dist)
+    groups = max(1, world // Mn)
+    total = float(groups * nc * a.steps)
+    value = total / t_max
+    ms_step = 1000.0 * t_max / a.steps
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if a.precision == "bf16" else "bf16x3",
+            "data": "synthetic (seeded random-init cGRU weights, Zipf ids, injected parent states)",
+            "config": workload_config(a, world), "gpu_launches": int(launches), "clocks": clk.summary(),
+            "combined_word_scores": "value counts each combined (parent, word) log-prob once",
+            "member_word_scores_per_s": value * Mn}
+    if dist is not None:
+        line["comm"] = comm_info(dist, torch)
+    if rank == 0 and not a.no_cpu_baseline:
+        line["parity"] = ensemble_parity(a, models, comms, members, streams, d, torch, nmt) if world == 1 else None
+    for c in comms:
+        c.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def ensemble_parity(a, models, comms, members, streams, d, torch, nmt) -> dict:
+    """The combined log-probs of 64 rows of a batch vs the oracle ensemble (float64 members)."""
+    import oracle as O
+    Mn = len(members)
+    R = 64
+    src = synth.make_source(d.vocab_src, a.src_len - 1, seed=9000)
+    s, y = synth.make_states(R, d.dim_hid, d.vocab_tgt, seed=9001)
+    off, words = synth.make_candidates(R, a.cands, d.vocab_tgt, seed=9002)
+    nc = len(words)
+    res = {}
+
+    def body(i):
+        torch.cuda.set_device(torch.cuda.current_device())
+        c = models[i].encode(src)
+        lp, _, _ = c.score_batch(c.inject_states(s, y), off, words)
+        c.close()
+        with torch.cuda.stream(streams[i]):
+            dl = torch.from_numpy(lp).cuda()
+            o = torch.empty_like(dl)
+            comms[i].combine(dl.data_ptr(), nc, 1.0 / Mn, 0, 0, o.data_ptr() if i == 0 else None, streams[i].cuda_stream)
+        streams[i].synchronize()
+        if i == 0:
+            res["out"] = o.cpu().numpy()
+
+    ts = [threading.Thread(target=body, args=(i,)) for i in range(Mn)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    refs = []
+    for m in members:
+        om = O.Model(d, synth.make_model(d, 2016 + m))
+        sess = O.Session(om, src)
+        ids = [sess.inject_state(s[i], int(y[i])) for i in range(R)]
+        refs.append(sess.score_batch(ids, off, words)[0])
+    ref = O.ensemble_combine(refs, [1.0 / Mn] * Mn, 0)
+    tol = 2e-2 if a.precision == "bf16" else 1e-3
+    err = float(np.max(np.abs(res["out"] - ref)))
+    return {"max_abs_dlogp_combined": err, "tol": tol, "ok": err < tol, "word_scores": nc,
+            "vs": f"float64 oracle ensemble of the {Mn} members (mode 0), 64 parents of one batch"}
+
+
+# ------------------------------------------------------------------------------------- launcher
+def relaunch_under_torchrun(a, argv) -> int:
+    """`python bench.py --gpus N` without torchrun: start N ranks with torchrun (one per GPU) and
+    relay rank 0's JSON line."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    env = dict(os.environ)
+    env["NMT_BENCH_LAUNCHED"] = "1"
+    return subprocess.call(cmd, env=env)
+
+
 def main(argv=None) -> None:
+    argv = sys.argv[1:] if argv is None else argv
     a = parse_args(argv)
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        sys.exit(relaunch_under_torchrun(a, argv))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
     dist = None
-    if world > 1:
+    if world > 1 and a.impl == "ours":
         import torch
         import torch.distributed as tdist
-        if a.impl == "ours":
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-            tdist.init_process_group("nccl")
-            dist = tdist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/nmt_bench_nccl.%h.%p.log")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+        dist = tdist
+        dist.barrier()
     if a.impl == "reference":
         run_reference(a, rank, world)
+    elif a.ensemble:
+        run_ensemble(a, rank, world, dist)
     else:
         run_ours(a, rank, world, dist)
     if dist is not None:

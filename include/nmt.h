@@ -303,13 +303,27 @@ NMT_API nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split
  * comm == NULL restores the full vocabulary.  rank/world must match the communicator.             */
 NMT_API nmt_status nmt_vocab_shard(nmt_model* m, int32_t rank, int32_t world, nmt_ensemble* comm);
 
-/* ---- ensemble hook (models as separately weighted features; north_star NCCL reduce)
- * One member per GPU/process.  nccl_unique_id points to the 128-byte ncclUniqueId broadcast by the
- * harness (torch process group).  combine: out = sum over members of (mode 0) weight*logp or
- * (mode 1) weight*exp(logp), then log in mode 1, reduced to `root` over NVLink; in and out are
- * [dev] float[n] on the member's model stream; out is written on the root only.                 */
+/* ---- ensemble hook and communicators (models as separately weighted features;
+ * north_star: members on separate GPUs, per-word probabilities combined over NVLink) ------------
+ * A communicator (nmt_ensemble) joins n members (or vocab-parallel ranks, nmt_vocab_shard) and has
+ * one of two transports:
+ *  - NCCL (nmt_ensemble_init): one member per process/GPU.  nccl_unique_id points to the 128-byte
+ *    ncclUniqueId made by rank 0 with nmt_ensemble_get_unique_id and broadcast by the harness (torch
+ *    process group).  NCCL is loaded at run time (NMT_ERR_NCCL if it cannot be).
+ *  - local (nmt_ensemble_init_local): all n members in THIS process, each driven by its own host
+ *    thread; devices[n] [host] (NULL -> all on device 0) may repeat, so several members can share a
+ *    GPU.  out[n] [host] receives one handle per rank; free each.  A collective waits up to 120 s for
+ *    every member's thread (then NMT_ERR_INVALID_ARG).
+ * nmt_ensemble_combine: member `rank` contributes member_logprob [dev, n floats, on its model's
+ * device] with its weight; every member's row is all-gathered, and the root writes out [dev, n]
+ * (ignored elsewhere) combining the members IN MEMBER ORDER (fp64 accumulation, deterministic):
+ *    mode 0 (log-linear):   out = sum_m w_m logp_m
+ *    mode 1 (interpolate):  out = mx + log sum_m w_m exp(logp_m - mx),  mx = max_m logp_m  (w_m >= 0)
+ * Issued asynchronously on `stream` (the member's model stream, or any stream ordered after the
+ * producer of member_logprob).  Every member must call it with the same n, mode and root.       */
 NMT_API nmt_status nmt_ensemble_init(int32_t n_members, int32_t rank, const void* nccl_unique_id, int32_t device,
                              nmt_ensemble** out);
+NMT_API nmt_status nmt_ensemble_init_local(int32_t n_members, const int32_t* devices, nmt_ensemble** out);
 NMT_API nmt_status nmt_ensemble_get_unique_id(void* out128);
 NMT_API nmt_status nmt_ensemble_combine(nmt_ensemble* e, const float* member_logprob, int32_t n, float weight,
                                 int32_t mode, int32_t root, float* out, void* stream);

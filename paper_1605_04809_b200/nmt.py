@@ -29,7 +29,7 @@ EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "n
            "nmt_ensemble_free", "nmt_params_average", "nmt_beam_step",
            "nmt_encode_batch", "nmt_save_params", "nmt_params_bytes", "nmt_random_params", "nmt_create_random",
            "nmt_debug_vocab", "nmt_score_batch_multi", "nmt_ctx_reserve", "nmt_score_sequences",
-           "nmt_vocab_shard", "nmt_debug_vocab_shards", "nmt_score_forest_multi"]
+           "nmt_vocab_shard", "nmt_debug_vocab_shards", "nmt_score_forest_multi", "nmt_ensemble_init_local"]
 
 
 N_STAGES = 19
@@ -171,6 +171,7 @@ def lib() -> C.CDLL:
             "nmt_test_gemm": (i32, [i32, i32, i32, i32, vp, vp, vp, vp]),
             "nmt_ensemble_init": (i32, [i32, i32, vp, i32, C.POINTER(vp)]),
             "nmt_ensemble_get_unique_id": (i32, [vp]),
+            "nmt_ensemble_init_local": (i32, [i32, vp, vp]),
             "nmt_ensemble_combine": (i32, [vp, vp, i32, C.c_float, i32, i32, vp, vp]),
             "nmt_ensemble_free": (None, [vp]),
             "nmt_encode_dev": (i32, [vp, vp, i32, C.POINTER(vp)]),
@@ -495,8 +496,24 @@ class Ensemble:
 
     def __init__(self, n_members: int, rank: int, unique_id: bytes, device: int):
         self._h = C.c_void_p()
+        self.n_members, self.rank = n_members, rank
         buf = (C.c_char * 128).from_buffer_copy(unique_id)
         _check(lib().nmt_ensemble_init(n_members, rank, C.cast(buf, C.c_void_p), device, C.byref(self._h)))
+
+    @classmethod
+    def local(cls, n_members: int, devices: Optional[Sequence[int]] = None) -> list:
+        """nmt_ensemble_init_local: n communicator handles of one in-process group (rank q = item q);
+        drive each member from its own thread."""
+        hs = (C.c_void_p * n_members)()
+        devs = None if devices is None else _c(devices, np.int32)
+        _check(lib().nmt_ensemble_init_local(n_members, _ptr(devs), C.cast(hs, C.c_void_p)))
+        out = []
+        for q in range(n_members):
+            e = cls.__new__(cls)
+            e._h = C.c_void_p(hs[q])
+            e.n_members, e.rank = n_members, q
+            out.append(e)
+        return out
 
     def combine(self, logp_ptr: int, n: int, weight: float, mode: int, root: int, out_ptr: Optional[int],
                 stream: Optional[int] = None) -> None:

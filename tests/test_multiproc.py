@@ -71,3 +71,31 @@ def test_c5_lpt_sharding_partitions_and_balances():
         lower = max(sum(costs) / world, max(costs))
         assert max(loads) <= 4 / 3 * lower + max(costs)
         assert max(loads) - min(loads) <= max(costs)
+
+
+def test_bench_launcher_spawns_ranks():
+    """`python bench.py --gpus 2` without torchrun in the environment starts torchrun itself (2 ranks,
+    127.0.0.1 rendezvous) and exactly one JSON line comes back, with n_gpus = 2 (the reference arm runs
+    on the host, so this works without a GPU)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["impl"] == "reference" and j["value"] > 0
+
+
+def test_bench_rejects_mismatched_world():
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2"],
+                       capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
