@@ -77,11 +77,30 @@ typedef struct {
   nmt_readout readout;
 } nmt_dims;
 
+/* Device memory (north_star: "PyTorch is used only for device memory, streams and process groups"):
+ * every device allocation of a model - weights, workspaces, state arenas - goes through dev_alloc /
+ * dev_free when they are set (e.g. PyTorch's caching allocator: the Python binding passes it), else
+ * through a private stream-ordered pool of the model.  Both are called on the calling thread during
+ * nmt_* calls, with the model's stream: dev_alloc(bytes, device, stream, alloc_ctx) returns device
+ * memory usable in stream order on `stream` (NULL -> NMT_ERR_OOM); dev_free(ptr, bytes, device,
+ * stream, alloc_ctx) may reuse it for later work on `stream` at once (work queued before on that
+ * stream finishes first).  No allocation after nmt_load synchronises the device.
+ * arena_bytes bounds the state arenas (per-context node tables, hash, cached states; live and
+ * released contexts): a call that would grow them beyond it first frees released contexts' arenas,
+ * then fails with NMT_ERR_CAPACITY before writing any output.  0 = unbounded.                   */
+typedef void* (*nmt_dev_alloc_fn)(size_t bytes, int32_t device, void* stream, void* alloc_ctx);
+typedef void (*nmt_dev_free_fn)(void* ptr, size_t bytes, int32_t device, void* stream, void* alloc_ctx);
+
 typedef struct {
   int32_t device;          /* CUDA device ordinal */
   nmt_precision precision; /* GEMM recipe, see above */
-  int32_t max_src_len;     /* 0 -> 64; at most 65534 (else NMT_ERR_INVALID_ARG) */
+  int32_t max_src_len;     /* 0 -> 64; at most 65534 and short enough for the attention's shared memory
+                              (about 1100 at H = 1024), else NMT_ERR_INVALID_ARG */
   void* stream;            /* cudaStream_t the model's work is issued on; NULL -> a private stream */
+  size_t arena_bytes;      /* state-arena budget in bytes, 0 = unbounded (see above) */
+  nmt_dev_alloc_fn dev_alloc; /* NULL (with dev_free NULL) -> the model's private pool */
+  nmt_dev_free_fn dev_free;
+  void* alloc_ctx;         /* passed through to dev_alloc / dev_free */
 } nmt_opts;
 
 typedef struct nmt_model nmt_model;
@@ -101,6 +120,9 @@ typedef int64_t nmt_state;
 NMT_API nmt_status nmt_load(const char* params_path, const nmt_opts* opts, nmt_model** out);
 NMT_API nmt_status nmt_load_buffer(const void* buf /*[host]*/, size_t len, const nmt_opts* opts, nmt_model** out);
 NMT_API nmt_status nmt_model_dims(const nmt_model* m, nmt_dims* out);
+/* Device bytes the model holds through its allocator now (live) and at most so far (peak), and the
+ * state-arena bytes counted against nmt_opts.arena_bytes (arena); any pointer may be NULL.       */
+NMT_API nmt_status nmt_model_memory(const nmt_model* m, size_t* live, size_t* peak, size_t* arena);
 /* Checkpoint averaging (NMT-k-Avg: "the element-wise average of all model weights in
  * the NMT ensembles", saved as a new model).  bufs[n] / lens[n] [host] are n params containers with
  * IDENTICAL headers (dims, readout, array names and shapes; else NMT_ERR_SHAPE naming the first

@@ -29,9 +29,18 @@
 using namespace nmt;
 
 static thread_local std::string g_err;
+
+// Diagnostic switches (stage skipping, split-K caps, encoder exchange layout, traces) exist only in
+// a -DNMT_DIAG build; the product library ignores the environment.
+#ifdef NMT_DIAG
+static const char* diag_env(const char* n) { return getenv(n); }
+#else
+static const char* diag_env(const char*) { return nullptr; }
+#endif
 static std::atomic<long long> g_launches{0};
 
 namespace nmt {
+std::mutex g_attr_mu;
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace nmt
 
@@ -47,7 +56,7 @@ static_assert(ST_N == NMT_N_STAGES, "stage table");
 static bool stage_skipped(int st) {
   static const unsigned mask = [] {
     unsigned mk = 0;
-    if (const char* e = getenv("NMT_SKIP"))
+    if (const char* e = diag_env("NMT_SKIP"))
       for (const char* p = e; *p;) {
         mk |= 1u << atoi(p);
         while (*p && *p != ',') ++p;
@@ -86,19 +95,102 @@ nmt_status guard(F&& f) {
   }
 }
 
+}  // namespace
+
+// ------------------------------------------------------------------------------------ device memory
+// Every device allocation of a model goes through its DevMem (include/nmt.h nmt_opts): the caller's
+// allocator hook (dev_alloc / dev_free, e.g. PyTorch's caching allocator via the Python binding) or,
+// without a hook, a private stream-ordered pool of the model (cudaMallocFromPoolAsync; the process's
+// default pool is left alone).  Allocations and frees are ordered on the model stream: none
+// synchronises the device.  Pointers are registered so that a free finds its allocator.
+struct DevMem {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  void* (*fa)(size_t, int32_t, void*, void*) = nullptr;
+  void (*ff)(void*, size_t, int32_t, void*, void*) = nullptr;
+  void* actx = nullptr;
+  cudaMemPool_t pool = nullptr;
+  std::atomic<size_t> live{0}, peak{0};
+  void init_pool() {
+    cudaMemPoolProps pp{};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = device;
+    CK(cudaMemPoolCreate(&pool, &pp));
+    uint64_t thr = (uint64_t)1 << 30;  // released blocks beyond 1 GiB go back to the device
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  void* alloc(size_t bytes) {
+    void* p = nullptr;
+    if (fa) {
+      p = fa(bytes, device, st, actx);
+      if (!p) throw NmtError(NMT_ERR_OOM, "device allocator hook returned NULL for " + std::to_string(bytes) + " bytes");
+    } else {
+      if (!pool) init_pool();
+      CK(cudaMallocFromPoolAsync(&p, bytes, pool, st));
+    }
+    const size_t l = live.fetch_add(bytes) + bytes;
+    size_t pk = peak.load();
+    while (l > pk && !peak.compare_exchange_weak(pk, l)) {
+    }
+    return p;
+  }
+  void release(void* p, size_t bytes) {
+    if (ff) ff(p, bytes, device, st, actx);
+    else cudaFreeAsync(p, st);
+    live.fetch_sub(bytes);
+  }
+  ~DevMem() {
+    if (pool) {
+      cudaSetDevice(device);
+      if (st) cudaStreamSynchronize(st);
+      cudaMemPoolDestroy(pool);
+    }
+  }
+};
+
+namespace {
+std::mutex g_reg_mu;
+std::unordered_map<void*, std::pair<DevMem*, size_t>> g_reg;  // live pointer -> (allocator, bytes)
+thread_local DevMem* tl_mem = nullptr;                       // allocator of the model being served
+
+struct MemScope {  // the calling thread allocates from `m` while the scope lives
+  DevMem* prev;
+  explicit MemScope(DevMem* m) : prev(tl_mem) { tl_mem = m; }
+  ~MemScope() { tl_mem = prev; }
+};
+
+void* raw_alloc(size_t bytes) {
+  if (!tl_mem) throw NmtError(NMT_ERR_CUDA, "internal: device allocation outside a model scope");
+  if (bytes == 0) bytes = 16;
+  void* p = tl_mem->alloc(bytes);
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  g_reg[p] = {tl_mem, bytes};
+  return p;
+}
+void raw_free(void* p) {
+  if (!p) return;
+  std::pair<DevMem*, size_t> e;
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    auto it = g_reg.find(p);
+    if (it == g_reg.end()) return;
+    e = it->second;
+    g_reg.erase(it);
+  }
+  e.first->release(p, e.second);
+}
+
+// zero-initialised device array (memset ordered on the allocator's stream)
 template <typename T>
 T* dalloc(size_t n) {
-  if (n == 0) n = 1;
-  void* p = nullptr;
-  CK(cudaMalloc(&p, n * sizeof(T)));
-  // legacy-stream memset + device sync: the model stream is non-blocking and must see zeros
-  CK(cudaMemset(p, 0, n * sizeof(T)));
-  CK(cudaDeviceSynchronize());
-  return static_cast<T*>(p);
+  T* p = static_cast<T*>(raw_alloc(std::max<size_t>(n, 1) * sizeof(T)));
+  CK(cudaMemsetAsync(p, 0, std::max<size_t>(n, 1) * sizeof(T), tl_mem->st));
+  return p;
 }
 template <typename T>
 void dfree(T*& p) {
-  if (p) cudaFree(p);
+  raw_free(p);
   p = nullptr;
 }
 
@@ -111,6 +203,7 @@ struct Arr {
 
 // ------------------------------------------------------------------------------------ model
 struct nmt_model {
+  DevMem mem;  // first member: destroyed last (the other members' buffers go back through it)
   int device = 0;
   cudaStream_t st = nullptr;
   bool own_stream = false;
@@ -192,6 +285,8 @@ struct nmt_model {
   cudaStream_t est = nullptr;
   cudaEvent_t enc_start_ev = nullptr;
   cudaEvent_t inj_copy_ev = nullptr, inj_done_ev = nullptr;
+  cudaEvent_t ws_ev = nullptr;  // end of the last workspace (re)allocation on the model stream
+  bool ws_fresh = false;        // the copy stream has not waited for ws_ev yet
   CUtensorMap tm_As, tm_X, tm_At;
   // multi-context step workspace (nmt_score_batch_multi): ints (bcount | snap | R | row_grp) and
   // the group descriptors (PlanDesc[G] | GrpStep[G])
@@ -221,7 +316,12 @@ struct nmt_model {
   std::atomic<int> refs{1};
   // released contexts kept for reuse (no cudaMalloc / memset per sentence)
   std::vector<nmt_ctx*> pool;
-  size_t pool_bytes = 0;  // arena bytes held by pooled contexts (trimmed above NMT_POOL_CAP_GB)
+  // state-arena accounting (nmt_opts.arena_bytes): bytes of the arenas of live AND pooled contexts
+  size_t arena_budget = 0;  // 0 = no limit
+  size_t arena_total = 0;
+  size_t pool_bytes = 0;    // of which pooled; released arenas beyond kPoolKeep are shrunk
+  static constexpr size_t kPoolKeep = (size_t)8 << 30;
+  void admit_arena(size_t extra);  // trims pooled contexts, else NMT_ERR_CAPACITY
   // CUDA-event profiling of the stages (mode 0 off, 1 vocabulary GEMM only, 2 all)
   int prof_mode = 0;
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> prof_pending;
@@ -239,6 +339,7 @@ struct nmt_model {
     return e;
   }
 
+  bool dying = false;
   ~nmt_model();
   void free_ws();
   void ensure_ws(int R, int NC);
@@ -257,7 +358,7 @@ static void free_all_model(nmt_model* m) {
   for (__nv_bfloat16** p : {&m->eb.A, &m->eb.ctxbf, &m->eb.Am}) dfree(*p);
   for (float** p : {&m->eb.h, &m->eb.G, &m->eb.P}) dfree(*p);
   dfree(m->eb.ints);
-  if (m->eb.blob) cudaFree(m->eb.blob);
+  raw_free(m->eb.blob);
   m->eb.blob = nullptr;
   m->free_ws();
   dfree(m->fws_i);
@@ -269,6 +370,8 @@ static void free_all_model(nmt_model* m) {
   m->pin = nullptr;
   if (m->pin2_ev) cudaEventDestroy(m->pin2_ev);
   m->pin2_ev = nullptr;
+  if (m->ws_ev) cudaEventDestroy(m->ws_ev);
+  m->ws_ev = nullptr;
   if (m->est) {
     cudaStreamSynchronize(m->est);
     cudaStreamDestroy(m->est);
@@ -304,6 +407,7 @@ struct ProfScope {  // CUDA events around one stage's launches on the model stre
 };
 
 nmt_model::~nmt_model() {
+  dying = true;
   cudaSetDevice(device);
   if (st) cudaStreamSynchronize(st);
   for (nmt_ctx* c : pool) delete c;
@@ -391,6 +495,10 @@ void nmt_model::ensure_ws(int R, int NC) {
   tm_As = make_tmap_bf16(A_s, R_cap, (uint64_t)sf * Hp, 128);
   tm_X = make_tmap_bf16(X, R_cap, (uint64_t)sf * 4 * Hp, 128);
   tm_At = make_tmap_bf16(A_t, R_cap, (uint64_t)sf * Ep, 128);
+  // the zero-fills above run on the model stream; the inject copy stream must not overtake them
+  if (!ws_ev) CK(cudaEventCreateWithFlags(&ws_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ws_ev, st));
+  ws_fresh = true;
 }
 
 // ------------------------------------------------------------------------------------ context
@@ -442,6 +550,8 @@ struct nmt_ctx {
   size_t arena_bytes() const {
     return (size_t)slot_cap * (m->Hp + m->Ep + 2) * 4 + (size_t)node_cap * 5 * 4 + (size_t)hcap * 12;
   }
+  size_t charged = 0;  // bytes of this context counted in the model's arena_total
+  nmt_model* acct = nullptr;  // the model whose arena_total counts them (not a reference)
   void shrink();
   void grow_nodes(int64_t need);
   void grow_slots(int64_t need);
@@ -478,14 +588,12 @@ void nmt_ctx::sync_counters() {
 // Arena growth is stream-ordered (cudaMallocAsync / copies / cudaFreeAsync on the model stream): no
 // host or device-wide synchronisation, so a growing context never stalls other work on the GPU.
 template <typename T>
-static T* salloc(size_t n, cudaStream_t st) {
-  void* p = nullptr;
-  CK(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st));
-  return static_cast<T*>(p);
+static T* salloc(size_t n, cudaStream_t) {
+  return static_cast<T*>(raw_alloc(std::max<size_t>(n, 1) * sizeof(T)));
 }
 template <typename T>
-static void sfree(T*& p, cudaStream_t st) {
-  if (p) cudaFreeAsync(p, st);
+static void sfree(T*& p, cudaStream_t) {
+  raw_free(p);
   p = nullptr;
 }
 template <typename T>
@@ -499,6 +607,12 @@ static T* grow_copy_async(T* old, size_t old_n, size_t new_n, cudaStream_t st) {
 void nmt_ctx::grow_nodes(int64_t need) {
   int64_t nc = std::max<int64_t>(need, (int64_t)node_cap * 2);
   if (nc > INT32_MAX / 2) throw NmtError(NMT_ERR_CAPACITY, "state arena: too many nodes");
+  int64_t nh = 1;
+  while (nh < 2 * nc) nh <<= 1;
+  const size_t extra = (size_t)(nc - node_cap) * 5 * 4 + (size_t)(nh > hcap ? nh - hcap : 0) * 12;
+  m->admit_arena(extra);
+  m->arena_total += extra;
+  charged += extra;
   cudaStream_t st = m->st;
   auto g = [&](int*& p, int fill) {
     int* q = grow_copy_async(p, node_cap, nc, st);
@@ -511,8 +625,6 @@ void nmt_ctx::grow_nodes(int64_t need) {
   g(node_src, 0);
   g(node_slot, -1);
   g(node_claim, INT32_MAX);
-  int64_t nh = 1;
-  while (nh < 2 * nc) nh <<= 1;
   if (nh != hcap) {
     unsigned long long* nk = salloc<unsigned long long>(nh, st);
     int* nv = salloc<int>(nh, st);
@@ -532,6 +644,9 @@ void nmt_ctx::grow_nodes(int64_t need) {
 // for one huge sentence does not keep GBs for the rest of the run
 void nmt_ctx::shrink() {
   cudaStream_t st = m->st;
+  const size_t arena = arena_bytes();
+  m->arena_total -= arena;
+  charged -= arena;
   for (int** p : {&node_word, &node_parent, &node_src, &node_slot, &node_claim, &hvals, &amax}) sfree(*p, st);
   sfree(hkeys, st);
   for (float** p : {&S, &T, &logZ}) sfree(*p, st);
@@ -544,6 +659,10 @@ void nmt_ctx::shrink() {
 void nmt_ctx::grow_slots(int64_t need) {
   int64_t nc = std::max<int64_t>(need, (int64_t)slot_cap * 2);
   if (nc > INT32_MAX / 2) throw NmtError(NMT_ERR_CAPACITY, "state arena: too many stepped nodes");
+  const size_t extra = (size_t)(nc - slot_cap) * (m->Hp + m->Ep + 2) * 4;
+  m->admit_arena(extra);
+  m->arena_total += extra;
+  charged += extra;
   cudaStream_t st = m->st;
   float* nS = grow_copy_async(S, (size_t)slot_cap * m->Hp, (size_t)nc * m->Hp, st);
   float* nT = grow_copy_async(T, (size_t)slot_cap * m->Ep, (size_t)nc * m->Ep, st);
@@ -573,7 +692,32 @@ static void model_release(nmt_model* m) {
   if (m && m->refs.fetch_sub(1) == 1) delete m;
 }
 
+// serialises the calls on a model (one writer per context) and routes the calling
+// thread's device allocations to the model's allocator
+struct ModelLock {
+  std::lock_guard<std::mutex> lk;
+  MemScope ms;
+  explicit ModelLock(nmt_model* m) : lk(m->mu), ms(&m->mem) { CK(cudaSetDevice(m->device)); }
+};
+
+// Before `extra` more arena bytes are allocated: within the budget, or pooled (released) contexts
+// are freed until it is, else NMT_ERR_CAPACITY (nothing has been allocated or written yet).
+void nmt_model::admit_arena(size_t extra) {
+  if (!arena_budget || arena_total + extra <= arena_budget) return;
+  while (!pool.empty() && arena_total + extra > arena_budget) {
+    nmt_ctx* c = pool.back();
+    pool.pop_back();
+    pool_bytes -= std::min(pool_bytes, c->arena_bytes());
+    delete c;  // (un-charges itself) stream-ordered frees: work queued on the model stream finishes first
+  }
+  if (arena_total + extra > arena_budget)
+    throw NmtError(NMT_ERR_CAPACITY, "state arena budget exceeded: arena_bytes = " + std::to_string(arena_budget) +
+                                         ", in use " + std::to_string(arena_total) + ", need " +
+                                         std::to_string(extra) + " more");
+}
+
 nmt_ctx::~nmt_ctx() {
+  if (acct && !acct->dying) acct->arena_total -= std::min(acct->arena_total, charged);
   if (m) {
     cudaSetDevice(m->device);
     cudaStreamSynchronize(m->st);
@@ -639,12 +783,7 @@ struct Upload {  // temporary device copy of one raw fp32 array
     d = dalloc<float>((size_t)a.rows * a.cols);
     CK(cudaMemcpyAsync(d, a.h, (size_t)a.rows * a.cols * 4, cudaMemcpyHostToDevice, st));
   }
-  ~Upload() {
-    if (d) {
-      cudaDeviceSynchronize();
-      cudaFree(d);
-    }
-  }
+  ~Upload() { dfree(d); }  // stream-ordered after the packing kernels that read it
 };
 
 static float* upload_vec(const std::vector<float>& v, cudaStream_t st) {
@@ -989,16 +1128,16 @@ static void parse_and_build(const char* buf, size_t len, const nmt_opts* opts, n
   }
   CK(cudaStreamCreateWithFlags(&m->est, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&m->enc_start_ev, cudaEventDisableTiming));
-  {  // arenas grow with cudaMallocAsync: keep released blocks in the device pool for reuse
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, o.device) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    cudaGetLastError();
-  }
+  m->mem.device = o.device;
+  m->mem.st = m->st;
+  if ((o.dev_alloc == nullptr) != (o.dev_free == nullptr))
+    throw NmtError(NMT_ERR_INVALID_ARG, "dev_alloc and dev_free must be given together");
+  m->mem.fa = o.dev_alloc;
+  m->mem.ff = o.dev_free;
+  m->mem.actx = o.alloc_ctx;
+  m->arena_budget = o.arena_bytes;
+  MemScope mscope(&m->mem);
   m->split = o.precision == NMT_PREC_FP32CLASS;
-  if (const char* ev = getenv("NMT_PAIR")) m->use_pair = atoi(ev) != 0;
   m->sf = m->split ? 2 : 1;
   m->E = E;
   m->H = H;
@@ -1009,6 +1148,10 @@ static void parse_and_build(const char* buf, size_t len, const nmt_opts* opts, n
   m->maxTx = o.max_src_len > 0 ? o.max_src_len : 64;
   if (m->maxTx > 65534)  // the encoder's exchange tags carry t + 1 in 16 bits
     throw NmtError(NMT_ERR_INVALID_ARG, "max_src_len > 65534");
+  if (attention_smem_bytes(2 * round_up(H, 128), m->maxTx, 4) > 232448)  // (rows per attention CTA <= 4)
+    throw NmtError(NMT_ERR_INVALID_ARG, "max_src_len " + std::to_string(m->maxTx) +
+                                            ": the attention energies of a source that long exceed the 227 KB of "
+                                            "shared memory per CTA");
   m->Ep = round_up(E + 2, 64);
   m->Hp = round_up(H, 128);
   m->Cp = 2 * m->Hp;
@@ -1124,7 +1267,7 @@ static void gemm_split(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b1
 
 static void gemm_auto(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b128, GemmShape& g, float* out,
                       int ldc, int rps, int M_max, cudaStream_t st) {
-  static const int ks_cap = getenv("NMT_MAX_KS") ? std::max(1, atoi(getenv("NMT_MAX_KS"))) : 4;  // (diagnostic)
+  static const int ks_cap = diag_env("NMT_MAX_KS") ? std::max(1, atoi(diag_env("NMT_MAX_KS"))) : 4;  // (diagnostic)
   const int max_ks = std::max(1, std::min(ks_cap, m->P_rows / rps));
   gemm_split(m, a, b128, g, out, ldc, rps, m->P_rows, M_max, max_ks, st);
 }
@@ -1182,7 +1325,7 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
   { ProfScope p_(m, ST_GATHER); step_elementwise(EW_GATHER, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   // D2: GEMM s.[U|Ux] with the GRU1 gates in its epilogue (one launch, no G1 round trip), or the
   // split-K GEMM + k_gru1 (multi-context steps, 1-CTA mode, NMT_FUSE_GRU1=0)
-  static const bool fuse_env = !(getenv("NMT_FUSE_GRU1") && atoi(getenv("NMT_FUSE_GRU1")) == 0);  // (diagnostic)
+  static const bool fuse_env = !(diag_env("NMT_FUSE_GRU1") && atoi(diag_env("NMT_FUSE_GRU1")) == 0);  // (diagnostic)
   if (fuse_env && !ms && m->use_pair && !stage_skipped(ST_GEMM_H1)) {
     ProfScope p_(m, ST_GEMM_H1);
     GemmShape g = gemm_shape(0, Rd, 4 * Hp, Hp, 0, sp, Hp, Hp);
@@ -1494,6 +1637,14 @@ nmt_status nmt_model_dims(const nmt_model* m, nmt_dims* out) {
 
 void nmt_model_free(nmt_model* m) { model_release(m); }
 
+nmt_status nmt_model_memory(const nmt_model* m, size_t* live, size_t* peak, size_t* arena) {
+  if (!m) return fail(NMT_ERR_INVALID_ARG, "model is NULL");
+  if (live) *live = m->mem.live.load();
+  if (peak) *peak = m->mem.peak.load();
+  if (arena) *arena = m->arena_total;
+  return NMT_OK;
+}
+
 // a context for a source of `len` tokens: a released arena from the model's pool, else a new one
 // (holds one model reference; the caller owns it)
 static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
@@ -1505,10 +1656,15 @@ static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
     m->pool_bytes -= std::min(m->pool_bytes, c->arena_bytes());
     m->refs.fetch_add(1);
   } else {
+    const size_t fixed = (size_t)2 * m->maxTx * m->Cp * 4 + CNT_N * 4;
+    m->admit_arena(fixed);
     c = new nmt_ctx();
     c->m = m;
     m->refs.fetch_add(1);
     std::unique_ptr<nmt_ctx> g(c);
+    m->arena_total += fixed;
+    c->charged = fixed;
+    c->acct = m;
     c->ctx = dalloc<float>((size_t)m->maxTx * m->Cp);
     c->pctx = dalloc<float>((size_t)m->maxTx * m->Cp);
     c->counters = dalloc<int>(CNT_N);
@@ -1531,7 +1687,7 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
   ctx_reset(c->dev(), c->hcap, st);  // counters, root node, empty hash table
   // E1-E7 on the encoder stream (ordered after everything queued on the model stream so far); the
   // model stream joins it before the context's first dependent kernel (nmt_ctx::join_enc)
-  static const bool sep = !(getenv("NMT_ENC_STREAM") && atoi(getenv("NMT_ENC_STREAM")) == 0);  // (diagnostic)
+  static const bool sep = !(diag_env("NMT_ENC_STREAM") && atoi(diag_env("NMT_ENC_STREAM")) == 0);  // (diagnostic)
   const cudaStream_t es = (sep && m->prof_mode == 0) ? m->est : st;
   if (es != st) {
     CK(cudaEventRecord(m->enc_start_ev, st));
@@ -1569,15 +1725,15 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
     }
     e.epoch = m->enc_epoch;
     {
-      const char* sw = getenv("NMT_ENC_HXSWAP");
-      const char* sd = getenv("NMT_ENC_HXSTRIDE");
-      const char* rp = getenv("NMT_ENC_HXREP");  // (diagnostic)
+      const char* sw = diag_env("NMT_ENC_HXSWAP");
+      const char* sd = diag_env("NMT_ENC_HXSTRIDE");
+      const char* rp = diag_env("NMT_ENC_HXREP");  // (diagnostic)
       e.hx_rep = rp ? std::max(1, std::min(8, atoi(rp))) : 1;  // (measured: replicas only add store work)
       e.hx_swap = sw ? atoi(sw) & 1 : 0;
       e.hx_stride = sd ? std::max<int64_t>(2 * e.hx_rep * m->Hp, std::min<int64_t>(atoll(sd), 65536))
                        : 2 * e.hx_rep * m->Hp;
     }
-    const bool trace = getenv("NMT_ENC_TRACE") != nullptr;  // diagnostic: per-step phase stamps
+    const bool trace = diag_env("NMT_ENC_TRACE") != nullptr;  // diagnostic: per-step phase stamps
     if (trace) CK(cudaMalloc(&e.trace, ((size_t)(len + 1) * 8 + 2 * 2 * m->NB) * sizeof(long long)));
     if (!stage_skipped(ST_ENC_RECUR)) enc_recur(e, len, es);
     if (trace) {
@@ -1713,10 +1869,10 @@ static void encode_batch_impl(nmt_model* m, int n, const int32_t* ids, const int
   const size_t blob_bytes = (size_t)3 * n * sizeof(float*) + (size_t)n * sizeof(CtxDev) + (size_t)n * 8;
   if (blob_bytes > w.blob_cap) {
     CK(cudaStreamSynchronize(st));
-    if (w.blob) cudaFree(w.blob);
+    raw_free(w.blob);
     w.blob = nullptr;
     w.blob_cap = std::max(blob_bytes, w.blob_cap * 2);
-    CK(cudaMalloc(&w.blob, w.blob_cap));
+    w.blob = raw_alloc(w.blob_cap);
   }
   std::vector<char> hb(blob_bytes);
   float** tp = reinterpret_cast<float**>(hb.data());
@@ -1808,7 +1964,7 @@ nmt_status nmt_encode(nmt_model* m, const int32_t* src, int32_t len, nmt_ctx** o
       return fail(NMT_ERR_TOKEN_RANGE, "source token " + std::to_string(src[i]) + " at " + std::to_string(i) +
                                            " outside [0, " + std::to_string(m->Vs) + ")");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     *out = encode_impl(m, src, nullptr, len);
   });
 }
@@ -1820,7 +1976,7 @@ nmt_status nmt_encode_dev(nmt_model* m, const int32_t* src, int32_t len, nmt_ctx
   if (len > m->maxTx)
     return fail(NMT_ERR_CAPACITY, "source length " + std::to_string(len) + " > max_src_len " + std::to_string(m->maxTx));
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     *out = encode_impl(m, nullptr, src, len);
   });
 }
@@ -1843,10 +1999,10 @@ nmt_status nmt_encode_batch(nmt_model* m, int32_t n, const int32_t* ids, const i
       return fail(NMT_ERR_TOKEN_RANGE, "source token " + std::to_string(ids[i]) + " at " + std::to_string(i) +
                                            " outside [0, " + std::to_string(m->Vs) + ")");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     // a few sentences: the single-sentence persistent recurrence kernel is faster than 2 Tx_max
     // launches (measured crossover ~10 sentences, profiles/r01/encode_batch.jsonl)
-    static const int small_n = getenv("NMT_ENCB_SMALL") ? atoi(getenv("NMT_ENCB_SMALL")) : 8;  // (diagnostic)
+    static const int small_n = diag_env("NMT_ENCB_SMALL") ? atoi(diag_env("NMT_ENCB_SMALL")) : 8;  // (diagnostic)
     if (n <= small_n) {
       std::vector<std::unique_ptr<nmt_ctx>> cs;
       for (int b = 0; b < n; ++b) cs.emplace_back(encode_impl(m, ids + offsets[b], nullptr, offsets[b + 1] - offsets[b]));
@@ -1859,24 +2015,27 @@ nmt_status nmt_encode_batch(nmt_model* m, int32_t n, const int32_t* ids, const i
 
 nmt_state nmt_root(const nmt_ctx* c) { return c ? 0 : -1; }
 
+// a released context goes back to the model's pool (arena kept for reuse; beyond kPoolKeep pooled
+// bytes it is first shrunk to the initial arena).  Called under the model lock.
+static void pool_ctx(nmt_model* m, nmt_ctx* c) {
+  try {
+    c->join_enc();  // later model-stream work on the reused arena follows its encoder
+    if (m->pool_bytes + c->arena_bytes() > nmt_model::kPoolKeep) c->shrink();
+  } catch (...) {
+  }
+  m->pool_bytes += c->arena_bytes();
+  c->m = nullptr;  // pooled arenas hold no model reference; stream order protects their reuse
+  m->pool.push_back(c);
+}
+
 void nmt_ctx_free(nmt_ctx* c) {
   if (!c) return;
   nmt_model* m = c->m;
   {
     std::lock_guard<std::mutex> lk(m->mu);
+    MemScope ms(&m->mem);
     cudaSetDevice(m->device);
-    try {
-      c->join_enc();  // later model-stream work on the reused arena follows its encoder
-    } catch (...) {
-    }
-    static const double cap_gb = getenv("NMT_POOL_CAP_GB") ? atof(getenv("NMT_POOL_CAP_GB")) : 32.0;
-    try {
-      if ((double)(m->pool_bytes + c->arena_bytes()) > cap_gb * (1 << 30)) c->shrink();
-    } catch (...) {
-    }
-    m->pool_bytes += c->arena_bytes();
-    c->m = nullptr;  // pooled arenas hold no model reference; stream order protects their reuse
-    m->pool.push_back(c);
+    pool_ctx(m, c);
   }
   model_release(m);
 }
@@ -1896,7 +2055,7 @@ nmt_status nmt_beam_step(nmt_ctx* c, int32_t np, const nmt_state* parents, int32
   nmt_model* m = c->m;
   if (k > m->V) return fail(NMT_ERR_INVALID_ARG, "k > vocab_tgt");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     cudaStream_t st = m->st;
     if (c->stale) c->sync_counters();
@@ -1991,7 +2150,7 @@ nmt_status nmt_score_batch(nmt_ctx* c, int32_t np, const nmt_state* parents, con
       return fail(NMT_ERR_TOKEN_RANGE, "cand_words[" + std::to_string(i) + "] = " + std::to_string(words[i]) +
                                            " outside [0, " + std::to_string(m->V) + ")");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     cudaStream_t st = m->st;
     if (c->stale) c->sync_counters();
@@ -2072,7 +2231,7 @@ static nmt_status debug_vocab_impl(nmt_model* m, int32_t R, const float* t, cons
   for (int i = 0; i < nc; ++i)
     if (words[i] < 0 || words[i] >= m->V) return fail(NMT_ERR_TOKEN_RANGE, "cand_words[" + std::to_string(i) + "]");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     cudaStream_t st = m->st;
     std::unique_ptr<nmt_ctx> cg(acquire_ctx(m, 1));
@@ -2141,9 +2300,7 @@ static nmt_status debug_vocab_impl(nmt_model* m, int32_t R, const float* t, cons
     std::memcpy(out_logZ, lz.data(), (size_t)R * 4);
     if (out_argmax) std::memcpy(out_argmax, am.data(), (size_t)R * 4);
     // the scratch arena goes back to the pool
-    nmt_ctx* cc = cg.release();
-    cc->m = nullptr;
-    m->pool.push_back(cc);
+    pool_ctx(m, cg.release());
     m->refs.fetch_sub(1);
   });
 }
@@ -2173,7 +2330,7 @@ nmt_status nmt_score_batch_multi(int32_t np, nmt_ctx* const* cpp, const nmt_stat
       return fail(NMT_ERR_TOKEN_RANGE, "cand_words[" + std::to_string(i) + "] = " + std::to_string(words[i]) +
                                            " outside [0, " + std::to_string(m->V) + ")");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     cudaStream_t st = m->st;
     // groups in first-appearance order of their context
@@ -2400,7 +2557,7 @@ nmt_status nmt_score_batch_dev(nmt_ctx* c, int32_t np, const int32_t* parents, c
   if (!parents || !off || (nc > 0 && (!words || !out_logp))) return fail(NMT_ERR_INVALID_ARG, "NULL device array");
   nmt_model* m = c->m;
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     m->ensure_ws(np, nc);
     c->ensure(nc, np);
@@ -2454,7 +2611,7 @@ static nmt_status score_forest_impl(nmt_ctx* c, int32_t n_pairs, const nmt_state
     if (pwords[k] < 0 || pwords[k] >= m->V)
       return fail(NMT_ERR_TOKEN_RANGE, "phrase_words[" + std::to_string(k) + "] outside [0, " + std::to_string(m->V) + ")");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     cudaStream_t st = m->st;
     if (c->stale) c->sync_counters();
@@ -2619,7 +2776,7 @@ static nmt_status score_forest_impl(nmt_ctx* c, int32_t n_pairs, const nmt_state
 nmt_status nmt_ctx_check(nmt_ctx* c) {
   if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(c->m->mu);
+    ModelLock lk(c->m);
     CK(cudaSetDevice(c->m->device));
     c->join_enc();
     int h[CNT_N];
@@ -2641,7 +2798,7 @@ nmt_status nmt_ctx_check(nmt_ctx* c) {
 nmt_status nmt_ctx_stats(nmt_ctx* c, int64_t* n_nodes, int64_t* n_stepped) {
   if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(c->m->mu);
+    ModelLock lk(c->m);
     CK(cudaSetDevice(c->m->device));
     c->sync_counters();
     if (n_nodes) *n_nodes = c->n_nodes;
@@ -2652,7 +2809,7 @@ nmt_status nmt_ctx_stats(nmt_ctx* c, int64_t* n_nodes, int64_t* n_stepped) {
 nmt_status nmt_vocab_shard(nmt_model* m, int32_t rank, int32_t world, nmt_ensemble* comm) {
   if (!m || world < 1 || rank < 0 || rank >= world) return fail(NMT_ERR_INVALID_ARG, "bad rank/world");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     CK(cudaStreamSynchronize(m->st));
     if (world == 1 || !comm) {
@@ -2675,7 +2832,7 @@ nmt_status nmt_vocab_shard(nmt_model* m, int32_t rank, int32_t world, nmt_ensemb
 nmt_status nmt_ctx_reserve(nmt_ctx* c, int64_t n_nodes, int64_t n_stepped) {
   if (!c || n_nodes < 0 || n_stepped < 0) return fail(NMT_ERR_INVALID_ARG, "bad argument");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(c->m->mu);
+    ModelLock lk(c->m);
     CK(cudaSetDevice(c->m->device));
     if (c->stale) c->sync_counters();
     if (n_nodes > c->node_cap) c->grow_nodes(n_nodes);
@@ -2689,7 +2846,7 @@ nmt_status nmt_inject_states(nmt_ctx* c, int32_t n, const float* s, const int32_
   for (int i = 0; i < n; ++i)
     if (y[i] < -1 || y[i] >= m->V) return fail(NMT_ERR_TOKEN_RANGE, "y_prev out of range");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     if (n == 0) return;
     cudaStream_t st = m->st;
@@ -2705,6 +2862,10 @@ nmt_status nmt_inject_states(nmt_ctx* c, int32_t n, const float* s, const int32_
       CK(cudaEventCreateWithFlags(&m->inj_done_ev, cudaEventDisableTiming));
     }
     CK(cudaStreamWaitEvent(m->cst, m->inj_done_ev, 0));
+    if (m->ws_fresh) {
+      CK(cudaStreamWaitEvent(m->cst, m->ws_ev, 0));
+      m->ws_fresh = false;
+    }
     CK(cudaMemcpyAsync(m->in_s, s, (size_t)n * m->H * 4, cudaMemcpyHostToDevice, m->cst));
     CK(cudaMemcpyAsync(m->in_y, y, (size_t)n * 4, cudaMemcpyHostToDevice, m->cst));
     CK(cudaEventRecord(m->inj_copy_ev, m->cst));
@@ -2728,7 +2889,7 @@ nmt_status nmt_inject_states_dev(nmt_ctx* c, int32_t n, const float* s, const in
   if (!c || n < 0 || (n > 0 && (!s || !y || !out))) return fail(NMT_ERR_INVALID_ARG, "bad argument");
   nmt_model* m = c->m;
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     if (n == 0) return;
     m->ensure_ws(1, 1);  // (workspace holds the inject block counter)
@@ -2752,7 +2913,7 @@ nmt_status nmt_profile(nmt_model* m, int32_t mode) {
 nmt_status nmt_profile_read(nmt_model* m, double* ms, int64_t* count) {
   if (!m) return fail(NMT_ERR_INVALID_ARG, "model is NULL");
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     CK(cudaStreamSynchronize(m->st));
     for (auto& t : m->prof_pending) {
@@ -2777,7 +2938,7 @@ nmt_status nmt_logprobs_full(nmt_ctx* c, nmt_state node, float* out) {
   if (!c || !out) return fail(NMT_ERR_INVALID_ARG, "NULL argument");
   nmt_model* m = c->m;
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     const int slot = step_single(m, c, (int)node, false);
     float* d = dalloc<float>(m->V);
@@ -2792,7 +2953,7 @@ nmt_status nmt_debug_encoder(nmt_ctx* c, float* ctx, float* pctx, float* s0) {
   if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");
   nmt_model* m = c->m;
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     const int H = m->H, Hp = m->Hp, Cp = m->Cp, Tx = c->Tx;
     c->join_enc();
@@ -2816,7 +2977,7 @@ nmt_status nmt_debug_intermediates(nmt_ctx* c, nmt_state node, float* s1, float*
   if (!c) return fail(NMT_ERR_INVALID_ARG, "ctx is NULL");
   nmt_model* m = c->m;
   return guard([&] {
-    std::lock_guard<std::mutex> lk(m->mu);
+    ModelLock lk(m);
     CK(cudaSetDevice(m->device));
     step_single(m, c, (int)node, true);
     cudaStream_t st = m->st;
@@ -2850,6 +3011,10 @@ nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_
   return guard([&] {
     cudaStream_t st;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    DevMem mem;
+    CK(cudaGetDevice(&mem.device));
+    mem.st = st;
+    MemScope mscope(&mem);
     const int sf = split ? 2 : 1, Mp = round_up(M, 128);
     __nv_bfloat16* a = dalloc<__nv_bfloat16>((size_t)Mp * sf * K);
     __nv_bfloat16* b = dalloc<__nv_bfloat16>((size_t)N * sf * K);
@@ -2878,7 +3043,7 @@ nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    if (getenv("NMT_BENCH_FLUSH")) {  // (diagnostic) cold L2: a 256 MiB write before every timed launch
+    if (diag_env("NMT_BENCH_FLUSH")) {  // (diagnostic) cold L2: a 256 MiB write before every timed launch
       void* fl = nullptr;
       CK(cudaMalloc(&fl, (size_t)256 << 20));
       float tot = 0.f;
@@ -2909,6 +3074,8 @@ nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_
     dfree(c);
     dfree(part);
     dfree(cpm);
+    CK(cudaStreamSynchronize(st));
+    mem.st = nullptr;
     cudaStreamDestroy(st);
   });
 }
@@ -2922,6 +3089,10 @@ nmt_status nmt_test_gemm(int32_t M, int32_t N, int32_t K, int32_t split, const f
     CK(cudaGetDevice(&dev));
     cudaStream_t st;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    DevMem mem;
+    mem.device = dev;
+    mem.st = st;
+    MemScope mscope(&mem);
     const int sf = split ? 2 : 1;
     const int Mp = round_up(M, 128);
     float *dA = dalloc<float>((size_t)M * K), *dB = dalloc<float>((size_t)K * N), *dC = dalloc<float>((size_t)M * N);
@@ -2943,6 +3114,8 @@ nmt_status nmt_test_gemm(int32_t M, int32_t N, int32_t K, int32_t split, const f
     dfree(db);
     dfree(a);
     dfree(b);
+    CK(cudaStreamSynchronize(st));
+    mem.st = nullptr;
     cudaStreamDestroy(st);
   });
 }

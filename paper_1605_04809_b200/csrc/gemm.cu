@@ -539,11 +539,8 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
                    const EpiParams& ep, int M_max, cudaStream_t st) {
   using S = GemmSmem<BN, STAGES, EPI, PAIR>;
   static_assert(S::BYTES <= 232448, "shared memory budget");
-  static bool attr_set = false;  // per template instance; set once per process (single device use)
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_gemm<BN, STAGES, EPI, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES));
-    attr_set = true;
-  }
+  static std::atomic<size_t> smem_attr[kMaxDevices];  // per template instance and device
+  ensure_smem_attr(k_gemm<BN, STAGES, EPI, PAIR>, smem_attr, (size_t)S::BYTES);
   const int CM = PAIR ? 2 * BM : BM;
   int tiles = 0;  // work items at M_max rows (EPI_STORE: per region, with its split count)
   for (int r = 0, nt0 = 0; r < g.nreg; ++r) {

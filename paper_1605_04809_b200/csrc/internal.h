@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
 #include <string>
 
 #include "../../include/nmt.h"
@@ -34,6 +36,23 @@ void note_launch();
     ::nmt::note_launch();      \
     CK(cudaGetLastError());    \
   } while (0)
+
+// The > 48 KB dynamic shared-memory opt-in is a per-device-context attribute of a kernel: set it once per
+// (kernel, device) at the largest size requested so far (thread-safe; models may live on several devices
+// and be driven by several threads).  `per_dev` is a function-local static of the launch site.
+constexpr int kMaxDevices = 64;
+extern std::mutex g_attr_mu;
+template <typename K>
+inline void ensure_smem_attr(K* kernel, std::atomic<size_t>* per_dev, size_t smem) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) throw NmtError(NMT_ERR_CUDA, "device ordinal beyond kMaxDevices");
+  if (smem <= per_dev[dev].load(std::memory_order_acquire)) return;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (smem <= per_dev[dev].load(std::memory_order_relaxed)) return;
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  per_dev[dev].store(smem, std::memory_order_release);
+}
 
 // Launch with the programmatic-stream-serialization attribute (PDL): the kernel may start while the
 // previous kernel of the stream drains; every kernel calls pdl_wait() before touching its inputs.

@@ -988,17 +988,19 @@ __global__ void k_full_row(const float* __restrict__ T, const float* __restrict_
   if (lane == 0) out[w] = s + bo[w] - logZ[slot];
 }
 
+size_t attention_smem_bytes(int Cp, int Tx, int rpb) {
+  const int nthr = Cp / 8;
+  const int nw = nthr / 32 > 0 ? nthr / 32 : 1;
+  const int Tx8 = (Tx + 7) & ~7;  // (as in the kernel: JB divides 8)
+  return (size_t)8 * nthr * 2 * sizeof(float4) + (size_t)(nw * rpb * Tx8 + rpb * Tx) * sizeof(float);
+}
+
 template <int RPB>
 static void launch_attention(const StepDev& d, const AttnCtx& a, int R_max, cudaStream_t st) {
   const int nthr = d.Cp / 8;
-  const int nw = nthr / 32 > 0 ? nthr / 32 : 1;
-  const int Tx8 = (a.Tx + 7) & ~7;  // (as in the kernel: JB divides 8)
-  const size_t smem = (size_t)8 * nthr * 2 * sizeof(float4) + (size_t)(nw * RPB * Tx8 + RPB * a.Tx) * sizeof(float);
-  static size_t attr = 0;  // > 48 KB of dynamic shared memory needs the opt-in
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_attention<RPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  const size_t smem = attention_smem_bytes(d.Cp, a.Tx, RPB);
+  static std::atomic<size_t> attr[kMaxDevices];  // > 48 KB of dynamic shared memory needs the opt-in
+  ensure_smem_attr(k_attention<RPB>, attr, smem);
   launch_pdl(k_attention<RPB>, (R_max + RPB - 1) / RPB, nthr, smem, st, d, a);
 }
 
@@ -1015,7 +1017,11 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
     case EW_GRU1: launch_pdl(k_gru1, gh, 256, 0, st, d, S); break;
     case EW_ATTN: {
       // one wave: rows per CTA = ceil(R / SMs) (<= 8), so every SM carries the same number of rows
+#ifdef NMT_DIAG
       static const int rpb_env = getenv("NMT_ATTN_RPB") ? atoi(getenv("NMT_ATTN_RPB")) : 0;  // (diagnostic)
+#else
+      constexpr int rpb_env = 0;
+#endif
       // rows per CTA: ceil(R / SMs), at most 4 (measured in the step at R = 1024: 4 rows x 256 CTAs is
       // ~28 us faster than one wave of 7-row CTAs, whose single CTA per SM hides less latency)
       int rpb = rpb_env > 0 ? std::min(8, rpb_env) : std::max(1, std::min(4, (R_max + kNumSMs - 1) / kNumSMs));
@@ -1746,11 +1752,8 @@ static void launch_recur2(const EncDev& e, int Tx, cudaStream_t st) {
   void* args[] = {&ee, &Tx};
   const size_t smem = (size_t)((e.H + 2 * e.NB - 1) / (2 * e.NB)) * 2 * e.H * sizeof(float) +
                       (Tx <= kPinMax ? (size_t)Tx * (3 * e.UPC + 1) * sizeof(float) : 0);
-  static size_t attr = 0;  // > 48 KB of dynamic shared memory needs the opt-in
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_enc_recur2<KI, TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  static std::atomic<size_t> attr[kMaxDevices];  // > 48 KB of dynamic shared memory needs the opt-in
+  ensure_smem_attr(k_enc_recur2<KI, TRACE>, attr, smem);
   CK(cudaLaunchCooperativeKernel((void*)k_enc_recur2<KI, TRACE>, dim3(2 * e.NB), dim3(32 * ((e.UPC + 1) / 2)), args,
                                  smem, st));
   note_launch();
@@ -1762,18 +1765,19 @@ static void launch_recur(const EncDev& e, int Tx, cudaStream_t st) {
   void* args[] = {&ee, &Tx};
   const size_t smem = (size_t)((e.H + 2 * e.NB - 1) / (2 * e.NB)) * 2 * e.H * sizeof(float) +
                       (Tx <= kPinMax ? (size_t)Tx * (3 * e.UPC + 1) * sizeof(float) : 0);
-  static size_t attr = 0;  // > 48 KB of dynamic shared memory needs the opt-in
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_enc_recur<KI, TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  static std::atomic<size_t> attr[kMaxDevices];  // > 48 KB of dynamic shared memory needs the opt-in
+  ensure_smem_attr(k_enc_recur<KI, TRACE>, attr, smem);
   CK(cudaLaunchCooperativeKernel((void*)k_enc_recur<KI, TRACE>, dim3(2 * e.NB), dim3(32 * e.UPC), args, smem, st));
   note_launch();
 }
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
   if (e.UPC > 14) throw NmtError(NMT_ERR_SHAPE, "encoder: UPC too large");
   // (the caller resets the tags and the barrier counter when the 16-bit epoch wraps)
+#ifdef NMT_DIAG
   static const bool v1 = getenv("NMT_ENC_V") && atoi(getenv("NMT_ENC_V")) == 1;  // (diagnostic: 1-unit warps)
+#else
+  constexpr bool v1 = false;
+#endif
   if (v1 && 32 * e.UPC < e.Hp / 4) throw NmtError(NMT_ERR_SHAPE, "encoder: fewer threads than polled words");
   if (!v1 && 2 * 32 * ((e.UPC + 1) / 2) < e.Hp / 4) throw NmtError(NMT_ERR_SHAPE, "encoder: > 2 polled words per thread");
   switch (e.Hp / 128) {

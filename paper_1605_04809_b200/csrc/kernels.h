@@ -182,6 +182,9 @@ void path_sum(const float* logp, const int* child, const int* off, const int* po
 void full_row(const float* T, const float* Wo32, const float* bo, const float* logZ, int slot, int Ep, int V,
               float* out, cudaStream_t st);
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st);
+// dynamic shared memory of the attention kernel for Cp context columns, Tx source positions and
+// `rpb` rows per CTA (load-time check of max_src_len against the 227 KB per-CTA limit)
+size_t attention_smem_bytes(int Cp, int Tx, int rpb);
 void encb_gates(const EncBatchDev& e, int t, int active, cudaStream_t st);
 void encb_mean(const EncBatchDev& e, cudaStream_t st);
 void encb_s0(const EncBatchDev& e, const float* S0w, int ks, int64_t ps, cudaStream_t st);

@@ -29,7 +29,8 @@ EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "n
            "nmt_ensemble_free", "nmt_params_average", "nmt_beam_step",
            "nmt_encode_batch", "nmt_save_params", "nmt_params_bytes", "nmt_random_params", "nmt_create_random",
            "nmt_debug_vocab", "nmt_score_batch_multi", "nmt_ctx_reserve", "nmt_score_sequences",
-           "nmt_vocab_shard", "nmt_debug_vocab_shards", "nmt_score_forest_multi", "nmt_ensemble_init_local"]
+           "nmt_vocab_shard", "nmt_debug_vocab_shards", "nmt_score_forest_multi", "nmt_ensemble_init_local",
+           "nmt_model_memory"]
 
 
 N_STAGES = 19
@@ -118,8 +119,64 @@ class Dims(C.Structure):
                 ("max_src_len", C.c_int32), ("readout", C.c_int32)]
 
 
+DEV_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p, C.c_void_p)
+DEV_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p, C.c_void_p)
+
+
 class Opts(C.Structure):
-    _fields_ = [("device", C.c_int32), ("precision", C.c_int32), ("max_src_len", C.c_int32), ("stream", C.c_void_p)]
+    _fields_ = [("device", C.c_int32), ("precision", C.c_int32), ("max_src_len", C.c_int32), ("stream", C.c_void_p),
+                ("arena_bytes", C.c_size_t), ("dev_alloc", DEV_ALLOC_FN), ("dev_free", DEV_FREE_FN),
+                ("alloc_ctx", C.c_void_p)]
+
+
+# PyTorch's caching allocator as the library's device allocator (include/nmt.h nmt_opts.dev_alloc):
+# the library's weights, workspaces and state arenas then show up in torch.cuda.memory_allocated()
+# and share torch's cache.  Called back from inside nmt_* calls (ctypes re-acquires the GIL).
+def _torch_alloc(nbytes, device, stream, ctx):
+    try:
+        import torch
+        return int(torch.cuda.caching_allocator_alloc(int(nbytes), int(device), int(stream or 0)))
+    except Exception:  # noqa: BLE001  (out of memory -> NULL -> NMT_ERR_OOM)
+        return None
+
+
+def _torch_free(ptr, nbytes, device, stream, ctx):
+    try:
+        import torch
+        torch.cuda.caching_allocator_delete(int(ptr))
+    except Exception:  # noqa: BLE001
+        pass
+
+
+_TORCH_ALLOC = DEV_ALLOC_FN(_torch_alloc)
+_TORCH_FREE = DEV_FREE_FN(_torch_free)
+
+# models and contexts alive in this process: released before interpreter teardown (the torch
+# allocator callbacks must not run after torch has gone)
+import atexit  # noqa: E402
+import weakref  # noqa: E402
+
+_LIVE = weakref.WeakSet()
+
+
+@atexit.register
+def _close_all():
+    for o in sorted(list(_LIVE), key=lambda x: 0 if isinstance(x, Context) else 1):
+        try:
+            o.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def _make_opts(device, precision, max_src_len, stream, allocator, arena_bytes) -> Opts:
+    if allocator == "auto":
+        import sys
+        allocator = "torch" if "torch" in sys.modules else None
+    if allocator == "torch":
+        return Opts(device, PRECISIONS[precision], max_src_len, stream, arena_bytes, _TORCH_ALLOC, _TORCH_FREE, None)
+    if allocator is not None:
+        raise ValueError("allocator must be 'torch', 'auto' or None")
+    return Opts(device, PRECISIONS[precision], max_src_len, stream, arena_bytes, DEV_ALLOC_FN(), DEV_FREE_FN(), None)
 
 
 _lib = None
@@ -155,6 +212,7 @@ def lib() -> C.CDLL:
             "nmt_load": (i32, [C.c_char_p, C.POINTER(Opts), C.POINTER(vp)]),
             "nmt_load_buffer": (i32, [vp, C.c_size_t, C.POINTER(Opts), C.POINTER(vp)]),
             "nmt_model_dims": (i32, [vp, C.POINTER(Dims)]),
+            "nmt_model_memory": (i32, [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
             "nmt_model_free": (None, [vp]),
             "nmt_encode": (i32, [vp, vp, i32, C.POINTER(vp)]),
             "nmt_root": (i64, [vp]),
@@ -220,9 +278,11 @@ class Model:
     """nmt_load / nmt_load_buffer.  `params` is a path or the bytes of a params container."""
 
     def __init__(self, params, precision: str = "bf16", device: int = 0, max_src_len: int = 64,
-                 stream: Optional[int] = None):
+                 stream: Optional[int] = None, allocator: Optional[str] = "auto", arena_bytes: int = 0):
+        """allocator: "torch" (PyTorch's caching allocator), None (the library's private pool) or
+        "auto" (torch when it is imported).  arena_bytes: state-arena budget (0 = unbounded)."""
         self._h = C.c_void_p()
-        opts = Opts(device, PRECISIONS[precision], max_src_len, stream)
+        opts = _make_opts(device, precision, max_src_len, stream, allocator, arena_bytes)
         if isinstance(params, (bytes, bytearray, memoryview)):
             buf = (C.c_char * len(params)).from_buffer_copy(params)
             _check(lib().nmt_load_buffer(C.cast(buf, C.c_void_p), len(params), C.byref(opts), C.byref(self._h)))
@@ -232,6 +292,13 @@ class Model:
         _check(lib().nmt_model_dims(self._h, C.byref(d)))
         self.dims = d
         self.precision = precision
+        _LIVE.add(self)
+
+    def memory(self) -> dict:
+        """nmt_model_memory: device bytes held now / at peak, and state-arena bytes."""
+        a, b, c = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        _check(lib().nmt_model_memory(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"live": a.value, "peak": b.value, "arena": c.value}
 
     def encode(self, src_ids: Sequence[int]) -> "Context":
         return Context(self, src_ids)
@@ -239,17 +306,18 @@ class Model:
     @classmethod
     def create_random(cls, dim_emb: int, dim_hid: int, vocab_src: int, vocab_tgt: int, readout: str = "tanh",
                       seed: int = 0, logit_std: float = 1.0, precision: str = "bf16", device: int = 0,
-                      max_src_len: int = 64) -> "Model":
+                      max_src_len: int = 64, allocator: Optional[str] = "auto") -> "Model":
         """nmt_create_random: the seeded synthetic model generated and loaded by the library."""
         m = cls.__new__(cls)
         m._h = C.c_void_p()
         d = Dims(dim_emb, dim_hid, vocab_src, vocab_tgt, max_src_len, READOUTS[readout])
-        opts = Opts(device, PRECISIONS[precision], max_src_len, None)
+        opts = _make_opts(device, precision, max_src_len, None, allocator, 0)
         _check(lib().nmt_create_random(C.byref(d), seed, logit_std, C.byref(opts), C.byref(m._h)))
         dd = Dims()
         _check(lib().nmt_model_dims(m._h, C.byref(dd)))
         m.dims = dd
         m.precision = precision
+        _LIVE.add(m)
         return m
 
     def save_params(self, path: str) -> None:
@@ -340,6 +408,7 @@ class Context:
             _check(lib().nmt_encode(model._h, _ptr(src), len(src), C.byref(self._h)))
             self.Tx = len(src)
         self.root = int(lib().nmt_root(self._h))
+        _LIVE.add(self)
 
     @property
     def handle(self) -> int:
@@ -352,6 +421,7 @@ class Context:
         c._h = C.c_void_p(handle)
         c.Tx = Tx
         c.root = int(lib().nmt_root(c._h))
+        _LIVE.add(c)
         return c
 
     def score_batch(self, parents, cand_offsets, cand_words, with_argmax: bool = True
