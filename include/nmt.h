@@ -281,6 +281,10 @@ NMT_API nmt_status nmt_profile(nmt_model* m, int32_t mode);
 NMT_API nmt_status nmt_profile_read(nmt_model* m, double* ms, int64_t* count);
 
 /* ---- test-only exports ----------------------------------------------------------------------- */
+/* live device allocations of every model of the process (count, bytes): 0 after all are freed     */
+NMT_API nmt_status nmt_device_allocations(int64_t* count, size_t* bytes);
+/* models and contexts (live or pooled) that exist in the process                                 */
+NMT_API nmt_status nmt_debug_live_objects(int64_t* models, int64_t* contexts);
 /* full log-prob row of one node over the whole vocab (normalisation tests); steps the node if
  * needed.  out [host, vocab_tgt floats]                                                          */
 NMT_API nmt_status nmt_logprobs_full(nmt_ctx* c, nmt_state node, float* out);

@@ -38,6 +38,7 @@ static const char* diag_env(const char* n) { return getenv(n); }
 static const char* diag_env(const char*) { return nullptr; }
 #endif
 static std::atomic<long long> g_launches{0};
+static std::atomic<long long> g_live_models{0}, g_live_ctxs{0};  // (test-only leak checks)
 
 namespace nmt {
 std::mutex g_attr_mu;
@@ -406,21 +407,6 @@ struct ProfScope {  // CUDA events around one stage's launches on the model stre
   }
 };
 
-nmt_model::~nmt_model() {
-  dying = true;
-  cudaSetDevice(device);
-  if (st) cudaStreamSynchronize(st);
-  for (nmt_ctx* c : pool) delete c;
-  pool.clear();
-  for (auto& t : prof_pending) {
-    cudaEventDestroy(std::get<1>(t));
-    cudaEventDestroy(std::get<2>(t));
-  }
-  for (cudaEvent_t e : prof_free) cudaEventDestroy(e);
-  free_all_model(this);
-  if (own_stream && st) cudaStreamDestroy(st);
-}
-
 void nmt_model::free_ws() {
   for (__nv_bfloat16** p : {&A_s, &X, &A_t}) dfree(*p);
   if (cst) cudaStreamSynchronize(cst);  // (a copy may still target in_s / in_y)
@@ -717,6 +703,7 @@ void nmt_model::admit_arena(size_t extra) {
 }
 
 nmt_ctx::~nmt_ctx() {
+  g_live_ctxs.fetch_sub(1);
   if (acct && !acct->dying) acct->arena_total -= std::min(acct->arena_total, charged);
   if (m) {
     cudaSetDevice(m->device);
@@ -729,6 +716,25 @@ nmt_ctx::~nmt_ctx() {
   dfree(hkeys);
   for (float** p : {&ctx, &pctx, &S, &T, &logZ}) dfree(*p);
   model_release(m);
+}
+
+// (defined after nmt_ctx: the pooled contexts are deleted with their destructor)
+nmt_model::~nmt_model() {
+  dying = true;
+  cudaSetDevice(device);
+  if (st) cudaStreamSynchronize(st);
+  for (nmt_ctx* c : pool) delete c;
+  pool.clear();
+  for (auto& t : prof_pending) {
+    cudaEventDestroy(std::get<1>(t));
+    cudaEventDestroy(std::get<2>(t));
+  }
+  for (cudaEvent_t e : prof_free) cudaEventDestroy(e);
+  free_all_model(this);
+  if (st) cudaStreamSynchronize(st);  // the stream-ordered frees above complete before the pool goes
+  mem.st = nullptr;
+  if (own_stream && st) cudaStreamDestroy(st);
+  g_live_models.fetch_sub(1);
 }
 
 // ------------------------------------------------------------------------------------ loading
@@ -1119,6 +1125,7 @@ static void parse_and_build(const char* buf, size_t len, const nmt_opts* opts, n
   CK(cudaGetDeviceProperties(&prop, o.device));
   if (prop.major != 10) throw NmtError(NMT_ERR_CUDA, std::string("libnmt needs an sm_100 GPU, found ") + prop.name);
   std::unique_ptr<nmt_model> m(new nmt_model());
+  g_live_models.fetch_add(1);
   m->device = o.device;
   if (o.stream) {
     m->st = static_cast<cudaStream_t>(o.stream);
@@ -1637,6 +1644,21 @@ nmt_status nmt_model_dims(const nmt_model* m, nmt_dims* out) {
 
 void nmt_model_free(nmt_model* m) { model_release(m); }
 
+nmt_status nmt_debug_live_objects(int64_t* models, int64_t* contexts) {
+  if (models) *models = g_live_models.load();
+  if (contexts) *contexts = g_live_ctxs.load();
+  return NMT_OK;
+}
+
+nmt_status nmt_device_allocations(int64_t* count, size_t* bytes) {
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  size_t b = 0;
+  for (auto& e : g_reg) b += e.second.second;
+  if (count) *count = (int64_t)g_reg.size();
+  if (bytes) *bytes = b;
+  return NMT_OK;
+}
+
 nmt_status nmt_model_memory(const nmt_model* m, size_t* live, size_t* peak, size_t* arena) {
   if (!m) return fail(NMT_ERR_INVALID_ARG, "model is NULL");
   if (live) *live = m->mem.live.load();
@@ -1659,6 +1681,7 @@ static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
     const size_t fixed = (size_t)2 * m->maxTx * m->Cp * 4 + CNT_N * 4;
     m->admit_arena(fixed);
     c = new nmt_ctx();
+    g_live_ctxs.fetch_add(1);
     c->m = m;
     m->refs.fetch_add(1);
     std::unique_ptr<nmt_ctx> g(c);

@@ -30,13 +30,27 @@ EXPORTS = ["nmt_last_error", "nmt_load", "nmt_load_buffer", "nmt_model_dims", "n
            "nmt_encode_batch", "nmt_save_params", "nmt_params_bytes", "nmt_random_params", "nmt_create_random",
            "nmt_debug_vocab", "nmt_score_batch_multi", "nmt_ctx_reserve", "nmt_score_sequences",
            "nmt_vocab_shard", "nmt_debug_vocab_shards", "nmt_score_forest_multi", "nmt_ensemble_init_local",
-           "nmt_model_memory"]
+           "nmt_model_memory", "nmt_device_allocations", "nmt_debug_live_objects"]
 
 
 N_STAGES = 19
 STAGES = ["plan", "gather", "gemm_h1", "gru1", "gemm_q", "attention", "gemm_g2", "gru2", "gemm_ro", "readout",
           "vocab_gemm_lse", "finalize", "gather_dot", "enc_gather", "enc_gemm_in", "enc_recurrence", "enc_init",
           "enc_pctx", "inject"]
+
+
+def device_allocations() -> Tuple[int, int]:
+    """nmt_device_allocations: (count, bytes) of the library's live device allocations."""
+    n, b = C.c_int64(), C.c_size_t()
+    _check(lib().nmt_device_allocations(C.byref(n), C.byref(b)))
+    return n.value, b.value
+
+
+def live_objects() -> Tuple[int, int]:
+    """nmt_debug_live_objects: (models, contexts incl. pooled) that exist in the process."""
+    a, b = C.c_int64(), C.c_int64()
+    _check(lib().nmt_debug_live_objects(C.byref(a), C.byref(b)))
+    return a.value, b.value
 
 
 def launch_count() -> int:
@@ -212,6 +226,8 @@ def lib() -> C.CDLL:
             "nmt_load": (i32, [C.c_char_p, C.POINTER(Opts), C.POINTER(vp)]),
             "nmt_load_buffer": (i32, [vp, C.c_size_t, C.POINTER(Opts), C.POINTER(vp)]),
             "nmt_model_dims": (i32, [vp, C.POINTER(Dims)]),
+            "nmt_device_allocations": (i32, [C.POINTER(C.c_int64), C.POINTER(C.c_size_t)]),
+            "nmt_debug_live_objects": (i32, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "nmt_model_memory": (i32, [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
             "nmt_model_free": (None, [vp]),
             "nmt_encode": (i32, [vp, vp, i32, C.POINTER(vp)]),

@@ -21,6 +21,8 @@ def test_torch_allocator_holds_the_library_memory():
     blob = synth.params_bytes(d, synth.make_model(d, 2016))
     torch.cuda.synchronize()
     base = torch.cuda.memory_allocated()
+    n0, b0 = nmt().device_allocations()
+    lo0 = nmt().live_objects()
     M = nmt().Model(blob, precision="bf16", allocator="torch")
     after_load = torch.cuda.memory_allocated()
     mem = M.memory()
@@ -37,9 +39,12 @@ def test_torch_allocator_holds_the_library_memory():
     assert after_step > after_load  # the step workspace and the grown arena came from torch
     assert M.memory()["arena"] > 0
     c.close()
+    assert nmt().live_objects() == (lo0[0] + 1, lo0[1] + 1)  # the released context is pooled
     M.close()
     torch.cuda.synchronize()
-    assert torch.cuda.memory_allocated() - base < 16 << 20  # everything went back to torch's cache
+    assert nmt().live_objects() == lo0, (lo0, nmt().live_objects())
+    assert nmt().device_allocations() == (n0, b0), (n0, b0, nmt().device_allocations())  # all freed
+    assert torch.cuda.memory_allocated() - base < 16 << 20, torch.cuda.memory_allocated() - base
 
 
 def test_private_pool_leaves_torch_alone():
