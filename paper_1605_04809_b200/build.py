@@ -24,18 +24,22 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, diag: bool = False, variant: str = "",
+          defines: tuple = ()) -> str:
     """diag: a separate libnmt_diag.so with the -DNMT_DIAG switches (stage skipping, traces, ...) for
-    measurements only; the product library ignores the environment."""
-    lib = os.path.join(HERE, "libnmt_diag.so") if diag else LIB
+    measurements only; the product library ignores the environment.  variant + defines: a diagnostic
+    A/B build libnmt_diag_<variant>.so with extra -D flags."""
+    if variant:
+        diag = True
+    lib = os.path.join(HERE, f"libnmt_diag_{variant}.so" if variant else "libnmt_diag.so") if diag else LIB
     if not diag and not force and not _stale():
         return LIB
-    bdir = os.path.join(BUILD, "diag") if diag else BUILD
+    bdir = os.path.join(BUILD, "diag" + (f"_{variant}" if variant else "")) if diag else BUILD
     os.makedirs(bdir, exist_ok=True)
 
     def compile_one(src: str) -> str:
         obj = os.path.join(bdir, os.path.splitext(src)[0] + ".o")
-        cmd = [NVCC, *FLAGS, *(["-DNMT_DIAG"] if diag else []), "-Xptxas", "-v" if verbose else "-O3", "-c",
+        cmd = [NVCC, *FLAGS, *(["-DNMT_DIAG"] if diag else []), *[f"-D{x}" for x in defines], "-Xptxas", "-v" if verbose else "-O3", "-c",
                os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -493,6 +493,7 @@ struct nmt_ctx {
   int Tx = 0;
   float* ctx = nullptr;   // [Tx][Cp]
   float* pctx = nullptr;  // [Tx][Cp]
+  float* epctx = nullptr;  // [Tx][Cp] exp(2 pctx), exponent clamped (attention, D4)
   int node_cap = 0, slot_cap = 0;
   int64_t hcap = 0;
   int* counters = nullptr;
@@ -714,7 +715,7 @@ nmt_ctx::~nmt_ctx() {
   if (enc_s0_ev) cudaEventDestroy(enc_s0_ev);
   for (int** p : {&counters, &node_word, &node_parent, &node_src, &node_slot, &node_claim, &hvals, &amax}) dfree(*p);
   dfree(hkeys);
-  for (float** p : {&ctx, &pctx, &S, &T, &logZ}) dfree(*p);
+  for (float** p : {&ctx, &pctx, &epctx, &S, &T, &logZ}) dfree(*p);
   model_release(m);
 }
 
@@ -1317,7 +1318,7 @@ struct MultiStep {
 static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = nullptr) {
   cudaStream_t st = m->st;
   StepDev d = step_view(m, c);
-  AttnCtx a{c->pctx, c->ctx, m->U_att, m->c_tt, c->Tx};
+  AttnCtx a{c->pctx, c->ctx, m->U_att, m->c_tt, c->Tx, c->epctx, c->counters};
   if (ms) {
     d.R = ms->R_dev;
     d.row_grp = ms->row_grp;
@@ -1430,9 +1431,31 @@ static PlanIO plan_io(nmt_model* m, int np, int nc, const int* par, const int* o
   return io;
 }
 
+// Pull the decoder GEMMs' weight matrices (bf16: 43 MB at En->Ru) into L2 at the start of a decoder
+// call: the planner and the state gather run while HBM streams them, so the GEMMs' first TMA loads and
+// their steady-state B stages hit L2 (measured per-GEMM phase stamps).  Skipped when the
+// matrices would take more than half of the 126 MB L2 (the vocabulary GEMM streams W_o through it).
+static void prefetch_decoder(nmt_model* m, bool fused_h1, cudaStream_t st) {
+  const size_t sf = m->split ? 2 : 1, Hp = m->Hp, Cp = m->Cp;
+  PrefetchList pl{};
+  auto add = [&](const void* p, size_t bytes) {
+    pl.ptr[pl.n] = p;
+    pl.bytes[pl.n++] = bytes;
+  };
+  if (fused_h1) add(m->W_h1g, 4 * Hp * sf * Hp * 2);
+  else add(m->W_h1, 3 * Hp * sf * Hp * 2);
+  add(m->W_q, Cp * sf * Hp * 2);
+  add(m->W_g2, 4 * Hp * sf * (Hp + Cp) * 2);
+  add(m->W_ro, (size_t)m->ROp * sf * (Cp + Hp) * 2);
+  size_t tot = 0;
+  for (int i = 0; i < pl.n; ++i) tot += pl.bytes[i];
+  if (tot <= ((size_t)63 << 20)) prefetch_weights_l2(pl, st);
+}
+
 static void run_call(nmt_model* m, nmt_ctx* c, const PlanIO& io, float* out_logp, int* out_child,
                      long long* out_child64, int* out_amax) {
   const CtxDev cd = c->dev();
+  if (io.n_par > 0) prefetch_decoder(m, m->use_pair, m->st);
   {
     ProfScope p_(m, ST_PLAN);
     plan(cd, io, c->counters + CNT_R, m->st);
@@ -1678,7 +1701,7 @@ static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
     m->pool_bytes -= std::min(m->pool_bytes, c->arena_bytes());
     m->refs.fetch_add(1);
   } else {
-    const size_t fixed = (size_t)2 * m->maxTx * m->Cp * 4 + CNT_N * 4;
+    const size_t fixed = (size_t)3 * m->maxTx * m->Cp * 4 + CNT_N * 4;
     m->admit_arena(fixed);
     c = new nmt_ctx();
     g_live_ctxs.fetch_add(1);
@@ -1690,6 +1713,7 @@ static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
     c->acct = m;
     c->ctx = dalloc<float>((size_t)m->maxTx * m->Cp);
     c->pctx = dalloc<float>((size_t)m->maxTx * m->Cp);
+    c->epctx = dalloc<float>((size_t)m->maxTx * m->Cp);
     c->counters = dalloc<int>(CNT_N);
     CK(cudaEventCreateWithFlags(&c->enc_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->enc_s0_ev, cudaEventDisableTiming));
@@ -1812,7 +1836,8 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
     }
     const size_t stride = (size_t)m->Tpad * m->Cp;
     gemm_store(m->tm_ctxbf, m->tm_Watt, g, m->ksplit_buf, m->Cp, g.ksplit * m->Tpad, nullptr, len, es, stride);
-    splitk_reduce(m->ksplit_buf, g.ksplit, stride, len, m->Cp, m->Cp, m->b_att, c->pctx, es);
+    splitk_reduce_pctx(m->ksplit_buf, g.ksplit, stride, len, m->Cp, m->Cp, m->b_att, c->pctx, c->epctx,
+                       c->counters + CNT_BIGP, es);
   }
   if (es != st) {
     CK(cudaEventRecord(c->enc_ev, es));
@@ -1889,7 +1914,7 @@ static void encode_batch_impl(nmt_model* m, int n, const int32_t* ids, const int
     for (int j = 0; j < L; ++j) hi[(size_t)n_tok + n + 1 + tok_off[i] + j] = i;
   }
   std::memcpy(&hi[n_tok], tok_off.data(), (size_t)(n + 1) * 4);
-  const size_t blob_bytes = (size_t)3 * n * sizeof(float*) + (size_t)n * sizeof(CtxDev) + (size_t)n * 8;
+  const size_t blob_bytes = (size_t)5 * n * sizeof(float*) + (size_t)n * sizeof(CtxDev) + (size_t)n * 8;
   if (blob_bytes > w.blob_cap) {
     CK(cudaStreamSynchronize(st));
     raw_free(w.blob);
@@ -1899,13 +1924,15 @@ static void encode_batch_impl(nmt_model* m, int n, const int32_t* ids, const int
   }
   std::vector<char> hb(blob_bytes);
   float** tp = reinterpret_cast<float**>(hb.data());
-  CtxDev* tc = reinterpret_cast<CtxDev*>(hb.data() + (size_t)3 * n * sizeof(float*));
-  int64_t* th = reinterpret_cast<int64_t*>(hb.data() + (size_t)3 * n * sizeof(float*) + (size_t)n * sizeof(CtxDev));
+  CtxDev* tc = reinterpret_cast<CtxDev*>(hb.data() + (size_t)5 * n * sizeof(float*));
+  int64_t* th = reinterpret_cast<int64_t*>(hb.data() + (size_t)5 * n * sizeof(float*) + (size_t)n * sizeof(CtxDev));
   int64_t hcap_max = 1;
   for (int i = 0; i < n; ++i) {
     tp[i] = cs[i]->ctx;
     tp[n + i] = cs[i]->pctx;
     tp[2 * n + i] = cs[i]->S;
+    tp[3 * n + i] = cs[i]->epctx;
+    tp[4 * n + i] = reinterpret_cast<float*>(cs[i]->counters);
     tc[i] = cs[i]->dev();
     th[i] = cs[i]->hcap;
     hcap_max = std::max(hcap_max, cs[i]->hcap);
@@ -1913,8 +1940,8 @@ static void encode_batch_impl(nmt_model* m, int n, const int32_t* ids, const int
   CK(cudaMemcpyAsync(w.ints, hi.data(), n_ints * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(w.blob, hb.data(), blob_bytes, cudaMemcpyHostToDevice, st));
   char* db = static_cast<char*>(w.blob);
-  ctx_reset_many(reinterpret_cast<const CtxDev*>(db + (size_t)3 * n * sizeof(float*)),
-                 reinterpret_cast<const int64_t*>(db + (size_t)3 * n * sizeof(float*) + (size_t)n * sizeof(CtxDev)), n,
+  ctx_reset_many(reinterpret_cast<const CtxDev*>(db + (size_t)5 * n * sizeof(float*)),
+                 reinterpret_cast<const int64_t*>(db + (size_t)5 * n * sizeof(float*) + (size_t)n * sizeof(CtxDev)), n,
                  hcap_max, st);
   EncBatchDev e{};
   e.n = n;
@@ -1935,6 +1962,8 @@ static void encode_batch_impl(nmt_model* m, int n, const int32_t* ids, const int
   e.ctx = dtp;
   e.pctx = dtp + n;
   e.S0 = dtp + 2 * n;
+  e.epctx = dtp + 3 * n;
+  e.cnt = reinterpret_cast<int* const*>(dtp + 4 * n);
   e.b_init = m->b_init;
   e.b_att = m->b_att;
   {  // E3/E4: the recurrences, h_{-1} = h_{Tx} = 0
@@ -2106,6 +2135,7 @@ nmt_status nmt_beam_step(nmt_ctx* c, int32_t np, const nmt_state* parents, int32
       CK(cudaMemsetAsync(m->in_off, 0, (size_t)(np + 1) * 4, st));
       PlanIO io = plan_io(m, np, 0, m->in_par, m->in_off, m->in_words);
       io.step_all = 1;
+      prefetch_decoder(m, m->use_pair, st);
       {
         ProfScope p_(m, ST_PLAN);
         plan(cd, io, c->counters + CNT_R, st);
@@ -2288,7 +2318,7 @@ static nmt_status debug_vocab_impl(nmt_model* m, int32_t R, const float* t, cons
     c->n_slots = R + 2;
     StepDev d = step_view(m, c);
     beam_gather(d, c->dev(), m->in_par, R, st);  // vocabulary operand rows [t | 1 (| lo)] from the arena
-    AttnCtx a{c->pctx, c->ctx, m->U_att, m->c_tt, 1};
+    AttnCtx a{c->pctx, c->ctx, m->U_att, m->c_tt, 1, c->epctx, c->counters};
     if (n_slices > 0) {  // vocab-parallel emulation: slice k as rank k of n_slices
       ensure_xbuf(m, n_slices);
       const int T = m->Vp / 256;
@@ -2464,7 +2494,7 @@ nmt_status nmt_score_batch_multi(int32_t np, nmt_ctx* const* cpp, const nmt_stat
       hd[g].out_logp = m->out_logp + cbase[g];
       hd[g].out_child = m->out_child + cbase[g];
       hd[g].out_argmax = m->out_amax + pbase[g];
-      hg[g] = GrpStep{c->S, c->T, c->logZ, c->amax, c->pctx, c->ctx, c->Tx};
+      hg[g] = GrpStep{c->S, c->T, c->logZ, c->amax, c->pctx, c->ctx, c->Tx, c->epctx, c->counters};
     }
     CK(cudaMemcpyAsync(m->in_par, hp, (size_t)np * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(m->in_off, ho, (size_t)(np + G) * 4, cudaMemcpyHostToDevice, st));
@@ -2472,6 +2502,7 @@ nmt_status nmt_score_batch_multi(int32_t np, nmt_ctx* const* cpp, const nmt_stat
     CK(cudaMemcpyAsync(d_R, hR, (size_t)(1 + total_rows) * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(m->mws_b, hdesc, need_b, cudaMemcpyHostToDevice, st));
     fill_i32(m->row_dst, total_rows, -1, st);
+    if (total_rows > 0) prefetch_decoder(m, false, st);  // (multi-context steps use GEMM + k_gru1)
     {
       ProfScope p_(m, ST_PLAN);
       plan_multi(d_desc, G, max_nc, max_np, st);
@@ -3060,6 +3091,7 @@ nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_
       if (epi == 1) gemm_lse(ta, tb, g, part, N, M, st, cpm);
       else if (epi == 4) gemm_lse_pair(ta, tb128, g, part, N, st, cpm);
       else if (epi == 2) gemm_store256(ta, tb, g, c, N, ksplit * Mp, nullptr, M, st, (size_t)Mp * N);
+      else if (epi == 3) gemm_store_pair(ta, tb128, g, c, N, ksplit * Mp, nullptr, M, st, (size_t)Mp * N);
       else gemm_store(ta, tb, g, c, N, ksplit * Mp, nullptr, M, st, (size_t)Mp * N);
     };
     for (int i = 0; i < 3; ++i) run();

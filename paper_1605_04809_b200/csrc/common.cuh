@@ -127,6 +127,33 @@ NMT_DEV void tmem_ld32_nowait(uint32_t taddr, float* v) {
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+// TMEM -> registers: 32 lanes x 8 consecutive 32-bit columns (pair with tmem_wait_ld8_dep)
+NMT_DEV void tmem_ld8_nowait(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+NMT_DEV void reg_dep8(float* v) {
+  asm volatile("" : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]));
+}
+// 256-bit global accesses (sm_100): one full 32-byte sector per thread
+NMT_DEV void ld8_nc(const float* p, float* v) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+NMT_DEV void ld8(const float* p, float* v) {
+  asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p)
+               : "memory");
+}
+NMT_DEV void st8(float* p, const float* v) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
 NMT_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 // wait for outstanding tcgen05.ld and pin the 32 loaded registers behind the wait (the "+f"
 // operands stop the compiler from hoisting their uses above it)
@@ -173,6 +200,16 @@ NMT_DEV float tanh_approx(float x) {
   return y;
 }
 NMT_DEV float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
+
+// packed fp32 pairs (sm_100 FFMA2 / FADD2 / FMUL2): two lanes' worth of FMA work per issue slot
+NMT_DEV unsigned long long f2_bits(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
+NMT_DEV float2 f2_from(unsigned long long b) { return *reinterpret_cast<float2*>(&b); }
+NMT_DEV float2 fma2(float2 a, float2 b, float2 c) {  // a * b + c, round to nearest
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return f2_from(d);
+}
+NMT_DEV void ffma2(float2& acc, float2 a, float2 b) { acc = fma2(a, b, acc); }
 
 // split x = hi + lo with hi, lo bf16 (RNE); |x - hi - lo| <= 2^-16 |x| roughly.
 NMT_DEV void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {

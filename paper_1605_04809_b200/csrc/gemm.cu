@@ -19,7 +19,11 @@
 // the logits never leave the chip (PAPER.md:120 computes P_i explicitly; we never do).
 #include <cuda.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
+#include <vector>
 #include <mutex>
 #include <tuple>
 #include <stdexcept>
@@ -142,6 +146,23 @@ NMT_DEV void gru_store4(__nv_bfloat16* p, int lo_off, float a, float b, float c,
                    gru_pk(c - __uint_as_float(h23 << 16), d - __uint_as_float(h23 & 0xffff0000u)));
 }
 
+// diagnostic phase stamps (NMT_DIAG builds with NMT_GEMM_TRACE): entry, prologue done, inputs ready,
+// first stage landed (MMA), last MMA issued, first accumulator ready (epilogue), epilogue done, exit
+#ifdef NMT_DIAG
+#define GTRACE(ev)                                                                              \
+  do {                                                                                          \
+    if (ep.trace) {                                                                             \
+      unsigned long long t_;                                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                    \
+      ep.trace[blockIdx.x * 8 + (ev)] = t_;                                                     \
+    }                                                                                           \
+  } while (0)
+#else
+#define GTRACE(ev) \
+  do {             \
+  } while (0)
+#endif
+
 template <int BN, int STAGES, int EPI, bool PAIR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -163,6 +184,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
+  if (threadIdx.x == 0) GTRACE(0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -187,7 +209,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) GTRACE(1);
   pdl_enter();  // prologue above overlaps the previous kernel; inputs (and M_dev) are read below
+  if (threadIdx.x == 0) GTRACE(2);
   const int M = g.M_dev ? *g.M_dev : g.M;
   const int unit = PAIR ? blockIdx.x / 2 : blockIdx.x, nunits = PAIR ? gridDim.x / 2 : gridDim.x;
   const Sched sc = make_sched<EPI>(g, M, CM, BN, nunits);
@@ -254,6 +278,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int i = 0; i < nkb; ++i) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
+            if (it == 0 && i == 0) GTRACE(3);
             const uint32_t a0 = smem_u32(sA + stage * S::A_BYTES);
             const uint32_t b0 = smem_u32(sB + stage * S::B_BYTES);
 #pragma unroll
@@ -274,6 +299,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           else mma_commit(&tfull[acc]);
         }
       }
+      GTRACE(4);
     }
   } else {  // ---------------- epilogue warps 2..9 (each CTA: its 128 rows of the tile)
     const int q = warp & 3;               // TMEM lane quadrant accessible to this warp
@@ -301,10 +327,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int n = itm.n0; n < itm.n1; ++n, ++it) {
         const int acc = it & 1;
         const uint32_t aph = (it >> 1) & 1;
+        const int colbase = n * BN + half * COLS;
+        // EPI_GRU: this warp's COLS = 128 columns are one 32-unit group [r | u | h~ | pad] of its row, done
+        // in 4 chunks of 8 units.  A chunk's gx (r, u, x) and previous-state values arrive as 256-bit loads
+        // (full 32-byte sectors) issued two chunks ahead; the first two are issued before the accumulator
+        // wait, so their latency hides under the main loop.
+        float gin[EPI == EPI_GRU ? 2 : 1][4][8];
+        const float* gxr = nullptr;
+        const float* sp = nullptr;
+        auto gru_fetch = [&](int c, float(&b)[4][8]) {
+          if (!valid) return;
+          ld8_nc(gxr + 8 * c, b[0]);
+          ld8_nc(gxr + ep.Hp + 8 * c, b[1]);
+          ld8_nc(gxr + 2 * ep.Hp + 8 * c, b[2]);
+          ld8(sp + 8 * c, b[3]);
+        };
+        if constexpr (EPI == EPI_GRU) {
+          if (valid) {
+            const int j0 = (colbase >> 7) * 32;
+            const int y = ep.row_y[grow];
+            gxr = ep.gx + (int64_t)(y < 0 ? ep.y_bos : y) * ep.gx_ld + j0;
+            sp = ep.S + (int64_t)ep.row_src[grow] * ep.Hp + j0;
+          }
+          gru_fetch(0, gin[0]);
+          gru_fetch(1, gin[1]);
+        }
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
+        if (it == 0 && warp == 2 && lane == 0) GTRACE(5);
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + half * COLS;
-        const int colbase = n * BN + half * COLS;
         if constexpr (EPI == EPI_STORE) {
           // TMEM -> registers (+bias) -> 128B-swizzled 32x32 smem tile -> TMA store (coalesced)
           uint8_t* stile = sC + (size_t)(warp - 2) * 2 * 4096;
@@ -364,38 +415,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         } else if constexpr (EPI == EPI_GRU) {
-          // this warp's COLS = 128 columns are one 32-unit group [r | u | h~ | pad] of its row
           static_assert(BN / 2 == 128, "EPI_GRU: one 32-unit group per epilogue warp");
-          float vr[32], vu[32], vx[32];
-          tmem_ld32_nowait(tbase, vr);
-          tmem_ld32_nowait(tbase + 32, vu);
-          tmem_ld32_nowait(tbase + 64, vx);
-          tmem_wait_ld_dep(vr);
-          reg_dep32(vu);
-          reg_dep32(vx);
-          if (valid) {
-            const int j0 = (colbase >> 7) * 32, Hp = ep.Hp;
-            const int y = ep.row_y[grow];
-            const float* gxr = ep.gx + (int64_t)(y < 0 ? ep.y_bos : y) * ep.gx_ld + j0;
-            const float* sp = ep.S + (int64_t)ep.row_src[grow] * Hp + j0;
-            float* s1 = ep.S1 + (int64_t)grow * Hp + j0;
-            __nv_bfloat16* xo = ep.X + (int64_t)grow * ep.ldx + j0;
+          const int j0 = (colbase >> 7) * 32;
+          float* s1 = ep.S1 + (int64_t)grow * ep.Hp + j0;
+          __nv_bfloat16* xo = ep.X + (int64_t)grow * ep.ldx + j0;
 #pragma unroll
-            for (int k = 0; k < 32; k += 4) {
-              const float4 er = __ldg(reinterpret_cast<const float4*>(gxr + k));
-              const float4 eu = __ldg(reinterpret_cast<const float4*>(gxr + Hp + k));
-              const float4 ec = __ldg(reinterpret_cast<const float4*>(gxr + 2 * Hp + k));
-              const float4 sv = *reinterpret_cast<const float4*>(sp + k);
-              float o[4];
-              const float erv[4] = {er.x, er.y, er.z, er.w}, euv[4] = {eu.x, eu.y, eu.z, eu.w};
-              const float ecv[4] = {ec.x, ec.y, ec.z, ec.w}, svv[4] = {sv.x, sv.y, sv.z, sv.w};
+          for (int c = 0; c < 4; ++c) {
+            float vr[8], vu[8], vx[8];
+            tmem_ld8_nowait(tbase + 8 * c, vr);
+            tmem_ld8_nowait(tbase + 32 + 8 * c, vu);
+            tmem_ld8_nowait(tbase + 64 + 8 * c, vx);
+            tmem_wait_ld();
+            reg_dep8(vr);
+            reg_dep8(vu);
+            reg_dep8(vx);
+            float(&b)[4][8] = gin[c & 1];
+            float o[8];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float rg = gru_sigm(erv[i] + vr[k + i]), ug = gru_sigm(euv[i] + vu[k + i]);
-                o[i] = ug * svv[i] + (1.f - ug) * tanhf(rg * vx[k + i] + ecv[i]);
-              }
-              *reinterpret_cast<float4*>(s1 + k) = make_float4(o[0], o[1], o[2], o[3]);
-              gru_store4(xo + k, ep.lo_x, o[0], o[1], o[2], o[3]);
+            for (int i = 0; i < 8; ++i) {
+              const float rg = gru_sigm(b[0][i] + vr[i]), ug = gru_sigm(b[1][i] + vu[i]);
+              o[i] = ug * b[3][i] + (1.f - ug) * tanhf(rg * vx[i] + b[2][i]);
+            }
+            if (c + 2 < 4) gru_fetch(c + 2, gin[c & 1]);
+            if (valid) {
+              st8(s1 + 8 * c, o);
+              gru_store4(xo + 8 * c, ep.lo_x, o[0], o[1], o[2], o[3]);
+              gru_store4(xo + 8 * c + 4, ep.lo_x, o[4], o[5], o[6], o[7]);
             }
           }
         } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
@@ -467,6 +512,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   }
   if (EPI == EPI_STORE && warp >= 2 && lane == 0) bulk_wait_all();
+  if (warp == 2 && lane == 0) GTRACE(6);
   __syncthreads();
   if constexpr (PAIR) cluster_sync();
   if (warp == 1) {
@@ -474,6 +520,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if constexpr (PAIR) tmem_dealloc_pair(tmem, 2 * BN);
     else tmem_dealloc(tmem, 2 * BN);
   }
+  if (threadIdx.x == 0) GTRACE(7);
 }
 
 // ------------------------------------------------------------------------------------- host side
@@ -565,6 +612,33 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = PAIR ? 2 : 1;
+#ifdef NMT_DIAG
+  if (getenv("NMT_GEMM_TRACE")) {  // (diagnostic) serialise, stamp every CTA's phases, print a summary
+    EpiParams et = ep;
+    CK(cudaMalloc(&et.trace, (size_t)grid * 8 * 8));
+    CK(cudaMemsetAsync(et.trace, 0, (size_t)grid * 8 * 8, st));
+    CK(cudaLaunchKernelEx(&cfg, k_gemm<BN, STAGES, EPI, PAIR>, a, b, c, g, et));
+    CK_LAUNCH();
+    std::vector<unsigned long long> h((size_t)grid * 8);
+    CK(cudaMemcpyAsync(h.data(), et.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFree(et.trace);
+    unsigned long long t0 = ~0ull;
+    for (int i = 0; i < grid; ++i) t0 = std::min(t0, h[(size_t)i * 8]);
+    fprintf(stderr, "[gemm_trace] BN=%d ST=%d EPI=%d PAIR=%d grid=%d nreg=%d ks=%d us from first entry (min/med/max):", BN,
+            STAGES, EPI, (int)PAIR, grid, g.nreg, g.ksplit);
+    for (int ev = 0; ev < 8; ++ev) {
+      std::vector<double> v;
+      for (int i = 0; i < grid; ++i)
+        if (h[(size_t)i * 8 + ev]) v.push_back((double)(h[(size_t)i * 8 + ev] - t0) * 1e-3);
+      if (v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      fprintf(stderr, " e%d %.1f/%.1f/%.1f", ev, v.front(), v[v.size() / 2], v.back());
+    }
+    fprintf(stderr, "\n");
+    return;
+  }
+#endif
   CK(cudaLaunchKernelEx(&cfg, k_gemm<BN, STAGES, EPI, PAIR>, a, b, c, g, ep));
   CK_LAUNCH();
 }

@@ -115,6 +115,7 @@ struct EpiParams {
   float* S1;           // [R][Hp] new state (fp32)
   __nv_bfloat16* X;    // [R][ldx] new state as the next GEMM's bf16 operand (lo at +lo_x if > 0)
   int ldx, lo_x, Hp;
+  unsigned long long* trace;  // diagnostic builds only (NMT_GEMM_TRACE): [CTA][8] globaltimer stamps
 };
 constexpr int kTopK = 8;  // NMT_TOPK_MAX: words per row kept by the top-k vocabulary epilogue
 
@@ -126,6 +127,10 @@ void gemm_store256(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& 
 // out[r][c] = bias[c] + sum_s part[s * stride + r * ldc + c]  (fixed order: deterministic)
 void splitk_reduce(const float* part, int ksplit, size_t stride, int M, int N, int ldc, const float* bias, float* out,
                    cudaStream_t st, __nv_bfloat16* out16 = nullptr);
+// the same for the attention keys: also out_e = exp(2 out) with the exponent clamped to +-kAttnExpClamp, and
+// bigp |= 1 where it was clamped
+void splitk_reduce_pctx(const float* part, int ksplit, size_t stride, int M, int N, int ldc, const float* bias,
+                        float* out, float* out_e, int* bigp, cudaStream_t st);
 void gemm_store_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float* out, int ldc,
                      int out_rows, const float* bias, int M_max, cudaStream_t st, size_t split_stride = 0);
 void gemm_topk_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float2* topk, int n_valid,

@@ -114,6 +114,35 @@ void splitk_reduce(const float* part, int ksplit, size_t stride, int M, int N, i
   CK_LAUNCH();
 }
 
+// exp(2 x) with the exponent clamped (attention keys/queries, D4: tanh(p + q) = 1 - 2 / (1 + e^2p e^2q));
+// returns whether it was clamped
+NMT_DEV float exp2x_clamped(float x, bool& big) {
+  const float y = 2.f * x;
+  big = fabsf(y) > kAttnExpClamp;
+  return expf(fminf(fmaxf(y, -kAttnExpClamp), kAttnExpClamp));
+}
+__global__ void k_splitk_reduce_pctx(const float* __restrict__ part, int ksplit, size_t stride, int M, int N, int ldc,
+                                     const float* __restrict__ bias, float* out, float* out_e, int* bigp) {
+  pdl_enter();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)M * N) return;
+  const int r = (int)(i / N), c = (int)(i % N);
+  float s = bias ? bias[c] : 0.f;
+  for (int k = 0; k < ksplit; ++k) s += part[k * stride + (size_t)r * ldc + c];
+  out[(size_t)r * ldc + c] = s;
+  bool big;
+  out_e[(size_t)r * ldc + c] = exp2x_clamped(s, big);
+  if (big) atomicOr(bigp, 1);
+}
+void splitk_reduce_pctx(const float* part, int ksplit, size_t stride, int M, int N, int ldc, const float* bias,
+                        float* out, float* out_e, int* bigp, cudaStream_t st) {
+  const int64_t n = (int64_t)M * N;
+  if (n <= 0) return;
+  launch_pdl(k_splitk_reduce_pctx, (unsigned)((n + 255) / 256), 256, 0, st, part, ksplit, stride, M, N, ldc, bias, out,
+             out_e, bigp);
+  CK_LAUNCH();
+}
+
 // ===================================================================================== planner
 // Device-side state cache (SURVEY §8(a) D0; PAPER.md:109 "collapsed edges", :121 "Cache state
 // pointers and probabilities at target nodes").  Keys (parent, word) -> child id in an open-
@@ -431,6 +460,7 @@ __global__ void k_ctx_reset(CtxDev c, int64_t hcap) {
     c.counters[CNT_SLOTS] = 2;  // slot 0 = s0, slot 1 = scratch
     c.counters[CNT_ERR] = 0;
     c.counters[CNT_R] = 0;
+    c.counters[CNT_BIGP] = 0;
     c.node_word[0] = -1;
     c.node_parent[0] = -1;
     c.node_src[0] = 0;
@@ -519,12 +549,22 @@ NMT_DEV float ld_sum(const float* p, int ks, int64_t stride) {
   return a;
 }
 
+NMT_DEV void prefetch_l2(const void* p, uint32_t bytes) {  // TMA-unit bulk prefetch into L2 (16-byte granules)
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __global__ void k_gather_state(StepDev d, const float* __restrict__ S) {
   pdl_enter();
   const int H4 = (d.H + 3) / 4;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = idx / H4, j = (idx % H4) * 4;
   if (r >= *d.R) return;
+  if (j == 0 && d.row_dst[r] >= 0) {  // the row's embedding projections, read by the GRU1 epilogue and the
+    const int y = d.row_y[r];          // readout: fetched into L2 now, under the GRU1 GEMM's main loop
+    const int64_t yr = y < 0 ? d.V : y;
+    prefetch_l2(d.Ex + yr * 3 * d.Hp, (uint32_t)(3 * d.Hp * sizeof(float)));
+    prefetch_l2(d.Eproj + yr * d.ROp, (uint32_t)(d.ROp * sizeof(float)));
+  }
   float4 v = make_float4(0.f, 0.f, 0.f, 0.f);  // dead rows of a multi-context step: zeros
   if (d.row_dst[r] >= 0) v = ld4((d.gs ? d.gs[d.row_grp[r]].S : S) + (int64_t)d.row_src[r] * d.Hp + j);
   store_split4(d.A_s + (int64_t)r * d.lda_s + j, d.lo_s, v);
@@ -583,20 +623,118 @@ NMT_DEV float warp_reduce_scatter32(float (&v)[32], int lane) {
   return v[0];
 }
 
-template <int RPB>
-__global__ void __launch_bounds__(256) k_attention(StepDev d, AttnCtx a) {
-  pdl_enter();
-  static_assert(RPB >= 1 && RPB <= 8, "rows per CTA");
+NMT_DEV float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// Energy pass of k_attention over positions [0, Tx): pctx or exp(2 pctx) slices of the thread's 8 columns
+// stream through a per-thread cp.async ring.
+//  tanh path (FAST = false): e_j = sum_k U_k tanh(p_jk + q_k), one SFU tanh per term.
+//  exp path (FAST = true): tanh(p + q) = 1 - 2 / (1 + e^2p e^2q), so with P = e^2p (per context) and
+//    Q = e^2q (per row) e_j = sum_k U_k - 2 sum_k U_k / (1 + P_jk Q_k); the constant cancels in the
+//    softmax.  Columns 0-3 of a thread take the reciprocal on the FMA pipe (bit-trick seed, negated, then
+//    one cubic Newton step r (1 + e + e^2), e = 1 - x r: |rel err| <= 5.1e-2 -> 1.3e-4, below
+//    tanh.approx's 2^-11) and columns 4-7 on the SFU (rcp.approx), so that both pipes finish together;
+//    the FMA work runs as packed fp32 pairs (FFMA2).  u2[0..1] = +2 U (they multiply -1/x), u2[2..3] = -2 U.
+template <int RPB, bool FAST>
+NMT_DEV void attn_energies(const float* pg, int Cp, int Tx, int nr, const float2 (&q2)[RPB][4],
+                           const float2 (&u2)[4], float4* mine, int rstride, int hoff, float* red, int warp, int lane,
+                           int Tx8) {
   constexpr int JB = RPB <= 4 ? 8 : 4;  // positions per reduce-scatter: JB x RPB <= 32 values
   constexpr int NST = 8;                // positions in flight
+  const float2 one2 = make_float2(1.f, 1.f);
+#pragma unroll
+  for (int i = 0; i < NST; ++i) {
+    if (i < Tx) {
+      cp_async16(mine + i * rstride, pg + (int64_t)i * Cp);
+      cp_async16(mine + i * rstride + hoff, pg + (int64_t)i * Cp + 4);
+    }
+    cp_async_commit();
+  }
+  for (int j0 = 0; j0 < Tx; j0 += JB) {
+    float e[32];  // e[jj * RPB + rr] partial energies of positions j0..j0+JB-1 (zero padded)
+#pragma unroll
+    for (int i = 0; i < 32; ++i) e[i] = 0.f;
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj) {
+      const int j = j0 + jj;
+      const int slot = j % NST;
+      cp_async_wait<NST - 1>();
+      const float4 n0 = mine[slot * rstride], n1 = mine[slot * rstride + hoff];
+      if (j + NST < Tx) {  // refill this slot with position j + NST
+        cp_async16(mine + slot * rstride, pg + (int64_t)(j + NST) * Cp);
+        cp_async16(mine + slot * rstride + hoff, pg + (int64_t)(j + NST) * Cp + 4);
+      }
+      cp_async_commit();
+#ifndef ATTN_NOCONT
+      if (j >= Tx) continue;  // (uniform: the tail of the last block of positions)
+#endif
+      const float2 p2[4] = {make_float2(n0.x, n0.y), make_float2(n0.z, n0.w), make_float2(n1.x, n1.y),
+                            make_float2(n1.z, n1.w)};
+#pragma unroll
+      for (int rr = 0; rr < RPB; ++rr) {
+        if (rr >= nr) continue;
+        if constexpr (FAST) {
+          float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {  // FMA-pipe reciprocals: rn = -1 / den
+            const float2 den = fma2(p2[k], q2[rr][k], one2);
+            const float2 r0 = make_float2(__int_as_float(0xFEF311C3u - __float_as_uint(den.x)),
+                                          __int_as_float(0xFEF311C3u - __float_as_uint(den.y)));
+            const float2 er = fma2(den, r0, one2);
+            const float2 rn = fma2(r0, fma2(er, er, er), r0);
+            acc = fma2(u2[k], rn, acc);
+          }
+#pragma unroll
+          for (int k = 2; k < 4; ++k) {  // SFU reciprocals
+            const float2 den = fma2(p2[k], q2[rr][k], one2);
+            acc = fma2(u2[k], make_float2(rcp_approx(den.x), rcp_approx(den.y)), acc);
+          }
+          e[jj * RPB + rr] = acc.x + acc.y;
+        } else {
+          float sacc = 0.f;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            sacc = fmaf(tanh_approx(p2[k].x + q2[rr][k].x), u2[k].x, sacc);
+            sacc = fmaf(tanh_approx(p2[k].y + q2[rr][k].y), u2[k].y, sacc);
+          }
+          e[jj * RPB + rr] = sacc;
+        }
+      }
+    }
+    const float tot = warp_reduce_scatter32(e, lane);  // lane = jj * RPB + rr
+    if (lane < JB * RPB) red[(warp * RPB + lane % RPB) * Tx8 + j0 + lane / RPB] = tot;
+  }
+  cp_async_wait<0>();
+}
+
+// D3-D5 attention.  Rows: with a multi-context step (d.gs) CTA b takes rows [RPB b, RPB b + RPB) (groups
+// start at multiples of 4); otherwise the R rows are split evenly over the grid (CTA b: rows
+// [R b / G, R (b + 1) / G)), so with two CTAs per SM every SM carries the same number of rows +-1.
+template <int RPB>
+__global__ void __launch_bounds__(256, 2) k_attention(StepDev d, AttnCtx a) {
+  pdl_enter();
+  static_assert(RPB >= 1 && RPB <= 8, "rows per CTA");
+  constexpr int NST = 8;
   const int R = *d.R;
-  const int r0 = blockIdx.x * RPB;
-  if (r0 >= R) return;
-  if (d.gs) {  // multi-context step: groups start at multiples of 4 rows and RPB divides 4
+  int r0, nr;
+  if (d.gs) {
+    r0 = blockIdx.x * RPB;
+    nr = min(RPB, R - r0);
+  } else {
+    r0 = (int)((int64_t)R * blockIdx.x / gridDim.x);
+    nr = (int)((int64_t)R * (blockIdx.x + 1) / gridDim.x) - r0;
+  }
+  if (nr <= 0) return;
+  const int* cnt = a.counters;
+  if (d.gs) {
     const GrpStep& g = d.gs[d.row_grp[r0]];
     a.pctx = g.pctx;
     a.ctx = g.ctx;
     a.Tx = g.Tx;
+    a.epctx = g.epctx;
+    cnt = g.counters;
   }
   const int Cp = d.Cp, Tx = a.Tx;
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -606,67 +744,53 @@ __global__ void __launch_bounds__(256) k_attention(StepDev d, AttnCtx a) {
   float* red = reinterpret_cast<float*>(ring + NST * blockDim.x * 2);  // [nw][RPB][Tx8]
   const int Tx8 = (Tx + 7) & ~7;
   float* alpha = red + nw * RPB * Tx8;                                  // [RPB][Tx]
+  // ring [NST][blockDim][2] float4: a thread's two 16-byte cp.async of a position fill one 32-byte chunk
+  // (measured: the [NST][2][blockDim] layout, conflict-free for the LDS.128 reads, is ~1.9x slower)
   float4* mine = ring + threadIdx.x * 2;
-  const int rstride = blockDim.x * 2;
+  const int rstride = blockDim.x * 2, hoff = 1;
   float q[RPB][8], u[8];
+  bool big = a.epctx == nullptr || cnt[CNT_BIGP] != 0;
+#ifdef NMT_DIAG
+  big |= d.diag_attn_slow != 0;  // (diagnostic A/B: force the tanh path)
+#endif
 #pragma unroll
   for (int rr = 0; rr < RPB; ++rr) {
-    const bool ok = r0 + rr < R;
+    const bool ok = rr < nr;
     const float* qp = d.Q + (int64_t)(r0 + rr) * Cp + c0;
     const float4 x0 = ok ? ld4_sum(qp, d.ks_q, d.ps_q) : make_float4(0, 0, 0, 0),
                  x1 = ok ? ld4_sum(qp + 4, d.ks_q, d.ps_q) : make_float4(0, 0, 0, 0);
     q[rr][0] = x0.x; q[rr][1] = x0.y; q[rr][2] = x0.z; q[rr][3] = x0.w;
     q[rr][4] = x1.x; q[rr][5] = x1.y; q[rr][6] = x1.z; q[rr][7] = x1.w;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) big |= fabsf(2.f * q[rr][k]) > kAttnExpClamp;
   }
   {
     const float4* up = reinterpret_cast<const float4*>(a.U_att + c0);
     const float4 x0 = up[0], x1 = up[1];
     u[0] = x0.x; u[1] = x0.y; u[2] = x0.z; u[3] = x0.w; u[4] = x1.x; u[5] = x1.y; u[6] = x1.z; u[7] = x1.w;
   }
-  const float* pg = a.pctx + c0;
-  // prologue: positions 0..NST-1 in flight (one commit group per position, possibly empty)
+  // exp path unless some exponent of this CTA's rows or of the context's keys had to be clamped
+  const bool fast = !__syncthreads_or(big);
+  {
+    float2 q2[RPB][4], u2[4];
 #pragma unroll
-  for (int i = 0; i < NST; ++i) {
-    if (i < Tx) {
-      cp_async16(mine + i * rstride, pg + (int64_t)i * Cp);
-      cp_async16(mine + i * rstride + 1, pg + (int64_t)i * Cp + 4);
+    for (int k = 0; k < 4; ++k) {
+      const float s = fast ? (k < 2 ? 2.f : -2.f) : 1.f;
+      u2[k] = make_float2(s * u[2 * k], s * u[2 * k + 1]);
+#pragma unroll
+      for (int rr = 0; rr < RPB; ++rr)
+        q2[rr][k] = fast ? make_float2(expf(2.f * q[rr][2 * k]), expf(2.f * q[rr][2 * k + 1]))
+                         : make_float2(q[rr][2 * k], q[rr][2 * k + 1]);
     }
-    cp_async_commit();
+    if (fast) attn_energies<RPB, true>(a.epctx + c0, Cp, Tx, nr, q2, u2, mine, rstride, hoff, red, warp, lane, Tx8);
+    else attn_energies<RPB, false>(a.pctx + c0, Cp, Tx, nr, q2, u2, mine, rstride, hoff, red, warp, lane, Tx8);
   }
-  for (int j0 = 0; j0 < Tx; j0 += JB) {
-    float e[32];  // e[jj * RPB + rr] partial energies of positions j0..j0+JB-1 (zero padded)
-#pragma unroll
-    for (int i = JB * RPB; i < 32; ++i) e[i] = 0.f;
-#pragma unroll
-    for (int jj = 0; jj < JB; ++jj) {
-      const int j = j0 + jj;
-      const int slot = j % NST;
-      cp_async_wait<NST - 1>();
-      const float4 n0 = mine[slot * rstride], n1 = mine[slot * rstride + 1];
-      // refill this slot with position j + NST
-      if (j + NST < Tx) {
-        cp_async16(mine + slot * rstride, pg + (int64_t)(j + NST) * Cp);
-        cp_async16(mine + slot * rstride + 1, pg + (int64_t)(j + NST) * Cp + 4);
-      }
-      cp_async_commit();
-      const float p[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
-#pragma unroll
-      for (int rr = 0; rr < RPB; ++rr) {
-        float s = 0.f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) s = fmaf(tanh_approx(p[k] + q[rr][k]), u[k], s);
-        e[jj * RPB + rr] = j < Tx ? s : 0.f;
-      }
-    }
-    const float tot = warp_reduce_scatter32(e, lane);  // lane = jj * RPB + rr
-    if (lane < JB * RPB) red[(warp * RPB + lane % RPB) * Tx8 + j0 + lane / RPB] = tot;
-  }
-  cp_async_wait<0>();
   __syncthreads();
-  for (int rr = warp; rr < RPB; rr += nw) {  // softmax over j for row rr
+  const float e0 = fast ? 0.f : a.c_tt;  // (a constant shift of all energies: no effect on alpha)
+  for (int rr = warp; rr < nr; rr += nw) {  // softmax over j for row rr
     float mx = -INFINITY;
     for (int j = lane; j < Tx; j += 32) {
-      float ev = a.c_tt;
+      float ev = e0;
       for (int w = 0; w < nw; ++w) ev += red[(w * RPB + rr) * Tx8 + j];
       alpha[rr * Tx + j] = ev;
       mx = fmaxf(mx, ev);
@@ -684,53 +808,67 @@ __global__ void __launch_bounds__(256) k_attention(StepDev d, AttnCtx a) {
     const float inv = 1.f / sum;
     for (int j = lane; j < Tx; j += 32) {
       alpha[rr * Tx + j] *= inv;
-      if (r0 + rr < R && d.alpha_out) d.alpha_out[(int64_t)(r0 + rr) * d.alpha_ld + j] = alpha[rr * Tx + j];
+      if (d.alpha_out) d.alpha_out[(int64_t)(r0 + rr) * d.alpha_ld + j] = alpha[rr * Tx + j];
     }
   }
   __syncthreads();
-  // context c = sum_j alpha_j ctx_j, ctx slices through the same ring
+  // context c = sum_j alpha_j ctx_j, ctx slices through the same ring (packed fp32 pairs)
   const float* cg = a.ctx + c0;
 #pragma unroll
   for (int i = 0; i < NST; ++i) {
     if (i < Tx) {
       cp_async16(mine + i * rstride, cg + (int64_t)i * Cp);
-      cp_async16(mine + i * rstride + 1, cg + (int64_t)i * Cp + 4);
+      cp_async16(mine + i * rstride + hoff, cg + (int64_t)i * Cp + 4);
     }
     cp_async_commit();
   }
-  float cacc[RPB][8];
+  float2 cacc[RPB][4];
 #pragma unroll
   for (int rr = 0; rr < RPB; ++rr)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) cacc[rr][k] = 0.f;
+    for (int k = 0; k < 4; ++k) cacc[rr][k] = make_float2(0.f, 0.f);
   for (int j = 0; j < Tx; ++j) {
     const int slot = j % NST;
     cp_async_wait<NST - 1>();
-    const float4 x0 = mine[slot * rstride], x1 = mine[slot * rstride + 1];
+    const float4 x0 = mine[slot * rstride], x1 = mine[slot * rstride + hoff];
     if (j + NST < Tx) {
       cp_async16(mine + slot * rstride, cg + (int64_t)(j + NST) * Cp);
-      cp_async16(mine + slot * rstride + 1, cg + (int64_t)(j + NST) * Cp + 4);
+      cp_async16(mine + slot * rstride + hoff, cg + (int64_t)(j + NST) * Cp + 4);
     }
     cp_async_commit();
-    const float cv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    const float2 cv[4] = {make_float2(x0.x, x0.y), make_float2(x0.z, x0.w), make_float2(x1.x, x1.y),
+                          make_float2(x1.z, x1.w)};
 #pragma unroll
     for (int rr = 0; rr < RPB; ++rr) {
-      const float al = alpha[rr * Tx + j];
+      if (rr < nr) {
+        const float al = alpha[rr * Tx + j];
+#ifdef ATTN_CTX_SCALAR
 #pragma unroll
-      for (int k = 0; k < 8; ++k) cacc[rr][k] = fmaf(al, cv[k], cacc[rr][k]);
+        for (int k = 0; k < 4; ++k) {
+          cacc[rr][k].x = fmaf(al, cv[k].x, cacc[rr][k].x);
+          cacc[rr][k].y = fmaf(al, cv[k].y, cacc[rr][k].y);
+        }
+#else
+        const float2 al2 = make_float2(al, al);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cacc[rr][k] = fma2(al2, cv[k], cacc[rr][k]);
+#endif
+      }
     }
   }
   cp_async_wait<0>();
 #pragma unroll
   for (int rr = 0; rr < RPB; ++rr) {
+    if (rr >= nr) break;
     const int r = r0 + rr;
-    if (r >= R) break;
     float4* o = reinterpret_cast<float4*>(d.Cf + (int64_t)r * Cp + c0);
-    o[0] = make_float4(cacc[rr][0], cacc[rr][1], cacc[rr][2], cacc[rr][3]);
-    o[1] = make_float4(cacc[rr][4], cacc[rr][5], cacc[rr][6], cacc[rr][7]);
+    const float4 v0 = make_float4(cacc[rr][0].x, cacc[rr][0].y, cacc[rr][1].x, cacc[rr][1].y);
+    const float4 v1 = make_float4(cacc[rr][2].x, cacc[rr][2].y, cacc[rr][3].x, cacc[rr][3].y);
+    o[0] = v0;
+    o[1] = v1;
     __nv_bfloat16* xp = d.X + (int64_t)r * d.ldx + d.Hp + c0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) store_split(xp + k, d.lo_x, cacc[rr][k]);
+    store_split4(xp, d.lo_x, v0);
+    store_split4(xp + 4, d.lo_x, v1);
   }
 }
 
@@ -973,6 +1111,29 @@ void path_sum(const float* logp, const int* child, const int* off, const int* po
   CK_LAUNCH();
 }
 
+// L2 prefetch of the decoder's weight matrices (issued at the start of a decoder call, before the
+// planner): the bulk prefetches only queue DRAM reads, so the planner and the state gather overlap
+// them and the decoder GEMMs' TMA loads hit L2 instead of waiting on HBM latency.
+__global__ void k_prefetch_l2(PrefetchList pl) {
+  pdl_enter();
+  constexpr uint32_t kChunk = 16u << 10;
+  for (int i = 0; i < pl.n; ++i) {
+    const char* b = static_cast<const char*>(pl.ptr[i]);
+    const size_t nchunk = (pl.bytes[i] + kChunk - 1) / kChunk;
+    for (size_t c = threadIdx.x + (size_t)blockIdx.x * blockDim.x; c < nchunk; c += (size_t)gridDim.x * blockDim.x) {
+      const size_t off = c * kChunk;
+      const size_t len = pl.bytes[i] - off < kChunk ? pl.bytes[i] - off : kChunk;
+      prefetch_l2(b + off, (uint32_t)(len & ~(size_t)15));
+    }
+  }
+}
+void prefetch_weights_l2(const PrefetchList& pl, cudaStream_t st) {
+  if (pl.n <= 0) return;
+  // spread over every SM: each SM's TMA unit works through its own share of the prefetches
+  launch_pdl(k_prefetch_l2, 2 * kNumSMs, 32, 0, st, pl);
+  CK_LAUNCH();
+}
+
 // full log-prob row of one stepped slot (test export)
 __global__ void k_full_row(const float* __restrict__ T, const float* __restrict__ Wo32, const float* __restrict__ bo,
                            const float* __restrict__ logZ, int slot, int Ep, int V, float* out) {
@@ -996,12 +1157,12 @@ size_t attention_smem_bytes(int Cp, int Tx, int rpb) {
 }
 
 template <int RPB>
-static void launch_attention(const StepDev& d, const AttnCtx& a, int R_max, cudaStream_t st) {
+static void launch_attention(const StepDev& d, const AttnCtx& a, int grid, cudaStream_t st) {
   const int nthr = d.Cp / 8;
   const size_t smem = attention_smem_bytes(d.Cp, a.Tx, RPB);
   static std::atomic<size_t> attr[kMaxDevices];  // > 48 KB of dynamic shared memory needs the opt-in
   ensure_smem_attr(k_attention<RPB>, attr, smem);
-  launch_pdl(k_attention<RPB>, (R_max + RPB - 1) / RPB, nthr, smem, st, d, a);
+  launch_pdl(k_attention<RPB>, grid, nthr, smem, st, d, a);
 }
 
 void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, float* T, float* logZ, int* amax,
@@ -1016,25 +1177,27 @@ void step_elementwise(int which, const StepDev& d, const AttnCtx& a, float* S, f
     case EW_GATHER: launch_pdl(k_gather_state, gh, 256, 0, st, d, S); break;
     case EW_GRU1: launch_pdl(k_gru1, gh, 256, 0, st, d, S); break;
     case EW_ATTN: {
-      // one wave: rows per CTA = ceil(R / SMs) (<= 8), so every SM carries the same number of rows
 #ifdef NMT_DIAG
-      static const int rpb_env = getenv("NMT_ATTN_RPB") ? atoi(getenv("NMT_ATTN_RPB")) : 0;  // (diagnostic)
-#else
-      constexpr int rpb_env = 0;
+      const_cast<StepDev&>(d).diag_attn_slow = getenv("NMT_ATTN_SLOW") ? 1 : 0;
 #endif
-      // rows per CTA: ceil(R / SMs), at most 4 (measured in the step at R = 1024: 4 rows x 256 CTAs is
-      // ~28 us faster than one wave of 7-row CTAs, whose single CTA per SM hides less latency)
-      int rpb = rpb_env > 0 ? std::min(8, rpb_env) : std::max(1, std::min(4, (R_max + kNumSMs - 1) / kNumSMs));
-      if (d.gs && (rpb == 3 || rpb > 4)) rpb = 4;  // multi-context rows: CTAs must not straddle a group
+      int rpb, grid;
+      if (d.gs) {  // multi-context rows: 4-row blocks must not straddle a group (groups start at multiples of 4)
+        rpb = std::max(1, std::min(4, (R_max + kNumSMs - 1) / kNumSMs));
+        if (rpb == 3) rpb = 4;
+        grid = (R_max + rpb - 1) / rpb;
+      } else {  // rows split evenly over two CTAs per SM (<= 4 rows each; more CTAs beyond 8 rows per SM)
+        grid = std::min(R_max, 2 * kNumSMs);
+        rpb = (R_max + grid - 1) / grid;
+        if (rpb > 4) {
+          rpb = 4;
+          grid = (R_max + 3) / 4;
+        }
+      }
       switch (rpb) {
-        case 1: launch_attention<1>(d, a, R_max, st); break;
-        case 2: launch_attention<2>(d, a, R_max, st); break;
-        case 3: launch_attention<3>(d, a, R_max, st); break;
-        case 4: launch_attention<4>(d, a, R_max, st); break;
-        case 5: launch_attention<5>(d, a, R_max, st); break;
-        case 6: launch_attention<6>(d, a, R_max, st); break;
-        case 7: launch_attention<7>(d, a, R_max, st); break;
-        default: launch_attention<8>(d, a, R_max, st); break;
+        case 1: launch_attention<1>(d, a, grid, st); break;
+        case 2: launch_attention<2>(d, a, grid, st); break;
+        case 3: launch_attention<3>(d, a, grid, st); break;
+        default: launch_attention<4>(d, a, grid, st); break;
       }
       break;
     }
@@ -1206,14 +1369,6 @@ void full_row(const float* T, const float* Wo32, const float* bo, const float* l
 // Tail (E5): each CTA publishes the time-mean of its units, one grid barrier, then the CTAs split
 // s0 = tanh(mean . W_init + b_init); their W_init rows are prefetched into shared memory at start.
 // The kernel also writes the bf16 hi|lo copy of ctx (E7 input) and the new context's counters.
-__device__ __forceinline__ void ffma2(float2& acc, float2 a, float2 b) {
-  unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(d)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
-        "l"(*reinterpret_cast<unsigned long long*>(&acc)));
-  acc = *reinterpret_cast<float2*>(&d);
-}
 __device__ __forceinline__ float sigmoid_fast(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
 __device__ __forceinline__ float tanh_fast(float x) {  // |err| ~ 1e-7 (not tanh.approx)
   const float e = __expf(2.f * fminf(fmaxf(x, -15.f), 15.f));
@@ -1876,6 +2031,11 @@ __global__ void k_encb_pctx(EncBatchDev e, const float* __restrict__ P, int ks, 
   const float4 bb = ld4(e.b_att + k);
   v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
   st4(e.pctx[b] + (int64_t)pos * Cp + k, v);
+  bool b0, b1, b2, b3;
+  const float4 ev = make_float4(exp2x_clamped(v.x, b0), exp2x_clamped(v.y, b1), exp2x_clamped(v.z, b2),
+                                exp2x_clamped(v.w, b3));
+  st4(e.epctx[b] + (int64_t)pos * Cp + k, ev);
+  if (b0 | b1 | b2 | b3) atomicOr(e.cnt[b] + CNT_BIGP, 1);
 }
 
 // context (re)initialisation of n arenas in one launch (k_ctx_reset per blockIdx.y)
@@ -1893,6 +2053,7 @@ __global__ void k_ctx_reset_many(const CtxDev* __restrict__ cs, const int64_t* _
     c.counters[CNT_SLOTS] = 2;
     c.counters[CNT_ERR] = 0;
     c.counters[CNT_R] = 0;
+    c.counters[CNT_BIGP] = 0;
     c.node_word[0] = -1;
     c.node_parent[0] = -1;
     c.node_src[0] = 0;

@@ -4,7 +4,10 @@
 
 namespace nmt {
 
-enum { CNT_NODES = 0, CNT_SLOTS = 1, CNT_ERR = 2, CNT_R = 3, CNT_N = 4 };
+// CNT_BIGP: set (atomicOr) by the pctx producers when some |2 pctx| > kAttnExpClamp, i.e. exp(2 pctx) was
+// clamped; the attention then takes its tanh path for the context (reset with the context)
+enum { CNT_NODES = 0, CNT_SLOTS = 1, CNT_ERR = 2, CNT_R = 3, CNT_BIGP = 4, CNT_N = 5 };
+constexpr float kAttnExpClamp = 43.f;  // exp(+-43)^2 stays inside the normal fp32 range
 enum { ERR_BAD_STATE = 1, ERR_TOKEN = 2, ERR_OFFSETS = 4 };
 
 // Per-context device arena + node table + (parent, word) -> child hash (the state cache).
@@ -53,6 +56,8 @@ struct GrpStep {
   const float* pctx;
   const float* ctx;
   int Tx;
+  const float* epctx;  // exp(2 pctx) (clamped) [Tx][Cp]
+  const int* counters;  // the context's counters (CNT_BIGP)
 };
 
 // Planner / gather-dot descriptor of one context of a multi-context call (blockIdx.y = group).
@@ -94,7 +99,15 @@ struct StepDev {
                                          // argmax) of this rank's vocabulary slice here (else null)
   int ks_g1, ks_q, ks_g2[3], ks_ro;      // split-K partial counts of the decoder GEMM outputs
   int64_t ps_g1, ps_q, ps_g2, ps_ro;     // floats between consecutive partials
+  int diag_attn_slow;                    // (diagnostic builds: force the attention's tanh path)
 };
+
+struct PrefetchList {  // device ranges to pull into L2 ahead of use (16-byte aligned)
+  int n;
+  const void* ptr[8];
+  size_t bytes[8];
+};
+void prefetch_weights_l2(const PrefetchList& pl, cudaStream_t st);
 
 struct AttnCtx {
   const float* pctx;   // [Tx][Cp]
@@ -102,6 +115,8 @@ struct AttnCtx {
   const float* U_att;  // [Cp]
   float c_tt;
   int Tx;
+  const float* epctx;   // [Tx][Cp] exp(2 pctx), exponent clamped to +-kAttnExpClamp
+  const int* counters;  // the context's counters (CNT_BIGP: some exponent was clamped)
 };
 
 struct EncDev {
@@ -139,6 +154,8 @@ struct EncBatchDev {
   __nv_bfloat16* Am;     // [n][4Hp] mean ctx hi | lo (s0 GEMM operand)
   float* const* ctx;     // [n] per-sentence ctx [Tx][Cp]
   float* const* pctx;    // [n] per-sentence pctx [Tx][Cp]
+  float* const* epctx;   // [n] per-sentence exp(2 pctx) [Tx][Cp] (clamped)
+  int* const* cnt;       // [n] per-sentence counters (CNT_BIGP)
   float* const* S0;      // [n] slot 0 of each sentence's state arena
   const float* b_init;   // [H]
   const float* b_att;    // [Cp]

@@ -28,6 +28,9 @@ def main(path: str, out_json: str) -> None:
     starts = [i for i, (n, _) in enumerate(launches) if n.startswith("k_enc_recur")]
     i0 = starts[-2] if len(starts) >= 2 else starts[-1]
     i1 = starts[-1] if len(starts) >= 2 else len(launches)
+    if "--step" in sys.argv:  # the k-th step of the list (bench.py appends its variants' steps after the headline's)
+        k = int(sys.argv[sys.argv.index("--step") + 1])
+        i0, i1 = starts[k], starts[k + 1]
     # a step = the launches from one encoder recurrence to the next (encode + inject + score)
     step = [x for x in launches[i0 - 1:i1 - 1] if not x[0].startswith("torch:")]
     tot = sum(t for _, t in step)
@@ -49,4 +52,4 @@ def main(path: str, out_json: str) -> None:
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])  # [--seq]: also print the step's launches in order
+    main(sys.argv[1], sys.argv[2])  # [--seq]: also print the step's launches in order; [--step k]: the k-th step
