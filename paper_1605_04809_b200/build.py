@@ -27,14 +27,16 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False, diag: bool = False, variant: str = "",
           defines: tuple = ()) -> str:
     """diag: a separate libnmt_diag.so with the -DNMT_DIAG switches (stage skipping, traces, ...) for
-    measurements only; the product library ignores the environment.  variant + defines: a diagnostic
-    A/B build libnmt_diag_<variant>.so with extra -D flags."""
+    measurements only; the product library ignores the environment.  variant + defines: an A/B build
+    libnmt_var_<variant>.so (libnmt_diag_<variant>.so with diag) with extra -D flags, for measurements."""
     if variant:
-        diag = True
-    lib = os.path.join(HERE, f"libnmt_diag_{variant}.so" if variant else "libnmt_diag.so") if diag else LIB
-    if not diag and not force and not _stale():
+        lib = os.path.join(HERE, f"libnmt_{'diag' if diag else 'var'}_{variant}.so")
+        bdir = os.path.join(BUILD, f"{'diag' if diag else 'var'}_{variant}")
+    else:
+        lib = os.path.join(HERE, "libnmt_diag.so") if diag else LIB
+        bdir = os.path.join(BUILD, "diag") if diag else BUILD
+    if not diag and not variant and not force and not _stale():
         return LIB
-    bdir = os.path.join(BUILD, "diag" + (f"_{variant}" if variant else "")) if diag else BUILD
     os.makedirs(bdir, exist_ok=True)
 
     def compile_one(src: str) -> str:

@@ -1431,31 +1431,9 @@ static PlanIO plan_io(nmt_model* m, int np, int nc, const int* par, const int* o
   return io;
 }
 
-// Pull the decoder GEMMs' weight matrices (bf16: 43 MB at En->Ru) into L2 at the start of a decoder
-// call: the planner and the state gather run while HBM streams them, so the GEMMs' first TMA loads and
-// their steady-state B stages hit L2 (measured per-GEMM phase stamps).  Skipped when the
-// matrices would take more than half of the 126 MB L2 (the vocabulary GEMM streams W_o through it).
-static void prefetch_decoder(nmt_model* m, bool fused_h1, cudaStream_t st) {
-  const size_t sf = m->split ? 2 : 1, Hp = m->Hp, Cp = m->Cp;
-  PrefetchList pl{};
-  auto add = [&](const void* p, size_t bytes) {
-    pl.ptr[pl.n] = p;
-    pl.bytes[pl.n++] = bytes;
-  };
-  if (fused_h1) add(m->W_h1g, 4 * Hp * sf * Hp * 2);
-  else add(m->W_h1, 3 * Hp * sf * Hp * 2);
-  add(m->W_q, Cp * sf * Hp * 2);
-  add(m->W_g2, 4 * Hp * sf * (Hp + Cp) * 2);
-  add(m->W_ro, (size_t)m->ROp * sf * (Cp + Hp) * 2);
-  size_t tot = 0;
-  for (int i = 0; i < pl.n; ++i) tot += pl.bytes[i];
-  if (tot <= ((size_t)63 << 20)) prefetch_weights_l2(pl, st);
-}
-
 static void run_call(nmt_model* m, nmt_ctx* c, const PlanIO& io, float* out_logp, int* out_child,
                      long long* out_child64, int* out_amax) {
   const CtxDev cd = c->dev();
-  if (io.n_par > 0) prefetch_decoder(m, m->use_pair, m->st);
   {
     ProfScope p_(m, ST_PLAN);
     plan(cd, io, c->counters + CNT_R, m->st);
@@ -2135,7 +2113,6 @@ nmt_status nmt_beam_step(nmt_ctx* c, int32_t np, const nmt_state* parents, int32
       CK(cudaMemsetAsync(m->in_off, 0, (size_t)(np + 1) * 4, st));
       PlanIO io = plan_io(m, np, 0, m->in_par, m->in_off, m->in_words);
       io.step_all = 1;
-      prefetch_decoder(m, m->use_pair, st);
       {
         ProfScope p_(m, ST_PLAN);
         plan(cd, io, c->counters + CNT_R, st);
@@ -2502,7 +2479,6 @@ nmt_status nmt_score_batch_multi(int32_t np, nmt_ctx* const* cpp, const nmt_stat
     CK(cudaMemcpyAsync(d_R, hR, (size_t)(1 + total_rows) * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(m->mws_b, hdesc, need_b, cudaMemcpyHostToDevice, st));
     fill_i32(m->row_dst, total_rows, -1, st);
-    if (total_rows > 0) prefetch_decoder(m, false, st);  // (multi-context steps use GEMM + k_gru1)
     {
       ProfScope p_(m, ST_PLAN);
       plan_multi(d_desc, G, max_nc, max_np, st);

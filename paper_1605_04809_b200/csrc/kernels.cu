@@ -1111,29 +1111,6 @@ void path_sum(const float* logp, const int* child, const int* off, const int* po
   CK_LAUNCH();
 }
 
-// L2 prefetch of the decoder's weight matrices (issued at the start of a decoder call, before the
-// planner): the bulk prefetches only queue DRAM reads, so the planner and the state gather overlap
-// them and the decoder GEMMs' TMA loads hit L2 instead of waiting on HBM latency.
-__global__ void k_prefetch_l2(PrefetchList pl) {
-  pdl_enter();
-  constexpr uint32_t kChunk = 16u << 10;
-  for (int i = 0; i < pl.n; ++i) {
-    const char* b = static_cast<const char*>(pl.ptr[i]);
-    const size_t nchunk = (pl.bytes[i] + kChunk - 1) / kChunk;
-    for (size_t c = threadIdx.x + (size_t)blockIdx.x * blockDim.x; c < nchunk; c += (size_t)gridDim.x * blockDim.x) {
-      const size_t off = c * kChunk;
-      const size_t len = pl.bytes[i] - off < kChunk ? pl.bytes[i] - off : kChunk;
-      prefetch_l2(b + off, (uint32_t)(len & ~(size_t)15));
-    }
-  }
-}
-void prefetch_weights_l2(const PrefetchList& pl, cudaStream_t st) {
-  if (pl.n <= 0) return;
-  // spread over every SM: each SM's TMA unit works through its own share of the prefetches
-  launch_pdl(k_prefetch_l2, 2 * kNumSMs, 32, 0, st, pl);
-  CK_LAUNCH();
-}
-
 // full log-prob row of one stepped slot (test export)
 __global__ void k_full_row(const float* __restrict__ T, const float* __restrict__ Wo32, const float* __restrict__ bo,
                            const float* __restrict__ logZ, int slot, int Ep, int V, float* out) {

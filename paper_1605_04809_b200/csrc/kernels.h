@@ -102,13 +102,6 @@ struct StepDev {
   int diag_attn_slow;                    // (diagnostic builds: force the attention's tanh path)
 };
 
-struct PrefetchList {  // device ranges to pull into L2 ahead of use (16-byte aligned)
-  int n;
-  const void* ptr[8];
-  size_t bytes[8];
-};
-void prefetch_weights_l2(const PrefetchList& pl, cudaStream_t st);
-
 struct AttnCtx {
   const float* pctx;   // [Tx][Cp]
   const float* ctx;    // [Tx][Cp]
