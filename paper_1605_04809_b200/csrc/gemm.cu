@@ -163,363 +163,417 @@ NMT_DEV void gru_store4(__nv_bfloat16* p, int lo_off, float a, float b, float c,
   } while (0)
 #endif
 
+// Per-CTA view of the engine's shared memory, barriers and TMEM, and the roles' pipeline positions
+// (a role function called twice in one launch would continue the same stage ring).
 template <int BN, int STAGES, int EPI, bool PAIR>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const __grid_constant__ CUtensorMap tmC, GemmShape g, EpiParams ep) {
+struct GemmCta {
   using S = GemmSmem<BN, STAGES, EPI, PAIR>;
-  constexpr int CM = PAIR ? 2 * BM : BM;  // rows of a tile (per CTA pair)
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * S::A_BYTES;
-  uint8_t* sC = sB + STAGES * S::B_BYTES;  // (1024-aligned: A/B stage sizes are multiples of 1 KB)
-  uint64_t* full = reinterpret_cast<uint64_t*>(sC + S::C_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  static constexpr int CM = PAIR ? 2 * BM : BM;  // rows of a tile (per CTA pair)
+  uint8_t *sA, *sB, *sC;
+  uint64_t *full, *empty, *tfull, *tempty;
+  uint32_t* tmem_slot;
+  uint32_t tmem;
+  int warp, lane;
+  uint32_t rank;
+  bool leader;
+  int unit, nunits;
+  // pipeline positions (each used by one role)
+  int p_stage = 0, m_stage = 0, m_it = 0, e_it = 0;
+  uint32_t p_phase = 0, m_phase = 0;
 
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
-  const bool leader = rank == 0;
-  if (threadIdx.x == 0) GTRACE(0);
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
-    if (EPI == EPI_STORE) tma_prefetch(&tmC);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], PAIR ? 2 : 1);  // (pair: the leader's expect_tx arrive + the peer's remote arrive)
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], (PAIR ? 2 : 1) * EPI_WARPS);
-    }
-    fence_barrier_init();
+  NMT_DEV void carve(uint8_t* smem_raw) {
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    sA = smem;
+    sB = smem + STAGES * S::A_BYTES;
+    sC = sB + STAGES * S::B_BYTES;  // (1024-aligned: A/B stage sizes are multiples of 1 KB)
+    full = reinterpret_cast<uint64_t*>(sC + S::C_BYTES);
+    empty = full + STAGES;
+    tfull = empty + STAGES;
+    tempty = tfull + 2;
+    tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    warp = threadIdx.x >> 5;
+    lane = threadIdx.x & 31;
+    rank = PAIR ? cluster_ctarank() : 0;
+    leader = rank == 0;
+    unit = PAIR ? blockIdx.x / 2 : blockIdx.x;
+    nunits = PAIR ? gridDim.x / 2 : gridDim.x;
   }
-  if (warp == 1) {
-    if constexpr (PAIR) tmem_alloc_pair(tmem_slot, 2 * BN);
-    else tmem_alloc(tmem_slot, 2 * BN);
+  // barrier init (warp 0) and TMEM allocation (warp 1), then a CTA / cluster barrier
+  NMT_DEV void setup() {
+    if (warp == 0 && lane == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&full[s], PAIR ? 2 : 1);  // (pair: the leader's expect_tx arrive + the peer's remote arrive)
+        mbar_init(&empty[s], 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        mbar_init(&tfull[a], 1);
+        mbar_init(&tempty[a], (PAIR ? 2 : 1) * EPI_WARPS);
+      }
+      fence_barrier_init();
+    }
+    if (warp == 1) {
+      if constexpr (PAIR) tmem_alloc_pair(tmem_slot, 2 * BN);
+      else tmem_alloc(tmem_slot, 2 * BN);
+    }
+    tc_fence_before();
+    if constexpr (PAIR) cluster_sync();
+    else __syncthreads();
+    tc_fence_after();
+    tmem = *tmem_slot;
   }
-  tc_fence_before();
-  if constexpr (PAIR) cluster_sync();
-  else __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) GTRACE(1);
-  pdl_enter();  // prologue above overlaps the previous kernel; inputs (and M_dev) are read below
-  if (threadIdx.x == 0) GTRACE(2);
-  const int M = g.M_dev ? *g.M_dev : g.M;
-  const int unit = PAIR ? blockIdx.x / 2 : blockIdx.x, nunits = PAIR ? gridDim.x / 2 : gridDim.x;
-  const Sched sc = make_sched<EPI>(g, M, CM, BN, nunits);
-  if ((EPI == EPI_LSE || EPI == EPI_TOPK) && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
+  NMT_DEV void teardown() {
+    __syncthreads();
+    if constexpr (PAIR) cluster_sync();
+    if (warp == 1) {
+      tc_fence_after();
+      if constexpr (PAIR) tmem_dealloc_pair(tmem, 2 * BN);
+      else tmem_dealloc(tmem, 2 * BN);
+    }
+  }
+};
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer (both CTAs of a pair)
-      const uint32_t full0 = PAIR ? mapa_shared(smem_u32(full), 0) : 0;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int w = unit; w < sc.items; w += nunits) {
-        const Item itm = sc.item(w);
-        for (int n = itm.n0; n < itm.n1; ++n) {
-          const TileCoord tc{itm.m, n, itm.s};
-          const RegionK rk = region_of(g, tc.n * BN);
-          const int nkbp = rk.k1 - rk.k0, nkb = g.passes * nkbp;
-          const int chunk = (nkb + rk.ks - 1) / rk.ks;
-          const int i1 = min(nkb, (tc.s + 1) * chunk);
-          for (int i = tc.s * chunk; i < i1; ++i) {
-            const int pass = i / nkbp, kb = rk.k0 + i % nkbp;
-            const int aoff = g.a_col0 + (pass == 2 ? g.a_lo_off : 0);
-            const int boff = (pass == 1 ? g.b_lo_off : 0);
-            mbar_wait(&empty[stage], phase ^ 1);
-            const int arow = tc.m * CM + rank * BM, brow = tc.n * BN + rank * S::B_ROWS + g.n_off;
-            const int bx = g.b_panel_rows ? 0 : boff + kb * BK;
-            const int by = g.b_panel_rows ? (boff / BK + kb) * g.b_panel_rows + brow : brow;
-            if constexpr (PAIR) {
-              if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (S::A_BYTES + S::B_BYTES));
-              else mbar_arrive_cluster(full0 + stage * 8);
-              tma_load_2d_pair(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, arow);
-              tma_load_2d_pair(&tmB, &full[stage], sB + stage * S::B_BYTES, bx, by);
-            } else {
-              mbar_arrive_expect_tx(&full[stage], S::A_BYTES + S::B_BYTES);
-              tma_load_2d(&tmA, &full[stage], sA + stage * S::A_BYTES, aoff + kb * BK, arow);
-              tma_load_2d(&tmB, &full[stage], sB + stage * S::B_BYTES, bx, by);
-            }
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
+// ---- TMA producer (one lane per CTA; both CTAs of a pair load their halves)
+template <int BN, int STAGES, int EPI, bool PAIR>
+NMT_DEV void gemm_produce(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap* tmA, const CUtensorMap* tmB,
+                          const GemmShape& g, const Sched& sc) {
+  using S = GemmSmem<BN, STAGES, EPI, PAIR>;
+  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR>::CM;
+  const uint32_t full0 = PAIR ? mapa_shared(smem_u32(cx.full), 0) : 0;
+  for (int w = cx.unit; w < sc.items; w += cx.nunits) {
+    const Item itm = sc.item(w);
+    for (int n = itm.n0; n < itm.n1; ++n) {
+      const TileCoord tc{itm.m, n, itm.s};
+      const RegionK rk = region_of(g, tc.n * BN);
+      const int nkbp = rk.k1 - rk.k0, nkb = g.passes * nkbp;
+      const int chunk = (nkb + rk.ks - 1) / rk.ks;
+      const int i1 = min(nkb, (tc.s + 1) * chunk);
+      for (int i = tc.s * chunk; i < i1; ++i) {
+        const int pass = i / nkbp, kb = rk.k0 + i % nkbp;
+        const int aoff = g.a_col0 + (pass == 2 ? g.a_lo_off : 0);
+        const int boff = (pass == 1 ? g.b_lo_off : 0);
+        const int stage = cx.p_stage;
+        mbar_wait(&cx.empty[stage], cx.p_phase ^ 1);
+        const int arow = tc.m * CM + cx.rank * BM, brow = tc.n * BN + cx.rank * S::B_ROWS + g.n_off;
+        const int bx = g.b_panel_rows ? 0 : boff + kb * BK;
+        const int by = g.b_panel_rows ? (boff / BK + kb) * g.b_panel_rows + brow : brow;
+        if constexpr (PAIR) {
+          if (cx.leader) mbar_arrive_expect_tx(&cx.full[stage], 2 * (S::A_BYTES + S::B_BYTES));
+          else mbar_arrive_cluster(full0 + stage * 8);
+          tma_load_2d_pair(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK, arow);
+          tma_load_2d_pair(tmB, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
+        } else {
+          mbar_arrive_expect_tx(&cx.full[stage], S::A_BYTES + S::B_BYTES);
+          tma_load_2d(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK, arow);
+          tma_load_2d(tmB, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
+        }
+        if (++cx.p_stage == STAGES) {
+          cx.p_stage = 0;
+          cx.p_phase ^= 1;
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ---------------- MMA issuer (the pair's leader)
-      constexpr uint32_t idesc = idesc_bf16(CM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int w = unit; w < sc.items; w += nunits) {
-        const Item itm = sc.item(w);
-        for (int n = itm.n0; n < itm.n1; ++n, ++it) {
-          const TileCoord tc{itm.m, n, itm.s};
-          const RegionK rk = region_of(g, tc.n * BN);
-          const int acc = it & 1;
-          const uint32_t aph = (it >> 1) & 1;
-          mbar_wait(&tempty[acc], aph ^ 1);
-          tc_fence_after();
-          const uint32_t d = tmem + acc * BN;
-          const int nkb_all = g.passes * (rk.k1 - rk.k0);
-          const int chunk = (nkb_all + rk.ks - 1) / rk.ks;
-          const int nkb = min(nkb_all, (tc.s + 1) * chunk) - tc.s * chunk;
-          for (int i = 0; i < nkb; ++i) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            if (it == 0 && i == 0) GTRACE(3);
-            const uint32_t a0 = smem_u32(sA + stage * S::A_BYTES);
-            const uint32_t b0 = smem_u32(sB + stage * S::B_BYTES);
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-              if constexpr (PAIR)
-                mma_bf16_pair(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
-              else
-                mma_bf16(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
-            }
-            if constexpr (PAIR) mma_commit_pair(&empty[stage]);
-            else mma_commit(&empty[stage]);
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-          if constexpr (PAIR) mma_commit_pair(&tfull[acc]);
-          else mma_commit(&tfull[acc]);
-        }
-      }
-      GTRACE(4);
-    }
-  } else {  // ---------------- epilogue warps 2..9 (each CTA: its 128 rows of the tile)
-    const int q = warp & 3;               // TMEM lane quadrant accessible to this warp
-    const int half = (warp - 2) >> 2;     // which half of the tile's columns
-    constexpr int COLS = BN / 2;
-    const int row_in_tile = q * 32 + lane;
-    const uint32_t tempty0 = PAIR ? mapa_shared(smem_u32(tempty), 0) : 0;
-    int it = 0;
-    for (int w = unit; w < sc.items; w += nunits) {
-      const Item itm = sc.item(w);
-      const int grow = itm.m * CM + rank * BM + row_in_tile;
-      const bool valid = grow < M;
-      constexpr float LOG2E = 1.4426950408889634f;
-      float mx = -INFINITY, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // LSE running state (per run)
-      int am = 0;
-      float tv[EPI == EPI_TOPK ? kTopK : 1];  // TOPK: best logits of the run, descending (ties: lower column)
-      int ti[EPI == EPI_TOPK ? kTopK : 1];
-      if constexpr (EPI == EPI_TOPK) {
-#pragma unroll
-        for (int q = 0; q < kTopK; ++q) {
-          tv[q] = -INFINITY;
-          ti[q] = INT32_MAX;
-        }
-      }
-      for (int n = itm.n0; n < itm.n1; ++n, ++it) {
-        const int acc = it & 1;
-        const uint32_t aph = (it >> 1) & 1;
-        const int colbase = n * BN + half * COLS;
-        // EPI_GRU: this warp's COLS = 128 columns are one 32-unit group [r | u | h~ | pad] of its row, done
-        // in 4 chunks of 8 units.  A chunk's gx (r, u, x) and previous-state values arrive as 256-bit loads
-        // (full 32-byte sectors) issued two chunks ahead; the first two are issued before the accumulator
-        // wait, so their latency hides under the main loop.
-        float gin[EPI == EPI_GRU ? 2 : 1][4][8];
-        const float* gxr = nullptr;
-        const float* sp = nullptr;
-        auto gru_fetch = [&](int c, float(&b)[4][8]) {
-          if (!valid) return;
-          ld8_nc(gxr + 8 * c, b[0]);
-          ld8_nc(gxr + ep.Hp + 8 * c, b[1]);
-          ld8_nc(gxr + 2 * ep.Hp + 8 * c, b[2]);
-          ld8(sp + 8 * c, b[3]);
-        };
-        if constexpr (EPI == EPI_GRU) {
-          if (valid) {
-            const int j0 = (colbase >> 7) * 32;
-            const int y = ep.row_y[grow];
-            gxr = ep.gx + (int64_t)(y < 0 ? ep.y_bos : y) * ep.gx_ld + j0;
-            sp = ep.S + (int64_t)ep.row_src[grow] * ep.Hp + j0;
-          }
-          gru_fetch(0, gin[0]);
-          gru_fetch(1, gin[1]);
-        }
-        mbar_wait(&tfull[acc], aph);
+  }
+}
+
+// ---- MMA issuer (the pair's leader, one lane)
+template <int BN, int STAGES, int EPI, bool PAIR>
+NMT_DEV void gemm_mma(GemmCta<BN, STAGES, EPI, PAIR>& cx, const GemmShape& g, const Sched& sc, const EpiParams& ep) {
+  using S = GemmSmem<BN, STAGES, EPI, PAIR>;
+  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR>::CM;
+  constexpr uint32_t idesc = idesc_bf16(CM, BN);
+  for (int w = cx.unit; w < sc.items; w += cx.nunits) {
+    const Item itm = sc.item(w);
+    for (int n = itm.n0; n < itm.n1; ++n, ++cx.m_it) {
+      const TileCoord tc{itm.m, n, itm.s};
+      const RegionK rk = region_of(g, tc.n * BN);
+      const int acc = cx.m_it & 1;
+      const uint32_t aph = (cx.m_it >> 1) & 1;
+      mbar_wait(&cx.tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d = cx.tmem + acc * BN;
+      const int nkb_all = g.passes * (rk.k1 - rk.k0);
+      const int chunk = (nkb_all + rk.ks - 1) / rk.ks;
+      const int nkb = min(nkb_all, (tc.s + 1) * chunk) - tc.s * chunk;
+      for (int i = 0; i < nkb; ++i) {
+        const int stage = cx.m_stage;
+        mbar_wait(&cx.full[stage], cx.m_phase);
         tc_fence_after();
-        if (it == 0 && warp == 2 && lane == 0) GTRACE(5);
-        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + half * COLS;
-        if constexpr (EPI == EPI_STORE) {
-          // TMEM -> registers (+bias) -> 128B-swizzled 32x32 smem tile -> TMA store (coalesced)
-          uint8_t* stile = sC + (size_t)(warp - 2) * 2 * 4096;
-          const int row0 = itm.s * ep.rows_per_split + itm.m * CM + rank * BM + q * 32;
-#pragma unroll 1
-          for (int c = 0; c < COLS; c += 32) {
-            uint8_t* buf = stile + ((c >> 5) & 1) * 4096;
-            if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer has read it
-            __syncwarp();
-            float v[32];
-            tmem_ld32_nowait(tbase + c, v);
-            tmem_wait_ld_dep(v);
-            if (ep.bias) {
-              const float4* b = reinterpret_cast<const float4*>(ep.bias + colbase + c);
+        if (cx.m_it == 0 && i == 0) GTRACE(3);
+        const uint32_t a0 = smem_u32(cx.sA + stage * S::A_BYTES);
+        const uint32_t b0 = smem_u32(cx.sB + stage * S::B_BYTES);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 bb = __ldg(b + j);
-                v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
-              }
-            }
+        for (int k = 0; k < BK / 16; ++k) {
+          if constexpr (PAIR)
+            mma_bf16_pair(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
+          else
+            mma_bf16(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
+        }
+        if constexpr (PAIR) mma_commit_pair(&cx.empty[stage]);
+        else mma_commit(&cx.empty[stage]);
+        if (++cx.m_stage == STAGES) {
+          cx.m_stage = 0;
+          cx.m_phase ^= 1;
+        }
+      }
+      if constexpr (PAIR) mma_commit_pair(&cx.tfull[acc]);
+      else mma_commit(&cx.tfull[acc]);
+    }
+  }
+  GTRACE(4);
+}
+
+// ---- epilogue warps 2..9 (each CTA: its 128 rows of the tile)
+template <int BN, int STAGES, int EPI, bool PAIR>
+NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap* tmC, const GemmShape& g, int M,
+                           const Sched& sc, const EpiParams& ep) {
+  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR>::CM;
+  const int warp = cx.warp, lane = cx.lane;
+  const uint32_t rank = cx.rank, tmem = cx.tmem;
+  const bool leader = cx.leader;
+  uint64_t* tfull = cx.tfull;
+  uint64_t* tempty = cx.tempty;
+  uint8_t* sC = cx.sC;
+  const int q = warp & 3;               // TMEM lane quadrant accessible to this warp
+  const int half = (warp - 2) >> 2;     // which half of the tile's columns
+  constexpr int COLS = BN / 2;
+  const int row_in_tile = q * 32 + lane;
+  const uint32_t tempty0 = PAIR ? mapa_shared(smem_u32(tempty), 0) : 0;
+  int& it = cx.e_it;
+  for (int w = cx.unit; w < sc.items; w += cx.nunits) {
+    const Item itm = sc.item(w);
+    const int grow = itm.m * CM + rank * BM + row_in_tile;
+    const bool valid = grow < M;
+    constexpr float LOG2E = 1.4426950408889634f;
+    float mx = -INFINITY, s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;  // LSE running state (per run)
+    int am = 0;
+    float tv[EPI == EPI_TOPK ? kTopK : 1];  // TOPK: best logits of the run, descending (ties: lower column)
+    int ti[EPI == EPI_TOPK ? kTopK : 1];
+    if constexpr (EPI == EPI_TOPK) {
+#pragma unroll
+      for (int q = 0; q < kTopK; ++q) {
+        tv[q] = -INFINITY;
+        ti[q] = INT32_MAX;
+      }
+    }
+    for (int n = itm.n0; n < itm.n1; ++n, ++it) {
+      const int acc = it & 1;
+      const uint32_t aph = (it >> 1) & 1;
+      const int colbase = n * BN + half * COLS;
+      // EPI_GRU: this warp's COLS = 128 columns are one 32-unit group [r | u | h~ | pad] of its row, done
+      // in 4 chunks of 8 units.  A chunk's gx (r, u, x) and previous-state values arrive as 256-bit loads
+      // (full 32-byte sectors) issued two chunks ahead; the first two are issued before the accumulator
+      // wait, so their latency hides under the main loop.
+      float gin[EPI == EPI_GRU ? 2 : 1][4][8];
+      const float* gxr = nullptr;
+      const float* sp = nullptr;
+      auto gru_fetch = [&](int c, float(&b)[4][8]) {
+        if (!valid) return;
+        ld8_nc(gxr + 8 * c, b[0]);
+        ld8_nc(gxr + ep.Hp + 8 * c, b[1]);
+        ld8_nc(gxr + 2 * ep.Hp + 8 * c, b[2]);
+        ld8(sp + 8 * c, b[3]);
+      };
+      if constexpr (EPI == EPI_GRU) {
+        if (valid) {
+          const int j0 = (colbase >> 7) * 32;
+          const int y = ep.row_y[grow];
+          gxr = ep.gx + (int64_t)(y < 0 ? ep.y_bos : y) * ep.gx_ld + j0;
+          sp = ep.S + (int64_t)ep.row_src[grow] * ep.Hp + j0;
+        }
+        gru_fetch(0, gin[0]);
+        gru_fetch(1, gin[1]);
+      }
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      if (it == 0 && warp == 2 && lane == 0) GTRACE(5);
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + half * COLS;
+      if constexpr (EPI == EPI_STORE) {
+        // TMEM -> registers (+bias) -> 128B-swizzled 32x32 smem tile -> TMA store (coalesced)
+        uint8_t* stile = sC + (size_t)(warp - 2) * 2 * 4096;
+        const int row0 = itm.s * ep.rows_per_split + itm.m * CM + rank * BM + q * 32;
+#pragma unroll 1
+        for (int c = 0; c < COLS; c += 32) {
+          uint8_t* buf = stile + ((c >> 5) & 1) * 4096;
+          if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer has read it
+          __syncwarp();
+          float v[32];
+          tmem_ld32_nowait(tbase + c, v);
+          tmem_wait_ld_dep(v);
+          if (ep.bias) {
+            const float4* b = reinterpret_cast<const float4*>(ep.bias + colbase + c);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              float4* dst = reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
-              *dst = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&tmC, buf, colbase + c, row0);
-              bulk_commit();
+              const float4 bb = __ldg(b + j);
+              v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
             }
           }
-        } else if constexpr (EPI == EPI_TOPK) {  // running top-kTopK of this warp's COLS logits of the row
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4* dst = reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
+            *dst = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(tmC, buf, colbase + c, row0);
+            bulk_commit();
+          }
+        }
+      } else if constexpr (EPI == EPI_TOPK) {  // running top-kTopK of this warp's COLS logits of the row
 #pragma unroll 1
-          for (int c = 0; c < COLS; c += 32) {
-            float v[32];
-            tmem_ld32_nowait(tbase + c, v);
-            tmem_wait_ld_dep(v);
-            const int col0 = colbase + c + g.n_off;
+        for (int c = 0; c < COLS; c += 32) {
+          float v[32];
+          tmem_ld32_nowait(tbase + c, v);
+          tmem_wait_ld_dep(v);
+          const int col0 = colbase + c + g.n_off;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (v[j] > tv[kTopK - 1] && col0 + j < ep.n_valid) {  // (rare once the list is full)
-                float x = v[j];
-                int xi = col0 + j;
+          for (int j = 0; j < 32; ++j) {
+            if (v[j] > tv[kTopK - 1] && col0 + j < ep.n_valid) {  // (rare once the list is full)
+              float x = v[j];
+              int xi = col0 + j;
 #pragma unroll
-                for (int q = 0; q < kTopK; ++q) {  // sorted insert; an equal value stays behind
-                  if (x > tv[q]) {
-                    const float tx = tv[q];
-                    const int txi = ti[q];
-                    tv[q] = x;
-                    ti[q] = xi;
-                    x = tx;
-                    xi = txi;
-                  }
+              for (int q = 0; q < kTopK; ++q) {  // sorted insert; an equal value stays behind
+                if (x > tv[q]) {
+                  const float tx = tv[q];
+                  const int txi = ti[q];
+                  tv[q] = x;
+                  ti[q] = xi;
+                  x = tx;
+                  xi = txi;
                 }
               }
             }
           }
-        } else if constexpr (EPI == EPI_GRU) {
-          static_assert(BN / 2 == 128, "EPI_GRU: one 32-unit group per epilogue warp");
-          const int j0 = (colbase >> 7) * 32;
-          float* s1 = ep.S1 + (int64_t)grow * ep.Hp + j0;
-          __nv_bfloat16* xo = ep.X + (int64_t)grow * ep.ldx + j0;
+        }
+      } else if constexpr (EPI == EPI_GRU) {
+        static_assert(BN / 2 == 128, "EPI_GRU: one 32-unit group per epilogue warp");
+        const int j0 = (colbase >> 7) * 32;
+        float* s1 = ep.S1 + (int64_t)grow * ep.Hp + j0;
+        __nv_bfloat16* xo = ep.X + (int64_t)grow * ep.ldx + j0;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float vr[8], vu[8], vx[8];
-            tmem_ld8_nowait(tbase + 8 * c, vr);
-            tmem_ld8_nowait(tbase + 32 + 8 * c, vu);
-            tmem_ld8_nowait(tbase + 64 + 8 * c, vx);
-            tmem_wait_ld();
-            reg_dep8(vr);
-            reg_dep8(vu);
-            reg_dep8(vx);
-            float(&b)[4][8] = gin[c & 1];
-            float o[8];
+        for (int c = 0; c < 4; ++c) {
+          float vr[8], vu[8], vx[8];
+          tmem_ld8_nowait(tbase + 8 * c, vr);
+          tmem_ld8_nowait(tbase + 32 + 8 * c, vu);
+          tmem_ld8_nowait(tbase + 64 + 8 * c, vx);
+          tmem_wait_ld();
+          reg_dep8(vr);
+          reg_dep8(vu);
+          reg_dep8(vx);
+          float(&b)[4][8] = gin[c & 1];
+          float o[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float rg = gru_sigm(b[0][i] + vr[i]), ug = gru_sigm(b[1][i] + vu[i]);
-              o[i] = ug * b[3][i] + (1.f - ug) * tanhf(rg * vx[i] + b[2][i]);
-            }
-            if (c + 2 < 4) gru_fetch(c + 2, gin[c & 1]);
-            if (valid) {
-              st8(s1 + 8 * c, o);
-              gru_store4(xo + 8 * c, ep.lo_x, o[0], o[1], o[2], o[3]);
-              gru_store4(xo + 8 * c + 4, ep.lo_x, o[4], o[5], o[6], o[7]);
-            }
+          for (int i = 0; i < 8; ++i) {
+            const float rg = gru_sigm(b[0][i] + vr[i]), ug = gru_sigm(b[1][i] + vu[i]);
+            o[i] = ug * b[3][i] + (1.f - ug) * tanhf(rg * vx[i] + b[2][i]);
           }
-        } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
+          if (c + 2 < 4) gru_fetch(c + 2, gin[c & 1]);
+          if (valid) {
+            st8(s1 + 8 * c, o);
+            gru_store4(xo + 8 * c, ep.lo_x, o[0], o[1], o[2], o[3]);
+            gru_store4(xo + 8 * c + 4, ep.lo_x, o[4], o[5], o[6], o[7]);
+          }
+        }
+      } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
 #pragma unroll 1
-          for (int c = 0; c < COLS; c += 64) {
-            float v[64];
-            tmem_ld32_nowait(tbase + c, v);
-            tmem_ld32_nowait(tbase + c + 32, v + 32);
-            tmem_wait_ld_dep(v);
-            reg_dep32(v + 32);
-            const int col0 = colbase + c + g.n_off;
-            if (col0 + 64 > ep.n_valid) {  // padded vocabulary columns (last tile only)
+        for (int c = 0; c < COLS; c += 64) {
+          float v[64];
+          tmem_ld32_nowait(tbase + c, v);
+          tmem_ld32_nowait(tbase + c + 32, v + 32);
+          tmem_wait_ld_dep(v);
+          reg_dep32(v + 32);
+          const int col0 = colbase + c + g.n_off;
+          if (col0 + 64 > ep.n_valid) {  // padded vocabulary columns (last tile only)
 #pragma unroll
-              for (int j = 0; j < 64; ++j)
-                if (col0 + j >= ep.n_valid) v[j] = -INFINITY;
-            }
-            float t32[32];  // tree max
+            for (int j = 0; j < 64; ++j)
+              if (col0 + j >= ep.n_valid) v[j] = -INFINITY;
+          }
+          float t32[32];  // tree max
 #pragma unroll
-            for (int j = 0; j < 32; ++j) t32[j] = fmaxf(v[j], v[j + 32]);
+          for (int j = 0; j < 32; ++j) t32[j] = fmaxf(v[j], v[j + 32]);
+#pragma unroll
+          for (int k = 16; k > 0; k >>= 1)
+#pragma unroll
+            for (int j = 0; j < k; ++j) t32[j] = fmaxf(t32[j], t32[j + k]);
+          const float cm = t32[0];
+          if (cm > mx) {  // new running max (rare after the first chunks): lowest index of it
+            int ix[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ix[j] = v[j] == cm ? j : (v[j + 32] == cm ? j + 32 : 64);
 #pragma unroll
             for (int k = 16; k > 0; k >>= 1)
 #pragma unroll
-              for (int j = 0; j < k; ++j) t32[j] = fmaxf(t32[j], t32[j + k]);
-            const float cm = t32[0];
-            if (cm > mx) {  // new running max (rare after the first chunks): lowest index of it
-              int ix[32];
+              for (int j = 0; j < k; ++j) ix[j] = min(ix[j], ix[j + k]);
+            const float f = ex2_approx((mx - cm) * LOG2E);
+            s0 *= f; s1 *= f; s2 *= f; s3 *= f;
+            mx = cm;
+            am = col0 + ix[0];
+          }
+          if (mx > -INFINITY) {
+            const float mb = mx * LOG2E;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) ix[j] = v[j] == cm ? j : (v[j + 32] == cm ? j + 32 : 64);
-#pragma unroll
-              for (int k = 16; k > 0; k >>= 1)
-#pragma unroll
-                for (int j = 0; j < k; ++j) ix[j] = min(ix[j], ix[j + k]);
-              const float f = ex2_approx((mx - cm) * LOG2E);
-              s0 *= f; s1 *= f; s2 *= f; s3 *= f;
-              mx = cm;
-              am = col0 + ix[0];
-            }
-            if (mx > -INFINITY) {
-              const float mb = mx * LOG2E;
-#pragma unroll
-              for (int j = 0; j < 64; j += 4) {
-                s0 += ex2_approx(fmaf(v[j], LOG2E, -mb));
-                s1 += ex2_approx(fmaf(v[j + 1], LOG2E, -mb));
-                s2 += ex2_approx(fmaf(v[j + 2], LOG2E, -mb));
-                s3 += ex2_approx(fmaf(v[j + 3], LOG2E, -mb));
-              }
+            for (int j = 0; j < 64; j += 4) {
+              s0 += ex2_approx(fmaf(v[j], LOG2E, -mb));
+              s1 += ex2_approx(fmaf(v[j + 1], LOG2E, -mb));
+              s2 += ex2_approx(fmaf(v[j + 2], LOG2E, -mb));
+              s3 += ex2_approx(fmaf(v[j + 3], LOG2E, -mb));
             }
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive(&tempty[acc]);
-          else mbar_arrive_cluster(tempty0 + acc * 8);
-        }
       }
-      if constexpr (EPI == EPI_LSE) {  // one partial per (row, run, half); empty runs give (-inf, 0)
-        if (valid)
-          ep.part[((size_t)grow * sc.cpm + itm.c) * 2 + half] =
-              make_float4(mx, (s0 + s1) + (s2 + s3), __int_as_float(am), 0.f);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_cluster(tempty0 + acc * 8);
       }
-      if constexpr (EPI == EPI_TOPK) {  // kTopK (logit, column) per (row, run, half)
-        if (valid) {
-          float2* dst = ep.topk + (((size_t)grow * sc.cpm + itm.c) * 2 + half) * kTopK;
+    }
+    if constexpr (EPI == EPI_LSE) {  // one partial per (row, run, half); empty runs give (-inf, 0)
+      if (valid)
+        ep.part[((size_t)grow * sc.cpm + itm.c) * 2 + half] =
+            make_float4(mx, (s0 + s1) + (s2 + s3), __int_as_float(am), 0.f);
+    }
+    if constexpr (EPI == EPI_TOPK) {  // kTopK (logit, column) per (row, run, half)
+      if (valid) {
+        float2* dst = ep.topk + (((size_t)grow * sc.cpm + itm.c) * 2 + half) * kTopK;
 #pragma unroll
-          for (int q = 0; q < kTopK; ++q) dst[q] = make_float2(tv[q], __int_as_float(ti[q]));
-        }
+        for (int q = 0; q < kTopK; ++q) dst[q] = make_float2(tv[q], __int_as_float(ti[q]));
       }
     }
   }
-  if (EPI == EPI_STORE && warp >= 2 && lane == 0) bulk_wait_all();
-  if (warp == 2 && lane == 0) GTRACE(6);
-  __syncthreads();
-  if constexpr (PAIR) cluster_sync();
-  if (warp == 1) {
-    tc_fence_after();
-    if constexpr (PAIR) tmem_dealloc_pair(tmem, 2 * BN);
-    else tmem_dealloc(tmem, 2 * BN);
+}
+
+template <int BN, int STAGES, int EPI, bool PAIR>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const __grid_constant__ CUtensorMap tmC, GemmShape g, EpiParams ep) {
+  extern __shared__ uint8_t smem_raw[];
+  GemmCta<BN, STAGES, EPI, PAIR> cx;
+  cx.carve(smem_raw);
+  if (threadIdx.x == 0) GTRACE(0);
+  if (cx.warp == 0 && cx.lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    if (EPI == EPI_STORE) tma_prefetch(&tmC);
   }
+  cx.setup();
+  if (threadIdx.x == 0) GTRACE(1);
+  pdl_enter();  // prologue above overlaps the previous kernel; inputs (and M_dev) are read below
+  if (threadIdx.x == 0) GTRACE(2);
+  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR>::CM;
+  const int M = g.M_dev ? *g.M_dev : g.M;
+  const Sched sc = make_sched<EPI>(g, M, CM, BN, cx.nunits);
+  if ((EPI == EPI_LSE || EPI == EPI_TOPK) && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
+  if (cx.warp == 0) {
+    if (cx.lane == 0) gemm_produce(cx, &tmA, &tmB, g, sc);
+  } else if (cx.warp == 1) {
+    if (cx.lane == 0 && cx.leader) gemm_mma(cx, g, sc, ep);
+  } else {
+    gemm_epilogue(cx, &tmC, g, M, sc, ep);
+  }
+  if (EPI == EPI_STORE && cx.warp >= 2 && cx.lane == 0) bulk_wait_all();
+  if (cx.warp == 2 && cx.lane == 0) GTRACE(6);
+  cx.teardown();
   if (threadIdx.x == 0) GTRACE(7);
 }
 
