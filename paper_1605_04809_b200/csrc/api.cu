@@ -227,6 +227,7 @@ struct nmt_model {
   float* Ex = nullptr;            // [V+1][3Hp]
   __nv_bfloat16* W_q = nullptr;   // [Cp][sf Hp]
   __nv_bfloat16* W_g2 = nullptr;  // [4Hp][sf (Hp+Cp)]
+  __nv_bfloat16* W_g2i = nullptr; // [4Hp][sf (Hp+Cp)] per 32-unit group [hx | r | u | cx] (fused GRU2 epilogue)
   float* b_nl = nullptr;          // [2Hp]
   float* bx_nl = nullptr;         // [Hp]
   __nv_bfloat16* W_ro = nullptr;  // [ROp][sf (Cp+Hp)]
@@ -235,7 +236,7 @@ struct nmt_model {
   float* W_o32 = nullptr;         // [V][Ep]
   float* b_o = nullptr;           // [V]
   bool use_pair = true;  // CTA-pair (cta_group::2) GEMMs where the shapes allow (NMT_PAIR=0 disables)
-  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128, tm_Wh1g;
+  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128, tm_Wh1g, tm_Wg2i;
   // encoder workspace
   int Tpad = 0;
   __nv_bfloat16* ctxbf = nullptr; // [Tpad][4Hp]
@@ -351,7 +352,7 @@ static void free_all_model(nmt_model* m) {
   for (float** p : {&m->EncIn, &m->Uarr, &m->W_initT, &m->b_init, &m->b_att, &m->U_att, &m->Ex, &m->b_nl, &m->bx_nl,
                     &m->Eproj, &m->W_o32, &m->b_o, &m->hbuf, &m->enc_mean, &m->ksplit_buf})
     dfree(*p);
-  for (__nv_bfloat16** p : {&m->W_h1g, &m->Watt, &m->W_h1, &m->W_q, &m->W_g2, &m->W_ro, &m->W_o, &m->ctxbf}) dfree(*p);
+  for (__nv_bfloat16** p : {&m->W_g2i, &m->W_h1g, &m->Watt, &m->W_h1, &m->W_q, &m->W_g2, &m->W_ro, &m->W_o, &m->ctxbf}) dfree(*p);
   dfree(m->bar);
   dfree(m->d_src);
   dfree(m->W_encb);
@@ -939,6 +940,34 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
     pack_T(Uxnl.d, H, H, H, m->W_g2, sf * ldg2, 2 * Hp, 0, 0, 0, H, Hp, lo, st);
     pack_T(Wcx.d, H, C, H, m->W_g2, sf * ldg2, 3 * Hp, Hp, 0, 1, H, Hp, lo, st);
   }
+  {  // the same weights interleaved per 32-unit group for the fused GRU2 epilogue (EPI_GRU2): B row
+     // (j / 32) * 128 + 32 p + j % 32 = part p (hx, r, u, cx) of unit j; K = [s1 (Hp) | c (Cp)]
+    std::vector<float> wg((size_t)ldg2 * 4 * Hp, 0.f);  // [K][N]
+    const float* Unl = hv("decoder_U_nl");
+    const float* Uxnl = hv("decoder_Ux_nl");
+    const float* Wcm = hv("decoder_Wc");
+    const float* Wcxm = hv("decoder_Wcx");
+    for (int j = 0; j < H; ++j) {
+      const size_t base = (size_t)(j / 32) * 128 + j % 32;
+      for (int k = 0; k < H; ++k) {
+        float* row = wg.data() + (size_t)k * 4 * Hp;
+        row[base] = Uxnl[(size_t)k * H + j];
+        row[base + 32] = Unl[(size_t)k * 2 * H + j];
+        row[base + 64] = Unl[(size_t)k * 2 * H + H + j];
+      }
+      for (int cc = 0; cc < C; ++cc) {
+        float* row = wg.data() + (size_t)(Hp + (cc < H ? cc : Hp + cc - H)) * 4 * Hp;
+        row[base + 32] = Wcm[(size_t)cc * 2 * H + j];
+        row[base + 64] = Wcm[(size_t)cc * 2 * H + H + j];
+        row[base + 96] = Wcxm[(size_t)cc * H + j];
+      }
+    }
+    float* dwg = upload_vec(wg, st);
+    m->W_g2i = dalloc<__nv_bfloat16>((size_t)4 * Hp * sf * ldg2);
+    pack_T(dwg, 4 * Hp, ldg2, 4 * Hp, m->W_g2i, sf * ldg2, 0, 0, 0, 0, H, Hp, m->split ? ldg2 : 0, st);
+    CK(cudaStreamSynchronize(st));
+    dfree(dwg);
+  }
   std::vector<float> bnl(2 * Hp, 0.f), bxnl(Hp, 0.f);
   for (int j = 0; j < H; ++j) {
     bnl[j] = hv("decoder_b_nl")[j];
@@ -1040,6 +1069,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   m->tm_Wh1g = make_tmap_bf16(m->W_h1g, 4 * Hp, sf * Hp, 128);
   m->tm_Wq = make_tmap_bf16(m->W_q, Cp, sf * Hp, 128);
   m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, 128);
+  m->tm_Wg2i = make_tmap_bf16(m->W_g2i, 4 * Hp, sf * ldg2, 128);
   m->tm_Wro = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 128);
   m->tm_Wo = make_tmap_bf16(m->W_o, (uint64_t)Vp * sf * Ep / 64, 64, 256);     // panel layout
   m->tm_Wo128 = make_tmap_bf16(m->W_o, (uint64_t)Vp * sf * Ep / 64, 64, 128);  // CTA-pair vocabulary GEMM: half tiles
@@ -1369,18 +1399,38 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
   }
   if (!ms) c->join_enc();  // ctx and pctx (the pctx GEMM overlapped the steps above)
   if (!stage_skipped(ST_ATTN)) { ProfScope p_(m, ST_ATTN); step_elementwise(EW_ATTN, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
-  if (!stage_skipped(ST_GEMM_G2)) {
+  if (m->use_pair && !stage_skipped(ST_GEMM_G2) && !stage_skipped(ST_GRU2)) {
+    // D6: GEMM [s1 | c] . W_g2 with GRU2 in its epilogue (one launch, no G2 partials)
     ProfScope p_(m, ST_GEMM_G2);
     GemmShape g = gemm_shape(0, Rd, 4 * Hp, Hp + Cp, 0, sp, 4 * Hp, Hp + Cp);
-    g.nreg = 3;
-    g.reg_n_end[0] = 2 * Hp, g.reg_k0[0] = 0, g.reg_k1[0] = Hp + Cp;  // gates: s1 U_nl + c Wc
-    g.reg_n_end[1] = 3 * Hp, g.reg_k0[1] = 0, g.reg_k1[1] = Hp;       // s1 Ux_nl
-    g.reg_n_end[2] = 4 * Hp, g.reg_k0[2] = Hp, g.reg_k1[2] = Hp + Cp; // c Wcx
-    gemm_auto(m, m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, rps, R_max, st);
-    for (int r = 0; r < 3; ++r) d.ks_g2[r] = g.reg_ks[r];
-    d.ps_g2 = (int64_t)rps * 4 * Hp;
+    EpiParams ep{};
+    ep.S1 = m->S1;
+    ep.X = m->X;
+    ep.ldx = d.ldx;
+    ep.lo_x = d.lo_x;
+    ep.Hp = Hp;
+    ep.Sout = ms ? nullptr : c->S;
+    ep.row_dst = m->row_dst;
+    ep.gs = d.gs;
+    ep.row_grp = d.row_grp;
+    ep.b_nl = m->b_nl;
+    ep.bx_nl = m->bx_nl;
+    ep.x_col = Hp + Cp;
+    gemm_gru2_pair(m->tm_X, m->tm_Wg2i, g, ep, R_max, st);
+  } else {  // (1-CTA GEMM mode, diagnostics): region GEMM with split-K partials + k_gru2
+    if (!stage_skipped(ST_GEMM_G2)) {
+      ProfScope p_(m, ST_GEMM_G2);
+      GemmShape g = gemm_shape(0, Rd, 4 * Hp, Hp + Cp, 0, sp, 4 * Hp, Hp + Cp);
+      g.nreg = 3;
+      g.reg_n_end[0] = 2 * Hp, g.reg_k0[0] = 0, g.reg_k1[0] = Hp + Cp;  // gates: s1 U_nl + c Wc
+      g.reg_n_end[1] = 3 * Hp, g.reg_k0[1] = 0, g.reg_k1[1] = Hp;       // s1 Ux_nl
+      g.reg_n_end[2] = 4 * Hp, g.reg_k0[2] = Hp, g.reg_k1[2] = Hp + Cp; // c Wcx
+      gemm_auto(m, m->tm_X, m->tm_Wg2, g, m->G2, 4 * Hp, rps, R_max, st);
+      for (int r = 0; r < 3; ++r) d.ks_g2[r] = g.reg_ks[r];
+      d.ps_g2 = (int64_t)rps * 4 * Hp;
+    }
+    if (!stage_skipped(ST_GRU2)) { ProfScope p_(m, ST_GRU2); step_elementwise(EW_GRU2, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   }
-  if (!stage_skipped(ST_GRU2)) { ProfScope p_(m, ST_GRU2); step_elementwise(EW_GRU2, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   if (!stage_skipped(ST_GEMM_RO)) {
     ProfScope p_(m, ST_GEMM_RO);
     GemmShape g = gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp);

@@ -31,12 +31,19 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "kernels.h"
 
 namespace nmt {
 
 constexpr int BM = 128, BK = 64;
 constexpr int EPI_STORE = 0, EPI_LSE = 1, EPI_TOPK = 2;  // TOPK: runs like LSE, keeps the kTopK best logits
 constexpr int EPI_GRU = 3;  // fused GRU gates (one tile per item like EPI_STORE, no split-K)
+// fused decoder GRU2 (D6): per 32-unit group the B rows are [hx | r | u | cx]; the s1 K range multiplies
+// rows hx, r, u (MMA N = 192 over the first 96 rows of each CTA's half) into accumulator D1, the c K range
+// rows r, u, cx (N = 192 from row 32) into D2, so no zero block is multiplied; single-buffered TMEM
+constexpr int EPI_GRU2 = 4;
+template <int EPI>
+constexpr bool single_acc() { return EPI == EPI_GRU2; }
 constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant, each owning half of the tile's columns
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
@@ -130,7 +137,10 @@ NMT_DEV RegionK region_of(const GemmShape& g, int n0) {
   return RegionK{g.reg_k0[r] / BK, g.reg_k1[r] / BK, g.reg_ks[r] > 0 ? g.reg_ks[r] : g.ksplit};
 }
 
-NMT_DEV float gru_sigm(float x) { return 1.f / (1.f + expf(-x)); }
+// GRU gate math of the fused epilogues on the SFU: ex2.approx + rcp.approx based, |err| ~ 1e-7 (the
+// IEEE expf / division / tanhf versions made these epilogues issue-bound: ~7 us per tile on 8 warps)
+NMT_DEV float gru_sigm(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+NMT_DEV float gru_tanh(float x) { return 1.f - __fdividef(2.f, 1.f + __expf(2.f * x)); }
 NMT_DEV uint32_t gru_pk(float lo, float hi) {
   uint32_t y;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(y) : "f"(hi), "f"(lo));
@@ -286,11 +296,12 @@ NMT_DEV void gemm_mma(GemmCta<BN, STAGES, EPI, PAIR>& cx, const GemmShape& g, co
     for (int n = itm.n0; n < itm.n1; ++n, ++cx.m_it) {
       const TileCoord tc{itm.m, n, itm.s};
       const RegionK rk = region_of(g, tc.n * BN);
-      const int acc = cx.m_it & 1;
-      const uint32_t aph = (cx.m_it >> 1) & 1;
+      const int acc = single_acc<EPI>() ? 0 : cx.m_it & 1;
+      const uint32_t aph = single_acc<EPI>() ? cx.m_it & 1 : (cx.m_it >> 1) & 1;
       mbar_wait(&cx.tempty[acc], aph ^ 1);
       tc_fence_after();
       const uint32_t d = cx.tmem + acc * BN;
+      const int nkb_s1 = ep.Hp / BK;  // (EPI_GRU2: k-blocks of the s1 range)
       const int nkb_all = g.passes * (rk.k1 - rk.k0);
       const int chunk = (nkb_all + rk.ks - 1) / rk.ks;
       const int nkb = min(nkb_all, (tc.s + 1) * chunk) - tc.s * chunk;
@@ -301,12 +312,25 @@ NMT_DEV void gemm_mma(GemmCta<BN, STAGES, EPI, PAIR>& cx, const GemmShape& g, co
         if (cx.m_it == 0 && i == 0) GTRACE(3);
         const uint32_t a0 = smem_u32(cx.sA + stage * S::A_BYTES);
         const uint32_t b0 = smem_u32(cx.sB + stage * S::B_BYTES);
+        if constexpr (EPI == EPI_GRU2) {
+          static_assert(PAIR && BN == 256, "EPI_GRU2: CTA pairs, 2 groups per tile");
+          constexpr uint32_t idesc2 = idesc_bf16(CM, 192);
+          const int kbp = i % (rk.k1 - rk.k0);        // k-block within the pass
+          const bool c_rng = kbp >= nkb_s1;
+          const int first = c_rng ? nkb_s1 : 0;       // first k-block of this accumulator's range
+          const uint32_t dd = d + (c_rng ? 192 : 0);  // D2 follows D1 (384 of the 512 columns)
+          const uint32_t bo = c_rng ? 32 * 128 : 0;   // rows r, u, cx start 32 rows into the half
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          if constexpr (PAIR)
-            mma_bf16_pair(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
-          else
-            mma_bf16(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16_pair(dd, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + bo + k * 32), idesc2, (i != first || k != 0));
+        } else {
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            if constexpr (PAIR)
+              mma_bf16_pair(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
+            else
+              mma_bf16(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
+          }
         }
         if constexpr (PAIR) mma_commit_pair(&cx.empty[stage]);
         else mma_commit(&cx.empty[stage]);
@@ -356,8 +380,8 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap
       }
     }
     for (int n = itm.n0; n < itm.n1; ++n, ++it) {
-      const int acc = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
+      const int acc = single_acc<EPI>() ? 0 : it & 1;
+      const uint32_t aph = single_acc<EPI>() ? it & 1 : (it >> 1) & 1;
       const int colbase = n * BN + half * COLS;
       // EPI_GRU: this warp's COLS = 128 columns are one 32-unit group [r | u | h~ | pad] of its row, done
       // in 4 chunks of 8 units.  A chunk's gx (r, u, x) and previous-state values arrive as 256-bit loads
@@ -382,6 +406,14 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap
         }
         gru_fetch(0, gin[0]);
         gru_fetch(1, gin[1]);
+      }
+      float s1in[EPI == EPI_GRU2 ? 4 : 1][8];  // EPI_GRU2: the row's s1 for the group's 32 units
+      if constexpr (EPI == EPI_GRU2) {
+        if (valid) {
+          const float* s1p = ep.S1 + (int64_t)grow * ep.Hp + (colbase >> 7) * 32;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) ld8(s1p + 8 * c, s1in[c]);
+        }
       }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
@@ -465,11 +497,47 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float rg = gru_sigm(b[0][i] + vr[i]), ug = gru_sigm(b[1][i] + vu[i]);
-            o[i] = ug * b[3][i] + (1.f - ug) * tanhf(rg * vx[i] + b[2][i]);
+            o[i] = ug * b[3][i] + (1.f - ug) * gru_tanh(rg * vx[i] + b[2][i]);
           }
           if (c + 2 < 4) gru_fetch(c + 2, gin[c & 1]);
           if (valid) {
             st8(s1 + 8 * c, o);
+            gru_store4(xo + 8 * c, ep.lo_x, o[0], o[1], o[2], o[3]);
+            gru_store4(xo + 8 * c + 4, ep.lo_x, o[4], o[5], o[6], o[7]);
+          }
+        }
+      } else if constexpr (EPI == EPI_GRU2) {
+        // this warp's group: units j0..j0+31; D1 = [hx | r | u] (s1 range), D2 = [r | u | cx] (c range)
+        const int j0 = (colbase >> 7) * 32;
+        const uint32_t t1 = tmem + ((uint32_t)(q * 32) << 16) + 96 * half, t2 = t1 + 192;
+        float* so = nullptr;
+        if (valid) {
+          const int dst = ep.row_dst[grow];
+          if (dst >= 0) so = (ep.gs ? ep.gs[ep.row_grp[grow]].S : ep.Sout) + (int64_t)dst * ep.Hp + j0;
+        }
+        __nv_bfloat16* xo = ep.X + (int64_t)grow * ep.ldx + ep.x_col + j0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float hx[8], r1[8], u1[8], r2[8], u2[8], cx8[8];
+          tmem_ld8_nowait(t1 + 8 * c, hx);
+          tmem_ld8_nowait(t1 + 32 + 8 * c, r1);
+          tmem_ld8_nowait(t1 + 64 + 8 * c, u1);
+          tmem_ld8_nowait(t2 + 8 * c, r2);
+          tmem_ld8_nowait(t2 + 32 + 8 * c, u2);
+          tmem_ld8_nowait(t2 + 64 + 8 * c, cx8);
+          tmem_wait_ld();
+          reg_dep8(hx); reg_dep8(r1); reg_dep8(u1); reg_dep8(r2); reg_dep8(u2); reg_dep8(cx8);
+          if (valid) {
+            float br[8], bu[8], bx[8], o[8];
+            ld8_nc(ep.b_nl + j0 + 8 * c, br);
+            ld8_nc(ep.b_nl + ep.Hp + j0 + 8 * c, bu);
+            ld8_nc(ep.bx_nl + j0 + 8 * c, bx);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float rg = gru_sigm((r1[i] + r2[i]) + br[i]), ug = gru_sigm((u1[i] + u2[i]) + bu[i]);
+              o[i] = ug * s1in[c][i] + (1.f - ug) * gru_tanh(rg * (hx[i] + bx[i]) + cx8[i]);
+            }
+            if (so) st8(so + 8 * c, o);
             gru_store4(xo + 8 * c, ep.lo_x, o[0], o[1], o[2], o[3]);
             gru_store4(xo + 8 * c + 4, ep.lo_x, o[4], o[5], o[6], o[7]);
           }
@@ -757,6 +825,14 @@ void gemm_gru_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmSh
   gemm_validate(g, 256);
   if (gemm_ks_max(g) != 1) throw NmtError(NMT_ERR_INVALID_ARG, "gemm: the fused GRU epilogue needs the full K sum");
   launch<256, 5, EPI_GRU, true>(a, b_half, b_half /*unused*/, g, ep, M_max, st);
+}
+
+void gemm_gru2_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, const EpiParams& ep, int M_max,
+                    cudaStream_t st) {
+  gemm_validate(g, 256);
+  if (gemm_ks_max(g) != 1 || g.nreg != 1 || ep.Hp % BK)
+    throw NmtError(NMT_ERR_INVALID_ARG, "gemm: the fused GRU2 epilogue needs the full K sum in one region");
+  launch<256, 5, EPI_GRU2, true>(a, b_half, b_half /*unused*/, g, ep, M_max, st);
 }
 
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,

@@ -116,6 +116,16 @@ struct EpiParams {
   __nv_bfloat16* X;    // [R][ldx] new state as the next GEMM's bf16 operand (lo at +lo_x if > 0)
   int ldx, lo_x, Hp;
   unsigned long long* trace;  // diagnostic builds only (NMT_GEMM_TRACE): [CTA][8] globaltimer stamps
+  // EPI_GRU2 (fused decoder GRU2, B rows per 32-unit group [hx | r | u | cx], s1 . U_nl K range on the
+  // first Hp columns of A, c . Wc on the rest): s2 = u*s1 + (1-u)*tanh(r*(hx + bx_nl) + cx),
+  // r = sigm(acc_r + b_nl[r]), u = sigm(acc_u + b_nl[u]); input s1 = S1 (above)
+  float* Sout;             // arena states [.][Hp]: s2 -> slot row_dst[r] (>= 0)
+  const int* row_dst;
+  const struct GrpStep* gs;  // multi-context step: per-group arenas (Sout unused), else null
+  const int* row_grp;
+  const float* b_nl;       // [2Hp]
+  const float* bx_nl;      // [Hp]
+  int x_col;               // column of s2 in X
 };
 constexpr int kTopK = 8;  // NMT_TOPK_MAX: words per row kept by the top-k vocabulary epilogue
 
@@ -140,6 +150,10 @@ void gemm_lse_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmSh
 // GEMM s.[U|Ux] with the GRU gates fused into the epilogue (CTA pairs, no split-K); see EPI_GRU
 void gemm_gru_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, const EpiParams& ep, int M_max,
                    cudaStream_t st);
+// GEMM [s1 | c] . W_g2 (interleaved per 32-unit group [hx | r | u | cx]) with the decoder's GRU2 fused
+// into the epilogue (EPI_GRU2; CTA pairs, no split-K, no partials)
+void gemm_gru2_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, const EpiParams& ep, int M_max,
+                    cudaStream_t st);
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
               cudaStream_t st, int* cpm_out);
 
