@@ -285,12 +285,16 @@ NMT_DEV void gemm_produce(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap*
   }
 }
 
-// ---- MMA issuer (the pair's leader, one lane)
+// ---- MMA issuer: the whole warp 1 of the pair's leader runs the (warp-uniform) loop, so descriptors and
+// TMEM addresses live in uniform registers; one elected lane issues a k-block's MMAs and its commit
+// (lane-divergent issue cost ~20 instructions per MMA in ELECT / R2UR broadcast loops)
 template <int BN, int STAGES, int EPI, bool PAIR>
 NMT_DEV void gemm_mma(GemmCta<BN, STAGES, EPI, PAIR>& cx, const GemmShape& g, const Sched& sc, const EpiParams& ep) {
   using S = GemmSmem<BN, STAGES, EPI, PAIR>;
   constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR>::CM;
   constexpr uint32_t idesc = idesc_bf16(CM, BN);
+  constexpr uint32_t idesc2 = idesc_bf16(CM, 192);  // (EPI_GRU2)
+  const uint64_t adesc0 = sdesc_sw128(smem_u32(cx.sA)), bdesc0 = sdesc_sw128(smem_u32(cx.sB));
   for (int w = cx.unit; w < sc.items; w += cx.nunits) {
     const Item itm = sc.item(w);
     for (int n = itm.n0; n < itm.n1; ++n, ++cx.m_it) {
@@ -309,41 +313,44 @@ NMT_DEV void gemm_mma(GemmCta<BN, STAGES, EPI, PAIR>& cx, const GemmShape& g, co
         const int stage = cx.m_stage;
         mbar_wait(&cx.full[stage], cx.m_phase);
         tc_fence_after();
-        if (cx.m_it == 0 && i == 0) GTRACE(3);
-        const uint32_t a0 = smem_u32(cx.sA + stage * S::A_BYTES);
-        const uint32_t b0 = smem_u32(cx.sB + stage * S::B_BYTES);
-        if constexpr (EPI == EPI_GRU2) {
-          static_assert(PAIR && BN == 256, "EPI_GRU2: CTA pairs, 2 groups per tile");
-          constexpr uint32_t idesc2 = idesc_bf16(CM, 192);
-          const int kbp = i % (rk.k1 - rk.k0);        // k-block within the pass
-          const bool c_rng = kbp >= nkb_s1;
-          const int first = c_rng ? nkb_s1 : 0;       // first k-block of this accumulator's range
-          const uint32_t dd = d + (c_rng ? 192 : 0);  // D2 follows D1 (384 of the 512 columns)
-          const uint32_t bo = c_rng ? 32 * 128 : 0;   // rows r, u, cx start 32 rows into the half
+        if (cx.lane == 0 && cx.m_it == 0 && i == 0) GTRACE(3);
+        // descriptor start-address field: (smem address >> 4), +2 per 32 bytes (16 bf16 of K)
+        const uint64_t ad = adesc0 + (uint64_t)(stage * (S::A_BYTES >> 4));
+        const uint64_t bd = bdesc0 + (uint64_t)(stage * (S::B_BYTES >> 4));
+        if (elect_one()) {
+          if constexpr (EPI == EPI_GRU2) {
+            static_assert(PAIR && BN == 256, "EPI_GRU2: CTA pairs, 2 groups per tile");
+            const int kbp = i % (rk.k1 - rk.k0);        // k-block within the pass
+            const bool c_rng = kbp >= nkb_s1;
+            const int first = c_rng ? nkb_s1 : 0;       // first k-block of this accumulator's range
+            const uint32_t dd = d + (c_rng ? 192 : 0);  // D2 follows D1 (384 of the 512 columns)
+            const uint64_t bo = c_rng ? (32 * 128) >> 4 : 0;  // rows r, u, cx start 32 rows into the half
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma_bf16_pair(dd, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + bo + k * 32), idesc2, (i != first || k != 0));
-        } else {
+            for (int k = 0; k < BK / 16; ++k) mma_bf16_pair(dd, ad + 2 * k, bd + bo + 2 * k, idesc2, (i != first || k != 0));
+          } else {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            if constexpr (PAIR)
-              mma_bf16_pair(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
-            else
-              mma_bf16(d, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), idesc, (i | k) != 0);
+            for (int k = 0; k < BK / 16; ++k) {
+              if constexpr (PAIR) mma_bf16_pair(d, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
+              else mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
+            }
           }
+          if constexpr (PAIR) mma_commit_pair(&cx.empty[stage]);
+          else mma_commit(&cx.empty[stage]);
         }
-        if constexpr (PAIR) mma_commit_pair(&cx.empty[stage]);
-        else mma_commit(&cx.empty[stage]);
+        __syncwarp();
         if (++cx.m_stage == STAGES) {
           cx.m_stage = 0;
           cx.m_phase ^= 1;
         }
       }
-      if constexpr (PAIR) mma_commit_pair(&cx.tfull[acc]);
-      else mma_commit(&cx.tfull[acc]);
+      if (elect_one()) {
+        if constexpr (PAIR) mma_commit_pair(&cx.tfull[acc]);
+        else mma_commit(&cx.tfull[acc]);
+      }
+      __syncwarp();
     }
   }
-  GTRACE(4);
+  if (cx.lane == 0) GTRACE(4);
 }
 
 // ---- epilogue warps 2..9 (each CTA: its 128 rows of the tile)
@@ -635,7 +642,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (cx.warp == 0) {
     if (cx.lane == 0) gemm_produce(cx, &tmA, &tmB, g, sc);
   } else if (cx.warp == 1) {
-    if (cx.lane == 0 && cx.leader) gemm_mma(cx, g, sc, ep);
+    if (cx.leader) gemm_mma(cx, g, sc, ep);  // (whole warp)
   } else {
     gemm_epilogue(cx, &tmC, g, M, sc, ep);
   }
