@@ -242,7 +242,8 @@ struct GemmCta {
   }
 };
 
-// ---- TMA producer (one lane per CTA; both CTAs of a pair load their halves)
+// ---- TMA producer: the whole warp 0 runs the (warp-uniform) loop, one elected lane issues (both CTAs of a
+// pair load their halves)
 template <int BN, int STAGES, int EPI, bool PAIR>
 NMT_DEV void gemm_produce(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap* tmA, const CUtensorMap* tmB,
                           const GemmShape& g, const Sched& sc) {
@@ -266,16 +267,19 @@ NMT_DEV void gemm_produce(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap*
         const int arow = tc.m * CM + cx.rank * BM, brow = tc.n * BN + cx.rank * S::B_ROWS + g.n_off;
         const int bx = g.b_panel_rows ? 0 : boff + kb * BK;
         const int by = g.b_panel_rows ? (boff / BK + kb) * g.b_panel_rows + brow : brow;
-        if constexpr (PAIR) {
-          if (cx.leader) mbar_arrive_expect_tx(&cx.full[stage], 2 * (S::A_BYTES + S::B_BYTES));
-          else mbar_arrive_cluster(full0 + stage * 8);
-          tma_load_2d_pair(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK, arow);
-          tma_load_2d_pair(tmB, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
-        } else {
-          mbar_arrive_expect_tx(&cx.full[stage], S::A_BYTES + S::B_BYTES);
-          tma_load_2d(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK, arow);
-          tma_load_2d(tmB, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
+        if (elect_one()) {
+          if constexpr (PAIR) {
+            if (cx.leader) mbar_arrive_expect_tx(&cx.full[stage], 2 * (S::A_BYTES + S::B_BYTES));
+            else mbar_arrive_cluster(full0 + stage * 8);
+            tma_load_2d_pair(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK, arow);
+            tma_load_2d_pair(tmB, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
+          } else {
+            mbar_arrive_expect_tx(&cx.full[stage], S::A_BYTES + S::B_BYTES);
+            tma_load_2d(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK, arow);
+            tma_load_2d(tmB, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
+          }
         }
+        __syncwarp();
         if (++cx.p_stage == STAGES) {
           cx.p_stage = 0;
           cx.p_phase ^= 1;
@@ -640,7 +644,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const Sched sc = make_sched<EPI>(g, M, CM, BN, cx.nunits);
   if ((EPI == EPI_LSE || EPI == EPI_TOPK) && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
   if (cx.warp == 0) {
-    if (cx.lane == 0) gemm_produce(cx, &tmA, &tmB, g, sc);
+    gemm_produce(cx, &tmA, &tmB, g, sc);  // (whole warp)
   } else if (cx.warp == 1) {
     if (cx.leader) gemm_mma(cx, g, sc, ep);  // (whole warp)
   } else {
