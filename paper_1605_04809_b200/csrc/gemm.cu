@@ -395,10 +395,9 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap
       const uint32_t aph = single_acc<EPI>() ? it & 1 : (it >> 1) & 1;
       const int colbase = n * BN + half * COLS;
       // EPI_GRU: this warp's COLS = 128 columns are one 32-unit group [r | u | h~ | pad] of its row, done
-      // in 4 chunks of 8 units.  A chunk's gx (r, u, x) and previous-state values arrive as 256-bit loads
-      // (full 32-byte sectors) issued two chunks ahead; the first two are issued before the accumulator
-      // wait, so their latency hides under the main loop.
-      float gin[EPI == EPI_GRU ? 2 : 1][4][8];
+      // in 4 chunks of 8 units.  The gx (r, u, x) and previous-state values arrive as 256-bit loads (full
+      // 32-byte sectors), all issued before the accumulator wait, so their latency hides under the main loop.
+      float gin[EPI == EPI_GRU ? 4 : 1][4][8];
       const float* gxr = nullptr;
       const float* sp = nullptr;
       auto gru_fetch = [&](int c, float(&b)[4][8]) {
@@ -415,16 +414,25 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap
           gxr = ep.gx + (int64_t)(y < 0 ? ep.y_bos : y) * ep.gx_ld + j0;
           sp = ep.S + (int64_t)ep.row_src[grow] * ep.Hp + j0;
         }
-        gru_fetch(0, gin[0]);
-        gru_fetch(1, gin[1]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) gru_fetch(c, gin[c]);  // all four chunks in flight under the main loop
       }
       float s1in[EPI == EPI_GRU2 ? 4 : 1][8];  // EPI_GRU2: the row's s1 for the group's 32 units
+      float bia[EPI == EPI_GRU2 ? 2 : 1][3][8];  // EPI_GRU2: b_nl (r, u) and bx_nl, two chunks ahead
+      auto bias_fetch = [&](int c, float(&b)[3][8]) {
+        const int jb = (colbase >> 7) * 32 + 8 * c;
+        ld8_nc(ep.b_nl + jb, b[0]);
+        ld8_nc(ep.b_nl + ep.Hp + jb, b[1]);
+        ld8_nc(ep.bx_nl + jb, b[2]);
+      };
       if constexpr (EPI == EPI_GRU2) {
         if (valid) {
           const float* s1p = ep.S1 + (int64_t)grow * ep.Hp + (colbase >> 7) * 32;
 #pragma unroll
           for (int c = 0; c < 4; ++c) ld8(s1p + 8 * c, s1in[c]);
         }
+        bias_fetch(0, bia[0]);
+        bias_fetch(1, bia[1]);
       }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
@@ -503,14 +511,13 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap
           reg_dep8(vr);
           reg_dep8(vu);
           reg_dep8(vx);
-          float(&b)[4][8] = gin[c & 1];
+          float(&b)[4][8] = gin[c];
           float o[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float rg = gru_sigm(b[0][i] + vr[i]), ug = gru_sigm(b[1][i] + vu[i]);
             o[i] = ug * b[3][i] + (1.f - ug) * gru_tanh(rg * vx[i] + b[2][i]);
           }
-          if (c + 2 < 4) gru_fetch(c + 2, gin[c & 1]);
           if (valid) {
             st8(s1 + 8 * c, o);
             gru_store4(xo + 8 * c, ep.lo_x, o[0], o[1], o[2], o[3]);
@@ -538,20 +545,19 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap
           tmem_ld8_nowait(t2 + 64 + 8 * c, cx8);
           tmem_wait_ld();
           reg_dep8(hx); reg_dep8(r1); reg_dep8(u1); reg_dep8(r2); reg_dep8(u2); reg_dep8(cx8);
+          float(&bb)[3][8] = bia[c & 1];
           if (valid) {
-            float br[8], bu[8], bx[8], o[8];
-            ld8_nc(ep.b_nl + j0 + 8 * c, br);
-            ld8_nc(ep.b_nl + ep.Hp + j0 + 8 * c, bu);
-            ld8_nc(ep.bx_nl + j0 + 8 * c, bx);
+            float o[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              const float rg = gru_sigm((r1[i] + r2[i]) + br[i]), ug = gru_sigm((u1[i] + u2[i]) + bu[i]);
-              o[i] = ug * s1in[c][i] + (1.f - ug) * gru_tanh(rg * (hx[i] + bx[i]) + cx8[i]);
+              const float rg = gru_sigm((r1[i] + r2[i]) + bb[0][i]), ug = gru_sigm((u1[i] + u2[i]) + bb[1][i]);
+              o[i] = ug * s1in[c][i] + (1.f - ug) * gru_tanh(rg * (hx[i] + bb[2][i]) + cx8[i]);
             }
             if (so) st8(so + 8 * c, o);
             gru_store4(xo + 8 * c, ep.lo_x, o[0], o[1], o[2], o[3]);
             gru_store4(xo + 8 * c + 4, ep.lo_x, o[4], o[5], o[6], o[7]);
           }
+          if (c + 2 < 4) bias_fetch(c + 2, bia[c & 1]);
         }
       } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
 #pragma unroll 1
