@@ -236,7 +236,7 @@ struct nmt_model {
   float* W_o32 = nullptr;         // [V][Ep]
   float* b_o = nullptr;           // [V]
   bool use_pair = true;  // CTA-pair (cta_group::2) GEMMs where the shapes allow (NMT_PAIR=0 disables)
-  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128, tm_Wh1g, tm_Wg2i;
+  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128, tm_Wh1g, tm_Wg2i, tm_Wro64;
   // encoder workspace
   int Tpad = 0;
   __nv_bfloat16* ctxbf = nullptr; // [Tpad][4Hp]
@@ -1071,6 +1071,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, 128);
   m->tm_Wg2i = make_tmap_bf16(m->W_g2i, 4 * Hp, sf * ldg2, 128);
   m->tm_Wro = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 128);
+  m->tm_Wro64 = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 64);  // (256 x 128 CTA-pair tiles: 64-row halves)
   m->tm_Wo = make_tmap_bf16(m->W_o, (uint64_t)Vp * sf * Ep / 64, 64, 256);     // panel layout
   m->tm_Wo128 = make_tmap_bf16(m->W_o, (uint64_t)Vp * sf * Ep / 64, 64, 128);  // CTA-pair vocabulary GEMM: half tiles
 
@@ -1431,14 +1432,40 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
     }
     if (!stage_skipped(ST_GRU2)) { ProfScope p_(m, ST_GRU2); step_elementwise(EW_GRU2, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   }
-  if (!stage_skipped(ST_GEMM_RO)) {
+#ifdef NO_FUSED_RO
+  if (false) {
+#else
+  if (m->use_pair && !stage_skipped(ST_GEMM_RO) && !stage_skipped(ST_READOUT)) {
+#endif
+    // D7: GEMM [c | s2] . [W_ctx; W_l] with the readout in its epilogue (one launch, no RO partials)
     ProfScope p_(m, ST_GEMM_RO);
     GemmShape g = gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp);
-    gemm_auto(m, m->tm_X, m->tm_Wro, g, m->RO_buf, m->ROp, rps, R_max, st);
-    d.ks_ro = g.reg_ks[0];
-    d.ps_ro = (int64_t)rps * m->ROp;
+    EpiParams ep{};
+    ep.ldc = m->ROp;
+    ep.Eproj = m->Eproj;
+    ep.V = m->V;
+    ep.E = m->E;
+    ep.Ep = Ep;
+    ep.maxout = m->maxout;
+    ep.Tout = ms ? nullptr : c->T;
+    ep.A_t = m->A_t;
+    ep.lda_t = d.lda_t;
+    ep.lo_t = d.lo_t;
+    ep.row_y = m->row_y;
+    ep.row_dst = m->row_dst;
+    ep.gs = d.gs;
+    ep.row_grp = d.row_grp;
+    gemm_readout_pair(m->tm_X, m->tm_Wro64, g, ep, R_max, st);
+  } else {  // (1-CTA GEMM mode, diagnostics): split-K GEMM + k_readout
+  if (!stage_skipped(ST_GEMM_RO)) {
+      ProfScope p_(m, ST_GEMM_RO);
+      GemmShape g = gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp);
+      gemm_auto(m, m->tm_X, m->tm_Wro, g, m->RO_buf, m->ROp, rps, R_max, st);
+      d.ks_ro = g.reg_ks[0];
+      d.ps_ro = (int64_t)rps * m->ROp;
+    }
+    if (!stage_skipped(ST_READOUT)) { ProfScope p_(m, ST_READOUT); step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   }
-  if (!stage_skipped(ST_READOUT)) { ProfScope p_(m, ST_READOUT); step_elementwise(EW_READOUT, d, a, c->S, c->T, c->logZ, c->amax, R_max, st); }
   if (m->vs_world > 1) {  // vocab-parallel (NEXT-2): this rank's slice, ONE all-gather, rank-order combine
     ensure_xbuf(m, m->vs_world);
     {
@@ -3086,7 +3113,7 @@ nmt_status nmt_debug_intermediates(nmt_ctx* c, nmt_state node, float* s1, float*
 
 nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_t epi, int32_t ksplit, int32_t iters,
                           float* ms_out) {
-  if (M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || !ms_out || (epi == 0 && N % 128) || (epi >= 1 && N % 256) || epi > 4)
+  if (M <= 0 || N <= 0 || K <= 0 || K % 64 || iters <= 0 || !ms_out || (epi == 0 && N % 128) || (epi >= 1 && epi != 5 && N % 256) || epi > 5)
     return fail(NMT_ERR_INVALID_ARG, "nmt_bench_gemm: bad shape");
   return guard([&] {
     cudaStream_t st;
@@ -3110,7 +3137,7 @@ nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_
       CK(cudaMemcpy(b, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice));
     }
     CUtensorMap ta = make_tmap_bf16(a, Mp, sf * K, 128), tb = make_tmap_bf16(b, N, sf * K, epi >= 1 ? 256 : 128);
-    CUtensorMap tb128 = make_tmap_bf16(b, N, sf * K, 128);
+    CUtensorMap tb128 = make_tmap_bf16(b, N, sf * K, 128), tb64 = make_tmap_bf16(b, N, sf * K, 64);
     GemmShape g = gemm_shape(M, nullptr, N, K, 0, split != 0, K, K);
     g.ksplit = ksplit;
     auto run = [&] {
@@ -3118,6 +3145,7 @@ nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_
       else if (epi == 4) gemm_lse_pair(ta, tb128, g, part, N, st, cpm);
       else if (epi == 2) gemm_store256(ta, tb, g, c, N, ksplit * Mp, nullptr, M, st, (size_t)Mp * N);
       else if (epi == 3) gemm_store_pair(ta, tb128, g, c, N, ksplit * Mp, nullptr, M, st, (size_t)Mp * N);
+      else if (epi == 5) gemm_store_pair128(ta, tb64, g, c, N, ksplit * Mp, nullptr, M, st, (size_t)Mp * N);
       else gemm_store(ta, tb, g, c, N, ksplit * Mp, nullptr, M, st, (size_t)Mp * N);
     };
     for (int i = 0; i < 3; ++i) run();

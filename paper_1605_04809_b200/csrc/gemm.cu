@@ -42,6 +42,9 @@ constexpr int EPI_GRU = 3;  // fused GRU gates (one tile per item like EPI_STORE
 // rows hx, r, u (MMA N = 192 over the first 96 rows of each CTA's half) into accumulator D1, the c K range
 // rows r, u, cx (N = 192 from row 32) into D2, so no zero block is multiplied; single-buffered TMEM
 constexpr int EPI_GRU2 = 4;
+// fused readout (D7) on 256 x 128 CTA-pair tiles: each epilogue warp's 64 columns give 32 maxout (or 64
+// tanh) outputs of its row
+constexpr int EPI_READOUT = 5;
 template <int EPI>
 constexpr bool single_acc() { return EPI == EPI_GRU2; }
 constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant, each owning half of the tile's columns
@@ -419,6 +422,16 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap
       }
       float s1in[EPI == EPI_GRU2 ? 4 : 1][8];  // EPI_GRU2: the row's s1 for the group's 32 units
       float bia[EPI == EPI_GRU2 ? 2 : 1][3][8];  // EPI_GRU2: b_nl (r, u) and bx_nl, two chunks ahead
+      float epj[EPI == EPI_READOUT ? COLS / 8 : 1][8];  // EPI_READOUT: Eproj[y] at the warp's columns
+      if constexpr (EPI == EPI_READOUT) {
+        if (valid) {
+          const int dst = ep.row_dst[grow];
+          const int y = dst >= 0 ? ep.row_y[grow] : -1;
+          const float* epr = ep.Eproj + (int64_t)(y < 0 ? ep.V : y) * ep.ldc + colbase;
+#pragma unroll
+          for (int c = 0; c < COLS / 8; ++c) ld8_nc(epr + 8 * c, epj[c]);
+        }
+      }
       auto bias_fetch = [&](int c, float(&b)[3][8]) {
         const int jb = (colbase >> 7) * 32 + 8 * c;
         ld8_nc(ep.b_nl + jb, b[0]);
@@ -558,6 +571,61 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap
             gru_store4(xo + 8 * c + 4, ep.lo_x, o[4], o[5], o[6], o[7]);
           }
           if (c + 2 < 4) bias_fetch(c + 2, bia[c & 1]);
+        }
+      } else if constexpr (EPI == EPI_READOUT) {
+        static_assert(COLS == 64, "EPI_READOUT: 64 readout columns per epilogue warp");
+        // (tcgen05.ld / wait are warp-collective: every lane loads, only valid rows write)
+        int dst = -1;
+        if (valid) dst = ep.row_dst[grow];
+        float* tr = dst >= 0 ? (ep.gs ? ep.gs[ep.row_grp[grow]].T : ep.Tout) + (int64_t)dst * ep.Ep : nullptr;
+        __nv_bfloat16* at = ep.A_t + (int64_t)grow * ep.lda_t;
+        const int E = ep.E;
+        // 8 outputs t[k0 .. k0 + 8) per pass: maxout pairs columns (2k, 2k + 1) (16 columns), tanh 8
+        const int npass = ep.maxout ? 4 : 8;
+#pragma unroll
+        for (int ps = 0; ps < 8; ++ps) {
+          if (ps >= npass) break;
+          float t[8];
+          if (ep.maxout) {
+            float a[16];
+            tmem_ld8_nowait(tbase + 16 * ps, a);
+            tmem_ld8_nowait(tbase + 16 * ps + 8, a + 8);
+            tmem_wait_ld();
+            reg_dep8(a);
+            reg_dep8(a + 8);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float* e = epj[(16 * ps + 2 * i) / 8];
+              const int o = (2 * i) % 8;
+              t[i] = fmaxf(a[2 * i] + e[o], a[2 * i + 1] + e[o + 1]);
+            }
+          } else {
+            float a[8];
+            tmem_ld8_nowait(tbase + 8 * ps, a);
+            tmem_wait_ld();
+            reg_dep8(a);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) t[i] = gru_tanh(a[i] + epj[ps][i]);
+          }
+          if (!valid) continue;
+          const int k0 = (ep.maxout ? colbase / 2 : colbase) + 8 * ps;
+          float hi[8], lo[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int k = k0 + i;
+            t[i] = k < E ? t[i] : 0.f;  // (t -> arena, zero past E)
+            const float av = k < E ? t[i] : ((k == E || (k == E + 1 && ep.lo_t == 0)) ? 1.f : 0.f);
+            hi[i] = av;
+            lo[i] = k < E ? av - __bfloat162float(__float2bfloat16_rn(av)) : 0.f;  // (bias columns: lo 0)
+          }
+          if (tr && k0 < ep.Ep) st8(tr + k0, t);
+          if (k0 < ep.Ep) {
+            *reinterpret_cast<uint4*>(at + k0) = make_uint4(gru_pk(hi[0], hi[1]), gru_pk(hi[2], hi[3]),
+                                                            gru_pk(hi[4], hi[5]), gru_pk(hi[6], hi[7]));
+            if (ep.lo_t > 0)
+              *reinterpret_cast<uint4*>(at + ep.lo_t + k0) = make_uint4(gru_pk(lo[0], lo[1]), gru_pk(lo[2], lo[3]),
+                                                                        gru_pk(lo[4], lo[5]), gru_pk(lo[6], lo[7]));
+          }
         }
       } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
 #pragma unroll 1
@@ -836,6 +904,13 @@ void gemm_store_pair(const CUtensorMap& a, const CUtensorMap& b_half, const Gemm
   launch<256, 5, EPI_STORE, true>(a, b_half, out_map(out, out_rows, ldc), g, ep, M_max, st);
 }
 
+// fp32 output GEMM on CTA pairs with 256 x 128 tiles (measurement / engine check of the BN = 128 pair shape)
+void gemm_store_pair128(const CUtensorMap& a, const CUtensorMap& b_q, const GemmShape& g, float* out, int ldc,
+                        int out_rows, const float* bias, int M_max, cudaStream_t st, size_t split_stride) {
+  const EpiParams ep = store_params(g, 128, out, ldc, bias, split_stride);
+  launch<128, 6, EPI_STORE, true>(a, b_q, out_map(out, out_rows, ldc), g, ep, M_max, st);
+}
+
 // fused vocabulary GEMM + online log-sum-exp partials; BN = 256.
 void gemm_gru_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, const EpiParams& ep, int M_max,
                    cudaStream_t st) {
@@ -850,6 +925,14 @@ void gemm_gru2_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmS
   if (gemm_ks_max(g) != 1 || g.nreg != 1 || ep.Hp % BK)
     throw NmtError(NMT_ERR_INVALID_ARG, "gemm: the fused GRU2 epilogue needs the full K sum in one region");
   launch<256, 5, EPI_GRU2, true>(a, b_half, b_half /*unused*/, g, ep, M_max, st);
+}
+
+void gemm_readout_pair(const CUtensorMap& a, const CUtensorMap& b_q, const GemmShape& g, const EpiParams& ep, int M_max,
+                       cudaStream_t st) {
+  gemm_validate(g, 128);
+  if (gemm_ks_max(g) != 1 || g.nreg != 1)
+    throw NmtError(NMT_ERR_INVALID_ARG, "gemm: the fused readout epilogue needs the full K sum in one region");
+  launch<128, 8, EPI_READOUT, true>(a, b_q, b_q /*unused*/, g, ep, M_max, st);
 }
 
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,

@@ -126,6 +126,13 @@ struct EpiParams {
   const float* b_nl;       // [2Hp]
   const float* bx_nl;      // [Hp]
   int x_col;               // column of s2 in X
+  // EPI_READOUT (fused readout D7; BN = 128 CTA-pair tiles, no split-K): t = maxout / tanh of
+  // (acc + Eproj[y]) -> arena T (slot row_dst) and the vocabulary GEMM's A operand (bias columns at E)
+  const float* Eproj;      // [V + 1][ROp] (row V: BOS / dead rows)
+  int V, E, Ep, maxout;
+  float* Tout;             // arena t [.][Ep]
+  __nv_bfloat16* A_t;      // [R][lda_t] (lo at +lo_t when > 0)
+  int lda_t, lo_t;
 };
 constexpr int kTopK = 8;  // NMT_TOPK_MAX: words per row kept by the top-k vocabulary epilogue
 
@@ -148,12 +155,18 @@ void gemm_topk_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmS
 void gemm_lse_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float4* part, int n_valid,
                    cudaStream_t st, int* cpm_out);
 // GEMM s.[U|Ux] with the GRU gates fused into the epilogue (CTA pairs, no split-K); see EPI_GRU
+void gemm_store_pair128(const CUtensorMap& a, const CUtensorMap& b_q, const GemmShape& g, float* out, int ldc,
+                        int out_rows, const float* bias, int M_max, cudaStream_t st, size_t split_stride = 0);
 void gemm_gru_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, const EpiParams& ep, int M_max,
                    cudaStream_t st);
 // GEMM [s1 | c] . W_g2 (interleaved per 32-unit group [hx | r | u | cx]) with the decoder's GRU2 fused
 // into the epilogue (EPI_GRU2; CTA pairs, no split-K, no partials)
 void gemm_gru2_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, const EpiParams& ep, int M_max,
                     cudaStream_t st);
+// GEMM [c | s2] . [W_ctx; W_l] with the readout (maxout or tanh over + Eproj[y]) fused into the epilogue
+// (EPI_READOUT; CTA pairs with 256 x 128 tiles, `b_q` = W_ro map with a 64-row box, no split-K)
+void gemm_readout_pair(const CUtensorMap& a, const CUtensorMap& b_q, const GemmShape& g, const EpiParams& ep, int M_max,
+                       cudaStream_t st);
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
               cudaStream_t st, int* cpm_out);
 
