@@ -243,6 +243,14 @@ struct nmt_model {
   float* hbuf = nullptr;
   float* enc_mean = nullptr;
   float* ksplit_buf = nullptr;  // split-K partials of the pctx GEMM
+  // projected-context step (D5 folded into D6 / D7): per context cw = [ctx.(W_g2 c rows) ; ctx.W_ctx] as B
+  // operands [NW][2 Apad] (hi | lo), NW = 4Hp + ROp rows, Apad = roundup(max_src_len, 64) token columns
+  int Apad = 0, NW = 0;
+  // E7 and the cw projections in ONE GEMM ctx . Wcat^T: Wcat = [Wc_att ; W_g2i c columns ; W_ro c columns]
+  // ([Cp + NW][2 Cp] bf16 hi | lo; m->Watt points at its first Cp rows)
+  CUtensorMap tm_Wcat;
+  int NCp = 0;                // Wcat rows, Cp + NW padded to the 256-column tile (zero rows)
+  float* enc_part = nullptr;  // [kEncSplit][Tpad][NCp] split-K partials
   int* bar = nullptr;
   unsigned enc_epoch = 0;      // encodes since the last reset of hbuf / bar (k_enc_recur tags)
   int* d_src = nullptr;
@@ -350,7 +358,7 @@ struct nmt_model {
 
 static void free_all_model(nmt_model* m) {
   for (float** p : {&m->EncIn, &m->Uarr, &m->W_initT, &m->b_init, &m->b_att, &m->U_att, &m->Ex, &m->b_nl, &m->bx_nl,
-                    &m->Eproj, &m->W_o32, &m->b_o, &m->hbuf, &m->enc_mean, &m->ksplit_buf})
+                    &m->Eproj, &m->W_o32, &m->b_o, &m->hbuf, &m->enc_mean, &m->ksplit_buf, &m->enc_part})
     dfree(*p);
   for (__nv_bfloat16** p : {&m->W_g2i, &m->W_h1g, &m->Watt, &m->W_h1, &m->W_q, &m->W_g2, &m->W_ro, &m->W_o, &m->ctxbf}) dfree(*p);
   dfree(m->bar);
@@ -495,6 +503,11 @@ struct nmt_ctx {
   float* ctx = nullptr;   // [Tx][Cp]
   float* pctx = nullptr;  // [Tx][Cp]
   float* epctx = nullptr;  // [Tx][Cp] exp(2 pctx), exponent clamped (attention, D4)
+  // projected-context operands (nmt_encode only): cw [NW][2 Apad] bf16, rows 0..4Hp = ctx.(c rows of W_g2i),
+  // rows 4Hp.. = ctx.W_ctx, columns = source positions (hi | lo); zero past Tx
+  __nv_bfloat16* cw = nullptr;
+  CUtensorMap tm_cw_g2, tm_cw_ro;  // B2 maps for the G2 (128-row box) and readout (64-row box) GEMMs
+  bool has_cw = false;
   int node_cap = 0, slot_cap = 0;
   int64_t hcap = 0;
   int* counters = nullptr;
@@ -717,6 +730,7 @@ nmt_ctx::~nmt_ctx() {
   for (int** p : {&counters, &node_word, &node_parent, &node_src, &node_slot, &node_claim, &hvals, &amax}) dfree(*p);
   dfree(hkeys);
   for (float** p : {&ctx, &pctx, &epctx, &S, &T, &logZ}) dfree(*p);
+  dfree(cw);
   model_release(m);
 }
 
@@ -1081,6 +1095,27 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   m->hbuf = dalloc<float>(2 * 2 * 131072);  // [2 dirs][stride >= 2Hp] 64-bit tagged words (1 MB)
   m->enc_mean = dalloc<float>(2 * H);
   m->ksplit_buf = dalloc<float>((size_t)8 * m->Tpad * Cp);
+  m->Apad = round_up(m->maxTx, 64);
+  m->NW = 4 * Hp + ROp;
+  m->NCp = round_up(Cp + m->NW, 256);
+  m->enc_part = dalloc<float>((size_t)kEncSplit * m->Tpad * m->NCp);
+  {  // Wcat: rows [0, Cp) = Wc_att (hi | lo), then the c columns of W_g2i and of W_ro (lo halves in split mode)
+    const int NC = m->NCp, ldg2 = Hp + Cp, ldro = Cp + Hp, sf = m->sf;
+    __nv_bfloat16* Wc = dalloc<__nv_bfloat16>((size_t)NC * 2 * Cp);
+    CK(cudaMemsetAsync(Wc, 0, (size_t)NC * 2 * Cp * 2, st));
+    CK(cudaMemcpyAsync(Wc, m->Watt, (size_t)Cp * 2 * Cp * 2, cudaMemcpyDeviceToDevice, st));
+    for (int h = 0; h < (m->split ? 2 : 1); ++h) {
+      CK(cudaMemcpy2DAsync(Wc + (size_t)Cp * 2 * Cp + h * Cp, (size_t)2 * Cp * 2, m->W_g2i + Hp + h * ldg2,
+                           (size_t)sf * ldg2 * 2, (size_t)Cp * 2, 4 * Hp, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpy2DAsync(Wc + (size_t)(Cp + 4 * Hp) * 2 * Cp + h * Cp, (size_t)2 * Cp * 2, m->W_ro + h * ldro,
+                           (size_t)sf * ldro * 2, (size_t)Cp * 2, ROp, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    dfree(m->Watt);
+    m->Watt = Wc;
+    m->tm_Watt = make_tmap_bf16(m->Watt, Cp, 2 * Cp, 128);
+    m->tm_Wcat = make_tmap_bf16(m->Watt, NC, 2 * Cp, 256);
+  }
   m->bar = dalloc<int>(2);
   m->d_src = dalloc<int>(m->maxTx);
   m->tm_ctxbf = make_tmap_bf16(m->ctxbf, m->Tpad, 4 * Hp, 128);
@@ -1346,9 +1381,16 @@ struct MultiStep {
 
 // one decoder forward step over the rows planned in m->row_* (count at c->counters[CNT_R]; or, for
 // a multi-context step, *ms->R_dev rows of the contexts in ms->gs, dead rows flagged row_dst < 0)
-static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = nullptr) {
+static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = nullptr, bool explicit_c = false) {
   cudaStream_t st = m->st;
   StepDev d = step_view(m, c);
+  // projected-context step (one context, CTA-pair GEMMs): attention writes alpha (bf16) into the c slot of X
+  // and the G2 / readout GEMMs multiply it with the context's cw = ctx . W (K = Kc) instead of c with W
+  // (K = Cp); c itself is never formed.  Multi-context steps (rows of several sentences share the GEMMs) and
+  // nmt_debug_intermediates (which reports c) take the explicit path.
+  const bool proj = !ms && !explicit_c && c->has_cw && m->use_pair;
+  const int Kc = proj ? round_up(c->Tx, 64) : 0;
+  d.proj_k = Kc;
   AttnCtx a{c->pctx, c->ctx, m->U_att, m->c_tt, c->Tx, c->epctx, c->counters};
   if (ms) {
     d.R = ms->R_dev;
@@ -1403,7 +1445,12 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
   if (m->use_pair && !stage_skipped(ST_GEMM_G2) && !stage_skipped(ST_GRU2)) {
     // D6: GEMM [s1 | c] . W_g2 with GRU2 in its epilogue (one launch, no G2 partials)
     ProfScope p_(m, ST_GEMM_G2);
-    GemmShape g = gemm_shape(0, Rd, 4 * Hp, Hp + Cp, 0, sp, 4 * Hp, Hp + Cp);
+    GemmShape g = gemm_shape(0, Rd, 4 * Hp, Hp + (proj ? Kc : Cp), 0, sp, 4 * Hp, Hp + Cp);
+    if (proj) {  // the alpha K range [Hp, Hp + Kc) reads B from cw
+      g.b2_kb0 = Hp / 64;
+      g.b2_kb1 = (Hp + Kc) / 64;
+      g.b2_lo_off = m->Apad;
+    }
     EpiParams ep{};
     ep.S1 = m->S1;
     ep.X = m->X;
@@ -1417,7 +1464,7 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
     ep.b_nl = m->b_nl;
     ep.bx_nl = m->bx_nl;
     ep.x_col = Hp + Cp;
-    gemm_gru2_pair(m->tm_X, m->tm_Wg2i, g, ep, R_max, st);
+    gemm_gru2_pair(m->tm_X, m->tm_Wg2i, g, ep, R_max, st, proj ? &c->tm_cw_g2 : nullptr);
   } else {  // (1-CTA GEMM mode, diagnostics): region GEMM with split-K partials + k_gru2
     if (!stage_skipped(ST_GEMM_G2)) {
       ProfScope p_(m, ST_GEMM_G2);
@@ -1439,7 +1486,13 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
 #endif
     // D7: GEMM [c | s2] . [W_ctx; W_l] with the readout in its epilogue (one launch, no RO partials)
     ProfScope p_(m, ST_GEMM_RO);
-    GemmShape g = gemm_shape(0, Rd, m->ROp, Cp + Hp, Hp, sp, 4 * Hp, Cp + Hp);
+    GemmShape g = gemm_shape(0, Rd, m->ROp, (proj ? Kc : Cp) + Hp, Hp, sp, 4 * Hp, Cp + Hp);
+    if (proj) {  // alpha K range [0, Kc) from cw, then s2 (A and B columns Cp - Kc further on)
+      g.b2_kb0 = 0;
+      g.b2_kb1 = Kc / 64;
+      g.b2_lo_off = m->Apad;
+      g.kjump = Cp - Kc;
+    }
     EpiParams ep{};
     ep.ldc = m->ROp;
     ep.Eproj = m->Eproj;
@@ -1455,7 +1508,7 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
     ep.row_dst = m->row_dst;
     ep.gs = d.gs;
     ep.row_grp = d.row_grp;
-    gemm_readout_pair(m->tm_X, m->tm_Wro64, g, ep, R_max, st);
+    gemm_readout_pair(m->tm_X, m->tm_Wro64, g, ep, R_max, st, proj ? &c->tm_cw_ro : nullptr);
   } else {  // (1-CTA GEMM mode, diagnostics): split-K GEMM + k_readout
   if (!stage_skipped(ST_GEMM_RO)) {
       ProfScope p_(m, ST_GEMM_RO);
@@ -1521,7 +1574,7 @@ static void run_call(nmt_model* m, nmt_ctx* c, const PlanIO& io, float* out_logp
 }
 
 // step one node (if not yet stepped) outside a score_batch; dst = scratch slot 1 when `scratch`
-static int step_single(nmt_model* m, nmt_ctx* c, int node, bool scratch) {
+static int step_single(nmt_model* m, nmt_ctx* c, int node, bool scratch, bool explicit_c = false) {
   cudaStream_t st = m->st;
   if (c->stale) c->sync_counters();
   if (node < 0 || node >= c->n_nodes) throw NmtError(NMT_ERR_BAD_STATE, "unknown state " + std::to_string(node));
@@ -1545,7 +1598,7 @@ static int step_single(nmt_model* m, nmt_ctx* c, int node, bool scratch) {
   CK(cudaMemcpyAsync(m->row_y, &info[0], 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(m->row_dst, &dst, 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(c->counters + CNT_R, &one, 4, cudaMemcpyHostToDevice, st));
-  run_step(m, c, 1);
+  run_step(m, c, 1, nullptr, explicit_c);
   if (!scratch) {
     CK(cudaMemcpyAsync(c->node_slot + node, &dst, 4, cudaMemcpyHostToDevice, st));
     const int ns = dst + 1;
@@ -1756,7 +1809,7 @@ static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
     m->pool_bytes -= std::min(m->pool_bytes, c->arena_bytes());
     m->refs.fetch_add(1);
   } else {
-    const size_t fixed = (size_t)3 * m->maxTx * m->Cp * 4 + CNT_N * 4;
+    const size_t fixed = (size_t)3 * m->maxTx * m->Cp * 4 + CNT_N * 4 + (size_t)m->NW * 2 * m->Apad * 2;
     m->admit_arena(fixed);
     c = new nmt_ctx();
     g_live_ctxs.fetch_add(1);
@@ -1769,6 +1822,9 @@ static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
     c->ctx = dalloc<float>((size_t)m->maxTx * m->Cp);
     c->pctx = dalloc<float>((size_t)m->maxTx * m->Cp);
     c->epctx = dalloc<float>((size_t)m->maxTx * m->Cp);
+    c->cw = dalloc<__nv_bfloat16>((size_t)m->NW * 2 * m->Apad);
+    c->tm_cw_g2 = make_tmap_bf16(c->cw, 4 * m->Hp, 2 * m->Apad, 128);
+    c->tm_cw_ro = make_tmap_bf16(c->cw + (size_t)4 * m->Hp * 2 * m->Apad, m->ROp, 2 * m->Apad, 64);
     c->counters = dalloc<int>(CNT_N);
     CK(cudaEventCreateWithFlags(&c->enc_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->enc_s0_ev, cudaEventDisableTiming));
@@ -1777,6 +1833,7 @@ static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
     g.release();
   }
   c->Tx = len;
+  c->has_cw = false;
   return c;
 }
 
@@ -1880,20 +1937,27 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
     CK(cudaEventRecord(c->enc_s0_ev, es));
     c->enc_s0_pending = true;
   }
-  if (!stage_skipped(ST_ENC_PCTX)) {  // E7: pctx = ctx.Wc_att + b_att
+  if (!stage_skipped(ST_ENC_PCTX)) {
+    // E7: pctx = ctx.Wc_att + b_att, and (CTA-pair models) the projected-context operands cw^T = W . ctx^T for
+    // the c rows of the fused GRU2 weights (W_g2i columns [Hp, Hp + Cp)) and W_ctx (W_ro columns [0, Cp)),
+    // so that the step's c . W = alpha . (ctx . W) (D5 folded into D6 / D7: K = roundup(Tx, 64) instead of
+    // Cp): ONE GEMM ctx . Wcat^T in the step's precision (single-pass bf16 in NMT_PREC_BF16, like the
+    // decoder's query GEMM; bf16x3 in NMT_PREC_FP32CLASS) and one reduce pass
     ProfScope p_(m, ST_ENC_PCTX);
-    // the attention keys follow the step's precision: single-pass bf16 in NMT_PREC_BF16 (like the
-    // decoder's query GEMM), bf16x3 in NMT_PREC_FP32CLASS
-    GemmShape g = gemm_shape(len, nullptr, m->Cp, m->Cp, 0, m->split, m->Cp, m->Cp);
-    {  // ~8 splits, none empty
-      const int nkb = g.passes * m->Cp / 64, chunk = (nkb + 7) / 8;
+    const bool cwx = m->use_pair;
+    const int NC = cwx ? m->NCp : m->Cp;
+    GemmShape g = gemm_shape(len, nullptr, NC, m->Cp, 0, m->split, m->Cp, m->Cp);
+    {  // <= kEncSplit splits, none empty
+      const int nkb = g.passes * m->Cp / 64, chunk = (nkb + kEncSplit - 1) / kEncSplit;
       g.ksplit = (nkb + chunk - 1) / chunk;
     }
-    const size_t stride = (size_t)m->Tpad * m->Cp;
-    gemm_store(m->tm_ctxbf, m->tm_Watt, g, m->ksplit_buf, m->Cp, g.ksplit * m->Tpad, nullptr, len, es, stride);
-    splitk_reduce_pctx(m->ksplit_buf, g.ksplit, stride, len, m->Cp, m->Cp, m->b_att, c->pctx, c->epctx,
-                       c->counters + CNT_BIGP, es);
+    const size_t stride = (size_t)m->Tpad * NC;
+    gemm_store256(m->tm_ctxbf, m->tm_Wcat, g, m->enc_part, NC, g.ksplit * m->Tpad, nullptr, len, es, stride);
+    enc_proj_reduce(m->enc_part, g.ksplit, stride, len, NC, m->Cp, m->b_att, c->pctx, c->epctx,
+                    c->counters + CNT_BIGP, m->NW, m->Apad, m->split, cwx ? c->cw : nullptr, es);
+    c->has_cw = cwx;
   }
+
   if (es != st) {
     CK(cudaEventRecord(c->enc_ev, es));
     c->enc_pending = true;
@@ -3086,7 +3150,7 @@ nmt_status nmt_debug_intermediates(nmt_ctx* c, nmt_state node, float* s1, float*
   return guard([&] {
     ModelLock lk(m);
     CK(cudaSetDevice(m->device));
-    step_single(m, c, (int)node, true);
+    step_single(m, c, (int)node, true, /*explicit_c=*/true);  // (reports c)
     cudaStream_t st = m->st;
     const int H = m->H, Hp = m->Hp, Cp = m->Cp;
     std::vector<float> hs1(Hp), hal(m->maxTx), hc(Cp), hs2(Hp), ht(m->Ep);

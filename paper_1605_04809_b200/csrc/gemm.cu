@@ -249,7 +249,7 @@ struct GemmCta {
 // pair load their halves)
 template <int BN, int STAGES, int EPI, bool PAIR>
 NMT_DEV void gemm_produce(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap* tmA, const CUtensorMap* tmB,
-                          const GemmShape& g, const Sched& sc) {
+                          const CUtensorMap* tmB2, const GemmShape& g, const Sched& sc) {
   using S = GemmSmem<BN, STAGES, EPI, PAIR>;
   constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR>::CM;
   const uint32_t full0 = PAIR ? mapa_shared(smem_u32(cx.full), 0) : 0;
@@ -268,18 +268,22 @@ NMT_DEV void gemm_produce(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap*
         const int stage = cx.p_stage;
         mbar_wait(&cx.empty[stage], cx.p_phase ^ 1);
         const int arow = tc.m * CM + cx.rank * BM, brow = tc.n * BN + cx.rank * S::B_ROWS + g.n_off;
-        const int bx = g.b_panel_rows ? 0 : boff + kb * BK;
-        const int by = g.b_panel_rows ? (boff / BK + kb) * g.b_panel_rows + brow : brow;
+        const bool in_b2 = kb >= g.b2_kb0 && kb < g.b2_kb1;  // (second B operand: never with B panels)
+        const int kj = (g.b2_kb1 > 0 && kb >= g.b2_kb1) ? g.kjump : 0;
+        const int bx = in_b2 ? (pass == 1 ? g.b2_lo_off : 0) + (kb - g.b2_kb0) * BK
+                             : (g.b_panel_rows ? 0 : boff + kb * BK + kj);
+        const int by = (!in_b2 && g.b_panel_rows) ? (boff / BK + kb) * g.b_panel_rows + brow : brow;
+        const CUtensorMap* tb = in_b2 ? tmB2 : tmB;
         if (elect_one()) {
           if constexpr (PAIR) {
             if (cx.leader) mbar_arrive_expect_tx(&cx.full[stage], 2 * (S::A_BYTES + S::B_BYTES));
             else mbar_arrive_cluster(full0 + stage * 8);
-            tma_load_2d_pair(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK, arow);
-            tma_load_2d_pair(tmB, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
+            tma_load_2d_pair(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK + kj, arow);
+            tma_load_2d_pair(tb, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
           } else {
             mbar_arrive_expect_tx(&cx.full[stage], S::A_BYTES + S::B_BYTES);
-            tma_load_2d(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK, arow);
-            tma_load_2d(tmB, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
+            tma_load_2d(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK + kj, arow);
+            tma_load_2d(tb, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
           }
         }
         __syncwarp();
@@ -707,7 +711,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (cx.warp == 0 && cx.lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    if (EPI == EPI_STORE) tma_prefetch(&tmC);
+    if (EPI == EPI_STORE || g.b2_kb1 > 0) tma_prefetch(&tmC);
   }
   cx.setup();
   if (threadIdx.x == 0) GTRACE(1);
@@ -718,7 +722,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const Sched sc = make_sched<EPI>(g, M, CM, BN, cx.nunits);
   if ((EPI == EPI_LSE || EPI == EPI_TOPK) && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
   if (cx.warp == 0) {
-    gemm_produce(cx, &tmA, &tmB, g, sc);  // (whole warp)
+    gemm_produce(cx, &tmA, &tmB, &tmC, g, sc);  // (whole warp; tmC = the second B operand when b2_kb1 > 0)
   } else if (cx.warp == 1) {
     if (cx.leader) gemm_mma(cx, g, sc, ep);  // (whole warp)
   } else {
@@ -919,20 +923,28 @@ void gemm_gru_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmSh
   launch<256, 5, EPI_GRU, true>(a, b_half, b_half /*unused*/, g, ep, M_max, st);
 }
 
+static void check_b2(const GemmShape& g, const CUtensorMap* b2) {
+  if (g.b2_kb1 > 0 && (!b2 || g.b2_kb0 >= g.b2_kb1 || g.b_panel_rows))
+    throw NmtError(NMT_ERR_INVALID_ARG, "gemm: bad second B operand range");
+}
+
+// `b2` (or null): second B operand for k-blocks [g.b2_kb0, g.b2_kb1) (projected-context step)
 void gemm_gru2_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, const EpiParams& ep, int M_max,
-                    cudaStream_t st) {
+                    cudaStream_t st, const CUtensorMap* b2) {
   gemm_validate(g, 256);
   if (gemm_ks_max(g) != 1 || g.nreg != 1 || ep.Hp % BK)
     throw NmtError(NMT_ERR_INVALID_ARG, "gemm: the fused GRU2 epilogue needs the full K sum in one region");
-  launch<256, 5, EPI_GRU2, true>(a, b_half, b_half /*unused*/, g, ep, M_max, st);
+  check_b2(g, b2);
+  launch<256, 5, EPI_GRU2, true>(a, b_half, b2 ? *b2 : b_half, g, ep, M_max, st);
 }
 
 void gemm_readout_pair(const CUtensorMap& a, const CUtensorMap& b_q, const GemmShape& g, const EpiParams& ep, int M_max,
-                       cudaStream_t st) {
+                       cudaStream_t st, const CUtensorMap* b2) {
   gemm_validate(g, 128);
   if (gemm_ks_max(g) != 1 || g.nreg != 1)
     throw NmtError(NMT_ERR_INVALID_ARG, "gemm: the fused readout epilogue needs the full K sum in one region");
-  launch<128, 8, EPI_READOUT, true>(a, b_q, b_q /*unused*/, g, ep, M_max, st);
+  check_b2(g, b2);
+  launch<128, 8, EPI_READOUT, true>(a, b_q, b2 ? *b2 : b_q, g, ep, M_max, st);
 }
 
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,

@@ -91,6 +91,11 @@ struct GemmShape {
                      // (every TMA box is one contiguous chunk): coordinate (0, kb * b_panel_rows + row)
   int n_off;         // EPI_LSE / EPI_TOPK: first B row (= vocabulary column) of the GEMM's N range (vocab
                      // slice of a vocab-parallel rank); reported columns are global
+  // second B operand (EPI_GRU2 / EPI_READOUT, the tensor map in the tmC slot): k-blocks [b2_kb0, b2_kb1) of
+  // the K range read B from it at k = (kb - b2_kb0) * 64 (+ b2_lo_off for the lo pass); k-blocks >= b2_kb1
+  // read A and B at k + kjump.  The projected-context step (D5 folded into D6/D7) uses it for the
+  // alpha K range, whose B rows are the context's ctx . W projections (nmt_ctx::cw).
+  int b2_kb0, b2_kb1, b2_lo_off, kjump;
 };
 
 struct EpiParams {
@@ -146,6 +151,13 @@ void splitk_reduce(const float* part, int ksplit, size_t stride, int M, int N, i
                    cudaStream_t st, __nv_bfloat16* out16 = nullptr);
 // the same for the attention keys: also out_e = exp(2 out) with the exponent clamped to +-kAttnExpClamp, and
 // bigp |= 1 where it was clamped
+// E7 pctx / exp(2 pctx) (+ b_att) from the split-K partials of the encoder's GEMM ctx . Wcat^T (columns < Cp)
+// and, when cw != null, the projected-context B operands cw[NW][2 Apad] (columns Cp.. transposed; bf16 hi | lo,
+// zero past Tx); Apad and NW multiples of 32
+constexpr int kEncSplit = 5;
+void enc_proj_reduce(const float* part, int ksplit, size_t stride, int Tx, int ldc, int Cp, const float* bias,
+                     float* pctx, float* epctx, int* bigp, int NW, int Apad, bool split, __nv_bfloat16* cw,
+                     cudaStream_t st);
 void splitk_reduce_pctx(const float* part, int ksplit, size_t stride, int M, int N, int ldc, const float* bias,
                         float* out, float* out_e, int* bigp, cudaStream_t st);
 void gemm_store_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float* out, int ldc,
@@ -160,13 +172,15 @@ void gemm_store_pair128(const CUtensorMap& a, const CUtensorMap& b_q, const Gemm
 void gemm_gru_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, const EpiParams& ep, int M_max,
                    cudaStream_t st);
 // GEMM [s1 | c] . W_g2 (interleaved per 32-unit group [hx | r | u | cx]) with the decoder's GRU2 fused
-// into the epilogue (EPI_GRU2; CTA pairs, no split-K, no partials)
+// into the epilogue (EPI_GRU2; CTA pairs, no split-K, no partials).  `b2`: the projected-context step's
+// second B operand (the context's ctx.[Wc|Wcx] rows for the alpha K range, GemmShape.b2_kb0/1), or null
 void gemm_gru2_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, const EpiParams& ep, int M_max,
-                    cudaStream_t st);
+                    cudaStream_t st, const CUtensorMap* b2 = nullptr);
 // GEMM [c | s2] . [W_ctx; W_l] with the readout (maxout or tanh over + Eproj[y]) fused into the epilogue
-// (EPI_READOUT; CTA pairs with 256 x 128 tiles, `b_q` = W_ro map with a 64-row box, no split-K)
+// (EPI_READOUT; CTA pairs with 256 x 128 tiles, `b_q` = W_ro map with a 64-row box, no split-K); `b2` as
+// for gemm_gru2_pair (the context's ctx.W_ctx rows)
 void gemm_readout_pair(const CUtensorMap& a, const CUtensorMap& b_q, const GemmShape& g, const EpiParams& ep, int M_max,
-                       cudaStream_t st);
+                       cudaStream_t st, const CUtensorMap* b2 = nullptr);
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
               cudaStream_t st, int* cpm_out);
 

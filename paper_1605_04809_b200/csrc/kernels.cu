@@ -144,6 +144,59 @@ void splitk_reduce_pctx(const float* part, int ksplit, size_t stride, int M, int
   CK_LAUNCH();
 }
 
+// E7 + projected-context operands in one pass over the split-K partials of the encoder's single GEMM
+// ctx . [Wc_att ; W_g2i c rows ; W_ro c rows]^T  (partials [ks][Tx..][ldc], ldc = Cp + NW):
+//   blocks [0, nb_p): pctx = sum + b_att and exp(2 pctx) (clamped, CNT_BIGP flag) for columns < Cp;
+//   blocks [nb_p, ..): 32 x 32 tiles of the remaining NW columns, transposed through shared memory into the
+//   B-operand rows cw[n][j] (bf16 hi at j, lo at Apad + j; zero for Tx <= j < Apad) of the D6 / D7 GEMMs'
+//   alpha K range (D5 folded into D6 / D7, nmt_ctx::cw).
+__global__ void __launch_bounds__(256) k_enc_proj_reduce(const float* __restrict__ part, int ksplit, size_t stride,
+                                                         int Tx, int ldc, int Cp, const float* __restrict__ bias,
+                                                         float* pctx, float* epctx, int* bigp, int nb_p, int NW,
+                                                         int Apad, int split, __nv_bfloat16* __restrict__ cw) {
+  pdl_enter();
+  if ((int)blockIdx.x < nb_p) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)Tx * Cp) return;
+    const int r = (int)(i / Cp), c = (int)(i % Cp);
+    float s = bias[c];
+    for (int k = 0; k < ksplit; ++k) s += part[k * stride + (size_t)r * ldc + c];
+    pctx[(size_t)r * Cp + c] = s;
+    bool big;
+    epctx[(size_t)r * Cp + c] = exp2x_clamped(s, big);
+    if (big) atomicOr(bigp, 1);
+    return;
+  }
+  __shared__ float tile[32][33];
+  const int t = blockIdx.x - nb_p, tj = Apad / 32;
+  const int n0 = (t / tj) * 32, j0 = (t % tj) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32 per pass
+  for (int jj = ty; jj < 32; jj += 8) {  // coalesced along the partials' columns n
+    const int j = j0 + jj;
+    float s = 0.f;
+    if (j < Tx)
+      for (int k = 0; k < ksplit; ++k) s += part[k * stride + (size_t)j * ldc + Cp + n0 + tx];
+    tile[jj][tx] = s;
+  }
+  __syncthreads();
+  for (int nn = ty; nn < 32; nn += 8) {  // coalesced along the B-operand rows' token columns j
+    const float v = tile[tx][nn];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    __nv_bfloat16* row = cw + (size_t)(n0 + nn) * 2 * Apad + j0 + tx;
+    row[0] = hi;
+    row[Apad] = __float2bfloat16_rn(split ? v - __bfloat162float(hi) : 0.f);
+  }
+}
+void enc_proj_reduce(const float* part, int ksplit, size_t stride, int Tx, int ldc, int Cp, const float* bias,
+                     float* pctx, float* epctx, int* bigp, int NW, int Apad, bool split, __nv_bfloat16* cw,
+                     cudaStream_t st) {
+  const int nb_p = (int)(((int64_t)Tx * Cp + 255) / 256);
+  const int nb_w = cw ? (NW / 32) * (Apad / 32) : 0;
+  launch_pdl(k_enc_proj_reduce, (unsigned)(nb_p + nb_w), 256, 0, st, part, ksplit, stride, Tx, ldc, Cp, bias, pctx,
+             epctx, bigp, nb_p, NW, Apad, (int)split, cw);
+  CK_LAUNCH();
+}
+
 // ===================================================================================== planner
 // Device-side state cache (SURVEY §8(a) D0; PAPER.md:109 "collapsed edges", :121 "Cache state
 // pointers and probabilities at target nodes").  Keys (parent, word) -> child id in an open-
@@ -777,6 +830,19 @@ __global__ void __launch_bounds__(256, 2) k_attention(StepDev d, AttnCtx a) {
     }
   }
   __syncthreads();
+  if (d.proj_k > 0) {  // projected-context step: alpha (bf16 hi | lo, zero past Tx) is the A operand of the
+                       // G2 / readout GEMMs, which multiply it with cw = ctx . W; no context pass
+    const int K = d.proj_k;
+    for (int i = threadIdx.x; i < nr * K; i += blockDim.x) {
+      const int rr = i / K, j = i % K;
+      const float v = j < Tx ? alpha[rr * Tx + j] : 0.f;
+      __nv_bfloat16* xp = d.X + (int64_t)(r0 + rr) * d.ldx + d.Hp + j;
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      xp[0] = h;
+      if (d.lo_x > 0) xp[d.lo_x] = __float2bfloat16_rn(v - __bfloat162float(h));
+    }
+    return;
+  }
   // context c = sum_j alpha_j ctx_j, ctx slices through the same ring (packed fp32 pairs)
   const float* cg = a.ctx + c0;
 #pragma unroll

@@ -100,6 +100,8 @@ struct StepDev {
   int ks_g1, ks_q, ks_g2[3], ks_ro;      // split-K partial counts of the decoder GEMM outputs
   int64_t ps_g1, ps_q, ps_g2, ps_ro;     // floats between consecutive partials
   int diag_attn_slow;                    // (diagnostic builds: force the attention's tanh path)
+  int proj_k;                            // projected-context step: attention writes alpha (bf16 hi | lo,
+                                         // zero past Tx) to X columns [Hp, Hp + proj_k) instead of c; 0: c
 };
 
 struct AttnCtx {

@@ -135,13 +135,16 @@ def test_score_batch_multi(readout, prec):
     assert lp[0] == lp[6] and ch[0] == ch[6]  # same (ctx, parent, word): same handle, same bits
     # the same request streams through per-context nmt_score_batch on fresh contexts: identical
     # child ids and argmax; log-probs equal up to fp32 summation order (the fused step's split-K
-    # factors and vocabulary runs depend on its total row count)
+    # factors and vocabulary runs depend on its total row count) in fp32class; in bf16 up to the
+    # operand rounding of the two D5-D7 forms (single context: alpha . (ctx . W) with bf16 alpha and
+    # ctx . W; multi-context: c . W with bf16 c, reading A30)
     fresh = [M.encode(s) for s in srcs]
     f1 = fresh[1].score_batch([0, 0], [0, 2, 4], [4, 5, 4, 10])
     f0 = fresh[0].score_batch([0], [0, 3], [6, 7, 8])
     f2 = fresh[2].score_batch([0], [0, 1], [9])
-    assert np.allclose(f1[0], lp[[0, 1, 6, 7]], atol=1e-4) and np.array_equal(f1[1], ch[[0, 1, 6, 7]])
-    assert np.allclose(f0[0], lp[2:5], atol=1e-4) and np.allclose(f2[0], lp[5:6], atol=1e-4)
+    at = 1e-4 if prec == "fp32class" else TOL[prec] / 4
+    assert np.allclose(f1[0], lp[[0, 1, 6, 7]], atol=at) and np.array_equal(f1[1], ch[[0, 1, 6, 7]])
+    assert np.allclose(f0[0], lp[2:5], atol=at) and np.allclose(f2[0], lp[5:6], atol=at)
     assert list(am) == [f1[2][0], f0[2][0], f2[2][0], f1[2][1]]
     # call 2: children of call 1 across contexts, against the oracle
     ctxs2 = [cs[0], cs[2], cs[1], cs[0]]
