@@ -210,6 +210,11 @@ NMT_DEV float2 fma2(float2 a, float2 b, float2 c) {  // a * b + c, round to near
   return f2_from(d);
 }
 NMT_DEV void ffma2(float2& acc, float2 a, float2 b) { acc = fma2(a, b, acc); }
+NMT_DEV float2 mul2(float2 a, float2 b) {  // a * b, round to nearest
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(d);
+}
 
 // split x = hi + lo with hi, lo bf16 (RNE); |x - hi - lo| <= 2^-16 |x| roughly.
 NMT_DEV void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {

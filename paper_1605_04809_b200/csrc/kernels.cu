@@ -651,10 +651,12 @@ NMT_DEV float rcp_approx(float x) {
 //  tanh path (FAST = false): e_j = sum_k U_k tanh(p_jk + q_k), one SFU tanh per term.
 //  exp path (FAST = true): tanh(p + q) = 1 - 2 / (1 + e^2p e^2q), so with P = e^2p (per context) and
 //    Q = e^2q (per row) e_j = sum_k U_k - 2 sum_k U_k / (1 + P_jk Q_k); the constant cancels in the
-//    softmax.  Columns 0-3 of a thread take the reciprocal on the FMA pipe (bit-trick seed, negated, then
-//    one cubic Newton step r (1 + e + e^2), e = 1 - x r: |rel err| <= 5.1e-2 -> 1.3e-4, below
-//    tanh.approx's 2^-11) and columns 4-7 on the SFU (rcp.approx), so that both pipes finish together;
-//    the FMA work runs as packed fp32 pairs (FFMA2).  u2[0..1] = +2 U (they multiply -1/x), u2[2..3] = -2 U.
+//    softmax.  Two terms share one reciprocal: U/a + U'/b = (U b + U' a) / (a b), paired across the packed
+//    fp32 pairs (columns c and c + 2 of the thread's 8) so every step is one FFMA2 / FMUL2.  Columns 0-3 take
+//    the pair reciprocal on the FMA pipe (bit-trick seed, negated, then one cubic Newton step
+//    r (1 + e + e^2), e = 1 - x r: |rel err| <= 5.1e-2 -> 1.3e-4, below tanh.approx's 2^-11), columns 4-7 on
+//    the SFU (rcp.approx): half a reciprocal per term, a quarter of them on the SFU.
+//    u2[0..1] = +2 U (they multiply -1/x), u2[2..3] = -2 U.
 template <int RPB, bool FAST>
 NMT_DEV void attn_energies(const float* pg, int Cp, int Tx, int nr, const float2 (&q2)[RPB][4],
                            const float2 (&u2)[4], float4* mine, int rstride, int hoff, float* red, int warp, int lane,
@@ -694,20 +696,19 @@ NMT_DEV void attn_energies(const float* pg, int Cp, int Tx, int nr, const float2
       for (int rr = 0; rr < RPB; ++rr) {
         if (rr >= nr) continue;
         if constexpr (FAST) {
-          float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {  // FMA-pipe reciprocals: rn = -1 / den
-            const float2 den = fma2(p2[k], q2[rr][k], one2);
-            const float2 r0 = make_float2(__int_as_float(0xFEF311C3u - __float_as_uint(den.x)),
-                                          __int_as_float(0xFEF311C3u - __float_as_uint(den.y)));
-            const float2 er = fma2(den, r0, one2);
-            const float2 rn = fma2(r0, fma2(er, er, er), r0);
-            acc = fma2(u2[k], rn, acc);
+          float2 acc;
+          {  // columns (0, 2) and (1, 3): FMA-pipe reciprocal of the pair product, rn = -1 / (a b)
+            const float2 d0 = fma2(p2[0], q2[rr][0], one2), d1 = fma2(p2[1], q2[rr][1], one2);
+            const float2 pr = mul2(d0, d1), nu = fma2(u2[0], d1, mul2(u2[1], d0));
+            const float2 r0 = make_float2(__int_as_float(0xFEF311C3u - __float_as_uint(pr.x)),
+                                          __int_as_float(0xFEF311C3u - __float_as_uint(pr.y)));
+            const float2 er = fma2(pr, r0, one2);
+            acc = mul2(nu, fma2(r0, fma2(er, er, er), r0));
           }
-#pragma unroll
-          for (int k = 2; k < 4; ++k) {  // SFU reciprocals
-            const float2 den = fma2(p2[k], q2[rr][k], one2);
-            acc = fma2(u2[k], make_float2(rcp_approx(den.x), rcp_approx(den.y)), acc);
+          {  // columns (4, 6) and (5, 7): SFU reciprocal of the pair product
+            const float2 d2 = fma2(p2[2], q2[rr][2], one2), d3 = fma2(p2[3], q2[rr][3], one2);
+            const float2 pr = mul2(d2, d3), nu = fma2(u2[2], d3, mul2(u2[3], d2));
+            acc = fma2(nu, make_float2(rcp_approx(pr.x), rcp_approx(pr.y)), acc);
           }
           e[jj * RPB + rr] = acc.x + acc.y;
         } else {

@@ -7,7 +7,9 @@ namespace nmt {
 // CNT_BIGP: set (atomicOr) by the pctx producers when some |2 pctx| > kAttnExpClamp, i.e. exp(2 pctx) was
 // clamped; the attention then takes its tanh path for the context (reset with the context)
 enum { CNT_NODES = 0, CNT_SLOTS = 1, CNT_ERR = 2, CNT_R = 3, CNT_BIGP = 4, CNT_N = 5 };
-constexpr float kAttnExpClamp = 43.f;  // exp(+-43)^2 stays inside the normal fp32 range
+// exp(+-21): a pair product (1 + e^2p e^2q)(1 + e^2p' e^2q') <= e^84.x stays inside the normal fp32 range and
+// below the reciprocal seed's limit (bits < 0x7EF311C3); |p|, |q| > 10.5 take the tanh path
+constexpr float kAttnExpClamp = 21.f;
 enum { ERR_BAD_STATE = 1, ERR_TOKEN = 2, ERR_OFFSETS = 4 };
 
 // Per-context device arena + node table + (parent, word) -> child hash (the state cache).

@@ -1,7 +1,7 @@
 """Attention (D3-D5) through both of its arithmetic paths, against the float64 oracle.
 
 The kernel evaluates tanh(p + q) as 1 - 2 / (1 + e^2p e^2q) with e^2p precomputed per context and e^2q per
-row (reading A30); when an exponent had to be clamped (|2 pctx| or |2 q| > 43) the context or
+row (reading A30); when an exponent had to be clamped (|2 pctx| or |2 q| > 21, kAttnExpClamp) the context or
 the CTA's rows take the direct tanh path.  These tests force each path with saturating weights
 (PAPER.md:13, :30 - the DL4MT cGRU attention) and check alpha, c and the scores against the oracle."""
 import numpy as np
@@ -41,7 +41,7 @@ def test_attention_paths_vs_oracle(sb, sq, prec):
     c = M.encode(src)
     sess = O.Session(om, src)
     if sb > 1:  # the keys really exceed the clamp
-        assert np.max(np.abs(2 * O.encode(om, src).pctx)) > 43
+        assert np.max(np.abs(2 * O.encode(om, src).pctx)) > 21
     g = c.debug_intermediates(c.root)
     r = sess.intermediates(0)
     tol = {"fp32class": 2e-4, "bf16": 2e-2}[prec]
