@@ -1194,13 +1194,18 @@ static void parse_and_build(const char* buf, size_t len, const nmt_opts* opts, n
   std::unique_ptr<nmt_model> m(new nmt_model());
   g_live_models.fetch_add(1);
   m->device = o.device;
+  // stream priorities: the encoder stream's E7 GEMM is needed only by the attention, so the model stream's
+  // planner and decoder prefix (the critical path after the recurrence) take SMs first
+  int prio_least = 0, prio_greatest = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+  static const bool prio = !(diag_env("NMT_STREAM_PRIO") && atoi(diag_env("NMT_STREAM_PRIO")) == 0);  // (diagnostic)
   if (o.stream) {
     m->st = static_cast<cudaStream_t>(o.stream);
   } else {
-    CK(cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithPriority(&m->st, cudaStreamNonBlocking, prio ? prio_greatest : 0));
     m->own_stream = true;
   }
-  CK(cudaStreamCreateWithFlags(&m->est, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithPriority(&m->est, cudaStreamNonBlocking, prio_least));
   CK(cudaEventCreateWithFlags(&m->enc_start_ev, cudaEventDisableTiming));
   m->mem.device = o.device;
   m->mem.st = m->st;

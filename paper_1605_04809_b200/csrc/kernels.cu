@@ -657,13 +657,68 @@ NMT_DEV float rcp_approx(float x) {
 //    r (1 + e + e^2), e = 1 - x r: |rel err| <= 5.1e-2 -> 1.3e-4, below tanh.approx's 2^-11), columns 4-7 on
 //    the SFU (rcp.approx): half a reciprocal per term, a quarter of them on the SFU.
 //    u2[0..1] = +2 U (they multiply -1/x), u2[2..3] = -2 U.
+// One block of JB positions j0.. of attn_energies: partial energies e[jj * RPB + rr] of this thread's 8 columns.
+// FULL (uniform): all JB positions < Tx and all RPB rows live, so the per-item checks are compiled out.
+template <int RPB, bool FAST, bool FULL>
+NMT_DEV void attn_block(float (&e)[32], const float* pg, int Cp, int Tx, int nr, int j0, const float2 (&q2)[RPB][4],
+                        const float2 (&u2)[4], float4* mine, int rstride, int hoff) {
+  constexpr int JB = RPB <= 4 ? 8 : 4;  // positions per reduce-scatter: JB x RPB <= 32 values
+  constexpr int NST = 8;                // positions in flight
+  const float2 one2 = make_float2(1.f, 1.f);
+  const float* gnext = pg + (int64_t)(j0 + NST) * Cp;  // refills: positions j0 + NST + jj
+#pragma unroll
+  for (int jj = 0; jj < JB; ++jj) {
+    const int j = j0 + jj;
+    const int slot = JB == NST ? jj : (j0 + jj) % NST;  // (JB == NST: j0 is a multiple of NST)
+    cp_async_wait<NST - 1>();
+    float4* sp = mine + slot * rstride;
+    const float4 n0 = sp[0], n1 = sp[hoff];
+    if (j + NST < Tx) {  // refill this slot with position j + NST
+      cp_async16(sp, gnext + (int64_t)jj * Cp);
+      cp_async16(sp + hoff, gnext + (int64_t)jj * Cp + 4);
+    }
+    cp_async_commit();
+    if (!FULL && j >= Tx) continue;  // (uniform: the tail of the last block of positions)
+    const float2 p2[4] = {make_float2(n0.x, n0.y), make_float2(n0.z, n0.w), make_float2(n1.x, n1.y),
+                          make_float2(n1.z, n1.w)};
+#pragma unroll
+    for (int rr = 0; rr < RPB; ++rr) {
+      if (!FULL && rr >= nr) continue;
+      if constexpr (FAST) {
+        float2 acc;
+        {  // columns (0, 2) and (1, 3): FMA-pipe reciprocal of the pair product, rn = -1 / (a b)
+          const float2 d0 = fma2(p2[0], q2[rr][0], one2), d1 = fma2(p2[1], q2[rr][1], one2);
+          const float2 pr = mul2(d0, d1), nu = fma2(u2[0], d1, mul2(u2[1], d0));
+          const float2 r0 = make_float2(__int_as_float(0xFEF311C3u - __float_as_uint(pr.x)),
+                                        __int_as_float(0xFEF311C3u - __float_as_uint(pr.y)));
+          const float2 er = fma2(pr, r0, one2);
+          acc = mul2(nu, fma2(r0, fma2(er, er, er), r0));
+        }
+        {  // columns (4, 6) and (5, 7): SFU reciprocal of the pair product
+          const float2 d2 = fma2(p2[2], q2[rr][2], one2), d3 = fma2(p2[3], q2[rr][3], one2);
+          const float2 pr = mul2(d2, d3), nu = fma2(u2[2], d3, mul2(u2[3], d2));
+          acc = fma2(nu, make_float2(rcp_approx(pr.x), rcp_approx(pr.y)), acc);
+        }
+        e[jj * RPB + rr] = acc.x + acc.y;
+      } else {
+        float sacc = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          sacc = fmaf(tanh_approx(p2[k].x + q2[rr][k].x), u2[k].x, sacc);
+          sacc = fmaf(tanh_approx(p2[k].y + q2[rr][k].y), u2[k].y, sacc);
+        }
+        e[jj * RPB + rr] = sacc;
+      }
+    }
+  }
+}
+
 template <int RPB, bool FAST>
 NMT_DEV void attn_energies(const float* pg, int Cp, int Tx, int nr, const float2 (&q2)[RPB][4],
                            const float2 (&u2)[4], float4* mine, int rstride, int hoff, float* red, int warp, int lane,
                            int Tx8) {
   constexpr int JB = RPB <= 4 ? 8 : 4;  // positions per reduce-scatter: JB x RPB <= 32 values
   constexpr int NST = 8;                // positions in flight
-  const float2 one2 = make_float2(1.f, 1.f);
 #pragma unroll
   for (int i = 0; i < NST; ++i) {
     if (i < Tx) {
@@ -676,52 +731,8 @@ NMT_DEV void attn_energies(const float* pg, int Cp, int Tx, int nr, const float2
     float e[32];  // e[jj * RPB + rr] partial energies of positions j0..j0+JB-1 (zero padded)
 #pragma unroll
     for (int i = 0; i < 32; ++i) e[i] = 0.f;
-#pragma unroll
-    for (int jj = 0; jj < JB; ++jj) {
-      const int j = j0 + jj;
-      const int slot = j % NST;
-      cp_async_wait<NST - 1>();
-      const float4 n0 = mine[slot * rstride], n1 = mine[slot * rstride + hoff];
-      if (j + NST < Tx) {  // refill this slot with position j + NST
-        cp_async16(mine + slot * rstride, pg + (int64_t)(j + NST) * Cp);
-        cp_async16(mine + slot * rstride + hoff, pg + (int64_t)(j + NST) * Cp + 4);
-      }
-      cp_async_commit();
-#ifndef ATTN_NOCONT
-      if (j >= Tx) continue;  // (uniform: the tail of the last block of positions)
-#endif
-      const float2 p2[4] = {make_float2(n0.x, n0.y), make_float2(n0.z, n0.w), make_float2(n1.x, n1.y),
-                            make_float2(n1.z, n1.w)};
-#pragma unroll
-      for (int rr = 0; rr < RPB; ++rr) {
-        if (rr >= nr) continue;
-        if constexpr (FAST) {
-          float2 acc;
-          {  // columns (0, 2) and (1, 3): FMA-pipe reciprocal of the pair product, rn = -1 / (a b)
-            const float2 d0 = fma2(p2[0], q2[rr][0], one2), d1 = fma2(p2[1], q2[rr][1], one2);
-            const float2 pr = mul2(d0, d1), nu = fma2(u2[0], d1, mul2(u2[1], d0));
-            const float2 r0 = make_float2(__int_as_float(0xFEF311C3u - __float_as_uint(pr.x)),
-                                          __int_as_float(0xFEF311C3u - __float_as_uint(pr.y)));
-            const float2 er = fma2(pr, r0, one2);
-            acc = mul2(nu, fma2(r0, fma2(er, er, er), r0));
-          }
-          {  // columns (4, 6) and (5, 7): SFU reciprocal of the pair product
-            const float2 d2 = fma2(p2[2], q2[rr][2], one2), d3 = fma2(p2[3], q2[rr][3], one2);
-            const float2 pr = mul2(d2, d3), nu = fma2(u2[2], d3, mul2(u2[3], d2));
-            acc = fma2(nu, make_float2(rcp_approx(pr.x), rcp_approx(pr.y)), acc);
-          }
-          e[jj * RPB + rr] = acc.x + acc.y;
-        } else {
-          float sacc = 0.f;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            sacc = fmaf(tanh_approx(p2[k].x + q2[rr][k].x), u2[k].x, sacc);
-            sacc = fmaf(tanh_approx(p2[k].y + q2[rr][k].y), u2[k].y, sacc);
-          }
-          e[jj * RPB + rr] = sacc;
-        }
-      }
-    }
+    if (j0 + JB <= Tx && nr == RPB) attn_block<RPB, FAST, true>(e, pg, Cp, Tx, nr, j0, q2, u2, mine, rstride, hoff);
+    else attn_block<RPB, FAST, false>(e, pg, Cp, Tx, nr, j0, q2, u2, mine, rstride, hoff);
     const float tot = warp_reduce_scatter32(e, lane);  // lane = jj * RPB + rr
     if (lane < JB * RPB) red[(warp * RPB + lane % RPB) * Tx8 + j0 + lane / RPB] = tot;
   }
@@ -798,7 +809,7 @@ __global__ void __launch_bounds__(256, 2) k_attention(StepDev d, AttnCtx a) {
       u2[k] = make_float2(s * u[2 * k], s * u[2 * k + 1]);
 #pragma unroll
       for (int rr = 0; rr < RPB; ++rr)
-        q2[rr][k] = fast ? make_float2(expf(2.f * q[rr][2 * k]), expf(2.f * q[rr][2 * k + 1]))
+        q2[rr][k] = fast ? make_float2(__expf(2.f * q[rr][2 * k]), __expf(2.f * q[rr][2 * k + 1]))
                          : make_float2(q[rr][2 * k], q[rr][2 * k + 1]);
     }
     if (fast) attn_energies<RPB, true>(a.epctx + c0, Cp, Tx, nr, q2, u2, mine, rstride, hoff, red, warp, lane, Tx8);

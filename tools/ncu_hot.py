@@ -1,11 +1,13 @@
 """Top warp-stall SASS lines of an ncu report (source page), optionally grouped by CUDA source line.
-  python tools/ncu_hot.py REPORT [N]"""
+  python tools/ncu_hot.py REPORT [N] [--inst]   (--inst: rank by instructions executed instead)"""
 import csv
 import subprocess
 import sys
 from collections import defaultdict
 
-rep, n = sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+rep, n = args[0], int(args[1]) if len(args) > 1 else 30
+COL = "Instructions Executed" if "--inst" in sys.argv else "Warp Stall Sampling (All Samples)"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(out.splitlines()))
@@ -21,7 +23,7 @@ for r in rows:
         continue
     if r[0] == "Line No":
         hdr = r
-        i_s = r.index("Warp Stall Sampling (All Samples)")
+        i_s = r.index(COL)
         continue
     if hdr is None or len(r) <= i_s:
         continue
