@@ -304,7 +304,7 @@ NMT_DEV void gemm_mma(GemmCta<BN, STAGES, EPI, PAIR>& cx, const GemmShape& g, co
   using S = GemmSmem<BN, STAGES, EPI, PAIR>;
   constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR>::CM;
   constexpr uint32_t idesc = idesc_bf16(CM, BN);
-  constexpr uint32_t idesc2 = idesc_bf16(CM, 192);  // (EPI_GRU2)
+  constexpr uint32_t idesc2 = idesc_bf16(CM, 192);  // (EPI_GRU2, EPI_GRU)
   const uint64_t adesc0 = sdesc_sw128(smem_u32(cx.sA)), bdesc0 = sdesc_sw128(smem_u32(cx.sB));
   for (int w = cx.unit; w < sc.items; w += cx.nunits) {
     const Item itm = sc.item(w);
@@ -341,7 +341,8 @@ NMT_DEV void gemm_mma(GemmCta<BN, STAGES, EPI, PAIR>& cx, const GemmShape& g, co
           } else {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
-              if constexpr (PAIR) mma_bf16_pair(d, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
+              // (EPI_GRU: N = 192, the first 96 B rows [r | u | x] of each CTA's group; the zero quarter is skipped)
+              if constexpr (PAIR) mma_bf16_pair(d, ad + 2 * k, bd + 2 * k, EPI == EPI_GRU ? idesc2 : idesc, (i | k) != 0);
               else mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0);
             }
           }
@@ -454,7 +455,7 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       if (it == 0 && warp == 2 && lane == 0) GTRACE(5);
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + half * COLS;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + half * (EPI == EPI_GRU ? 96 : COLS);
       if constexpr (EPI == EPI_STORE) {
         // TMEM -> registers (+bias) -> 128B-swizzled 32x32 smem tile -> TMA store (coalesced)
         uint8_t* stile = sC + (size_t)(warp - 2) * 2 * 4096;
