@@ -1345,8 +1345,9 @@ static void gemm_split(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b1
 }
 
 static void gemm_auto(nmt_model* m, const CUtensorMap& a, const CUtensorMap& b128, GemmShape& g, float* out,
-                      int ldc, int rps, int M_max, cudaStream_t st) {
-  static const int ks_cap = diag_env("NMT_MAX_KS") ? std::max(1, atoi(diag_env("NMT_MAX_KS"))) : 4;  // (diagnostic)
+                      int ldc, int rps, int M_max, cudaStream_t st, int cap = 4) {
+  static const int ks_env = diag_env("NMT_MAX_KS") ? std::max(1, atoi(diag_env("NMT_MAX_KS"))) : 0;  // (diagnostic)
+  const int ks_cap = ks_env ? ks_env : cap;
   const int max_ks = std::max(1, std::min(ks_cap, m->P_rows / rps));
   gemm_split(m, a, b128, g, out, ldc, rps, m->P_rows, M_max, max_ks, st);
 }
@@ -1441,7 +1442,8 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
   if (!stage_skipped(ST_GEMM_Q)) {
     ProfScope p_(m, ST_GEMM_Q);
     GemmShape g = gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp);
-    gemm_auto(m, m->tm_X, m->tm_Wq, g, m->Q, Cp, rps, R_max, st);
+    // no split-K: every attention CTA starts by reading its rows' q, one partial is one load (A/B: -1 us)
+    gemm_auto(m, m->tm_X, m->tm_Wq, g, m->Q, Cp, rps, R_max, st, 1);
     d.ks_q = g.reg_ks[0];
     d.ps_q = (int64_t)rps * Cp;
   }

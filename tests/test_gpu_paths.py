@@ -140,3 +140,35 @@ def test_c3_full_shape_stack_sampled():
     print(f"\n[C3 full shape] {len(words)} naive words, edges {st['edges_per_depth']}, rows {st['rows_per_depth']}, "
           f"sampled max|dlogp| per word = {worst:.2e}")
     assert worst < TOL["bf16"]
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32class"])
+def test_projected_and_explicit_context_forms(bench_model, prec):
+    """Both forms of D5-D7 (reading A31) on the same source and requests: a context from
+    nmt_encode takes the projected single-context step (c . W = alpha . (ctx . W), K = Tx), a context from
+    the batched encoder (nmt_encode_batch of > 8 sentences) the explicit one (c formed by the attention,
+    K = 2H); the batched encoder's own arithmetic differs within the precision (reading A27).  Both against the oracle, and
+    against each other within the precisions' operand rounding."""
+    d, p, blob = bench_model
+    M = nmt().Model(blob, precision=prec)
+    src, s, y, off, words = _c2_inputs(d, seed=71, R=96, cands=3, Tx=37)
+    c_proj = M.encode(src)
+    others = [synth.make_source(d.vocab_src, 20 + k, seed=900 + k) for k in range(9)]
+    batch = M.encode_batch([src] + others)  # (> 8 sentences: the batched encoder, contexts without cw)
+    c_expl = batch[0]
+    ids_p = c_proj.inject_states(s, y)
+    ids_e = c_expl.inject_states(s, y)
+    lp_p, ch_p, am_p = c_proj.score_batch(ids_p, off, words)
+    lp_e, ch_e, am_e = c_expl.score_batch(ids_e, off, words)
+    assert np.array_equal(ch_p - ch_p.min(), ch_e - ch_e.min())
+    om = O.Model(d, p)
+    rows = list(range(0, 96, 12))
+    out = O.step(om, O.encode(om, src), s[rows].astype(np.float64), y[rows])
+    rl = np.concatenate([O.log_softmax(out["z"][j])[words[off[r]:off[r + 1]]] for j, r in enumerate(rows)])
+    got_p = np.concatenate([lp_p[off[r]:off[r + 1]] for r in rows])
+    got_e = np.concatenate([lp_e[off[r]:off[r + 1]] for r in rows])
+    err_p, err_e = float(np.max(np.abs(got_p - rl))), float(np.max(np.abs(got_e - rl)))
+    print(f"\n[A31 forms] {prec}: projected {err_p:.2e}, explicit {err_e:.2e}, "
+          f"between {np.max(np.abs(lp_p - lp_e)):.2e}")
+    assert err_p < TOL[prec] and err_e < TOL[prec]
+    assert np.max(np.abs(lp_p - lp_e)) < (5e-4 if prec == "fp32class" else TOL[prec])
