@@ -406,14 +406,19 @@ def run_ours(a, rank: int, world: int, dist) -> None:
     wl = Workload(M, d, a, rank, Cn, torch)
     flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
     # ---------------- timed region (value): per-step CUDA events on the model stream, L2 flushed between steps
-    M.profile(1)
-    M.profile_read()
+    M.profile(0)
     with ClockSampler(dev) as clk:
         t_local, launches = timed_dev(wl, a, stream, flush, dist, torch, nmt)
-    stage_ms, stage_cnt = M.profile_read()
-    M.profile(0)
     last_set = (a.steps - 1) % Workload.NSETS
     dev_logp = wl.logp.cpu().numpy().copy()  # the last timed step's output (compared with the host path below)
+    # ---------------- the same W + K steps again with CUDA events around every vocab-GEMM launch (on the model
+    # stream): the dominant kernel's live duration for the roofline.  Events between PDL-chained kernels
+    # serialise them (measured +13 us per step), so they stay out of the region that gives `value`.
+    M.profile(1)
+    M.profile_read()
+    t_local_ev, _ = timed_dev(wl, a, stream, flush, dist, torch, nmt)
+    stage_ms, stage_cnt = M.profile_read()
+    M.profile(0)
     t_max = reduce_max(t_local, dist)
     total_scores = reduce_sum(float(R * Cn * a.steps), dist)
     value = total_scores / t_max
@@ -422,7 +427,7 @@ def run_ours(a, rank: int, world: int, dist) -> None:
     vi = nmt.STAGES.index("vocab_gemm_lse")
     vocab_ms = stage_ms[vi] / max(1, stage_cnt[vi])
     flops = 2.0 * R * d.vocab_tgt * d.dim_emb
-    achieved = flops / (vocab_ms / 1000.0) / 1e12
+    achieved = flops / (vocab_ms / 1000.0) / 1e12 if vocab_ms > 0 else float("nan")
     peaks = measured_peaks()
     traffic, traffic_src = ncu_traffic()
     roof = {"kernel": "k_gemm<256,6,EPI_LSE,pair> (CTA-pair vocab GEMM + online log-sum-exp)", "bound": "tensor",
@@ -430,7 +435,10 @@ def run_ours(a, rank: int, world: int, dist) -> None:
             "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
             "traffic_source": f"ncu --set full capture summarised in {traffic_src} (not measured in this run)",
             "peak_source": peaks["source"] + " bf16 burst", "algorithmic_flops_per_launch": flops,
-            "avg_launch_ms": vocab_ms, "share_of_step": vocab_ms / (1000.0 * t_local / a.steps)}
+            "avg_launch_ms": vocab_ms, "share_of_step": vocab_ms / (1000.0 * t_local_ev / a.steps),
+            "timing": "CUDA events around each launch on the model stream over a second pass of the same W + K "
+                      "steps (events there cost the PDL overlap: ms_per_step_with_events)",
+            "ms_per_step_with_events": 1000.0 * t_local_ev / a.steps}
     sf = step_flops(R, Tx, d)
     ms_step = 1000.0 * t_max / a.steps
     step_roof = {"algorithmic_flops_per_step": sf["per_step"], "per_row": sf["per_row"], "encoder": sf["encoder"],
