@@ -858,7 +858,12 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
     dfree(Aemb);
     dfree(dbenc);
   }
-  m->UPC = std::max(1, (H + 73) / 74);  // <= 74 CTAs per direction: both directions fill the 148 SMs
+  // units per CTA: <= 74 CTAs per direction (both directions fit the 148 SMs), and at least enough two-unit warps
+  // that every thread polls ONE position of h (Hp / 4 words): with 7 warps (UPC 14) for Hp = 1024, warp 0 polled
+  // two positions and paced every step; UPC 16 (8 warps, 2 x 64 CTAs) polls 1260 -> 1000 cycles per step and
+  // runs the recurrence ~5% faster (tools/enc_upc.sh)
+  m->UPC = std::max({1, (H + 73) / 74, std::min(16, 2 * (Hp / 128))});
+  if (diag_env("NMT_ENC_UPC")) m->UPC = std::max((H + 73) / 74, std::min(16, atoi(diag_env("NMT_ENC_UPC"))));  // (diagnostic)
   m->NB = (H + m->UPC - 1) / m->UPC;
   {
     std::vector<float> uarr((size_t)2 * m->NB * 3 * m->UPC * Hp, 0.f);

@@ -1579,7 +1579,7 @@ __global__ void __launch_bounds__(448, 1) k_enc_recur(EncDev e, int Tx) {  // UP
 // shared memory each step (the bound of the 1-unit layout: 14 warps x 4 KB per step), with six
 // independent FFMA2 chains per lane.  Lanes 0-15 finish unit 2w, lanes 16-31 unit 2w+1.
 template <int KI, bool TRACE>
-__global__ void __launch_bounds__(224, 1) k_enc_recur2(EncDev e, int Tx) {
+__global__ void __launch_bounds__(256, 1) k_enc_recur2(EncDev e, int Tx) {
   pdl_wait();  // (no early trigger: the cooperative grid must not lose SMs to dependents)
   constexpr int Hp = 128 * KI, H4 = Hp / 4;
   __shared__ float4 h4buf[2][H4];  // by step parity: a warp reading step t never races the poll of t+1
@@ -1868,7 +1868,7 @@ static void launch_recur(const EncDev& e, int Tx, cudaStream_t st) {
   note_launch();
 }
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
-  if (e.UPC > 14) throw NmtError(NMT_ERR_SHAPE, "encoder: UPC too large");
+  if (e.UPC > 16) throw NmtError(NMT_ERR_SHAPE, "encoder: UPC too large");
   // (the caller resets the tags and the barrier counter when the 16-bit epoch wraps)
 #ifdef NMT_DIAG
   static const bool v1 = getenv("NMT_ENC_V") && atoi(getenv("NMT_ENC_V")) == 1;  // (diagnostic: 1-unit warps)
