@@ -1097,7 +1097,8 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   // ---- encoder workspace
   m->Tpad = round_up(m->maxTx, 128);
   m->ctxbf = dalloc<__nv_bfloat16>((size_t)m->Tpad * 4 * Hp);
-  m->hbuf = dalloc<float>(2 * 2 * 131072);  // [2 dirs][stride >= 2Hp] 64-bit tagged words (1 MB)
+  m->hbuf = dalloc<float>((size_t)2 * 2 * Hp);  // [2 dirs][2 parities][Hp] tagged h words (k_enc_recur2)
+  CK(cudaMemsetAsync(m->hbuf, 0, (size_t)2 * 2 * Hp * sizeof(float), st));  // (tag 0: no step's tag)
   m->enc_mean = dalloc<float>(2 * H);
   m->ksplit_buf = dalloc<float>((size_t)8 * m->Tpad * Cp);
   m->Apad = round_up(m->maxTx, 64);
@@ -1884,7 +1885,7 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
     e.encin = m->EncIn;
     e.ctx = c->ctx;
     e.ctxbf = m->ctxbf;
-    e.hx = reinterpret_cast<unsigned long long*>(m->hbuf);
+    e.hx = reinterpret_cast<unsigned*>(m->hbuf);
     e.mean = m->enc_mean;
     e.bar = m->bar;
     e.err = c->counters + CNT_ERR;
@@ -1892,21 +1893,11 @@ static nmt_ctx* encode_impl(nmt_model* m, const int32_t* src_host, const int32_t
     e.b_init = m->b_init;
     e.S0 = c->S;
     ProfScope p_(m, ST_ENC_RECUR);
-    if (++m->enc_epoch > 65535) {  // tags carry a 16-bit epoch: reset them before it repeats
-      CK(cudaMemsetAsync(m->hbuf, 0, (size_t)2 * 2 * 131072 * sizeof(float), es));
+    if (++m->enc_epoch > 65535) {  // the tail barrier counter grows by the grid size per encode: reset it
       CK(cudaMemsetAsync(m->bar, 0, sizeof(int), es));
       m->enc_epoch = 1;
     }
     e.epoch = m->enc_epoch;
-    {
-      const char* sw = diag_env("NMT_ENC_HXSWAP");
-      const char* sd = diag_env("NMT_ENC_HXSTRIDE");
-      const char* rp = diag_env("NMT_ENC_HXREP");  // (diagnostic)
-      e.hx_rep = rp ? std::max(1, std::min(8, atoi(rp))) : 1;  // (measured: replicas only add store work)
-      e.hx_swap = sw ? atoi(sw) & 1 : 0;
-      e.hx_stride = sd ? std::max<int64_t>(2 * e.hx_rep * m->Hp, std::min<int64_t>(atoll(sd), 65536))
-                       : 2 * e.hx_rep * m->Hp;
-    }
     const bool trace = diag_env("NMT_ENC_TRACE") != nullptr;  // diagnostic: per-step phase stamps
     if (trace) CK(cudaMalloc(&e.trace, ((size_t)(len + 1) * 8 + 2 * 2 * m->NB) * sizeof(long long)));
     if (!stage_skipped(ST_ENC_RECUR)) enc_recur(e, len, es);

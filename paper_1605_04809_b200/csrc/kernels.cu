@@ -1295,289 +1295,32 @@ void full_row(const float* T, const float* Wo32, const float* bo, const float* l
 }
 
 // ===================================================================================== encoder
-// E1-E6 in one persistent cooperative kernel.  CTAs [0, NB) run the forward direction,
-// [NB, 2NB) the backward one (both fill the 148 SMs).  Each CTA owns UPC hidden units, one WARP
-// per unit: the warp keeps the unit's three columns of [U | Ux] (r, u and candidate gates) in
-// REGISTERS for the whole sentence (lane l holds the float4s k = l + 32 i of each), so a time step
-// reads no weights at all, and the warp's butterfly reduction leaves the three dot products in
-// every lane, which evaluates the GRU update itself (no shared-memory hop, one barrier per step).
-// The dot products use packed FFMA2.  The input projections x_j.[W|Wx] + [b|bx] are rows of a
-// table precomputed per source word at load (E1+E2 become a gather, fetched one step ahead).
-// h_t is exchanged through global memory as 64-bit (value, tag = epoch:t+1) words: a reader polls until
-// every word carries the tag of the step it needs, which merges the grid-wide barrier into the
-// data read (one L2 round trip per step).  Double-buffered by parity: a writer is at most one step
-// ahead of the slowest reader.  The 16-bit encode epoch in the tag (and a barrier counter that only
-// grows) means no buffer is reset between calls.
+// E1-E6 in one persistent cooperative kernel (k_enc_recur2).  CTAs [0, NB) run the forward direction,
+// [NB, 2NB) the backward one.  Each CTA owns UPC hidden units, two per warp: the warp keeps the units'
+// columns of [U | Ux] (r, u and candidate gates) in REGISTERS for the whole sentence, so a time step reads
+// no weights at all.  The dot products use packed FFMA2.  The input projections x_j.[W|Wx] + [b|bx] are
+// rows of a table precomputed per source word at load (E1+E2 become a gather into shared memory).
+// h_t is exchanged through global memory as 32-bit words: the fp32 value with its two low mantissa bits
+// replaced by the tag (t + 1) mod 4 (a relative perturbation <= 2^-22).  A reader polls until every word
+// carries the tag of the step it needs, which merges the grid-wide barrier into the data read (one L2
+// round trip per step).  Double-buffered by step parity: a writer is at most one step ahead of the
+// slowest reader, and the word a reader finds in its buffer is from step t, t - 2 or t - 4..., whose tags
+// differ mod 4.  Each encode zeroes the words after its final grid barrier (tag 0 matches neither first
+// read, tags 1 and 2), so the next encode starts clean with no reset between calls; a barrier counter that
+// only grows serves the tail.
 // Tail (E5): each CTA publishes the time-mean of its units, one grid barrier, then the CTAs split
 // s0 = tanh(mean . W_init + b_init); their W_init rows are prefetched into shared memory at start.
-// The kernel also writes the bf16 hi|lo copy of ctx (E7 input) and the new context's counters.
+// The kernel also writes the bf16 hi|lo copy of ctx (E7 input).
 __device__ __forceinline__ float sigmoid_fast(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
 __device__ __forceinline__ float tanh_fast(float x) {  // |err| ~ 1e-7 (not tanh.approx)
   const float e = __expf(2.f * fminf(fmaxf(x, -15.f), 15.f));
   return 1.f - __fdividef(2.f, e + 1.f);
 }
 constexpr int kPinMax = 512;  // sources up to this length have their input projections staged in smem
-template <int KI, bool TRACE>  // Hp = 128 * KI; TRACE: clock64 phase stamps (diagnostic build of the kernel)
-__global__ void __launch_bounds__(448, 1) k_enc_recur(EncDev e, int Tx) {  // UPC <= 14 warps (<= 4 per SMSP: 128 regs)
-  pdl_wait();  // (no early trigger: the cooperative grid must not lose SMs to dependents)
-  constexpr int Hp = 128 * KI, H4 = Hp / 4;
-  __shared__ float4 h4buf[2][H4];  // by step parity: a warp reading step t never races the poll of t+1
-  const int NB = e.NB, UPC = e.UPC, H = e.H;
-  const int nthr = blockDim.x;
-  const int dir = blockIdx.x / NB, cb = blockIdx.x % NB;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int jj = cb * UPC + warp;  // this warp's hidden unit
-  const bool unit = jj < H;
-  long long* tr = (TRACE && blockIdx.x == 0 && threadIdx.x == 0) ? e.trace : nullptr;
-  if (TRACE && tr) {
-    tr[Tx * 8 + 0] = clock64();
-    unsigned long long g;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-    tr[Tx * 8 + 5] = (long long)g;
-  }
-  const int C = 2 * H;
-  const int per = (H + gridDim.x - 1) / gridDim.x;  // s0 outputs of this CTA (tail)
-  extern __shared__ __align__(16) float wsm[];       // [per][C] rows of W_init^T (tail)
-  __shared__ __align__(8) uint64_t wbar;  // completion of their bulk copy
-  const int o_first = blockIdx.x * per, n_out = max(0, min(per, H - o_first));
-  const bool bulk = (C % 4) == 0;  // 16-byte rows: one bulk copy per row, in flight during the loop
-  if (bulk && threadIdx.x == 0) {
-    mbar_init(&wbar, 1);
-    fence_barrier_init();
-    mbar_arrive_expect_tx(&wbar, (uint32_t)(n_out * C * 4));
-    for (int r = 0; r < n_out; ++r)
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(smem_u32(wsm + r * C)), "l"(e.W_initT + (int64_t)(o_first + r) * C), "r"(C * 4),
-                   "r"(smem_u32(&wbar)) : "memory");
-  }
-  float4 wr[KI], wu[KI], wx[KI];
-  {
-    const float4* src = reinterpret_cast<const float4*>(e.Uarr) + (size_t)(dir * NB + cb) * 3 * UPC * H4;
-#pragma unroll
-    for (int i = 0; i < KI; ++i) {
-      wr[i] = src[(size_t)warp * H4 + lane + 32 * i];
-      wu[i] = src[(size_t)(UPC + warp) * H4 + lane + 32 * i];
-      wx[i] = src[(size_t)(2 * UPC + warp) * H4 + lane + 32 * i];
-    }
-  }
-  if (!bulk)
-    for (int i = threadIdx.x; i < n_out * C; i += nthr) wsm[i] = __ldg(e.W_initT + (int64_t)o_first * C + i);
-  unsigned long long* hx = e.hx + (size_t)(dir ^ e.hx_swap) * e.hx_stride;  // [2][Hp] tagged words of this direction
-  const unsigned ep = e.epoch << 16;
-  float hself = 0.f, hsum = 0.f;
-  // input projections (independent of h) are fetched one step ahead: the table rows live in HBM;
-  // the source id one step before that, so no dependent load sits on the step's critical path
-  const int* srcp = e.src;
-  const int sdir = dir == 0 ? 1 : -1, s0 = dir == 0 ? 0 : Tx - 1;  // position of step t = s0 + sdir t
-  const float* encin = e.encin + dir * 3 * Hp + jj;
-  const int Vs = e.Vs;
-#define NMT_FETCH_PIN(ID, R_, U_, X_)                                              \
-  {                                                                                \
-    int id_ = (ID);                                                                \
-    if (id_ < 0 || id_ >= Vs) { /* device-resident ids are validated here */      \
-      if (lane == 0) atomicOr(e.err, ERR_TOKEN);  /* (nmt_ctx_check reports it) */ \
-      id_ = 0;                                                                     \
-    }                                                                              \
-    const float* pin_ = encin + (int64_t)id_ * 6 * Hp;                             \
-    R_ = __ldg(pin_);                                                              \
-    U_ = __ldg(pin_ + Hp);                                                         \
-    X_ = __ldg(pin_ + 2 * Hp);                                                     \
-  }
-  // Tx <= kPinMax: the whole sentence's projections of this CTA's units are gathered into shared
-  // memory at start (ids first, then 4-byte cp.async gathers that overlap the weight loads), so a
-  // step reads them with LDS; longer sources fetch one step ahead from HBM (NMT_FETCH_PIN).
-  const bool pre = Tx <= kPinMax;
-  float* pin_s = wsm + per * C;                                     // [Tx][3][UPC]
-  int* ids_s = reinterpret_cast<int*>(pin_s + (pre ? Tx * 3 * UPC : 0));  // [Tx]
-  float n_r = 0.f, n_u = 0.f, n_x = 0.f;
-  int id_next = 0;
-  if (pre) {
-    for (int t = threadIdx.x; t < Tx; t += nthr) {
-      int id = __ldg(srcp + s0 + sdir * t);
-      if (id < 0 || id >= Vs) {  // device-resident ids are validated here (nmt_ctx_check)
-        atomicOr(e.err, ERR_TOKEN);
-        id = 0;
-      }
-      ids_s[t] = id;
-    }
-    __syncthreads();
-    const int per_t = 3 * UPC;
-    for (int i = threadIdx.x; i < Tx * per_t; i += nthr) {
-      const int t = i / per_t, g = (i % per_t) / UPC, u = i % UPC;
-      const int unit_j = cb * UPC + u;
-      if (unit_j < H)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(pin_s + i)),
-                     "l"(e.encin + (int64_t)ids_s[t] * 6 * Hp + dir * 3 * Hp + g * Hp + unit_j) : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  } else {
-    id_next = Tx > 1 ? __ldg(srcp + s0 + sdir) : 0;
-    if (unit) NMT_FETCH_PIN(__ldg(srcp + s0), n_r, n_u, n_x);
-  }
-  if (TRACE && tr) {
-    // (weights are in registers once used: force completion for the stamp with a dependent read)
-    tr[Tx * 8 + 1] = clock64() + (long long)(wr[KI - 1].w == 12345.f) + (long long)(wx[0].x == 12345.f);
-  }
-  // polling: thread k < Hp/4 owns the 4 tagged words of units 4k..4k+3 (one 256-bit load)
-  const int kq = threadIdx.x;
-  const bool poller = kq < H4 && 4 * kq < H;
-  const unsigned need = (4 * kq + 3 < H) ? 0xFu : ((1u << max(0, min(4, H - 4 * kq))) - 1u);  // real units only
-  if (pre) {
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();  // (the gathered projections are visible to every warp)
-  }
-  int npolls = 0;
-  long long cyc_poll = 0, cyc_loop0 = TRACE ? clock64() : 0;
-  for (int t = 0; t < Tx; ++t) {
-    if (TRACE && tr) tr[t * 8 + 0] = clock64();
-    const int j = s0 + sdir * t;
-    float p_r = n_r, p_u = n_u, p_x = n_x;
-    if (!pre) {
-      if (unit && t + 1 < Tx) NMT_FETCH_PIN(id_next, n_r, n_u, n_x);
-      if (t + 2 < Tx) id_next = __ldg(srcp + s0 + sdir * (t + 2));
-    }
-    // (measured: issuing the poll before the fetch above is ~20% slower per step)
-    unsigned long long a = 0, b = 0, c = 0, d = 0;
-    const unsigned long long* hsrc = hx + (size_t)(t & 1) * Hp + 4 * kq;
-    if (t > 0 && poller)
-      asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
-                   : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(hsrc) : "memory");
-    if (TRACE && tr) tr[t * 8 + 1] = clock64();
-    float2 ar = make_float2(0.f, 0.f), au = ar, ax = ar;  // (3 chains: the 96 weight registers leave room for no more)
-    if (t > 0) {
-      const unsigned tag = ep | (unsigned)t;  // h_{t-1} was written with tag (t-1)+1
-      float4* h4 = h4buf[t & 1];
-      if (poller) {
-        const long long t0 = clock64();
-        while (true) {
-          ++npolls;
-          const unsigned ok = ((unsigned)(a >> 32) == tag) | (((unsigned)(b >> 32) == tag) << 1) |
-                              (((unsigned)(c >> 32) == tag) << 2) | (((unsigned)(d >> 32) == tag) << 3);
-          if ((ok & need) == need) break;
-          if (clock64() - t0 > (1ll << 32)) asm volatile("trap;");  // watchdog (~2 s): fail, never hang
-          asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
-                       : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(hsrc) : "memory");
-        }
-        // units >= H inside this float4 carry no tag: they are 0
-        h4[kq] = make_float4((need & 1) ? __uint_as_float((unsigned)a) : 0.f, (need & 2) ? __uint_as_float((unsigned)b) : 0.f,
-                             (need & 4) ? __uint_as_float((unsigned)c) : 0.f, (need & 8) ? __uint_as_float((unsigned)d) : 0.f);
-      } else if (kq < H4) {
-        h4[kq] = make_float4(0.f, 0.f, 0.f, 0.f);  // padded units (H < Hp) are never written
-      }
-      if (TRACE && tr) tr[t * 8 + 2] = clock64();
-      const long long cb0 = TRACE ? clock64() : 0;
-      __syncthreads();  // (the only barrier of a step: buffer t&1 is rewritten at t+2, after t+1's barrier)
-      if (TRACE && tr) tr[t * 8 + 3] = clock64();
-      if (TRACE) cyc_poll += clock64() - cb0;  // (barrier wait: this CTA's pollers waiting for h)
-#pragma unroll
-      for (int i = 0; i < KI; ++i) {
-        const float4 h = h4[lane + 32 * i];
-        const float2 hlo = make_float2(h.x, h.y), hhi = make_float2(h.z, h.w);
-        ffma2(ar, make_float2(wr[i].x, wr[i].y), hlo);
-        ffma2(au, make_float2(wu[i].x, wu[i].y), hlo);
-        ffma2(ax, make_float2(wx[i].x, wx[i].y), hlo);
-        ffma2(ar, make_float2(wr[i].z, wr[i].w), hhi);
-        ffma2(au, make_float2(wu[i].z, wu[i].w), hhi);
-        ffma2(ax, make_float2(wx[i].z, wx[i].w), hhi);
-      }
-    }
-    // (h_0 = 0: the dot products are 0 at t = 0)
-    float dr = ar.x + ar.y, du = au.x + au.y, dx = ax.x + ax.y;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {  // butterfly: every lane ends with the same sums
-      dr += __shfl_xor_sync(0xffffffffu, dr, o);
-      du += __shfl_xor_sync(0xffffffffu, du, o);
-      dx += __shfl_xor_sync(0xffffffffu, dx, o);
-    }
-    if (TRACE && tr) tr[t * 8 + 4] = clock64();
-    if (unit) {
-      if (pre) {
-        const float* pt = pin_s + t * 3 * UPC + warp;
-        p_r = pt[0];
-        p_u = pt[UPC];
-        p_x = pt[2 * UPC];
-      }
-      const float rg = sigmoid_fast(p_r + dr);
-      const float ug = sigmoid_fast(p_u + du);
-      const float ht = tanh_fast(rg * dx + p_x);
-      hself = ug * hself + (1.f - ug) * ht;
-      hsum += hself;
-      const int cidx = dir * Hp + jj;  // padded context column
-      if (lane == 0) {
-        const unsigned long long word = ((unsigned long long)(ep | (unsigned)(t + 1)) << 32) | __float_as_uint(hself);
-        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(hx + (size_t)((t + 1) & 1) * Hp + jj), "l"(word)
-                     : "memory");
-      } else if (lane == 1) {
-        e.ctx[(int64_t)j * 2 * Hp + cidx] = hself;
-      } else if (lane == 2) {
-        __nv_bfloat16 hi, lo;
-        split_bf16(hself, hi, lo);
-        e.ctxbf[(int64_t)j * 4 * Hp + cidx] = hi;
-        e.ctxbf[(int64_t)j * 4 * Hp + 2 * Hp + cidx] = lo;
-      }
-    }
-    if (TRACE && tr) {
-      tr[t * 8 + 5] = clock64();
-      tr[t * 8 + 6] = npolls;
-    }
-  }
-#undef NMT_FETCH_PIN
-  // ---- E5: time means -> grid barrier -> s0 slices
-  if (TRACE && tr) tr[Tx * 8 + 2] = clock64();
-  if (TRACE && threadIdx.x == 0) {  // per-CTA: [loop cycles, barrier-wait cycles] after the CTA-0 trace
-    e.trace[(Tx + 1) * 8 + 2 * blockIdx.x] = clock64() - cyc_loop0;
-    e.trace[(Tx + 1) * 8 + 2 * blockIdx.x + 1] = cyc_poll;
-  }
-  if (unit && lane == 0) e.mean[dir * H + jj] = hsum / (float)Tx;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(e.bar) : "memory");
-    int v;
-    const long long t0 = clock64();
-    do {
-      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(e.bar) : "memory");
-      if (clock64() - t0 > (1ll << 32)) asm volatile("trap;");
-    } while (v < (int)(e.epoch * gridDim.x));
-  }
-  __syncthreads();
-  if (TRACE && tr) tr[Tx * 8 + 3] = clock64();
-  // all 2H means at once (C <= 2Hp floats = the two h buffers), then a warp per s0 output
-  float* msm = reinterpret_cast<float*>(h4buf);
-  for (int k = threadIdx.x; k < C; k += nthr) msm[k] = __ldcg(e.mean + k);
-  __syncthreads();
-  if (warp < n_out) {
-    if (bulk) mbar_wait(&wbar, 0);
-    const int o = o_first + warp;
-    const float* wrow = wsm + warp * C;
-    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-    if (bulk) {
-      for (int k = 4 * lane; k < C; k += 128) {
-        const float4 mv = *reinterpret_cast<const float4*>(msm + k), wv = *reinterpret_cast<const float4*>(wrow + k);
-        acc0 = fmaf(mv.x, wv.x, acc0);
-        acc1 = fmaf(mv.y, wv.y, acc1);
-        acc2 = fmaf(mv.z, wv.z, acc2);
-        acc3 = fmaf(mv.w, wv.w, acc3);
-      }
-    } else {
-      for (int k = lane; k < C; k += 32) acc0 = fmaf(msm[k], wrow[k], acc0);
-    }
-    float sacc = (acc0 + acc1) + (acc2 + acc3);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, off);
-    if (lane == 0) e.S0[o] = tanhf(sacc + e.b_init[o]);
-  }
-  if (TRACE && tr) {
-    tr[Tx * 8 + 4] = clock64();
-    unsigned long long g;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-    tr[Tx * 8 + 6] = (long long)g;
-  }
-}
-
-// Variant with TWO units per warp (UPC <= 14 -> <= 7 warps): the warp keeps 6 weight columns in
-// registers (192 per lane, up to 255 allowed at 224 threads), so half as many warps read h from
-// shared memory each step (the bound of the 1-unit layout: 14 warps x 4 KB per step), with six
-// independent FFMA2 chains per lane.  Lanes 0-15 finish unit 2w, lanes 16-31 unit 2w+1.
+// TWO units per warp (UPC <= 16 -> <= 8 warps): the warp keeps 6 weight columns in registers (192 per
+// lane, up to 255 allowed at 256 threads), so only UPC / 2 warps read h from shared memory each step, with
+// six independent FFMA2 chains per lane.  Lanes 0-15 finish unit 2w, lanes 16-31 unit 2w+1.
+// (template parameter KI: Hp = 128 KI; TRACE: clock64 phase stamps, diagnostic build)
 template <int KI, bool TRACE>
 __global__ void __launch_bounds__(256, 1) k_enc_recur2(EncDev e, int Tx) {
   pdl_wait();  // (no early trigger: the cooperative grid must not lose SMs to dependents)
@@ -1632,8 +1375,7 @@ __global__ void __launch_bounds__(256, 1) k_enc_recur2(EncDev e, int Tx) {
   }
   if (!bulk)
     for (int i = threadIdx.x; i < n_out * C; i += nthr) wsm[i] = __ldg(e.W_initT + (int64_t)o_first * C + i);
-  unsigned long long* hx = e.hx + (size_t)(dir ^ e.hx_swap) * e.hx_stride;  // [2][Hp] tagged words
-  const unsigned ep = e.epoch << 16;
+  unsigned* hx = e.hx + (size_t)dir * 2 * Hp;  // [2 parities][Hp] tagged words of this direction
   const int sdir = dir == 0 ? 1 : -1, s0 = dir == 0 ? 0 : Tx - 1;  // position of step t = s0 + sdir t
   // input projections of all steps (Tx <= kPinMax): ids, then 4-byte cp.async gathers
   const bool pre = Tx <= kPinMax;
@@ -1691,23 +1433,22 @@ __global__ void __launch_bounds__(256, 1) k_enc_recur2(EncDev e, int Tx) {
     if (TRACE && tr) tr[t * 8 + 1] = clock64();
     float2 ara = make_float2(0.f, 0.f), aua = ara, axa = ara, arb = ara, aub = ara, axb = ara;
     if (t > 0) {
-      const unsigned tag = ep | (unsigned)t;  // h_{t-1} was written with tag (t-1)+1
+      const unsigned tag = (unsigned)t & 3u;  // h_{t-1} was written with tag ((t-1)+1) mod 4
       float4* h4 = h4buf[t & 1];
-      const unsigned long long* hsrc = hx + ((size_t)(t & 1) * e.hx_rep + cb % e.hx_rep) * Hp;
+      const unsigned* hsrc = hx + (size_t)(t & 1) * Hp;
       // <= 2 positions per thread (host-checked): both 256-bit loads are in flight before any wait
       const int k0 = threadIdx.x, k1 = threadIdx.x + nthr;
       const bool h0 = k0 < H4 && 4 * k0 < H, h1 = k1 < H4 && 4 * k1 < H;
       const unsigned need0 = (4 * k0 + 3 < H) ? 0xFu : ((1u << max(0, H - 4 * k0)) - 1u);  // real units only
       const unsigned need1 = (4 * k1 + 3 < H) ? 0xFu : ((1u << max(0, H - 4 * k1)) - 1u);
-      unsigned long long a0 = 0, b0 = 0, c0 = 0, d0 = 0, a1 = 0, b1 = 0, c1 = 0, d1 = 0;
+      unsigned a0 = 0, b0 = 0, c0 = 0, d0 = 0, a1 = 0, b1 = 0, c1 = 0, d1 = 0;
       if (h0)
-        asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
-                     : "=l"(a0), "=l"(b0), "=l"(c0), "=l"(d0) : "l"(hsrc + 4 * k0) : "memory");
+        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a0), "=r"(b0), "=r"(c0), "=r"(d0) : "l"(hsrc + 4 * k0) : "memory");
       if (h1)
-        asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
-                     : "=l"(a1), "=l"(b1), "=l"(c1), "=l"(d1) : "l"(hsrc + 4 * k1) : "memory");
-      auto settle = [&](bool has, int k, unsigned need, unsigned long long& a, unsigned long long& b,
-                        unsigned long long& c, unsigned long long& d) {
+        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a1), "=r"(b1), "=r"(c1), "=r"(d1) : "l"(hsrc + 4 * k1) : "memory");
+      auto settle = [&](bool has, int k, unsigned need, unsigned& a, unsigned& b, unsigned& c, unsigned& d) {
         if (!has) {
           if (k < H4) h4[k] = make_float4(0.f, 0.f, 0.f, 0.f);  // padded units (H < Hp) are never written
           return;
@@ -1715,15 +1456,15 @@ __global__ void __launch_bounds__(256, 1) k_enc_recur2(EncDev e, int Tx) {
         const long long tw = clock64();
         while (true) {
           ++npolls;
-          const unsigned ok = ((unsigned)(a >> 32) == tag) | (((unsigned)(b >> 32) == tag) << 1) |
-                              (((unsigned)(c >> 32) == tag) << 2) | (((unsigned)(d >> 32) == tag) << 3);
+          const unsigned ok = ((a & 3u) == tag) | (((b & 3u) == tag) << 1) | (((c & 3u) == tag) << 2) |
+                              (((d & 3u) == tag) << 3);
           if ((ok & need) == need) break;
           if (clock64() - tw > (1ll << 32)) asm volatile("trap;");  // watchdog (~2 s): fail, never hang
-          asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
-                       : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(hsrc + 4 * k) : "memory");
+          asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "l"(hsrc + 4 * k) : "memory");
         }
-        h4[k] = make_float4((need & 1) ? __uint_as_float((unsigned)a) : 0.f, (need & 2) ? __uint_as_float((unsigned)b) : 0.f,
-                            (need & 4) ? __uint_as_float((unsigned)c) : 0.f, (need & 8) ? __uint_as_float((unsigned)d) : 0.f);
+        h4[k] = make_float4((need & 1) ? __uint_as_float(a & ~3u) : 0.f, (need & 2) ? __uint_as_float(b & ~3u) : 0.f,
+                            (need & 4) ? __uint_as_float(c & ~3u) : 0.f, (need & 8) ? __uint_as_float(d & ~3u) : 0.f);
       };
       settle(h0, k0, need0, a0, b0, c0, d0);
       settle(h1, k1, need1, a1, b1, c1, d1);
@@ -1772,10 +1513,10 @@ __global__ void __launch_bounds__(256, 1) k_enc_recur2(EncDev e, int Tx) {
       hsum += hself;
       const int cidx = dir * Hp + jj;  // padded context column
       const int role = lane & 15;
-      if (role >= 3 + 0 && role < 3 + e.hx_rep) {  // lanes 3.. publish h_t to every replica (one store each)
-        const unsigned long long word = ((unsigned long long)(ep | (unsigned)(t + 1)) << 32) | __float_as_uint(hself);
-        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;"
-                     ::"l"(hx + ((size_t)((t + 1) & 1) * e.hx_rep + (role - 3)) * Hp + jj), "l"(word) : "memory");
+      if (role == 3) {  // publish h_t, tagged (t + 1) mod 4
+        const unsigned word = (__float_as_uint(hself) & ~3u) | ((unsigned)(t + 1) & 3u);
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(hx + (size_t)((t + 1) & 1) * Hp + jj), "r"(word)
+                     : "memory");
       } else if (role == 1) {
         e.ctx[(int64_t)j * 2 * Hp + cidx] = hself;
       } else if (role == 2) {
@@ -1809,6 +1550,10 @@ __global__ void __launch_bounds__(256, 1) k_enc_recur2(EncDev e, int Tx) {
   }
   __syncthreads();
   if (TRACE && tr) tr[Tx * 8 + 3] = clock64();
+  if (unit && (lane & 15) == 3) {  // every CTA has read its last h: zero this unit's words for the next encode
+    hx[jj] = 0u;
+    hx[Hp + jj] = 0u;
+  }
   // all 2H means at once (C <= 2Hp floats = the two h buffers), then a warp per s0 output
   float* msm = reinterpret_cast<float*>(h4buf);
   for (int k = threadIdx.x; k < C; k += nthr) msm[k] = __ldcg(e.mean + k);
@@ -1856,44 +1601,18 @@ static void launch_recur2(const EncDev& e, int Tx, cudaStream_t st) {
   note_launch();
 }
 
-template <int KI, bool TRACE>
-static void launch_recur(const EncDev& e, int Tx, cudaStream_t st) {
-  EncDev ee = e;
-  void* args[] = {&ee, &Tx};
-  const size_t smem = (size_t)((e.H + 2 * e.NB - 1) / (2 * e.NB)) * 2 * e.H * sizeof(float) +
-                      (Tx <= kPinMax ? (size_t)Tx * (3 * e.UPC + 1) * sizeof(float) : 0);
-  static std::atomic<size_t> attr[kMaxDevices];  // > 48 KB of dynamic shared memory needs the opt-in
-  ensure_smem_attr(k_enc_recur<KI, TRACE>, attr, smem);
-  CK(cudaLaunchCooperativeKernel((void*)k_enc_recur<KI, TRACE>, dim3(2 * e.NB), dim3(32 * e.UPC), args, smem, st));
-  note_launch();
-}
 void enc_recur(const EncDev& e, int Tx, cudaStream_t st) {
   if (e.UPC > 16) throw NmtError(NMT_ERR_SHAPE, "encoder: UPC too large");
-  // (the caller resets the tags and the barrier counter when the 16-bit epoch wraps)
-#ifdef NMT_DIAG
-  static const bool v1 = getenv("NMT_ENC_V") && atoi(getenv("NMT_ENC_V")) == 1;  // (diagnostic: 1-unit warps)
-#else
-  constexpr bool v1 = false;
-#endif
-  if (v1 && 32 * e.UPC < e.Hp / 4) throw NmtError(NMT_ERR_SHAPE, "encoder: fewer threads than polled words");
-  if (!v1 && 2 * 32 * ((e.UPC + 1) / 2) < e.Hp / 4) throw NmtError(NMT_ERR_SHAPE, "encoder: > 2 polled words per thread");
+  if (2 * 32 * ((e.UPC + 1) / 2) < e.Hp / 4) throw NmtError(NMT_ERR_SHAPE, "encoder: > 2 polled words per thread");
   switch (e.Hp / 128) {
-    case 1: v1 ? (e.trace ? launch_recur<1, true>(e, Tx, st) : launch_recur<1, false>(e, Tx, st))
-            : (e.trace ? launch_recur2<1, true>(e, Tx, st) : launch_recur2<1, false>(e, Tx, st)); break;
-    case 2: v1 ? (e.trace ? launch_recur<2, true>(e, Tx, st) : launch_recur<2, false>(e, Tx, st))
-            : (e.trace ? launch_recur2<2, true>(e, Tx, st) : launch_recur2<2, false>(e, Tx, st)); break;
-    case 3: v1 ? (e.trace ? launch_recur<3, true>(e, Tx, st) : launch_recur<3, false>(e, Tx, st))
-            : (e.trace ? launch_recur2<3, true>(e, Tx, st) : launch_recur2<3, false>(e, Tx, st)); break;
-    case 4: v1 ? (e.trace ? launch_recur<4, true>(e, Tx, st) : launch_recur<4, false>(e, Tx, st))
-            : (e.trace ? launch_recur2<4, true>(e, Tx, st) : launch_recur2<4, false>(e, Tx, st)); break;
-    case 5: v1 ? (e.trace ? launch_recur<5, true>(e, Tx, st) : launch_recur<5, false>(e, Tx, st))
-            : (e.trace ? launch_recur2<5, true>(e, Tx, st) : launch_recur2<5, false>(e, Tx, st)); break;
-    case 6: v1 ? (e.trace ? launch_recur<6, true>(e, Tx, st) : launch_recur<6, false>(e, Tx, st))
-            : (e.trace ? launch_recur2<6, true>(e, Tx, st) : launch_recur2<6, false>(e, Tx, st)); break;
-    case 7: v1 ? (e.trace ? launch_recur<7, true>(e, Tx, st) : launch_recur<7, false>(e, Tx, st))
-            : (e.trace ? launch_recur2<7, true>(e, Tx, st) : launch_recur2<7, false>(e, Tx, st)); break;
-    case 8: v1 ? (e.trace ? launch_recur<8, true>(e, Tx, st) : launch_recur<8, false>(e, Tx, st))
-            : (e.trace ? launch_recur2<8, true>(e, Tx, st) : launch_recur2<8, false>(e, Tx, st)); break;
+    case 1: e.trace ? launch_recur2<1, true>(e, Tx, st) : launch_recur2<1, false>(e, Tx, st); break;
+    case 2: e.trace ? launch_recur2<2, true>(e, Tx, st) : launch_recur2<2, false>(e, Tx, st); break;
+    case 3: e.trace ? launch_recur2<3, true>(e, Tx, st) : launch_recur2<3, false>(e, Tx, st); break;
+    case 4: e.trace ? launch_recur2<4, true>(e, Tx, st) : launch_recur2<4, false>(e, Tx, st); break;
+    case 5: e.trace ? launch_recur2<5, true>(e, Tx, st) : launch_recur2<5, false>(e, Tx, st); break;
+    case 6: e.trace ? launch_recur2<6, true>(e, Tx, st) : launch_recur2<6, false>(e, Tx, st); break;
+    case 7: e.trace ? launch_recur2<7, true>(e, Tx, st) : launch_recur2<7, false>(e, Tx, st); break;
+    case 8: e.trace ? launch_recur2<8, true>(e, Tx, st) : launch_recur2<8, false>(e, Tx, st); break;
     default: throw NmtError(NMT_ERR_SHAPE, "encoder: dim_hid > 1024");
   }
 }

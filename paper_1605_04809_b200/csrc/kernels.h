@@ -119,17 +119,14 @@ struct AttnCtx {
 
 struct EncDev {
   int H, Hp, NB, UPC, Vs;
-  int hx_swap;           // diagnostic: direction -> exchange buffer mapping (NMT_ENC_HXSWAP)
-  int64_t hx_stride;     // u64 words between the two directions' exchange buffers (>= 2 rep Hp)
-  int hx_rep;            // replicas of the exchange buffer (readers spread over them: less L2 contention)
-  unsigned epoch;        // 1..65535, per encode: tags and the tail barrier need no reset between calls
+  unsigned epoch;        // 1..65535, per encode: target of the tail grid barrier's growing counter
   long long* trace;      // diagnostic (NMT_ENC_TRACE): [Tx][8] clock64 phase stamps of CTA 0, thread 0
   const float* Uarr;     // [2][NB][3*UPC][Hp] recurrent weights per CTA (rows zero-padded to Hp)
   const int* src;        // [Tx] source ids (device)
   const float* encin;    // [Vs][6Hp] precomputed x.[W|Wx] + [b|bx] of both directions per source word
   float* ctx;            // [Tx][2Hp]
   __nv_bfloat16* ctxbf;  // [Tx][4Hp] hi | lo copy for the pctx GEMM
-  unsigned long long* hx;  // [2 dirs][2 parities][Hp] (tag << 32 | float bits)
+  unsigned* hx;          // [2 dirs][2 parities][Hp] fp32 h with the tag (t + 1) mod 4 in the 2 low bits (zero between encodes)
   float* mean;           // [2H] mean_j ctx_j (real indices)
   int* bar;              // [1] tail grid barrier
   int* err;              // validation flags of the context
