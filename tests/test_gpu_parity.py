@@ -262,3 +262,39 @@ def test_enru_large_batch_sampled(enru, prec):
         worst = max(worst, float(np.max(np.abs(lp[off[i]:off[i + 1]] - rl))))
     print(f"\n[parity] En->Ru R={R} {prec}: sampled max|dlogp| = {worst:.3e}")
     assert worst < TOL[prec]
+
+
+# ------------------------------------------------------------------------ irregular shapes (padding)
+@pytest.mark.parametrize("readout,prec", CONFIGS, ids=["-".join(c) for c in CONFIGS])
+def test_irregular_dims_two_steps(readout, prec):
+    """Dimensions that are multiples of nothing (E 13, H 37, V_s 61, V_t 517, Tx 23 and 67 rows): every
+    padded extent - Hp, Cp, Ep, ROp, Vp, the E7 operand's rows, the projected-context K range, the encoder's
+    units per CTA and its exchange words past H - against the oracle, over a two-step tree."""
+    d = synth.Dims(13, 37, 61, 517, readout)
+    p = synth.make_model(d, 11)
+    om = O.Model(d, p)
+    M = nmt().Model(synth.params_bytes(d, p), precision=prec)
+    src = synth.make_source(d.vocab_src, 22, seed=5)
+    c = M.encode(src)
+    sess = O.Session(om, src)
+    ctx, _, s0 = c.debug_encoder()
+    ref = O.encode(om, src)
+    assert np.max(np.abs(ctx - ref.ctx)) < 1e-4 and np.max(np.abs(s0 - ref.s0)) < 1e-4
+    rng = np.random.default_rng(3)
+    w1 = [int(x) for x in rng.choice(d.vocab_tgt, size=9, replace=False)]
+    lp1, ch1, am1 = c.score_batch([0], [0, 9], w1)
+    rl1, rc1, _ = sess.score_batch([0], [0, 9], w1)
+    assert list(ch1) == list(rc1)
+    parents = [int(x) for x in ch1] * 7 + [0]  # 64 parents, duplicates and the (stepped) root
+    off = [0]
+    words = []
+    for _ in parents:
+        k = int(rng.integers(1, 5))
+        words += [int(x) for x in rng.choice(d.vocab_tgt, size=k, replace=False)]
+        off.append(len(words))
+    lp, ch, am = c.score_batch(parents, off, words)
+    rl, rc, ra = sess.score_batch(parents, off, words)
+    assert list(ch) == list(rc)
+    err = max(float(np.max(np.abs(lp1 - rl1))), float(np.max(np.abs(lp - rl))))
+    print(f"\n[irregular {readout}-{prec}] max|dlogp| = {err:.2e}")
+    assert err < TOL[prec]
