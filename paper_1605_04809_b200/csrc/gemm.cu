@@ -50,20 +50,26 @@ constexpr bool single_acc() { return EPI == EPI_GRU2; }
 constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant, each owning half of the tile's columns
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
+constexpr int kAresKB = 8;  // ARES: k-blocks of the resident A tile (K <= 512: the vocabulary GEMM's Ep)
+
 // PAIR (cta_group::2): a cluster of 2 CTAs computes 256 x BN tiles - M = 256 across the pair, each
 // CTA holds its 128 rows of A and HALF of the B tile, so per SM a k-block moves (16 + BN/8) KB for
 // the MMA work of a 128 x BN tile.  Protocol (as CUTLASS' 2SM kernels): both CTAs TMA into their own
 // smem and count bytes on the leader's full barrier (+1 remote arrive from the peer); the leader
 // issues the MMAs and commits with multicast to both CTAs' empty / tfull barriers; every epilogue
 // warp of both CTAs arrives on the leader's tempty barrier.
-template <int BN, int STAGES, int EPI, bool PAIR>
+template <int BN, int STAGES, int EPI, bool PAIR, bool ARES = false>
 struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_ROWS = PAIR ? BN / 2 : BN;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   // EPI_STORE: per epilogue warp two 32 x 32 fp32 staging tiles (128B-swizzled) for TMA stores
   static constexpr int C_BYTES = EPI == 0 ? EPI_WARPS * 2 * 4096 : 0;
-  static constexpr int BYTES = 1024 + STAGES * (A_BYTES + B_BYTES) + C_BYTES + (2 * STAGES + 4) * 8 + 16;
+  // ARES (A resident): the A tile of a work item's m-tile, all its k-blocks (K <= kAresKB * 64), stays in
+  // shared memory for the item's whole n-run; the stage ring carries only B
+  static constexpr int A_RING = ARES ? 0 : A_BYTES;
+  static constexpr int A_RES = ARES ? kAresKB * A_BYTES : 0;
+  static constexpr int BYTES = 1024 + A_RES + STAGES * (A_RING + B_BYTES) + C_BYTES + (2 * STAGES + 6) * 8 + 16;
 };
 
 struct RegionK {
@@ -178,12 +184,13 @@ NMT_DEV void gru_store4(__nv_bfloat16* p, int lo_off, float a, float b, float c,
 
 // Per-CTA view of the engine's shared memory, barriers and TMEM, and the roles' pipeline positions
 // (a role function called twice in one launch would continue the same stage ring).
-template <int BN, int STAGES, int EPI, bool PAIR>
+template <int BN, int STAGES, int EPI, bool PAIR, bool ARES = false>
 struct GemmCta {
-  using S = GemmSmem<BN, STAGES, EPI, PAIR>;
+  using S = GemmSmem<BN, STAGES, EPI, PAIR, ARES>;
   static constexpr int CM = PAIR ? 2 * BM : BM;  // rows of a tile (per CTA pair)
   uint8_t *sA, *sB, *sC;
   uint64_t *full, *empty, *tfull, *tempty;
+  uint64_t *afull, *aempty;  // ARES: resident A tile landed / released by the MMAs of its item
   uint32_t* tmem_slot;
   uint32_t tmem;
   int warp, lane;
@@ -191,19 +198,21 @@ struct GemmCta {
   bool leader;
   int unit, nunits;
   // pipeline positions (each used by one role)
-  int p_stage = 0, m_stage = 0, m_it = 0, e_it = 0;
+  int p_stage = 0, m_stage = 0, m_it = 0, e_it = 0, p_item = 0, m_item = 0;
   uint32_t p_phase = 0, m_phase = 0;
 
   NMT_DEV void carve(uint8_t* smem_raw) {
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    sA = smem;
-    sB = smem + STAGES * S::A_BYTES;
+    sA = smem;  // ARES: the resident A tile [kAresKB][A_BYTES]; else the A halves of the stage ring
+    sB = smem + S::A_RES + STAGES * S::A_RING;
     sC = sB + STAGES * S::B_BYTES;  // (1024-aligned: A/B stage sizes are multiples of 1 KB)
     full = reinterpret_cast<uint64_t*>(sC + S::C_BYTES);
     empty = full + STAGES;
     tfull = empty + STAGES;
     tempty = tfull + 2;
-    tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    afull = tempty + 2;
+    aempty = afull + 1;
+    tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
     warp = threadIdx.x >> 5;
     lane = threadIdx.x & 31;
     rank = PAIR ? cluster_ctarank() : 0;
@@ -222,6 +231,8 @@ struct GemmCta {
         mbar_init(&tfull[a], 1);
         mbar_init(&tempty[a], (PAIR ? 2 : 1) * EPI_WARPS);
       }
+      mbar_init(afull, PAIR ? 2 : 1);
+      mbar_init(aempty, 1);
       fence_barrier_init();
     }
     if (warp == 1) {
@@ -247,14 +258,34 @@ struct GemmCta {
 
 // ---- TMA producer: the whole warp 0 runs the (warp-uniform) loop, one elected lane issues (both CTAs of a
 // pair load their halves)
-template <int BN, int STAGES, int EPI, bool PAIR>
-NMT_DEV void gemm_produce(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap* tmA, const CUtensorMap* tmB,
+template <int BN, int STAGES, int EPI, bool PAIR, bool ARES = false>
+NMT_DEV void gemm_produce(GemmCta<BN, STAGES, EPI, PAIR, ARES>& cx, const CUtensorMap* tmA, const CUtensorMap* tmB,
                           const CUtensorMap* tmB2, const GemmShape& g, const Sched& sc) {
-  using S = GemmSmem<BN, STAGES, EPI, PAIR>;
-  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR>::CM;
+  using S = GemmSmem<BN, STAGES, EPI, PAIR, ARES>;
+  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR, ARES>::CM;
   const uint32_t full0 = PAIR ? mapa_shared(smem_u32(cx.full), 0) : 0;
   for (int w = cx.unit; w < sc.items; w += cx.nunits) {
     const Item itm = sc.item(w);
+    if constexpr (ARES) {  // the item's A tile once: all k-blocks (single pass, one region, no split)
+      const RegionK rk = region_of(g, itm.n0 * BN);
+      const int nkb = rk.k1 - rk.k0;
+      if (cx.p_item > 0) mbar_wait(cx.aempty, (cx.p_item - 1) & 1);  // the previous item's MMAs are done with A
+      const int arow = itm.m * CM + cx.rank * BM;
+      if (elect_one()) {
+        if constexpr (PAIR) {
+          if (cx.leader) mbar_arrive_expect_tx(cx.afull, 2 * nkb * S::A_BYTES);
+          else mbar_arrive_cluster(mapa_shared(smem_u32(cx.afull), 0));
+          for (int kb = 0; kb < nkb; ++kb)
+            tma_load_2d_pair(tmA, cx.afull, cx.sA + kb * S::A_BYTES, g.a_col0 + (rk.k0 + kb) * BK, arow);
+        } else {
+          mbar_arrive_expect_tx(cx.afull, nkb * S::A_BYTES);
+          for (int kb = 0; kb < nkb; ++kb)
+            tma_load_2d(tmA, cx.afull, cx.sA + kb * S::A_BYTES, g.a_col0 + (rk.k0 + kb) * BK, arow);
+        }
+      }
+      __syncwarp();
+      ++cx.p_item;
+    }
     for (int n = itm.n0; n < itm.n1; ++n) {
       const TileCoord tc{itm.m, n, itm.s};
       const RegionK rk = region_of(g, tc.n * BN);
@@ -276,13 +307,15 @@ NMT_DEV void gemm_produce(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap*
         const CUtensorMap* tb = in_b2 ? tmB2 : tmB;
         if (elect_one()) {
           if constexpr (PAIR) {
-            if (cx.leader) mbar_arrive_expect_tx(&cx.full[stage], 2 * (S::A_BYTES + S::B_BYTES));
+            if (cx.leader) mbar_arrive_expect_tx(&cx.full[stage], 2 * (S::A_RING + S::B_BYTES));
             else mbar_arrive_cluster(full0 + stage * 8);
-            tma_load_2d_pair(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK + kj, arow);
+            if constexpr (!ARES)
+              tma_load_2d_pair(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK + kj, arow);
             tma_load_2d_pair(tb, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
           } else {
-            mbar_arrive_expect_tx(&cx.full[stage], S::A_BYTES + S::B_BYTES);
-            tma_load_2d(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK + kj, arow);
+            mbar_arrive_expect_tx(&cx.full[stage], S::A_RING + S::B_BYTES);
+            if constexpr (!ARES)
+              tma_load_2d(tmA, &cx.full[stage], cx.sA + stage * S::A_BYTES, aoff + kb * BK + kj, arow);
             tma_load_2d(tb, &cx.full[stage], cx.sB + stage * S::B_BYTES, bx, by);
           }
         }
@@ -299,15 +332,19 @@ NMT_DEV void gemm_produce(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap*
 // ---- MMA issuer: the whole warp 1 of the pair's leader runs the (warp-uniform) loop, so descriptors and
 // TMEM addresses live in uniform registers; one elected lane issues a k-block's MMAs and its commit
 // (lane-divergent issue cost ~20 instructions per MMA in ELECT / R2UR broadcast loops)
-template <int BN, int STAGES, int EPI, bool PAIR>
-NMT_DEV void gemm_mma(GemmCta<BN, STAGES, EPI, PAIR>& cx, const GemmShape& g, const Sched& sc, const EpiParams& ep) {
-  using S = GemmSmem<BN, STAGES, EPI, PAIR>;
-  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR>::CM;
+template <int BN, int STAGES, int EPI, bool PAIR, bool ARES = false>
+NMT_DEV void gemm_mma(GemmCta<BN, STAGES, EPI, PAIR, ARES>& cx, const GemmShape& g, const Sched& sc, const EpiParams& ep) {
+  using S = GemmSmem<BN, STAGES, EPI, PAIR, ARES>;
+  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR, ARES>::CM;
   constexpr uint32_t idesc = idesc_bf16(CM, BN);
   constexpr uint32_t idesc2 = idesc_bf16(CM, 192);  // (EPI_GRU2, EPI_GRU)
   const uint64_t adesc0 = sdesc_sw128(smem_u32(cx.sA)), bdesc0 = sdesc_sw128(smem_u32(cx.sB));
   for (int w = cx.unit; w < sc.items; w += cx.nunits) {
     const Item itm = sc.item(w);
+    if constexpr (ARES) {
+      mbar_wait(cx.afull, cx.m_item & 1);  // the item's resident A tile
+      tc_fence_after();
+    }
     for (int n = itm.n0; n < itm.n1; ++n, ++cx.m_it) {
       const TileCoord tc{itm.m, n, itm.s};
       const RegionK rk = region_of(g, tc.n * BN);
@@ -326,7 +363,7 @@ NMT_DEV void gemm_mma(GemmCta<BN, STAGES, EPI, PAIR>& cx, const GemmShape& g, co
         tc_fence_after();
         if (cx.lane == 0 && cx.m_it == 0 && i == 0) GTRACE(3);
         // descriptor start-address field: (smem address >> 4), +2 per 32 bytes (16 bf16 of K)
-        const uint64_t ad = adesc0 + (uint64_t)(stage * (S::A_BYTES >> 4));
+        const uint64_t ad = adesc0 + (uint64_t)((ARES ? i : stage) * (S::A_BYTES >> 4));  // (ARES: k-block i)
         const uint64_t bd = bdesc0 + (uint64_t)(stage * (S::B_BYTES >> 4));
         if (elect_one()) {
           if constexpr (EPI == EPI_GRU2) {
@@ -361,15 +398,23 @@ NMT_DEV void gemm_mma(GemmCta<BN, STAGES, EPI, PAIR>& cx, const GemmShape& g, co
       }
       __syncwarp();
     }
+    if constexpr (ARES) {  // the item's MMAs done: both CTAs' producers may reload A
+      if (elect_one()) {
+        if constexpr (PAIR) mma_commit_pair(cx.aempty);
+        else mma_commit(cx.aempty);
+      }
+      __syncwarp();
+      ++cx.m_item;
+    }
   }
   if (cx.lane == 0) GTRACE(4);
 }
 
 // ---- epilogue warps 2..9 (each CTA: its 128 rows of the tile)
-template <int BN, int STAGES, int EPI, bool PAIR>
-NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap* tmC, const GemmShape& g, int M,
+template <int BN, int STAGES, int EPI, bool PAIR, bool ARES = false>
+NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR, ARES>& cx, const CUtensorMap* tmC, const GemmShape& g, int M,
                            const Sched& sc, const EpiParams& ep) {
-  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR>::CM;
+  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR, ARES>::CM;
   const int warp = cx.warp, lane = cx.lane;
   const uint32_t rank = cx.rank, tmem = cx.tmem;
   const bool leader = cx.leader;
@@ -701,12 +746,12 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR>& cx, const CUtensorMap
   }
 }
 
-template <int BN, int STAGES, int EPI, bool PAIR>
+template <int BN, int STAGES, int EPI, bool PAIR, bool ARES = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmC, GemmShape g, EpiParams ep) {
   extern __shared__ uint8_t smem_raw[];
-  GemmCta<BN, STAGES, EPI, PAIR> cx;
+  GemmCta<BN, STAGES, EPI, PAIR, ARES> cx;
   cx.carve(smem_raw);
   if (threadIdx.x == 0) GTRACE(0);
   if (cx.warp == 0 && cx.lane == 0) {
@@ -718,7 +763,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (threadIdx.x == 0) GTRACE(1);
   pdl_enter();  // prologue above overlaps the previous kernel; inputs (and M_dev) are read below
   if (threadIdx.x == 0) GTRACE(2);
-  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR>::CM;
+  constexpr int CM = GemmCta<BN, STAGES, EPI, PAIR, ARES>::CM;
   const int M = g.M_dev ? *g.M_dev : g.M;
   const Sched sc = make_sched<EPI>(g, M, CM, BN, cx.nunits);
   if ((EPI == EPI_LSE || EPI == EPI_TOPK) && blockIdx.x == 0 && threadIdx.x == 0 && ep.cpm_out) *ep.cpm_out = sc.cpm;
@@ -793,13 +838,13 @@ static const CUtensorMap& out_map(const float* out, uint64_t rows, uint64_t ldc)
   return it->second;
 }
 
-template <int BN, int STAGES, int EPI, bool PAIR>
+template <int BN, int STAGES, int EPI, bool PAIR, bool ARES = false>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmShape& g,
                    const EpiParams& ep, int M_max, cudaStream_t st) {
-  using S = GemmSmem<BN, STAGES, EPI, PAIR>;
+  using S = GemmSmem<BN, STAGES, EPI, PAIR, ARES>;
   static_assert(S::BYTES <= 232448, "shared memory budget");
   static std::atomic<size_t> smem_attr[kMaxDevices];  // per template instance and device
-  ensure_smem_attr(k_gemm<BN, STAGES, EPI, PAIR>, smem_attr, (size_t)S::BYTES);
+  ensure_smem_attr(k_gemm<BN, STAGES, EPI, PAIR, ARES>, smem_attr, (size_t)S::BYTES);
   const int CM = PAIR ? 2 * BM : BM;
   int tiles = 0;  // work items at M_max rows (EPI_STORE: per region, with its split count)
   for (int r = 0, nt0 = 0; r < g.nreg; ++r) {
@@ -829,7 +874,7 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
     EpiParams et = ep;
     CK(cudaMalloc(&et.trace, (size_t)grid * 8 * 8));
     CK(cudaMemsetAsync(et.trace, 0, (size_t)grid * 8 * 8, st));
-    CK(cudaLaunchKernelEx(&cfg, k_gemm<BN, STAGES, EPI, PAIR>, a, b, c, g, et));
+    CK(cudaLaunchKernelEx(&cfg, k_gemm<BN, STAGES, EPI, PAIR, ARES>, a, b, c, g, et));
     CK_LAUNCH();
     std::vector<unsigned long long> h((size_t)grid * 8);
     CK(cudaMemcpyAsync(h.data(), et.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
@@ -851,7 +896,7 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
     return;
   }
 #endif
-  CK(cudaLaunchKernelEx(&cfg, k_gemm<BN, STAGES, EPI, PAIR>, a, b, c, g, ep));
+  CK(cudaLaunchKernelEx(&cfg, k_gemm<BN, STAGES, EPI, PAIR, ARES>, a, b, c, g, ep));
   CK_LAUNCH();
 }
 
@@ -980,7 +1025,17 @@ void gemm_lse_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmSh
   ep.n_valid = n_valid;
   ep.n_tiles = g.N / 256;
   ep.cpm_out = cpm_out;
-  launch<256, 6, EPI_LSE, true>(a, b_half, b_half /*unused*/, g, ep, kNumSMs * BM, st);
+  // single-pass bf16 with K <= 512: the A tile stays resident for the unit's whole n-run (one L2 read of A
+  // per item instead of one per n-tile: half the L2 -> SM bytes of the kernel)
+  const bool ares = g.passes == 1 && g.nreg == 1 && g.ksplit == 1 && (g.reg_k1[0] - g.reg_k0[0]) <= kAresKB * BK;
+#ifdef NMT_DIAG
+  if (getenv("NMT_VOCAB_NOARES")) {
+    launch<256, 6, EPI_LSE, true>(a, b_half, b_half /*unused*/, g, ep, kNumSMs * BM, st);
+    return;
+  }
+#endif
+  if (ares) launch<256, 6, EPI_LSE, true, true>(a, b_half, b_half /*unused*/, g, ep, kNumSMs * BM, st);
+  else launch<256, 6, EPI_LSE, true>(a, b_half, b_half /*unused*/, g, ep, kNumSMs * BM, st);
 }
 
 }  // namespace nmt
