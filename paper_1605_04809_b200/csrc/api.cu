@@ -1579,10 +1579,9 @@ static void run_call(nmt_model* m, nmt_ctx* c, const PlanIO& io, float* out_logp
   const CtxDev cd = c->dev();
   {
     ProfScope p_(m, ST_PLAN);
-    // the join with the encoder's recurrence (s0 in slot 0) goes between the planner's first kernel and the
-    // rest: the intern kernel runs before the cooperative recurrence, flags/assign after it anyway, and the
-    // stream wait there costs no PDL overlap (before the state gather it cost ~3 us per step)
-    plan(cd, io, c->counters + CNT_R, m->st, [c] { c->join_enc_s0(); });
+    // (the planner needs nothing from the encoder: with the recurrence on 128 of the 148 SMs it runs beside
+    // it; the step joins the recurrence (s0 in slot 0) only before the state gather)
+    plan(cd, io, c->counters + CNT_R, m->st);
   }
   run_step(m, c, io.n_par);
   ProfScope p_(m, ST_GATHERDOT);
