@@ -11,7 +11,6 @@
 //              log p(w) = t.W_o[:,w] + b_o[w] - logsumexp_v(t W_o + b_o)
 // Device layouts: hidden dims padded to Hp = roundup(H,128), context dims to
 // Cp = 2 Hp with cmap(i) = i < H ? i : Hp + i - H, embedding/readout width to Ep = roundup(E+2,64).
-#include <functional>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -425,14 +424,13 @@ __global__ void __launch_bounds__(kPlanBlock) k_plan_assign(CtxDev c, PlanIO io,
   }
 }
 
-void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st, const std::function<void()>& after_intern) {
+void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st) {
   const int n = io.n_cand > io.n_par ? io.n_cand : io.n_par;
   const PlanDesc* none = nullptr;
   if (n > 0) {
     launch_pdl(k_plan_intern, (n + 255) / 256, 256, 0, st, c, io, none);
     CK_LAUNCH();
   }
-  if (after_intern) after_intern();  // (e.g. a stream wait: it costs the PDL overlap of this boundary only)
   const int Bc = (io.n_cand + kPlanBlock - 1) / kPlanBlock, Bp = (io.n_par + kPlanBlock - 1) / kPlanBlock;
   const int B = Bc + Bp > 0 ? Bc + Bp : 1;
   launch_pdl(k_plan_flags, B, kPlanBlock, 0, st, c, io, Bc, none);

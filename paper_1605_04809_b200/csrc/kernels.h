@@ -1,6 +1,5 @@
 // kernels.h - device-side views and launchers of the non-GEMM kernels (kernels.cu).
 #pragma once
-#include <functional>
 #include "internal.h"
 
 namespace nmt {
@@ -170,8 +169,7 @@ void beam_gather(const StepDev& d, const CtxDev& c, const int* parents, int n, c
 void topk_merge(const float2* topk, const int* cpm_dev, int n, int k, int* out_words, cudaStream_t st);
 void ctx_reset(const CtxDev& c, int64_t hcap, cudaStream_t st);
 void fill_i32(int* p, int64_t n, int v, cudaStream_t st);
-void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st,
-          const std::function<void()>& after_intern = nullptr);
+void plan(const CtxDev& c, const PlanIO& io, int* R_dev, cudaStream_t st);
 // G groups at once: descs [dev, G]; max_cand / max_par = the largest group's counts
 void plan_multi(const PlanDesc* descs, int G, int max_cand, int max_par, cudaStream_t st);
 void rehash(const unsigned long long* okeys, const int* ovals, int64_t ocap, unsigned long long* nkeys, int* nvals,
