@@ -3200,10 +3200,12 @@ nmt_status nmt_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t split, int32_
     {  // small random operands (values do not matter for timing)
       std::vector<__nv_bfloat16> h((size_t)Mp * sf * K);
       for (size_t i = 0; i < h.size(); ++i) h[i] = __float2bfloat16_rn((float)((i * 2654435761u) % 1000) * 1e-3f - 0.5f);
-      CK(cudaMemcpy(a, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(a, h.data(), h.size() * 2, cudaMemcpyHostToDevice, st));  // (stream-ordered pool memory)
+      CK(cudaStreamSynchronize(st));
       std::vector<__nv_bfloat16> hb((size_t)N * sf * K);
       for (size_t i = 0; i < hb.size(); ++i) hb[i] = __float2bfloat16_rn((float)((i * 40503u) % 1000) * 1e-3f - 0.5f);
-      CK(cudaMemcpy(b, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(b, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
     }
     CUtensorMap ta = make_tmap_bf16(a, Mp, sf * K, 128), tb = make_tmap_bf16(b, N, sf * K, epi >= 1 ? 256 : 128);
     CUtensorMap tb128 = make_tmap_bf16(b, N, sf * K, 128), tb64 = make_tmap_bf16(b, N, sf * K, 64);
@@ -3275,17 +3277,19 @@ nmt_status nmt_test_gemm(int32_t M, int32_t N, int32_t K, int32_t split, const f
     const int Mp = round_up(M, 128);
     float *dA = dalloc<float>((size_t)M * K), *dB = dalloc<float>((size_t)K * N), *dC = dalloc<float>((size_t)M * N);
     float* db = bias ? dalloc<float>(N) : nullptr;
-    CK(cudaMemcpy(dA, A, (size_t)M * K * 4, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(dB, B, (size_t)K * N * 4, cudaMemcpyHostToDevice));
-    if (bias) CK(cudaMemcpy(db, bias, (size_t)N * 4, cudaMemcpyHostToDevice));
+    // (the buffers come from a stream-ordered pool on `st`: every access goes through `st`; a legacy-stream
+    // cudaMemcpy may run before the allocation is mapped - a rare garbage input seen once in ~10 suite runs)
+    CK(cudaMemcpyAsync(dA, A, (size_t)M * K * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dB, B, (size_t)K * N * 4, cudaMemcpyHostToDevice, st));
+    if (bias) CK(cudaMemcpyAsync(db, bias, (size_t)N * 4, cudaMemcpyHostToDevice, st));
     __nv_bfloat16* a = dalloc<__nv_bfloat16>((size_t)Mp * sf * K);
     __nv_bfloat16* b = dalloc<__nv_bfloat16>((size_t)N * sf * K);
     pack_rows(dA, K, M, K, a, sf * K, 0, split ? K : 0, st);
     pack_T(dB, N, K, N, b, sf * K, 0, 0, 0, 0, 1, 1, split ? K : 0, st);
     CUtensorMap ta = make_tmap_bf16(a, Mp, sf * K, 128), tb = make_tmap_bf16(b, N, sf * K, 128);
     gemm_store(ta, tb, gemm_shape(M, nullptr, N, K, 0, split != 0, K, K), dC, N, M, db, M, st);
+    CK(cudaMemcpyAsync(C, dC, (size_t)M * N * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    CK(cudaMemcpy(C, dC, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
     dfree(dA);
     dfree(dB);
     dfree(dC);
