@@ -236,7 +236,7 @@ struct nmt_model {
   float* W_o32 = nullptr;         // [V][Ep]
   float* b_o = nullptr;           // [V]
   bool use_pair = true;  // CTA-pair (cta_group::2) GEMMs where the shapes allow (NMT_PAIR=0 disables)
-  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128, tm_Wh1g, tm_Wg2i, tm_Wro64;
+  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wq64, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128, tm_Wh1g, tm_Wg2i, tm_Wro64;
   // encoder workspace
   int Tpad = 0;
   __nv_bfloat16* ctxbf = nullptr; // [Tpad][4Hp]
@@ -1087,6 +1087,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   m->tm_Wh1 = make_tmap_bf16(m->W_h1, 3 * Hp, sf * Hp, 128);
   m->tm_Wh1g = make_tmap_bf16(m->W_h1g, 4 * Hp, sf * Hp, 128);
   m->tm_Wq = make_tmap_bf16(m->W_q, Cp, sf * Hp, 128);
+  m->tm_Wq64 = make_tmap_bf16(m->W_q, Cp, sf * Hp, 64);  // (256 x 128 CTA-pair tiles: 64-row halves)
   m->tm_Wg2 = make_tmap_bf16(m->W_g2, 4 * Hp, sf * ldg2, 128);
   m->tm_Wg2i = make_tmap_bf16(m->W_g2i, 4 * Hp, sf * ldg2, 128);
   m->tm_Wro = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 128);
@@ -1448,8 +1449,16 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
   if (!stage_skipped(ST_GEMM_Q)) {
     ProfScope p_(m, ST_GEMM_Q);
     GemmShape g = gemm_shape(0, Rd, Cp, Hp, 0, sp, 4 * Hp, Hp);
-    // no split-K: every attention CTA starts by reading its rows' q, one partial is one load (A/B: -1 us)
-    gemm_auto(m, m->tm_X, m->tm_Wq, g, m->Q, Cp, rps, R_max, st, 1);
+    // no split-K: every attention CTA starts by reading its rows' q, one partial is one load (A/B: -1 us).
+    // CTA pairs with 256 x 128 tiles: N = Cp = 2H gives 4 x 16 pair tiles at R = 1024, i.e. 128 CTAs (256 x 256
+    // tiles kept 64 SMs busy)
+    static const bool q128 = !(diag_env("NMT_Q128") && atoi(diag_env("NMT_Q128")) == 0);  // (diagnostic A/B)
+    if (q128 && m->use_pair && Cp % 128 == 0) {
+      gemm_store_pair128(m->tm_X, m->tm_Wq64, g, m->Q, Cp, m->P_rows, nullptr, R_max, st, 0);
+      g.reg_ks[0] = 1;
+    } else {
+      gemm_auto(m, m->tm_X, m->tm_Wq, g, m->Q, Cp, rps, R_max, st, 1);
+    }
     d.ks_q = g.reg_ks[0];
     d.ps_q = (int64_t)rps * Cp;
   }
