@@ -236,7 +236,7 @@ struct nmt_model {
   float* W_o32 = nullptr;         // [V][Ep]
   float* b_o = nullptr;           // [V]
   bool use_pair = true;  // CTA-pair (cta_group::2) GEMMs where the shapes allow (NMT_PAIR=0 disables)
-  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wq64, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128, tm_Wh1g, tm_Wg2i, tm_Wro64;
+  CUtensorMap tm_Watt, tm_Wh1, tm_Wq, tm_Wq64, tm_Wg2, tm_Wro, tm_Wo, tm_Wo128, tm_Wh1g, tm_Wg2i, tm_Wro64, tm_Wro32;
   // encoder workspace
   int Tpad = 0;
   __nv_bfloat16* ctxbf = nullptr; // [Tpad][4Hp]
@@ -506,7 +506,7 @@ struct nmt_ctx {
   // projected-context operands (nmt_encode only): cw [NW][2 Apad] bf16, rows 0..4Hp = ctx.(c rows of W_g2i),
   // rows 4Hp.. = ctx.W_ctx, columns = source positions (hi | lo); zero past Tx
   __nv_bfloat16* cw = nullptr;
-  CUtensorMap tm_cw_g2, tm_cw_ro;  // B2 maps for the G2 (128-row box) and readout (64-row box) GEMMs
+  CUtensorMap tm_cw_g2, tm_cw_ro, tm_cw_ro32;  // B2 maps: G2 (128-row box), readout (64- and 32-row boxes)
   bool has_cw = false;
   int node_cap = 0, slot_cap = 0;
   int64_t hcap = 0;
@@ -1092,6 +1092,7 @@ static void build_model(nmt_model* m, const std::map<std::string, Arr>& A) {
   m->tm_Wg2i = make_tmap_bf16(m->W_g2i, 4 * Hp, sf * ldg2, 128);
   m->tm_Wro = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 128);
   m->tm_Wro64 = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 64);  // (256 x 128 CTA-pair tiles: 64-row halves)
+  m->tm_Wro32 = make_tmap_bf16(m->W_ro, ROp, sf * ldro, 32);  // (256 x 64 CTA-pair tiles: 32-row halves)
   m->tm_Wo = make_tmap_bf16(m->W_o, (uint64_t)Vp * sf * Ep / 64, 64, 256);     // panel layout
   m->tm_Wo128 = make_tmap_bf16(m->W_o, (uint64_t)Vp * sf * Ep / 64, 64, 128);  // CTA-pair vocabulary GEMM: half tiles
 
@@ -1530,7 +1531,11 @@ static void run_step(nmt_model* m, nmt_ctx* c, int R_max, const MultiStep* ms = 
     ep.row_dst = m->row_dst;
     ep.gs = d.gs;
     ep.row_grp = d.row_grp;
-    gemm_readout_pair(m->tm_X, m->tm_Wro64, g, ep, R_max, st, proj ? &c->tm_cw_ro : nullptr);
+    static const bool ro64 = !(diag_env("NMT_RO64") && atoi(diag_env("NMT_RO64")) == 0);  // (diagnostic A/B)
+    if (ro64 && m->ROp % 64 == 0)  // 256 x 64 pair tiles: 128 CTAs for ROp = 1024 at R = 1024
+      gemm_readout_pair64(m->tm_X, m->tm_Wro32, g, ep, R_max, st, proj ? &c->tm_cw_ro32 : nullptr);
+    else
+      gemm_readout_pair(m->tm_X, m->tm_Wro64, g, ep, R_max, st, proj ? &c->tm_cw_ro : nullptr);
   } else {  // (1-CTA GEMM mode, diagnostics): split-K GEMM + k_readout
   if (!stage_skipped(ST_GEMM_RO)) {
       ProfScope p_(m, ST_GEMM_RO);
@@ -1849,6 +1854,7 @@ static nmt_ctx* acquire_ctx(nmt_model* m, int len) {
     c->cw = dalloc<__nv_bfloat16>((size_t)m->NW * 2 * m->Apad);
     c->tm_cw_g2 = make_tmap_bf16(c->cw, 4 * m->Hp, 2 * m->Apad, 128);
     c->tm_cw_ro = make_tmap_bf16(c->cw + (size_t)4 * m->Hp * 2 * m->Apad, m->ROp, 2 * m->Apad, 64);
+    c->tm_cw_ro32 = make_tmap_bf16(c->cw + (size_t)4 * m->Hp * 2 * m->Apad, m->ROp, 2 * m->Apad, 32);
     c->counters = dalloc<int>(CNT_N);
     CK(cudaEventCreateWithFlags(&c->enc_ev, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->enc_s0_ev, cudaEventDisableTiming));

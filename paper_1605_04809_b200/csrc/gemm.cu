@@ -623,7 +623,7 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR, ARES>& cx, const CUten
           if (c + 2 < 4) bias_fetch(c + 2, bia[c & 1]);
         }
       } else if constexpr (EPI == EPI_READOUT) {
-        static_assert(COLS == 64, "EPI_READOUT: 64 readout columns per epilogue warp");
+        static_assert(COLS == 64 || COLS == 32, "EPI_READOUT: 64 or 32 readout columns per epilogue warp");
         // (tcgen05.ld / wait are warp-collective: every lane loads, only valid rows write)
         int dst = -1;
         if (valid) dst = ep.row_dst[grow];
@@ -631,34 +631,7 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR, ARES>& cx, const CUten
         __nv_bfloat16* at = ep.A_t + (int64_t)grow * ep.lda_t;
         const int E = ep.E;
         // 8 outputs t[k0 .. k0 + 8) per pass: maxout pairs columns (2k, 2k + 1) (16 columns), tanh 8
-        const int npass = ep.maxout ? 4 : 8;
-#pragma unroll
-        for (int ps = 0; ps < 8; ++ps) {
-          if (ps >= npass) break;
-          float t[8];
-          if (ep.maxout) {
-            float a[16];
-            tmem_ld8_nowait(tbase + 16 * ps, a);
-            tmem_ld8_nowait(tbase + 16 * ps + 8, a + 8);
-            tmem_wait_ld();
-            reg_dep8(a);
-            reg_dep8(a + 8);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float* e = epj[(16 * ps + 2 * i) / 8];
-              const int o = (2 * i) % 8;
-              t[i] = fmaxf(a[2 * i] + e[o], a[2 * i + 1] + e[o + 1]);
-            }
-          } else {
-            float a[8];
-            tmem_ld8_nowait(tbase + 8 * ps, a);
-            tmem_wait_ld();
-            reg_dep8(a);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) t[i] = gru_tanh(a[i] + epj[ps][i]);
-          }
-          if (!valid) continue;
-          const int k0 = (ep.maxout ? colbase / 2 : colbase) + 8 * ps;
+        auto emit = [&](int k0, float(&t)[8]) {
           float hi[8], lo[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -675,6 +648,35 @@ NMT_DEV void gemm_epilogue(GemmCta<BN, STAGES, EPI, PAIR, ARES>& cx, const CUten
             if (ep.lo_t > 0)
               *reinterpret_cast<uint4*>(at + ep.lo_t + k0) = make_uint4(gru_pk(lo[0], lo[1]), gru_pk(lo[2], lo[3]),
                                                                         gru_pk(lo[4], lo[5]), gru_pk(lo[6], lo[7]));
+          }
+        };
+        if (ep.maxout) {
+#pragma unroll
+          for (int ps = 0; ps < COLS / 16; ++ps) {
+            float a[16], t[8];
+            tmem_ld8_nowait(tbase + 16 * ps, a);
+            tmem_ld8_nowait(tbase + 16 * ps + 8, a + 8);
+            tmem_wait_ld();
+            reg_dep8(a);
+            reg_dep8(a + 8);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float* e = epj[(16 * ps + 2 * i) / 8];
+              const int o = (2 * i) % 8;
+              t[i] = fmaxf(a[2 * i] + e[o], a[2 * i + 1] + e[o + 1]);
+            }
+            if (valid) emit(colbase / 2 + 8 * ps, t);
+          }
+        } else {
+#pragma unroll
+          for (int ps = 0; ps < COLS / 8; ++ps) {
+            float a[8], t[8];
+            tmem_ld8_nowait(tbase + 8 * ps, a);
+            tmem_wait_ld();
+            reg_dep8(a);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) t[i] = gru_tanh(a[i] + epj[ps][i]);
+            if (valid) emit(colbase + 8 * ps, t);
           }
         }
       } else {  // EPI_LSE: online (max, sum exp, argmax) over this warp's COLS logits of the row
@@ -991,6 +993,17 @@ void gemm_readout_pair(const CUtensorMap& a, const CUtensorMap& b_q, const GemmS
     throw NmtError(NMT_ERR_INVALID_ARG, "gemm: the fused readout epilogue needs the full K sum in one region");
   check_b2(g, b2);
   launch<128, 8, EPI_READOUT, true>(a, b_q, b2 ? *b2 : b_q, g, ep, M_max, st);
+}
+
+// the same on 256 x 64 CTA-pair tiles (`b_e` / `b2`: maps with 32-row boxes): twice the CTAs of the 256 x 128
+// shape for the readout's narrow N (ROp = 1024 at E = 500: 4 x 16 pair tiles = 128 CTAs at R = 1024)
+void gemm_readout_pair64(const CUtensorMap& a, const CUtensorMap& b_e, const GemmShape& g, const EpiParams& ep,
+                         int M_max, cudaStream_t st, const CUtensorMap* b2) {
+  gemm_validate(g, 64);
+  if (gemm_ks_max(g) != 1 || g.nreg != 1)
+    throw NmtError(NMT_ERR_INVALID_ARG, "gemm: the fused readout epilogue needs the full K sum in one region");
+  check_b2(g, b2);
+  launch<64, 10, EPI_READOUT, true>(a, b_e, b2 ? *b2 : b_e, g, ep, M_max, st);
 }
 
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,

@@ -181,6 +181,8 @@ void gemm_gru2_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmS
 // for gemm_gru2_pair (the context's ctx.W_ctx rows)
 void gemm_readout_pair(const CUtensorMap& a, const CUtensorMap& b_q, const GemmShape& g, const EpiParams& ep, int M_max,
                        cudaStream_t st, const CUtensorMap* b2 = nullptr);
+void gemm_readout_pair64(const CUtensorMap& a, const CUtensorMap& b_e, const GemmShape& g, const EpiParams& ep,
+                         int M_max, cudaStream_t st, const CUtensorMap* b2 = nullptr);
 void gemm_lse(const CUtensorMap& a, const CUtensorMap& b, const GemmShape& g, float4* part, int n_valid, int M_max,
               cudaStream_t st, int* cpm_out);
 
