@@ -291,7 +291,9 @@ NMT_API nmt_status nmt_logprobs_full(nmt_ctx* c, nmt_state node, float* out);
 /* encoder outputs: ctx [Tx x 2H], pctx [Tx x 2H], s0 [H]; any pointer may be NULL [host]         */
 NMT_API nmt_status nmt_debug_encoder(nmt_ctx* c, float* ctx, float* pctx, float* s0);
 /* per-stage intermediates of one node's step (without caching): s1[H], alpha[Tx], c[2H], s2[H],
- * t[E], logZ[1], argmax[1]; any pointer may be NULL [host]                                       */
+ * t[E], logZ[1], argmax[1]; any pointer may be NULL [host].  The step forms c explicitly (D5); the
+ * scoring calls of a single context fold it into D6/D7 as alpha . (ctx . W) (reading A31),
+ * equal up to the precision's operand rounding.                                                   */
 NMT_API nmt_status nmt_debug_intermediates(nmt_ctx* c, nmt_state node, float* s1, float* alpha, float* ctxv,
                                    float* s2, float* t, float* logZ, int32_t* argmax);
 /* The vocabulary stage alone (D8 + D9, SURVEY §8(b) "minimum slice"): R rows of readout outputs
