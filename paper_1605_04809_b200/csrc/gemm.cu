@@ -1027,7 +1027,9 @@ void gemm_topk_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmS
   ep.n_valid = n_valid;
   ep.n_tiles = g.N / 256;
   ep.cpm_out = cpm_out;
-  launch<256, 6, EPI_TOPK, true>(a, b_half, b_half /*unused*/, g, ep, kNumSMs * BM, st);
+  const bool ares = g.passes == 1 && g.nreg == 1 && g.ksplit == 1 && (g.reg_k1[0] - g.reg_k0[0]) <= kAresKB * BK;
+  if (ares) launch<256, 6, EPI_TOPK, true, true>(a, b_half, b_half /*unused*/, g, ep, kNumSMs * BM, st);  // (as LSE)
+  else launch<256, 6, EPI_TOPK, true>(a, b_half, b_half /*unused*/, g, ep, kNumSMs * BM, st);
 }
 
 void gemm_lse_pair(const CUtensorMap& a, const CUtensorMap& b_half, const GemmShape& g, float4* part, int n_valid,
